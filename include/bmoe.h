@@ -1,0 +1,240 @@
+/*
+ * bmoe.h — C-ABI of libbmoe.so, the B200 (sm_100a) BuddyMoE hot path.
+ *
+ * The reference (arxiv 2511.10054, package `buddysim`, pure Python/numpy)
+ * has no FFI: its "operator API" is a set of Python functions. Each entry
+ * point below replaces one of them; the reference function it stands in for
+ * is cited as file:line relative to the reference's pkg/src/buddysim/.
+ * INTEGRATION.md shows the ctypes binding a buddysim maintainer would add.
+ *
+ * Conventions
+ *   - All sizes are int64_t. All pointers are DEVICE pointers unless the
+ *     parameter name ends in `_host`.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as
+ *     void*); no call synchronises the device unless documented.
+ *   - The caller owns every buffer; kernels never allocate. Handles
+ *     (bm_cache) own only what their create call documents.
+ *   - Return value: BM_OK or an error code; no exceptions cross the ABI.
+ *     bm_last_error() returns the thread-local message of the last failure.
+ *     Codes map onto the reference taxonomy (errors.py:9-38):
+ *       BM_EINVAL->InputError, BM_ECONFIG->ConfigurationError,
+ *       BM_EDEGENERATE->DegeneratePivotError, BM_EINVARIANT->InvariantViolation,
+ *       BM_ECUDA->InternalError.
+ *   - Plans use kind codes 0 kept / 1 substituted / 2 ondemand_fallback /
+ *     3 dropped (substitution.py:25-28).
+ *   - Buddy tables are dense: ids[E][K] int32 (-1 padded, stored rank order),
+ *     weights[E][K] float64, lens[E] int32 (buddies.py:35-76).
+ */
+#ifndef BMOE_H
+#define BMOE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BM_ABI_VERSION 1
+
+enum { BM_OK = 0, BM_EINVAL = 1, BM_ECONFIG = 2, BM_EDEGENERATE = 3, BM_EINVARIANT = 4, BM_ECUDA = 5 };
+enum { BM_KIND_KEPT = 0, BM_KIND_SUBSTITUTED = 1, BM_KIND_ONDEMAND = 2, BM_KIND_DROPPED = 3 };
+enum { BM_FALLBACK_PREFETCH = 0, BM_FALLBACK_DROP = 1 };                 /* substitution.py:30-31 */
+enum { BM_METHOD_BUDDY = 0, BM_METHOD_ORIGINAL = 1, BM_METHOD_IDENTITY = 2 };
+enum { BM_ACT_TANH = 0, BM_ACT_SWIGLU = 1 };
+enum { BM_POLICY_LRU = 0, BM_POLICY_LFU = 1, BM_POLICY_FREQ_STATIC = 2 };  /* memtier.py:31-34 */
+enum { BM_EV_HIT = 0, BM_EV_MISS_ONDEMAND = 1, BM_EV_MISS_SUBSTITUTED = 2, BM_EV_PREFETCH_ISSUE = 3,
+       BM_EV_PREFETCH_COMPLETE = 4, BM_EV_EVICT = 5, BM_EV_DROP = 6 };  /* memtier.py:20-26 */
+
+typedef void *bm_stream_t;
+
+int bm_abi_version(void);
+const char *bm_last_error(void);
+/* Number of SMs of the current device (grid sizing); -1 without a device. */
+int bm_device_sm_count(void);
+
+/* ---------------------------------------------------------------- K1 router
+ * Fused fp32 gate: z = x Wg^T + b; top-k of z by value desc, expert id asc;
+ * p~ = softmax(z/T) restricted to the selected set and renormalised (f64
+ * math, stored f32); TAE = -sum p~ ln p~ / ln k clamped to [0,1] (k=1 -> 0);
+ * margin = p~[0]-p~[1] (k=1 -> 1); token_allowed = !(TAE <= tau) &&
+ * !(gamma >= 0 && margin >= gamma). tau < 0 never forbids; gamma < 0
+ * disables the margin check. logits/tae/margin may be NULL.
+ * Replaces model.route_batch (model.py:231-280) and gating.tae/margin/
+ * token_gate (gating.py:71-108). x[B,d], wg[E,d], bias[E] fp32 row-major.
+ * Limits: E <= 256, k <= 32, k <= E. */
+int bm_gate_topk(const float *x, const float *wg, const float *bias, int64_t B, int64_t E, int64_t d,
+                 int64_t k, double temperature, double tau, double gamma, float *logits, int32_t *topk,
+                 float *probs, double *tae, double *margin, uint8_t *token_allowed, bm_stream_t stream);
+
+/* Selection + gates from given float64 logits[B,E] (the "identical logits
+ * give identical indices" parity boundary, model.py:259-263). probs64 may be
+ * NULL; probs (f32) may be NULL. */
+int bm_select_topk_f64(const double *logits, int64_t B, int64_t E, int64_t k, double temperature, double tau,
+                       double gamma, int32_t *topk, float *probs, double *probs64, double *tae, double *margin,
+                       uint8_t *token_allowed, bm_stream_t stream);
+
+/* ------------------------------------------------------- K2 buddy remap
+ * One warp per token; Alg. 1 of the paper as implemented by
+ * substitution.substitute_token (substitution.py:146-190) under one
+ * residency snapshot, with the batch distribution gate of
+ * gating.distribution_gate/evaluate_gates (gating.py:126-165):
+ *   delta = #non-resident requested slots / (B*k) (duplicates counted),
+ *   batch_allowed = !(delta >= beta); a token may substitute iff
+ *   token_allowed[b] && batch_allowed.
+ * method BUDDY: slot order; a resident original is kept; else, if allowed and
+ *   used < rho (rho < 0 = unlimited), the first of ids[orig][0:min(len,H)]
+ *   (Psi-ordered when eta or kappa > 0, substitution.py:107-143) that is
+ *   resident and not yet assigned to the token; else fallback kind.
+ * method ORIGINAL: substitution.ondemand_plan (substitution.py:217-224).
+ * method IDENTITY: substitution.identity_plan (substitution.py:211-214).
+ * resident_bitmap: ceil(E/32) words, bit e of word e/32 = resident.
+ * logits (for eta/kappa z-scores, :98-104) are float64 when logits_f64 != 0,
+ * else float32; may be NULL when eta == kappa == 0. partition_of may be NULL.
+ * delta_out / batch_allowed_out: single device scalars (may be NULL).
+ * Limits: E <= 256, k <= 32, H <= 256. */
+int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed, const void *logits, int32_t logits_f64,
+                   int64_t B, int64_t k, int64_t E, const uint32_t *resident_bitmap, const int32_t *tbl_ids,
+                   const double *tbl_w, const int32_t *tbl_len, int64_t tbl_stride, int64_t H, int64_t rho,
+                   int32_t fallback, int32_t method, double beta, double eta, double kappa,
+                   int32_t use_local_logit, const int32_t *partition_of, double hop, int32_t *executed,
+                   uint8_t *kind, int32_t *used, double *delta_out, uint8_t *batch_allowed_out,
+                   bm_stream_t stream);
+
+/* ------------------------------------------ K3 permute / K5 combine
+ * bm_permute: stable grouping of the executed (token, slot) pairs by expert
+ * (dropped slots excluded, model.py:294-305). Outputs expert_count[E] (real
+ * rows), expert_offset[E+1] (segment starts, each segment padded to a
+ * multiple of row_align rows; offset[E] = total padded rows), row_token[r]
+ * (-1 on padding rows; caller sizes it bmoe_permute_rows_max()), slot_row[B*k]
+ * (-1 for dropped). Single CTA; deterministic. */
+int64_t bm_permute_rows_max(int64_t B, int64_t k, int64_t E, int64_t row_align);
+int bm_permute(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E, int64_t row_align,
+               int32_t *expert_count, int32_t *expert_offset, int32_t *row_token, int32_t *slot_row,
+               bm_stream_t stream);
+
+/* Gather token rows into the permuted activation buffer (128-bit loads).
+ * layout 0: plain row-major fp32 x_perm[r_max][d].
+ * layout 1: bf16 "UMMA K-major SW128" planes: x_perm[d/64][r_max][64] with
+ *           the 16-byte chunk j of row r stored at chunk (j ^ (r & 7)) —
+ *           the exact shared-memory image the tcgen05 GEMM consumes.
+ * Padding rows are zero-filled. */
+int bm_gather_rows(const float *x, int64_t B, int64_t d, const int32_t *row_token, const int32_t *expert_offset,
+                   int64_t E, int64_t r_max, int32_t layout, void *x_perm, bm_stream_t stream);
+
+/* y[b] = sum_s p~[b,s] * [kind != dropped] * y_perm[slot_row[b,s]]  (model.py:334-340,
+ * original weights, no renormalisation of dropped mass); then, if h_in is
+ * not NULL, out = layer_update(h_in, y) = (h + scale*y)/max(rms, 1e-12)
+ * (model.py:343-347), else out = y. Fixed slot order: deterministic. */
+int bm_combine(const float *y_perm, const int32_t *slot_row, const float *probs, const uint8_t *kind, int64_t B,
+               int64_t k, int64_t d, const float *h_in, float residual_scale, float *out, bm_stream_t stream);
+
+/* ------------------------------------------------- K4 grouped expert FFN
+ * Expert weights live in an "arena" of equally sized buffers; buffer b holds
+ *   SWIGLU: [W1 (f x d) | W3 (f x d) | W2 (d x f)]   y = (silu(x W1^T) * (x W3^T)) W2^T
+ *   TANH:   [Win^T (f x d) | Wout^T (d x f)]         y = tanh(x Win) Wout (model.py:85-99)
+ * row-major; buf_of_expert[E] (device) maps an expert id to its buffer.
+ *
+ * fp32 parity mode (SIMT FFMA, fp32 weights and activations): x_perm is
+ * layout 0 [r_max][d]; h_ws is fp32 [r_max][f]; y_perm fp32 [r_max][d]. */
+int bm_expert_ffn_f32(const float *x_perm, const int32_t *expert_count, const int32_t *expert_offset, int64_t E,
+                      int64_t d, int64_t f, int32_t act, const float *w_arena, int64_t buf_elems,
+                      const int32_t *buf_of_expert, int64_t r_max, float *h_ws, float *y_perm,
+                      bm_stream_t stream);
+
+/* bf16 tensor-core mode: persistent stream-K tcgen05/TMEM/TMA GEMMs with
+ * weights as the M=128 operand ("swap-AB": decode token counts are the N
+ * dimension), fused SwiGLU/tanh in the split-K fixup, deterministic (no
+ * atomics). x_perm is layout 1 (bf16 SW128 planes over d). Workspace from
+ * bm_expert_ffn_bf16_workspace(): holds the fp32 partial tiles and the
+ * SW128 bf16 intermediate H. y_perm fp32 [r_max][d].
+ * Requires d % 128 == 0, f % 128 == 0. n_tile (16..256, multiple of 16)
+ * caps the per-tile token count; larger expert segments are chunked. */
+int64_t bm_expert_ffn_bf16_workspace(int64_t E, int64_t d, int64_t f, int64_t r_max, int64_t n_tile);
+int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const int32_t *expert_offset, int64_t E,
+                       int64_t d, int64_t f, int32_t act, const void *w_arena, int64_t n_bufs,
+                       const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
+                       int64_t workspace_bytes, float *y_perm, bm_stream_t stream);
+
+/* Kernel timing for the bench's roofline: after bm_set_kernel_timing(1)
+ * every bm_expert_ffn_bf16 call records CUDA events on its stream around its
+ * two GEMM kernels; bm_kernel_times() waits for them and writes 2 floats per
+ * call (GEMM1 ms, GEMM2 ms), returning the count written (-1 on error).
+ * bm_set_kernel_timing() clears the record. */
+int bm_set_kernel_timing(int32_t enable);
+int64_t bm_kernel_times(float *out_host, int64_t cap);
+
+/* ------------------------------------- K6/K7 co-activation and buddy ranking
+ * bm_coact_count: topk[N][k] int32 (distinct ids per row, profiler.py:76-80)
+ * accumulated into counts[E] and the symmetric pair matrix pairs[E][E] as
+ * uint64 (binary mode: each present pair adds 1, profiler.py:86-92).
+ * Shared-memory-privatised per-CTA counters, flushed with 64-bit adds.
+ * Warm-up down-weighting is applied by the caller by counting the warm-up
+ * token range separately (the weights are exact dyadic scalars).
+ * Accumulates (does not clear). Limits: E <= 256, k <= 32. */
+int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t E, unsigned long long *counts,
+                   unsigned long long *pairs, bm_stream_t stream);
+/* Weighted mass (profiler.py:93-95): pw[i][j] += w * min(p~_a, p~_b), f64
+ * atomics (order-dependent: tolerance-level parity only). */
+int bm_coact_weighted(const int32_t *topk, const float *probs, int64_t N, int64_t k, int64_t E, double w,
+                      double *pair_weights, bm_stream_t stream);
+/* out[i] = w_warm * warm[i] + main[i] as float64 (exact for counts < 2^53). */
+int bm_counts_to_f64(const unsigned long long *warm, const unsigned long long *main_, int64_t n, double w_warm,
+                     double *out, bm_stream_t stream);
+/* bm_buddy_rank: per pivot (one warp), bit-exact with buddies.build_table
+ * (buddies.py:79-129) over profiler.conditional_row (profiler.py:98-119):
+ * row = M[p] + eps, row[p] = 0, total = numpy pairwise sum, q = row/total,
+ * order = sort by (-q, id), t = first r with sequential cumsum >= alpha-1e-9
+ * (else nnz), len = min(t, nnz, k_max); total <= 0 -> empty list.
+ * Writes ids[E][k_max] (-1 padded), weights[E][k_max], lens[E]. E <= 1024. */
+int bm_buddy_rank(const double *pair_matrix, int64_t E, double eps, double alpha, int64_t k_max, int32_t *ids,
+                  double *weights, int32_t *lens, bm_stream_t stream);
+
+/* ----------------------------------------------- expert cache control plane
+ * Exact replica of memtier.ResidencyState/access/prefetch/settle
+ * (memtier.py:96-300) for all layers, one shared transfer channel and
+ * simulated clock (memtier.py:72-93), plus the next-layer predictor
+ * (harness.py:209-218). Host-only C++; decisions are bit-exact with the
+ * reference (same f64 clock arithmetic). */
+typedef struct bm_cache bm_cache;
+typedef struct {
+    double time_ms;
+    int32_t kind, layer, token, expert;
+    int64_t bytes;
+    double stall_ms;
+} bm_event;
+
+int bm_cache_create(int32_t num_layers, int32_t num_experts, int32_t capacity, int32_t policy,
+                    const int32_t *initial_host /* [L][capacity], -1 padded, ascending */,
+                    const double *static_freq_host /* [L][E] or NULL */, double expert_load_ms, double hit_ms,
+                    double prefetch_ms, int64_t expert_bytes, bm_cache **out);
+void bm_cache_destroy(bm_cache *c);
+/* mode 0 ondemand / 1 substituted_away (memtier.py:217-254). */
+int bm_cache_access(bm_cache *c, int32_t layer, int32_t expert, int32_t mode, int32_t token, bm_event *ev_out_host);
+/* The plan replay of harness.py:363-378 for one batch-layer: dropped -> drop
+ * event; substituted -> access(orig, substituted_away) then access(executed);
+ * else access(executed). Returns through out_host[4]: executed slots,
+ * ondemand misses, substitutions, read bytes. */
+int bm_cache_apply_plan(bm_cache *c, int32_t layer, int64_t B, int64_t k, const int32_t *tokens_host,
+                        const int32_t *topk_host, const int32_t *executed_host, const uint8_t *kind_host,
+                        int64_t *out_host);
+int bm_cache_prefetch(bm_cache *c, int32_t layer, const int32_t *experts_host, int64_t n);
+int bm_cache_settle(bm_cache *c, int32_t layer);
+int bm_cache_advance(bm_cache *c, double ms);
+int bm_cache_now(const bm_cache *c, double *now_host);
+int bm_cache_snapshot(const bm_cache *c, int32_t layer, uint8_t *mask_host, uint32_t *bitmap_host);
+/* Top-m of counts[E] (count desc, id asc), m = capacity - #nonzero. */
+int bm_cache_predict(const bm_cache *c, int32_t layer, const int32_t *counts_host, int32_t *out_host,
+                     int64_t *n_out_host);
+int64_t bm_cache_num_events(const bm_cache *c);
+int bm_cache_events(const bm_cache *c, int64_t start, int64_t n, bm_event *out_host);
+void bm_cache_clear_events(bm_cache *c);
+/* Per-layer state for inspection: last_use[E] int64, freq[E] f64, pending
+ * count, waste evictions, unused-prefetch residents. */
+int bm_cache_layer_state(const bm_cache *c, int32_t layer, int64_t *last_use_host, double *freq_host,
+                         int64_t *scalars_host /* [tick, n_pending, waste, unused_resident] */);
+int bm_cache_pending(const bm_cache *c, int32_t layer, double *done_host, int32_t *expert_host, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMOE_H */

@@ -1,0 +1,104 @@
+"""ctypes binding of libbmoe.so (include/bmoe.h).
+
+There is no CPU fallback: if the library is missing or fails to load, every
+product entry point raises NativeLibraryError. ``build()`` in
+__graft_entry__.py (or ``python -m paper_2511_10054_b200.build``) produces it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import NativeLibraryError, raise_for
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libbmoe.so")
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int32
+F64 = C.c_double
+F32 = C.c_float
+
+
+class Event(C.Structure):
+    _fields_ = [("time_ms", C.c_double), ("kind", C.c_int32), ("layer", C.c_int32), ("token", C.c_int32),
+                ("expert", C.c_int32), ("bytes", C.c_int64), ("stall_ms", C.c_double)]
+
+
+_SIGS = {
+    "bm_abi_version": (C.c_int, []),
+    "bm_last_error": (C.c_char_p, []),
+    "bm_device_sm_count": (C.c_int, []),
+    "bm_gate_topk": (C.c_int, [P, P, P, I64, I64, I64, I64, F64, F64, F64, P, P, P, P, P, P, P]),
+    "bm_select_topk_f64": (C.c_int, [P, I64, I64, I64, F64, F64, F64, P, P, P, P, P, P, P]),
+    "bm_buddy_remap": (C.c_int, [P, P, P, I32, I64, I64, I64, P, P, P, P, I64, I64, I64, I32, I32, F64, F64, F64,
+                                 I32, P, F64, P, P, P, P, P, P]),
+    "bm_permute_rows_max": (I64, [I64, I64, I64, I64]),
+    "bm_permute": (C.c_int, [P, P, I64, I64, I64, I64, P, P, P, P, P]),
+    "bm_gather_rows": (C.c_int, [P, I64, I64, P, P, I64, I64, I32, P, P]),
+    "bm_combine": (C.c_int, [P, P, P, P, I64, I64, I64, P, F32, P, P]),
+    "bm_expert_ffn_f32": (C.c_int, [P, P, P, I64, I64, I64, I32, P, I64, P, I64, P, P, P]),
+    "bm_expert_ffn_bf16_workspace": (I64, [I64, I64, I64, I64, I64]),
+    "bm_expert_ffn_bf16": (C.c_int, [P, P, P, I64, I64, I64, I32, P, I64, P, I64, I64, P, I64, P, P]),
+    "bm_set_kernel_timing": (C.c_int, [I32]),
+    "bm_kernel_times": (I64, [P, I64]),
+    "bm_coact_count": (C.c_int, [P, I64, I64, I64, P, P, P]),
+    "bm_coact_weighted": (C.c_int, [P, P, I64, I64, I64, F64, P, P]),
+    "bm_counts_to_f64": (C.c_int, [P, P, I64, F64, P, P]),
+    "bm_buddy_rank": (C.c_int, [P, I64, F64, F64, I64, P, P, P, P]),
+    "bm_cache_create": (C.c_int, [I32, I32, I32, I32, P, P, F64, F64, F64, I64, P]),
+    "bm_cache_destroy": (None, [P]),
+    "bm_cache_access": (C.c_int, [P, I32, I32, I32, I32, P]),
+    "bm_cache_apply_plan": (C.c_int, [P, I32, I64, I64, P, P, P, P, P]),
+    "bm_cache_prefetch": (C.c_int, [P, I32, P, I64]),
+    "bm_cache_settle": (C.c_int, [P, I32]),
+    "bm_cache_advance": (C.c_int, [P, F64]),
+    "bm_cache_now": (C.c_int, [P, P]),
+    "bm_cache_snapshot": (C.c_int, [P, I32, P, P]),
+    "bm_cache_predict": (C.c_int, [P, I32, P, P, P]),
+    "bm_cache_num_events": (I64, [P]),
+    "bm_cache_events": (C.c_int, [P, I64, I64, P]),
+    "bm_cache_clear_events": (None, [P]),
+    "bm_cache_layer_state": (C.c_int, [P, I32, P, P, P]),
+    "bm_cache_pending": (C.c_int, [P, I32, P, P, I64]),
+}
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """The loaded library; raises NativeLibraryError if it is unavailable."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise NativeLibraryError(
+                f"{_LIB_PATH} not built; run `python -m paper_2511_10054_b200.build` (no CPU fallback exists)")
+        try:
+            h = C.CDLL(_LIB_PATH)
+        except OSError as e:  # pragma: no cover - environment specific
+            raise NativeLibraryError(f"cannot load {_LIB_PATH}: {e}") from e
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(h, name, None)
+            if fn is None:
+                raise NativeLibraryError(f"{_LIB_PATH} does not export {name}")
+            fn.restype = res
+            fn.argtypes = args
+        _lib = h
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def call(name: str, *args) -> int:
+    """Call an int-returning ABI function and raise the mapped exception on error."""
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        raise_for(rc, f"{name}: {lib().bm_last_error().decode(errors='replace')}")
+    return rc

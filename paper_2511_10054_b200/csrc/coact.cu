@@ -1,0 +1,273 @@
+// K6 co-activation counting (shared-memory-privatised triangular counters)
+// and K7 buddy ranking (one warp per pivot, bit-exact f64 in numpy order).
+// Reference: profiler.observe / conditional_row (profiler.py:67-119),
+// buddies.cft_prefix / build_table (buddies.py:79-129).
+#include "common.cuh"
+#include "numpy_order.cuh"
+
+namespace bm {
+namespace {
+
+constexpr int kCountThreads = 512;
+constexpr int kMaxE = 256;
+constexpr int kMaxK = 32;
+
+// packed upper triangle incl. diagonal: (i <= j) -> i*E - i*(i-1)/2 + (j-i)
+__device__ __forceinline__ int tri(int i, int j, int E) { return i * E - ((i * (i - 1)) >> 1) + (j - i); }
+
+__global__ void __launch_bounds__(kCountThreads) coact_count_kernel(const int32_t *__restrict__ topk, long long N,
+                                                                    int k, int E, long long per_block,
+                                                                    unsigned long long *__restrict__ counts,
+                                                                    unsigned long long *__restrict__ pairs) {
+    extern __shared__ uint32_t tcount[];  // E*(E+1)/2
+    const int ntri = E * (E + 1) / 2;
+    for (int i = threadIdx.x; i < ntri; i += blockDim.x) tcount[i] = 0;
+    __syncthreads();
+    const long long t0 = (long long)blockIdx.x * per_block;
+    const long long t1 = min(N, t0 + per_block);
+    if (k == 8) {
+        for (long long t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+            const int4 *p = reinterpret_cast<const int4 *>(topk + t * 8);
+            int4 a = __ldg(p), b = __ldg(p + 1);
+            int id[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                atomicAdd(&tcount[tri(id[x], id[x], E)], 1u);
+#pragma unroll
+                for (int y = x + 1; y < 8; ++y) {
+                    int i = min(id[x], id[y]), j = max(id[x], id[y]);
+                    atomicAdd(&tcount[tri(i, j, E)], 1u);
+                }
+            }
+        }
+    } else {
+        for (long long t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+            int id[kMaxK];
+            for (int x = 0; x < k; ++x) id[x] = __ldg(topk + t * k + x);
+            for (int x = 0; x < k; ++x) {
+                atomicAdd(&tcount[tri(id[x], id[x], E)], 1u);
+                for (int y = x + 1; y < k; ++y) {
+                    int i = min(id[x], id[y]), j = max(id[x], id[y]);
+                    atomicAdd(&tcount[tri(i, j, E)], 1u);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // flush: diagonal -> counts, off-diagonal -> both mirror cells
+    for (int i = 0; i < E; ++i) {
+        const int base = tri(i, i, E);
+        for (int j = i + threadIdx.x; j < E; j += blockDim.x) {
+            const uint32_t v = tcount[base + (j - i)];
+            if (!v) continue;
+            if (j == i) {
+                atomicAdd(&counts[i], (unsigned long long)v);
+            } else {
+                atomicAdd(&pairs[(size_t)i * E + j], (unsigned long long)v);
+                atomicAdd(&pairs[(size_t)j * E + i], (unsigned long long)v);
+            }
+        }
+    }
+}
+
+__global__ void coact_weighted_kernel(const int32_t *__restrict__ topk, const float *__restrict__ probs, long long N,
+                                      int k, int E, double w, double *__restrict__ pw) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    for (int x = 0; x < k; ++x) {
+        const int i = topk[t * k + x];
+        const double pa = probs[t * k + x];
+        for (int y = x + 1; y < k; ++y) {
+            const int j = topk[t * k + y];
+            const double m = w * fmin(pa, (double)probs[t * k + y]);
+            atomicAdd(&pw[(size_t)i * E + j], m);
+            atomicAdd(&pw[(size_t)j * E + i], m);
+        }
+    }
+}
+
+// x + 1.0 applied n times with f64 rounding after every step, in O(#binades):
+// inside a binade [2^m, 2^(m+1)) with m >= 0 adding 1.0 is exact until the
+// result would reach 2^(m+1); only the crossing step rounds.
+__device__ double add_ones_sequential(double x, unsigned long long n) {
+    while (n > 0) {
+        if (x >= 1.0 && x < 9007199254740992.0) {  // 2^53
+            int ex;
+            frexp(x, &ex);                      // x in [2^(ex-1), 2^ex)
+            const double U = ldexp(1.0, ex);
+            const double dd = dsub(U, x);       // exact
+            unsigned long long j = (unsigned long long)ceil(dd) - 1ULL;  // steps keeping x + j < U
+            if (j > n) j = n;
+            x = dadd(x, (double)j);              // exact
+            n -= j;
+            if (n == 0) break;
+        }
+        x = dadd(x, 1.0);  // the one rounded step (or x < 1 / x >= 2^53)
+        --n;
+        if (x >= 9007199254740992.0) {
+            // beyond 2^53 adding 1.0 rounds to even each step: x stays put
+            // when its ulp is 2 and x + 1 ties to x. Fall back to stepping.
+            while (n > 0) {
+                double y = dadd(x, 1.0);
+                if (y == x) { n = 0; break; }
+                x = y;
+                --n;
+            }
+        }
+    }
+    return x;
+}
+
+// Reference accumulation order per cell (profiler.py:81-95): the warm-up
+// tokens (global index < warmup_steps) come first and each adds w, then
+// every later token adds 1.0 — all sequentially in f64. w == 0 tokens are
+// skipped (:83-84). Exact for any w, not only dyadic ones.
+__global__ void counts_to_f64_kernel(const unsigned long long *warm, const unsigned long long *main_, long long n,
+                                     double w, double *out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double x = 0.0;
+    if (warm && w != 0.0) {
+        const unsigned long long c = warm[i];
+        for (unsigned long long t = 0; t < c; ++t) x = dadd(x, w);
+    }
+    out[i] = add_ones_sequential(x, main_[i]);
+}
+
+constexpr int kRankWarps = 4;
+constexpr int kRankMaxE = 1024;
+
+__global__ void __launch_bounds__(kRankWarps * 32) buddy_rank_kernel(const double *__restrict__ M, int E, double eps,
+                                                                      double thr, int k_max, int32_t *ids,
+                                                                      double *weights, int32_t *lens) {
+    __shared__ double q[kRankWarps][kRankMaxE];
+    __shared__ int order[kRankWarps][kRankMaxE];
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const int p = blockIdx.x * kRankWarps + warp;
+    if (p >= E) return;
+    double *qw = q[warp];
+    int *ow = order[warp];
+    // conditional_row (profiler.py:113-119): row + eps, diagonal forced to 0
+    for (int j = lane; j < E; j += 32) qw[j] = (j == p) ? 0.0 : dadd(M[(size_t)p * E + j], eps);
+    __syncwarp();
+    double total = 0.0;
+    if (lane == 0) total = pairwise_sum(qw, E);
+    total = __shfl_sync(0xffffffffu, total, 0);
+    int32_t *oid = ids + (size_t)p * k_max;
+    double *ow_w = weights + (size_t)p * k_max;
+    if (!(total > 0.0)) {  // degenerate pivot -> empty list (buddies.py:118-123)
+        for (int r = lane; r < k_max; r += 32) {
+            oid[r] = -1;
+            ow_w[r] = 0.0;
+        }
+        if (lane == 0) lens[p] = 0;
+        return;
+    }
+    for (int j = lane; j < E; j += 32) qw[j] = ddiv(qw[j], total);
+    __syncwarp();
+    // stable argsort(-q): rank = #(strictly larger) + #(equal with lower id)
+    int nnz = 0;
+    for (int j = lane; j < E; j += 32) {
+        const double v = qw[j];
+        int rank = 0;
+        for (int i = 0; i < E; ++i) {
+            const double u = qw[i];
+            rank += (u > v || (u == v && i < j)) ? 1 : 0;
+        }
+        ow[rank] = j;
+        nnz += (v != 0.0) ? 1 : 0;
+    }
+    for (int off = 16; off > 0; off >>= 1) nnz += __shfl_xor_sync(0xffffffffu, nnz, off);
+    __syncwarp();
+    // cft_prefix (buddies.py:86-95): sequential cumsum, first index >= alpha - tol
+    int t = nnz;
+    if (lane == 0) {
+        double cum = 0.0;
+        for (int r = 0; r < nnz; ++r) {
+            cum = dadd(cum, qw[ow[r]]);
+            if (cum >= thr) {
+                t = r + 1;
+                break;
+            }
+        }
+    }
+    t = __shfl_sync(0xffffffffu, t, 0);
+    const int n = min(t, k_max);
+    for (int r = lane; r < k_max; r += 32) {
+        if (r < n) {
+            oid[r] = ow[r];
+            ow_w[r] = qw[ow[r]];
+        } else {
+            oid[r] = -1;
+            ow_w[r] = 0.0;
+        }
+    }
+    if (lane == 0) lens[p] = n;
+}
+
+}  // namespace
+}  // namespace bm
+
+using namespace bm;
+
+extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t E, unsigned long long *counts,
+                              unsigned long long *pairs, bm_stream_t stream) {
+    BM_REQUIRE(N >= 0 && k >= 1 && k <= kMaxK && E >= 1 && E <= kMaxE && k <= E, BM_EINVAL,
+               "bm_coact_count: bad shape N=%lld k=%lld E=%lld", (long long)N, (long long)k, (long long)E);
+    BM_REQUIRE(counts && pairs && (topk || N == 0), BM_EINVAL, "bm_coact_count: null pointer");
+    if (N == 0) return BM_OK;
+    const size_t smem = (size_t)E * (E + 1) / 2 * sizeof(uint32_t);
+    BM_CUDA_TRY(cudaFuncSetAttribute(coact_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    BM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coact_count_kernel, kCountThreads, smem));
+    if (per_sm < 1) per_sm = 1;
+    long long blocks = (long long)sm_count() * per_sm;
+    // at least ~4 tokens per thread per block so the flush amortises
+    long long min_per_block = 4LL * kCountThreads;
+    long long need = (N + min_per_block - 1) / min_per_block;
+    if (need < blocks) blocks = need;
+    if (blocks < 1) blocks = 1;
+    long long per_block = (N + blocks - 1) / blocks;
+    if (k == 8 && (reinterpret_cast<uintptr_t>(topk) & 15) != 0) {
+        BM_REQUIRE(false, BM_EINVAL, "bm_coact_count: k=8 trace must be 16-byte aligned");
+    }
+    coact_count_kernel<<<(unsigned)blocks, kCountThreads, smem, as_stream(stream)>>>(topk, N, (int)k, (int)E,
+                                                                                     per_block, counts, pairs);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_coact_weighted(const int32_t *topk, const float *probs, int64_t N, int64_t k, int64_t E, double w,
+                                 double *pair_weights, bm_stream_t stream) {
+    BM_REQUIRE(N >= 0 && k >= 1 && E >= 1 && pair_weights && (N == 0 || (topk && probs)), BM_EINVAL,
+               "bm_coact_weighted: bad args");
+    if (N == 0 || w == 0.0) return BM_OK;
+    coact_weighted_kernel<<<(unsigned)((N + 255) / 256), 256, 0, as_stream(stream)>>>(topk, probs, N, (int)k, (int)E,
+                                                                                      w, pair_weights);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_counts_to_f64(const unsigned long long *warm, const unsigned long long *main_, int64_t n,
+                                double w_warm, double *out, bm_stream_t stream) {
+    BM_REQUIRE(main_ && out && n >= 0, BM_EINVAL, "bm_counts_to_f64: bad args");
+    if (n == 0) return BM_OK;
+    counts_to_f64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(warm, main_, n, w_warm, out);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_buddy_rank(const double *pair_matrix, int64_t E, double eps, double alpha, int64_t k_max,
+                             int32_t *ids, double *weights, int32_t *lens, bm_stream_t stream) {
+    BM_REQUIRE(E >= 1 && E <= kRankMaxE, BM_EINVAL, "bm_buddy_rank: E=%lld out of range", (long long)E);
+    BM_REQUIRE(alpha > 0.0 && alpha <= 1.0, BM_EINVAL, "alpha must be in (0, 1]");
+    BM_REQUIRE(k_max >= 1, BM_EINVAL, "k_max must be >= 1");
+    BM_REQUIRE(eps >= 0.0, BM_EINVAL, "laplace_eps must be nonnegative");
+    BM_REQUIRE(pair_matrix && ids && weights && lens, BM_EINVAL, "bm_buddy_rank: null pointer");
+    const double thr = alpha - 1e-9;  // buddies.py:25,94
+    buddy_rank_kernel<<<(unsigned)((E + kRankWarps - 1) / kRankWarps), kRankWarps * 32, 0, as_stream(stream)>>>(
+        pair_matrix, (int)E, eps, thr, (int)k_max, ids, weights, lens);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}

@@ -1,0 +1,460 @@
+// bf16 grouped expert FFN on 5th-gen tensor cores (sm_100a).
+//
+// Decode is weight-streaming: every executed expert's W1/W3/W2 must cross
+// HBM once per layer-step while the token count per expert is tiny. So the
+// weights are the M=128 operand ("swap-AB") fed by TMA with 128B swizzle,
+// the permuted tokens are the N operand (16..n_tile columns) moved by plain
+// bulk copies of a pre-swizzled image (gather_sw128), and accumulators live
+// in TMEM. One persistent CTA per SM walks an equal share of the global
+// (tile, k-block) iteration space ("stream-K"), so HBM traffic is balanced
+// across all 148 SMs regardless of how many experts a step executes.
+// Split tiles are reduced deterministically (fixed CTA order, no atomics)
+// by a fixup kernel that also applies SwiGLU / tanh and writes GEMM2's B
+// operand in the same swizzled image.
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM
+// allocator, w3 idle, w4-7 epilogue (TMEM lane quadrants 0-3).
+//
+// Reference semantics: Expert.__call__ / forward_batch (model.py:85-99,
+// 318-340); SwiGLU is the Mixtral/Qwen3/DSV2 expert (no reference oracle).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace bm {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBM = 128;             // weight rows per tile (UMMA M)
+constexpr int kBK = 64;              // K per stage (one 128-byte swizzle row)
+constexpr int kATileBytes = kBM * kBK * 2;  // 16 KB
+constexpr int kMaxE = 256;
+constexpr int kSmemBudget = 220 * 1024;  // dynamic; static smem (schedule, barriers) comes on top
+
+struct Sched {
+    // device-side schedule, identical in every kernel that needs it
+    int n_act;
+    int act_e[kMaxE];
+    int act_nch[kMaxE];
+    int tile_prefix[kMaxE + 1];
+};
+
+struct GemmParams {
+    const int32_t *count;
+    const int32_t *offset;
+    const int32_t *buf_of_expert;
+    int E, M, K, nmat, n_tile;
+    int a_rows_per_buf, a_row_off0, a_row_off1;
+    const uint8_t *b_planes;  // [K/64][r_max][128 B]
+    long long b_plane_bytes;
+    float *partials;           // slot = (tile + cta) * nmat * n_tile * 128 floats
+    int num_ctas;              // launched grid (persistent)
+};
+
+__device__ void build_sched(Sched &s, const int32_t *count, int E, int n_tile, int mtiles) {
+    int n = 0, run = 0;
+    s.tile_prefix[0] = 0;
+    for (int e = 0; e < E; ++e) {
+        const int c = count[e];
+        if (c <= 0) continue;
+        const int npad = (c + 15) & ~15;
+        const int nch = (npad + n_tile - 1) / n_tile;
+        s.act_e[n] = e;
+        s.act_nch[n] = nch;
+        run += nch * mtiles;
+        s.tile_prefix[++n] = run;
+    }
+    s.n_act = n;
+}
+
+struct TileInfo {
+    int e, mtile, chunk, n;  // n = columns (tokens, padded to 16) of this tile
+    int row0;                // first permuted row of the chunk
+};
+
+__device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int mtiles, int n_tile,
+                                                const int32_t *count, const int32_t *offset) {
+    int lo = 0, hi = s.n_act - 1;
+    while (lo < hi) {  // last a with tile_prefix[a] <= t
+        int mid = (lo + hi + 1) >> 1;
+        if (s.tile_prefix[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    TileInfo ti;
+    ti.e = s.act_e[lo];
+    const int local = t - s.tile_prefix[lo];
+    const int nch = s.act_nch[lo];
+    ti.mtile = local / nch;
+    ti.chunk = local % nch;
+    const int npad = (count[ti.e] + 15) & ~15;
+    ti.n = min(n_tile, npad - ti.chunk * n_tile);
+    ti.row0 = offset[ti.e] + ti.chunk * n_tile;
+    return ti;
+}
+
+__device__ __forceinline__ long long range_start(int c, long long T, int G) { return (long long)c * T / G; }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ Sched sched;
+    __shared__ __align__(8) uint64_t bars[64];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const int mtiles = p.M / kBM;
+    const int kb_per_tile = p.K / kBK;
+
+    if (threadIdx.x == 0) build_sched(sched, p.count, p.E, p.n_tile, mtiles);
+    __syncthreads();
+    const long long T = (long long)sched.tile_prefix[sched.n_act] * kb_per_tile;
+    const int G = (int)min((long long)p.num_ctas, T);
+    const int cta = blockIdx.x;
+    if (cta >= G) return;  // uniform for the whole CTA
+    const long long it0 = range_start(cta, T, G), it1 = range_start(cta + 1, T, G);
+
+    // smem carve-up: stages of [A0 | A1 | B], 1024-aligned
+    const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t b_bytes_max = (uint32_t)p.n_tile * 128u;
+    const uint32_t stage_bytes = (uint32_t)p.nmat * kATileBytes + ((b_bytes_max + 1023u) & ~1023u);
+    const int stages = min(16, (int)((kSmemBudget - 1024) / stage_bytes));
+    const int acc_stages = (2 * p.nmat * p.n_tile <= 512) ? 2 : 1;
+    const uint32_t acc_cols = acc_stages == 2 ? 256u : 512u;
+
+    const uint32_t full0 = ptx::smem_u32(&bars[0]);        // [stages]
+    const uint32_t empty0 = ptx::smem_u32(&bars[16]);      // [stages]
+    const uint32_t tfull0 = ptx::smem_u32(&bars[32]);      // [2]
+    const uint32_t tempty0 = ptx::smem_u32(&bars[34]);     // [2]
+
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < stages; ++s) {
+            ptx::mbar_init(full0 + 8 * s, 1);
+            ptx::mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull0 + 8 * a, 1);
+            ptx::mbar_init(tempty0 + 8 * a, 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_a);
+    if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(&tmem_base_sh), 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = tmem_base_sh;
+
+    if (warp == 0 && lane == 0) {
+        // ===================== TMA producer =====================
+        const uint64_t pol = ptx::policy_evict_first();  // weights stream through once
+        int stage = 0;
+        uint32_t phase = 0;
+        long long it = it0;
+        while (it < it1) {
+            const int tile = (int)(it / kb_per_tile);
+            const int kb_end = (int)min((long long)kb_per_tile, it1 - (long long)tile * kb_per_tile);
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile, p.count, p.offset);
+            const int buf = p.buf_of_expert[ti.e];
+            const int arow = buf * p.a_rows_per_buf + ti.mtile * kBM;
+            const uint32_t bbytes = (uint32_t)ti.n * 128u;
+            for (int kb = (int)(it - (long long)tile * kb_per_tile); kb < kb_end; ++kb, ++it) {
+                ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+                const uint32_t sA = base + (uint32_t)stage * stage_bytes;
+                const uint32_t sB = sA + (uint32_t)p.nmat * kATileBytes;
+                const uint32_t fb = full0 + 8 * stage;
+                ptx::mbar_expect_tx(fb, (uint32_t)p.nmat * kATileBytes + bbytes);
+                ptx::tma_load_2d(sA, &tmap_a, fb, kb * kBK, arow + p.a_row_off0, pol);
+                if (p.nmat == 2) ptx::tma_load_2d(sA + kATileBytes, &tmap_a, fb, kb * kBK, arow + p.a_row_off1, pol);
+                ptx::bulk_load(sB, p.b_planes + (long long)kb * p.b_plane_bytes + (long long)ti.row0 * 128, bbytes, fb);
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ===================== MMA issuer (single thread) =====================
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        long long it = it0;
+        while (it < it1) {
+            const int tile = (int)(it / kb_per_tile);
+            const int kb_end = (int)min((long long)kb_per_tile, it1 - (long long)tile * kb_per_tile);
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile, p.count, p.offset);
+            const uint32_t idesc = ptx::idesc_bf16_f32(kBM, (uint32_t)ti.n);
+            ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1u);
+            ptx::tc_fence_after();
+            const uint32_t dcol = tmem_base + (uint32_t)acc * acc_cols;
+            bool first = true;
+            for (int kb = (int)(it - (long long)tile * kb_per_tile); kb < kb_end; ++kb, ++it) {
+                ptx::mbar_wait(full0 + 8 * stage, phase);
+                ptx::tc_fence_after();
+                const uint32_t sA = base + (uint32_t)stage * stage_bytes;
+                const uint32_t sB = sA + (uint32_t)p.nmat * kATileBytes;
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                    const uint64_t bdesc = ptx::sw128_desc(sB + kk * 32);
+                    for (int m = 0; m < p.nmat; ++m) {
+                        const uint64_t adesc = ptx::sw128_desc(sA + m * kATileBytes + kk * 32);
+                        ptx::mma_bf16(dcol + (uint32_t)(m * p.n_tile), adesc, bdesc, idesc,
+                                      (first && kk == 0) ? 0u : 1u);
+                    }
+                }
+                first = false;
+                ptx::mma_commit(empty0 + 8 * stage);  // frees the smem stage when these MMAs finish
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+            ptx::mma_commit(tfull0 + 8 * acc);  // accumulator ready for the epilogue
+            if (acc_stages == 2) {
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1u;
+            } else {
+                acc_phase ^= 1u;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue: TMEM -> fp32 partial slot =====================
+        const int q = warp - 4;  // TMEM lane quadrant
+        const int m_local = q * 32 + (int)lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        long long it = it0;
+        while (it < it1) {
+            const int tile = (int)(it / kb_per_tile);
+            const long long tile_end = (long long)(tile + 1) * kb_per_tile;
+            it = min(tile_end, it1);
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile, p.count, p.offset);
+            ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
+            ptx::tc_fence_after();
+            const long long slot = (long long)tile + cta;
+            float *dst = p.partials + slot * (long long)p.nmat * p.n_tile * kBM;
+            const uint32_t tbase = tmem_base + (uint32_t)acc * acc_cols + ((uint32_t)(q * 32) << 16);
+            for (int m = 0; m < p.nmat; ++m) {
+                for (int c0 = 0; c0 < ti.n; c0 += 16) {
+                    float v[16];
+                    ptx::tmem_ld16(tbase + (uint32_t)(m * p.n_tile + c0), v);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) dst[((long long)m * p.n_tile + c0 + j) * kBM + m_local] = v[j];
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty0 + 8 * acc);
+            if (acc_stages == 2) {
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1u;
+            } else {
+                acc_phase ^= 1u;
+            }
+        }
+    }
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
+}
+
+// ---------------------------------------------------------------- fixups
+__device__ __forceinline__ int cta_of(long long i, long long T, int G) {
+    return (int)(((i + 1) * (long long)G - 1) / T);
+}
+
+// mode 0: SwiGLU (nmat 2) / 1: tanh (nmat 1) -> H as bf16 SW128 planes
+// mode 2: plain (nmat 1) -> y_perm fp32 [r_max][M]
+__global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, uint4 *h_planes, int h_rmax,
+                                                        float *y_perm) {
+    __shared__ Sched sched;
+    const int mtiles = p.M / kBM;
+    const int kb_per_tile = p.K / kBK;
+    if (threadIdx.x == 0) build_sched(sched, p.count, p.E, p.n_tile, mtiles);
+    __syncthreads();
+    const int ntiles = sched.tile_prefix[sched.n_act];
+    const long long T = (long long)ntiles * kb_per_tile;
+    const int G = (int)min((long long)p.num_ctas, T);
+    const int m_local = threadIdx.x;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile, p.count, p.offset);
+        const int c0 = cta_of((long long)tile * kb_per_tile, T, G);
+        const int c1 = cta_of((long long)(tile + 1) * kb_per_tile - 1, T, G);
+        const long long slot_elems = (long long)p.nmat * p.n_tile * kBM;
+        const int m = ti.mtile * kBM + m_local;
+        for (int n = 0; n < ti.n; ++n) {
+            float g = 0.f, u = 0.f;
+            for (int c = c0; c <= c1; ++c) {
+                const float *src = p.partials + ((long long)tile + c) * slot_elems;
+                g += src[(long long)n * kBM + m_local];
+                if (p.nmat == 2) u += src[((long long)p.n_tile + n) * kBM + m_local];
+            }
+            const int row = ti.row0 + n;
+            if (mode == 2) {
+                y_perm[(long long)row * p.M + m] = g;
+            } else {
+                const float h = mode == 0 ? (g / (1.0f + expf(-g))) * u : tanhf(g);
+                // bf16 SW128 image: plane m/64, chunk (m%64)/8 at position chunk ^ (row & 7)
+                __nv_bfloat16 *hp = reinterpret_cast<__nv_bfloat16 *>(h_planes);
+                const int plane = m >> 6, chunk = (m & 63) >> 3;
+                const long long idx = ((long long)plane * h_rmax + row) * 64 + ((chunk ^ (row & 7)) << 3) + (m & 7);
+                hp[idx] = __float2bfloat16_rn(h);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------- host helpers
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+int make_weight_map(CUtensorMap *map, const void *arena, long long rows, int K) {
+    PFN_encodeTiled enc = get_encode();
+    BM_REQUIRE(enc, BM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(arena), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    BM_REQUIRE(r == CUDA_SUCCESS, BM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return BM_OK;
+}
+
+long long max_tiles(long long E, long long M, long long r_max, long long n_tile) {
+    const long long segs = std::min(E, std::max(1LL, r_max / 16));
+    return (M / kBM) * (segs + r_max / n_tile + 1);
+}
+
+// kernel timing (for the bench's roofline), off by default
+struct Timing {
+    bool enabled = false;
+    std::vector<cudaEvent_t> ev;  // 3 per call: before G1, between, after G2
+    std::mutex mu;
+} g_timing;
+
+int record_event(cudaStream_t s) {
+    cudaEvent_t e;
+    BM_CUDA_TRY(cudaEventCreate(&e));
+    BM_CUDA_TRY(cudaEventRecord(e, s));
+    g_timing.ev.push_back(e);
+    return BM_OK;
+}
+
+}  // namespace
+}  // namespace bm
+
+using namespace bm;
+
+extern "C" int64_t bm_expert_ffn_bf16_workspace(int64_t E, int64_t d, int64_t f, int64_t r_max, int64_t n_tile) {
+    const long long M = std::max(d, f);
+    const long long slots = max_tiles(E, M, r_max, n_tile) + sm_count() + 1;
+    const long long partial_bytes = slots * 2 * n_tile * kBM * 4;
+    const long long h_bytes = (f / 64) * r_max * 128;
+    return ((partial_bytes + 1023) / 1024) * 1024 + h_bytes;
+}
+
+extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const int32_t *expert_offset,
+                                  int64_t E, int64_t d, int64_t f, int32_t act, const void *w_arena, int64_t n_bufs,
+                                  const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
+                                  int64_t workspace_bytes, float *y_perm, bm_stream_t stream) {
+    BM_REQUIRE(x_perm && expert_count && expert_offset && w_arena && buf_of_expert && workspace && y_perm,
+               BM_EINVAL, "bm_expert_ffn_bf16: null pointer");
+    BM_REQUIRE(E >= 1 && E <= kMaxE, BM_EINVAL, "E out of range");
+    BM_REQUIRE(d % kBM == 0 && f % kBM == 0 && d > 0 && f > 0, BM_EINVAL, "d and f must be multiples of 128");
+    BM_REQUIRE(n_tile >= 16 && n_tile <= 256 && n_tile % 16 == 0, BM_EINVAL, "n_tile must be 16..256, multiple of 16");
+    BM_REQUIRE(act == BM_ACT_SWIGLU || act == BM_ACT_TANH, BM_EINVAL, "bad activation");
+    BM_REQUIRE(r_max % 16 == 0, BM_EINVAL, "r_max must be a multiple of 16");
+    BM_REQUIRE(workspace_bytes >= bm_expert_ffn_bf16_workspace(E, d, f, r_max, n_tile), BM_EINVAL,
+               "workspace too small");
+    if (r_max == 0) return BM_OK;
+    cudaStream_t s = as_stream(stream);
+    const long long buf_elems = (act == BM_ACT_SWIGLU ? 3 : 2) * d * f;
+    const long long slots_bytes = ((workspace_bytes - (f / 64) * r_max * 128) / 1024) * 1024;
+    float *partials = static_cast<float *>(workspace);
+    uint8_t *h_planes = static_cast<uint8_t *>(workspace) + slots_bytes;
+    const int G = sm_count();
+
+    // A operand views of the weight arena
+    CUtensorMap map1, map2;
+    if (int rc = make_weight_map(&map1, w_arena, n_bufs * (buf_elems / d), (int)d)) return rc;
+    if (int rc = make_weight_map(&map2, w_arena, n_bufs * (buf_elems / f), (int)f)) return rc;
+
+    GemmParams g1{expert_count, expert_offset, buf_of_expert, (int)E, (int)f, (int)d,
+                  act == BM_ACT_SWIGLU ? 2 : 1, (int)n_tile, (int)(buf_elems / d), 0, (int)f,
+                  static_cast<const uint8_t *>(x_perm), r_max * 128, partials, G};
+    GemmParams g2{expert_count, expert_offset, buf_of_expert, (int)E, (int)d, (int)f, 1, (int)n_tile,
+                  (int)(buf_elems / f), act == BM_ACT_SWIGLU ? (int)(2 * d) : (int)d, 0, h_planes, r_max * 128,
+                  partials, G};
+
+    static bool attr_set = false;
+    if (!attr_set) {
+        BM_CUDA_TRY(cudaFuncSetAttribute(ffn_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+        attr_set = true;
+    }
+    const bool timing = g_timing.enabled;
+    std::lock_guard<std::mutex> lk(g_timing.mu);
+    if (timing && record_event(s)) return BM_ECUDA;
+    ffn_gemm_kernel<<<G, kThreads, kSmemBudget, s>>>(map1, g1);
+    BM_LAUNCH_CHECK();
+    if (timing && record_event(s)) return BM_ECUDA;
+    const int fix_blocks = 4 * G;
+    ffn_fixup_kernel<<<fix_blocks, kBM, 0, s>>>(g1, act == BM_ACT_SWIGLU ? 0 : 1, reinterpret_cast<uint4 *>(h_planes),
+                                                (int)r_max, nullptr);
+    BM_LAUNCH_CHECK();
+    if (timing && record_event(s)) return BM_ECUDA;
+    ffn_gemm_kernel<<<G, kThreads, kSmemBudget, s>>>(map2, g2);
+    BM_LAUNCH_CHECK();
+    if (timing && record_event(s)) return BM_ECUDA;
+    ffn_fixup_kernel<<<fix_blocks, kBM, 0, s>>>(g2, 2, nullptr, 0, y_perm);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_set_kernel_timing(int32_t enable) {
+    std::lock_guard<std::mutex> lk(g_timing.mu);
+    for (cudaEvent_t e : g_timing.ev) cudaEventDestroy(e);
+    g_timing.ev.clear();
+    g_timing.enabled = enable != 0;
+    return BM_OK;
+}
+
+// Two floats per bm_expert_ffn_bf16 call since timing was enabled: GEMM1
+// and GEMM2 kernel durations in ms (CUDA events on the launching stream).
+extern "C" int64_t bm_kernel_times(float *out_host, int64_t cap) {
+    std::lock_guard<std::mutex> lk(g_timing.mu);
+    int64_t n = 0;
+    for (size_t i = 0; i + 3 < g_timing.ev.size() && n + 2 <= cap; i += 4) {
+        if (cudaEventSynchronize(g_timing.ev[i + 3]) != cudaSuccess) return -1;
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, g_timing.ev[i], g_timing.ev[i + 1]);
+        cudaEventElapsedTime(&b, g_timing.ev[i + 2], g_timing.ev[i + 3]);
+        out_host[n++] = a;
+        out_host[n++] = b;
+    }
+    return n;
+}

@@ -1,0 +1,202 @@
+// K1 — fused router: GEMV + bias + warp top-k + renormalised softmax + TAE /
+// margin token gate. One CTA per token. Replaces model.route_batch
+// (reference model.py:231-280) and gating.tae/margin/token_gate
+// (gating.py:71-108).
+#include <float.h>
+#include <math.h>
+
+#include "common.cuh"
+
+namespace bm {
+namespace {
+
+constexpr int kGateThreads = 256;
+constexpr int kMaxE = 256;
+constexpr int kMaxK = 32;
+
+template <typename T>
+struct Cand {
+    T v;
+    int i;
+};
+
+// Reference order: stable argsort of -z => value descending, ties to the
+// lower expert id (model.py:261).
+template <typename T>
+__device__ __forceinline__ bool better(T av, int ai, T bv, int bi) {
+    return av > bv || (av == bv && ai < bi);
+}
+
+template <typename T>
+__device__ void select_and_gate(const T *z, int E, int k, double temperature, double tau, double gamma,
+                                int32_t *topk, float *probs, double *probs64, double *tae, double *margin,
+                                uint8_t *allowed) {
+    // called by one full warp
+    const unsigned lane = lane_id();
+    unsigned taken = 0;  // bit j: element lane + 32*j already selected
+    __shared__ int sel_i[kMaxK];
+    __shared__ double sel_z[kMaxK];
+    for (int s = 0; s < k; ++s) {
+        T bv = T(0);
+        int bi = INT_MAX;
+        bool have = false;
+        for (int j = 0; lane + 32 * j < (unsigned)E; ++j) {
+            if (taken & (1u << j)) continue;
+            int e = lane + 32 * j;
+            T v = z[e];
+            if (!have || better(v, e, bv, bi)) {
+                bv = v;
+                bi = e;
+                have = true;
+            }
+        }
+        if (!have) bi = INT_MAX;
+        for (int off = 16; off > 0; off >>= 1) {
+            T ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (oi != INT_MAX && (bi == INT_MAX || better(ov, oi, bv, bi))) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if ((unsigned)(bi & 31) == lane) taken |= 1u << (bi >> 5);
+        if (lane == 0) {
+            sel_i[s] = bi;
+            sel_z[s] = (double)bv;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        // softmax(z/T) restricted to the selection (model.py:259,262-263):
+        // the max over all E of z/T is the top-1's, the full denominator
+        // cancels in the renormalisation.
+        double zmax = sel_z[0] / temperature;
+        double e[kMaxK];
+        double s = 0.0;
+        for (int i = 0; i < k; ++i) {
+            e[i] = exp(sel_z[i] / temperature - zmax);
+            s += e[i];
+        }
+        double h = 0.0;
+        for (int i = 0; i < k; ++i) {
+            double p = e[i] / s;
+            e[i] = p;
+            topk[i] = sel_i[i];
+            if (probs) probs[i] = (float)p;
+            if (probs64) probs64[i] = p;
+            if (p > 0.0) h -= p * log(p);
+        }
+        double t = 0.0, m = 1.0;
+        if (k > 1) {
+            t = fmin(1.0, fmax(0.0, h / log((double)k)));
+            m = e[0] - e[1];
+        }
+        if (tae) *tae = t;
+        if (margin) *margin = m;
+        bool ok = !(t <= tau);
+        if (gamma >= 0.0 && m >= gamma) ok = false;
+        if (allowed) *allowed = ok ? 1 : 0;
+    }
+}
+
+__global__ void __launch_bounds__(kGateThreads) gate_kernel(const float *__restrict__ x, const float *__restrict__ wg,
+                                                            const float *__restrict__ bias, int E, int d, int k,
+                                                            double temperature, double tau, double gamma,
+                                                            float *logits, int32_t *topk, float *probs, double *tae,
+                                                            double *margin, uint8_t *allowed) {
+    extern __shared__ __align__(16) float smem_x[];
+    __shared__ float z[kMaxE];
+    const int b = blockIdx.x;
+    const float *xr = x + (size_t)b * d;
+    const bool vec = (d % 4) == 0;
+    if (vec) {
+        const float4 *src = reinterpret_cast<const float4 *>(xr);
+        float4 *dst = reinterpret_cast<float4 *>(smem_x);
+        for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
+    } else {
+        for (int i = threadIdx.x; i < d; i += blockDim.x) smem_x[i] = xr[i];
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const unsigned lane = lane_id();
+    for (int e = warp; e < E; e += nwarps) {
+        const float *w = wg + (size_t)e * d;
+        float acc = 0.f;
+        if (vec) {
+            const float4 *w4 = reinterpret_cast<const float4 *>(w);
+            const float4 *x4 = reinterpret_cast<const float4 *>(smem_x);
+            for (int i = lane; i < d / 4; i += 32) {
+                float4 a = __ldg(w4 + i), c = x4[i];
+                acc = fmaf(a.x, c.x, acc);
+                acc = fmaf(a.y, c.y, acc);
+                acc = fmaf(a.z, c.z, acc);
+                acc = fmaf(a.w, c.w, acc);
+            }
+        } else {
+            for (int i = lane; i < d; i += 32) acc = fmaf(__ldg(w + i), smem_x[i], acc);
+        }
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) {
+            float v = acc + (bias ? bias[e] : 0.f);
+            z[e] = v;
+            if (logits) logits[(size_t)b * E + e] = v;
+        }
+    }
+    __syncthreads();
+    if (warp == 0)
+        select_and_gate<float>(z, E, k, temperature, tau, gamma, topk + (size_t)b * k, probs ? probs + (size_t)b * k : nullptr,
+                               nullptr, tae ? tae + b : nullptr, margin ? margin + b : nullptr,
+                               allowed ? allowed + b : nullptr);
+}
+
+__global__ void __launch_bounds__(32) select_f64_kernel(const double *__restrict__ logits, int E, int k,
+                                                        double temperature, double tau, double gamma,
+                                                        int32_t *topk, float *probs, double *probs64,
+                                                        double *tae, double *margin, uint8_t *allowed) {
+    __shared__ double z[kMaxE];
+    const int b = blockIdx.x;
+    for (int e = threadIdx.x; e < E; e += 32) z[e] = logits[(size_t)b * E + e];
+    __syncwarp();
+    select_and_gate<double>(z, E, k, temperature, tau, gamma, topk + (size_t)b * k,
+                            probs ? probs + (size_t)b * k : nullptr, probs64 ? probs64 + (size_t)b * k : nullptr,
+                            tae ? tae + b : nullptr, margin ? margin + b : nullptr, allowed ? allowed + b : nullptr);
+}
+
+}  // namespace
+}  // namespace bm
+
+using namespace bm;
+
+extern "C" int bm_gate_topk(const float *x, const float *wg, const float *bias, int64_t B, int64_t E, int64_t d,
+                            int64_t k, double temperature, double tau, double gamma, float *logits, int32_t *topk,
+                            float *probs, double *tae, double *margin, uint8_t *token_allowed, bm_stream_t stream) {
+    BM_REQUIRE(B >= 0 && E >= 1 && E <= kMaxE && d >= 1 && k >= 1 && k <= kMaxK && k <= E, BM_EINVAL,
+               "bm_gate_topk: bad shape B=%lld E=%lld d=%lld k=%lld", (long long)B, (long long)E, (long long)d,
+               (long long)k);
+    BM_REQUIRE(temperature > 0.0, BM_EINVAL, "temperature must be > 0");
+    BM_REQUIRE(x && wg && topk, BM_EINVAL, "bm_gate_topk: null pointer");
+    if (B == 0) return BM_OK;
+    size_t smem = (size_t)d * sizeof(float);
+    BM_REQUIRE(smem <= 200 * 1024, BM_EINVAL, "bm_gate_topk: d=%lld too large", (long long)d);
+    if (smem > 48 * 1024)
+        BM_CUDA_TRY(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gate_kernel<<<(unsigned)B, kGateThreads, smem, as_stream(stream)>>>(x, wg, bias, (int)E, (int)d, (int)k,
+                                                                      temperature, tau, gamma, logits, topk, probs,
+                                                                      tae, margin, token_allowed);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_select_topk_f64(const double *logits, int64_t B, int64_t E, int64_t k, double temperature,
+                                  double tau, double gamma, int32_t *topk, float *probs, double *probs64,
+                                  double *tae, double *margin, uint8_t *token_allowed, bm_stream_t stream) {
+    BM_REQUIRE(B >= 0 && E >= 1 && E <= kMaxE && k >= 1 && k <= kMaxK && k <= E, BM_EINVAL,
+               "bm_select_topk_f64: bad shape");
+    BM_REQUIRE(temperature > 0.0, BM_EINVAL, "temperature must be > 0");
+    BM_REQUIRE(logits && topk, BM_EINVAL, "bm_select_topk_f64: null pointer");
+    if (B == 0) return BM_OK;
+    select_f64_kernel<<<(unsigned)B, 32, 0, as_stream(stream)>>>(logits, (int)E, (int)k, temperature, tau, gamma,
+                                                                topk, probs, probs64, tae, margin, token_allowed);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}

@@ -1,0 +1,230 @@
+// K3 permute (warp-scan histogram, stable), row gather into the GEMM's
+// operand layout, and K5 combine + layer_update epilogue.
+// Reference semantics: model._plan_arrays / forward_batch / layer_update
+// (model.py:294-347).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace bm {
+namespace {
+
+constexpr int kPermThreads = 1024;
+constexpr int kPermMaxE = 256;
+
+__global__ void __launch_bounds__(kPermThreads) permute_kernel(const int32_t *__restrict__ executed,
+                                                               const uint8_t *__restrict__ kind, int nslots, int k,
+                                                               int E, int align, int32_t *expert_count,
+                                                               int32_t *expert_offset, int32_t *row_token,
+                                                               int32_t *slot_row) {
+    __shared__ int cnt[kPermMaxE];
+    __shared__ int off[kPermMaxE + 1];
+    __shared__ int base[kPermMaxE];
+    __shared__ int warp_cnt[kPermThreads / 32][kPermMaxE];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const unsigned lane = lane_id();
+    for (int e = tid; e < E; e += blockDim.x) {
+        cnt[e] = 0;
+        base[e] = 0;
+    }
+    __syncthreads();
+    // pass 1: histogram of executed experts (dropped slots excluded)
+    for (int i = tid; i < nslots; i += blockDim.x)
+        if (kind[i] != BM_KIND_DROPPED) atomicAdd(&cnt[executed[i]], 1);
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int e = 0; e < E; ++e) {
+            off[e] = run;
+            run += (cnt[e] + align - 1) / align * align;
+        }
+        off[E] = run;
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += blockDim.x) expert_count[e] = cnt[e];
+    for (int e = tid; e <= E; e += blockDim.x) expert_offset[e] = off[e];
+    // padding rows
+    for (int e = 0; e < E; ++e)
+        for (int r = off[e] + cnt[e] + tid; r < off[e + 1]; r += blockDim.x) row_token[r] = -1;
+    // pass 2: stable rank of each slot inside its expert segment, chunk by chunk
+    const int nw = blockDim.x >> 5;
+    for (int c0 = 0; c0 < nslots; c0 += blockDim.x) {
+        for (int i = tid; i < nw * E; i += blockDim.x) (&warp_cnt[0][0])[(i / E) * kPermMaxE + (i % E)] = 0;
+        __syncthreads();
+        const int i = c0 + tid;
+        int e = -1;
+        if (i < nslots && kind[i] != BM_KIND_DROPPED) e = executed[i];
+        const unsigned peers = __match_any_sync(0xffffffffu, e);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        if (e >= 0 && rank == 0) warp_cnt[warp][e] = __popc(peers);
+        __syncthreads();
+        // exclusive prefix over warps, per expert
+        for (int x = tid; x < E; x += blockDim.x) {
+            int run = 0;
+            for (int w = 0; w < nw; ++w) {
+                int v = warp_cnt[w][x];
+                warp_cnt[w][x] = run;
+                run += v;
+            }
+            cnt[x] = run;  // reuse cnt as this chunk's total
+        }
+        __syncthreads();
+        if (i < nslots) {
+            if (e >= 0) {
+                const int row = off[e] + base[e] + warp_cnt[warp][e] + rank;
+                row_token[row] = i / k;
+                slot_row[i] = row;
+            } else {
+                slot_row[i] = -1;
+            }
+        }
+        __syncthreads();
+        for (int x = tid; x < E; x += blockDim.x) base[x] += cnt[x];
+        __syncthreads();
+    }
+}
+
+// layout 0: fp32 row-major [r_max][d]
+__global__ void gather_f32_kernel(const float *__restrict__ x, int d, const int32_t *__restrict__ row_token,
+                                  const int32_t *__restrict__ expert_offset, int E, float *__restrict__ out) {
+    const int rows = expert_offset[E];
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    const int t = row_token[r];
+    float *dst = out + (size_t)r * d;
+    if ((d & 3) == 0) {
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
+        const float4 *s4 = reinterpret_cast<const float4 *>(x + (size_t)(t < 0 ? 0 : t) * d);
+        for (int i = threadIdx.x; i < d / 4; i += blockDim.x) d4[i] = t < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : s4[i];
+    } else {
+        for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = t < 0 ? 0.f : x[(size_t)t * d + i];
+    }
+}
+
+// layout 1: bf16 SW128 K-major planes [d/64][r_max][64], 16-byte chunk j of
+// row r at chunk position j ^ (r & 7) — the smem image of a 128B-swizzled
+// UMMA operand, so the GEMM moves it with a plain bulk copy.
+__global__ void gather_sw128_kernel(const float *__restrict__ x, int d, const int32_t *__restrict__ row_token,
+                                    const int32_t *__restrict__ expert_offset, int E, int r_max,
+                                    uint4 *__restrict__ out) {
+    const int rows = expert_offset[E];
+    const int chunks_per_row = d / 8;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)rows * chunks_per_row) return;
+    const int r = (int)(idx / chunks_per_row);
+    const int c = (int)(idx % chunks_per_row);  // 8-column chunk index along d
+    const int plane = c >> 3, j = c & 7;
+    const int t = row_token[r];
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t >= 0) {
+        const float4 *s = reinterpret_cast<const float4 *>(x + (size_t)t * d + (size_t)c * 8);
+        float4 a = s[0], b = s[1];
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y), p1 = __floats2bfloat162_rn(a.z, a.w);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(b.x, b.y), p3 = __floats2bfloat162_rn(b.z, b.w);
+        v.x = *reinterpret_cast<uint32_t *>(&p0);
+        v.y = *reinterpret_cast<uint32_t *>(&p1);
+        v.z = *reinterpret_cast<uint32_t *>(&p2);
+        v.w = *reinterpret_cast<uint32_t *>(&p3);
+    }
+    out[((size_t)plane * r_max + r) * 8 + (j ^ (r & 7))] = v;
+}
+
+constexpr int kCombineThreads = 256;
+
+__global__ void __launch_bounds__(kCombineThreads) combine_kernel(const float *__restrict__ y_perm,
+                                                                  const int32_t *__restrict__ slot_row,
+                                                                  const float *__restrict__ probs,
+                                                                  const uint8_t *__restrict__ kind, int k, int d,
+                                                                  const float *__restrict__ h_in, float scale,
+                                                                  float *__restrict__ out) {
+    extern __shared__ __align__(16) float hbuf[];
+    __shared__ float red[kCombineThreads / 32];
+    const int b = blockIdx.x;
+    float ssq = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        float y = 0.f;
+        for (int s = 0; s < k; ++s) {
+            const int r = slot_row[b * k + s];
+            if (r < 0 || kind[b * k + s] == BM_KIND_DROPPED) continue;
+            y = fmaf(probs[b * k + s], y_perm[(size_t)r * d + i], y);
+        }
+        if (h_in) {
+            float h = fmaf(scale, y, h_in[(size_t)b * d + i]);
+            hbuf[i] = h;
+            ssq = fmaf(h, h, ssq);
+        } else {
+            out[(size_t)b * d + i] = y;
+        }
+    }
+    if (!h_in) return;
+    for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+    if (lane_id() == 0) red[threadIdx.x >> 5] = ssq;
+    __syncthreads();
+    float tot = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    const float rms = sqrtf(tot / (float)d);
+    const float inv = 1.0f / fmaxf(rms, 1e-12f);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) out[(size_t)b * d + i] = hbuf[i] * inv;
+}
+
+}  // namespace
+}  // namespace bm
+
+using namespace bm;
+
+extern "C" int64_t bm_permute_rows_max(int64_t B, int64_t k, int64_t E, int64_t row_align) {
+    int64_t n = B * k;
+    int64_t segs = n < E ? n : E;
+    return n + segs * (row_align - 1);
+}
+
+extern "C" int bm_permute(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E,
+                          int64_t row_align, int32_t *expert_count, int32_t *expert_offset, int32_t *row_token,
+                          int32_t *slot_row, bm_stream_t stream) {
+    BM_REQUIRE(B >= 0 && k >= 1 && E >= 1 && E <= kPermMaxE && row_align >= 1 && row_align <= 256, BM_EINVAL,
+               "bm_permute: bad shape");
+    BM_REQUIRE(executed && kind && expert_count && expert_offset && row_token && slot_row, BM_EINVAL,
+               "bm_permute: null pointer");
+    permute_kernel<<<1, kPermThreads, 0, as_stream(stream)>>>(executed, kind, (int)(B * k), (int)k, (int)E,
+                                                             (int)row_align, expert_count, expert_offset,
+                                                             row_token, slot_row);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_gather_rows(const float *x, int64_t B, int64_t d, const int32_t *row_token,
+                              const int32_t *expert_offset, int64_t E, int64_t r_max, int32_t layout, void *x_perm,
+                              bm_stream_t stream) {
+    BM_REQUIRE(x && row_token && expert_offset && x_perm && d >= 1 && r_max >= 0, BM_EINVAL, "bm_gather_rows: bad args");
+    (void)B;
+    if (r_max == 0) return BM_OK;
+    if (layout == 0) {
+        gather_f32_kernel<<<(unsigned)r_max, 256, 0, as_stream(stream)>>>(x, (int)d, row_token, expert_offset,
+                                                                          (int)E, static_cast<float *>(x_perm));
+    } else if (layout == 1) {
+        BM_REQUIRE(d % 64 == 0, BM_EINVAL, "SW128 layout needs d %% 64 == 0");
+        long long n = r_max * (d / 8);
+        gather_sw128_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+            x, (int)d, row_token, expert_offset, (int)E, (int)r_max, static_cast<uint4 *>(x_perm));
+    } else {
+        BM_REQUIRE(false, BM_EINVAL, "bm_gather_rows: unknown layout %d", layout);
+    }
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_combine(const float *y_perm, const int32_t *slot_row, const float *probs, const uint8_t *kind,
+                          int64_t B, int64_t k, int64_t d, const float *h_in, float residual_scale, float *out,
+                          bm_stream_t stream) {
+    BM_REQUIRE(y_perm && slot_row && probs && kind && out && B >= 0 && k >= 1 && d >= 1, BM_EINVAL,
+               "bm_combine: bad args");
+    if (B == 0) return BM_OK;
+    size_t smem = h_in ? (size_t)d * sizeof(float) : 0;
+    BM_REQUIRE(smem <= 200 * 1024, BM_EINVAL, "bm_combine: d too large");
+    if (smem > 48 * 1024)
+        BM_CUDA_TRY(cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    combine_kernel<<<(unsigned)B, kCombineThreads, smem, as_stream(stream)>>>(y_perm, slot_row, probs, kind, (int)k,
+                                                                            (int)d, h_in, residual_scale, out);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}

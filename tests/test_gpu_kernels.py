@@ -1,0 +1,312 @@
+"""Parity of every CUDA kernel against the oracle / reference golden vectors.
+
+All tests call through the C-ABI (libbmoe.so via ctypes). Bit-exact for
+integer / index / table work; tolerances are stated where floating point
+differs (fp32 mode rel 1e-5, bf16 mode rel 2e-2 vs an fp32 reference).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import golden
+from paper_2511_10054_b200 import ops
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _t(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def _corpus(name):
+    g = golden(name)
+    for i in range(g["E"].shape[0]):
+        E, k = int(g["E"][i]), int(g["k"][i])
+        yield dict(E=E, k=k, topk=g["topk"][i, :k], logits=g["logits"][i, :E], mask=g["mask"][i, :E],
+                   ids=g["ids"][i, :E], w=g["w"][i, :E], lens=g["lens"][i, :E], h=int(g["h"][i]),
+                   rho=int(g["rho"][i]), allowed=bool(g["allowed"][i]), eta=float(g["eta"][i]),
+                   kappa=float(g["kappa"][i]), part=g["part"][i, :E] if g["has_part"][i] else None,
+                   fallback=int(g["fallback"][i]), executed=g["executed"][i, :k], kind=g["kind"][i, :k],
+                   used=int(g["used"][i]))
+
+
+@pytest.mark.parametrize("name", ["remap_corpus_20260819.npz", "remap_corpus_1234.npz"])
+def test_remap_kernel_bit_exact_on_reference_corpus(cuda_ok, name):
+    """K2 vs the reference planner on the acceptance (1000, seed 20260819) and
+    fuzz (300, seed 1234) corpora, incl. Psi ordering, rho, H, drop fallback."""
+    n = 0
+    for c in _corpus(name):
+        table = ops.DeviceTable(_t(c["ids"]), _t(c["w"]), _t(c["lens"]))
+        plan = ops.buddy_remap(
+            _t(c["topk"][None, :], torch.int32), _t(np.array([c["allowed"]], np.uint8)),
+            ops.bitmap_from_mask(c["mask"], DEV), table, H=c["h"], rho=None if c["rho"] < 0 else c["rho"],
+            fallback=c["fallback"], beta=2.0, eta=c["eta"], kappa=c["kappa"],
+            partition_of=None if c["part"] is None else _t(c["part"], torch.int32), hop=1.0,
+            logits=_t(c["logits"][None, :]))
+        ex = plan.executed.cpu().numpy()[0]
+        kd = plan.kind.cpu().numpy()[0]
+        assert list(ex) == list(c["executed"]), (n, ex, c)
+        assert list(kd) == list(c["kind"]), (n, kd, c)
+        assert int(plan.used.cpu()[0]) == c["used"]
+        n += 1
+    assert n in (1000, 300)
+
+
+def test_remap_batch_gates_and_methods(cuda_ok):
+    """Batch semantics: delta over requested slots (duplicates counted), the
+    beta bypass, ondemand_plan and identity_plan (gating.py:126-165,
+    substitution.py:211-224) against the oracle on a random batch."""
+    rng = np.random.default_rng(3)
+    E, k, B = 64, 6, 48
+    topk = np.stack([rng.choice(E, k, replace=False) for _ in range(B)])
+    mask = rng.random(E) < 0.5
+    lists_ids = [rng.permutation([j for j in range(E) if j != p])[:16] for p in range(E)]
+    ids, w, lens = O.table_from_lists(lists_ids, [np.sort(rng.random(16))[::-1] for _ in range(E)], 16)
+    allowed = rng.random(B) < 0.8
+    table = ops.DeviceTable(_t(ids), _t(w), _t(lens))
+    bm = ops.bitmap_from_mask(mask, DEV)
+    for beta in (1.0, 0.5, 0.3):
+        delta, batch_ok = O.distribution_gate(topk.ravel(), mask, beta)
+        plan = ops.buddy_remap(_t(topk, torch.int32), _t(allowed.astype(np.uint8)), bm, table, H=8, rho=2,
+                               beta=beta)
+        ex_o, kd_o, used_o = O.remap_batch(topk, None, mask, ids, w, lens, allowed & batch_ok, 8, 2)
+        assert np.array_equal(plan.executed.cpu().numpy(), ex_o)
+        assert np.array_equal(plan.kind.cpu().numpy(), kd_o)
+        assert np.array_equal(plan.used.cpu().numpy(), used_o)
+        assert float(plan.delta.cpu()[0]) == delta and bool(plan.batch_allowed.cpu()[0]) == batch_ok
+    ex_o, kd_o, _ = O.ondemand_plan(topk, mask)
+    plan = ops.buddy_remap(_t(topk, torch.int32), None, bm, None, method=ops.METHOD_ORIGINAL, num_experts=E)
+    assert np.array_equal(plan.executed.cpu().numpy(), ex_o) and np.array_equal(plan.kind.cpu().numpy(), kd_o)
+    plan = ops.buddy_remap(_t(topk, torch.int32), None, bm, None, method=ops.METHOD_IDENTITY, num_experts=E)
+    assert np.array_equal(plan.executed.cpu().numpy(), topk) and not plan.kind.cpu().numpy().any()
+
+
+@pytest.mark.parametrize("name", ["routing_tiny.npz", "routing_default.npz", "routing_e128.npz"])
+def test_select_from_reference_logits_bit_exact(cuda_ok, name):
+    """Identical logits give identical indices (model.py:259-263)."""
+    g = golden(name)
+    k = g["topk"].shape[1]
+    r = ops.select_topk_f64(_t(g["logits"]), k, float(g["T"]))
+    assert np.array_equal(r.topk.cpu().numpy(), g["topk"])
+    np.testing.assert_allclose(r.probs64.cpu().numpy(), g["probs"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(r.tae.cpu().numpy(), g["tae"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(r.margin.cpu().numpy(), g["margin"], rtol=0, atol=1e-12)
+
+
+def test_select_ties_to_lower_index(cuda_ok):
+    # test_model.py:115-120: all-equal logits select [0,1,2,3]
+    r = ops.select_topk_f64(torch.zeros(3, 8, dtype=torch.float64, device=DEV), 4)
+    assert r.topk.cpu().numpy().tolist() == [[0, 1, 2, 3]] * 3
+    z = torch.tensor([[1.0, 3.0, 3.0, 2.0, 3.0]], dtype=torch.float64, device=DEV)
+    assert ops.select_topk_f64(z, 3).topk.cpu().numpy().tolist() == [[1, 2, 4]]
+
+
+@pytest.mark.parametrize("name", ["routing_tiny.npz", "routing_default.npz", "routing_e128.npz"])
+def test_fused_gate_fp32(cuda_ok, name):
+    """K1 fp32 GEMV: logits within normwise 1e-5 of the f64 reference; given
+    its own fp32 logits the selection/gates equal the oracle bit-exactly."""
+    g = golden(name)
+    k = g["topk"].shape[1]
+    T = float(g["T"])
+    x, wg, b = g["x"], g["gate_w"], g["gate_b"]
+    r = ops.gate_topk(_t(x, torch.float32), _t(wg, torch.float32), _t(b, torch.float32), k, T, tau=0.5)
+    z = r.logits.cpu().numpy().astype(np.float64)
+    scale = np.linalg.norm(x, axis=1)[:, None] * np.linalg.norm(wg, axis=1).max()
+    assert np.all(np.abs(z - g["logits"]) <= 1e-5 * scale)
+    tk, pr = O.select_topk(z, k, T)
+    assert np.array_equal(r.topk.cpu().numpy(), tk)
+    np.testing.assert_allclose(r.probs.cpu().numpy(), pr, rtol=1e-6, atol=1e-7)
+    tae_o = np.array([O.tae(p) for p in pr])
+    np.testing.assert_allclose(r.tae.cpu().numpy(), tae_o, rtol=0, atol=1e-12)
+    exempt = np.abs(tae_o - 0.5) < 1e-12
+    ok_o = np.array([O.token_gate(p, 0.5) for p in pr])
+    assert np.array_equal(r.allowed.cpu().numpy().astype(bool)[~exempt], ok_o[~exempt])
+    # routing agreement with the f64 reference end to end (reported)
+    agree = np.mean(np.all(r.topk.cpu().numpy() == g["topk"], axis=1))
+    assert agree >= 0.99
+
+
+@pytest.mark.parametrize("name", ["coact_tiny.npz", "coact_default_w05.npz", "coact_e128.npz",
+                                  "coact_e160_noeps.npz"])
+def test_coact_and_rank_bit_exact(cuda_ok, name):
+    """K6 counts and K7 tables vs the reference's observe + build_table."""
+    g = golden(name)
+    E, ws, ww = int(g["E"]), int(g["warmup_steps"]), float(g["warmup_weight"])
+    topk = _t(g["topk"], torch.int32)
+    warm_c, warm_p = ops.coact_count(topk[:ws], E)
+    main_c, main_p = ops.coact_count(topk[ws:], E)
+    counts = ops.counts_to_f64(main_c, warm_c, ww).cpu().numpy()
+    pairs = ops.counts_to_f64(main_p, warm_p, ww).cpu().numpy()
+    assert np.array_equal(counts, g["counts"]) and np.array_equal(pairs, g["pairs"])
+    pw = ops.coact_weighted(topk[ws:], _t(g["probs"][ws:], torch.float32), E, 1.0)
+    if ww:
+        ops.coact_weighted(topk[:ws], _t(g["probs"][:ws], torch.float32), E, ww, pw)
+    np.testing.assert_allclose(pw.cpu().numpy(), g["pw"], rtol=1e-5, atol=1e-9)
+    for i in range(int(g["nbuild"])):
+        alpha, kmax, mode = float(g[f"b{i}_alpha"]), int(g[f"b{i}_kmax"]), str(g[f"b{i}_mode"])
+        M = _t(g["pairs"] if mode == "binary" else g["pw"])
+        t = ops.buddy_rank(M, float(g["eps"]), alpha, kmax)
+        assert np.array_equal(t.ids.cpu().numpy(), g[f"b{i}_ids"]), (name, i)
+        assert np.array_equal(t.lens.cpu().numpy(), g[f"b{i}_lens"]), (name, i)
+        assert np.array_equal(t.weights.cpu().numpy(), g[f"b{i}_w"]), (name, i)
+
+
+def test_coact_counts_large_random_vs_oracle(cuda_ok):
+    """Many CTAs + the k=8 vector path: 2M tokens, E=128 (bincount oracle)."""
+    rng = np.random.default_rng(11)
+    N, E, k = 2_000_000, 128, 8
+    pop = 1.0 / np.arange(1, E + 1) ** 0.8
+    pop /= pop.sum()
+    # distinct ids per row: Gumbel top-k over log-popularity
+    gumb = rng.gumbel(size=(N, E)).astype(np.float32) + np.log(pop).astype(np.float32)
+    topk = np.argpartition(-gumb, k, axis=1)[:, :k].astype(np.int32)
+    del gumb
+    c, p = ops.coact_count(_t(topk), E)
+    oc, op, _, _ = O.coact_count(topk, None, E, 0, 0, 0.0)
+    assert np.array_equal(c.cpu().numpy().astype(np.float64), oc)
+    assert np.array_equal(p.cpu().numpy().astype(np.float64), op)
+
+
+def _arena_tanh(w_in, w_out):
+    # buffer layout TANH: [Win^T (f x d) | Wout^T (d x f)]
+    E = w_in.shape[0]
+    return np.concatenate([np.transpose(w_in, (0, 2, 1)).reshape(E, -1),
+                           np.transpose(w_out, (0, 2, 1)).reshape(E, -1)], axis=1)
+
+
+def test_forward_tanh_fp32_vs_reference(cuda_ok):
+    """permute -> gather -> fp32 FFN -> combine (+layer_update) vs the
+    reference forward_batch on the same plan (model.py:318-347): rel 1e-5."""
+    from paper_2511_10054_b200 import substrate as S
+    g = golden("forward_tiny.npz")
+    spec = S.ModelSpec(num_layers=2, experts_per_layer=8, top_k=2, hidden_dim=128, ffn_dim=256, num_clusters=8)
+    w_in, w_out = S.layer_stack(spec, 0)
+    arena = _t(_arena_tanh(w_in, w_out), torch.float32)
+    E, d, f = 8, 128, 256
+    ex, kd = _t(g["executed"], torch.int32), _t(g["kind"], torch.uint8)
+    perm = ops.permute(ex, kd, E)
+    xs = _t(g["x"], torch.float32)
+    xp = ops.gather_rows(xs, perm, 0)
+    y_perm = ops.expert_ffn_f32(xp, perm, arena, _t(np.arange(E, dtype=np.int32)), d, f, ops.ACT_TANH)
+    probs = _t(g["probs"], torch.float32)
+    y = ops.combine(y_perm, perm, probs, kd).cpu().numpy()
+    # a token whose slots are all dropped has y == 0 exactly (no renormalisation)
+    rel = np.linalg.norm(y - g["y"], axis=1) / np.maximum(np.linalg.norm(g["y"], axis=1), 1.0)
+    assert rel.max() <= 1e-5, rel.max()
+    h = ops.combine(y_perm, perm, probs, kd, h_in=xs).cpu().numpy()
+    relh = np.linalg.norm(h - g["h"], axis=1) / np.linalg.norm(g["h"], axis=1)
+    assert relh.max() <= 1e-5, relh.max()
+
+
+def _rand_swiglu(rng, E, d, f, dtype=np.float32):
+    w1 = (rng.standard_normal((E, f, d)) / np.sqrt(d)).astype(dtype)
+    w3 = (rng.standard_normal((E, f, d)) / np.sqrt(d)).astype(dtype)
+    w2 = (rng.standard_normal((E, d, f)) / np.sqrt(f)).astype(dtype)
+    return w1, w3, w2
+
+
+def _plan(rng, B, E, k, drop=0.1):
+    topk = np.stack([rng.choice(E, k, replace=False) for _ in range(B)]).astype(np.int32)
+    kind = np.where(rng.random((B, k)) < drop, 3, 0).astype(np.uint8)
+    p = rng.random((B, k)) + 0.05
+    return topk, kind, (p / p.sum(1, keepdims=True)).astype(np.float32)
+
+
+def test_forward_swiglu_fp32_vs_oracle(cuda_ok):
+    rng = np.random.default_rng(5)
+    E, d, f, B, k = 8, 256, 384, 24, 2
+    w1, w3, w2 = _rand_swiglu(rng, E, d, f)
+    arena = _t(np.concatenate([w1.reshape(E, -1), w3.reshape(E, -1), w2.reshape(E, -1)], axis=1))
+    topk, kind, probs = _plan(rng, B, E, k)
+    x = rng.standard_normal((B, d)).astype(np.float32)
+    perm = ops.permute(_t(topk), _t(kind), E)
+    xp = ops.gather_rows(_t(x), perm, 0)
+    yp = ops.expert_ffn_f32(xp, perm, arena, _t(np.arange(E, dtype=np.int32)), d, f, ops.ACT_SWIGLU)
+    y = ops.combine(yp, perm, _t(probs), _t(kind)).cpu().numpy()
+    ref = O.forward(x, topk, kind, probs.astype(np.float64),
+                    lambda e, xr: O.ffn_swiglu(xr, w1[e].astype(np.float64), w3[e].astype(np.float64),
+                                               w2[e].astype(np.float64)))
+    rel = np.linalg.norm(y - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
+    assert rel.max() <= 1e-5, rel.max()
+
+
+def _bf16_case(rng, E, d, f, B, k, act, n_tile=64, bufs=None, drop=0.1):
+    topk, kind, probs = _plan(rng, B, E, k, drop)
+    x = rng.standard_normal((B, d)).astype(np.float32)
+    nb = E if bufs is None else bufs
+    gen = torch.Generator(device=DEV)
+    gen.manual_seed(int(rng.integers(1 << 30)))
+    nmat = 3 if act == ops.ACT_SWIGLU else 2
+    arena = torch.empty(nb, nmat * d * f, device=DEV, dtype=torch.bfloat16)
+    for bb in range(nb):  # N(0, 1/fan_in) per matrix, generated on the device
+        row = arena[bb]
+        for m in range(nmat):
+            fan_in = f if m == nmat - 1 else d
+            row[m * d * f:(m + 1) * d * f].copy_(
+                torch.randn(d * f, device=DEV, generator=gen).mul_(fan_in ** -0.5))
+    buf_of = rng.permutation(nb)[:E].astype(np.int32)
+    perm = ops.permute(_t(topk), _t(kind), E)
+    xs = _t(x)
+    xp = ops.gather_rows(xs, perm, 1)
+    ws = ops.FfnWorkspace(E, d, f, perm.r_max, n_tile)
+    yp = ops.expert_ffn_bf16(xp, perm, arena, _t(buf_of), d, f, act, ws)
+    y = ops.combine(yp, perm, _t(probs), _t(kind))
+    # fp32 torch reference over the same bf16-rounded weights and inputs;
+    # H is rounded to bf16 like the kernel's GEMM2 operand
+    xr = xs.to(torch.bfloat16).float()
+    ref = torch.zeros(B, d, device=DEV)
+    for e in range(E):
+        sel = [(b, s) for b in range(B) for s in range(k) if topk[b, s] == e and kind[b, s] != 3]
+        if not sel:
+            continue
+        row = arena[int(buf_of[e])].float()
+        xb = xr[[b for b, _ in sel]]
+        if act == ops.ACT_SWIGLU:
+            W1, W3, W2 = row[: f * d].view(f, d), row[f * d: 2 * f * d].view(f, d), row[2 * f * d:].view(d, f)
+            h = torch.nn.functional.silu(xb @ W1.T) * (xb @ W3.T)
+        else:
+            Wi, W2 = row[: f * d].view(f, d), row[f * d:].view(d, f)
+            h = torch.tanh(xb @ Wi.T)
+        out = h.to(torch.bfloat16).float() @ W2.T
+        for i, (b, s) in enumerate(sel):
+            ref[b] += float(probs[b, s]) * out[i]
+        del row
+    return y, ref, (xp, perm, arena, buf_of, ws)
+
+
+@pytest.mark.parametrize("E,d,f,B,k,act,n_tile", [
+    (8, 128, 256, 16, 2, ops.ACT_SWIGLU, 64),     # tiny
+    (8, 128, 256, 16, 2, ops.ACT_TANH, 64),       # the reference expert
+    (8, 4096, 14336, 1, 2, ops.ACT_SWIGLU, 64),   # Mixtral decode B=1
+    (8, 4096, 14336, 32, 2, ops.ACT_SWIGLU, 64),  # Mixtral decode B=32
+    (128, 2048, 768, 64, 8, ops.ACT_SWIGLU, 64),  # Qwen3-shaped
+    (64, 2048, 1408, 16, 6, ops.ACT_SWIGLU, 32),  # DSV2-shaped, narrow n tile
+    (4, 256, 512, 200, 2, ops.ACT_SWIGLU, 64),    # many tokens per expert: N chunking
+    (4, 256, 512, 200, 2, ops.ACT_SWIGLU, 256),   # widest tile, single TMEM stage
+])
+def test_bf16_tcgen05_ffn_vs_fp32_reference(cuda_ok, E, d, f, B, k, act, n_tile):
+    """K4 bf16 tensor-core grouped FFN: rel 2e-2 (normwise per token) vs fp32."""
+    rng = np.random.default_rng(E * 1000 + B)
+    y, ref, _ = _bf16_case(rng, E, d, f, B, k, act, n_tile)
+    rel = (torch.linalg.norm(y - ref, dim=1) / torch.linalg.norm(ref, dim=1).clamp_min(1e-30)).max().item()
+    assert rel <= 2e-2, rel
+
+
+def test_bf16_ffn_deterministic_and_buffer_indirection(cuda_ok):
+    """Two runs are bitwise identical (no split-K atomics); experts live in
+    arbitrary arena buffers (buf_of_expert indirection, 12 buffers for 8)."""
+    rng = np.random.default_rng(9)
+    y, ref, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, 8, 512, 1024, 40, 2, ops.ACT_SWIGLU, bufs=12)
+    rel = (torch.linalg.norm(y - ref, dim=1) / torch.linalg.norm(ref, dim=1)).max().item()
+    assert rel <= 2e-2
+    d, f = 512, 1024
+    rows = int(perm.offset[-1])  # rows past the last segment are never written
+    y1 = ops.expert_ffn_bf16(xp, perm, arena, _t(buf_of), d, f, ops.ACT_SWIGLU, ws)[:rows]
+    y2 = ops.expert_ffn_bf16(xp, perm, arena, _t(buf_of), d, f, ops.ACT_SWIGLU, ws)[:rows]
+    assert torch.equal(y1, y2)
