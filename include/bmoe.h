@@ -234,6 +234,63 @@ int bm_cache_layer_state(const bm_cache *c, int32_t layer, int64_t *last_use_hos
                          int64_t *scalars_host /* [tick, n_pending, waste, unused_resident] */);
 int bm_cache_pending(const bm_cache *c, int32_t layer, double *done_host, int32_t *expert_host, int64_t cap);
 
+/* ------------------------------------------------ offloaded decode engine
+ * The run_simulation inner loop (harness.py:315-393) over real memory: the
+ * control plane above decides hits/misses/evictions/prefetches exactly as
+ * the reference; the data plane keeps every layer's resident experts in a
+ * pool of fixed HBM buffers (capacity per layer + `staging` transient
+ * buffers), fetches misses from a pinned host mirror with cudaMemcpyAsync on
+ * copy streams, and orders buffer reuse with CUDA events. Per layer-step:
+ * prefetch(l+1) -> settle(l) -> K1 gate -> K2 remap on the residency
+ * snapshot -> plan readback -> control-plane replay -> H2D fetch of
+ * executed-but-absent experts -> K3 permute -> K4 grouped FFN -> K5 combine
+ * + layer_update (in place on h). */
+typedef struct bm_engine bm_engine;
+typedef struct {
+    int32_t num_layers, num_experts, top_k, d, f, act;
+    int32_t max_batch, capacity, staging; /* staging <= 0: automatic */
+    int32_t method, policy, search_rank_h, fallback, prefetch_enabled, n_tile;
+    int32_t fp32_weights; /* 1: fp32 arena + SIMT FFN (parity), 0: bf16 + tcgen05 */
+    int64_t rho;          /* < 0 unlimited */
+    double beta, temperature, gamma; /* gamma < 0: margin gate off */
+    double load_ms, hit_ms, compute_ms, prefetch_ms; /* control-plane cost model (memtier.py:39-58) */
+    int64_t expert_bytes;                            /* reported per miss (CostModel.expert_bytes) */
+} bm_engine_config;
+
+typedef struct {
+    int64_t tokens, executed_slots, ondemand_misses, substitutions, drops;
+    int64_t physical_fetches, prefetch_copies, h2d_bytes, gate_forbidden, batch_bypassed;
+    int64_t ffn_calls, ffn_experts, ffn_rows; /* grouped-FFN launches, sum of distinct executed experts / rows */
+    double sim_now_ms;   /* control-plane clock */
+    double stall_ms;     /* measured: compute stream waiting on expert fetches (CUDA events) */
+} bm_engine_stats;
+
+/* host_mirror[l]: pinned host memory, num_experts buffers of the arena
+ * layout (bf16 or fp32 per fp32_weights). gate_w [L][E][d], gate_b [L][E]
+ * fp32 device. Table (method BUDDY): tbl_ids [L][E][K] int32, tbl_len [L][E]
+ * device. tau_host [L] (token gate thresholds; < 0 never forbids).
+ * initial_host [L][capacity] residents (-1 padded); static_freq_host [L][E]
+ * for freq_static (else NULL). */
+int bm_engine_create(const bm_engine_config *cfg, const void *const *host_mirror, const float *gate_w,
+                     const float *gate_b, const int32_t *tbl_ids, const int32_t *tbl_len, int32_t tbl_k,
+                     const double *tau_host, const int32_t *initial_host, const double *static_freq_host,
+                     bm_engine **out);
+void bm_engine_destroy(bm_engine *e);
+/* One decode step over all layers, h [B][d] fp32 device, updated in place.
+ * tokens_host[B]: global token ids (events). Enqueues on `stream`; returns
+ * after the last layer's kernels are enqueued. */
+int bm_engine_step(bm_engine *e, float *h, int64_t B, const int32_t *tokens_host, bm_stream_t stream);
+/* Accumulated stats (synchronises the engine's events); reset clears them. */
+int bm_engine_stats_get(bm_engine *e, bm_engine_stats *out_host, int32_t reset);
+bm_cache *bm_engine_cache(bm_engine *e);
+/* Bytes of device memory held by the engine (arena + workspaces). */
+int64_t bm_engine_device_bytes(const bm_engine *e);
+
+/* Pinned host allocation of exact size (cudaHostAlloc, portable). */
+int bm_host_alloc(int64_t bytes, void **out);
+int bm_host_free(void *p);
+int bm_memcpy(void *dst, const void *src, int64_t bytes, bm_stream_t stream); /* cudaMemcpyAsync default kind */
+
 #ifdef __cplusplus
 }
 #endif

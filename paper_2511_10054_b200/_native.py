@@ -26,7 +26,38 @@ class Event(C.Structure):
                 ("expert", C.c_int32), ("bytes", C.c_int64), ("stall_ms", C.c_double)]
 
 
+class EngineConfig(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("num_experts", C.c_int32), ("top_k", C.c_int32), ("d", C.c_int32),
+                ("f", C.c_int32), ("act", C.c_int32), ("max_batch", C.c_int32), ("capacity", C.c_int32),
+                ("staging", C.c_int32), ("method", C.c_int32), ("policy", C.c_int32),
+                ("search_rank_h", C.c_int32), ("fallback", C.c_int32), ("prefetch_enabled", C.c_int32),
+                ("n_tile", C.c_int32), ("fp32_weights", C.c_int32), ("rho", C.c_int64), ("beta", C.c_double),
+                ("temperature", C.c_double), ("gamma", C.c_double), ("load_ms", C.c_double),
+                ("hit_ms", C.c_double), ("compute_ms", C.c_double), ("prefetch_ms", C.c_double),
+                ("expert_bytes", C.c_int64)]
+
+
+class EngineStats(C.Structure):
+    _fields_ = [("tokens", C.c_int64), ("executed_slots", C.c_int64), ("ondemand_misses", C.c_int64),
+                ("substitutions", C.c_int64), ("drops", C.c_int64), ("physical_fetches", C.c_int64),
+                ("prefetch_copies", C.c_int64), ("h2d_bytes", C.c_int64), ("gate_forbidden", C.c_int64),
+                ("batch_bypassed", C.c_int64), ("ffn_calls", C.c_int64), ("ffn_experts", C.c_int64),
+                ("ffn_rows", C.c_int64), ("sim_now_ms", C.c_double), ("stall_ms", C.c_double)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 _SIGS = {
+    "bm_engine_create": (C.c_int, [P, P, P, P, P, P, I32, P, P, P, P]),
+    "bm_engine_destroy": (None, [P]),
+    "bm_engine_step": (C.c_int, [P, P, I64, P, P]),
+    "bm_engine_stats_get": (C.c_int, [P, P, I32]),
+    "bm_engine_cache": (P, [P]),
+    "bm_engine_device_bytes": (I64, [P]),
+    "bm_host_alloc": (C.c_int, [I64, P]),
+    "bm_host_free": (C.c_int, [P]),
+    "bm_memcpy": (C.c_int, [P, P, I64, P]),
     "bm_abi_version": (C.c_int, []),
     "bm_last_error": (C.c_char_p, []),
     "bm_device_sm_count": (C.c_int, []),

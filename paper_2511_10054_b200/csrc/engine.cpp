@@ -1,0 +1,469 @@
+// Offloaded-MoE decode engine: the reference's per-layer decode loop
+// (harness.py:315-393) driven over real memory. The control plane
+// (cache.cpp) makes every hit / miss / eviction / prefetch decision exactly
+// like memtier; this file is the data plane that makes those decisions
+// physical: a pool of equally sized HBM expert buffers (capacity per layer
+// plus transient staging), H2D fetches from a pinned host mirror on copy
+// streams, CUDA events ordering buffer reuse, and the kernel sequence
+// gate -> remap -> permute -> grouped FFN -> combine per layer.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/bmoe.h"
+
+namespace bm {
+void set_error(const char *fmt, ...);
+}
+
+#define ENG_CUDA(expr)                                                                                    \
+    do {                                                                                                  \
+        cudaError_t _e = (expr);                                                                          \
+        if (_e != cudaSuccess) {                                                                          \
+            bm::set_error("engine %s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e));      \
+            return BM_ECUDA;                                                                              \
+        }                                                                                                 \
+    } while (0)
+#define ENG_TRY(expr)             \
+    do {                          \
+        int _rc = (expr);         \
+        if (_rc != BM_OK) return _rc; \
+    } while (0)
+
+namespace {
+
+struct Buffer {
+    void *dev = nullptr;
+    cudaEvent_t free_ev = nullptr;  // last compute that read it (borrowed per-layer event)
+};
+
+}  // namespace
+
+struct bm_engine {
+    bm_engine_config cfg{};
+    int L = 0, E = 0, k = 0, d = 0, f = 0, cap = 0, S = 0, nbufs = 0, reserve = 0, K = 0;
+    size_t buf_bytes = 0;
+    int64_t buf_elems = 0;
+    uint8_t *arena = nullptr;
+    std::vector<Buffer> bufs;
+    std::vector<int> free_list;
+    std::vector<std::vector<int>> phys;            // [L][E] buffer id or -1
+    std::vector<std::vector<cudaEvent_t>> ready;   // [L][E] copy-complete events
+    std::vector<std::vector<uint8_t>> ready_pending;
+    std::vector<cudaEvent_t> layer_done;           // [L]
+    std::vector<const uint8_t *> host_mirror;
+    const float *gate_w = nullptr, *gate_b = nullptr;
+    const int32_t *tbl_ids = nullptr, *tbl_len = nullptr;
+    std::vector<double> tau;
+    bm_cache *cache = nullptr;
+    // device workspaces
+    float *logits = nullptr, *probs = nullptr, *y_perm = nullptr, *h_ws = nullptr;
+    double *tae = nullptr, *margin = nullptr, *delta = nullptr;
+    int32_t *topk = nullptr, *executed = nullptr, *used = nullptr;
+    uint8_t *kind = nullptr, *allowed = nullptr, *batch_ok = nullptr;
+    uint32_t *bitmap_dev[2] = {nullptr, nullptr};
+    int32_t *buf_of_dev[2] = {nullptr, nullptr};
+    int32_t *count = nullptr, *offset = nullptr, *row_token = nullptr, *slot_row = nullptr;
+    void *x_perm = nullptr, *ffn_ws = nullptr;
+    int64_t ffn_ws_bytes = 0, r_max = 0, device_bytes = 0;
+    // pinned staging
+    uint32_t *bitmap_host[2] = {nullptr, nullptr};
+    int32_t *buf_of_host[2] = {nullptr, nullptr};
+    int32_t *topk_h = nullptr, *exec_h = nullptr;
+    uint8_t *kind_h = nullptr, *allowed_h = nullptr, *batch_ok_h = nullptr;
+    cudaEvent_t plan_ev = nullptr;
+    cudaStream_t copy_stream = nullptr, prefetch_stream = nullptr;
+    std::vector<std::vector<int32_t>> prev_counts;  // [L][E]
+    int parity = 0;
+    bm_engine_stats stats{};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev;
+    std::vector<uint8_t> mask_tmp;
+    std::vector<double> pend_done;
+    std::vector<int32_t> pend_exp;
+
+    template <typename T>
+    int dmalloc(T **p, size_t n) {
+        ENG_CUDA(cudaMalloc(reinterpret_cast<void **>(p), n * sizeof(T) + 16));
+        device_bytes += (int64_t)(n * sizeof(T));
+        return BM_OK;
+    }
+    template <typename T>
+    int hmalloc(T **p, size_t n) {
+        ENG_CUDA(cudaHostAlloc(reinterpret_cast<void **>(p), n * sizeof(T) + 16, cudaHostAllocPortable));
+        return BM_OK;
+    }
+
+    std::vector<int> pending_experts(int layer) {
+        int64_t sc[4];
+        bm_cache_layer_state(cache, layer, nullptr, nullptr, sc);
+        pend_done.resize(sc[1] + 1);
+        pend_exp.resize(sc[1] + 1);
+        bm_cache_pending(cache, layer, pend_done.data(), pend_exp.data(), sc[1]);
+        return std::vector<int>(pend_exp.begin(), pend_exp.begin() + sc[1]);
+    }
+
+    int alloc_buffer(int *out) {
+        if (free_list.empty()) {
+            bm::set_error("engine: expert buffer pool exhausted (staging too small)");
+            return BM_EINVARIANT;
+        }
+        *out = free_list.back();
+        free_list.pop_back();
+        return BM_OK;
+    }
+
+    // H2D of expert e of layer l into a fresh buffer on stream s
+    int fetch(int l, int e, cudaStream_t s) {
+        int b;
+        ENG_TRY(alloc_buffer(&b));
+        if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(s, bufs[b].free_ev, 0));
+        ENG_CUDA(cudaMemcpyAsync(bufs[b].dev, host_mirror[l] + (size_t)e * buf_bytes, buf_bytes,
+                                 cudaMemcpyHostToDevice, s));
+        ENG_CUDA(cudaEventRecord(ready[l][e], s));
+        ready_pending[l][e] = 1;
+        phys[l][e] = b;
+        stats.h2d_bytes += (int64_t)buf_bytes;
+        return BM_OK;
+    }
+
+    int layer_step(int l, float *h, int64_t B, const int32_t *tokens, cudaStream_t s) {
+        const int par = parity;
+        parity ^= 1;
+        // 1. speculative loads for the next layer (harness.py:321-326)
+        if (cfg.prefetch_enabled && L > 1) {
+            const int t = l + 1 < L ? l + 1 : 0;
+            int32_t preds[1024];
+            int64_t np = 0;
+            ENG_TRY(bm_cache_predict(cache, t, prev_counts[t].data(), preds, &np));
+            if (np > 0) {
+                std::vector<int> before = pending_experts(t);
+                ENG_TRY(bm_cache_prefetch(cache, t, preds, np));
+                std::vector<int> after = pending_experts(t);
+                for (int e : after) {
+                    if (std::find(before.begin(), before.end(), e) != before.end()) continue;
+                    if (phys[t][e] >= 0 || (int)free_list.size() <= reserve) continue;  // keep the on-demand reserve
+                    ENG_TRY(fetch(t, e, prefetch_stream));
+                    ++stats.prefetch_copies;
+                }
+            }
+        }
+        // 2. commit completed transfers (harness.py:327-329)
+        ENG_TRY(bm_cache_settle(cache, l));
+        // 3. K1 router
+        ENG_TRY(bm_gate_topk(h, gate_w + (size_t)l * E * d, gate_b + (size_t)l * E, B, E, d, k, cfg.temperature,
+                             tau[l], cfg.gamma, logits, topk, probs, tae, margin, allowed, s));
+        // 4. snapshot + K2 remap (harness.py:331-361)
+        const int words = (E + 31) / 32;
+        ENG_TRY(bm_cache_snapshot(cache, l, nullptr, bitmap_host[par]));
+        ENG_CUDA(cudaMemcpyAsync(bitmap_dev[par], bitmap_host[par], words * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        ENG_TRY(bm_buddy_remap(topk, allowed, nullptr, 0, B, k, E, bitmap_dev[par],
+                               tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr, nullptr,
+                               tbl_len ? tbl_len + (size_t)l * E : nullptr, K > 0 ? K : 1, cfg.search_rank_h,
+                               cfg.rho, cfg.fallback, cfg.method, cfg.beta, 0.0, 0.0, 1, nullptr, 1.0, executed,
+                               kind, used, delta, batch_ok, s));
+        // 5. plan readback for the sequential cache replay
+        ENG_CUDA(cudaMemcpyAsync(topk_h, topk, B * k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        ENG_CUDA(cudaMemcpyAsync(exec_h, executed, B * k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        ENG_CUDA(cudaMemcpyAsync(kind_h, kind, B * k, cudaMemcpyDeviceToHost, s));
+        ENG_CUDA(cudaMemcpyAsync(allowed_h, allowed, B, cudaMemcpyDeviceToHost, s));
+        ENG_CUDA(cudaMemcpyAsync(batch_ok_h, batch_ok, 1, cudaMemcpyDeviceToHost, s));
+        ENG_CUDA(cudaEventRecord(plan_ev, s));
+        ENG_CUDA(cudaEventSynchronize(plan_ev));
+        if (cfg.method == BM_METHOD_BUDDY) {
+            for (int64_t b = 0; b < B; ++b) stats.gate_forbidden += allowed_h[b] ? 0 : 1;
+            stats.batch_bypassed += batch_ok_h[0] ? 0 : 1;
+        }
+        // 6. control plane: replay accesses in (token, slot) order (harness.py:363-382)
+        int64_t out4[4];
+        ENG_TRY(bm_cache_apply_plan(cache, l, B, k, tokens, topk_h, exec_h, kind_h, out4));
+        stats.executed_slots += out4[0];
+        stats.ondemand_misses += out4[1];
+        stats.substitutions += out4[2];
+        ENG_TRY(bm_cache_advance(cache, cfg.compute_ms * (double)out4[0]));
+        std::vector<int32_t> &cnt = prev_counts[l];  // harness.py:384-389
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (int64_t i = 0; i < B * k; ++i) {
+            if (kind_h[i] == BM_KIND_DROPPED) {
+                ++stats.drops;
+                continue;
+            }
+            ++cnt[exec_h[i]];
+        }
+        // 7. data plane: every executed expert must be in HBM before the GEMM
+        std::vector<cudaEvent_t> waits;
+        ++stats.ffn_calls;
+        for (int e = 0; e < E; ++e) {
+            if (!cnt[e]) continue;
+            ++stats.ffn_experts;
+            stats.ffn_rows += cnt[e];
+            if (phys[l][e] < 0) {
+                ENG_TRY(fetch(l, e, copy_stream));
+                ++stats.physical_fetches;
+            }
+            if (ready_pending[l][e]) {
+                waits.push_back(ready[l][e]);
+                ready_pending[l][e] = 0;
+            }
+        }
+        if (!waits.empty()) {
+            cudaEvent_t a, bb;
+            ENG_CUDA(cudaEventCreate(&a));
+            ENG_CUDA(cudaEventCreate(&bb));
+            ENG_CUDA(cudaEventRecord(a, s));
+            for (cudaEvent_t w : waits) ENG_CUDA(cudaStreamWaitEvent(s, w, 0));
+            ENG_CUDA(cudaEventRecord(bb, s));
+            stall_ev.emplace_back(a, bb);
+        }
+        for (int e = 0; e < E; ++e) buf_of_host[par][e] = phys[l][e] >= 0 ? phys[l][e] : 0;
+        ENG_CUDA(cudaMemcpyAsync(buf_of_dev[par], buf_of_host[par], E * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        // 8. K3 permute -> K4 grouped FFN -> K5 combine + layer_update (in place)
+        ENG_TRY(bm_permute(executed, kind, B, k, E, 16, count, offset, row_token, slot_row, s));
+        if (cfg.fp32_weights) {
+            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, E, r_max, 0, x_perm, s));
+            ENG_TRY(bm_expert_ffn_f32(static_cast<float *>(x_perm), count, offset, E, d, f, cfg.act,
+                                      reinterpret_cast<const float *>(arena), buf_elems, buf_of_dev[par], r_max,
+                                      h_ws, y_perm, s));
+        } else {
+            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, E, r_max, 1, x_perm, s));
+            ENG_TRY(bm_expert_ffn_bf16(x_perm, count, offset, E, d, f, cfg.act, arena, nbufs, buf_of_dev[par],
+                                       r_max, cfg.n_tile, ffn_ws, ffn_ws_bytes, y_perm, s));
+        }
+        ENG_TRY(bm_combine(y_perm, slot_row, probs, kind, B, k, d, h, 0.5f, h, s));
+        // 9. release buffers of experts the control plane no longer holds
+        ENG_CUDA(cudaEventRecord(layer_done[l], s));
+        ENG_TRY(bm_cache_snapshot(cache, l, mask_tmp.data(), nullptr));
+        std::vector<int> pend = pending_experts(l);
+        for (int e = 0; e < E; ++e) {
+            const int b = phys[l][e];
+            if (b < 0 || mask_tmp[e] || std::find(pend.begin(), pend.end(), e) != pend.end()) continue;
+            bufs[b].free_ev = layer_done[l];
+            free_list.push_back(b);
+            phys[l][e] = -1;
+            ready_pending[l][e] = 0;
+        }
+        return BM_OK;
+    }
+
+    void release() {
+        if (arena) cudaFree(arena);
+        for (auto &v : ready)
+            for (cudaEvent_t e : v)
+                if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : layer_done)
+            if (e) cudaEventDestroy(e);
+        for (auto &p : stall_ev) {
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+        void *dptrs[] = {logits, probs, y_perm, h_ws, tae, margin, delta, topk, executed, used, kind, allowed,
+                         batch_ok, bitmap_dev[0], bitmap_dev[1], buf_of_dev[0], buf_of_dev[1], count, offset,
+                         row_token, slot_row, x_perm, ffn_ws};
+        for (void *p : dptrs)
+            if (p) cudaFree(p);
+        void *hptrs[] = {bitmap_host[0], bitmap_host[1], buf_of_host[0], buf_of_host[1], topk_h, exec_h, kind_h,
+                         allowed_h, batch_ok_h};
+        for (void *p : hptrs)
+            if (p) cudaFreeHost(p);
+        if (plan_ev) cudaEventDestroy(plan_ev);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (prefetch_stream) cudaStreamDestroy(prefetch_stream);
+        if (cache) bm_cache_destroy(cache);
+    }
+};
+
+static int engine_init(bm_engine *g, const bm_engine_config *c, const void *const *host_mirror, const float *gate_w,
+                       const float *gate_b, const int32_t *tbl_ids, const int32_t *tbl_len, int32_t tbl_k,
+                       const double *tau_host, const int32_t *initial_host, const double *static_freq_host) {
+    g->cfg = *c;
+    g->L = c->num_layers;
+    g->E = c->num_experts;
+    g->k = c->top_k;
+    g->d = c->d;
+    g->f = c->f;
+    g->cap = c->capacity;
+    g->K = tbl_k;
+    const int L = g->L, E = g->E, k = g->k;
+    if (L < 1 || E < 1 || E > 256 || k < 1 || k > E || c->max_batch < 1 || g->cap < 0 || g->cap > E) {
+        bm::set_error("engine: bad configuration");
+        return BM_ECONFIG;
+    }
+    if (c->method == BM_METHOD_BUDDY && (!tbl_ids || !tbl_len || tbl_k < 1)) {
+        bm::set_error("engine: buddy method needs a buddy table per layer");
+        return BM_ECONFIG;
+    }
+    g->buf_elems = (int64_t)(c->act == BM_ACT_SWIGLU ? 3 : 2) * c->d * c->f;
+    g->buf_bytes = (size_t)g->buf_elems * (c->fp32_weights ? 4 : 2);
+    g->reserve = std::min(E - g->cap, c->max_batch * k);
+    g->S = c->staging > 0 ? c->staging : g->reserve + g->cap;
+    if (g->S < g->reserve) {
+        bm::set_error("engine: staging (%d) below the on-demand reserve (%d)", g->S, g->reserve);
+        return BM_ECONFIG;
+    }
+    g->nbufs = L * g->cap + g->S;
+    g->host_mirror.resize(L);
+    for (int l = 0; l < L; ++l) g->host_mirror[l] = static_cast<const uint8_t *>(host_mirror[l]);
+    g->gate_w = gate_w;
+    g->gate_b = gate_b;
+    g->tbl_ids = tbl_ids;
+    g->tbl_len = tbl_len;
+    g->tau.assign(tau_host, tau_host + L);
+    // control plane
+    std::vector<int32_t> init((size_t)L * std::max(g->cap, 1), -1);
+    if (initial_host) memcpy(init.data(), initial_host, (size_t)L * g->cap * sizeof(int32_t));
+    ENG_TRY(bm_cache_create(L, E, g->cap, c->policy, init.data(), static_freq_host, c->load_ms, c->hit_ms,
+                            c->prefetch_ms, c->expert_bytes, &g->cache));
+    // data plane
+    ENG_CUDA(cudaMalloc(&g->arena, (size_t)g->nbufs * g->buf_bytes));
+    g->device_bytes += (int64_t)g->nbufs * (int64_t)g->buf_bytes;
+    g->bufs.resize(g->nbufs);
+    for (int b = 0; b < g->nbufs; ++b) g->bufs[b].dev = g->arena + (size_t)b * g->buf_bytes;
+    for (int b = g->nbufs - 1; b >= 0; --b) g->free_list.push_back(b);
+    g->phys.assign(L, std::vector<int>(E, -1));
+    g->ready.assign(L, std::vector<cudaEvent_t>(E, nullptr));
+    g->ready_pending.assign(L, std::vector<uint8_t>(E, 0));
+    g->layer_done.assign(L, nullptr);
+    for (int l = 0; l < L; ++l) {
+        for (int e = 0; e < E; ++e) ENG_CUDA(cudaEventCreateWithFlags(&g->ready[l][e], cudaEventDisableTiming));
+        ENG_CUDA(cudaEventCreateWithFlags(&g->layer_done[l], cudaEventDisableTiming));
+    }
+    ENG_CUDA(cudaEventCreateWithFlags(&g->plan_ev, cudaEventDisableTiming | cudaEventBlockingSync));
+    ENG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+    ENG_CUDA(cudaStreamCreateWithFlags(&g->prefetch_stream, cudaStreamNonBlocking));
+    // initial residents: synchronous upload
+    std::vector<uint8_t> mask(E);
+    for (int l = 0; l < L; ++l) {
+        ENG_TRY(bm_cache_snapshot(g->cache, l, mask.data(), nullptr));
+        for (int e = 0; e < E; ++e) {
+            if (!mask[e]) continue;
+            int b;
+            ENG_TRY(g->alloc_buffer(&b));
+            ENG_CUDA(cudaMemcpy(g->bufs[b].dev, g->host_mirror[l] + (size_t)e * g->buf_bytes, g->buf_bytes,
+                                cudaMemcpyHostToDevice));
+            g->phys[l][e] = b;
+        }
+    }
+    // workspaces
+    const int64_t Bm = c->max_batch;
+    g->r_max = bm_permute_rows_max(Bm, k, E, 16);
+    g->r_max = (g->r_max + 15) / 16 * 16;
+    ENG_TRY(g->dmalloc(&g->logits, Bm * E));
+    ENG_TRY(g->dmalloc(&g->probs, Bm * k));
+    ENG_TRY(g->dmalloc(&g->tae, Bm));
+    ENG_TRY(g->dmalloc(&g->margin, Bm));
+    ENG_TRY(g->dmalloc(&g->delta, 1));
+    ENG_TRY(g->dmalloc(&g->topk, Bm * k));
+    ENG_TRY(g->dmalloc(&g->executed, Bm * k));
+    ENG_TRY(g->dmalloc(&g->used, Bm));
+    ENG_TRY(g->dmalloc(&g->kind, Bm * k));
+    ENG_TRY(g->dmalloc(&g->allowed, Bm));
+    ENG_TRY(g->dmalloc(&g->batch_ok, 1));
+    for (int i = 0; i < 2; ++i) {
+        ENG_TRY(g->dmalloc(&g->bitmap_dev[i], (E + 31) / 32));
+        ENG_TRY(g->dmalloc(&g->buf_of_dev[i], E));
+        ENG_TRY(g->hmalloc(&g->bitmap_host[i], (E + 31) / 32));
+        ENG_TRY(g->hmalloc(&g->buf_of_host[i], E));
+    }
+    ENG_TRY(g->dmalloc(&g->count, E));
+    ENG_TRY(g->dmalloc(&g->offset, E + 1));
+    ENG_TRY(g->dmalloc(&g->row_token, g->r_max + 16));
+    ENG_TRY(g->dmalloc(&g->slot_row, Bm * k));
+    ENG_TRY(g->dmalloc(&g->y_perm, (size_t)g->r_max * g->d));
+    if (c->fp32_weights) {
+        ENG_TRY(g->dmalloc(reinterpret_cast<float **>(&g->x_perm), (size_t)g->r_max * g->d));
+        ENG_TRY(g->dmalloc(&g->h_ws, (size_t)g->r_max * g->f));
+    } else {
+        ENG_TRY(g->dmalloc(reinterpret_cast<uint16_t **>(&g->x_perm), (size_t)g->r_max * g->d));
+        ENG_CUDA(cudaMemset(g->x_perm, 0, (size_t)g->r_max * g->d * 2));
+        g->ffn_ws_bytes = bm_expert_ffn_bf16_workspace(E, g->d, g->f, g->r_max, c->n_tile);
+        ENG_TRY(g->dmalloc(reinterpret_cast<uint8_t **>(&g->ffn_ws), (size_t)g->ffn_ws_bytes));
+    }
+    ENG_TRY(g->hmalloc(&g->topk_h, Bm * k));
+    ENG_TRY(g->hmalloc(&g->exec_h, Bm * k));
+    ENG_TRY(g->hmalloc(&g->kind_h, Bm * k));
+    ENG_TRY(g->hmalloc(&g->allowed_h, Bm));
+    ENG_TRY(g->hmalloc(&g->batch_ok_h, 1));
+    g->prev_counts.assign(L, std::vector<int32_t>(E, 0));
+    g->mask_tmp.assign(E, 0);
+    return BM_OK;
+}
+
+extern "C" int bm_engine_create(const bm_engine_config *cfg, const void *const *host_mirror, const float *gate_w,
+                                const float *gate_b, const int32_t *tbl_ids, const int32_t *tbl_len, int32_t tbl_k,
+                                const double *tau_host, const int32_t *initial_host, const double *static_freq_host,
+                                bm_engine **out) {
+    if (!cfg || !host_mirror || !gate_w || !gate_b || !tau_host || !out) {
+        bm::set_error("bm_engine_create: null argument");
+        return BM_EINVAL;
+    }
+    bm_engine *g = new bm_engine();
+    int rc = engine_init(g, cfg, host_mirror, gate_w, gate_b, tbl_ids, tbl_len, tbl_k, tau_host, initial_host,
+                         static_freq_host);
+    if (rc != BM_OK) {
+        g->release();
+        delete g;
+        return rc;
+    }
+    *out = g;
+    return BM_OK;
+}
+
+extern "C" void bm_engine_destroy(bm_engine *e) {
+    if (!e) return;
+    cudaDeviceSynchronize();
+    e->release();
+    delete e;
+}
+
+extern "C" int bm_engine_step(bm_engine *e, float *h, int64_t B, const int32_t *tokens_host, bm_stream_t stream) {
+    if (!e || !h || B < 1 || B > e->cfg.max_batch) {
+        bm::set_error("bm_engine_step: bad arguments (B=%lld)", (long long)B);
+        return BM_EINVAL;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    for (int l = 0; l < e->L; ++l) ENG_TRY(e->layer_step(l, h, B, tokens_host, s));
+    e->stats.tokens += B;
+    return BM_OK;
+}
+
+extern "C" int bm_engine_stats_get(bm_engine *e, bm_engine_stats *out, int32_t reset) {
+    if (!e || !out) return BM_EINVAL;
+    double stall = 0.0;
+    for (auto &p : e->stall_ev) {
+        ENG_CUDA(cudaEventSynchronize(p.second));
+        float ms = 0.f;
+        ENG_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+        stall += ms;
+    }
+    e->stats.stall_ms += stall;
+    for (auto &p : e->stall_ev) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    e->stall_ev.clear();
+    ENG_TRY(bm_cache_now(e->cache, &e->stats.sim_now_ms));
+    *out = e->stats;
+    if (reset) e->stats = bm_engine_stats{};
+    return BM_OK;
+}
+
+extern "C" bm_cache *bm_engine_cache(bm_engine *e) { return e ? e->cache : nullptr; }
+
+extern "C" int64_t bm_engine_device_bytes(const bm_engine *e) { return e ? e->device_bytes : 0; }
+
+extern "C" int bm_host_alloc(int64_t bytes, void **out) {
+    if (!out || bytes <= 0) return BM_EINVAL;
+    ENG_CUDA(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable));
+    return BM_OK;
+}
+
+extern "C" int bm_host_free(void *p) {
+    if (p) ENG_CUDA(cudaFreeHost(p));
+    return BM_OK;
+}
+
+extern "C" int bm_memcpy(void *dst, const void *src, int64_t bytes, bm_stream_t stream) {
+    ENG_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, reinterpret_cast<cudaStream_t>(stream)));
+    return BM_OK;
+}

@@ -1,0 +1,186 @@
+"""Offloaded decode engine: Python handle over bm_engine (include/bmoe.h).
+
+``DecodeEngine.step(h, tokens)`` is one decode step through every layer —
+the tensor form of the reference's run_simulation inner loop
+(harness.py:315-393) — with a real expert cache: HBM buffers under a
+capacity budget, pinned-host fetches on copy streams, and the exact
+memtier replica deciding hits, misses, evictions and prefetches.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigurationError
+from .ops import ACT_SWIGLU, FALLBACK_PREFETCH, METHOD_BUDDY
+
+POLICIES = {"lru": 0, "lfu": 1, "freq_static": 2}
+METHODS = {"buddy": 0, "original": 1, "identity": 2}
+
+
+class HostMirror:
+    """Pinned host memory holding every expert of one layer in the arena
+    layout (cudaHostAlloc of the exact size, not torch's power-of-two pool)."""
+
+    def __init__(self, nbytes: int):
+        ptr = C.c_void_p()
+        N.call("bm_host_alloc", int(nbytes), C.byref(ptr))
+        self.ptr = ptr.value
+        self.nbytes = int(nbytes)
+
+    def as_tensor(self, dtype=torch.uint8) -> torch.Tensor:
+        buf = (C.c_uint8 * self.nbytes).from_address(self.ptr)
+        return torch.frombuffer(buf, dtype=torch.uint8).view(dtype)
+
+    def close(self):
+        if self.ptr:
+            N.lib().bm_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fill_mirror_from_device(mirror: HostMirror, src: torch.Tensor, offset: int = 0):
+    """Synchronous device -> pinned host copy into the mirror at a byte offset."""
+    n = src.numel() * src.element_size()
+    s = torch.cuda.current_stream()
+    N.call("bm_memcpy", mirror.ptr + offset, src.data_ptr(), n, s.cuda_stream)
+    s.synchronize()
+
+
+@dataclass
+class EngineSpec:
+    num_layers: int
+    num_experts: int
+    top_k: int
+    d: int
+    f: int
+    capacity: int
+    max_batch: int
+    act: int = ACT_SWIGLU
+    method: str = "buddy"
+    policy: str = "lru"
+    search_rank_h: int = 16
+    rho: int | None = None
+    fallback: int = FALLBACK_PREFETCH
+    beta: float = 1.0
+    temperature: float = 1.0
+    gamma: float | None = None
+    prefetch: bool = True
+    n_tile: int = 64
+    fp32_weights: bool = False
+    staging: int = 0
+    load_ms: float = 9.5
+    hit_ms: float = 0.0
+    compute_ms: float = 0.5
+    prefetch_ms: float | None = None
+    pcie_bw_bytes_per_s: float = 4.0e6
+    expert_bytes: int | None = None
+
+    @property
+    def buf_elems(self) -> int:
+        return (3 if self.act == ACT_SWIGLU else 2) * self.d * self.f
+
+    @property
+    def buf_bytes(self) -> int:
+        return self.buf_elems * (4 if self.fp32_weights else 2)
+
+
+class DecodeEngine:
+    def __init__(self, spec: EngineSpec, mirrors, gate_w: torch.Tensor, gate_b: torch.Tensor,
+                 tbl_ids: torch.Tensor | None, tbl_len: torch.Tensor | None, taus, initial,
+                 static_freq=None):
+        if spec.method not in METHODS or spec.policy not in POLICIES:
+            raise ConfigurationError(f"unknown method/policy {spec.method}/{spec.policy}")
+        self.spec = spec
+        self.mirrors = mirrors  # keep alive
+        self.gate_w = gate_w.contiguous()
+        self.gate_b = gate_b.contiguous()
+        self.tbl_ids = None if tbl_ids is None else tbl_ids.contiguous()
+        self.tbl_len = None if tbl_len is None else tbl_len.contiguous()
+        cfg = N.EngineConfig()
+        cfg.num_layers, cfg.num_experts, cfg.top_k = spec.num_layers, spec.num_experts, spec.top_k
+        cfg.d, cfg.f, cfg.act = spec.d, spec.f, spec.act
+        cfg.max_batch, cfg.capacity, cfg.staging = spec.max_batch, spec.capacity, spec.staging
+        cfg.method, cfg.policy = METHODS[spec.method], POLICIES[spec.policy]
+        cfg.search_rank_h, cfg.fallback = spec.search_rank_h, spec.fallback
+        cfg.prefetch_enabled, cfg.n_tile = int(spec.prefetch), spec.n_tile
+        cfg.fp32_weights = int(spec.fp32_weights)
+        cfg.rho = -1 if spec.rho is None else int(spec.rho)
+        cfg.beta, cfg.temperature = spec.beta, spec.temperature
+        cfg.gamma = -1.0 if spec.gamma is None else spec.gamma
+        ebytes = spec.expert_bytes if spec.expert_bytes is not None else spec.buf_bytes
+        cfg.load_ms, cfg.hit_ms, cfg.compute_ms = spec.load_ms, spec.hit_ms, spec.compute_ms
+        cfg.prefetch_ms = spec.prefetch_ms if spec.prefetch_ms is not None else \
+            1000.0 * ebytes / spec.pcie_bw_bytes_per_s
+        cfg.expert_bytes = ebytes
+        L, E = spec.num_layers, spec.num_experts
+        ptrs = (C.c_void_p * L)(*[m.ptr for m in mirrors])
+        tau = (C.c_double * L)(*[(-1.0 if t is None else float(t)) for t in taus])
+        cap = max(spec.capacity, 1)
+        init = np.full((L, cap), -1, np.int32)
+        for l, row in enumerate(initial):
+            init[l, :len(row)] = row
+        sf = None
+        if static_freq is not None:
+            sf = np.ascontiguousarray(np.asarray(static_freq, np.float64).reshape(L, E))
+        h = C.c_void_p()
+        N.call("bm_engine_create", C.byref(cfg), ptrs, self.gate_w.data_ptr(), self.gate_b.data_ptr(),
+               None if self.tbl_ids is None else self.tbl_ids.data_ptr(),
+               None if self.tbl_len is None else self.tbl_len.data_ptr(),
+               0 if self.tbl_ids is None else int(self.tbl_ids.shape[-1]),
+               tau, init.ctypes.data, None if sf is None else sf.ctypes.data, C.byref(h))
+        self._h = h.value
+        self._cfg = cfg
+
+    def step(self, h: torch.Tensor, tokens) -> torch.Tensor:
+        """One decode step (all layers) on h [B,d] fp32, in place."""
+        B = h.shape[0]
+        tok = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32))
+        N.call("bm_engine_step", self._h, h.data_ptr(), B, tok.ctypes.data, torch.cuda.current_stream().cuda_stream)
+        return h
+
+    def stats(self, reset: bool = False) -> dict:
+        st = N.EngineStats()
+        N.call("bm_engine_stats_get", self._h, C.byref(st), int(reset))
+        return st.as_dict()
+
+    def device_bytes(self) -> int:
+        return int(N.lib().bm_engine_device_bytes(self._h))
+
+    def events(self):
+        """The control plane's event log as an [n,7] float64 array
+        (time, kind, layer, token, expert, bytes, stall) — memtier.SimEvent."""
+        c = N.lib().bm_engine_cache(self._h)
+        n = int(N.lib().bm_cache_num_events(c))
+        arr = (N.Event * max(n, 1))()
+        if n:
+            N.call("bm_cache_events", c, 0, n, arr)
+        return np.array([(e.time_ms, e.kind, e.layer, e.token, e.expert, e.bytes, e.stall_ms) for e in arr[:n]],
+                        dtype=np.float64).reshape(-1, 7)
+
+    def snapshot(self, layer: int) -> np.ndarray:
+        c = N.lib().bm_engine_cache(self._h)
+        m = np.zeros(self.spec.num_experts, np.uint8)
+        N.call("bm_cache_snapshot", c, layer, m.ctypes.data, None)
+        return m.astype(bool)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().bm_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,159 @@
+"""Synthetic offloaded-MoE workloads at the BASELINE shapes.
+
+Weights are random-init N(0, 1/fan_in) in bf16 (no checkpoints), generated
+on the GPU per expert and copied into per-layer pinned host mirrors. The
+router follows the reference's substrate recipe (unit cluster directions,
+Zipf-like bias, Gaussian-mixture token stream; substrate.py restating
+model.py:122-222, 350-375) at the named d/E, so routing is skewed and
+clustered the way the paper's buddy tables assume.
+
+Profiling (the paper's offline stage) runs on the GPU, layer-major: route
+the profile stream (K1), count co-activations (K6), forward with every
+expert resident (K3-K5), then rank buddies (K7) and calibrate tau from the
+TAE samples — cmd_profile + cmd_build (harness.py:70-158) over tensors.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops, substrate
+from .engine import DecodeEngine, EngineSpec, HostMirror, fill_mirror_from_device
+
+SHAPES = {
+    # name: (E, k, d, f, cache_rate)
+    "mixtral": (8, 2, 4096, 14336, 0.5),
+    "qwen3": (128, 8, 2048, 768, 0.25),
+    "dsv2lite": (64, 6, 2048, 1408, 0.5),
+    "tiny": (8, 2, 128, 256, 0.5),
+}
+
+
+def initial_residents(num_experts: int, capacity: int, seed: int, layer: int):
+    """Seeded-permutation prefix, nested across capacities (memtier.py:132-140)."""
+    if capacity <= 0:
+        return []
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 21, layer]))
+    return sorted(int(v) for v in rng.permutation(num_experts)[:capacity])
+
+
+def host_mem_available() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 64 << 30
+
+
+@dataclass
+class Workload:
+    name: str
+    spec: substrate.ModelSpec
+    eng: EngineSpec
+    mirrors: list
+    gate_w: torch.Tensor
+    gate_b: torch.Tensor
+    tbl_ids: torch.Tensor
+    tbl_len: torch.Tensor
+    taus: list
+    initial: list
+    profile_seconds: float = 0.0
+    mean_buddies: float = 0.0
+    extra: dict = field(default_factory=dict)
+
+    def engine(self, method: str = "buddy", **overrides) -> DecodeEngine:
+        kw = dict(self.eng.__dict__)
+        kw.update(overrides)
+        kw["method"] = method
+        es = EngineSpec(**kw)
+        return DecodeEngine(es, self.mirrors, self.gate_w, self.gate_b,
+                            self.tbl_ids if method == "buddy" else None,
+                            self.tbl_len if method == "buddy" else None,
+                            self.taus, self.initial)
+
+    def tokens(self, seed: int, n: int) -> np.ndarray:
+        return substrate.token_stream(self.spec, seed, n).astype(np.float32)
+
+    def close(self):
+        for m in self.mirrors:
+            m.close()
+
+
+def _gen_expert(gen, d, f, device):
+    """One SwiGLU expert [W1 | W3 | W2] bf16, N(0, 1/fan_in)."""
+    out = torch.empty(3 * d * f, device=device, dtype=torch.bfloat16)
+    out[: 2 * d * f].normal_(0.0, d ** -0.5, generator=gen)
+    out[2 * d * f:].normal_(0.0, f ** -0.5, generator=gen)
+    return out
+
+
+def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: int = 0,
+          profile_tokens: int = 4096, alpha: float = 0.95, k_max: int | None = None, tau_percentile: float = 15.0,
+          clusters: int | None = None, n_tile: int = 64, device: str = "cuda", rho: int | None = 3,
+          log=None) -> Workload:
+    import time
+    E, k, d, f, rate = SHAPES[name]
+    cap = int(math.floor(rate * E))
+    k_max = k_max if k_max is not None else min(16, E - 1)
+    spec = substrate.ModelSpec(num_layers=layers, experts_per_layer=E, top_k=k, hidden_dim=d, ffn_dim=f,
+                               num_clusters=clusters if clusters is not None else min(E, 8), seed=7)
+    gw, gb = substrate.gate_weights(spec)
+    gate_w = torch.from_numpy(gw.astype(np.float32)).to(device)
+    gate_b = torch.from_numpy(gb.astype(np.float32)).to(device)
+    buf_elems = 3 * d * f
+    buf_bytes = buf_elems * 2
+    t0 = time.time()
+    mirrors = []
+    gen = torch.Generator(device=device)
+    arena = torch.empty(E, buf_elems, device=device, dtype=torch.bfloat16)
+    ids_all = torch.full((layers, E, k_max), -1, device=device, dtype=torch.int32)
+    len_all = torch.zeros(layers, E, device=device, dtype=torch.int32)
+    taus = []
+    x = torch.from_numpy(substrate.token_stream(spec, 1, profile_tokens).astype(np.float32)).to(device)
+    warm = min(256, profile_tokens)
+    ws = None
+    mean_len = []
+    for l in range(layers):
+        gen.manual_seed(seed * 100003 + l)
+        for e in range(E):
+            arena[e].copy_(_gen_expert(gen, d, f, device))
+        m = HostMirror(E * buf_bytes)
+        fill_mirror_from_device(m, arena)
+        mirrors.append(m)
+        # ---- profile this layer (full residency) ----
+        r = ops.gate_topk(x, gate_w[l], gate_b[l], k)
+        wc, wp = ops.coact_count(r.topk[:warm], E)
+        mc, mp = ops.coact_count(r.topk[warm:], E)
+        pairs = ops.counts_to_f64(mp, wp, 0.0)           # profile.warmup_weight = 0 (config.py:80)
+        t = ops.buddy_rank(pairs, 1e-3, alpha, k_max)
+        ids_all[l], len_all[l] = t.ids, t.lens
+        mean_len.append(float(t.lens.float().mean()))
+        s, _ = torch.sort(r.tae)                          # calibrate_tau, nearest rank (gating.py:111-123)
+        idx = max(1, math.ceil(tau_percentile * s.numel() / 100.0)) - 1
+        taus.append(float(s[min(idx, s.numel() - 1)]))
+        kept = torch.zeros_like(r.topk, dtype=torch.uint8)  # identity plan: full residency
+        perm = ops.permute(r.topk, kept, E)
+        if ws is None or ws.r_max < perm.r_max:
+            ws = ops.FfnWorkspace(E, d, f, perm.r_max, 256, device)
+        xp = ops.gather_rows(x, perm, 1)
+        yp = ops.expert_ffn_bf16(xp, perm, arena, torch.arange(E, device=device, dtype=torch.int32), d, f,
+                                 ops.ACT_SWIGLU, ws)
+        x = ops.combine(yp, perm, r.probs, kept, h_in=x)
+        if log:
+            log(f"layer {l}: mirror {buf_bytes * E / 2**30:.2f} GiB, tau {taus[-1]:.4f}, "
+                f"mean buddies {mean_len[-1]:.2f}, {time.time() - t0:.1f}s")
+    torch.cuda.synchronize()
+    del arena, ws
+    initial = [initial_residents(E, cap, 0, l) for l in range(layers)]
+    es = EngineSpec(num_layers=layers, num_experts=E, top_k=k, d=d, f=f, capacity=cap, max_batch=max_batch,
+                    act=ops.ACT_SWIGLU, search_rank_h=k_max, rho=rho, n_tile=n_tile, expert_bytes=buf_bytes)
+    return Workload(name, spec, es, mirrors, gate_w, gate_b, ids_all, len_all, taus, initial,
+                    profile_seconds=time.time() - t0, mean_buddies=float(np.mean(mean_len)))
