@@ -149,6 +149,17 @@ int bm_expert_ffn_f32(const float *x_perm, const int32_t *expert_count, const in
  * SW128 bf16 intermediate H. y_perm fp32 [r_max][d].
  * Requires d % 128 == 0, f % 128 == 0. n_tile (16..256, multiple of 16)
  * caps the per-tile token count; larger expert segments are chunked. */
+/* bf16 expert buffers use the HBM-native "UMMA-tiled" layout: each weight
+ * matrix W[M][K] is stored as 16 KB blocks (128 rows x 64 columns, rows in
+ * the 128-byte-swizzled K-major shared-memory image), ordered
+ * [m-tile][k-block][matrix], with W1/W3 interleaved per block for SwiGLU:
+ *   SWIGLU buffer: [W1|W3 interleaved blocks (2*f*d) | W2 blocks (d*f)]
+ *   TANH buffer:   [Win^T blocks (f*d) | Wout^T blocks (d*f)]
+ * so one k-step of every matrix is one contiguous bulk copy. bm_pack_expert_bf16
+ * converts row-major matrices (w1,w3: [f][d], w2: [d][f]; TANH: w1 = Win^T,
+ * w2 = Wout^T, w3 = NULL) into one buffer. */
+int bm_pack_expert_bf16(const void *w1, const void *w3, const void *w2, int64_t d, int64_t f, int32_t act, void *dst,
+                        bm_stream_t stream);
 int64_t bm_expert_ffn_bf16_workspace(int64_t E, int64_t d, int64_t f, int64_t r_max, int64_t n_tile);
 int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const int32_t *expert_offset, int64_t E,
                        int64_t d, int64_t f, int32_t act, const void *w_arena, int64_t n_bufs,

@@ -7,6 +7,7 @@
 // streams, CUDA events ordering buffer reuse, and the kernel sequence
 // gate -> remap -> permute -> grouped FFN -> combine per layer.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -227,8 +228,14 @@ struct bm_engine {
                                       h_ws, y_perm, s));
         } else {
             ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, E, r_max, 1, x_perm, s));
+            // the host already knows every expert's row count: size the GEMM's
+            // token tile to it (smaller B stages -> deeper pipeline, more chains)
+            int maxc = 0;
+            for (int e = 0; e < E; ++e) maxc = std::max(maxc, (int)cnt[e]);
+            int nt = std::min(cfg.n_tile, std::max(16, (maxc + 15) / 16 * 16));
+            if (getenv("BMOE_NTILE_FIXED")) nt = cfg.n_tile;
             ENG_TRY(bm_expert_ffn_bf16(x_perm, count, offset, E, d, f, cfg.act, arena, nbufs, buf_of_dev[par],
-                                       r_max, cfg.n_tile, ffn_ws, ffn_ws_bytes, y_perm, s));
+                                       r_max, nt, ffn_ws, ffn_ws_bytes, y_perm, s));
         }
         ENG_TRY(bm_combine(y_perm, slot_row, probs, kind, B, k, d, h, 0.5f, h, s));
         // 9. release buffers of experts the control plane no longer holds

@@ -2,24 +2,29 @@
 //
 // Decode is weight-streaming: every executed expert's W1/W3/W2 must cross
 // HBM once per layer-step while the token count per expert is tiny. So the
-// weights are the M=128 operand ("swap-AB") fed by TMA with 128B swizzle,
-// the permuted tokens are the N operand (16..n_tile columns) moved by plain
-// bulk copies of a pre-swizzled image (gather_sw128), and accumulators live
-// in TMEM. One persistent CTA per SM walks an equal share of the global
-// (tile, k-block) iteration space ("stream-K"), so HBM traffic is balanced
-// across all 148 SMs regardless of how many experts a step executes.
-// Split tiles are reduced deterministically (fixed CTA order, no atomics)
-// by a fixup kernel that also applies SwiGLU / tanh and writes GEMM2's B
-// operand in the same swizzled image.
+// weights are the M=128 operand ("swap-AB"), stored in HBM already in the
+// UMMA-tiled, 128B-swizzled image (bm_pack_expert_bf16) so each pipeline
+// stage is ONE contiguous bulk copy (TMA engine, UBLKCP) of KPS k-blocks of
+// every matrix; the permuted tokens are the N operand (16..n_tile columns,
+// moved the same way from a pre-swizzled image written by gather_sw128 /
+// the GEMM1 fixup); accumulators live in TMEM. One persistent CTA per SM
+// walks an equal share of the global (tile, k-step) iteration space
+// ("stream-K"), so HBM traffic is balanced over all 148 SMs however many
+// experts a step executes. Split tiles are reduced deterministically (fixed
+// CTA order, no atomics) by a fixup kernel that also applies SwiGLU / tanh
+// and writes GEMM2's B operand in the same swizzled image.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM
-// allocator, w3 idle, w4-7 epilogue (TMEM lane quadrants 0-3).
+// Warp roles (256 threads): w0 producer (bulk copies), w1 MMA issuer (one
+// thread; descriptors are precomputed per stage and advanced by compile-time
+// offsets — at decode N the MMA *issue* rate, not the math, bounds the weight
+// stream), w2 TMEM allocator, w3 idle, w4-7 epilogue (TMEM lane quadrants).
 //
 // Reference semantics: Expert.__call__ / forward_batch (model.py:85-99,
 // 318-340); SwiGLU is the Mixtral/Qwen3/DSV2 expert (no reference oracle).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include <mutex>
 #include <vector>
@@ -31,11 +36,11 @@ namespace bm {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kBM = 128;             // weight rows per tile (UMMA M)
-constexpr int kBK = 64;              // K per stage (one 128-byte swizzle row)
+constexpr int kBM = 128;                    // weight rows per tile (UMMA M)
+constexpr int kBK = 64;                     // K per k-block (one 128-byte swizzle row)
 constexpr int kATileBytes = kBM * kBK * 2;  // 16 KB
 constexpr int kMaxE = 256;
-constexpr int kSmemBudget = 220 * 1024;  // dynamic; static smem (schedule, barriers) comes on top
+constexpr int kSmemBudget = 220 * 1024;     // dynamic; static smem (schedule, barriers) comes on top
 
 struct Sched {
     // device-side schedule, identical in every kernel that needs it
@@ -49,12 +54,14 @@ struct GemmParams {
     const int32_t *count;
     const int32_t *offset;
     const int32_t *buf_of_expert;
-    int E, M, K, nmat, n_tile;
-    int a_rows_per_buf, a_row_off0, a_row_off1;
+    int E, M, K, nmat, n_tile, kps;
+    const uint8_t *arena;     // expert buffers in the UMMA-tiled layout
+    long long buf_bytes;      // bytes per buffer
+    long long mat_off;        // byte offset of this GEMM's weight region inside a buffer
     const uint8_t *b_planes;  // [K/64][r_max][128 B]
     long long b_plane_bytes;
-    float *partials;           // slot = (tile + cta) * nmat * n_tile * 128 floats
-    int num_ctas;              // launched grid (persistent)
+    float *partials;          // slot (tile + cta): nmat * n_tile * 128 floats
+    int num_ctas;             // launched grid (persistent)
 };
 
 __device__ void build_sched(Sched &s, const int32_t *count, int E, int n_tile, int mtiles) {
@@ -78,8 +85,8 @@ struct TileInfo {
     int row0;                // first permuted row of the chunk
 };
 
-__device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int mtiles, int n_tile,
-                                                const int32_t *count, const int32_t *offset) {
+__device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int n_tile, const int32_t *count,
+                                                const int32_t *offset) {
     int lo = 0, hi = s.n_act - 1;
     while (lo < hi) {  // last a with tile_prefix[a] <= t
         int mid = (lo + hi + 1) >> 1;
@@ -99,8 +106,8 @@ __device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int mtile
 
 __device__ __forceinline__ long long range_start(int c, long long T, int G) { return (long long)c * T / G; }
 
-__global__ void __launch_bounds__(kThreads, 1)
-    ffn_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, GemmParams p) {
+template <int NMAT, int KPS>
+__global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ Sched sched;
     __shared__ __align__(8) uint64_t bars[64];
@@ -109,28 +116,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     const int mtiles = p.M / kBM;
-    const int kb_per_tile = p.K / kBK;
+    const int steps_per_tile = p.K / (kBK * KPS);  // pipeline steps per tile
 
     if (threadIdx.x == 0) build_sched(sched, p.count, p.E, p.n_tile, mtiles);
     __syncthreads();
-    const long long T = (long long)sched.tile_prefix[sched.n_act] * kb_per_tile;
+    const long long T = (long long)sched.tile_prefix[sched.n_act] * steps_per_tile;
     const int G = (int)min((long long)p.num_ctas, T);
     const int cta = blockIdx.x;
     if (cta >= G) return;  // uniform for the whole CTA
     const long long it0 = range_start(cta, T, G), it1 = range_start(cta + 1, T, G);
 
-    // smem carve-up: stages of [A0 | A1 | B], 1024-aligned
+    // smem: stages of [A: KPS x NMAT x 16 KB | B: KPS x bsz], 1024-aligned
+    constexpr uint32_t kAStage = (uint32_t)(KPS * NMAT) * kATileBytes;
     const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
-    const uint32_t b_bytes_max = (uint32_t)p.n_tile * 128u;
-    const uint32_t stage_bytes = (uint32_t)p.nmat * kATileBytes + ((b_bytes_max + 1023u) & ~1023u);
+    const uint32_t bsz = ((uint32_t)p.n_tile * 128u + 1023u) & ~1023u;
+    const uint32_t stage_bytes = kAStage + (uint32_t)KPS * bsz;
     const int stages = min(16, (int)((kSmemBudget - 1024) / stage_bytes));
-    const int acc_stages = (2 * p.nmat * p.n_tile <= 512) ? 2 : 1;
+    // TMEM: accumulator stage [NMAT][n_tile] fp32 columns, double-buffered when it fits
+    const int acc_stages = (2 * NMAT * p.n_tile <= 512) ? 2 : 1;
     const uint32_t acc_cols = acc_stages == 2 ? 256u : 512u;
 
-    const uint32_t full0 = ptx::smem_u32(&bars[0]);        // [stages]
-    const uint32_t empty0 = ptx::smem_u32(&bars[16]);      // [stages]
-    const uint32_t tfull0 = ptx::smem_u32(&bars[32]);      // [2]
-    const uint32_t tempty0 = ptx::smem_u32(&bars[34]);     // [2]
+    const uint32_t full0 = ptx::smem_u32(&bars[0]);     // [stages]
+    const uint32_t empty0 = ptx::smem_u32(&bars[16]);   // [stages]
+    const uint32_t tfull0 = ptx::smem_u32(&bars[32]);   // [2]
+    const uint32_t tempty0 = ptx::smem_u32(&bars[34]);  // [2]
 
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -143,7 +152,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_a);
     if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(&tmem_base_sh), 512);
     ptx::tc_fence_before();
     __syncthreads();
@@ -151,27 +159,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = tmem_base_sh;
 
     if (warp == 0 && lane == 0) {
-        // ===================== TMA producer =====================
+        // ===================== producer =====================
         const uint64_t pol = ptx::policy_evict_first();  // weights stream through once
         int stage = 0;
         uint32_t phase = 0;
         long long it = it0;
         while (it < it1) {
-            const int tile = (int)(it / kb_per_tile);
-            const int kb_end = (int)min((long long)kb_per_tile, it1 - (long long)tile * kb_per_tile);
-            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile, p.count, p.offset);
+            const int tile = (int)(it / steps_per_tile);
+            const int st_end = (int)min((long long)steps_per_tile, it1 - (long long)tile * steps_per_tile);
+            const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
             const int buf = p.buf_of_expert[ti.e];
-            const int arow = buf * p.a_rows_per_buf + ti.mtile * kBM;
+            // the m-tile's blocks are contiguous along k: [mt][kb][NMAT][16 KB]
+            const uint8_t *a_src = p.arena + (long long)buf * p.buf_bytes + p.mat_off +
+                                   (long long)ti.mtile * steps_per_tile * kAStage;
+            const uint8_t *b_src = p.b_planes + (long long)ti.row0 * 128;
             const uint32_t bbytes = (uint32_t)ti.n * 128u;
-            for (int kb = (int)(it - (long long)tile * kb_per_tile); kb < kb_end; ++kb, ++it) {
+            for (int st = (int)(it - (long long)tile * steps_per_tile); st < st_end; ++st, ++it) {
                 ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1u);
                 const uint32_t sA = base + (uint32_t)stage * stage_bytes;
-                const uint32_t sB = sA + (uint32_t)p.nmat * kATileBytes;
+                const uint32_t sB = sA + kAStage;
                 const uint32_t fb = full0 + 8 * stage;
-                ptx::mbar_expect_tx(fb, (uint32_t)p.nmat * kATileBytes + bbytes);
-                ptx::tma_load_2d(sA, &tmap_a, fb, kb * kBK, arow + p.a_row_off0, pol);
-                if (p.nmat == 2) ptx::tma_load_2d(sA + kATileBytes, &tmap_a, fb, kb * kBK, arow + p.a_row_off1, pol);
-                ptx::bulk_load(sB, p.b_planes + (long long)kb * p.b_plane_bytes + (long long)ti.row0 * 128, bbytes, fb);
+                ptx::mbar_expect_tx(fb, kAStage + (uint32_t)KPS * bbytes);
+                ptx::bulk_load_hint(sA, a_src + (long long)st * kAStage, kAStage, fb, pol);
+#pragma unroll
+                for (int i = 0; i < KPS; ++i)
+                    ptx::bulk_load(sB + i * bsz, b_src + (long long)(st * KPS + i) * p.b_plane_bytes, bbytes, fb);
                 if (++stage == stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -180,35 +192,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1 && lane == 0) {
         // ===================== MMA issuer (single thread) =====================
+        // Descriptor start addresses advance in 16-byte units: k-subblock kk
+        // (+32 B) -> +2, matrix/k-block (+16 KB) -> +1024, B k-block -> +bsz/16.
+        const uint64_t desc0 = ptx::sw128_desc(base);
+        const uint64_t stage_d = stage_bytes >> 4, bsz_d = bsz >> 4;
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         long long it = it0;
         while (it < it1) {
-            const int tile = (int)(it / kb_per_tile);
-            const int kb_end = (int)min((long long)kb_per_tile, it1 - (long long)tile * kb_per_tile);
-            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile, p.count, p.offset);
+            const int tile = (int)(it / steps_per_tile);
+            const int st_end = (int)min((long long)steps_per_tile, it1 - (long long)tile * steps_per_tile);
+            const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
             const uint32_t idesc = ptx::idesc_bf16_f32(kBM, (uint32_t)ti.n);
             ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1u);
             ptx::tc_fence_after();
-            const uint32_t dcol = tmem_base + (uint32_t)acc * acc_cols;
-            bool first = true;
-            for (int kb = (int)(it - (long long)tile * kb_per_tile); kb < kb_end; ++kb, ++it) {
+            const uint32_t d0 = tmem_base + (uint32_t)acc * acc_cols;
+            const uint32_t d1 = d0 + (uint32_t)p.n_tile;
+            uint32_t accum = 0;
+            for (int st = (int)(it - (long long)tile * steps_per_tile); st < st_end; ++st, ++it) {
                 ptx::mbar_wait(full0 + 8 * stage, phase);
                 ptx::tc_fence_after();
-                const uint32_t sA = base + (uint32_t)stage * stage_bytes;
-                const uint32_t sB = sA + (uint32_t)p.nmat * kATileBytes;
+                const uint64_t a = desc0 + (uint64_t)stage * stage_d;
+                const uint64_t b = a + (kAStage >> 4);
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk) {
-                    const uint64_t bdesc = ptx::sw128_desc(sB + kk * 32);
-                    for (int m = 0; m < p.nmat; ++m) {
-                        const uint64_t adesc = ptx::sw128_desc(sA + m * kATileBytes + kk * 32);
-                        ptx::mma_bf16(dcol + (uint32_t)(m * p.n_tile), adesc, bdesc, idesc,
-                                      (first && kk == 0) ? 0u : 1u);
+                for (int i = 0; i < KPS; ++i) {
+                    const uint64_t bi = b + (uint64_t)i * bsz_d;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        ptx::mma_bf16(d0, a + (uint64_t)((i * NMAT) * (kATileBytes >> 4) + 2 * kk), bi + 2 * kk, idesc,
+                                      accum);
+                        if (NMAT == 2)
+                            ptx::mma_bf16(d1, a + (uint64_t)((i * NMAT + 1) * (kATileBytes >> 4) + 2 * kk),
+                                          bi + 2 * kk, idesc, accum);
+                        accum = 1u;
                     }
                 }
-                first = false;
                 ptx::mma_commit(empty0 + 8 * stage);  // frees the smem stage when these MMAs finish
                 if (++stage == stages) {
                     stage = 0;
@@ -231,16 +251,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t acc_phase = 0;
         long long it = it0;
         while (it < it1) {
-            const int tile = (int)(it / kb_per_tile);
-            const long long tile_end = (long long)(tile + 1) * kb_per_tile;
+            const int tile = (int)(it / steps_per_tile);
+            const long long tile_end = (long long)(tile + 1) * steps_per_tile;
             it = min(tile_end, it1);
-            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile, p.count, p.offset);
+            const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             ptx::tc_fence_after();
             const long long slot = (long long)tile + cta;
-            float *dst = p.partials + slot * (long long)p.nmat * p.n_tile * kBM;
+            float *dst = p.partials + slot * (long long)NMAT * p.n_tile * kBM;
             const uint32_t tbase = tmem_base + (uint32_t)acc * acc_cols + ((uint32_t)(q * 32) << 16);
-            for (int m = 0; m < p.nmat; ++m) {
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m) {
                 for (int c0 = 0; c0 < ti.n; c0 += 16) {
                     float v[16];
                     ptx::tmem_ld16(tbase + (uint32_t)(m * p.n_tile + c0), v);
@@ -277,17 +298,17 @@ __global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, 
                                                         float *y_perm) {
     __shared__ Sched sched;
     const int mtiles = p.M / kBM;
-    const int kb_per_tile = p.K / kBK;
+    const int steps_per_tile = p.K / (kBK * p.kps);  // must match ffn_gemm_kernel's iteration space
     if (threadIdx.x == 0) build_sched(sched, p.count, p.E, p.n_tile, mtiles);
     __syncthreads();
     const int ntiles = sched.tile_prefix[sched.n_act];
-    const long long T = (long long)ntiles * kb_per_tile;
+    const long long T = (long long)ntiles * steps_per_tile;
     const int G = (int)min((long long)p.num_ctas, T);
     const int m_local = threadIdx.x;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile, p.count, p.offset);
-        const int c0 = cta_of((long long)tile * kb_per_tile, T, G);
-        const int c1 = cta_of((long long)(tile + 1) * kb_per_tile - 1, T, G);
+        const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
+        const int c0 = cta_of((long long)tile * steps_per_tile, T, G);
+        const int c1 = cta_of((long long)(tile + 1) * steps_per_tile - 1, T, G);
         const long long slot_elems = (long long)p.nmat * p.n_tile * kBM;
         const int m = ti.mtile * kBM + m_local;
         for (int n = 0; n < ti.n; ++n) {
@@ -312,37 +333,21 @@ __global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, 
     }
 }
 
-// ---------------------------------------------------------- host helpers
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
-                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                                    CUtensorMapFloatOOBfill);
-
-PFN_encodeTiled get_encode() {
-    static PFN_encodeTiled fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled>(p);
-    });
-    return fn;
-}
-
-int make_weight_map(CUtensorMap *map, const void *arena, long long rows, int K) {
-    PFN_encodeTiled enc = get_encode();
-    BM_REQUIRE(enc, BM_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(arena), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    BM_REQUIRE(r == CUDA_SUCCESS, BM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    return BM_OK;
+// Pack a row-major bf16 matrix W[M][K] into the UMMA-tiled expert layout:
+// 16 KB block (mt, kb, slot) at ((mt*K/64 + kb)*nmat + slot) * 16 KB holds
+// rows mt*128.. of columns kb*64.., row r's 16-byte chunk j at
+// r*128 + (j ^ (r & 7))*16 — the SW128 K-major smem image, so the GEMM's
+// producer moves whole k-steps of every matrix with one contiguous bulk copy.
+__global__ void pack_tiles_kernel(const uint4 *__restrict__ src, int M, int K, int nmat, int slot,
+                                  uint8_t *__restrict__ dst) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long cpr = K / 8;  // 16-byte chunks per row
+    if (idx >= (long long)M * cpr) return;
+    const int row = (int)(idx / cpr), c = (int)(idx % cpr);
+    const int kb = c >> 3, j = c & 7, mt = row >> 7, r = row & 127;
+    const long long off =
+        (((long long)mt * (K / 64) + kb) * nmat + slot) * kATileBytes + r * 128 + ((j ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4 *>(dst + off) = src[idx];
 }
 
 long long max_tiles(long long E, long long M, long long r_max, long long n_tile) {
@@ -353,7 +358,7 @@ long long max_tiles(long long E, long long M, long long r_max, long long n_tile)
 // kernel timing (for the bench's roofline), off by default
 struct Timing {
     bool enabled = false;
-    std::vector<cudaEvent_t> ev;  // 3 per call: before G1, between, after G2
+    std::vector<cudaEvent_t> ev;  // 4 per call: before/after GEMM1, before/after GEMM2
     std::mutex mu;
 } g_timing;
 
@@ -363,6 +368,42 @@ int record_event(cudaStream_t s) {
     BM_CUDA_TRY(cudaEventRecord(e, s));
     g_timing.ev.push_back(e);
     return BM_OK;
+}
+
+typedef void (*GemmFn)(GemmParams);
+
+template <int NMAT, int KPS>
+int launch_gemm(const GemmParams &g, int G, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        BM_CUDA_TRY(cudaFuncSetAttribute(ffn_gemm_kernel<NMAT, KPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSmemBudget));
+        attr = true;
+    }
+    ffn_gemm_kernel<NMAT, KPS><<<G, kThreads, kSmemBudget, s>>>(g);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+int launch_gemm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
+    if (g.nmat == 2) {
+        if (g.kps == 1) return launch_gemm<2, 1>(g, G, s);
+        if (g.kps == 2) return launch_gemm<2, 2>(g, G, s);
+        return launch_gemm<2, 4>(g, G, s);
+    }
+    if (g.kps == 1) return launch_gemm<1, 1>(g, G, s);
+    if (g.kps == 2) return launch_gemm<1, 2>(g, G, s);
+    return launch_gemm<1, 4>(g, G, s);
+}
+
+// k-blocks per pipeline stage: the largest of {4,2,1} dividing K/64 whose
+// stage fits twice in shared memory (BMOE_KPS overrides for tuning).
+int kps_for(int nmat, long long K, long long n_tile) {
+    int kps = 4;
+    if (const char *ev = getenv("BMOE_KPS")) kps = atoi(ev);
+    const long long per_kb = (long long)nmat * kATileBytes + ((n_tile * 128 + 1023) / 1024) * 1024;
+    while (kps > 1 && ((K / kBK) % kps || kps * per_kb > (kSmemBudget - 1024) / 2)) kps >>= 1;
+    return kps < 1 ? 1 : (kps > 4 ? 4 : kps);
 }
 
 }  // namespace
@@ -391,44 +432,34 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
     BM_REQUIRE(r_max % 16 == 0, BM_EINVAL, "r_max must be a multiple of 16");
     BM_REQUIRE(workspace_bytes >= bm_expert_ffn_bf16_workspace(E, d, f, r_max, n_tile), BM_EINVAL,
                "workspace too small");
+    (void)n_bufs;
     if (r_max == 0) return BM_OK;
     cudaStream_t s = as_stream(stream);
-    const long long buf_elems = (act == BM_ACT_SWIGLU ? 3 : 2) * d * f;
+    const long long buf_bytes = (act == BM_ACT_SWIGLU ? 3 : 2) * d * f * 2;
     const long long slots_bytes = ((workspace_bytes - (f / 64) * r_max * 128) / 1024) * 1024;
     float *partials = static_cast<float *>(workspace);
     uint8_t *h_planes = static_cast<uint8_t *>(workspace) + slots_bytes;
     const int G = sm_count();
-
-    // A operand views of the weight arena
-    CUtensorMap map1, map2;
-    if (int rc = make_weight_map(&map1, w_arena, n_bufs * (buf_elems / d), (int)d)) return rc;
-    if (int rc = make_weight_map(&map2, w_arena, n_bufs * (buf_elems / f), (int)f)) return rc;
-
-    GemmParams g1{expert_count, expert_offset, buf_of_expert, (int)E, (int)f, (int)d,
-                  act == BM_ACT_SWIGLU ? 2 : 1, (int)n_tile, (int)(buf_elems / d), 0, (int)f,
-                  static_cast<const uint8_t *>(x_perm), r_max * 128, partials, G};
+    const uint8_t *arena = static_cast<const uint8_t *>(w_arena);
+    const int nmat1 = act == BM_ACT_SWIGLU ? 2 : 1;
+    GemmParams g1{expert_count, expert_offset, buf_of_expert, (int)E, (int)f, (int)d, nmat1, (int)n_tile,
+                  kps_for(nmat1, d, n_tile), arena, buf_bytes, 0, static_cast<const uint8_t *>(x_perm),
+                  r_max * 128, partials, G};
     GemmParams g2{expert_count, expert_offset, buf_of_expert, (int)E, (int)d, (int)f, 1, (int)n_tile,
-                  (int)(buf_elems / f), act == BM_ACT_SWIGLU ? (int)(2 * d) : (int)d, 0, h_planes, r_max * 128,
+                  kps_for(1, f, n_tile), arena, buf_bytes, (long long)nmat1 * f * d * 2, h_planes, r_max * 128,
                   partials, G};
 
-    static bool attr_set = false;
-    if (!attr_set) {
-        BM_CUDA_TRY(cudaFuncSetAttribute(ffn_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
-        attr_set = true;
-    }
     const bool timing = g_timing.enabled;
     std::lock_guard<std::mutex> lk(g_timing.mu);
     if (timing && record_event(s)) return BM_ECUDA;
-    ffn_gemm_kernel<<<G, kThreads, kSmemBudget, s>>>(map1, g1);
-    BM_LAUNCH_CHECK();
+    if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
     if (timing && record_event(s)) return BM_ECUDA;
     const int fix_blocks = 4 * G;
     ffn_fixup_kernel<<<fix_blocks, kBM, 0, s>>>(g1, act == BM_ACT_SWIGLU ? 0 : 1, reinterpret_cast<uint4 *>(h_planes),
                                                 (int)r_max, nullptr);
     BM_LAUNCH_CHECK();
     if (timing && record_event(s)) return BM_ECUDA;
-    ffn_gemm_kernel<<<G, kThreads, kSmemBudget, s>>>(map2, g2);
-    BM_LAUNCH_CHECK();
+    if (int rc = launch_gemm_dispatch(g2, G, s)) return rc;
     if (timing && record_event(s)) return BM_ECUDA;
     ffn_fixup_kernel<<<fix_blocks, kBM, 0, s>>>(g2, 2, nullptr, 0, y_perm);
     BM_LAUNCH_CHECK();
@@ -457,4 +488,24 @@ extern "C" int64_t bm_kernel_times(float *out_host, int64_t cap) {
         out_host[n++] = b;
     }
     return n;
+}
+
+extern "C" int bm_pack_expert_bf16(const void *w1, const void *w3, const void *w2, int64_t d, int64_t f, int32_t act,
+                                   void *dst, bm_stream_t stream) {
+    BM_REQUIRE(w1 && w2 && dst && (act == BM_ACT_TANH || w3), BM_EINVAL, "bm_pack_expert_bf16: null pointer");
+    BM_REQUIRE(d % kBM == 0 && f % kBM == 0, BM_EINVAL, "d and f must be multiples of 128");
+    cudaStream_t s = as_stream(stream);
+    uint8_t *out = static_cast<uint8_t *>(dst);
+    const long long n1 = f * d / 8;
+    const unsigned g = (unsigned)((n1 + 255) / 256);
+    if (act == BM_ACT_SWIGLU) {
+        pack_tiles_kernel<<<g, 256, 0, s>>>(static_cast<const uint4 *>(w1), (int)f, (int)d, 2, 0, out);
+        pack_tiles_kernel<<<g, 256, 0, s>>>(static_cast<const uint4 *>(w3), (int)f, (int)d, 2, 1, out);
+        pack_tiles_kernel<<<g, 256, 0, s>>>(static_cast<const uint4 *>(w2), (int)d, (int)f, 1, 0, out + 2 * f * d * 2);
+    } else {
+        pack_tiles_kernel<<<g, 256, 0, s>>>(static_cast<const uint4 *>(w1), (int)f, (int)d, 1, 0, out);
+        pack_tiles_kernel<<<g, 256, 0, s>>>(static_cast<const uint4 *>(w2), (int)d, (int)f, 1, 0, out + f * d * 2);
+    }
+    BM_LAUNCH_CHECK();
+    return BM_OK;
 }

@@ -218,6 +218,32 @@ def expert_ffn_f32(x_perm, perm: Permutation, w_arena, buf_of_expert, d: int, f:
     return y
 
 
+def pack_expert_bf16(w1, w3, w2, act: int, out=None):
+    """Row-major bf16 expert matrices -> one UMMA-tiled buffer (bmoe.h layout).
+    SwiGLU: w1, w3 [f,d], w2 [d,f]. Tanh: w1 = Win^T [f,d], w2 = Wout^T [d,f], w3 None."""
+    f, d = w1.shape
+    n = (3 if act == ACT_SWIGLU else 2) * d * f
+    if out is None:
+        out = torch.empty(n, device=w1.device, dtype=torch.bfloat16)
+    for t, nm in ((w1, "w1"), (w2, "w2")) + (((w3, "w3"),) if act == ACT_SWIGLU else ()):
+        _cuda(t, nm, torch.bfloat16)
+    N.call("bm_pack_expert_bf16", _p(w1), _p(w3), _p(w2), d, f, act, _p(out), _s())
+    return out
+
+
+def pack_arena_bf16(arena_rowmajor, d: int, f: int, act: int):
+    """[n_bufs, buf_elems] row-major arena -> UMMA-tiled arena (same shape)."""
+    out = torch.empty_like(arena_rowmajor)
+    for b in range(arena_rowmajor.shape[0]):
+        row = arena_rowmajor[b]
+        if act == ACT_SWIGLU:
+            pack_expert_bf16(row[: f * d].view(f, d), row[f * d: 2 * f * d].view(f, d), row[2 * f * d:].view(d, f),
+                             act, out[b])
+        else:
+            pack_expert_bf16(row[: f * d].view(f, d), None, row[f * d:].view(d, f), act, out[b])
+    return out
+
+
 class FfnWorkspace:
     """Reusable workspace for the bf16 tcgen05 grouped FFN."""
 

@@ -123,8 +123,10 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     mean_len = []
     for l in range(layers):
         gen.manual_seed(seed * 100003 + l)
-        for e in range(E):
-            arena[e].copy_(_gen_expert(gen, d, f, device))
+        for e in range(E):  # row-major N(0, 1/fan_in), then the UMMA-tiled HBM layout
+            w = _gen_expert(gen, d, f, device)
+            ops.pack_expert_bf16(w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d), w[2 * f * d:].view(d, f),
+                                 ops.ACT_SWIGLU, arena[e])
         m = HostMirror(E * buf_bytes)
         fill_mirror_from_device(m, arena)
         mirrors.append(m)

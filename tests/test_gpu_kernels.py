@@ -255,7 +255,8 @@ def _bf16_case(rng, E, d, f, B, k, act, n_tile=64, bufs=None, drop=0.1):
     xs = _t(x)
     xp = ops.gather_rows(xs, perm, 1)
     ws = ops.FfnWorkspace(E, d, f, perm.r_max, n_tile)
-    yp = ops.expert_ffn_bf16(xp, perm, arena, _t(buf_of), d, f, act, ws)
+    tiled = ops.pack_arena_bf16(arena, d, f, act)
+    yp = ops.expert_ffn_bf16(xp, perm, tiled, _t(buf_of), d, f, act, ws)
     y = ops.combine(yp, perm, _t(probs), _t(kind))
     # fp32 torch reference over the same bf16-rounded weights and inputs;
     # H is rounded to bf16 like the kernel's GEMM2 operand
@@ -277,7 +278,7 @@ def _bf16_case(rng, E, d, f, B, k, act, n_tile=64, bufs=None, drop=0.1):
         for i, (b, s) in enumerate(sel):
             ref[b] += float(probs[b, s]) * out[i]
         del row
-    return y, ref, (xp, perm, arena, buf_of, ws)
+    return y, ref, (xp, perm, tiled, buf_of, ws)
 
 
 @pytest.mark.parametrize("E,d,f,B,k,act,n_tile", [

@@ -1,0 +1,84 @@
+"""Microbenchmark of the bf16 grouped expert FFN (K4) alone, decode-shaped.
+
+    python tools/ffn_microbench.py [--experts-active 4] [--tokens 16] [--iters 50]
+
+Builds a Mixtral-shaped arena (8 experts, d=4096, f=14336, UMMA-tiled bf16),
+routes `tokens` tokens top-2 over the first `experts-active` experts, and
+times bm_expert_ffn_bf16's two GEMM kernels with CUDA events (the library's
+kernel-timing hook). Each iteration rotates through 4 arena copies so the
+weights are never L2-resident (126 MB L2 vs 1.4 GB per call).
+Prints one JSON line: per-kernel ms, algorithmic GB/s, fraction of measured HBM.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2511_10054_b200 import _native as N  # noqa: E402
+from paper_2511_10054_b200 import ops  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--experts-active", type=int, default=4)
+    ap.add_argument("--tokens", type=int, default=16)
+    ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--d", type=int, default=4096)
+    ap.add_argument("--f", type=int, default=14336)
+    ap.add_argument("--E", type=int, default=8)
+    ap.add_argument("--n-tile", type=int, default=16)
+    ap.add_argument("--copies", type=int, default=4)
+    args = ap.parse_args()
+    E, d, f, B, A = args.E, args.d, args.f, args.tokens, args.experts_active
+    dev = "cuda"
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    arenas = []
+    for _ in range(args.copies):
+        ar = torch.empty(E, 3 * d * f, device=dev, dtype=torch.bfloat16)
+        for e in range(E):
+            w = torch.randn(3 * d * f, device=dev, generator=g).to(torch.bfloat16)
+            ops.pack_expert_bf16(w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d), w[2 * f * d:].view(d, f),
+                                 ops.ACT_SWIGLU, ar[e])
+        arenas.append(ar)
+    rng = np.random.default_rng(0)
+    topk = np.stack([rng.choice(A, 2, replace=False) for _ in range(B)]).astype(np.int32)
+    kind = np.zeros_like(topk, dtype=np.uint8)
+    perm = ops.permute(torch.from_numpy(topk).to(dev), torch.from_numpy(kind).to(dev), E)
+    x = torch.randn(B, d, device=dev)
+    xp = ops.gather_rows(x, perm, 1)
+    ws = ops.FfnWorkspace(E, d, f, perm.r_max, args.n_tile)
+    bufs = torch.arange(E, device=dev, dtype=torch.int32)
+    for i in range(5):
+        ops.expert_ffn_bf16(xp, perm, arenas[i % len(arenas)], bufs, d, f, ops.ACT_SWIGLU, ws)
+    torch.cuda.synchronize()
+    N.lib().bm_set_kernel_timing(1)
+    for i in range(args.iters):
+        ops.expert_ffn_bf16(xp, perm, arenas[i % len(arenas)], bufs, d, f, ops.ACT_SWIGLU, ws)
+    buf = np.zeros(2 * args.iters + 4, np.float32)
+    n = int(N.lib().bm_kernel_times(buf.ctypes.data, buf.size))
+    N.lib().bm_set_kernel_timing(0)
+    g1, g2 = float(np.median(buf[0:n:2])), float(np.median(buf[1:n:2]))
+    n_exp = int((perm.count > 0).sum())
+    b1 = n_exp * 2 * d * f * 2 + B * 2 * d * 2
+    b2 = n_exp * d * f * 2 + B * 2 * f * 2
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        peak = 6650.0
+    out = {"experts": n_exp, "tokens": B, "n_tile": args.n_tile, "gemm1_ms": g1, "gemm2_ms": g2,
+           "gemm1_gbs": b1 / g1 / 1e6, "gemm2_gbs": b2 / g2 / 1e6, "pair_gbs": (b1 + b2) / (g1 + g2) / 1e6,
+           "peak_gbs": peak, "gemm1_frac": b1 / g1 / 1e6 / peak, "gemm2_frac": b2 / g2 / 1e6 / peak,
+           "env": {k: v for k, v in os.environ.items() if k.startswith("BMOE_")}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
