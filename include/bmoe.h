@@ -244,6 +244,14 @@ void bm_cache_clear_events(bm_cache *c);
 int bm_cache_layer_state(const bm_cache *c, int32_t layer, int64_t *last_use_host, double *freq_host,
                          int64_t *scalars_host /* [tick, n_pending, waste, unused_resident] */);
 int bm_cache_pending(const bm_cache *c, int32_t layer, double *done_host, int32_t *expert_host, int64_t cap);
+/* Clock / cost model accessors (SimClock + PcieChannel state, CostModel),
+ * so a caller that owns the clock (memtier's free functions take it as an
+ * argument) can drive the replica. */
+int bm_cache_set_clock(bm_cache *c, double now, double free_at);
+int bm_cache_get_clock(const bm_cache *c, double *now_host, double *free_at_host);
+int bm_cache_set_costs(bm_cache *c, double expert_load_ms, double hit_ms, double prefetch_ms, int64_t expert_bytes);
+/* ResidencyState.insert (memtier.py:172-195); *victim_host = evicted id or -1. */
+int bm_cache_insert(bm_cache *c, int32_t layer, int32_t expert, int32_t via_prefetch, int32_t *victim_host);
 
 /* ------------------------------------------------ offloaded decode engine
  * The run_simulation inner loop (harness.py:315-393) over real memory: the

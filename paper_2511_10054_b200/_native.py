@@ -94,6 +94,10 @@ _SIGS = {
     "bm_cache_clear_events": (None, [P]),
     "bm_cache_layer_state": (C.c_int, [P, I32, P, P, P]),
     "bm_cache_pending": (C.c_int, [P, I32, P, P, I64]),
+    "bm_cache_set_clock": (C.c_int, [P, F64, F64]),
+    "bm_cache_get_clock": (C.c_int, [P, P, P]),
+    "bm_cache_set_costs": (C.c_int, [P, F64, F64, F64, I64]),
+    "bm_cache_insert": (C.c_int, [P, I32, I32, I32, P]),
 }
 
 _lib = None

@@ -235,7 +235,13 @@ extern "C" int bm_cache_apply_plan(bm_cache *c, int32_t layer, int64_t B, int64_
             if (kd == BM_KIND_SUBSTITUTED) {  // harness.py:371-373
                 ++subs;
                 c->access(L, orig, true, tok);
-                c->access(L, ex, false, tok);
+                // the stand-in was resident at snapshot time but an earlier
+                // token of this batch may have evicted it: then it misses too
+                bm_event ev = c->access(L, ex, false, tok);
+                if (ev.kind == BM_EV_MISS_ONDEMAND) {
+                    ++ondemand;
+                    bytes += ev.bytes;
+                }
             } else {
                 bm_event ev = c->access(L, ex, false, tok);
                 if (ev.kind == BM_EV_MISS_ONDEMAND) {
@@ -366,6 +372,49 @@ extern "C" int bm_cache_layer_state(const bm_cache *c, int32_t layer, int64_t *l
         scalars_host[2] = L.waste;
         scalars_host[3] = unused;
     }
+    return BM_OK;
+}
+
+extern "C" int bm_cache_set_clock(bm_cache *c, double now, double free_at) {
+    if (!c) return BM_EINVAL;
+    c->now = now;
+    c->free_at = free_at;
+    return BM_OK;
+}
+
+extern "C" int bm_cache_get_clock(const bm_cache *c, double *now_host, double *free_at_host) {
+    if (!c || !now_host || !free_at_host) return BM_EINVAL;
+    *now_host = c->now;
+    *free_at_host = c->free_at;
+    return BM_OK;
+}
+
+extern "C" int bm_cache_set_costs(bm_cache *c, double expert_load_ms, double hit_ms, double prefetch_ms,
+                                  int64_t expert_bytes) {
+    if (!c || expert_load_ms < 0 || hit_ms < 0 || prefetch_ms < 0 || expert_bytes <= 0) {
+        bm::set_error("bm_cache_set_costs: bad cost model");
+        return BM_ECONFIG;
+    }
+    c->load_ms = expert_load_ms;
+    c->hit_ms = hit_ms;
+    c->prefetch_ms = prefetch_ms;
+    c->expert_bytes = expert_bytes;
+    return BM_OK;
+}
+
+extern "C" int bm_cache_insert(bm_cache *c, int32_t layer, int32_t expert, int32_t via_prefetch, int32_t *victim_host) {
+    if (int rc = check_layer(c, layer)) return rc;
+    Layer &L = c->layers[layer];
+    if (expert < 0 || expert >= L.E) {
+        bm::set_error("expert id out of range");
+        return BM_EINVAL;
+    }
+    const int v = L.insert(expert, via_prefetch != 0);
+    if (L.resident > L.cap) {  // memtier.py:193-194
+        bm::set_error("residency exceeded capacity");
+        return BM_EINVARIANT;
+    }
+    if (victim_host) *victim_host = v;
     return BM_OK;
 }
 

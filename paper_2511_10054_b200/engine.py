@@ -168,6 +168,18 @@ class DecodeEngine:
         return np.array([(e.time_ms, e.kind, e.layer, e.token, e.expert, e.bytes, e.stall_ms) for e in arr[:n]],
                         dtype=np.float64).reshape(-1, 7)
 
+    def finish(self):
+        """Commit every in-flight transfer whose time has come, all layers —
+        the reference's end-of-run settle (harness.py:395-396)."""
+        c = N.lib().bm_engine_cache(self._h)
+        for l in range(self.spec.num_layers):
+            N.call("bm_cache_settle", c, l)
+
+    def sorted_events(self):
+        """Event log ordered by time, ties in log order (harness.py:397)."""
+        ev = self.events()
+        return ev[np.argsort(ev[:, 0], kind="stable")] if len(ev) else ev
+
     def snapshot(self, layer: int) -> np.ndarray:
         c = N.lib().bm_engine_cache(self._h)
         m = np.zeros(self.spec.num_experts, np.uint8)
