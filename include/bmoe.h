@@ -199,6 +199,23 @@ int bm_counts_to_f64(const unsigned long long *warm, const unsigned long long *m
  * Writes ids[E][k_max] (-1 padded), weights[E][k_max], lens[E]. E <= 1024. */
 int bm_buddy_rank(const double *pair_matrix, int64_t E, double eps, double alpha, int64_t k_max, int32_t *ids,
                   double *weights, int32_t *lens, bm_stream_t stream);
+/* profiler.conditional_row for every pivot (profiler.py:98-119): q_out[E][E],
+ * degenerate_out[E] = 1 where the row has no mass (caller raises). */
+int bm_conditional_rows(const double *pair_matrix, int64_t E, double eps, double *q_out, uint8_t *degenerate_out,
+                        bm_stream_t stream);
+/* buddies.cft_prefix (buddies.py:79-95) on R given rows q[R][E]: t_out[R] =
+ * min(t, nnz), order_out[R][E] = stable descending order (-1 past t),
+ * degenerate_out[R] = 1 where the row sums to <= 0. */
+int bm_cft_prefix(const double *q_rows, int64_t R, int64_t E, double alpha, int32_t *t_out, int32_t *order_out,
+                  uint8_t *degenerate_out, bm_stream_t stream);
+/* gating.tae / margin / token_gate from given renormalised probabilities
+ * p[B][k] f64 (gating.py:71-108). */
+int bm_gate_from_probs(const double *probs, int64_t B, int64_t k, double tau, double gamma, double *tae,
+                       double *margin, uint8_t *token_allowed, bm_stream_t stream);
+/* gating.distribution_gate (gating.py:126-145): delta over n requested ids
+ * (duplicates counted) against the residency bitmap; allowed = !(delta >= beta). */
+int bm_distribution_gate(const int32_t *requested, int64_t n, const uint32_t *resident_bitmap, double beta,
+                         double *delta_out, uint8_t *allowed_out, bm_stream_t stream);
 
 /* ----------------------------------------------- expert cache control plane
  * Exact replica of memtier.ResidencyState/access/prefetch/settle

@@ -79,6 +79,10 @@ _SIGS = {
     "bm_coact_weighted": (C.c_int, [P, P, I64, I64, I64, F64, P, P]),
     "bm_counts_to_f64": (C.c_int, [P, P, I64, F64, P, P]),
     "bm_buddy_rank": (C.c_int, [P, I64, F64, F64, I64, P, P, P, P]),
+    "bm_conditional_rows": (C.c_int, [P, I64, F64, P, P, P]),
+    "bm_cft_prefix": (C.c_int, [P, I64, I64, F64, P, P, P, P]),
+    "bm_gate_from_probs": (C.c_int, [P, I64, I64, F64, F64, P, P, P, P]),
+    "bm_distribution_gate": (C.c_int, [P, I64, P, F64, P, P, P]),
     "bm_cache_create": (C.c_int, [I32, I32, I32, I32, P, P, F64, F64, F64, I64, P]),
     "bm_cache_destroy": (None, [P]),
     "bm_cache_access": (C.c_int, [P, I32, I32, I32, I32, P]),

@@ -137,35 +137,46 @@ __global__ void counts_to_f64_kernel(const unsigned long long *warm, const unsig
 constexpr int kRankWarps = 4;
 constexpr int kRankMaxE = 1024;
 
+// rows_are_q: M already holds conditional rows q (cft_prefix on a given row);
+// q_out / degenerate_out (optional) export profiler.conditional_row.
 __global__ void __launch_bounds__(kRankWarps * 32) buddy_rank_kernel(const double *__restrict__ M, int E, double eps,
                                                                       double thr, int k_max, int32_t *ids,
-                                                                      double *weights, int32_t *lens) {
+                                                                      double *weights, int32_t *lens, int rows_are_q,
+                                                                      double *q_out, uint8_t *degenerate_out, int R) {
     __shared__ double q[kRankWarps][kRankMaxE];
     __shared__ int order[kRankWarps][kRankMaxE];
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     const int p = blockIdx.x * kRankWarps + warp;
-    if (p >= E) return;
+    if (p >= R) return;
     double *qw = q[warp];
     int *ow = order[warp];
     // conditional_row (profiler.py:113-119): row + eps, diagonal forced to 0
-    for (int j = lane; j < E; j += 32) qw[j] = (j == p) ? 0.0 : dadd(M[(size_t)p * E + j], eps);
+    for (int j = lane; j < E; j += 32)
+        qw[j] = rows_are_q ? M[(size_t)p * E + j] : ((j == p) ? 0.0 : dadd(M[(size_t)p * E + j], eps));
     __syncwarp();
     double total = 0.0;
     if (lane == 0) total = pairwise_sum(qw, E);
     total = __shfl_sync(0xffffffffu, total, 0);
-    int32_t *oid = ids + (size_t)p * k_max;
-    double *ow_w = weights + (size_t)p * k_max;
+    int32_t *oid = ids ? ids + (size_t)p * k_max : nullptr;
+    double *ow_w = weights ? weights + (size_t)p * k_max : nullptr;
+    if (degenerate_out && lane == 0) degenerate_out[p] = !(total > 0.0);
     if (!(total > 0.0)) {  // degenerate pivot -> empty list (buddies.py:118-123)
-        for (int r = lane; r < k_max; r += 32) {
+        for (int r = lane; r < k_max && oid; r += 32) {
             oid[r] = -1;
             ow_w[r] = 0.0;
         }
-        if (lane == 0) lens[p] = 0;
+        if (q_out)
+            for (int j = lane; j < E; j += 32) q_out[(size_t)p * E + j] = 0.0;
+        if (lane == 0 && lens) lens[p] = 0;
         return;
     }
-    for (int j = lane; j < E; j += 32) qw[j] = ddiv(qw[j], total);
+    if (!rows_are_q)
+        for (int j = lane; j < E; j += 32) qw[j] = ddiv(qw[j], total);
     __syncwarp();
+    if (q_out)
+        for (int j = lane; j < E; j += 32) q_out[(size_t)p * E + j] = qw[j];
+    if (!lens) return;  // conditional rows only
     // stable argsort(-q): rank = #(strictly larger) + #(equal with lower id)
     int nnz = 0;
     for (int j = lane; j < E; j += 32) {
@@ -267,7 +278,33 @@ extern "C" int bm_buddy_rank(const double *pair_matrix, int64_t E, double eps, d
     BM_REQUIRE(pair_matrix && ids && weights && lens, BM_EINVAL, "bm_buddy_rank: null pointer");
     const double thr = alpha - 1e-9;  // buddies.py:25,94
     buddy_rank_kernel<<<(unsigned)((E + kRankWarps - 1) / kRankWarps), kRankWarps * 32, 0, as_stream(stream)>>>(
-        pair_matrix, (int)E, eps, thr, (int)k_max, ids, weights, lens);
+        pair_matrix, (int)E, eps, thr, (int)k_max, ids, weights, lens, 0, nullptr, nullptr, (int)E);
     BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_conditional_rows(const double *pair_matrix, int64_t E, double eps, double *q_out,
+                                   uint8_t *degenerate_out, bm_stream_t stream) {
+    BM_REQUIRE(E >= 1 && E <= kRankMaxE && pair_matrix && q_out, BM_EINVAL, "bm_conditional_rows: bad args");
+    BM_REQUIRE(eps >= 0.0, BM_EINVAL, "laplace_eps must be nonnegative");
+    buddy_rank_kernel<<<(unsigned)((E + kRankWarps - 1) / kRankWarps), kRankWarps * 32, 0, as_stream(stream)>>>(
+        pair_matrix, (int)E, eps, 0.0, 1, nullptr, nullptr, nullptr, 0, q_out, degenerate_out, (int)E);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+extern "C" int bm_cft_prefix(const double *q_rows, int64_t R, int64_t E, double alpha, int32_t *t_out,
+                             int32_t *order_out, uint8_t *degenerate_out, bm_stream_t stream) {
+    BM_REQUIRE(R >= 0 && E >= 1 && E <= kRankMaxE && q_rows && t_out && order_out, BM_EINVAL,
+               "bm_cft_prefix: bad args");
+    BM_REQUIRE(alpha > 0.0 && alpha <= 1.0, BM_EINVAL, "alpha must be in (0, 1]");
+    if (R == 0) return BM_OK;
+    // k_max = E: the list length is min(t, nnz) exactly as cft_prefix returns it
+    double *wscratch = nullptr;
+    BM_CUDA_TRY(cudaMallocAsync(&wscratch, (size_t)R * E * sizeof(double), as_stream(stream)));
+    buddy_rank_kernel<<<(unsigned)((R + kRankWarps - 1) / kRankWarps), kRankWarps * 32, 0, as_stream(stream)>>>(
+        q_rows, (int)E, 0.0, alpha - 1e-9, (int)E, order_out, wscratch, t_out, 1, nullptr, degenerate_out, (int)R);
+    BM_LAUNCH_CHECK();
+    BM_CUDA_TRY(cudaFreeAsync(wscratch, as_stream(stream)));
     return BM_OK;
 }

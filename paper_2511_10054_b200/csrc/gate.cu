@@ -200,3 +200,48 @@ extern "C" int bm_select_topk_f64(const double *logits, int64_t B, int64_t E, in
     BM_LAUNCH_CHECK();
     return BM_OK;
 }
+
+// ---------------------------------------------------------------- gates from given probabilities
+namespace bm {
+namespace {
+// TAE / margin / token gate of given renormalised probabilities p[B][k]
+// (gating.tae / margin / token_gate, gating.py:71-108): one thread per token.
+__global__ void gate_from_probs_kernel(const double *__restrict__ p, int B, int k, double tau, double gamma,
+                                       double *tae, double *margin, uint8_t *allowed) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const double *r = p + (size_t)b * k;
+    double h = 0.0, top1 = -1.0, top2 = -1.0;
+    for (int i = 0; i < k; ++i) {
+        const double v = r[i];
+        if (v > 0.0) h -= v * log(v);
+        if (v > top1) {
+            top2 = top1;
+            top1 = v;
+        } else if (v > top2) {
+            top2 = v;
+        }
+    }
+    double t = 0.0, m = 1.0;
+    if (k > 1) {
+        t = fmin(1.0, fmax(0.0, h / log((double)k)));
+        m = top1 - top2;
+    }
+    if (tae) tae[b] = t;
+    if (margin) margin[b] = m;
+    bool ok = !(t <= tau);
+    if (gamma >= 0.0 && m >= gamma) ok = false;
+    if (allowed) allowed[b] = ok ? 1 : 0;
+}
+}  // namespace
+}  // namespace bm
+
+extern "C" int bm_gate_from_probs(const double *probs, int64_t B, int64_t k, double tau, double gamma, double *tae,
+                                  double *margin, uint8_t *token_allowed, bm_stream_t stream) {
+    BM_REQUIRE(probs && B >= 0 && k >= 1, BM_EINVAL, "bm_gate_from_probs: bad args");
+    if (B == 0) return BM_OK;
+    bm::gate_from_probs_kernel<<<(unsigned)((B + 127) / 128), 128, 0, bm::as_stream(stream)>>>(
+        probs, (int)B, (int)k, tau, gamma, tae, margin, token_allowed);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}

@@ -236,3 +236,40 @@ extern "C" int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed,
     BM_LAUNCH_CHECK();
     return BM_OK;
 }
+
+// ---------------------------------------------------------------- distribution gate alone
+namespace bm {
+namespace {
+__global__ void __launch_bounds__(256) distribution_gate_kernel(const int32_t *__restrict__ req, long long n,
+                                                                const uint32_t *__restrict__ bitmap, double beta,
+                                                                double *delta_out, uint8_t *allowed_out) {
+    __shared__ int part[8];
+    int miss = 0;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        const int e = req[i];
+        miss += ((bitmap[e >> 5] >> (e & 31)) & 1u) ? 0 : 1;
+    }
+    for (int off = 16; off > 0; off >>= 1) miss += __shfl_xor_sync(0xffffffffu, miss, off);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = miss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long tot = 0;
+        for (int w = 0; w < 8; ++w) tot += part[w];
+        const double d = ddiv((double)tot, (double)n);  // np.mean of bools: exact integer / count
+        *delta_out = d;
+        if (allowed_out) *allowed_out = !(d >= beta) ? 1 : 0;
+    }
+}
+}  // namespace
+}  // namespace bm
+
+// gating.distribution_gate (gating.py:126-145) over n requested ids (duplicates counted).
+extern "C" int bm_distribution_gate(const int32_t *requested, int64_t n, const uint32_t *resident_bitmap,
+                                    double beta, double *delta_out, uint8_t *allowed_out, bm_stream_t stream) {
+    BM_REQUIRE(requested && resident_bitmap && delta_out && n >= 1, BM_EINVAL,
+               "requested expert set is empty or null");
+    bm::distribution_gate_kernel<<<1, 256, 0, bm::as_stream(stream)>>>(requested, n, resident_bitmap, beta, delta_out,
+                                                                       allowed_out);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
