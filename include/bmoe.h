@@ -319,6 +319,14 @@ int bm_engine_step(bm_engine *e, float *h, int64_t B, const int32_t *tokens_host
 /* Accumulated stats (synchronises the engine's events); reset clears them. */
 int bm_engine_stats_get(bm_engine *e, bm_engine_stats *out_host, int32_t reset);
 bm_cache *bm_engine_cache(bm_engine *e);
+/* Optional per-layer-step trace for parity checks: layer, batch size, the
+ * residency bitmap the remap saw, batch gate, and per token/slot topk,
+ * token gate, executed id and kind (all host memory; set_trace clears). */
+int bm_engine_set_trace(bm_engine *e, int32_t enable);
+int bm_engine_trace_size(const bm_engine *e, int64_t *records_host, int64_t *tokens_host);
+int bm_engine_trace_get(const bm_engine *e, int32_t *layer_host, int32_t *B_host, uint32_t *bitmaps_host,
+                        uint8_t *batch_ok_host, int32_t *topk_host, uint8_t *allowed_host, int32_t *executed_host,
+                        uint8_t *kind_host);
 /* Bytes of device memory held by the engine (arena + workspaces). */
 int64_t bm_engine_device_bytes(const bm_engine *e);
 

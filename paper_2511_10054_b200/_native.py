@@ -54,6 +54,9 @@ _SIGS = {
     "bm_engine_step": (C.c_int, [P, P, I64, P, P]),
     "bm_engine_stats_get": (C.c_int, [P, P, I32]),
     "bm_engine_cache": (P, [P]),
+    "bm_engine_set_trace": (C.c_int, [P, I32]),
+    "bm_engine_trace_size": (C.c_int, [P, P, P]),
+    "bm_engine_trace_get": (C.c_int, [P, P, P, P, P, P, P, P, P]),
     "bm_engine_device_bytes": (I64, [P]),
     "bm_host_alloc": (C.c_int, [I64, P]),
     "bm_host_free": (C.c_int, [P]),

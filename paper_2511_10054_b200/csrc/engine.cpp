@@ -83,6 +83,11 @@ struct bm_engine {
     std::vector<uint8_t> mask_tmp;
     std::vector<double> pend_done;
     std::vector<int32_t> pend_exp;
+    // optional per-layer-step trace (routing, gates, snapshot, plan) for parity checks
+    bool tracing = false;
+    std::vector<int32_t> tr_layer, tr_B, tr_topk, tr_exec;
+    std::vector<uint8_t> tr_allowed, tr_batch_ok, tr_kind;
+    std::vector<uint32_t> tr_bitmap;
 
     template <typename T>
     int dmalloc(T **p, size_t n) {
@@ -175,6 +180,16 @@ struct bm_engine {
         if (cfg.method == BM_METHOD_BUDDY) {
             for (int64_t b = 0; b < B; ++b) stats.gate_forbidden += allowed_h[b] ? 0 : 1;
             stats.batch_bypassed += batch_ok_h[0] ? 0 : 1;
+        }
+        if (tracing) {
+            tr_layer.push_back(l);
+            tr_B.push_back((int32_t)B);
+            tr_topk.insert(tr_topk.end(), topk_h, topk_h + B * k);
+            tr_exec.insert(tr_exec.end(), exec_h, exec_h + B * k);
+            tr_kind.insert(tr_kind.end(), kind_h, kind_h + B * k);
+            tr_allowed.insert(tr_allowed.end(), allowed_h, allowed_h + B);
+            tr_batch_ok.push_back(batch_ok_h[0]);
+            tr_bitmap.insert(tr_bitmap.end(), bitmap_host[par], bitmap_host[par] + words);
         }
         // 6. control plane: replay accesses in (token, slot) order (harness.py:363-382)
         int64_t out4[4];
@@ -456,6 +471,44 @@ extern "C" int bm_engine_stats_get(bm_engine *e, bm_engine_stats *out, int32_t r
 }
 
 extern "C" bm_cache *bm_engine_cache(bm_engine *e) { return e ? e->cache : nullptr; }
+
+extern "C" int bm_engine_set_trace(bm_engine *e, int32_t enable) {
+    if (!e) return BM_EINVAL;
+    e->tracing = enable != 0;
+    e->tr_layer.clear();
+    e->tr_B.clear();
+    e->tr_topk.clear();
+    e->tr_exec.clear();
+    e->tr_kind.clear();
+    e->tr_allowed.clear();
+    e->tr_batch_ok.clear();
+    e->tr_bitmap.clear();
+    return BM_OK;
+}
+
+extern "C" int bm_engine_trace_size(const bm_engine *e, int64_t *records, int64_t *tokens) {
+    if (!e || !records || !tokens) return BM_EINVAL;
+    *records = (int64_t)e->tr_layer.size();
+    *tokens = (int64_t)e->tr_allowed.size();
+    return BM_OK;
+}
+
+extern "C" int bm_engine_trace_get(const bm_engine *e, int32_t *layer, int32_t *B, uint32_t *bitmaps, uint8_t *batch_ok,
+                                   int32_t *topk, uint8_t *allowed, int32_t *executed, uint8_t *kind) {
+    if (!e) return BM_EINVAL;
+    auto cp = [](auto &v, auto *dst) {
+        if (dst && !v.empty()) memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(e->tr_layer, layer);
+    cp(e->tr_B, B);
+    cp(e->tr_bitmap, bitmaps);
+    cp(e->tr_batch_ok, batch_ok);
+    cp(e->tr_topk, topk);
+    cp(e->tr_allowed, allowed);
+    cp(e->tr_exec, executed);
+    cp(e->tr_kind, kind);
+    return BM_OK;
+}
 
 extern "C" int64_t bm_engine_device_bytes(const bm_engine *e) { return e ? e->device_bytes : 0; }
 

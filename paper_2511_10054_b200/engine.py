@@ -168,6 +168,36 @@ class DecodeEngine:
         return np.array([(e.time_ms, e.kind, e.layer, e.token, e.expert, e.bytes, e.stall_ms) for e in arr[:n]],
                         dtype=np.float64).reshape(-1, 7)
 
+    def set_trace(self, enable: bool = True):
+        N.call("bm_engine_set_trace", self._h, int(enable))
+
+    def trace(self) -> list:
+        """Per layer-step records: dict(layer, bitmap, batch_ok, topk, allowed, executed, kind)."""
+        nr, nt = C.c_int64(), C.c_int64()
+        N.call("bm_engine_trace_size", self._h, C.byref(nr), C.byref(nt))
+        nr, nt = nr.value, nt.value
+        k, words = self.spec.top_k, (self.spec.num_experts + 31) // 32
+        lay = np.zeros(max(nr, 1), np.int32)
+        Bs = np.zeros(max(nr, 1), np.int32)
+        bms = np.zeros(max(nr, 1) * words, np.uint32)
+        bok = np.zeros(max(nr, 1), np.uint8)
+        tk = np.zeros(max(nt, 1) * k, np.int32)
+        al = np.zeros(max(nt, 1), np.uint8)
+        ex = np.zeros(max(nt, 1) * k, np.int32)
+        kd = np.zeros(max(nt, 1) * k, np.uint8)
+        N.call("bm_engine_trace_get", self._h, lay.ctypes.data, Bs.ctypes.data, bms.ctypes.data, bok.ctypes.data,
+               tk.ctypes.data, al.ctypes.data, ex.ctypes.data, kd.ctypes.data)
+        out, t0 = [], 0
+        for i in range(nr):
+            B = int(Bs[i])
+            bits = bms[i * words:(i + 1) * words]
+            mask = np.array([(bits[e >> 5] >> (e & 31)) & 1 for e in range(self.spec.num_experts)], bool)
+            out.append(dict(layer=int(lay[i]), mask=mask, batch_ok=bool(bok[i]),
+                            topk=tk[t0 * k:(t0 + B) * k].reshape(B, k), allowed=al[t0:t0 + B].astype(bool),
+                            executed=ex[t0 * k:(t0 + B) * k].reshape(B, k), kind=kd[t0 * k:(t0 + B) * k].reshape(B, k)))
+            t0 += B
+        return out
+
     def finish(self):
         """Commit every in-flight transfer whose time has come, all layers —
         the reference's end-of-run settle (harness.py:395-396)."""

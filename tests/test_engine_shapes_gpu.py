@@ -1,0 +1,84 @@
+"""Size-independent parity at the BASELINE shapes (Mixtral-8x7B, Qwen3-30B-A3B,
+DeepSeek-V2-Lite routed experts), bf16 tensor-core engine with few layers:
+
+* every layer-step's remap plan equals the oracle planner run on the very
+  routing, gates and residency snapshot the GPU saw (bit-exact);
+* the control plane's full event log equals the oracle cache replica
+  replaying those plans (bit-exact), i.e. hit/miss/evict/prefetch decisions;
+* the delta/batch gate equals the oracle's on the same snapshot;
+* buffers: the engine never exceeds its HBM pool (no InvariantViolation).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2511_10054_b200 import workload as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_replay(wl, trace, B, n_steps, L):
+    """Replay harness.py:315-393 decisions with the oracle: plans from the
+    traced routing, then the memtier replica; returns the event array."""
+    E, cap = wl.eng.num_experts, wl.eng.capacity
+    st = [O.Residency(E, cap, O.POLICY_LRU, O.initial_residents(E, cap, O.POLICY_LRU, 0, l), None, l)
+          for l in range(L)]
+    clock, log = O.Clock(), []
+    prev = [dict() for _ in range(L)]
+    ebytes = wl.eng.expert_bytes
+    pre_ms = 1000.0 * ebytes / wl.eng.pcie_bw_bytes_per_s
+    ids_all = wl.tbl_ids.cpu().numpy()
+    lens_all = wl.tbl_len.cpu().numpy()
+    i = 0
+    for step in range(n_steps):
+        toks = np.arange(step * B, (step + 1) * B)
+        for l in range(L):
+            rec = trace[i]
+            i += 1
+            assert rec["layer"] == l
+            t = (l + 1) % L
+            O.prefetch(st[t], O.predict_for_layer(cap, prev[t]), clock, pre_ms, log)
+            O.settle(st[l], clock, ebytes, log)
+            assert np.array_equal(rec["mask"], st[l].mask), "snapshot differs"
+            delta, bok = O.distribution_gate(rec["topk"].ravel(), st[l].mask, wl.eng.beta)
+            assert bok == rec["batch_ok"]
+            ex, kd, _ = O.remap_batch(rec["topk"], None, st[l].mask, ids_all[l], np.zeros(ids_all[l].shape),
+                                      lens_all[l], rec["allowed"] & bok, wl.eng.search_rank_h,
+                                      -1 if wl.eng.rho is None else wl.eng.rho)
+            assert np.array_equal(ex, rec["executed"]) and np.array_equal(kd, rec["kind"]), f"plan differs at {i}"
+            slots = 0
+            for b in range(B):
+                for s in range(rec["topk"].shape[1]):
+                    if kd[b, s] == O.KIND_SUBSTITUTED:
+                        O.access(st[l], int(rec["topk"][b, s]), clock, wl.eng.load_ms, wl.eng.hit_ms, ebytes, True,
+                                 int(toks[b]), log)
+                    O.access(st[l], int(ex[b, s]), clock, wl.eng.load_ms, wl.eng.hit_ms, ebytes, False,
+                             int(toks[b]), log)
+                    slots += 1
+            clock.now += wl.eng.compute_ms * slots
+            cnt = {}
+            for e in ex.ravel():
+                cnt[int(e)] = cnt.get(int(e), 0) + 1
+            prev[l] = cnt
+    return np.array(log, np.float64).reshape(-1, 7)
+
+
+@pytest.mark.parametrize("name,layers,B", [("mixtral", 2, 16), ("qwen3", 3, 16), ("dsv2lite", 3, 8)])
+def test_engine_decisions_bit_exact_at_baseline_shapes(cuda_ok, name, layers, B):
+    wl = W.build(name, layers=layers, max_batch=B, profile_tokens=2048)
+    eng = wl.engine("buddy")
+    eng.set_trace(True)
+    steps = 4
+    x = torch.from_numpy(wl.tokens(2, steps * B)).cuda()
+    for s in range(steps):
+        eng.step(x[s * B:(s + 1) * B], np.arange(s * B, (s + 1) * B))
+    torch.cuda.synchronize()
+    ev = eng.events()
+    ref = _oracle_replay(wl, eng.trace(), B, steps, layers)
+    assert ev.shape == ref.shape and np.array_equal(ev, ref)
+    st = eng.stats()
+    assert st["tokens"] == steps * B and np.isfinite(x.cpu().numpy()).all()
+    eng.close()
+    wl.close()
