@@ -1,0 +1,180 @@
+"""Decode-loop drivers of the reference harness on the B200 engine:
+``run_simulation`` (harness.py:221-424), ``run_oracle`` (:175-186) and
+``fidelity`` (:189-206).
+
+Only the hot-path parts of the reference harness are here (SURVEY §8 rows
+R17, R18, R22); the CLI, config files and report formatting are out of scope.
+``run_simulation`` takes the reference's dotted configuration keys as a
+dict (defaults from config.py:64-111), builds the synthetic model, and
+replays the evaluation stream through ``DecodeEngine`` (fp32 parity mode with
+the reference's tanh experts), so its event log, counters and outputs are
+comparable one to one with the reference's SimResult.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import memtier, ops, substrate
+from .engine import DecodeEngine, EngineSpec, HostMirror
+from .errors import ConfigurationError
+
+DEFAULTS = {
+    "model.layers": 24, "model.experts": 64, "model.top_k": 6, "model.hidden_dim": 32, "model.ffn_dim": 64,
+    "model.seed": 7, "model.skew": 0.8, "model.clusters": 8, "model.cluster_spread": 0.1,
+    "stream.seed": 1, "stream.num_tokens": 10000, "stream.batch": 16, "cache.rate": 0.75, "cache.policy": "lru",
+    "cost.expert_load_ms": 9.5, "cost.hit_ms": 0.0, "cost.expert_compute_ms": 0.5,
+    "cost.pcie_bw_bytes_per_s": 4.0e6, "gate.temperature": 1.0, "gate.beta": 1.0, "gate.margin_gamma": None,
+    "sub.h": 16, "sub.rho": None, "sub.fallback": "prefetch_original", "prefetch.enabled": True,
+    "method": "buddy", "run.seed": 0, "fidelity.readout_classes": 16,
+}
+
+
+@dataclass
+class SimResult:
+    metrics: memtier.RunMetrics
+    outputs: np.ndarray
+    events: list
+    tau_by_layer: list
+    trace: list
+
+
+def _spec(c) -> substrate.ModelSpec:
+    return substrate.ModelSpec(num_layers=c["model.layers"], experts_per_layer=c["model.experts"],
+                               top_k=c["model.top_k"], hidden_dim=c["model.hidden_dim"], ffn_dim=c["model.ffn_dim"],
+                               seed=c["model.seed"], skew=c["model.skew"], num_clusters=c["model.clusters"],
+                               cluster_spread=c["model.cluster_spread"]).validate()
+
+
+def _tanh_arena(spec, layer):
+    w_in, w_out = substrate.layer_stack(spec, layer)
+    E = w_in.shape[0]
+    return np.concatenate([np.transpose(w_in, (0, 2, 1)).reshape(E, -1),
+                           np.transpose(w_out, (0, 2, 1)).reshape(E, -1)], axis=1).astype(np.float32)
+
+
+def run_oracle(spec: substrate.ModelSpec, x: np.ndarray, temperature: float = 1.0, batch: int = 256) -> np.ndarray:
+    """Full-residency forward (identity plans) through K1, K3-K5 (harness.py:175-186)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    gw, gb = substrate.gate_weights(spec)
+    gw = torch.tensor(gw, dtype=torch.float32, device=dev)
+    gb = torch.tensor(gb, dtype=torch.float32, device=dev)
+    arenas = [torch.tensor(_tanh_arena(spec, l), device=dev) for l in range(spec.num_layers)]
+    E, k, d, f = spec.experts_per_layer, spec.top_k, spec.hidden_dim, spec.ffn_dim
+    bufs = torch.arange(E, dtype=torch.int32, device=dev)
+    out = np.empty_like(x)
+    for b0 in range(0, x.shape[0], batch):
+        h = torch.tensor(x[b0:b0 + batch], dtype=torch.float32, device=dev)
+        for l in range(spec.num_layers):
+            r = ops.gate_topk(h, gw[l], gb[l], k, temperature)
+            kept = torch.zeros_like(r.topk, dtype=torch.uint8)
+            perm = ops.permute(r.topk, kept, E)
+            yp = ops.expert_ffn_f32(ops.gather_rows(h, perm, 0), perm, arenas[l], bufs, d, f, ops.ACT_TANH)
+            h = ops.combine(yp, perm, r.probs, kept, h_in=h)
+        out[b0:b0 + batch] = h.double().cpu().numpy()
+    return out
+
+
+def fidelity(outputs: np.ndarray, oracle: np.ndarray, readout: np.ndarray) -> tuple:
+    """(mean cosine, argmax agreement) on the GPU (harness.py:189-206);
+    bitwise-equal rows score exactly 1.0."""
+    if outputs.shape != oracle.shape:
+        raise ConfigurationError("fidelity shapes do not match")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    a = torch.tensor(outputs, dtype=torch.float64, device=dev)
+    b = torch.tensor(oracle, dtype=torch.float64, device=dev)
+    r = torch.tensor(readout, dtype=torch.float64, device=dev)
+    denom = torch.clamp(torch.linalg.norm(a, dim=1) * torch.linalg.norm(b, dim=1), min=1e-30)
+    cos = torch.clamp((a * b).sum(1) / denom, -1.0, 1.0)
+    cos = torch.where((a == b).all(1), torch.ones_like(cos), cos)
+    agree = ((a @ r.T).argmax(1) == (b @ r.T).argmax(1)).double().mean()
+    return float(cos.mean().item()), float(agree.item())
+
+
+def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=None) -> SimResult:
+    """The reference decode replay (harness.py:221-424) on the engine.
+    ``tables``: dense (ids[L,E,K] int32, lens[L,E] int32) or a list of
+    buddies.BuddyTable; ``tau_by_layer``: calibrated thresholds."""
+    c = dict(DEFAULTS)
+    c.update(cfg)
+    spec = _spec(c)
+    L, E = spec.num_layers, spec.experts_per_layer
+    method = c["method"]
+    if method not in ("buddy", "original"):
+        raise ConfigurationError(f"method {method!r} is not a hot-path method (buddy|original)")
+    cap = int(np.floor(c["cache.rate"] * E))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    mirrors = []
+    for l in range(L):
+        a = _tanh_arena(spec, l)
+        m = HostMirror(a.nbytes)
+        m.as_tensor(torch.float32).copy_(torch.from_numpy(a).view(-1))
+        mirrors.append(m)
+    gw, gb = substrate.gate_weights(spec)
+    ids = lens = None
+    if method == "buddy":
+        if tables is None or tau_by_layer is None:
+            raise ConfigurationError("buddy method needs one buddy table and one tau per layer")
+        table_objs = isinstance(tables, (list, tuple)) and hasattr(tables[0], "ids")
+        if table_objs:
+            K = max(max([len(t.ids(p)) for t in tables for p in range(E)]), 1)
+            ids_np = np.full((L, E, K), -1, np.int32)
+            lens_np = np.zeros((L, E), np.int32)
+            for l, t in enumerate(tables):
+                for p in range(E):
+                    n = len(t.ids(p))
+                    ids_np[l, p, :n] = t.ids(p)
+                    lens_np[l, p] = n
+        else:
+            ids_np, lens_np = tables
+        ids = torch.tensor(np.asarray(ids_np, np.int32), device=dev)
+        lens = torch.tensor(np.asarray(lens_np, np.int32), device=dev)
+        if table_objs and c["sub.h"] > tables[0].k_max:
+            raise ConfigurationError("sub.h exceeds the table's k_max")
+    taus = list(tau_by_layer) if method == "buddy" else [-1.0] * L
+    es = EngineSpec(num_layers=L, num_experts=E, top_k=spec.top_k, d=spec.hidden_dim, f=spec.ffn_dim,
+                    capacity=cap, max_batch=c["stream.batch"], act=ops.ACT_TANH, method=method,
+                    policy=c["cache.policy"], search_rank_h=c["sub.h"], rho=c["sub.rho"],
+                    fallback=0 if c["sub.fallback"] == "prefetch_original" else 1, beta=c["gate.beta"],
+                    temperature=c["gate.temperature"], gamma=c["gate.margin_gamma"], prefetch=c["prefetch.enabled"],
+                    fp32_weights=True, expert_bytes=2 * spec.hidden_dim * spec.ffn_dim * 8,
+                    load_ms=c["cost.expert_load_ms"], hit_ms=c["cost.hit_ms"], compute_ms=c["cost.expert_compute_ms"],
+                    pcie_bw_bytes_per_s=c["cost.pcie_bw_bytes_per_s"])
+    initial = [memtier.initial_residents(E, cap, c["cache.policy"], c["run.seed"], l) for l in range(L)]
+    eng = DecodeEngine(es, mirrors, torch.tensor(gw, dtype=torch.float32, device=dev),
+                       torch.tensor(gb, dtype=torch.float32, device=dev), ids, lens, taus, initial)
+    eng.set_trace(True)
+    n, B = c["stream.num_tokens"], c["stream.batch"]
+    x = substrate.token_stream(spec, c["stream.seed"], n)
+    h = torch.tensor(x, dtype=torch.float32, device=dev)
+    for b0 in range(0, n, B):
+        eng.step(h[b0:b0 + B], np.arange(b0, min(n, b0 + B)))
+    torch.cuda.synchronize()
+    eng.finish()
+    events = memtier.events_from_array(eng.sorted_events())
+    st = eng.stats()
+    waste = 0  # wasted prefetches (harness.py:400): evicted unused + still-unused residents
+    cache = N.lib().bm_engine_cache(eng._h)
+    sc = np.zeros(4, np.int64)
+    for l in range(L):
+        N.call("bm_cache_layer_state", cache, l, None, None, sc.ctypes.data)
+        waste += int(sc[2] + sc[3])
+    m = memtier.step_metrics(events, tokens=n, compute_ms=c["cost.expert_compute_ms"] * st["executed_slots"],
+                             waste_bytes=waste * es.expert_bytes)
+    m.substitutions = st["substitutions"]
+    m.gate_token_forbidden = st["gate_forbidden"]
+    m.gate_batch_bypassed = st["batch_bypassed"]
+    outputs = h.double().cpu().numpy()
+    if oracle_outputs is None:
+        oracle_outputs = run_oracle(spec, x, c["gate.temperature"], batch=B)
+    m.fidelity_cosine, m.fidelity_argmax = fidelity(outputs, oracle_outputs,
+                                                    substrate.readout_head(spec, c["fidelity.readout_classes"]))
+    trace = eng.trace()
+    eng.close()
+    for mm in mirrors:
+        mm.close()
+    return SimResult(metrics=m, outputs=outputs, events=events, tau_by_layer=taus, trace=trace)

@@ -75,6 +75,27 @@ def test_engine_event_log_equals_reference(cuda_ok, method):
     eng.close()
 
 
+@pytest.mark.parametrize("method", ["buddy", "original"])
+def test_run_simulation_metrics_equal_reference(cuda_ok, method):
+    """harness.run_simulation on the engine reproduces the reference SimResult
+    metrics (counters and simulated times exactly; fidelity within 1e-6)."""
+    from paper_2511_10054_b200 import harness
+    g = golden("sim_tiny.npz")
+    cfg = {"model.layers": 4, "model.experts": 8, "model.top_k": 2, "model.hidden_dim": 128,
+           "model.ffn_dim": 256, "model.clusters": 8, "stream.batch": 16, "cache.rate": 0.5, "sub.h": 7,
+           "sub.rho": 3, "stream.seed": 2, "stream.num_tokens": 320, "method": method}
+    tables = (np.stack([g[f"ids_L{l}"] for l in range(L)]), np.stack([g[f"lens_L{l}"] for l in range(L)]))
+    r = harness.run_simulation(cfg, tables=tables if method == "buddy" else None,
+                               tau_by_layer=list(g["taus"]) if method == "buddy" else None)
+    m = r.metrics
+    ref = g[f"{method}_metrics"]
+    got = np.array([m.tokens_per_s, m.stall_ms, m.compute_ms, m.hits, m.misses_ondemand, m.misses_substituted,
+                    m.drops, m.prefetch_issued, m.prefetch_completed, m.evictions, m.read_bytes, m.substitutions,
+                    m.gate_token_forbidden, m.gate_batch_bypassed])
+    assert np.array_equal(got, ref[:14]), (got, ref[:14])
+    assert abs(m.fidelity_cosine - ref[14]) <= 1e-6 and abs(m.fidelity_argmax - ref[15]) <= 1e-9
+
+
 def test_engine_bf16_tensor_core_mode_same_decisions(cuda_ok):
     """The bf16 tcgen05 path makes the same cache decisions on this workload
     (routing is robust to bf16 expert outputs here) and stays within the bf16
