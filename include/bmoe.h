@@ -112,6 +112,12 @@ int bm_permute(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t 
                int32_t *expert_count, int32_t *expert_offset, int32_t *row_token, int32_t *slot_row,
                bm_stream_t stream);
 
+/* Extend a plan [B][k] with S always-executed shared experts E..E+S-1 (kind
+ * kept, weight 1): outputs [B][k+S] (DeepSeek-V2-style shared experts). */
+int bm_append_shared(const int32_t *executed, const uint8_t *kind, const float *probs, int64_t B, int64_t k,
+                     int64_t E, int64_t S, int32_t *executed_ext, uint8_t *kind_ext, float *probs_ext,
+                     bm_stream_t stream);
+
 /* Gather token rows into the permuted activation buffer (128-bit loads).
  * layout 0: plain row-major fp32 x_perm[r_max][d].
  * layout 1: bf16 "UMMA K-major SW128" planes: x_perm[d/64][r_max][64] with
@@ -291,6 +297,9 @@ typedef struct {
     double beta, temperature, gamma; /* gamma < 0: margin gate off */
     double load_ms, hit_ms, compute_ms, prefetch_ms; /* control-plane cost model (memtier.py:39-58) */
     int64_t expert_bytes;                            /* reported per miss (CostModel.expert_bytes) */
+    int32_t num_shared; /* always-resident shared experts per layer (DeepSeek-V2-style), outside the budget:
+                           host_mirror[l] then holds num_experts + num_shared buffers, the shared ones are
+                           uploaded once and added to every token with weight 1 */
 } bm_engine_config;
 
 typedef struct {

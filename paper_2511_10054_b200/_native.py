@@ -34,7 +34,7 @@ class EngineConfig(C.Structure):
                 ("n_tile", C.c_int32), ("fp32_weights", C.c_int32), ("rho", C.c_int64), ("beta", C.c_double),
                 ("temperature", C.c_double), ("gamma", C.c_double), ("load_ms", C.c_double),
                 ("hit_ms", C.c_double), ("compute_ms", C.c_double), ("prefetch_ms", C.c_double),
-                ("expert_bytes", C.c_int64)]
+                ("expert_bytes", C.c_int64), ("num_shared", C.c_int32)]
 
 
 class EngineStats(C.Structure):
@@ -69,6 +69,7 @@ _SIGS = {
     "bm_buddy_remap": (C.c_int, [P, P, P, I32, I64, I64, I64, P, P, P, P, I64, I64, I64, I32, I32, F64, F64, F64,
                                  I32, P, F64, P, P, P, P, P, P]),
     "bm_permute_rows_max": (I64, [I64, I64, I64, I64]),
+    "bm_append_shared": (C.c_int, [P, P, P, I64, I64, I64, I64, P, P, P, P]),
     "bm_permute": (C.c_int, [P, P, I64, I64, I64, I64, P, P, P, P, P]),
     "bm_gather_rows": (C.c_int, [P, I64, I64, P, P, I64, I64, I32, P, P]),
     "bm_combine": (C.c_int, [P, P, P, P, I64, I64, I64, P, F32, P, P]),

@@ -67,6 +67,12 @@ struct bm_engine {
     uint32_t *bitmap_dev[2] = {nullptr, nullptr};
     int32_t *buf_of_dev[2] = {nullptr, nullptr};
     int32_t *count = nullptr, *offset = nullptr, *row_token = nullptr, *slot_row = nullptr;
+    // shared experts (always resident, outside the budget): plan extended to k + Ssh slots
+    int Ssh = 0;
+    int32_t *exec_ext = nullptr;
+    uint8_t *kind_ext = nullptr;
+    float *probs_ext = nullptr;
+    std::vector<int> shared_buf;  // [L][Ssh] buffer ids
     void *x_perm = nullptr, *ffn_ws = nullptr;
     int64_t ffn_ws_bytes = 0, r_max = 0, device_bytes = 0;
     // pinned staging
@@ -233,26 +239,40 @@ struct bm_engine {
             stall_ev.emplace_back(a, bb);
         }
         for (int e = 0; e < E; ++e) buf_of_host[par][e] = phys[l][e] >= 0 ? phys[l][e] : 0;
-        ENG_CUDA(cudaMemcpyAsync(buf_of_dev[par], buf_of_host[par], E * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        for (int sx = 0; sx < Ssh; ++sx) buf_of_host[par][E + sx] = shared_buf[(size_t)l * Ssh + sx];
+        const int Et = E + Ssh, kt = k + Ssh;
+        ENG_CUDA(cudaMemcpyAsync(buf_of_dev[par], buf_of_host[par], Et * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        stats.ffn_experts += Ssh;
+        stats.ffn_rows += (int64_t)B * Ssh;
         // 8. K3 permute -> K4 grouped FFN -> K5 combine + layer_update (in place)
-        ENG_TRY(bm_permute(executed, kind, B, k, E, 16, count, offset, row_token, slot_row, s));
+        const int32_t *pe = executed;
+        const uint8_t *pk = kind;
+        const float *pp = probs;
+        if (Ssh) {  // every token also runs the shared experts with weight 1
+            ENG_TRY(bm_append_shared(executed, kind, probs, B, k, E, Ssh, exec_ext, kind_ext, probs_ext, s));
+            pe = exec_ext;
+            pk = kind_ext;
+            pp = probs_ext;
+        }
+        ENG_TRY(bm_permute(pe, pk, B, kt, Et, 16, count, offset, row_token, slot_row, s));
         if (cfg.fp32_weights) {
-            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, E, r_max, 0, x_perm, s));
-            ENG_TRY(bm_expert_ffn_f32(static_cast<float *>(x_perm), count, offset, E, d, f, cfg.act,
+            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 0, x_perm, s));
+            ENG_TRY(bm_expert_ffn_f32(static_cast<float *>(x_perm), count, offset, Et, d, f, cfg.act,
                                       reinterpret_cast<const float *>(arena), buf_elems, buf_of_dev[par], r_max,
                                       h_ws, y_perm, s));
         } else {
-            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, E, r_max, 1, x_perm, s));
+            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 1, x_perm, s));
             // the host already knows every expert's row count: size the GEMM's
             // token tile to it (smaller B stages -> deeper pipeline, more chains)
             int maxc = 0;
             for (int e = 0; e < E; ++e) maxc = std::max(maxc, (int)cnt[e]);
+            if (Ssh) maxc = std::max(maxc, (int)B);
             int nt = std::min(cfg.n_tile, std::max(16, (maxc + 15) / 16 * 16));
             if (getenv("BMOE_NTILE_FIXED")) nt = cfg.n_tile;
-            ENG_TRY(bm_expert_ffn_bf16(x_perm, count, offset, E, d, f, cfg.act, arena, nbufs, buf_of_dev[par],
+            ENG_TRY(bm_expert_ffn_bf16(x_perm, count, offset, Et, d, f, cfg.act, arena, nbufs, buf_of_dev[par],
                                        r_max, nt, ffn_ws, ffn_ws_bytes, y_perm, s));
         }
-        ENG_TRY(bm_combine(y_perm, slot_row, probs, kind, B, k, d, h, 0.5f, h, s));
+        ENG_TRY(bm_combine(y_perm, slot_row, pp, pk, B, kt, d, h, 0.5f, h, s));
         // 9. release buffers of experts the control plane no longer holds
         ENG_CUDA(cudaEventRecord(layer_done[l], s));
         ENG_TRY(bm_cache_snapshot(cache, l, mask_tmp.data(), nullptr));
@@ -279,7 +299,8 @@ struct bm_engine {
             cudaEventDestroy(p.first);
             cudaEventDestroy(p.second);
         }
-        void *dptrs[] = {logits, probs, y_perm, h_ws, tae, margin, delta, topk, executed, used, kind, allowed,
+        void *dptrs[] = {exec_ext, kind_ext, probs_ext, logits, probs, y_perm, h_ws, tae, margin, delta, topk,
+                         executed, used, kind, allowed,
                          batch_ok, bitmap_dev[0], bitmap_dev[1], buf_of_dev[0], buf_of_dev[1], count, offset,
                          row_token, slot_row, x_perm, ffn_ws};
         for (void *p : dptrs)
@@ -307,7 +328,8 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     g->cap = c->capacity;
     g->K = tbl_k;
     const int L = g->L, E = g->E, k = g->k;
-    if (L < 1 || E < 1 || E > 256 || k < 1 || k > E || c->max_batch < 1 || g->cap < 0 || g->cap > E) {
+    if (L < 1 || E < 1 || E + (c->num_shared > 0 ? c->num_shared : 0) > 256 || k < 1 || k > E ||
+        c->max_batch < 1 || g->cap < 0 || g->cap > E) {
         bm::set_error("engine: bad configuration");
         return BM_ECONFIG;
     }
@@ -323,7 +345,8 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
         bm::set_error("engine: staging (%d) below the on-demand reserve (%d)", g->S, g->reserve);
         return BM_ECONFIG;
     }
-    g->nbufs = L * g->cap + g->S;
+    g->Ssh = c->num_shared > 0 ? c->num_shared : 0;
+    g->nbufs = L * (g->cap + g->Ssh) + g->S;
     g->host_mirror.resize(L);
     for (int l = 0; l < L; ++l) g->host_mirror[l] = static_cast<const uint8_t *>(host_mirror[l]);
     g->gate_w = gate_w;
@@ -366,9 +389,20 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
             g->phys[l][e] = b;
         }
     }
+    // shared experts: permanent buffers, outside the budget
+    g->shared_buf.assign((size_t)L * g->Ssh, -1);
+    for (int l = 0; l < L; ++l)
+        for (int sx = 0; sx < g->Ssh; ++sx) {
+            int b;
+            ENG_TRY(g->alloc_buffer(&b));
+            ENG_CUDA(cudaMemcpy(g->bufs[b].dev, g->host_mirror[l] + (size_t)(E + sx) * g->buf_bytes, g->buf_bytes,
+                                cudaMemcpyHostToDevice));
+            g->shared_buf[(size_t)l * g->Ssh + sx] = b;
+        }
     // workspaces
     const int64_t Bm = c->max_batch;
-    g->r_max = bm_permute_rows_max(Bm, k, E, 16);
+    const int Et = E + g->Ssh, kt = k + g->Ssh;
+    g->r_max = bm_permute_rows_max(Bm, kt, Et, 16);
     g->r_max = (g->r_max + 15) / 16 * 16;
     ENG_TRY(g->dmalloc(&g->logits, Bm * E));
     ENG_TRY(g->dmalloc(&g->probs, Bm * k));
@@ -383,14 +417,19 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     ENG_TRY(g->dmalloc(&g->batch_ok, 1));
     for (int i = 0; i < 2; ++i) {
         ENG_TRY(g->dmalloc(&g->bitmap_dev[i], (E + 31) / 32));
-        ENG_TRY(g->dmalloc(&g->buf_of_dev[i], E));
+        ENG_TRY(g->dmalloc(&g->buf_of_dev[i], Et));
         ENG_TRY(g->hmalloc(&g->bitmap_host[i], (E + 31) / 32));
-        ENG_TRY(g->hmalloc(&g->buf_of_host[i], E));
+        ENG_TRY(g->hmalloc(&g->buf_of_host[i], Et));
     }
-    ENG_TRY(g->dmalloc(&g->count, E));
-    ENG_TRY(g->dmalloc(&g->offset, E + 1));
+    ENG_TRY(g->dmalloc(&g->count, Et));
+    ENG_TRY(g->dmalloc(&g->offset, Et + 1));
     ENG_TRY(g->dmalloc(&g->row_token, g->r_max + 16));
-    ENG_TRY(g->dmalloc(&g->slot_row, Bm * k));
+    ENG_TRY(g->dmalloc(&g->slot_row, Bm * kt));
+    if (g->Ssh) {
+        ENG_TRY(g->dmalloc(&g->exec_ext, Bm * kt));
+        ENG_TRY(g->dmalloc(&g->kind_ext, Bm * kt));
+        ENG_TRY(g->dmalloc(&g->probs_ext, Bm * kt));
+    }
     ENG_TRY(g->dmalloc(&g->y_perm, (size_t)g->r_max * g->d));
     if (c->fp32_weights) {
         ENG_TRY(g->dmalloc(reinterpret_cast<float **>(&g->x_perm), (size_t)g->r_max * g->d));
@@ -398,7 +437,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     } else {
         ENG_TRY(g->dmalloc(reinterpret_cast<uint16_t **>(&g->x_perm), (size_t)g->r_max * g->d));
         ENG_CUDA(cudaMemset(g->x_perm, 0, (size_t)g->r_max * g->d * 2));
-        g->ffn_ws_bytes = bm_expert_ffn_bf16_workspace(E, g->d, g->f, g->r_max, c->n_tile);
+        g->ffn_ws_bytes = bm_expert_ffn_bf16_workspace(Et, g->d, g->f, g->r_max, c->n_tile);
         ENG_TRY(g->dmalloc(reinterpret_cast<uint8_t **>(&g->ffn_ws), (size_t)g->ffn_ws_bytes));
     }
     ENG_TRY(g->hmalloc(&g->topk_h, Bm * k));

@@ -167,10 +167,40 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const float *_
     for (int i = threadIdx.x; i < d; i += blockDim.x) out[(size_t)b * d + i] = hbuf[i] * inv;
 }
 
+__global__ void append_shared_kernel(const int32_t *__restrict__ ex, const uint8_t *__restrict__ kd,
+                                     const float *__restrict__ pr, int B, int k, int E, int S, int32_t *ex2,
+                                     uint8_t *kd2, float *pr2) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const int kt = k + S;
+    for (int s = 0; s < k; ++s) {
+        ex2[b * kt + s] = ex[b * k + s];
+        kd2[b * kt + s] = kd[b * k + s];
+        pr2[b * kt + s] = pr[b * k + s];
+    }
+    for (int s = 0; s < S; ++s) {
+        ex2[b * kt + k + s] = E + s;
+        kd2[b * kt + k + s] = BM_KIND_KEPT;
+        pr2[b * kt + k + s] = 1.0f;
+    }
+}
+
 }  // namespace
 }  // namespace bm
 
 using namespace bm;
+
+extern "C" int bm_append_shared(const int32_t *executed, const uint8_t *kind, const float *probs, int64_t B, int64_t k,
+                                int64_t E, int64_t S, int32_t *executed_ext, uint8_t *kind_ext, float *probs_ext,
+                                bm_stream_t stream) {
+    BM_REQUIRE(executed && kind && probs && executed_ext && kind_ext && probs_ext && B >= 0 && S >= 0, BM_EINVAL,
+               "bm_append_shared: bad args");
+    if (B == 0) return BM_OK;
+    append_shared_kernel<<<(unsigned)((B + 127) / 128), 128, 0, as_stream(stream)>>>(
+        executed, kind, probs, (int)B, (int)k, (int)E, (int)S, executed_ext, kind_ext, probs_ext);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
 
 extern "C" int64_t bm_permute_rows_max(int64_t B, int64_t k, int64_t E, int64_t row_align) {
     int64_t n = B * k;

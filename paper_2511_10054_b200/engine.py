@@ -85,6 +85,7 @@ class EngineSpec:
     prefetch_ms: float | None = None
     pcie_bw_bytes_per_s: float = 4.0e6
     expert_bytes: int | None = None
+    num_shared: int = 0
 
     @property
     def buf_elems(self) -> int:
@@ -123,6 +124,7 @@ class DecodeEngine:
         cfg.prefetch_ms = spec.prefetch_ms if spec.prefetch_ms is not None else \
             1000.0 * ebytes / spec.pcie_bw_bytes_per_s
         cfg.expert_bytes = ebytes
+        cfg.num_shared = int(spec.num_shared)
         L, E = spec.num_layers, spec.num_experts
         ptrs = (C.c_void_p * L)(*[m.ptr for m in mirrors])
         tau = (C.c_double * L)(*[(-1.0 if t is None else float(t)) for t in taus])

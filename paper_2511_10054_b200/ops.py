@@ -181,6 +181,19 @@ def permute(executed, kind, num_experts: int, align: int = ROW_ALIGN) -> Permuta
     return p
 
 
+def append_shared(executed, kind, probs, num_experts: int, num_shared: int):
+    """Plan [B,k] -> [B,k+S] with shared experts E..E+S-1 (kept, weight 1)."""
+    B, k = executed.shape
+    kt = k + num_shared
+    dev = executed.device
+    ex = torch.empty(B, kt, device=dev, dtype=torch.int32)
+    kd = torch.empty(B, kt, device=dev, dtype=torch.uint8)
+    pr = torch.empty(B, kt, device=dev, dtype=torch.float32)
+    N.call("bm_append_shared", _p(executed), _p(kind), _p(probs), B, k, num_experts, num_shared, _p(ex), _p(kd),
+           _p(pr), _s())
+    return ex, kd, pr
+
+
 def gather_rows(x, perm: Permutation, layout: int = 0):
     """Permuted activations: layout 0 fp32 [r_max,d]; layout 1 bf16 SW128 planes."""
     _cuda(x, "x", torch.float32)

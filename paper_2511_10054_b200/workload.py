@@ -32,6 +32,7 @@ SHAPES = {
     "dsv2lite": (64, 6, 2048, 1408, 0.5),
     "tiny": (8, 2, 128, 256, 0.5),
 }
+SHARED = {"dsv2lite": 2}  # always-resident shared experts (outside the cache budget)
 
 
 def initial_residents(num_experts: int, capacity: int, seed: int, layer: int):
@@ -101,6 +102,7 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
           log=None) -> Workload:
     import time
     E, k, d, f, rate = SHAPES[name]
+    S = SHARED.get(name, 0)
     cap = int(math.floor(rate * E))
     k_max = k_max if k_max is not None else min(16, E - 1)
     spec = substrate.ModelSpec(num_layers=layers, experts_per_layer=E, top_k=k, hidden_dim=d, ffn_dim=f,
@@ -113,7 +115,7 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     t0 = time.time()
     mirrors = []
     gen = torch.Generator(device=device)
-    arena = torch.empty(E, buf_elems, device=device, dtype=torch.bfloat16)
+    arena = torch.empty(E + S, buf_elems, device=device, dtype=torch.bfloat16)
     ids_all = torch.full((layers, E, k_max), -1, device=device, dtype=torch.int32)
     len_all = torch.zeros(layers, E, device=device, dtype=torch.int32)
     taus = []
@@ -123,11 +125,11 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     mean_len = []
     for l in range(layers):
         gen.manual_seed(seed * 100003 + l)
-        for e in range(E):  # row-major N(0, 1/fan_in), then the UMMA-tiled HBM layout
+        for e in range(E + S):  # row-major N(0, 1/fan_in), then the UMMA-tiled HBM layout
             w = _gen_expert(gen, d, f, device)
             ops.pack_expert_bf16(w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d), w[2 * f * d:].view(d, f),
                                  ops.ACT_SWIGLU, arena[e])
-        m = HostMirror(E * buf_bytes)
+        m = HostMirror((E + S) * buf_bytes)
         fill_mirror_from_device(m, arena)
         mirrors.append(m)
         # ---- profile this layer (full residency) ----
@@ -142,13 +144,16 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
         idx = max(1, math.ceil(tau_percentile * s.numel() / 100.0)) - 1
         taus.append(float(s[min(idx, s.numel() - 1)]))
         kept = torch.zeros_like(r.topk, dtype=torch.uint8)  # identity plan: full residency
-        perm = ops.permute(r.topk, kept, E)
+        ex, kd, pr = r.topk, kept, r.probs
+        if S:
+            ex, kd, pr = ops.append_shared(ex, kd, pr, E, S)
+        perm = ops.permute(ex, kd, E + S)
         if ws is None or ws.r_max < perm.r_max:
-            ws = ops.FfnWorkspace(E, d, f, perm.r_max, 256, device)
+            ws = ops.FfnWorkspace(E + S, d, f, perm.r_max, 256, device)
         xp = ops.gather_rows(x, perm, 1)
-        yp = ops.expert_ffn_bf16(xp, perm, arena, torch.arange(E, device=device, dtype=torch.int32), d, f,
+        yp = ops.expert_ffn_bf16(xp, perm, arena, torch.arange(E + S, device=device, dtype=torch.int32), d, f,
                                  ops.ACT_SWIGLU, ws)
-        x = ops.combine(yp, perm, r.probs, kept, h_in=x)
+        x = ops.combine(yp, perm, pr, kd, h_in=x)
         if log:
             log(f"layer {l}: mirror {buf_bytes * E / 2**30:.2f} GiB, tau {taus[-1]:.4f}, "
                 f"mean buddies {mean_len[-1]:.2f}, {time.time() - t0:.1f}s")
@@ -156,6 +161,7 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     del arena, ws
     initial = [initial_residents(E, cap, 0, l) for l in range(layers)]
     es = EngineSpec(num_layers=layers, num_experts=E, top_k=k, d=d, f=f, capacity=cap, max_batch=max_batch,
-                    act=ops.ACT_SWIGLU, search_rank_h=k_max, rho=rho, n_tile=n_tile, expert_bytes=buf_bytes)
+                    act=ops.ACT_SWIGLU, search_rank_h=k_max, rho=rho, n_tile=n_tile, expert_bytes=buf_bytes,
+                    num_shared=S)
     return Workload(name, spec, es, mirrors, gate_w, gate_b, ids_all, len_all, taus, initial,
                     profile_seconds=time.time() - t0, mean_buddies=float(np.mean(mean_len)))

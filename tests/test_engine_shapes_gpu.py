@@ -65,6 +65,50 @@ def _oracle_replay(wl, trace, B, n_steps, L):
     return np.array(log, np.float64).reshape(-1, 7)
 
 
+def test_dsv2_shared_experts_numerics(cuda_ok):
+    """DeepSeek-V2-Lite shape: 64 routed (top-6) + 2 always-resident shared
+    experts. One layer-step of the bf16 engine vs an fp32 torch reference that
+    applies the engine's own plan plus both shared experts with weight 1,
+    then layer_update: rel 2e-2 per token."""
+    wl = W.build("dsv2lite", layers=1, max_batch=8, profile_tokens=512)
+    E, S, d, f = 64, 2, 2048, 1408
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(0)  # workload seed 0, layer 0: regenerate the row-major weights
+    experts = [W._gen_expert(gen, d, f, "cuda").float() for _ in range(E + S)]
+    eng = wl.engine("buddy")
+    eng.set_trace(True)
+    x = torch.from_numpy(wl.tokens(2, 8)).cuda()
+    h0 = x.clone()
+    eng.step(x, np.arange(8))
+    torch.cuda.synchronize()
+    rec = eng.trace()[0]
+    from paper_2511_10054_b200 import ops
+    r = ops.gate_topk(h0, wl.gate_w[0], wl.gate_b[0], 6)
+    probs = r.probs.cpu().numpy()
+    assert np.array_equal(r.topk.cpu().numpy(), rec["topk"])
+    xb = h0.to(torch.bfloat16).float()
+
+    def ffn(e, v):
+        w = experts[e]
+        W1, W3, W2 = w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d), w[2 * f * d:].view(d, f)
+        hh = torch.nn.functional.silu(v @ W1.T) * (v @ W3.T)
+        return hh.to(torch.bfloat16).float() @ W2.T
+
+    y = torch.zeros_like(h0)
+    for b in range(8):
+        for s in range(6):
+            if rec["kind"][b, s] != 3:
+                y[b] += float(probs[b, s]) * ffn(int(rec["executed"][b, s]), xb[b:b + 1])[0]
+        for sx in range(S):
+            y[b] += ffn(E + sx, xb[b:b + 1])[0]
+    ref = h0 + 0.5 * y
+    ref = ref / ref.pow(2).mean(1, keepdim=True).sqrt()
+    rel = (torch.linalg.norm(x - ref, dim=1) / torch.linalg.norm(ref, dim=1)).max().item()
+    assert rel <= 2e-2, rel
+    eng.close()
+    wl.close()
+
+
 @pytest.mark.parametrize("name,layers,B", [("mixtral", 2, 16), ("qwen3", 3, 16), ("dsv2lite", 3, 8)])
 def test_engine_decisions_bit_exact_at_baseline_shapes(cuda_ok, name, layers, B):
     wl = W.build(name, layers=layers, max_batch=B, profile_tokens=2048)
