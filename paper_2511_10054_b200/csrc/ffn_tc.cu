@@ -62,6 +62,11 @@ struct GemmParams {
     long long b_plane_bytes;
     float *partials;          // slot (tile + cta): nmat * n_tile * 128 floats
     int num_ctas;             // launched grid (persistent)
+    int mode;                 // epilogue: 0 SwiGLU -> H, 1 tanh -> H, 2 plain -> y_perm
+    int fuse;                 // finish wholly-owned tiles in the GEMM epilogue (decode-width tiles)
+    uint8_t *h_planes;        // GEMM1 output: bf16 SW128 planes [M/64][h_rmax][64]
+    int h_rmax;
+    float *y_perm;            // GEMM2 output: fp32 [r_max][M]
 };
 
 __device__ void build_sched(Sched &s, const int32_t *count, int E, int n_tile, int mtiles) {
@@ -253,20 +258,62 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         while (it < it1) {
             const int tile = (int)(it / steps_per_tile);
             const long long tile_end = (long long)(tile + 1) * steps_per_tile;
+            // this CTA owns the whole tile: finish it here (activation / output),
+            // otherwise park an fp32 partial for the deterministic fixup
+            const bool whole = p.fuse && it == (long long)tile * steps_per_tile && tile_end <= it1;
             it = min(tile_end, it1);
             const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             ptx::tc_fence_after();
-            const long long slot = (long long)tile + cta;
-            float *dst = p.partials + slot * (long long)NMAT * p.n_tile * kBM;
             const uint32_t tbase = tmem_base + (uint32_t)acc * acc_cols + ((uint32_t)(q * 32) << 16);
-#pragma unroll
-            for (int m = 0; m < NMAT; ++m) {
+            if (whole) {
+                const int m = ti.mtile * kBM + m_local;
                 for (int c0 = 0; c0 < ti.n; c0 += 16) {
-                    float v[16];
-                    ptx::tmem_ld16(tbase + (uint32_t)(m * p.n_tile + c0), v);
+                    float g[16];
+                    ptx::tmem_ld16(tbase + (uint32_t)c0, g);
+                    if (p.mode == 2) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) dst[((long long)m * p.n_tile + c0 + j) * kBM + m_local] = v[j];
+                        for (int j = 0; j < 16; ++j) p.y_perm[(long long)(ti.row0 + c0 + j) * p.M + m] = g[j];
+                    } else {
+                        float u[16];
+                        if (NMAT == 2) ptx::tmem_ld16(tbase + (uint32_t)(p.n_tile + c0), u);
+                        // lanes hold consecutive m: pack pairs to bf16x2, gather 8 m's
+                        // (16 bytes, one swizzle chunk) per lane group, one 128-bit store
+                        const int mg = ti.mtile * kBM + q * 32 + ((int)lane & ~7);  // group's first m
+                        const int plane = mg >> 6, chunk = (mg & 63) >> 3;
+                        const int gbase = (int)lane & ~7;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float hv = NMAT == 2 ? (g[j] / (1.0f + expf(-g[j]))) * u[j] : tanhf(g[j]);
+                            const float ov = __shfl_xor_sync(0xffffffffu, hv, 1);
+                            const __nv_bfloat162 pr2 = (lane & 1) ? __floats2bfloat162_rn(ov, hv)
+                                                                  : __floats2bfloat162_rn(hv, ov);
+                            const uint32_t w = *reinterpret_cast<const uint32_t *>(&pr2);
+                            uint4 v4;
+                            v4.x = __shfl_sync(0xffffffffu, w, gbase + 0);
+                            v4.y = __shfl_sync(0xffffffffu, w, gbase + 2);
+                            v4.z = __shfl_sync(0xffffffffu, w, gbase + 4);
+                            v4.w = __shfl_sync(0xffffffffu, w, gbase + 6);
+                            if (((int)lane & 7) == (j & 7)) {
+                                const int row = ti.row0 + c0 + j;
+                                uint4 *dstp = reinterpret_cast<uint4 *>(p.h_planes) +
+                                              (((long long)plane * p.h_rmax + row) * 8 + (chunk ^ (row & 7)));
+                                *dstp = v4;
+                            }
+                        }
+                    }
+                }
+            } else {
+                const long long slot = (long long)tile + cta;
+                float *dst = p.partials + slot * (long long)NMAT * p.n_tile * kBM;
+#pragma unroll
+                for (int m = 0; m < NMAT; ++m) {
+                    for (int c0 = 0; c0 < ti.n; c0 += 16) {
+                        float v[16];
+                        ptx::tmem_ld16(tbase + (uint32_t)(m * p.n_tile + c0), v);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) dst[((long long)m * p.n_tile + c0 + j) * kBM + m_local] = v[j];
+                    }
                 }
             }
             ptx::tc_fence_before();
@@ -309,6 +356,7 @@ __global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, 
         const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
         const int c0 = cta_of((long long)tile * steps_per_tile, T, G);
         const int c1 = cta_of((long long)(tile + 1) * steps_per_tile - 1, T, G);
+        if (p.fuse && c0 == c1) continue;  // one CTA owned it: its epilogue already wrote the result
         const long long slot_elems = (long long)p.nmat * p.n_tile * kBM;
         const int m = ti.mtile * kBM + m_local;
         for (int n = 0; n < ti.n; ++n) {
@@ -442,12 +490,17 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
     const int G = sm_count();
     const uint8_t *arena = static_cast<const uint8_t *>(w_arena);
     const int nmat1 = act == BM_ACT_SWIGLU ? 2 : 1;
+    // Fused epilogues pay off for decode-width tiles (they remove most fixup
+    // work); for wide prefill tiles the accumulator is single-buffered and the
+    // MMA would wait on the longer epilogue, so partials + fixup are faster.
+    int fuse = n_tile <= 64 ? 1 : 0;
+    if (const char *ev = getenv("BMOE_FUSE")) fuse = atoi(ev);
     GemmParams g1{expert_count, expert_offset, buf_of_expert, (int)E, (int)f, (int)d, nmat1, (int)n_tile,
                   kps_for(nmat1, d, n_tile), arena, buf_bytes, 0, static_cast<const uint8_t *>(x_perm),
-                  r_max * 128, partials, G};
+                  r_max * 128, partials, G, act == BM_ACT_SWIGLU ? 0 : 1, fuse, h_planes, (int)r_max, nullptr};
     GemmParams g2{expert_count, expert_offset, buf_of_expert, (int)E, (int)d, (int)f, 1, (int)n_tile,
                   kps_for(1, f, n_tile), arena, buf_bytes, (long long)nmat1 * f * d * 2, h_planes, r_max * 128,
-                  partials, G};
+                  partials, G, 2, fuse, nullptr, 0, y_perm};
 
     const bool timing = g_timing.enabled;
     std::lock_guard<std::mutex> lk(g_timing.mu);

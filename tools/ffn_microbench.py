@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--E", type=int, default=8)
     ap.add_argument("--n-tile", type=int, default=16)
     ap.add_argument("--copies", type=int, default=4)
+    ap.add_argument("--k", type=int, default=2, help="slots per token (top-k)")
     args = ap.parse_args()
     E, d, f, B, A = args.E, args.d, args.f, args.tokens, args.experts_active
     dev = "cuda"
@@ -49,7 +50,7 @@ def main():
                                  ops.ACT_SWIGLU, ar[e])
         arenas.append(ar)
     rng = np.random.default_rng(0)
-    topk = np.stack([rng.choice(A, 2, replace=False) for _ in range(B)]).astype(np.int32)
+    topk = np.stack([rng.choice(A, args.k, replace=False) for _ in range(B)]).astype(np.int32)
     kind = np.zeros_like(topk, dtype=np.uint8)
     perm = ops.permute(torch.from_numpy(topk).to(dev), torch.from_numpy(kind).to(dev), E)
     x = torch.randn(B, d, device=dev)
@@ -67,13 +68,15 @@ def main():
     N.lib().bm_set_kernel_timing(0)
     g1, g2 = float(np.median(buf[0:n:2])), float(np.median(buf[1:n:2]))
     n_exp = int((perm.count > 0).sum())
-    b1 = n_exp * 2 * d * f * 2 + B * 2 * d * 2
-    b2 = n_exp * d * f * 2 + B * 2 * f * 2
+    b1 = n_exp * 2 * d * f * 2 + B * args.k * d * 2
+    b2 = n_exp * d * f * 2 + B * args.k * f * 2
+    flops1, flops2 = 2.0 * B * args.k * d * f * 2, 2.0 * B * args.k * d * f  # 6*d*f per (token, slot)
     try:
         peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
         peak = 6650.0
-    out = {"experts": n_exp, "tokens": B, "n_tile": args.n_tile, "gemm1_ms": g1, "gemm2_ms": g2,
+    out = {"experts": n_exp, "tokens": B, "k": args.k, "n_tile": args.n_tile, "gemm1_ms": g1, "gemm2_ms": g2,
+           "tflops_pair": (flops1 + flops2) / (g1 + g2) / 1e9,
            "gemm1_gbs": b1 / g1 / 1e6, "gemm2_gbs": b2 / g2 / 1e6, "pair_gbs": (b1 + b2) / (g1 + g2) / 1e6,
            "peak_gbs": peak, "gemm1_frac": b1 / g1 / 1e6 / peak, "gemm2_frac": b2 / g2 / 1e6 / peak,
            "env": {k: v for k, v in os.environ.items() if k.startswith("BMOE_")}}
