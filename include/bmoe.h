@@ -178,6 +178,7 @@ int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const in
  * call (GEMM1 ms, GEMM2 ms), returning the count written (-1 on error).
  * bm_set_kernel_timing() clears the record. */
 int bm_set_kernel_timing(int32_t enable);
+int bm_kernel_timing_enabled(void);
 int64_t bm_kernel_times(float *out_host, int64_t cap);
 
 /* ------------------------------------- K6/K7 co-activation and buddy ranking

@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <vector>
 
 #include "../../include/bmoe.h"
@@ -83,7 +84,16 @@ struct bm_engine {
     cudaEvent_t plan_ev = nullptr;
     cudaStream_t copy_stream = nullptr, prefetch_stream = nullptr;
     std::vector<std::vector<int32_t>> prev_counts;  // [L][E]
-    int parity = 0;
+    // packed plan readback, per-layer staging (graph-stable addresses), graphs
+    uint8_t *plan_dev = nullptr, *plan_host = nullptr;
+    float *h_int = nullptr;                       // engine-owned hidden state [max_batch][d]
+    uint32_t *bm_dev_all = nullptr, *bm_host_all = nullptr;
+    int32_t *bo_dev_all = nullptr, *bo_host_all = nullptr;
+    std::vector<uint32_t *> bm_dev_l, bm_host_l;  // per-layer residency bitmaps
+    std::vector<int32_t *> bo_dev_l, bo_host_l;   // per-layer buffer maps (E + shared)
+    cudaStream_t cap_stream = nullptr;
+    bool use_graphs = true;
+    std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> g_pre, g_post;
     bm_engine_stats stats{};
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev;
     std::vector<uint8_t> mask_tmp;
@@ -140,9 +150,90 @@ struct bm_engine {
         return BM_OK;
     }
 
+    // plan pack [topk | executed | kind | allowed | batch_ok] for batch B (device + pinned host)
+    void carve(int64_t B) {
+        topk = reinterpret_cast<int32_t *>(plan_dev);
+        executed = topk + B * k;
+        kind = reinterpret_cast<uint8_t *>(executed + B * k);
+        allowed = kind + B * k;
+        batch_ok = allowed + B;
+        topk_h = reinterpret_cast<int32_t *>(plan_host);
+        exec_h = topk_h + B * k;
+        kind_h = reinterpret_cast<uint8_t *>(exec_h + B * k);
+        allowed_h = kind_h + B * k;
+        batch_ok_h = allowed_h + B;
+    }
+    static size_t plan_bytes(int64_t B, int k) { return (size_t)B * k * 9 + (size_t)B + 1; }
+
+    // K1 gate, snapshot upload, K2 remap, packed plan readback
+    int enqueue_pre(int l, float *h, int64_t B, cudaStream_t s) {
+        const int words = (E + 31) / 32;
+        ENG_TRY(bm_gate_topk(h, gate_w + (size_t)l * E * d, gate_b + (size_t)l * E, B, E, d, k, cfg.temperature,
+                             tau[l], cfg.gamma, logits, topk, probs, tae, margin, allowed, s));
+        ENG_CUDA(cudaMemcpyAsync(bm_dev_l[l], bm_host_l[l], words * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        ENG_TRY(bm_buddy_remap(topk, allowed, nullptr, 0, B, k, E, bm_dev_l[l],
+                               tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr, nullptr,
+                               tbl_len ? tbl_len + (size_t)l * E : nullptr, K > 0 ? K : 1, cfg.search_rank_h,
+                               cfg.rho, cfg.fallback, cfg.method, cfg.beta, 0.0, 0.0, 1, nullptr, 1.0, executed,
+                               kind, used, delta, batch_ok, s));
+        ENG_CUDA(cudaMemcpyAsync(plan_host, plan_dev, plan_bytes(B, k), cudaMemcpyDeviceToHost, s));
+        return BM_OK;
+    }
+
+    // buffer-map upload, K3 permute, gather, K4 grouped FFN, K5 combine (in place)
+    int enqueue_post(int l, float *h, int64_t B, cudaStream_t s) {
+        const int Et = E + Ssh, kt = k + Ssh;
+        ENG_CUDA(cudaMemcpyAsync(bo_dev_l[l], bo_host_l[l], Et * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        const int32_t *pe = executed;
+        const uint8_t *pk = kind;
+        const float *pp = probs;
+        if (Ssh) {  // every token also runs the shared experts with weight 1
+            ENG_TRY(bm_append_shared(executed, kind, probs, B, k, E, Ssh, exec_ext, kind_ext, probs_ext, s));
+            pe = exec_ext;
+            pk = kind_ext;
+            pp = probs_ext;
+        }
+        ENG_TRY(bm_permute(pe, pk, B, kt, Et, 16, count, offset, row_token, slot_row, s));
+        if (cfg.fp32_weights) {
+            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 0, x_perm, s));
+            ENG_TRY(bm_expert_ffn_f32(static_cast<float *>(x_perm), count, offset, Et, d, f, cfg.act,
+                                      reinterpret_cast<const float *>(arena), buf_elems, bo_dev_l[l], r_max, h_ws,
+                                      y_perm, s));
+        } else {
+            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 1, x_perm, s));
+            // no expert gets more than B rows: size the token tile to the batch
+            const int nt = std::min(cfg.n_tile, std::max(16, (int)((B + 15) / 16 * 16)));
+            ENG_TRY(bm_expert_ffn_bf16(x_perm, count, offset, Et, d, f, cfg.act, arena, nbufs, bo_dev_l[l], r_max,
+                                       nt, ffn_ws, ffn_ws_bytes, y_perm, s));
+        }
+        ENG_TRY(bm_combine(y_perm, slot_row, pp, pk, B, kt, d, h, 0.5f, h, s));
+        return BM_OK;
+    }
+
+    // Replay a per-(layer, B) CUDA graph of enqueue_pre/post (captured on the
+    // second occurrence; the first runs eagerly and warms lazy attributes).
+    template <typename Body>
+    int run(std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> &cache_g, int l, float *h, int64_t B,
+            cudaStream_t s, Body body) {
+        if (!use_graphs || bm_kernel_timing_enabled()) return body(s);
+        auto &slot = cache_g[{l, B}];
+        if (slot.second == nullptr) {
+            if (slot.first++ == 0) return body(s);
+            cudaGraph_t g;
+            ENG_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+            int rc = body(cap_stream);
+            cudaError_t ce = cudaStreamEndCapture(cap_stream, &g);
+            if (rc != BM_OK) return rc;
+            ENG_CUDA(ce);
+            ENG_CUDA(cudaGraphInstantiate(&slot.second, g, 0));
+            cudaGraphDestroy(g);
+        }
+        ENG_CUDA(cudaGraphLaunch(slot.second, s));
+        return BM_OK;
+    }
+
     int layer_step(int l, float *h, int64_t B, const int32_t *tokens, cudaStream_t s) {
-        const int par = parity;
-        parity ^= 1;
+        carve(B);
         // 1. speculative loads for the next layer (harness.py:321-326)
         if (cfg.prefetch_enabled && L > 1) {
             const int t = l + 1 < L ? l + 1 : 0;
@@ -163,24 +254,10 @@ struct bm_engine {
         }
         // 2. commit completed transfers (harness.py:327-329)
         ENG_TRY(bm_cache_settle(cache, l));
-        // 3. K1 router
-        ENG_TRY(bm_gate_topk(h, gate_w + (size_t)l * E * d, gate_b + (size_t)l * E, B, E, d, k, cfg.temperature,
-                             tau[l], cfg.gamma, logits, topk, probs, tae, margin, allowed, s));
-        // 4. snapshot + K2 remap (harness.py:331-361)
+        // 3-5. K1 router, snapshot, K2 remap, plan readback (harness.py:331-361)
         const int words = (E + 31) / 32;
-        ENG_TRY(bm_cache_snapshot(cache, l, nullptr, bitmap_host[par]));
-        ENG_CUDA(cudaMemcpyAsync(bitmap_dev[par], bitmap_host[par], words * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        ENG_TRY(bm_buddy_remap(topk, allowed, nullptr, 0, B, k, E, bitmap_dev[par],
-                               tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr, nullptr,
-                               tbl_len ? tbl_len + (size_t)l * E : nullptr, K > 0 ? K : 1, cfg.search_rank_h,
-                               cfg.rho, cfg.fallback, cfg.method, cfg.beta, 0.0, 0.0, 1, nullptr, 1.0, executed,
-                               kind, used, delta, batch_ok, s));
-        // 5. plan readback for the sequential cache replay
-        ENG_CUDA(cudaMemcpyAsync(topk_h, topk, B * k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        ENG_CUDA(cudaMemcpyAsync(exec_h, executed, B * k * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        ENG_CUDA(cudaMemcpyAsync(kind_h, kind, B * k, cudaMemcpyDeviceToHost, s));
-        ENG_CUDA(cudaMemcpyAsync(allowed_h, allowed, B, cudaMemcpyDeviceToHost, s));
-        ENG_CUDA(cudaMemcpyAsync(batch_ok_h, batch_ok, 1, cudaMemcpyDeviceToHost, s));
+        ENG_TRY(bm_cache_snapshot(cache, l, nullptr, bm_host_l[l]));
+        ENG_TRY(run(g_pre, l, h, B, s, [&](cudaStream_t st) { return enqueue_pre(l, h, B, st); }));
         ENG_CUDA(cudaEventRecord(plan_ev, s));
         ENG_CUDA(cudaEventSynchronize(plan_ev));
         if (cfg.method == BM_METHOD_BUDDY) {
@@ -195,7 +272,7 @@ struct bm_engine {
             tr_kind.insert(tr_kind.end(), kind_h, kind_h + B * k);
             tr_allowed.insert(tr_allowed.end(), allowed_h, allowed_h + B);
             tr_batch_ok.push_back(batch_ok_h[0]);
-            tr_bitmap.insert(tr_bitmap.end(), bitmap_host[par], bitmap_host[par] + words);
+            tr_bitmap.insert(tr_bitmap.end(), bm_host_l[l], bm_host_l[l] + words);
         }
         // 6. control plane: replay accesses in (token, slot) order (harness.py:363-382)
         int64_t out4[4];
@@ -238,41 +315,13 @@ struct bm_engine {
             ENG_CUDA(cudaEventRecord(bb, s));
             stall_ev.emplace_back(a, bb);
         }
-        for (int e = 0; e < E; ++e) buf_of_host[par][e] = phys[l][e] >= 0 ? phys[l][e] : 0;
-        for (int sx = 0; sx < Ssh; ++sx) buf_of_host[par][E + sx] = shared_buf[(size_t)l * Ssh + sx];
-        const int Et = E + Ssh, kt = k + Ssh;
-        ENG_CUDA(cudaMemcpyAsync(buf_of_dev[par], buf_of_host[par], Et * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        int32_t *bo = bo_host_l[l];
+        for (int e = 0; e < E; ++e) bo[e] = phys[l][e] >= 0 ? phys[l][e] : 0;
+        for (int sx = 0; sx < Ssh; ++sx) bo[E + sx] = shared_buf[(size_t)l * Ssh + sx];
         stats.ffn_experts += Ssh;
         stats.ffn_rows += (int64_t)B * Ssh;
-        // 8. K3 permute -> K4 grouped FFN -> K5 combine + layer_update (in place)
-        const int32_t *pe = executed;
-        const uint8_t *pk = kind;
-        const float *pp = probs;
-        if (Ssh) {  // every token also runs the shared experts with weight 1
-            ENG_TRY(bm_append_shared(executed, kind, probs, B, k, E, Ssh, exec_ext, kind_ext, probs_ext, s));
-            pe = exec_ext;
-            pk = kind_ext;
-            pp = probs_ext;
-        }
-        ENG_TRY(bm_permute(pe, pk, B, kt, Et, 16, count, offset, row_token, slot_row, s));
-        if (cfg.fp32_weights) {
-            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 0, x_perm, s));
-            ENG_TRY(bm_expert_ffn_f32(static_cast<float *>(x_perm), count, offset, Et, d, f, cfg.act,
-                                      reinterpret_cast<const float *>(arena), buf_elems, buf_of_dev[par], r_max,
-                                      h_ws, y_perm, s));
-        } else {
-            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 1, x_perm, s));
-            // the host already knows every expert's row count: size the GEMM's
-            // token tile to it (smaller B stages -> deeper pipeline, more chains)
-            int maxc = 0;
-            for (int e = 0; e < E; ++e) maxc = std::max(maxc, (int)cnt[e]);
-            if (Ssh) maxc = std::max(maxc, (int)B);
-            int nt = std::min(cfg.n_tile, std::max(16, (maxc + 15) / 16 * 16));
-            if (getenv("BMOE_NTILE_FIXED")) nt = cfg.n_tile;
-            ENG_TRY(bm_expert_ffn_bf16(x_perm, count, offset, Et, d, f, cfg.act, arena, nbufs, buf_of_dev[par],
-                                       r_max, nt, ffn_ws, ffn_ws_bytes, y_perm, s));
-        }
-        ENG_TRY(bm_combine(y_perm, slot_row, pp, pk, B, kt, d, h, 0.5f, h, s));
+        // 8. K3 -> K4 -> K5 (in place on h)
+        ENG_TRY(run(g_post, l, h, B, s, [&](cudaStream_t st) { return enqueue_post(l, h, B, st); }));
         // 9. release buffers of experts the control plane no longer holds
         ENG_CUDA(cudaEventRecord(layer_done[l], s));
         ENG_TRY(bm_cache_snapshot(cache, l, mask_tmp.data(), nullptr));
@@ -299,17 +348,18 @@ struct bm_engine {
             cudaEventDestroy(p.first);
             cudaEventDestroy(p.second);
         }
-        void *dptrs[] = {exec_ext, kind_ext, probs_ext, logits, probs, y_perm, h_ws, tae, margin, delta, topk,
-                         executed, used, kind, allowed,
-                         batch_ok, bitmap_dev[0], bitmap_dev[1], buf_of_dev[0], buf_of_dev[1], count, offset,
-                         row_token, slot_row, x_perm, ffn_ws};
+        for (auto *m : {&g_pre, &g_post})
+            for (auto &kv : *m)
+                if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
+        void *dptrs[] = {exec_ext, kind_ext, probs_ext, logits, probs, y_perm, h_ws, tae, margin, delta, used,
+                         plan_dev, h_int, bm_dev_all, bo_dev_all, count, offset, row_token, slot_row, x_perm, ffn_ws};
         for (void *p : dptrs)
             if (p) cudaFree(p);
-        void *hptrs[] = {bitmap_host[0], bitmap_host[1], buf_of_host[0], buf_of_host[1], topk_h, exec_h, kind_h,
-                         allowed_h, batch_ok_h};
+        void *hptrs[] = {plan_host, bm_host_all, bo_host_all};
         for (void *p : hptrs)
             if (p) cudaFreeHost(p);
         if (plan_ev) cudaEventDestroy(plan_ev);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (prefetch_stream) cudaStreamDestroy(prefetch_stream);
         if (cache) bm_cache_destroy(cache);
@@ -373,7 +423,10 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
         for (int e = 0; e < E; ++e) ENG_CUDA(cudaEventCreateWithFlags(&g->ready[l][e], cudaEventDisableTiming));
         ENG_CUDA(cudaEventCreateWithFlags(&g->layer_done[l], cudaEventDisableTiming));
     }
-    ENG_CUDA(cudaEventCreateWithFlags(&g->plan_ev, cudaEventDisableTiming | cudaEventBlockingSync));
+    // spin-wait on the plan readback: the host round trip is on the critical path
+    ENG_CUDA(cudaEventCreateWithFlags(&g->plan_ev, cudaEventDisableTiming));
+    ENG_CUDA(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+    if (const char *ev = getenv("BMOE_GRAPHS")) g->use_graphs = atoi(ev) != 0;
     ENG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     ENG_CUDA(cudaStreamCreateWithFlags(&g->prefetch_stream, cudaStreamNonBlocking));
     // initial residents: synchronous upload
@@ -409,17 +462,21 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     ENG_TRY(g->dmalloc(&g->tae, Bm));
     ENG_TRY(g->dmalloc(&g->margin, Bm));
     ENG_TRY(g->dmalloc(&g->delta, 1));
-    ENG_TRY(g->dmalloc(&g->topk, Bm * k));
-    ENG_TRY(g->dmalloc(&g->executed, Bm * k));
     ENG_TRY(g->dmalloc(&g->used, Bm));
-    ENG_TRY(g->dmalloc(&g->kind, Bm * k));
-    ENG_TRY(g->dmalloc(&g->allowed, Bm));
-    ENG_TRY(g->dmalloc(&g->batch_ok, 1));
-    for (int i = 0; i < 2; ++i) {
-        ENG_TRY(g->dmalloc(&g->bitmap_dev[i], (E + 31) / 32));
-        ENG_TRY(g->dmalloc(&g->buf_of_dev[i], Et));
-        ENG_TRY(g->hmalloc(&g->bitmap_host[i], (E + 31) / 32));
-        ENG_TRY(g->hmalloc(&g->buf_of_host[i], Et));
+    const size_t pb = bm_engine::plan_bytes(Bm, k) + 64;
+    ENG_TRY(g->dmalloc(&g->plan_dev, pb));
+    ENG_TRY(g->hmalloc(&g->plan_host, pb));
+    ENG_TRY(g->dmalloc(&g->h_int, (size_t)Bm * g->d));
+    const int words = (E + 31) / 32;
+    ENG_TRY(g->dmalloc(&g->bm_dev_all, (size_t)L * words));
+    ENG_TRY(g->hmalloc(&g->bm_host_all, (size_t)L * words));
+    ENG_TRY(g->dmalloc(&g->bo_dev_all, (size_t)L * Et));
+    ENG_TRY(g->hmalloc(&g->bo_host_all, (size_t)L * Et));
+    for (int l = 0; l < L; ++l) {
+        g->bm_dev_l.push_back(g->bm_dev_all + (size_t)l * words);
+        g->bm_host_l.push_back(g->bm_host_all + (size_t)l * words);
+        g->bo_dev_l.push_back(g->bo_dev_all + (size_t)l * Et);
+        g->bo_host_l.push_back(g->bo_host_all + (size_t)l * Et);
     }
     ENG_TRY(g->dmalloc(&g->count, Et));
     ENG_TRY(g->dmalloc(&g->offset, Et + 1));
@@ -440,11 +497,6 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
         g->ffn_ws_bytes = bm_expert_ffn_bf16_workspace(Et, g->d, g->f, g->r_max, c->n_tile);
         ENG_TRY(g->dmalloc(reinterpret_cast<uint8_t **>(&g->ffn_ws), (size_t)g->ffn_ws_bytes));
     }
-    ENG_TRY(g->hmalloc(&g->topk_h, Bm * k));
-    ENG_TRY(g->hmalloc(&g->exec_h, Bm * k));
-    ENG_TRY(g->hmalloc(&g->kind_h, Bm * k));
-    ENG_TRY(g->hmalloc(&g->allowed_h, Bm));
-    ENG_TRY(g->hmalloc(&g->batch_ok_h, 1));
     g->prev_counts.assign(L, std::vector<int32_t>(E, 0));
     g->mask_tmp.assign(E, 0);
     return BM_OK;
@@ -483,7 +535,10 @@ extern "C" int bm_engine_step(bm_engine *e, float *h, int64_t B, const int32_t *
         return BM_EINVAL;
     }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    for (int l = 0; l < e->L; ++l) ENG_TRY(e->layer_step(l, h, B, tokens_host, s));
+    // the layers run on an engine-owned copy of h so captured graphs see fixed addresses
+    ENG_CUDA(cudaMemcpyAsync(e->h_int, h, (size_t)B * e->d * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    for (int l = 0; l < e->L; ++l) ENG_TRY(e->layer_step(l, e->h_int, B, tokens_host, s));
+    ENG_CUDA(cudaMemcpyAsync(h, e->h_int, (size_t)B * e->d * sizeof(float), cudaMemcpyDeviceToDevice, s));
     e->stats.tokens += B;
     return BM_OK;
 }

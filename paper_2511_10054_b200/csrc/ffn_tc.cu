@@ -527,6 +527,8 @@ extern "C" int bm_set_kernel_timing(int32_t enable) {
     return BM_OK;
 }
 
+extern "C" int bm_kernel_timing_enabled(void) { return g_timing.enabled ? 1 : 0; }
+
 // Two floats per bm_expert_ffn_bf16 call since timing was enabled: GEMM1
 // and GEMM2 kernel durations in ms (CUDA events on the launching stream).
 extern "C" int64_t bm_kernel_times(float *out_host, int64_t cap) {

@@ -75,10 +75,13 @@ class Workload:
         kw.update(overrides)
         kw["method"] = method
         es = EngineSpec(**kw)
+        initial = self.initial
+        if "capacity" in overrides:
+            initial = [initial_residents(es.num_experts, es.capacity, 0, l) for l in range(es.num_layers)]
         return DecodeEngine(es, self.mirrors, self.gate_w, self.gate_b,
                             self.tbl_ids if method == "buddy" else None,
                             self.tbl_len if method == "buddy" else None,
-                            self.taus, self.initial)
+                            self.taus, initial)
 
     def tokens(self, seed: int, n: int) -> np.ndarray:
         return substrate.token_stream(self.spec, seed, n).astype(np.float32)
