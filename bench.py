@@ -295,6 +295,26 @@ def run_profile_bench(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def measure_h2d(wl) -> float:
+    """GB/s of cudaMemcpyAsync from the pinned host mirror into HBM (one
+    expert at a time, 4 experts): the PCIe roofline of an expert fetch."""
+    import torch
+    from paper_2511_10054_b200 import _native as N
+    nb = wl.eng.buf_bytes
+    dst = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream()
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for e in range(4):
+            N.call("bm_memcpy", dst.data_ptr(), wl.mirrors[0].ptr + (e % wl.eng.num_experts) * nb, nb, s.cuda_stream)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, 4 * nb / (a.elapsed_time(b) / 1e3) / 1e9)
+    return best
+
+
 def _timed(eng, x_work, B, steps, offset, torch):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
@@ -384,6 +404,10 @@ def main():
     ach = bytes_g1 / (g1_ms / 1e3) / 1e9
     ach_pair = (bytes_g1 + bytes_g2) / ((g1_ms + g2_ms) / 1e3) / 1e9
 
+    # ---------------- fetch roofline: measured pinned H2D copy rate ----------------
+    h2d_peak = measure_h2d(wl)
+    fetch_gbs = st["h2d_bytes"] / (st["stall_ms"] / 1e3) / 1e9 if st["stall_ms"] > 0 else None
+
     # ---------------- end to end through the public API, host buffers ----------------
     out_host = torch.empty_like(x_host)
     h = torch.empty(B, D_MODEL, device="cuda")
@@ -447,6 +471,9 @@ def main():
                      "gemm2_avg_launch_ms": g2_ms, "pair_achieved_gbs": ach_pair, "peak_kind": peak_kind,
                      "experts_per_launch": n_exp, "rows_per_launch": rows},
         "cpu_baseline": cpu,
+        "fetch_roofline": {"bound": "pcie", "achieved": fetch_gbs, "peak": h2d_peak, "unit": "GB/s",
+                           "frac": (fetch_gbs / h2d_peak) if fetch_gbs else None,
+                           "note": "expert-miss bytes / measured fetch stall vs pinned H2D copy of one expert"},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": B * D_MODEL * 4,
                 "d2h_bytes_per_step": B * D_MODEL * 4},
         "gpu_launches": kernels_per_layer * L * K,
