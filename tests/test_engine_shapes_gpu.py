@@ -109,7 +109,8 @@ def test_dsv2_shared_experts_numerics(cuda_ok):
     wl.close()
 
 
-@pytest.mark.parametrize("name,layers,B", [("mixtral", 2, 16), ("qwen3", 3, 16), ("dsv2lite", 3, 8)])
+@pytest.mark.parametrize("name,layers,B", [("mixtral", 2, 16), ("qwen3", 3, 16), ("dsv2lite", 3, 8),
+                                           ("qwen3", 2, 512)])  # the last one is a prefill-sized batch
 def test_engine_decisions_bit_exact_at_baseline_shapes(cuda_ok, name, layers, B):
     wl = W.build(name, layers=layers, max_batch=B, profile_tokens=2048)
     eng = wl.engine("buddy")

@@ -1,0 +1,32 @@
+"""Small invocation of every kernel, for compute-sanitizer runs:
+    compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+    compute-sanitizer --tool racecheck python tools/sanitize_smoke.py
+"""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import __graft_entry__  # noqa: E402
+
+if __name__ == "__main__":
+    __graft_entry__.smoke()
+    import numpy as np
+    import torch
+    from paper_2511_10054_b200 import ops
+    # remap with Psi ordering and H > 32 (multi-chunk ballots), E not a multiple of 32
+    rng = np.random.default_rng(1)
+    E, k, B, K = 100, 6, 40, 64
+    topk = np.stack([rng.choice(E, k, replace=False) for _ in range(B)]).astype(np.int32)
+    ids = np.stack([rng.permutation([j for j in range(E) if j != p])[:K] for p in range(E)]).astype(np.int32)
+    w = np.sort(rng.random((E, K)), axis=1)[:, ::-1].copy()
+    t = ops.DeviceTable(torch.from_numpy(ids).cuda(), torch.from_numpy(w).cuda(),
+                        torch.full((E,), K, dtype=torch.int32).cuda())
+    plan = ops.buddy_remap(torch.from_numpy(topk).cuda(), torch.ones(B, dtype=torch.uint8).cuda(),
+                           ops.bitmap_from_mask(rng.random(E) < 0.3, "cuda"), t, H=50, rho=None, eta=0.2, kappa=0.1,
+                           partition_of=torch.from_numpy((np.arange(E) * 3 // E).astype(np.int32)).cuda(),
+                           logits=torch.randn(B, E, dtype=torch.float64).cuda())
+    torch.cuda.synchronize()
+    print("sanitize smoke ok")
