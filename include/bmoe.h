@@ -118,6 +118,12 @@ int bm_append_shared(const int32_t *executed, const uint8_t *kind, const float *
                      int64_t E, int64_t S, int32_t *executed_ext, uint8_t *kind_ext, float *probs_ext,
                      bm_stream_t stream);
 
+/* count_a[e] = mask[e] ? 0 : count[e], count_b[e] = mask[e] ? count[e] : 0 —
+ * splits one grouped FFN into experts already in HBM (run while the
+ * others are still being fetched) and the fetched ones. */
+int bm_split_counts(const int32_t *expert_count, const int32_t *mask, int64_t E, int32_t *count_a, int32_t *count_b,
+                    bm_stream_t stream);
+
 /* Gather token rows into the permuted activation buffer (128-bit loads).
  * layout 0: plain row-major fp32 x_perm[r_max][d].
  * layout 1: bf16 "UMMA K-major SW128" planes: x_perm[d/64][r_max][64] with

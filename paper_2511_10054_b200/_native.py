@@ -70,6 +70,7 @@ _SIGS = {
                                  I32, P, F64, P, P, P, P, P, P]),
     "bm_permute_rows_max": (I64, [I64, I64, I64, I64]),
     "bm_append_shared": (C.c_int, [P, P, P, I64, I64, I64, I64, P, P, P, P]),
+    "bm_split_counts": (C.c_int, [P, P, I64, P, P, P]),
     "bm_permute": (C.c_int, [P, P, I64, I64, I64, I64, P, P, P, P, P]),
     "bm_gather_rows": (C.c_int, [P, I64, I64, P, P, I64, I64, I32, P, P]),
     "bm_combine": (C.c_int, [P, P, P, P, I64, I64, I64, P, F32, P, P]),

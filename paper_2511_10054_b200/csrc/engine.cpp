@@ -93,7 +93,9 @@ struct bm_engine {
     std::vector<int32_t *> bo_dev_l, bo_host_l;   // per-layer buffer maps (E + shared)
     cudaStream_t cap_stream = nullptr;
     bool use_graphs = true;
-    std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> g_pre, g_post;
+    std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> g_pre, g_post, g_post2;
+    int32_t *count_a = nullptr, *count_b = nullptr;  // split expert counts (resident / fetched)
+    bool overlap_fetch = true;  // run resident experts' GEMMs while misses stream in (BMOE_OVERLAP=0 disables)
     bm_engine_stats stats{};
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev;
     std::vector<uint8_t> mask_tmp;
@@ -180,43 +182,59 @@ struct bm_engine {
         return BM_OK;
     }
 
-    // buffer-map upload, K3 permute, gather, K4 grouped FFN, K5 combine (in place)
-    int enqueue_post(int l, float *h, int64_t B, cudaStream_t s) {
+    // Post phase, part 1 (before the fetch waits): buffer map + fetch mask
+    // upload, K3 permute, gather, and — bf16 path — K4 over the experts that
+    // are already in HBM, overlapping the H2D copies of the missing ones.
+    int enqueue_post1(int l, float *h, int64_t B, cudaStream_t s) {
         const int Et = E + Ssh, kt = k + Ssh;
-        ENG_CUDA(cudaMemcpyAsync(bo_dev_l[l], bo_host_l[l], Et * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        ENG_CUDA(cudaMemcpyAsync(bo_dev_l[l], bo_host_l[l], 2 * Et * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         const int32_t *pe = executed;
         const uint8_t *pk = kind;
-        const float *pp = probs;
         if (Ssh) {  // every token also runs the shared experts with weight 1
             ENG_TRY(bm_append_shared(executed, kind, probs, B, k, E, Ssh, exec_ext, kind_ext, probs_ext, s));
             pe = exec_ext;
             pk = kind_ext;
-            pp = probs_ext;
         }
         ENG_TRY(bm_permute(pe, pk, B, kt, Et, 16, count, offset, row_token, slot_row, s));
         if (cfg.fp32_weights) {
             ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 0, x_perm, s));
+            return BM_OK;  // the fp32 parity path runs in one piece after the waits
+        }
+        ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 1, x_perm, s));
+        ENG_TRY(bm_split_counts(count, bo_dev_l[l] + Et, Et, count_a, count_b, s));
+        return ffn_bf16(l, B, count_a, s);
+    }
+
+    int ffn_bf16(int l, int64_t B, const int32_t *cnt, cudaStream_t s) {
+        const int Et = E + Ssh;
+        // no expert gets more than B rows: size the token tile to the batch
+        const int nt = std::min(cfg.n_tile, std::max(16, (int)((B + 15) / 16 * 16)));
+        return bm_expert_ffn_bf16(x_perm, cnt, offset, Et, d, f, cfg.act, arena, nbufs, bo_dev_l[l], r_max, nt,
+                                  ffn_ws, ffn_ws_bytes, y_perm, s);
+    }
+
+    // Post phase, part 2 (after the waits): K4 over the fetched experts, K5 combine (in place)
+    int enqueue_post2(int l, float *h, int64_t B, bool fetched, cudaStream_t s) {
+        const int Et = E + Ssh, kt = k + Ssh;
+        if (cfg.fp32_weights) {
             ENG_TRY(bm_expert_ffn_f32(static_cast<float *>(x_perm), count, offset, Et, d, f, cfg.act,
                                       reinterpret_cast<const float *>(arena), buf_elems, bo_dev_l[l], r_max, h_ws,
                                       y_perm, s));
-        } else {
-            ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 1, x_perm, s));
-            // no expert gets more than B rows: size the token tile to the batch
-            const int nt = std::min(cfg.n_tile, std::max(16, (int)((B + 15) / 16 * 16)));
-            ENG_TRY(bm_expert_ffn_bf16(x_perm, count, offset, Et, d, f, cfg.act, arena, nbufs, bo_dev_l[l], r_max,
-                                       nt, ffn_ws, ffn_ws_bytes, y_perm, s));
+        } else if (fetched) {
+            ENG_TRY(ffn_bf16(l, B, count_b, s));
         }
-        ENG_TRY(bm_combine(y_perm, slot_row, pp, pk, B, kt, d, h, 0.5f, h, s));
+        ENG_TRY(bm_combine(y_perm, slot_row, Ssh ? probs_ext : probs, Ssh ? kind_ext : kind, B, kt, d, h, 0.5f, h, s));
         return BM_OK;
     }
 
     // Replay a per-(layer, B) CUDA graph of enqueue_pre/post (captured on the
     // second occurrence; the first runs eagerly and warms lazy attributes).
     template <typename Body>
-    int run(std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> &cache_g, int l, float *h, int64_t B,
-            cudaStream_t s, Body body) {
+    int run(std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> &cache_g, int l, int variant,
+            float *h, int64_t B, cudaStream_t s, Body body) {
+        (void)h;
         if (!use_graphs || bm_kernel_timing_enabled()) return body(s);
-        auto &slot = cache_g[{l, B}];
+        auto &slot = cache_g[{l * 2 + variant, B}];
         if (slot.second == nullptr) {
             if (slot.first++ == 0) return body(s);
             cudaGraph_t g;
@@ -257,7 +275,7 @@ struct bm_engine {
         // 3-5. K1 router, snapshot, K2 remap, plan readback (harness.py:331-361)
         const int words = (E + 31) / 32;
         ENG_TRY(bm_cache_snapshot(cache, l, nullptr, bm_host_l[l]));
-        ENG_TRY(run(g_pre, l, h, B, s, [&](cudaStream_t st) { return enqueue_pre(l, h, B, st); }));
+        ENG_TRY(run(g_pre, l, 0, h, B, s, [&](cudaStream_t st) { return enqueue_pre(l, h, B, st); }));
         ENG_CUDA(cudaEventRecord(plan_ev, s));
         ENG_CUDA(cudaEventSynchronize(plan_ev));
         if (cfg.method == BM_METHOD_BUDDY) {
@@ -292,6 +310,7 @@ struct bm_engine {
         }
         // 7. data plane: every executed expert must be in HBM before the GEMM
         std::vector<cudaEvent_t> waits;
+        std::vector<int> wait_experts;
         ++stats.ffn_calls;
         for (int e = 0; e < E; ++e) {
             if (!cnt[e]) continue;
@@ -303,10 +322,29 @@ struct bm_engine {
             }
             if (ready_pending[l][e]) {
                 waits.push_back(ready[l][e]);
+                wait_experts.push_back(e);
                 ready_pending[l][e] = 0;
             }
         }
-        if (!waits.empty()) {
+        const int Et = E + Ssh;
+        int32_t *bo = bo_host_l[l];  // [buffer map (Et) | fetched-this-step mask (Et)]
+        for (int e = 0; e < E; ++e) {
+            bo[e] = phys[l][e] >= 0 ? phys[l][e] : 0;
+            bo[Et + e] = 0;
+        }
+        for (int sx = 0; sx < Ssh; ++sx) {
+            bo[E + sx] = shared_buf[(size_t)l * Ssh + sx];
+            bo[Et + E + sx] = 0;
+        }
+        for (int e : wait_experts) bo[Et + e] = 1;
+        if (!overlap_fetch && !waits.empty())  // A/B switch: everything after the waits
+            for (int e = 0; e < Et; ++e) bo[Et + e] = 1;
+        stats.ffn_experts += Ssh;
+        stats.ffn_rows += (int64_t)B * Ssh;
+        // 8. K3 -> K4 (resident experts) || H2D of the missing ones -> K4 (fetched) -> K5
+        ENG_TRY(run(g_post, l, 0, h, B, s, [&](cudaStream_t st) { return enqueue_post1(l, h, B, st); }));
+        const bool fetched = !waits.empty();
+        if (fetched) {
             cudaEvent_t a, bb;
             ENG_CUDA(cudaEventCreate(&a));
             ENG_CUDA(cudaEventCreate(&bb));
@@ -315,13 +353,8 @@ struct bm_engine {
             ENG_CUDA(cudaEventRecord(bb, s));
             stall_ev.emplace_back(a, bb);
         }
-        int32_t *bo = bo_host_l[l];
-        for (int e = 0; e < E; ++e) bo[e] = phys[l][e] >= 0 ? phys[l][e] : 0;
-        for (int sx = 0; sx < Ssh; ++sx) bo[E + sx] = shared_buf[(size_t)l * Ssh + sx];
-        stats.ffn_experts += Ssh;
-        stats.ffn_rows += (int64_t)B * Ssh;
-        // 8. K3 -> K4 -> K5 (in place on h)
-        ENG_TRY(run(g_post, l, h, B, s, [&](cudaStream_t st) { return enqueue_post(l, h, B, st); }));
+        ENG_TRY(run(g_post2, l, fetched ? 1 : 0, h, B, s,
+                    [&](cudaStream_t st) { return enqueue_post2(l, h, B, fetched, st); }));
         // 9. release buffers of experts the control plane no longer holds
         ENG_CUDA(cudaEventRecord(layer_done[l], s));
         ENG_TRY(bm_cache_snapshot(cache, l, mask_tmp.data(), nullptr));
@@ -348,11 +381,12 @@ struct bm_engine {
             cudaEventDestroy(p.first);
             cudaEventDestroy(p.second);
         }
-        for (auto *m : {&g_pre, &g_post})
+        for (auto *m : {&g_pre, &g_post, &g_post2})
             for (auto &kv : *m)
                 if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
         void *dptrs[] = {exec_ext, kind_ext, probs_ext, logits, probs, y_perm, h_ws, tae, margin, delta, used,
-                         plan_dev, h_int, bm_dev_all, bo_dev_all, count, offset, row_token, slot_row, x_perm, ffn_ws};
+                         plan_dev, h_int, bm_dev_all, bo_dev_all, count, offset, row_token, slot_row, x_perm, ffn_ws,
+                         count_a, count_b};
         for (void *p : dptrs)
             if (p) cudaFree(p);
         void *hptrs[] = {plan_host, bm_host_all, bo_host_all};
@@ -427,6 +461,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     ENG_CUDA(cudaEventCreateWithFlags(&g->plan_ev, cudaEventDisableTiming));
     ENG_CUDA(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
     if (const char *ev = getenv("BMOE_GRAPHS")) g->use_graphs = atoi(ev) != 0;
+    if (const char *ev = getenv("BMOE_OVERLAP")) g->overlap_fetch = atoi(ev) != 0;
     ENG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     ENG_CUDA(cudaStreamCreateWithFlags(&g->prefetch_stream, cudaStreamNonBlocking));
     // initial residents: synchronous upload
@@ -470,13 +505,15 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     const int words = (E + 31) / 32;
     ENG_TRY(g->dmalloc(&g->bm_dev_all, (size_t)L * words));
     ENG_TRY(g->hmalloc(&g->bm_host_all, (size_t)L * words));
-    ENG_TRY(g->dmalloc(&g->bo_dev_all, (size_t)L * Et));
-    ENG_TRY(g->hmalloc(&g->bo_host_all, (size_t)L * Et));
+    ENG_TRY(g->dmalloc(&g->bo_dev_all, (size_t)L * 2 * Et));
+    ENG_TRY(g->hmalloc(&g->bo_host_all, (size_t)L * 2 * Et));
+    ENG_TRY(g->dmalloc(&g->count_a, Et));
+    ENG_TRY(g->dmalloc(&g->count_b, Et));
     for (int l = 0; l < L; ++l) {
         g->bm_dev_l.push_back(g->bm_dev_all + (size_t)l * words);
         g->bm_host_l.push_back(g->bm_host_all + (size_t)l * words);
-        g->bo_dev_l.push_back(g->bo_dev_all + (size_t)l * Et);
-        g->bo_host_l.push_back(g->bo_host_all + (size_t)l * Et);
+        g->bo_dev_l.push_back(g->bo_dev_all + (size_t)l * 2 * Et);
+        g->bo_host_l.push_back(g->bo_host_all + (size_t)l * 2 * Et);
     }
     ENG_TRY(g->dmalloc(&g->count, Et));
     ENG_TRY(g->dmalloc(&g->offset, Et + 1));

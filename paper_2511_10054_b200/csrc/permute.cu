@@ -167,6 +167,15 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const float *_
     for (int i = threadIdx.x; i < d; i += blockDim.x) out[(size_t)b * d + i] = hbuf[i] * inv;
 }
 
+__global__ void split_counts_kernel(const int32_t *__restrict__ count, const int32_t *__restrict__ mask, int E,
+                                    int32_t *ca, int32_t *cb) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const int c = count[e];
+    ca[e] = mask[e] ? 0 : c;
+    cb[e] = mask[e] ? c : 0;
+}
+
 __global__ void append_shared_kernel(const int32_t *__restrict__ ex, const uint8_t *__restrict__ kd,
                                      const float *__restrict__ pr, int B, int k, int E, int S, int32_t *ex2,
                                      uint8_t *kd2, float *pr2) {
@@ -189,6 +198,15 @@ __global__ void append_shared_kernel(const int32_t *__restrict__ ex, const uint8
 }  // namespace bm
 
 using namespace bm;
+
+extern "C" int bm_split_counts(const int32_t *expert_count, const int32_t *mask, int64_t E, int32_t *count_a,
+                               int32_t *count_b, bm_stream_t stream) {
+    BM_REQUIRE(expert_count && mask && count_a && count_b && E >= 1, BM_EINVAL, "bm_split_counts: bad args");
+    split_counts_kernel<<<(unsigned)((E + 255) / 256), 256, 0, as_stream(stream)>>>(expert_count, mask, (int)E, count_a,
+                                                                                  count_b);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
 
 extern "C" int bm_append_shared(const int32_t *executed, const uint8_t *kind, const float *probs, int64_t B, int64_t k,
                                 int64_t E, int64_t S, int32_t *executed_ext, uint8_t *kind_ext, float *probs_ext,
