@@ -315,6 +315,7 @@ typedef struct {
     int64_t ffn_calls, ffn_experts, ffn_rows; /* grouped-FFN launches, sum of distinct executed experts / rows */
     double sim_now_ms;   /* control-plane clock */
     double stall_ms;     /* measured: compute stream waiting on expert fetches (CUDA events) */
+    double copy_ms;      /* measured: copy-stream time spent in expert H2D copies (CUDA events) */
 } bm_engine_stats;
 
 /* host_mirror[l]: pinned host memory, num_experts buffers of the arena

@@ -63,10 +63,10 @@ struct bm_engine {
     // device workspaces
     float *logits = nullptr, *probs = nullptr, *y_perm = nullptr, *h_ws = nullptr;
     double *tae = nullptr, *margin = nullptr, *delta = nullptr;
-    int32_t *topk = nullptr, *executed = nullptr, *used = nullptr;
+    int32_t *used = nullptr;
+    // views into the packed plan buffers, re-carved per batch size (carve())
+    int32_t *topk = nullptr, *executed = nullptr;
     uint8_t *kind = nullptr, *allowed = nullptr, *batch_ok = nullptr;
-    uint32_t *bitmap_dev[2] = {nullptr, nullptr};
-    int32_t *buf_of_dev[2] = {nullptr, nullptr};
     int32_t *count = nullptr, *offset = nullptr, *row_token = nullptr, *slot_row = nullptr;
     // shared experts (always resident, outside the budget): plan extended to k + Ssh slots
     int Ssh = 0;
@@ -76,9 +76,7 @@ struct bm_engine {
     std::vector<int> shared_buf;  // [L][Ssh] buffer ids
     void *x_perm = nullptr, *ffn_ws = nullptr;
     int64_t ffn_ws_bytes = 0, r_max = 0, device_bytes = 0;
-    // pinned staging
-    uint32_t *bitmap_host[2] = {nullptr, nullptr};
-    int32_t *buf_of_host[2] = {nullptr, nullptr};
+    // host views into the pinned plan pack
     int32_t *topk_h = nullptr, *exec_h = nullptr;
     uint8_t *kind_h = nullptr, *allowed_h = nullptr, *batch_ok_h = nullptr;
     cudaEvent_t plan_ev = nullptr;
@@ -97,7 +95,7 @@ struct bm_engine {
     int32_t *count_a = nullptr, *count_b = nullptr;  // split expert counts (resident / fetched)
     bool overlap_fetch = true;  // run resident experts' GEMMs while misses stream in (BMOE_OVERLAP=0 disables)
     bm_engine_stats stats{};
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev, copy_ev;
     std::vector<uint8_t> mask_tmp;
     std::vector<double> pend_done;
     std::vector<int32_t> pend_exp;
@@ -143,8 +141,14 @@ struct bm_engine {
         int b;
         ENG_TRY(alloc_buffer(&b));
         if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(s, bufs[b].free_ev, 0));
+        cudaEvent_t c0, c1;  // copy-engine busy time, for the PCIe roofline
+        ENG_CUDA(cudaEventCreate(&c0));
+        ENG_CUDA(cudaEventCreate(&c1));
+        ENG_CUDA(cudaEventRecord(c0, s));
         ENG_CUDA(cudaMemcpyAsync(bufs[b].dev, host_mirror[l] + (size_t)e * buf_bytes, buf_bytes,
                                  cudaMemcpyHostToDevice, s));
+        ENG_CUDA(cudaEventRecord(c1, s));
+        copy_ev.emplace_back(c0, c1);
         ENG_CUDA(cudaEventRecord(ready[l][e], s));
         ready_pending[l][e] = 1;
         phys[l][e] = b;
@@ -377,10 +381,11 @@ struct bm_engine {
                 if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : layer_done)
             if (e) cudaEventDestroy(e);
-        for (auto &p : stall_ev) {
-            cudaEventDestroy(p.first);
-            cudaEventDestroy(p.second);
-        }
+        for (auto *evs : {&stall_ev, &copy_ev})
+            for (auto &p : *evs) {
+                cudaEventDestroy(p.first);
+                cudaEventDestroy(p.second);
+            }
         for (auto *m : {&g_pre, &g_post, &g_post2})
             for (auto &kv : *m)
                 if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
@@ -582,19 +587,19 @@ extern "C" int bm_engine_step(bm_engine *e, float *h, int64_t B, const int32_t *
 
 extern "C" int bm_engine_stats_get(bm_engine *e, bm_engine_stats *out, int32_t reset) {
     if (!e || !out) return BM_EINVAL;
-    double stall = 0.0;
-    for (auto &p : e->stall_ev) {
-        ENG_CUDA(cudaEventSynchronize(p.second));
-        float ms = 0.f;
-        ENG_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
-        stall += ms;
+    for (auto *evs : {&e->stall_ev, &e->copy_ev}) {
+        double sum = 0.0;
+        for (auto &p : *evs) {
+            ENG_CUDA(cudaEventSynchronize(p.second));
+            float ms = 0.f;
+            ENG_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+            sum += ms;
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+        evs->clear();
+        (evs == &e->stall_ev ? e->stats.stall_ms : e->stats.copy_ms) += sum;
     }
-    e->stats.stall_ms += stall;
-    for (auto &p : e->stall_ev) {
-        cudaEventDestroy(p.first);
-        cudaEventDestroy(p.second);
-    }
-    e->stall_ev.clear();
     ENG_TRY(bm_cache_now(e->cache, &e->stats.sim_now_ms));
     *out = e->stats;
     if (reset) e->stats = bm_engine_stats{};

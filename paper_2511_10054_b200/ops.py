@@ -9,7 +9,6 @@ is a thin adapter over these functions.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import torch
@@ -323,11 +322,3 @@ def buddy_rank(pair_matrix64, eps: float, alpha: float, k_max: int) -> DeviceTab
 
 def sm_count() -> int:
     return int(N.lib().bm_device_sm_count())
-
-
-def isfinite_all(x) -> bool:
-    return bool(torch.isfinite(x).all().item())
-
-
-def nan_to_none(v):
-    return None if v is None or (isinstance(v, float) and math.isnan(v)) else v
