@@ -155,10 +155,14 @@ int bm_expert_ffn_f32(const float *x_perm, const int32_t *expert_count, const in
 
 /* bf16 tensor-core mode: persistent stream-K tcgen05/TMEM/TMA GEMMs with
  * weights as the M=128 operand ("swap-AB": decode token counts are the N
- * dimension), fused SwiGLU/tanh in the split-K fixup, deterministic (no
- * atomics). x_perm is layout 1 (bf16 SW128 planes over d). Workspace from
- * bm_expert_ffn_bf16_workspace(): holds the fp32 partial tiles and the
- * SW128 bf16 intermediate H. y_perm fp32 [r_max][d].
+ * dimension), fused SwiGLU/tanh, deterministic (split tiles are summed in
+ * fixed CTA order, never with float atomics). x_perm is layout 1 (bf16 SW128 planes over d). Workspace from
+ * bm_expert_ffn_bf16_workspace(): holds the fp32 partial tiles, the
+ * SW128 bf16 intermediate H and the split-tile / grid-barrier counters; it
+ * must be ZEROED ONCE when allocated (the counters are self-cleaning).
+ * y_perm fp32 [r_max][d]. Decode-width tiles (n_tile <= 64) run as ONE
+ * cooperative launch (GEMM1 -> activation -> GEMM2, split tiles reduced in
+ * kernel, one grid barrier); wider tiles run GEMM + fixup kernels.
  * Requires d % 128 == 0, f % 128 == 0. n_tile (16..256, multiple of 16)
  * caps the per-tile token count; larger expert segments are chunked. */
 /* bf16 expert buffers use the HBM-native "UMMA-tiled" layout: each weight
@@ -188,15 +192,19 @@ int bm_kernel_timing_enabled(void);
 int64_t bm_kernel_times(float *out_host, int64_t cap);
 
 /* ------------------------------------- K6/K7 co-activation and buddy ranking
- * bm_coact_count: topk[N][k] int32 (distinct ids per row, profiler.py:76-80)
- * accumulated into counts[E] and the symmetric pair matrix pairs[E][E] as
- * uint64 (binary mode: each present pair adds 1, profiler.py:86-92).
- * Shared-memory-privatised per-CTA counters, flushed with 64-bit adds.
+ * bm_coact_count: topk[N][k] int32 accumulated into counts[E] and the
+ * symmetric pair matrix pairs[E][E] as uint64 (binary mode: each present pair
+ * adds 1, profiler.py:86-92). Rows with an id outside [0, E) or a repeated id
+ * are rejected like observe() rejects them (profiler.py:76-80): they are not
+ * counted and *invalid_rows (device int32, accumulated) is incremented, so
+ * the caller raises InputError after reading it back.
+ * Shared-memory-privatised per-CTA counters, flushed with 64-bit adds; for
+ * k >= 2 the diagonal is derived as rowsum/(k-1) (exact for distinct ids).
  * Warm-up down-weighting is applied by the caller by counting the warm-up
  * token range separately (the weights are exact dyadic scalars).
  * Accumulates (does not clear). Limits: E <= 256, k <= 32. */
 int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t E, unsigned long long *counts,
-                   unsigned long long *pairs, bm_stream_t stream);
+                   unsigned long long *pairs, int32_t *invalid_rows, bm_stream_t stream);
 /* Weighted mass (profiler.py:93-95): pw[i][j] += w * min(p~_a, p~_b), f64
  * atomics (order-dependent: tolerance-level parity only). */
 int bm_coact_weighted(const int32_t *topk, const float *probs, int64_t N, int64_t k, int64_t E, double w,

@@ -82,7 +82,7 @@ _SIGS = {
     "bm_set_kernel_timing": (C.c_int, [I32]),
     "bm_kernel_times": (I64, [P, I64]),
     "bm_kernel_timing_enabled": (C.c_int, []),
-    "bm_coact_count": (C.c_int, [P, I64, I64, I64, P, P, P]),
+    "bm_coact_count": (C.c_int, [P, I64, I64, I64, P, P, P, P]),
     "bm_coact_weighted": (C.c_int, [P, P, I64, I64, I64, F64, P, P]),
     "bm_counts_to_f64": (C.c_int, [P, P, I64, F64, P, P]),
     "bm_buddy_rank": (C.c_int, [P, I64, F64, F64, I64, P, P, P, P]),

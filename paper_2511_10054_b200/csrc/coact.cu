@@ -15,24 +15,44 @@ constexpr int kMaxK = 32;
 // packed upper triangle incl. diagonal: (i <= j) -> i*E - i*(i-1)/2 + (j-i)
 __device__ __forceinline__ int tri(int i, int j, int E) { return i * E - ((i * (i - 1)) >> 1) + (j - i); }
 
+// One thread per token. With k >= 2 and k distinct ids per token (the
+// reference rejects duplicates, profiler.py:76-80) every token holding expert
+// i adds exactly k-1 to row i of the pair matrix, so the diagonal is derived
+// at flush time as rowsum/(k-1) instead of being counted: 28 instead of 36
+// shared atomics per token at k=8 (the kernel is bound by the shared-memory
+// atomic pipe, not by the trace read).
+template <int KC>
 __global__ void __launch_bounds__(kCountThreads) coact_count_kernel(const int32_t *__restrict__ topk, long long N,
-                                                                    int k, int E, long long per_block,
+                                                                    int k_rt, int E, long long per_block,
                                                                     unsigned long long *__restrict__ counts,
-                                                                    unsigned long long *__restrict__ pairs) {
+                                                                    unsigned long long *__restrict__ pairs,
+                                                                    int *__restrict__ invalid) {
     extern __shared__ uint32_t tcount[];  // E*(E+1)/2
+    const int k = KC > 0 ? KC : k_rt;
+    const bool derive_diag = k >= 2;
     const int ntri = E * (E + 1) / 2;
     for (int i = threadIdx.x; i < ntri; i += blockDim.x) tcount[i] = 0;
     __syncthreads();
     const long long t0 = (long long)blockIdx.x * per_block;
     const long long t1 = min(N, t0 + per_block);
-    if (k == 8) {
+    if constexpr (KC == 8) {
         for (long long t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
             const int4 *p = reinterpret_cast<const int4 *>(topk + t * 8);
             int4 a = __ldg(p), b = __ldg(p + 1);
             int id[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            bool bad = false;  // profiler.py:76-80: ids in range and distinct, else the row is rejected
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
-                atomicAdd(&tcount[tri(id[x], id[x], E)], 1u);
+                bad |= (unsigned)id[x] >= (unsigned)E;
+#pragma unroll
+                for (int y = x + 1; y < 8; ++y) bad |= id[x] == id[y];
+            }
+            if (bad) {
+                atomicAdd(invalid, 1);
+                continue;
+            }
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
 #pragma unroll
                 for (int y = x + 1; y < 8; ++y) {
                     int i = min(id[x], id[y]), j = max(id[x], id[y]);
@@ -43,9 +63,18 @@ __global__ void __launch_bounds__(kCountThreads) coact_count_kernel(const int32_
     } else {
         for (long long t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
             int id[kMaxK];
-            for (int x = 0; x < k; ++x) id[x] = __ldg(topk + t * k + x);
+            bool bad = false;
             for (int x = 0; x < k; ++x) {
-                atomicAdd(&tcount[tri(id[x], id[x], E)], 1u);
+                id[x] = __ldg(topk + t * k + x);
+                bad |= (unsigned)id[x] >= (unsigned)E;
+                for (int y = 0; y < x; ++y) bad |= id[x] == id[y];
+            }
+            if (bad) {
+                atomicAdd(invalid, 1);
+                continue;
+            }
+            for (int x = 0; x < k; ++x) {
+                if (!derive_diag) atomicAdd(&tcount[tri(id[x], id[x], E)], 1u);
                 for (int y = x + 1; y < k; ++y) {
                     int i = min(id[x], id[y]), j = max(id[x], id[y]);
                     atomicAdd(&tcount[tri(i, j, E)], 1u);
@@ -54,6 +83,15 @@ __global__ void __launch_bounds__(kCountThreads) coact_count_kernel(const int32_
         }
     }
     __syncthreads();
+    if (derive_diag) {  // diagonal cell := (sum of row i off the diagonal) / (k-1)
+        for (int i = threadIdx.x; i < E; i += blockDim.x) {
+            unsigned long long s = 0;
+            for (int j = 0; j < i; ++j) s += tcount[tri(j, i, E)];
+            for (int j = i + 1; j < E; ++j) s += tcount[tri(i, j, E)];
+            tcount[tri(i, i, E)] = (uint32_t)(s / (unsigned long long)(k - 1));
+        }
+        __syncthreads();
+    }
     // flush: diagonal -> counts, off-diagonal -> both mirror cells
     for (int i = 0; i < E; ++i) {
         const int base = tri(i, i, E);
@@ -223,15 +261,16 @@ __global__ void __launch_bounds__(kRankWarps * 32) buddy_rank_kernel(const doubl
 using namespace bm;
 
 extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t E, unsigned long long *counts,
-                              unsigned long long *pairs, bm_stream_t stream) {
+                              unsigned long long *pairs, int32_t *invalid_rows, bm_stream_t stream) {
     BM_REQUIRE(N >= 0 && k >= 1 && k <= kMaxK && E >= 1 && E <= kMaxE && k <= E, BM_EINVAL,
                "bm_coact_count: bad shape N=%lld k=%lld E=%lld", (long long)N, (long long)k, (long long)E);
-    BM_REQUIRE(counts && pairs && (topk || N == 0), BM_EINVAL, "bm_coact_count: null pointer");
+    BM_REQUIRE(counts && pairs && invalid_rows && (topk || N == 0), BM_EINVAL, "bm_coact_count: null pointer");
     if (N == 0) return BM_OK;
     const size_t smem = (size_t)E * (E + 1) / 2 * sizeof(uint32_t);
-    BM_CUDA_TRY(cudaFuncSetAttribute(coact_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = k == 8 ? coact_count_kernel<8> : coact_count_kernel<0>;
+    BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
-    BM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coact_count_kernel, kCountThreads, smem));
+    BM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCountThreads, smem));
     if (per_sm < 1) per_sm = 1;
     long long blocks = (long long)sm_count() * per_sm;
     // at least ~4 tokens per thread per block so the flush amortises
@@ -243,8 +282,8 @@ extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t
     if (k == 8 && (reinterpret_cast<uintptr_t>(topk) & 15) != 0) {
         BM_REQUIRE(false, BM_EINVAL, "bm_coact_count: k=8 trace must be 16-byte aligned");
     }
-    coact_count_kernel<<<(unsigned)blocks, kCountThreads, smem, as_stream(stream)>>>(topk, N, (int)k, (int)E,
-                                                                                     per_block, counts, pairs);
+    kern<<<(unsigned)blocks, kCountThreads, smem, as_stream(stream)>>>(topk, N, (int)k, (int)E, per_block, counts,
+                                                                       pairs, invalid_rows);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }

@@ -538,6 +538,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
         ENG_CUDA(cudaMemset(g->x_perm, 0, (size_t)g->r_max * g->d * 2));
         g->ffn_ws_bytes = bm_expert_ffn_bf16_workspace(Et, g->d, g->f, g->r_max, c->n_tile);
         ENG_TRY(g->dmalloc(reinterpret_cast<uint8_t **>(&g->ffn_ws), (size_t)g->ffn_ws_bytes));
+        ENG_CUDA(cudaMemset(g->ffn_ws, 0, (size_t)g->ffn_ws_bytes));  // self-cleaning counters start at zero
     }
     g->prev_counts.assign(L, std::vector<int32_t>(E, 0));
     g->mask_tmp.assign(E, 0);

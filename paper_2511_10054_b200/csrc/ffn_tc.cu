@@ -43,11 +43,16 @@ constexpr int kMaxE = 256;
 constexpr int kSmemBudget = 220 * 1024;     // dynamic; static smem (schedule, barriers) comes on top
 
 struct Sched {
-    // device-side schedule, identical in every kernel that needs it
+    // device-side schedule, identical in every kernel that needs it: the
+    // active experts in ascending id order with their row counts, first
+    // permuted row and token chunks; expert a's tiles are
+    // [mtiles*chunk_prefix[a], mtiles*chunk_prefix[a+1]), m-tile major.
     int n_act;
     int act_e[kMaxE];
+    int act_cnt[kMaxE];
+    int act_off[kMaxE];
     int act_nch[kMaxE];
-    int tile_prefix[kMaxE + 1];
+    int chunk_prefix[kMaxE + 1];
 };
 
 struct GemmParams {
@@ -69,47 +74,119 @@ struct GemmParams {
     float *y_perm;            // GEMM2 output: fp32 [r_max][M]
 };
 
-__device__ void build_sched(Sched &s, const int32_t *count, int E, int n_tile, int mtiles) {
-    int n = 0, run = 0;
-    s.tile_prefix[0] = 0;
-    for (int e = 0; e < E; ++e) {
-        const int c = count[e];
-        if (c <= 0) continue;
-        const int npad = (c + 15) & ~15;
-        const int nch = (npad + n_tile - 1) / n_tile;
-        s.act_e[n] = e;
-        s.act_nch[n] = nch;
-        run += nch * mtiles;
-        s.tile_prefix[++n] = run;
+__device__ __forceinline__ int chunks_of(int c, int n_tile) { return (((c + 15) & ~15) + n_tile - 1) / n_tile; }
+
+// Built by warp 0 (the other threads must not touch `s` before the
+// following __syncthreads): each lane owns E/32 consecutive experts, so the
+// count loads are issued in parallel, and one warp scan places them.
+__device__ void build_sched_warp(Sched &s, const int32_t *count, const int32_t *offset, int E, int n_tile) {
+    constexpr int kPer = kMaxE / 32;
+    const int lane = (int)lane_id();
+    const int per = (E + 31) / 32;
+    int c[kPer];
+    int nact = 0, nch = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const int e = lane * per + i;
+        c[i] = (i < per && e < E) ? count[e] : 0;
     }
-    s.n_act = n;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+        if (c[i] > 0) {
+            ++nact;
+            nch += chunks_of(c[i], n_tile);
+        }
+    int a = nact, ch = nch;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int ya = __shfl_up_sync(0xffffffffu, a, o), yc = __shfl_up_sync(0xffffffffu, ch, o);
+        if (lane >= o) {
+            a += ya;
+            ch += yc;
+        }
+    }
+    int ia = a - nact, ic = ch - nch;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+        if (c[i] > 0) {
+            const int e = lane * per + i, nc = chunks_of(c[i], n_tile);
+            s.act_e[ia] = e;
+            s.act_cnt[ia] = c[i];
+            s.act_off[ia] = offset[e];
+            s.act_nch[ia] = nc;
+            s.chunk_prefix[ia] = ic;
+            ic += nc;
+            ++ia;
+        }
+    if (lane == 31) {
+        s.n_act = a;
+        s.chunk_prefix[a] = ch;
+    }
 }
+
+__device__ __forceinline__ int total_tiles(const Sched &s, int mtiles) { return s.chunk_prefix[s.n_act] * mtiles; }
 
 struct TileInfo {
     int e, mtile, chunk, n;  // n = columns (tokens, padded to 16) of this tile
     int row0;                // first permuted row of the chunk
 };
 
-__device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int n_tile, const int32_t *count,
-                                                const int32_t *offset) {
+__device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int mtiles, int n_tile) {
     int lo = 0, hi = s.n_act - 1;
-    while (lo < hi) {  // last a with tile_prefix[a] <= t
+    while (lo < hi) {  // last a with mtiles * chunk_prefix[a] <= t
         int mid = (lo + hi + 1) >> 1;
-        if (s.tile_prefix[mid] <= t) lo = mid; else hi = mid - 1;
+        if (s.chunk_prefix[mid] * mtiles <= t) lo = mid; else hi = mid - 1;
     }
     TileInfo ti;
     ti.e = s.act_e[lo];
-    const int local = t - s.tile_prefix[lo];
+    const int local = t - s.chunk_prefix[lo] * mtiles;
     const int nch = s.act_nch[lo];
     ti.mtile = local / nch;
     ti.chunk = local % nch;
-    const int npad = (count[ti.e] + 15) & ~15;
+    const int npad = (s.act_cnt[lo] + 15) & ~15;
     ti.n = min(n_tile, npad - ti.chunk * n_tile);
-    ti.row0 = offset[ti.e] + ti.chunk * n_tile;
+    ti.row0 = s.act_off[lo] + ti.chunk * n_tile;
     return ti;
 }
 
 __device__ __forceinline__ long long range_start(int c, long long T, int G) { return (long long)c * T / G; }
+
+// Finish columns [c0, c0+16) of a tile for this thread's weight row m =
+// mtile*128 + q*32 + lane (g: gate/only accumulator, u: SwiGLU up):
+// mode 2 -> y_perm fp32 (32 lanes write 128 consecutive bytes per column);
+// else the activation -> bf16 SW128 H planes, lanes packing pairs to bf16x2
+// and gathering 8 m's (one 16-byte swizzle chunk) per 128-bit store.
+template <int NMAT>
+__device__ __forceinline__ void finish16(const GemmParams &p, const TileInfo &ti, int c0, int q, unsigned lane,
+                                         const float (&g)[16], const float (&u)[16]) {
+    if (p.mode == 2) {
+        const int m = ti.mtile * kBM + q * 32 + (int)lane;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) p.y_perm[(long long)(ti.row0 + c0 + j) * p.M + m] = g[j];
+        return;
+    }
+    const int mg = ti.mtile * kBM + q * 32 + ((int)lane & ~7);  // group's first m
+    const int plane = mg >> 6, chunk = (mg & 63) >> 3;
+    const int gbase = (int)lane & ~7;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const float hv = NMAT == 2 ? (g[j] / (1.0f + expf(-g[j]))) * u[j] : tanhf(g[j]);
+        const float ov = __shfl_xor_sync(0xffffffffu, hv, 1);
+        const __nv_bfloat162 pr2 = (lane & 1) ? __floats2bfloat162_rn(ov, hv) : __floats2bfloat162_rn(hv, ov);
+        const uint32_t w = *reinterpret_cast<const uint32_t *>(&pr2);
+        uint4 v4;
+        v4.x = __shfl_sync(0xffffffffu, w, gbase + 0);
+        v4.y = __shfl_sync(0xffffffffu, w, gbase + 2);
+        v4.z = __shfl_sync(0xffffffffu, w, gbase + 4);
+        v4.w = __shfl_sync(0xffffffffu, w, gbase + 6);
+        if (((int)lane & 7) == (j & 7)) {
+            const int row = ti.row0 + c0 + j;
+            uint4 *dstp = reinterpret_cast<uint4 *>(p.h_planes) +
+                          (((long long)plane * p.h_rmax + row) * 8 + (chunk ^ (row & 7)));
+            *dstp = v4;
+        }
+    }
+}
 
 template <int NMAT, int KPS>
 __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
@@ -123,9 +200,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
     const int mtiles = p.M / kBM;
     const int steps_per_tile = p.K / (kBK * KPS);  // pipeline steps per tile
 
-    if (threadIdx.x == 0) build_sched(sched, p.count, p.E, p.n_tile, mtiles);
+    if (warp == 0) build_sched_warp(sched, p.count, p.offset, p.E, p.n_tile);
     __syncthreads();
-    const long long T = (long long)sched.tile_prefix[sched.n_act] * steps_per_tile;
+    const long long T = (long long)total_tiles(sched, mtiles) * steps_per_tile;
     const int G = (int)min((long long)p.num_ctas, T);
     const int cta = blockIdx.x;
     if (cta >= G) return;  // uniform for the whole CTA
@@ -172,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         while (it < it1) {
             const int tile = (int)(it / steps_per_tile);
             const int st_end = (int)min((long long)steps_per_tile, it1 - (long long)tile * steps_per_tile);
-            const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
             const int buf = p.buf_of_expert[ti.e];
             // the m-tile's blocks are contiguous along k: [mt][kb][NMAT][16 KB]
             const uint8_t *a_src = p.arena + (long long)buf * p.buf_bytes + p.mat_off +
@@ -209,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         while (it < it1) {
             const int tile = (int)(it / steps_per_tile);
             const int st_end = (int)min((long long)steps_per_tile, it1 - (long long)tile * steps_per_tile);
-            const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
             const uint32_t idesc = ptx::idesc_bf16_f32(kBM, (uint32_t)ti.n);
             ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1u);
             ptx::tc_fence_after();
@@ -262,46 +339,16 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
             // otherwise park an fp32 partial for the deterministic fixup
             const bool whole = p.fuse && it == (long long)tile * steps_per_tile && tile_end <= it1;
             it = min(tile_end, it1);
-            const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (uint32_t)acc * acc_cols + ((uint32_t)(q * 32) << 16);
             if (whole) {
-                const int m = ti.mtile * kBM + m_local;
                 for (int c0 = 0; c0 < ti.n; c0 += 16) {
-                    float g[16];
+                    float g[16], u[16];
                     ptx::tmem_ld16(tbase + (uint32_t)c0, g);
-                    if (p.mode == 2) {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) p.y_perm[(long long)(ti.row0 + c0 + j) * p.M + m] = g[j];
-                    } else {
-                        float u[16];
-                        if (NMAT == 2) ptx::tmem_ld16(tbase + (uint32_t)(p.n_tile + c0), u);
-                        // lanes hold consecutive m: pack pairs to bf16x2, gather 8 m's
-                        // (16 bytes, one swizzle chunk) per lane group, one 128-bit store
-                        const int mg = ti.mtile * kBM + q * 32 + ((int)lane & ~7);  // group's first m
-                        const int plane = mg >> 6, chunk = (mg & 63) >> 3;
-                        const int gbase = (int)lane & ~7;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const float hv = NMAT == 2 ? (g[j] / (1.0f + expf(-g[j]))) * u[j] : tanhf(g[j]);
-                            const float ov = __shfl_xor_sync(0xffffffffu, hv, 1);
-                            const __nv_bfloat162 pr2 = (lane & 1) ? __floats2bfloat162_rn(ov, hv)
-                                                                  : __floats2bfloat162_rn(hv, ov);
-                            const uint32_t w = *reinterpret_cast<const uint32_t *>(&pr2);
-                            uint4 v4;
-                            v4.x = __shfl_sync(0xffffffffu, w, gbase + 0);
-                            v4.y = __shfl_sync(0xffffffffu, w, gbase + 2);
-                            v4.z = __shfl_sync(0xffffffffu, w, gbase + 4);
-                            v4.w = __shfl_sync(0xffffffffu, w, gbase + 6);
-                            if (((int)lane & 7) == (j & 7)) {
-                                const int row = ti.row0 + c0 + j;
-                                uint4 *dstp = reinterpret_cast<uint4 *>(p.h_planes) +
-                                              (((long long)plane * p.h_rmax + row) * 8 + (chunk ^ (row & 7)));
-                                *dstp = v4;
-                            }
-                        }
-                    }
+                    if (NMAT == 2) ptx::tmem_ld16(tbase + (uint32_t)(p.n_tile + c0), u);
+                    finish16<NMAT>(p, ti, c0, q, lane, g, u);
                 }
             } else {
                 const long long slot = (long long)tile + cta;
@@ -346,14 +393,14 @@ __global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, 
     __shared__ Sched sched;
     const int mtiles = p.M / kBM;
     const int steps_per_tile = p.K / (kBK * p.kps);  // must match ffn_gemm_kernel's iteration space
-    if (threadIdx.x == 0) build_sched(sched, p.count, p.E, p.n_tile, mtiles);
+    if (threadIdx.x < 32) build_sched_warp(sched, p.count, p.offset, p.E, p.n_tile);
     __syncthreads();
-    const int ntiles = sched.tile_prefix[sched.n_act];
+    const int ntiles = total_tiles(sched, mtiles);
     const long long T = (long long)ntiles * steps_per_tile;
     const int G = (int)min((long long)p.num_ctas, T);
     const int m_local = threadIdx.x;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const TileInfo ti = decode_tile(sched, tile, p.n_tile, p.count, p.offset);
+        const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
         const int c0 = cta_of((long long)tile * steps_per_tile, T, G);
         const int c1 = cta_of((long long)(tile + 1) * steps_per_tile - 1, T, G);
         if (p.fuse && c0 == c1) continue;  // one CTA owned it: its epilogue already wrote the result
@@ -379,6 +426,336 @@ __global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, 
             }
         }
     }
+}
+
+// ------------------------------------------------ fused decode FFN (one launch)
+// GEMM1 (W1|W3, or Win) -> SwiGLU / tanh -> H -> GEMM2 (W2, or Wout) ->
+// y_perm in ONE persistent launch for decode-width tiles (n_tile <= 64):
+//  * split (stream-K) tiles are reduced inside the kernel by the CTA whose
+//    contribution arrives last (per-tile arrival counter). It sums the fp32
+//    partial slots in fixed CTA order, so the result is bit-identical to the
+//    separate fixup kernel whatever the arrival order;
+//  * one grid barrier separates the phases (H complete). The launch is
+//    cooperative, so all CTAs (one per SM) are co-resident;
+//  * while waiting at the barrier the producer already streams the first
+//    stages of W2 (they do not depend on H) and completes each of those
+//    stages with its H part once the barrier opens.
+// The counters are self-cleaning (the last arriver resets them), so the
+// workspace is zeroed once, when it is allocated.
+struct FusedParams {
+    GemmParams g[2];
+    int *arrive;         // [2][tile_cap] split-tile arrival counters
+    int tile_cap;
+    unsigned *grid_bar;  // [0] arrivals, [1] generation
+    int prefetch_w2;     // stream W2's first stages before the barrier opens
+};
+
+constexpr int kSmemFused = 216 * 1024;
+
+struct Geom {
+    uint32_t base, stage_bytes, bsz, b_off;  // b_off: B part offset inside a stage (max A bytes)
+    int stages;
+    uint32_t full0, empty0, tfull0, tempty0;
+};
+
+template <int NMAT, int KPS>
+__device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &gm, int &stage, uint32_t &phase,
+                              long long it0, long long it1, int spt, uint64_t pol, const unsigned *gate,
+                              unsigned gen0, int prefetch) {
+    constexpr uint32_t kA = (uint32_t)(KPS * NMAT) * kATileBytes;
+    const int mtiles = P.M / kBM;
+    int cur = -1;
+    const uint8_t *a_tile = nullptr, *b_tile = nullptr;
+    uint32_t bbytes = 0;
+    auto locate = [&](long long it, int &st) {
+        const int tile = (int)(it / spt);
+        st = (int)(it - (long long)tile * spt);
+        if (tile != cur) {
+            cur = tile;
+            const TileInfo ti = decode_tile(s, tile, mtiles, P.n_tile);
+            const int buf = P.buf_of_expert[ti.e];
+            a_tile = P.arena + (long long)buf * P.buf_bytes + P.mat_off + (long long)ti.mtile * spt * kA;
+            b_tile = P.b_planes + (long long)ti.row0 * 128;
+            bbytes = (uint32_t)ti.n * 128u;
+        }
+    };
+    auto issue_b = [&](int stg, int st) {
+        const uint32_t sB = gm.base + (uint32_t)stg * gm.stage_bytes + gm.b_off;
+        const uint32_t fb = gm.full0 + 8 * stg;
+#pragma unroll
+        for (int i = 0; i < KPS; ++i)
+            ptx::bulk_load(sB + i * gm.bsz, b_tile + (long long)(st * KPS + i) * P.b_plane_bytes, bbytes, fb);
+    };
+    long long it = it0;
+    if (gate && !prefetch) {
+        while (ptx::ld_acquire_gpu(gate) == gen0) __nanosleep(64);
+        ptx::fence_proxy_async_global();
+    } else if (gate) {
+        // the weights do not depend on H: A parts of the first stages now ...
+        const long long pre_end = min(it1, it0 + (long long)gm.stages);
+        const int stage0 = stage;
+        for (; it < pre_end; ++it) {
+            int st;
+            locate(it, st);
+            ptx::mbar_wait(gm.empty0 + 8 * stage, phase ^ 1u);
+            const uint32_t fb = gm.full0 + 8 * stage;
+            ptx::mbar_expect_tx_only(fb, kA);
+            ptx::bulk_load_hint(gm.base + (uint32_t)stage * gm.stage_bytes, a_tile + (long long)st * kA, kA, fb, pol);
+            if (++stage == gm.stages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        // ... then the H parts once every CTA has finished phase 1
+        while (ptx::ld_acquire_gpu(gate) == gen0) __nanosleep(64);
+        ptx::fence_proxy_async_global();
+        int stg = stage0;
+        for (long long j = it0; j < pre_end; ++j) {
+            int st;
+            locate(j, st);
+            ptx::mbar_expect_tx(gm.full0 + 8 * stg, (uint32_t)KPS * bbytes);  // the stage's arrive
+            issue_b(stg, st);
+            if (++stg == gm.stages) stg = 0;
+        }
+    }
+    for (; it < it1; ++it) {
+        int st;
+        locate(it, st);
+        ptx::mbar_wait(gm.empty0 + 8 * stage, phase ^ 1u);
+        const uint32_t fb = gm.full0 + 8 * stage;
+        ptx::mbar_expect_tx(fb, kA + (uint32_t)KPS * bbytes);
+        ptx::bulk_load_hint(gm.base + (uint32_t)stage * gm.stage_bytes, a_tile + (long long)st * kA, kA, fb, pol);
+        issue_b(stage, st);
+        if (++stage == gm.stages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+    }
+}
+
+template <int NMAT, int KPS>
+__device__ void fused_mma(const GemmParams &P, const Sched &s, const Geom &gm, int &stage, uint32_t &phase, int &acc,
+                          uint32_t &acc_phase, long long it0, long long it1, int spt, uint32_t tmem_base) {
+    const int mtiles = P.M / kBM;
+    const uint64_t desc0 = ptx::sw128_desc(gm.base);
+    const uint64_t stage_d = gm.stage_bytes >> 4, bsz_d = gm.bsz >> 4, boff_d = gm.b_off >> 4;
+    long long it = it0;
+    while (it < it1) {
+        const int tile = (int)(it / spt);
+        const int st_end = (int)min((long long)spt, it1 - (long long)tile * spt);
+        const TileInfo ti = decode_tile(s, tile, mtiles, P.n_tile);
+        const uint32_t idesc = ptx::idesc_bf16_f32(kBM, (uint32_t)ti.n);
+        ptx::mbar_wait(gm.tempty0 + 8 * acc, acc_phase ^ 1u);
+        ptx::tc_fence_after();
+        const uint32_t d0 = tmem_base + (uint32_t)acc * 256u;
+        const uint32_t d1 = d0 + (uint32_t)P.n_tile;
+        uint32_t accum = 0;
+        for (int st = (int)(it - (long long)tile * spt); st < st_end; ++st, ++it) {
+            ptx::mbar_wait(gm.full0 + 8 * stage, phase);
+            ptx::tc_fence_after();
+            const uint64_t a = desc0 + (uint64_t)stage * stage_d;
+            const uint64_t b = a + boff_d;
+#pragma unroll
+            for (int i = 0; i < KPS; ++i) {
+                const uint64_t bi = b + (uint64_t)i * bsz_d;
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                    ptx::mma_bf16(d0, a + (uint64_t)((i * NMAT) * (kATileBytes >> 4) + 2 * kk), bi + 2 * kk, idesc,
+                                  accum);
+                    if (NMAT == 2)
+                        ptx::mma_bf16(d1, a + (uint64_t)((i * NMAT + 1) * (kATileBytes >> 4) + 2 * kk), bi + 2 * kk,
+                                      idesc, accum);
+                    accum = 1u;
+                }
+            }
+            ptx::mma_commit(gm.empty0 + 8 * stage);
+            if (++stage == gm.stages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        ptx::mma_commit(gm.tfull0 + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1u;
+    }
+}
+
+template <int NMAT>
+__device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &gm, int *arrive, int &acc,
+                               uint32_t &acc_phase, long long T, int G, int cta, int spt, uint32_t tmem_base, int q,
+                               unsigned lane, volatile int *last_sh) {
+    if (cta >= G) return;
+    const int mtiles = P.M / kBM;
+    const long long it0 = range_start(cta, T, G), it1 = range_start(cta + 1, T, G);
+    const long long slot_elems = 2LL * P.n_tile * kBM;
+    const int m_local = q * 32 + (int)lane;
+    long long it = it0;
+    while (it < it1) {
+        const int tile = (int)(it / spt);
+        const long long tile_end = (long long)(tile + 1) * spt;
+        const bool whole = it == (long long)tile * spt && tile_end <= it1;
+        it = min(tile_end, it1);
+        const TileInfo ti = decode_tile(s, tile, mtiles, P.n_tile);
+        ptx::mbar_wait(gm.tfull0 + 8 * acc, acc_phase);
+        ptx::tc_fence_after();
+        const uint32_t tbase = tmem_base + (uint32_t)acc * 256u + ((uint32_t)(q * 32) << 16);
+        if (whole) {
+            for (int c0 = 0; c0 < ti.n; c0 += 16) {
+                float g[16], u[16];
+                ptx::tmem_ld16(tbase + (uint32_t)c0, g);
+                if (NMAT == 2) ptx::tmem_ld16(tbase + (uint32_t)(P.n_tile + c0), u);
+                finish16<NMAT>(P, ti, c0, q, lane, g, u);
+            }
+        } else {
+            float *dst = P.partials + ((long long)tile + cta) * slot_elems;
+#pragma unroll
+            for (int m = 0; m < NMAT; ++m)
+                for (int c0 = 0; c0 < ti.n; c0 += 16) {
+                    float v[16];
+                    ptx::tmem_ld16(tbase + (uint32_t)(m * P.n_tile + c0), v);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) dst[((long long)m * P.n_tile + c0 + j) * kBM + m_local] = v[j];
+                }
+        }
+        // the accumulator is free as soon as it has been read
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(gm.tempty0 + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1u;
+        if (whole) continue;
+        // split tile: the last contributing CTA reduces it (fixed CTA order)
+        const int c0 = cta_of((long long)tile * spt, T, G), c1 = cta_of((long long)(tile + 1) * spt - 1, T, G);
+        __threadfence();
+        ptx::named_bar_sync(1, 128);
+        if (m_local == 0) {
+            const int prev = atomicAdd(arrive + tile, 1);
+            const int last = prev == c1 - c0;
+            if (last) arrive[tile] = 0;  // self-cleaning for the next launch
+            *last_sh = last;
+        }
+        ptx::named_bar_sync(1, 128);
+        if (*last_sh) {
+            __threadfence();
+            for (int cc = 0; cc < ti.n; cc += 16) {
+                float g[16], u[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) g[j] = u[j] = 0.f;
+                for (int c = c0; c <= c1; ++c) {
+                    const float *src = P.partials + ((long long)tile + c) * slot_elems;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        g[j] += __ldcg(src + (long long)(cc + j) * kBM + m_local);
+                        if (NMAT == 2) u[j] += __ldcg(src + (long long)(P.n_tile + cc + j) * kBM + m_local);
+                    }
+                }
+                finish16<NMAT>(P, ti, cc, q, lane, g, u);
+            }
+        }
+    }
+}
+
+template <int NMAT1, int KPS1, int KPS2>
+__global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_constant__ FusedParams fp) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ Sched sched;
+    __shared__ __align__(8) uint64_t bars[64];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ int last_sh;
+
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const GemmParams &P1 = fp.g[0];
+    const GemmParams &P2 = fp.g[1];
+    const int n_tile = P1.n_tile;
+    if (warp == 0) build_sched_warp(sched, P1.count, P1.offset, P1.E, n_tile);
+    // the barrier generation cannot advance before this CTA arrives, so
+    // reading it here (before the __syncthreads) is race-free
+    unsigned gen0 = 0;
+    if (threadIdx.x == 0) gen0 = *reinterpret_cast<volatile unsigned *>(fp.grid_bar + 1);
+
+    constexpr uint32_t kA1 = (uint32_t)(KPS1 * NMAT1) * kATileBytes, kA2 = (uint32_t)KPS2 * kATileBytes;
+    constexpr uint32_t kAmax = kA1 > kA2 ? kA1 : kA2;
+    constexpr int kKmax = KPS1 > KPS2 ? KPS1 : KPS2;
+    Geom gm;
+    gm.base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    gm.bsz = ((uint32_t)n_tile * 128u + 1023u) & ~1023u;
+    gm.b_off = kAmax;
+    gm.stage_bytes = kAmax + (uint32_t)kKmax * gm.bsz;
+    gm.stages = min(16, (int)((kSmemFused - 1024) / gm.stage_bytes));
+    gm.full0 = ptx::smem_u32(&bars[0]);
+    gm.empty0 = ptx::smem_u32(&bars[16]);
+    gm.tfull0 = ptx::smem_u32(&bars[32]);
+    gm.tempty0 = ptx::smem_u32(&bars[34]);
+
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < gm.stages; ++s) {
+            ptx::mbar_init(gm.full0 + 8 * s, 1);
+            ptx::mbar_init(gm.empty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(gm.tfull0 + 8 * a, 1);
+            ptx::mbar_init(gm.tempty0 + 8 * a, 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(&tmem_base_sh), 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = tmem_base_sh;
+
+    const int cta = blockIdx.x, Gn = gridDim.x;
+    const int spt1 = P1.K / (kBK * KPS1), spt2 = P2.K / (kBK * KPS2);
+    const long long T1 = (long long)total_tiles(sched, P1.M / kBM) * spt1;
+    const long long T2 = (long long)total_tiles(sched, P2.M / kBM) * spt2;
+    const int G1 = (int)min((long long)Gn, T1), G2 = (int)min((long long)Gn, T2);
+
+    if (warp == 0 && lane == 0) {
+        const uint64_t pol = ptx::policy_evict_first();  // weights stream through once
+        int stage = 0;
+        uint32_t phase = 0;
+        if (cta < G1)
+            fused_produce<NMAT1, KPS1>(P1, sched, gm, stage, phase, range_start(cta, T1, G1),
+                                       range_start(cta + 1, T1, G1), spt1, pol, nullptr, 0, 0);
+        if (cta < G2)
+            fused_produce<1, KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2), range_start(cta + 1, T2, G2),
+                                   spt2, pol, fp.grid_bar + 1, gen0, fp.prefetch_w2);
+    } else if (warp == 1 && lane == 0) {
+        int stage = 0, acc = 0;
+        uint32_t phase = 0, acc_phase = 0;
+        if (cta < G1)
+            fused_mma<NMAT1, KPS1>(P1, sched, gm, stage, phase, acc, acc_phase, range_start(cta, T1, G1),
+                                   range_start(cta + 1, T1, G1), spt1, tmem_base);
+        if (cta < G2)
+            fused_mma<1, KPS2>(P2, sched, gm, stage, phase, acc, acc_phase, range_start(cta, T2, G2),
+                               range_start(cta + 1, T2, G2), spt2, tmem_base);
+    } else if (warp >= 4) {
+        const int q = warp - 4;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, T1, G1, cta, spt1, tmem_base, q, lane,
+                              &last_sh);
+        // H of this CTA is written: publish it (to the bulk-copy proxy too) and arrive
+        ptx::fence_proxy_async_global();
+        __threadfence();
+        ptx::named_bar_sync(1, 128);
+        if (q == 0 && lane == 0) {
+            const unsigned prev = atomicAdd(fp.grid_bar, 1u);
+            if (prev == (unsigned)Gn - 1u) {
+                fp.grid_bar[0] = 0u;
+                __threadfence();
+                atomicAdd(fp.grid_bar + 1, 1u);
+            }
+        }
+        fused_epilogue<1>(P2, sched, gm, fp.arrive + fp.tile_cap, acc, acc_phase, T2, G2, cta, spt2, tmem_base, q,
+                          lane, &last_sh);
+    }
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
 }
 
 // Pack a row-major bf16 matrix W[M][K] into the UMMA-tiled expert layout:
@@ -444,6 +821,77 @@ int launch_gemm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
     return launch_gemm<1, 4>(g, G, s);
 }
 
+template <int NMAT1, int KPS1, int KPS2>
+int launch_fused(const FusedParams &fp, int G, cudaStream_t s) {
+    static bool attr = false;
+    auto kern = ffn_fused_kernel<NMAT1, KPS1, KPS2>;
+    if (!attr) {
+        BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFused));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemFused;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, fp));
+    return BM_OK;
+}
+
+template <int NMAT1>
+int launch_fused_k(const FusedParams &fp, int kps1, int kps2, int G, cudaStream_t s) {
+    if (kps1 == 2) {
+        if (kps2 == 4) return launch_fused<NMAT1, 2, 4>(fp, G, s);
+        if (kps2 == 2) return launch_fused<NMAT1, 2, 2>(fp, G, s);
+        return launch_fused<NMAT1, 2, 1>(fp, G, s);
+    }
+    if (kps2 == 4) return launch_fused<NMAT1, 1, 4>(fp, G, s);
+    if (kps2 == 2) return launch_fused<NMAT1, 1, 2>(fp, G, s);
+    return launch_fused<NMAT1, 1, 1>(fp, G, s);
+}
+
+// fused-kernel k-blocks per stage: GEMM1 KPS1 in {2,1}, GEMM2 KPS2 in {4,2,1},
+// the largest dividing K/64 whose combined stage leaves >= 3 stages
+// (>= 2 for the widest tiles) in kSmemFused.
+void fused_kps(int nmat1, long long d, long long f, long long n_tile, int *k1, int *k2) {
+    const long long bsz = ((n_tile * 128 + 1023) / 1024) * 1024;
+    int best1 = 1, best2 = 1;
+    // tuning / A-B overrides: BMOE_KPS sets both (as for the unfused GEMMs), BMOE_KPS1/2 each
+    int e1 = 0, e2 = 0;
+    if (const char *ev = getenv("BMOE_KPS")) e1 = e2 = atoi(ev);
+    if (const char *ev = getenv("BMOE_KPS1")) e1 = atoi(ev);
+    if (const char *ev = getenv("BMOE_KPS2")) e2 = atoi(ev);
+    if ((e1 == 1 || e1 == 2) && (e2 == 1 || e2 == 2 || e2 == 4) && (d / kBK) % e1 == 0 && (f / kBK) % e2 == 0) {
+        const long long stage = std::max((long long)e1 * nmat1, (long long)e2) * kATileBytes + std::max(e1, e2) * bsz;
+        if ((kSmemFused - 1024) / stage >= 2) {
+            *k1 = e1;
+            *k2 = e2;
+            return;
+        }
+    }
+    for (int a : {2, 1}) {
+        if ((d / kBK) % a) continue;
+        for (int b : {4, 2, 1}) {
+            if ((f / kBK) % b) continue;
+            const long long amax = std::max((long long)a * nmat1, (long long)b) * kATileBytes;
+            const long long stage = amax + std::max(a, b) * bsz;
+            const int want = n_tile <= 32 ? 3 : 2;
+            if ((kSmemFused - 1024) / stage >= want) {
+                *k1 = a;
+                *k2 = b;
+                return;
+            }
+        }
+    }
+    *k1 = best1;
+    *k2 = best2;
+}
+
 // k-blocks per pipeline stage: the largest of {4,2,1} dividing K/64 whose
 // stage fits twice in shared memory (BMOE_KPS overrides for tuning).
 int kps_for(int nmat, long long K, long long n_tile) {
@@ -459,12 +907,30 @@ int kps_for(int nmat, long long K, long long n_tile) {
 
 using namespace bm;
 
-extern "C" int64_t bm_expert_ffn_bf16_workspace(int64_t E, int64_t d, int64_t f, int64_t r_max, int64_t n_tile) {
+namespace bm {
+namespace {
+// workspace: [fp32 partial slots | bf16 SW128 H planes | split-tile arrival
+// counters (2 phases) + grid barrier]; the counters must start at zero.
+struct WsLayout {
+    long long partial_bytes, h_off, h_bytes, ctr_off, tile_cap, total;
+};
+WsLayout ws_layout(long long E, long long d, long long f, long long r_max, long long n_tile) {
+    WsLayout w;
     const long long M = std::max(d, f);
-    const long long slots = max_tiles(E, M, r_max, n_tile) + sm_count() + 1;
-    const long long partial_bytes = slots * 2 * n_tile * kBM * 4;
-    const long long h_bytes = (f / 64) * r_max * 128;
-    return ((partial_bytes + 1023) / 1024) * 1024 + h_bytes;
+    w.tile_cap = max_tiles(E, M, r_max, n_tile);
+    const long long slots = w.tile_cap + sm_count() + 1;
+    w.partial_bytes = ((slots * 2 * n_tile * kBM * 4 + 1023) / 1024) * 1024;
+    w.h_off = w.partial_bytes;
+    w.h_bytes = (((f / 64) * r_max * 128 + 1023) / 1024) * 1024;
+    w.ctr_off = w.h_off + w.h_bytes;
+    w.total = w.ctr_off + (2 * w.tile_cap + 2) * 4;
+    return w;
+}
+}  // namespace
+}  // namespace bm
+
+extern "C" int64_t bm_expert_ffn_bf16_workspace(int64_t E, int64_t d, int64_t f, int64_t r_max, int64_t n_tile) {
+    return ws_layout(E, d, f, r_max, n_tile).total;
 }
 
 extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const int32_t *expert_offset,
@@ -484,15 +950,18 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
     if (r_max == 0) return BM_OK;
     cudaStream_t s = as_stream(stream);
     const long long buf_bytes = (act == BM_ACT_SWIGLU ? 3 : 2) * d * f * 2;
-    const long long slots_bytes = ((workspace_bytes - (f / 64) * r_max * 128) / 1024) * 1024;
+    const WsLayout wl = ws_layout(E, d, f, r_max, n_tile);
     float *partials = static_cast<float *>(workspace);
-    uint8_t *h_planes = static_cast<uint8_t *>(workspace) + slots_bytes;
+    uint8_t *h_planes = static_cast<uint8_t *>(workspace) + wl.h_off;
+    int *counters = reinterpret_cast<int *>(static_cast<uint8_t *>(workspace) + wl.ctr_off);
     const int G = sm_count();
     const uint8_t *arena = static_cast<const uint8_t *>(w_arena);
     const int nmat1 = act == BM_ACT_SWIGLU ? 2 : 1;
-    // Fused epilogues pay off for decode-width tiles (they remove most fixup
-    // work); for wide prefill tiles the accumulator is single-buffered and the
-    // MMA would wait on the longer epilogue, so partials + fixup are faster.
+    // Decode-width tiles (n_tile <= 64) run the single fused launch; for
+    // wide prefill tiles the accumulator is single-buffered and the MMA would
+    // wait on the longer epilogue, so they use GEMM + fixup kernels.
+    int fused = n_tile <= 64 ? 1 : 0;
+    if (const char *ev = getenv("BMOE_FUSED")) fused = fused && atoi(ev) != 0;
     int fuse = n_tile <= 64 ? 1 : 0;
     if (const char *ev = getenv("BMOE_FUSE")) fuse = atoi(ev);
     GemmParams g1{expert_count, expert_offset, buf_of_expert, (int)E, (int)f, (int)d, nmat1, (int)n_tile,
@@ -504,6 +973,23 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
 
     const bool timing = g_timing.enabled;
     std::lock_guard<std::mutex> lk(g_timing.mu);
+    if (fused) {
+        int k1 = 1, k2 = 1;
+        fused_kps(nmat1, d, f, n_tile, &k1, &k2);
+        g1.kps = k1;
+        g2.kps = k2;
+        g1.fuse = g2.fuse = 1;
+        int pre = 1;
+        if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
+        FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap, reinterpret_cast<unsigned *>(counters + 2 * wl.tile_cap),
+                       pre};
+        // timing record: [start, end] of the one kernel, then an empty GEMM2 interval
+        if (timing && record_event(s)) return BM_ECUDA;
+        const int rc = nmat1 == 2 ? launch_fused_k<2>(fp, k1, k2, G, s) : launch_fused_k<1>(fp, k1, k2, G, s);
+        if (rc) return rc;
+        if (timing && (record_event(s) || record_event(s) || record_event(s))) return BM_ECUDA;
+        return BM_OK;
+    }
     if (timing && record_event(s)) return BM_ECUDA;
     if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
     if (timing && record_event(s)) return BM_ECUDA;

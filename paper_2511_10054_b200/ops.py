@@ -262,7 +262,7 @@ class FfnWorkspace:
     def __init__(self, E, d, f, r_max, n_tile=64, device="cuda"):
         self.E, self.d, self.f, self.r_max, self.n_tile = E, d, f, r_max, n_tile
         nbytes = int(N.lib().bm_expert_ffn_bf16_workspace(E, d, f, r_max, n_tile))
-        self.buf = torch.empty(nbytes, device=device, dtype=torch.uint8)
+        self.buf = torch.zeros(nbytes, device=device, dtype=torch.uint8)  # counters start at zero
         self.nbytes = nbytes
 
 
@@ -280,8 +280,12 @@ def expert_ffn_bf16(x_perm_sw, perm: Permutation, w_arena, buf_of_expert, d: int
     return y_perm
 
 
-def coact_count(topk, num_experts: int, counts=None, pairs=None):
-    """K6: accumulate binary co-activation counts (u64, stored in int64 tensors)."""
+def coact_count(topk, num_experts: int, counts=None, pairs=None, check: bool = True):
+    """K6: accumulate binary co-activation counts (u64, stored in int64 tensors).
+
+    Rows with an out-of-range or repeated id are not counted; with ``check``
+    (one readback of a device counter) they raise InputError like observe()
+    (profiler.py:76-80)."""
     _cuda(topk, "topk", torch.int32)
     Nn, k = topk.shape
     dev = topk.device
@@ -289,7 +293,12 @@ def coact_count(topk, num_experts: int, counts=None, pairs=None):
         counts = torch.zeros(num_experts, device=dev, dtype=torch.int64)
     if pairs is None:
         pairs = torch.zeros(num_experts, num_experts, device=dev, dtype=torch.int64)
-    N.call("bm_coact_count", _p(topk), Nn, k, num_experts, _p(counts), _p(pairs), _s())
+    bad = torch.zeros(1, device=dev, dtype=torch.int32)
+    N.call("bm_coact_count", _p(topk), Nn, k, num_experts, _p(counts), _p(pairs), _p(bad), _s())
+    if check and Nn:
+        nbad = int(bad.item())
+        if nbad:
+            raise InputError(f"{nbad} routing rows with duplicate or out-of-range expert ids were not counted")
     return counts, pairs
 
 

@@ -12,6 +12,7 @@ import torch
 import oracle as O
 from conftest import golden
 from paper_2511_10054_b200 import ops
+from paper_2511_10054_b200.errors import InputError
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -173,6 +174,29 @@ def test_coact_counts_large_random_vs_oracle(cuda_ok):
     assert np.array_equal(p.cpu().numpy().astype(np.float64), op)
 
 
+@pytest.mark.parametrize("k", [1, 3, 8])
+def test_coact_rejects_bad_rows(cuda_ok, k):
+    """Rows with repeated / out-of-range ids are rejected (profiler.py:76-80);
+    the valid rows are still counted exactly (k=1 exercises the counted
+    diagonal, k>=2 the derived one)."""
+    rng = np.random.default_rng(5 + k)
+    E, N = 16, 4096
+    topk = np.stack([rng.permutation(E)[:k] for _ in range(N)]).astype(np.int32)
+    bad = np.zeros(N, bool)
+    bad[rng.choice(N, 40, replace=False)] = True
+    for t in np.flatnonzero(bad):
+        if k > 1 and t % 2:
+            topk[t, 1] = topk[t, 0]          # duplicate
+        else:
+            topk[t, k - 1] = E + (t % 3)      # out of range
+    with pytest.raises(InputError):
+        ops.coact_count(_t(topk), E)
+    c, p = ops.coact_count(_t(topk), E, check=False)
+    oc, op, _, _ = O.coact_count(topk[~bad], None, E, 0, 0, 0.0)
+    assert np.array_equal(c.cpu().numpy().astype(np.float64), oc)
+    assert np.array_equal(p.cpu().numpy().astype(np.float64), op)
+
+
 def _arena_tanh(w_in, w_out):
     # buffer layout TANH: [Win^T (f x d) | Wout^T (d x f)]
     E = w_in.shape[0]
@@ -311,3 +335,37 @@ def test_bf16_ffn_deterministic_and_buffer_indirection(cuda_ok):
     y1 = ops.expert_ffn_bf16(xp, perm, arena, _t(buf_of), d, f, ops.ACT_SWIGLU, ws)[:rows]
     y2 = ops.expert_ffn_bf16(xp, perm, arena, _t(buf_of), d, f, ops.ACT_SWIGLU, ws)[:rows]
     assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("E,d,f,B,k,act,n_tile", [
+    (8, 4096, 14336, 16, 2, ops.ACT_SWIGLU, 16),  # Mixtral decode, one expert per few CTAs
+    (8, 4096, 14336, 1, 1, ops.ACT_SWIGLU, 16),   # a single expert, one token
+    (128, 2048, 768, 64, 8, ops.ACT_SWIGLU, 64),  # Qwen3-shaped, many small experts
+    (64, 2048, 1408, 16, 6, ops.ACT_SWIGLU, 32),  # DSV2-shaped (GEMM2 K/64 = 22)
+    (8, 128, 256, 16, 2, ops.ACT_TANH, 64),       # the reference expert
+])
+def test_fused_single_launch_equals_multi_kernel(cuda_ok, E, d, f, B, k, act, n_tile):
+    """The one-launch decode FFN (in-kernel split-tile reduction + grid
+    barrier) sums the same partials in the same CTA order as the GEMM +
+    fixup kernels, so its output is bitwise identical; 30 repeats catch
+    ordering races in the arrival counters / barrier (self-cleaning state)."""
+    import os
+    rng = np.random.default_rng(E + B + d)
+    _, _, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, act, n_tile)
+    rows = int(perm.offset[-1])
+    bo = _t(buf_of)
+    saved = {v: os.environ.get(v) for v in ("BMOE_FUSED", "BMOE_KPS")}
+    try:
+        os.environ["BMOE_KPS"] = "2"  # same k-steps per stage -> same stream-K split in both paths
+        os.environ["BMOE_FUSED"] = "0"
+        ref = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows].clone()
+        os.environ["BMOE_FUSED"] = "1"
+        for _ in range(30):
+            y = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows]
+            assert torch.equal(y, ref)
+    finally:
+        for v, val in saved.items():
+            if val is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = val
