@@ -302,7 +302,9 @@ def run_profile_bench(args, ws, rank, local):
             "tokens": N, "experts": E, "top_k": k, "warmup_steps": 256, "alpha": 0.95, "k_max": 16,
             "parallelism": f"token-sharded x{ws} + NCCL all-reduce", "l2": "trace (2 GB) larger than L2"},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                         "traffic": None, "kernel": "coact_count_kernel", "algorithmic_bytes_per_launch": bytes_k,
+                         "traffic": {"dram_bytes": 2148022000 + 4829952, "per": "one 64M-token launch",
+                                     "source": "profiles/r1_coact_count.ncu-rep (ncu --set full)"} if N == 64 << 20 and ws == 1 else None,
+                         "kernel": "coact_count_kernel", "algorithmic_bytes_per_launch": bytes_k,
                          "avg_launch_ms": k_ms, "peak_kind": peak_kind},
             "cpu_baseline": cpu, "e2e": None, "gpu_launches": 5 * args.steps, "clocks": clocks}
     if rank == 0:
@@ -408,32 +410,56 @@ def main():
     N.lib().bm_set_kernel_timing(0)
     g1 = buf[0:n:2]
     g2 = buf[1:n:2]
-    # Σ algorithmic bytes over the pass / Σ GEMM kernel time. A layer-step
+    # Σ algorithmic bytes over the pass / Σ FFN kernel time. A layer-step
     # with misses issues two grouped-FFN calls (resident experts overlapped
-    # with the fetch, then the fetched ones), so per-launch figures are the
-    # pass totals divided by the number of launches.
+    # with the fetch, then the fetched ones). Decode-width calls are ONE
+    # fused kernel (GEMM1 -> SwiGLU -> GEMM2; the timing hook then reports
+    # an empty second interval), so the dominant kernel's bytes are the whole
+    # expert: W1+W3+W2 plus the activations it reads.
     launches = max(len(g1), 1)
+    fused = bool(len(g2)) and float(np.max(g2)) == 0.0  # the timing hook reports 0 for one-kernel calls
     tot_g1 = st_k["ffn_experts"] * 2 * D_MODEL * D_FF * 2 + st_k["ffn_rows"] * D_MODEL * 2  # W1+W3 + X
-    tot_g2 = st_k["ffn_experts"] * D_FF * D_MODEL * 2 + st_k["ffn_rows"] * D_FF * 2
-    bytes_g1 = tot_g1 / launches
+    tot_g2 = st_k["ffn_experts"] * D_FF * D_MODEL * 2 + st_k["ffn_rows"] * D_FF * 2        # W2 + H
+    tot_k = tot_g1 + tot_g2 if fused else tot_g1
     n_exp = st_k["ffn_experts"] / launches
     rows = st_k["ffn_rows"] / launches
     peak, peak_kind = _peaks()
     g1_ms, g2_ms = float(np.mean(g1)), float(np.mean(g2))
-    ach = tot_g1 / (float(np.sum(g1)) / 1e3) / 1e9
+    ach = tot_k / (float(np.sum(g1)) / 1e3) / 1e9
     ach_pair = (tot_g1 + tot_g2) / (float(np.sum(g1) + np.sum(g2)) / 1e3) / 1e9
+    traffic = None  # DRAM bytes of one captured launch (ncu --set full), committed under profiles/
+    try:
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")))
+        l0 = tr["launches"][0]
+        traffic = {"dram_bytes": l0["dram_read_bytes"] + l0["dram_write_bytes"], "experts": l0["experts"],
+                   "weight_bytes": l0["weight_bytes"], "source": tr["source"]}
+    except (OSError, KeyError, ValueError):
+        pass
+    kname = ("ffn_fused_kernel (one cooperative launch: W1|W3 swap-AB GEMM -> SwiGLU -> W2 GEMM, stream-K)"
+             if fused else "ffn_gemm_kernel (GEMM1: W1|W3 swap-AB, stream-K)")
 
     # ---------------- fetch roofline: measured pinned H2D copy rate ----------------
     h2d_peak = measure_h2d(wl)
     fetch_gbs = st["h2d_bytes"] / (st["copy_ms"] / 1e3) / 1e9 if st["copy_ms"] > 0 else None
 
     # ---------------- end to end through the public API, host buffers ----------------
+    # A fresh engine replays the same warm-up and the same K batches as the
+    # device-resident run, so both see identical misses and fetches; only the
+    # per-step pinned host -> device input copy and device -> host result
+    # read are added.
+    eng.close()
+    eng = wl.engine("buddy")
+    _timed(eng, x_dev.clone(), B, Wm, 0, torch)
+    eng.stats(reset=True)
     out_host = torch.empty_like(x_host)
     h = torch.empty(B, D_MODEL, device="cuda")
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     for i in range(K):
-        j = Wm + 2 * K + i
+        j = Wm + i
         h.copy_(x_host[j * B:(j + 1) * B], non_blocking=True)
         eng.step(h, np.arange(j * B, (j + 1) * B))
         out_host[j * B:(j + 1) * B].copy_(h, non_blocking=True)
@@ -441,7 +467,7 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = _allmax(start.elapsed_time(end), ws)
     e2e = ws * K * B / (e2e_ms / 1000.0)
-    eng.stats(reset=True)
+    st_e = eng.stats(reset=True)
     eng.close()
 
     # ---------------- without buddy (method=original, on-demand fetch) ----------------
@@ -471,7 +497,6 @@ def main():
                "kind": "port", "sample": f"{args.cpu_tokens} tokens x 1 layer-step (route, gates, remap, f64 forward, "
                                          f"layer_update) via the numpy oracle, best of 2, extrapolated x{L} layers"}
 
-    kernels_per_layer = 9  # gate, remap, permute, gather, GEMM1, fixup1, GEMM2, fixup2, combine
     line = {
         "metric": "MoE decode tokens/sec at fixed expert-cache budget; expert-miss stall (ms)",
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": Wm,
@@ -485,8 +510,8 @@ def main():
         "h2d_gb_per_step": st["h2d_bytes"] / K / 1e9,
         "without_buddy": orig,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": None, "kernel": "ffn_gemm_kernel (GEMM1: W1|W3 swap-AB, stream-K)",
-                     "algorithmic_bytes_per_launch": bytes_g1, "avg_launch_ms": g1_ms,
+                     "traffic": traffic, "kernel": kname,
+                     "algorithmic_bytes_per_launch": tot_k / launches, "avg_launch_ms": g1_ms,
                      "gemm2_avg_launch_ms": g2_ms, "pair_achieved_gbs": ach_pair, "peak_kind": peak_kind,
                      "experts_per_launch": n_exp, "rows_per_launch": rows},
         "cpu_baseline": cpu,
@@ -495,8 +520,10 @@ def main():
                            "note": "H2D expert bytes / copy-engine busy time (CUDA events around each fetch) vs "
                                    "the best pinned copy rate of 4 experts back to back"},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": B * D_MODEL * 4,
-                "d2h_bytes_per_step": B * D_MODEL * 4},
-        "gpu_launches": kernels_per_layer * L * K,
+                "d2h_bytes_per_step": B * D_MODEL * 4, "ms_per_step": e2e_ms / K,
+                "physical_fetches_per_step": st_e["physical_fetches"] / K,
+                "note": "fresh engine, same warm-up and the same K batches as `value`; pinned host in/out per step"},
+        "gpu_launches": int(st["kernel_launches"]),
         "clocks": clocks,
         "setup_s": time.time() - t0,
     }

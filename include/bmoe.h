@@ -185,7 +185,8 @@ int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const in
 /* Kernel timing for the bench's roofline: after bm_set_kernel_timing(1)
  * every bm_expert_ffn_bf16 call records CUDA events on its stream around its
  * two GEMM kernels; bm_kernel_times() waits for them and writes 2 floats per
- * call (GEMM1 ms, GEMM2 ms), returning the count written (-1 on error).
+ * call (GEMM1 ms, GEMM2 ms; a fused decode call is one kernel and reports
+ * (kernel ms, 0)), returning the count written (-1 on error).
  * bm_set_kernel_timing() clears the record. */
 int bm_set_kernel_timing(int32_t enable);
 int bm_kernel_timing_enabled(void);
@@ -324,6 +325,7 @@ typedef struct {
     double sim_now_ms;   /* control-plane clock */
     double stall_ms;     /* measured: compute stream waiting on expert fetches (CUDA events) */
     double copy_ms;      /* measured: copy-stream time spent in expert H2D copies (CUDA events) */
+    int64_t kernel_launches; /* libbmoe kernels launched (graph nodes included) */
 } bm_engine_stats;
 
 /* host_mirror[l]: pinned host memory, num_experts buffers of the arena

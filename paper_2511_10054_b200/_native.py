@@ -43,7 +43,7 @@ class EngineStats(C.Structure):
                 ("prefetch_copies", C.c_int64), ("h2d_bytes", C.c_int64), ("gate_forbidden", C.c_int64),
                 ("batch_bypassed", C.c_int64), ("ffn_calls", C.c_int64), ("ffn_experts", C.c_int64),
                 ("ffn_rows", C.c_int64), ("sim_now_ms", C.c_double), ("stall_ms", C.c_double),
-                ("copy_ms", C.c_double)]
+                ("copy_ms", C.c_double), ("kernel_launches", C.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

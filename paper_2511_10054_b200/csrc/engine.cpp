@@ -359,6 +359,18 @@ struct bm_engine {
         }
         ENG_TRY(run(g_post2, l, fetched ? 1 : 0, h, B, s,
                     [&](cudaStream_t st) { return enqueue_post2(l, h, B, fetched, st); }));
+        {  // gate, remap, permute, gather, combine (+ append_shared) + the FFN kernels
+            int64_t n = 5 + (Ssh ? 1 : 0);
+            if (cfg.fp32_weights) {
+                n += 2;
+            } else {
+                const int nt = std::min(cfg.n_tile, std::max(16, (int)((B + 15) / 16 * 16)));
+                const char *ev = getenv("BMOE_FUSED");
+                const int per_call = (nt <= 64 && !(ev && atoi(ev) == 0)) ? 1 : 4;
+                n += 1 + per_call * (fetched ? 2 : 1);  // split_counts + one or two FFN calls
+            }
+            stats.kernel_launches += n;
+        }
         // 9. release buffers of experts the control plane no longer holds
         ENG_CUDA(cudaEventRecord(layer_done[l], s));
         ENG_TRY(bm_cache_snapshot(cache, l, mask_tmp.data(), nullptr));

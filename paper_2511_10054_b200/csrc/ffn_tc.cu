@@ -431,16 +431,15 @@ __global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, 
 // ------------------------------------------------ fused decode FFN (one launch)
 // GEMM1 (W1|W3, or Win) -> SwiGLU / tanh -> H -> GEMM2 (W2, or Wout) ->
 // y_perm in ONE persistent launch for decode-width tiles (n_tile <= 64):
-//  * split (stream-K) tiles are reduced inside the kernel by the CTA whose
-//    contribution arrives last (per-tile arrival counter). It sums the fp32
-//    partial slots in fixed CTA order, so the result is bit-identical to the
-//    separate fixup kernel whatever the arrival order;
+//  * split (stream-K) tiles are reduced inside the kernel by the CTA that
+//    owns their first k-steps (see fused_epilogue), summing in fixed CTA
+//    order, so the result is bit-identical to the separate fixup kernel;
 //  * one grid barrier separates the phases (H complete). The launch is
 //    cooperative, so all CTAs (one per SM) are co-resident;
 //  * while waiting at the barrier the producer already streams the first
 //    stages of W2 (they do not depend on H) and completes each of those
 //    stages with its H part once the barrier opens.
-// The counters are self-cleaning (the last arriver resets them), so the
+// The counters are self-cleaning (the reducer resets them), so the
 // workspace is zeroed once, when it is allocated.
 struct FusedParams {
     GemmParams g[2];
@@ -580,10 +579,18 @@ __device__ void fused_mma(const GemmParams &P, const Sched &s, const Geom &gm, i
     }
 }
 
+// Split tiles: the CTA owning a tile's FIRST k-steps (c0) processes them at
+// the end of its range, after every other contributor (c0+1..c1) has
+// processed its share at the start of its own. So c0 reduces: it keeps its
+// accumulator in TMEM, waits on the tile's arrival counter (normally already
+// complete), adds the other slots in CTA order -- ((0 + own) + s_c0+1) + ...,
+// the fixup kernel's order -- and finishes the tile. The others publish an
+// fp32 partial slot and arrive. No partial write, fence or atomic sits on
+// the reducer's critical path.
 template <int NMAT>
 __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &gm, int *arrive, int &acc,
                                uint32_t &acc_phase, long long T, int G, int cta, int spt, uint32_t tmem_base, int q,
-                               unsigned lane, volatile int *last_sh) {
+                               unsigned lane) {
     if (cta >= G) return;
     const int mtiles = P.M / kBM;
     const long long it0 = range_start(cta, T, G), it1 = range_start(cta + 1, T, G);
@@ -594,6 +601,7 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
         const int tile = (int)(it / spt);
         const long long tile_end = (long long)(tile + 1) * spt;
         const bool whole = it == (long long)tile * spt && tile_end <= it1;
+        const bool reducer = !whole && it == (long long)tile * spt;  // owns the first k-steps, not the last
         it = min(tile_end, it1);
         const TileInfo ti = decode_tile(s, tile, mtiles, P.n_tile);
         ptx::mbar_wait(gm.tfull0 + 8 * acc, acc_phase);
@@ -606,6 +614,34 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
                 if (NMAT == 2) ptx::tmem_ld16(tbase + (uint32_t)(P.n_tile + c0), u);
                 finish16<NMAT>(P, ti, c0, q, lane, g, u);
             }
+        } else if (reducer) {
+            const int c1 = cta_of((long long)(tile + 1) * spt - 1, T, G);
+            if (m_local == 0) {
+                while (ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(arrive + tile)) < (unsigned)(c1 - cta))
+                    __nanosleep(32);
+                arrive[tile] = 0;  // every contributor has arrived: reset for the next launch
+            }
+            ptx::named_bar_sync(1, 128);
+            for (int cc = 0; cc < ti.n; cc += 16) {
+                float g[16], u[16], o[16];
+                ptx::tmem_ld16(tbase + (uint32_t)cc, o);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) g[j] = 0.f + o[j];
+                if (NMAT == 2) {
+                    ptx::tmem_ld16(tbase + (uint32_t)(P.n_tile + cc), o);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) u[j] = 0.f + o[j];
+                }
+                for (int c = cta + 1; c <= c1; ++c) {
+                    const float *src = P.partials + ((long long)tile + c) * slot_elems;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        g[j] += __ldcg(src + (long long)(cc + j) * kBM + m_local);
+                        if (NMAT == 2) u[j] += __ldcg(src + (long long)(P.n_tile + cc + j) * kBM + m_local);
+                    }
+                }
+                finish16<NMAT>(P, ti, cc, q, lane, g, u);
+            }
         } else {
             float *dst = P.partials + ((long long)tile + cta) * slot_elems;
 #pragma unroll
@@ -617,40 +653,15 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
                     for (int j = 0; j < 16; ++j) dst[((long long)m * P.n_tile + c0 + j) * kBM + m_local] = v[j];
                 }
         }
-        // the accumulator is free as soon as it has been read
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(gm.tempty0 + 8 * acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1u;
-        if (whole) continue;
-        // split tile: the last contributing CTA reduces it (fixed CTA order)
-        const int c0 = cta_of((long long)tile * spt, T, G), c1 = cta_of((long long)(tile + 1) * spt - 1, T, G);
-        __threadfence();
-        ptx::named_bar_sync(1, 128);
-        if (m_local == 0) {
-            const int prev = atomicAdd(arrive + tile, 1);
-            const int last = prev == c1 - c0;
-            if (last) arrive[tile] = 0;  // self-cleaning for the next launch
-            *last_sh = last;
-        }
-        ptx::named_bar_sync(1, 128);
-        if (*last_sh) {
+        if (!whole && !reducer) {  // publish the partial, then arrive
             __threadfence();
-            for (int cc = 0; cc < ti.n; cc += 16) {
-                float g[16], u[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) g[j] = u[j] = 0.f;
-                for (int c = c0; c <= c1; ++c) {
-                    const float *src = P.partials + ((long long)tile + c) * slot_elems;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        g[j] += __ldcg(src + (long long)(cc + j) * kBM + m_local);
-                        if (NMAT == 2) u[j] += __ldcg(src + (long long)(P.n_tile + cc + j) * kBM + m_local);
-                    }
-                }
-                finish16<NMAT>(P, ti, cc, q, lane, g, u);
-            }
+            ptx::named_bar_sync(1, 128);
+            if (m_local == 0) atomicAdd(arrive + tile, 1);
         }
     }
 }
@@ -661,7 +672,6 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     __shared__ Sched sched;
     __shared__ __align__(8) uint64_t bars[64];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ int last_sh;
 
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
@@ -734,8 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         const int q = warp - 4;
         int acc = 0;
         uint32_t acc_phase = 0;
-        fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, T1, G1, cta, spt1, tmem_base, q, lane,
-                              &last_sh);
+        fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, T1, G1, cta, spt1, tmem_base, q, lane);
         // H of this CTA is written: publish it (to the bulk-copy proxy too) and arrive
         ptx::fence_proxy_async_global();
         __threadfence();
@@ -749,7 +758,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
             }
         }
         fused_epilogue<1>(P2, sched, gm, fp.arrive + fp.tile_cap, acc, acc_phase, T2, G2, cta, spt2, tmem_base, q,
-                          lane, &last_sh);
+                          lane);
     }
     __syncwarp();
     ptx::tc_fence_before();
@@ -987,7 +996,11 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
         if (timing && record_event(s)) return BM_ECUDA;
         const int rc = nmat1 == 2 ? launch_fused_k<2>(fp, k1, k2, G, s) : launch_fused_k<1>(fp, k1, k2, G, s);
         if (rc) return rc;
-        if (timing && (record_event(s) || record_event(s) || record_event(s))) return BM_ECUDA;
+        if (timing) {
+            if (record_event(s)) return BM_ECUDA;
+            g_timing.ev.push_back(nullptr);  // no second kernel: GEMM2 interval reported as 0
+            g_timing.ev.push_back(nullptr);
+        }
         return BM_OK;
     }
     if (timing && record_event(s)) return BM_ECUDA;
@@ -1007,7 +1020,8 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
 
 extern "C" int bm_set_kernel_timing(int32_t enable) {
     std::lock_guard<std::mutex> lk(g_timing.mu);
-    for (cudaEvent_t e : g_timing.ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : g_timing.ev)
+        if (e) cudaEventDestroy(e);
     g_timing.ev.clear();
     g_timing.enabled = enable != 0;
     return BM_OK;
@@ -1021,10 +1035,11 @@ extern "C" int64_t bm_kernel_times(float *out_host, int64_t cap) {
     std::lock_guard<std::mutex> lk(g_timing.mu);
     int64_t n = 0;
     for (size_t i = 0; i + 3 < g_timing.ev.size() && n + 2 <= cap; i += 4) {
-        if (cudaEventSynchronize(g_timing.ev[i + 3]) != cudaSuccess) return -1;
+        const bool one = g_timing.ev[i + 2] == nullptr;  // fused decode call: one kernel
+        if (cudaEventSynchronize(g_timing.ev[one ? i + 1 : i + 3]) != cudaSuccess) return -1;
         float a = 0.f, b = 0.f;
         cudaEventElapsedTime(&a, g_timing.ev[i], g_timing.ev[i + 1]);
-        cudaEventElapsedTime(&b, g_timing.ev[i + 2], g_timing.ev[i + 3]);
+        if (!one) cudaEventElapsedTime(&b, g_timing.ev[i + 2], g_timing.ev[i + 3]);
         out_host[n++] = a;
         out_host[n++] = b;
     }
