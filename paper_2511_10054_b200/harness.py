@@ -1,9 +1,14 @@
-"""Decode-loop drivers of the reference harness on the B200 engine:
-``run_simulation`` (harness.py:221-424), ``run_oracle`` (:175-186) and
-``fidelity`` (:189-206).
+"""Drivers of the reference harness on the B200 kernels:
+``run_profile`` (cmd_profile, harness.py:70-117: routing + K6 co-activation
+counts + entropy samples over the profiling stream, BSST / CSV /
+tae_samples.txt files), ``run_build`` (cmd_build, :134-157: K7 tables, BSBT /
+CSV files), ``calibrate_taus`` (the tau step of cmd_simulate, :476-484),
+``run_simulation`` (:221-424), ``run_oracle`` (:175-186) and ``fidelity``
+(:189-206).
 
 Only the hot-path parts of the reference harness are here (SURVEY §8 rows
-R17, R18, R22); the CLI, config files and report formatting are out of scope.
+R6, R17-R22 and §8(f) rows 1-2); the CLI, config-file parsing and report
+formatting are out of scope.
 ``run_simulation`` takes the reference's dotted configuration keys as a
 dict (defaults from config.py:64-111), builds the synthetic model, and
 replays the evaluation stream through ``DecodeEngine`` (fp32 parity mode with
@@ -18,10 +23,12 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+import os
+
 from . import _native as N
-from . import memtier, ops, substrate
+from . import buddies, gating, memtier, ops, profiler, substrate
 from .engine import DecodeEngine, EngineSpec, HostMirror
-from .errors import ConfigurationError
+from .errors import CalibrationError, ConfigurationError, FormatError
 
 DEFAULTS = {
     "model.layers": 24, "model.experts": 64, "model.top_k": 6, "model.hidden_dim": 32, "model.ffn_dim": 64,
@@ -31,7 +38,36 @@ DEFAULTS = {
     "cost.pcie_bw_bytes_per_s": 4.0e6, "gate.temperature": 1.0, "gate.beta": 1.0, "gate.margin_gamma": None,
     "sub.h": 16, "sub.rho": None, "sub.fallback": "prefetch_original", "prefetch.enabled": True,
     "method": "buddy", "run.seed": 0, "fidelity.readout_classes": 16,
+    "stream.warmup_steps": 256, "profile.laplace_eps": 1e-3, "profile.warmup_weight": 0.0,
+    "builder.alpha": "0.95", "builder.k_max": 16, "builder.mode": "binary", "gate.tau_percentile": 15.0,
 }
+
+
+def _cfg(cfg: dict) -> dict:
+    c = dict(DEFAULTS)
+    c.update(cfg or {})
+    return c
+
+
+# file names of the reference harness (harness.py:47-65)
+def stats_path(out_dir, layer):
+    return os.path.join(out_dir, f"stats_L{layer:02d}.bin")
+
+
+def coact_path(out_dir, layer):
+    return os.path.join(out_dir, f"coact_L{layer:02d}.csv")
+
+
+def table_path(out_dir, layer):
+    return os.path.join(out_dir, f"buddies_L{layer:02d}.bin")
+
+
+def table_csv_path(out_dir, layer):
+    return os.path.join(out_dir, f"buddies_L{layer:02d}.csv")
+
+
+def tae_path(out_dir):
+    return os.path.join(out_dir, "tae_samples.txt")
 
 
 @dataclass
@@ -178,3 +214,134 @@ def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=Non
     for mm in mirrors:
         mm.close()
     return SimResult(metrics=m, outputs=outputs, events=events, tau_by_layer=taus, trace=trace)
+
+
+# ------------------------------------------------------------------ profile
+
+
+@dataclass
+class ProfileResult:
+    stats: list            # profiler.CoActivationStats per layer (device counters)
+    tae_samples: list      # float64 CUDA tensor of entropy samples per layer, token order
+    paths: dict
+
+
+def run_profile(cfg: dict, out_dir: str | None = None) -> ProfileResult:
+    """cmd_profile (harness.py:70-117) on the GPU: the full-residency forward
+    over the profiling stream (K1 router, identity plans, K3-K5 fp32 tanh
+    experts), K6 co-activation counting per layer with the global token index
+    as the step (warm-up by global index, profiler.py:81-95) and the K1
+    entropy (TAE) of every token collected on the device. With ``out_dir``
+    the reference's files are written: stats_LXX.bin (BSST v1),
+    coact_LXX.csv and tae_samples.txt ("bsim/1", one `layer value` line per
+    sample in routing order)."""
+    c = _cfg(cfg)
+    spec = _spec(c)
+    L, E, k, d, f = spec.num_layers, spec.experts_per_layer, spec.top_k, spec.hidden_dim, spec.ffn_dim
+    T = float(c["gate.temperature"])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    gw, gb = substrate.gate_weights(spec)
+    gw = torch.tensor(gw, dtype=torch.float32, device=dev)
+    gb = torch.tensor(gb, dtype=torch.float32, device=dev)
+    arenas = [torch.tensor(_tanh_arena(spec, l), device=dev) for l in range(L)]
+    bufs = torch.arange(E, dtype=torch.int32, device=dev)
+    stats = [profiler.CoActivationStats(layer=l, num_experts=E, warmup_steps=c["stream.warmup_steps"],
+                                        warmup_weight=c["profile.warmup_weight"],
+                                        laplace_eps=c["profile.laplace_eps"]) for l in range(L)]
+    weighted = c["builder.mode"] == "weighted" or c["profile.warmup_weight"] != 0.0
+    n, B = c["stream.num_tokens"], c["stream.batch"]
+    x = substrate.token_stream(spec, c["stream.seed"], n)
+    xd = torch.tensor(x, dtype=torch.float32, device=dev)
+    tae = [[] for _ in range(L)]
+    for b0 in range(0, n, B):
+        h = xd[b0:b0 + B]
+        for l in range(L):
+            r = ops.gate_topk(h, gw[l], gb[l], k, T)
+            stats[l].observe_tensors(r.topk, r.probs if weighted else None, b0)
+            tae[l].append(r.tae)
+            kept = torch.zeros_like(r.topk, dtype=torch.uint8)
+            perm = ops.permute(r.topk, kept, E)
+            yp = ops.expert_ffn_f32(ops.gather_rows(h, perm, 0), perm, arenas[l], bufs, d, f, ops.ACT_TANH)
+            h = ops.combine(yp, perm, r.probs, kept, h_in=h)
+    samples = [torch.cat(t) for t in tae]
+    paths = {}
+    if out_dir is not None:
+        os.makedirs(out_dir, exist_ok=True)
+        paths = {"stats": [], "coact": [], "tae": tae_path(out_dir)}
+        for l, st in enumerate(stats):
+            profiler.save_stats(st, stats_path(out_dir, l))
+            profiler.export_coactivation_csv(st, coact_path(out_dir, l), mode="binary")
+            paths["stats"].append(stats_path(out_dir, l))
+            paths["coact"].append(coact_path(out_dir, l))
+        save_tae_samples(samples, paths["tae"])
+    return ProfileResult(stats=stats, tae_samples=samples, paths=paths)
+
+
+def save_tae_samples(samples, path) -> None:
+    """tae_samples.txt (harness.py:112-116): "bsim/1" then `layer repr(value)`."""
+    with open(path, "w") as fh:
+        fh.write("bsim/1\n")
+        for l, t in enumerate(samples):
+            vals = t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t, np.float64)
+            fh.writelines(f"{l} {float(v)!r}\n" for v in vals)
+
+
+def load_tae_samples(path) -> dict:
+    """harness.load_tae_samples (harness.py:120-129)."""
+    out: dict = {}
+    with open(path) as fh:
+        if fh.readline().strip() != "bsim/1":
+            raise FormatError(f"{path}: bad or missing version header")
+        for line in fh:
+            layer, value = line.split()
+            out.setdefault(int(layer), []).append(float(value))
+    return out
+
+
+def calibrate_taus(samples, percentile: float = 15.0) -> list:
+    """Per-layer tau by nearest rank over a GPU sort (gating.calibrate_tau,
+    gating.py:111-123; the tau step of cmd_simulate, harness.py:476-484).
+    ``samples``: list (layer order) or dict layer -> samples; CUDA tensors
+    stay on the device."""
+    if isinstance(samples, dict):
+        layers = sorted(samples)
+        if layers != list(range(len(layers))):
+            missing = next(l for l in range(len(layers) + 1) if l not in samples)
+            raise CalibrationError(f"no entropy samples for layer {missing}")
+        samples = [samples[l] for l in layers]
+    return [gating.calibrate_tau(s, percentile) for s in samples]
+
+
+def _alphas(c, L) -> list:
+    parts = [p.strip() for p in str(c["builder.alpha"]).split(",") if p.strip()]
+    try:
+        vals = [float(p) for p in parts]
+    except ValueError:
+        raise ConfigurationError(f"bad builder.alpha {c['builder.alpha']!r}") from None
+    if len(vals) == 1:
+        vals = vals * L
+    if len(vals) != L:
+        raise ConfigurationError(f"builder.alpha needs 1 or {L} values, got {len(vals)}")
+    if not all(0.0 < v <= 1.0 for v in vals):
+        raise ConfigurationError("builder.alpha values must be in (0, 1]")
+    return vals
+
+
+def run_build(cfg: dict, stats=None, profile_dir: str | None = None, out_dir: str | None = None) -> list:
+    """cmd_build (harness.py:134-157): one K7 buddy table per layer from the
+    profiled stats (given, or loaded from profile_dir's BSST files); with
+    ``out_dir`` writes buddies_LXX.bin (BSBT v1) and buddies_LXX.csv."""
+    c = _cfg(cfg)
+    L = c["model.layers"]
+    if stats is None:
+        if profile_dir is None:
+            raise ConfigurationError("run_build needs stats or a profile_dir")
+        stats = [profiler.load_stats(stats_path(profile_dir, l)) for l in range(L)]
+    alphas = _alphas(c, L)
+    tables = [buddies.build_table(stats[l], alphas[l], c["builder.k_max"], c["builder.mode"]) for l in range(L)]
+    if out_dir is not None:
+        os.makedirs(out_dir, exist_ok=True)
+        for l, t in enumerate(tables):
+            buddies.save_table(t, table_path(out_dir, l))
+            buddies.export_table_csv(t, table_csv_path(out_dir, l))
+    return tables

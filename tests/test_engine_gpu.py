@@ -114,3 +114,48 @@ def test_engine_bf16_tensor_core_mode_same_decisions(cuda_ok):
           f"events identical for the first {first}/{len(ref)}")
     assert np.median(rel) <= 2e-2, np.median(rel)
     eng.close()
+
+
+def test_profile_build_pipeline_matches_reference(cuda_ok, tmp_path):
+    """cmd_profile -> cmd_build on the GPU (harness.run_profile / run_build):
+    co-activation counts and buddy tables bit-exact vs the reference's files
+    for the tiny config; entropy samples within the fp32-router tolerance and
+    the calibrated taus equal to 1e-6; the written BSST / BSBT /
+    tae_samples.txt files load back identically; and the simulation driven by
+    these self-built tables and taus reproduces the reference's event log."""
+    from paper_2511_10054_b200 import buddies, harness, profiler
+    g = golden("sim_tiny.npz")
+    TINY = {"model.layers": 4, "model.experts": 8, "model.top_k": 2, "model.hidden_dim": 128,
+            "model.ffn_dim": 256, "model.clusters": 8, "stream.batch": 16, "cache.rate": 0.5, "sub.h": 7}
+    cfg = dict(TINY)
+    cfg["stream.num_tokens"] = 2000
+    pdir, bdir = str(tmp_path / "p"), str(tmp_path / "b")
+    prof = harness.run_profile(cfg, pdir)
+    for l in range(4):
+        assert np.array_equal(prof.stats[l].counts, g[f"counts_L{l}"]), l
+        assert np.array_equal(prof.stats[l].pair_counts, g[f"pairs_L{l}"]), l
+        np.testing.assert_allclose(prof.tae_samples[l].cpu().numpy(), g[f"tae_L{l}"], rtol=0, atol=2e-6)
+    taus = harness.calibrate_taus(prof.tae_samples, 15.0)
+    np.testing.assert_allclose(taus, g["taus"], rtol=0, atol=2e-6)
+    # files round-trip through the reference formats
+    loaded = harness.load_tae_samples(prof.paths["tae"])
+    assert sorted(loaded) == [0, 1, 2, 3] and len(loaded[0]) == 2000
+    assert harness.calibrate_taus(loaded, 15.0) == taus
+    tables = harness.run_build(dict(cfg, **{"builder.k_max": 7}), profile_dir=pdir, out_dir=bdir)
+    for l in range(4):
+        st = profiler.load_stats(harness.stats_path(pdir, l))
+        assert np.array_equal(st.pair_counts, g[f"pairs_L{l}"])
+        t = buddies.load_table(harness.table_path(bdir, l))
+        for p in range(8):
+            n = int(g[f"lens_L{l}"][p])
+            assert list(t.ids(p)) == list(g[f"ids_L{l}"][p, :n]) == list(tables[l].ids(p)), (l, p)
+            assert np.array_equal(t.weights(p), g[f"w_L{l}"][p, :n])
+    sim = dict(TINY)
+    sim.update({"method": "buddy", "stream.seed": 2, "stream.num_tokens": 320, "sub.rho": 3})
+    r = harness.run_simulation(sim, tables=tables, tau_by_layer=taus)
+    m = r.metrics
+    got = np.array([m.tokens_per_s, m.stall_ms, m.compute_ms, m.hits, m.misses_ondemand, m.misses_substituted,
+                    m.drops, m.prefetch_issued, m.prefetch_completed, m.evictions, m.read_bytes, m.substitutions,
+                    m.gate_token_forbidden, m.gate_batch_bypassed])
+    assert np.array_equal(got, g["buddy_metrics"][:14]), (got, g["buddy_metrics"][:14])
+    assert len(r.events) == len(g["buddy_events"])
