@@ -29,4 +29,22 @@ if __name__ == "__main__":
                            partition_of=torch.from_numpy((np.arange(E) * 3 // E).astype(np.int32)).cuda(),
                            logits=torch.randn(B, E, dtype=torch.float64).cuda())
     torch.cuda.synchronize()
+    # fused decode FFN with many split tiles (n_tile 16, 148 CTAs over a small
+    # problem) and the multi-kernel path on the same inputs: bitwise equal
+    E2, d, f, B2 = 8, 512, 1024, 40
+    tk = np.stack([rng.choice(E2, 2, replace=False) for _ in range(B2)]).astype(np.int32)
+    perm = ops.permute(torch.from_numpy(tk).cuda(), torch.zeros(B2, 2, dtype=torch.uint8).cuda(), E2)
+    xp = ops.gather_rows(torch.randn(B2, d).cuda(), perm, 1)
+    w = (torch.randn(E2, 3 * d * f).cuda() * 0.03).to(torch.bfloat16)
+    arena = ops.pack_arena_bf16(w, d, f, ops.ACT_SWIGLU)
+    ws = ops.FfnWorkspace(E2, d, f, perm.r_max, 16)
+    bo = torch.arange(E2, dtype=torch.int32).cuda()
+    rows = int(perm.offset[-1])
+    os.environ["BMOE_KPS"] = "2"
+    y1 = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
+    os.environ["BMOE_FUSED"] = "0"
+    y0 = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
+    del os.environ["BMOE_FUSED"], os.environ["BMOE_KPS"]
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
     print("sanitize smoke ok")
