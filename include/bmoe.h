@@ -316,6 +316,9 @@ typedef struct {
     int32_t num_shared; /* always-resident shared experts per layer (DeepSeek-V2-style), outside the budget:
                            host_mirror[l] then holds num_experts + num_shared buffers, the shared ones are
                            uploaded once and added to every token with weight 1 */
+    int32_t fetch_codec; /* 0: host_mirror[l] = raw buffers back to back; 1 (bf16 only): host_mirror[l] is an
+                            exponent-coded layer image (bm_xfer_layer_header + one blob per expert), fetched
+                            piece by piece through a staging ring and rebuilt in HBM by bm_xfer_decode_piece */
 } bm_engine_config;
 
 typedef struct {
@@ -326,6 +329,7 @@ typedef struct {
     double stall_ms;     /* measured: compute stream waiting on expert fetches (CUDA events) */
     double copy_ms;      /* measured: copy-stream time spent in expert H2D copies (CUDA events) */
     int64_t kernel_launches; /* libbmoe kernels launched (graph nodes included) */
+    int64_t wire_bytes;      /* bytes actually moved host -> device for expert fetches (coded or raw) */
 } bm_engine_stats;
 
 /* host_mirror[l]: pinned host memory, num_experts buffers of the arena
@@ -356,6 +360,47 @@ int bm_engine_trace_get(const bm_engine *e, int32_t *layer_host, int32_t *B_host
                         uint8_t *kind_host);
 /* Bytes of device memory held by the engine (arena + workspaces). */
 int64_t bm_engine_device_bytes(const bm_engine *e);
+
+/* ------------------------------------------------ fetch codec (expert transfer)
+ * Lossless exponent coding of bf16 expert buffers for the H2D fetch (no
+ * reference counterpart: the reference's transfer is an analytic cost,
+ * memtier.py:41-58; this only changes how many bytes cross PCIe, never the
+ * bytes that land in HBM). A value keeps its sign+mantissa byte; its exponent
+ * becomes a 3-bit code against a per-2048-value window (7 binades), code 7
+ * escaping to a per-chunk exponent stream. ~11.2 bits per value for
+ * N(0, s) weights. Blobs are split into self-contained pieces of
+ * BM_XFER_PIECE_VALUES values (the fetch pipeline's unit). */
+#define BM_XFER_PIECE_VALUES (8 * 1024 * 1024)
+typedef struct {
+    uint32_t magic;        /* "BXC1" */
+    uint32_t n_pieces;
+    uint64_t n_values;
+    uint32_t piece_values; /* BM_XFER_PIECE_VALUES */
+    uint32_t reserved;
+    uint64_t piece_off[1]; /* [n_pieces + 1] byte offsets from the blob start; the last = blob bytes */
+} bm_xfer_blob_header;
+typedef struct {
+    uint32_t magic; /* "BXP1" */
+    uint32_t n_chunks, n_esc;
+    uint32_t off_planes, off_base, off_escoff, off_esc, bytes; /* from the piece start; low bytes at 32 */
+} bm_xfer_piece_header;
+typedef struct {
+    uint32_t magic; /* "BXL1" */
+    uint32_t count; /* experts in the layer image (num_experts + num_shared) */
+    uint64_t raw_bytes;    /* decoded bytes per expert */
+    uint64_t blob_off[1];  /* [count + 1], 256-byte aligned offsets from the image start */
+} bm_xfer_layer_header;
+/* Upper bound of a blob for n_values (a positive multiple of 2048), -1 otherwise. */
+int64_t bm_xfer_blob_bound(int64_t n_values);
+/* Encode n_values bf16 at src (device) into blob (device, 256-byte aligned,
+ * blob_cap bytes). Synchronises `stream`; *blob_bytes_host = blob size. */
+int bm_xfer_encode(const uint16_t *src, int64_t n_values, uint8_t *blob, int64_t blob_cap, int64_t *blob_bytes_host,
+                   bm_stream_t stream);
+/* Decode a whole blob (device) into dst [n_values] bf16 (device). */
+int bm_xfer_decode(const uint8_t *blob, uint16_t *dst, int64_t n_values, bm_stream_t stream);
+/* Decode one piece (device copy, 256-byte aligned) of n_chunks chunks into
+ * dst (the piece's first value). */
+int bm_xfer_decode_piece(const uint8_t *piece, uint16_t *dst, int64_t n_chunks, bm_stream_t stream);
 
 /* Pinned host allocation of exact size (cudaHostAlloc, portable). */
 int bm_host_alloc(int64_t bytes, void **out);

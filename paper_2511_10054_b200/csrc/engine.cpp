@@ -41,6 +41,18 @@ struct Buffer {
     cudaEvent_t free_ev = nullptr;  // last compute that read it (borrowed per-layer event)
 };
 
+// Staging ring of the coded fetch path: coded pieces land in a slot on the
+// copy stream, a high-priority decode stream rebuilds them into the target
+// HBM buffer; a slot is refilled only after its previous decode finished.
+constexpr int kRingSlots = 4;
+struct Ring {
+    uint8_t *slot[kRingSlots] = {};
+    cudaEvent_t copied[kRingSlots] = {}, decoded[kRingSlots] = {};
+    bool used[kRingSlots] = {};
+    int next = 0;
+    cudaStream_t dec = nullptr;
+};
+
 }  // namespace
 
 struct bm_engine {
@@ -56,6 +68,9 @@ struct bm_engine {
     std::vector<std::vector<uint8_t>> ready_pending;
     std::vector<cudaEvent_t> layer_done;           // [L]
     std::vector<const uint8_t *> host_mirror;
+    bool coded = false;       // host_mirror[l] is an exponent-coded layer image (cfg.fetch_codec)
+    size_t ring_slot_bytes = 0;
+    Ring ring_copy, ring_prefetch;
     const float *gate_w = nullptr, *gate_b = nullptr;
     const int32_t *tbl_ids = nullptr, *tbl_len = nullptr;
     std::vector<double> tau;
@@ -136,23 +151,81 @@ struct bm_engine {
         return BM_OK;
     }
 
+    const bm_xfer_blob_header *blob_of(int l, int e) const {
+        const auto *lh = reinterpret_cast<const bm_xfer_layer_header *>(host_mirror[l]);
+        return reinterpret_cast<const bm_xfer_blob_header *>(host_mirror[l] + lh->blob_off[e]);
+    }
+
+    // Coded transfer of expert e of layer l into dst: each piece is copied
+    // into a ring slot on stream s and decoded on the ring's decode stream.
+    // Returns the wire bytes; the decode stream holds the completion.
+    int enqueue_coded(int l, int e, void *dst, cudaStream_t s, Ring &r, int64_t *wire) {
+        const bm_xfer_blob_header *bh = blob_of(l, e);
+        const uint8_t *blob = reinterpret_cast<const uint8_t *>(bh);
+        *wire = 0;
+        for (uint32_t p = 0; p < bh->n_pieces; ++p) {
+            const int j = r.next;
+            r.next = (r.next + 1) % kRingSlots;
+            if (r.used[j]) ENG_CUDA(cudaStreamWaitEvent(s, r.decoded[j], 0));
+            const size_t sz = (size_t)(bh->piece_off[p + 1] - bh->piece_off[p]);
+            ENG_CUDA(cudaMemcpyAsync(r.slot[j], blob + bh->piece_off[p], sz, cudaMemcpyHostToDevice, s));
+            ENG_CUDA(cudaEventRecord(r.copied[j], s));
+            ENG_CUDA(cudaStreamWaitEvent(r.dec, r.copied[j], 0));
+            const auto *ph = reinterpret_cast<const bm_xfer_piece_header *>(blob + bh->piece_off[p]);
+            ENG_TRY(bm_xfer_decode_piece(r.slot[j], static_cast<uint16_t *>(dst) + (size_t)p * bh->piece_values,
+                                         ph->n_chunks, r.dec));
+            ENG_CUDA(cudaEventRecord(r.decoded[j], r.dec));
+            r.used[j] = true;
+            *wire += (int64_t)sz;
+            ++stats.kernel_launches;
+        }
+        return BM_OK;
+    }
+
     // H2D of expert e of layer l into a fresh buffer on stream s
     int fetch(int l, int e, cudaStream_t s) {
         int b;
         ENG_TRY(alloc_buffer(&b));
-        if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(s, bufs[b].free_ev, 0));
         cudaEvent_t c0, c1;  // copy-engine busy time, for the PCIe roofline
         ENG_CUDA(cudaEventCreate(&c0));
         ENG_CUDA(cudaEventCreate(&c1));
-        ENG_CUDA(cudaEventRecord(c0, s));
-        ENG_CUDA(cudaMemcpyAsync(bufs[b].dev, host_mirror[l] + (size_t)e * buf_bytes, buf_bytes,
-                                 cudaMemcpyHostToDevice, s));
-        ENG_CUDA(cudaEventRecord(c1, s));
+        cudaStream_t done = s;
+        if (coded) {
+            Ring &r = (s == prefetch_stream) ? ring_prefetch : ring_copy;
+            if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(r.dec, bufs[b].free_ev, 0));  // the decode writes it
+            ENG_CUDA(cudaEventRecord(c0, s));
+            int64_t wire = 0;
+            ENG_TRY(enqueue_coded(l, e, bufs[b].dev, s, r, &wire));
+            ENG_CUDA(cudaEventRecord(c1, s));
+            stats.wire_bytes += wire;
+            done = r.dec;
+        } else {
+            if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(s, bufs[b].free_ev, 0));
+            ENG_CUDA(cudaEventRecord(c0, s));
+            ENG_CUDA(cudaMemcpyAsync(bufs[b].dev, host_mirror[l] + (size_t)e * buf_bytes, buf_bytes,
+                                     cudaMemcpyHostToDevice, s));
+            ENG_CUDA(cudaEventRecord(c1, s));
+            stats.wire_bytes += (int64_t)buf_bytes;
+        }
         copy_ev.emplace_back(c0, c1);
-        ENG_CUDA(cudaEventRecord(ready[l][e], s));
+        ENG_CUDA(cudaEventRecord(ready[l][e], done));
         ready_pending[l][e] = 1;
         phys[l][e] = b;
         stats.h2d_bytes += (int64_t)buf_bytes;
+        return BM_OK;
+    }
+
+    // synchronous upload (initial residents, shared experts)
+    int upload(int l, int e, int b) {
+        if (!coded) {
+            ENG_CUDA(cudaMemcpy(bufs[b].dev, host_mirror[l] + (size_t)e * buf_bytes, buf_bytes,
+                                cudaMemcpyHostToDevice));
+            return BM_OK;
+        }
+        int64_t wire = 0;
+        ENG_TRY(enqueue_coded(l, e, bufs[b].dev, copy_stream, ring_copy, &wire));
+        ENG_CUDA(cudaStreamSynchronize(ring_copy.dec));
+        ENG_CUDA(cudaStreamSynchronize(copy_stream));
         return BM_OK;
     }
 
@@ -411,6 +484,14 @@ struct bm_engine {
             if (p) cudaFreeHost(p);
         if (plan_ev) cudaEventDestroy(plan_ev);
         if (cap_stream) cudaStreamDestroy(cap_stream);
+        for (Ring *r : {&ring_copy, &ring_prefetch}) {
+            for (int j = 0; j < kRingSlots; ++j) {
+                if (r->slot[j]) cudaFree(r->slot[j]);
+                if (r->copied[j]) cudaEventDestroy(r->copied[j]);
+                if (r->decoded[j]) cudaEventDestroy(r->decoded[j]);
+            }
+            if (r->dec) cudaStreamDestroy(r->dec);
+        }
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (prefetch_stream) cudaStreamDestroy(prefetch_stream);
         if (cache) bm_cache_destroy(cache);
@@ -450,6 +531,31 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     g->nbufs = L * (g->cap + g->Ssh) + g->S;
     g->host_mirror.resize(L);
     for (int l = 0; l < L; ++l) g->host_mirror[l] = static_cast<const uint8_t *>(host_mirror[l]);
+    g->coded = c->fetch_codec == 1;
+    if (c->fetch_codec != 0 && !(g->coded && !c->fp32_weights)) {
+        bm::set_error("engine: fetch_codec %d unsupported (0 raw, 1 exponent-coded bf16)", c->fetch_codec);
+        return BM_ECONFIG;
+    }
+    if (g->coded) {  // validate every layer image, size the staging ring by the largest piece
+        const int cnt = E + (c->num_shared > 0 ? c->num_shared : 0);
+        for (int l = 0; l < L; ++l) {
+            const auto *lh = reinterpret_cast<const bm_xfer_layer_header *>(g->host_mirror[l]);
+            if (lh->magic != 0x314C5842u || (int)lh->count != cnt || lh->raw_bytes != g->buf_bytes) {
+                bm::set_error("engine: layer %d mirror is not a coded image of %d experts x %zu bytes", l, cnt,
+                              g->buf_bytes);
+                return BM_ECONFIG;
+            }
+            for (int e = 0; e < cnt; ++e) {
+                const bm_xfer_blob_header *bh = g->blob_of(l, e);
+                if (bh->magic != 0x31435842u || bh->n_values * 2 != g->buf_bytes) {
+                    bm::set_error("engine: layer %d expert %d blob is corrupt", l, e);
+                    return BM_ECONFIG;
+                }
+                for (uint32_t p = 0; p < bh->n_pieces; ++p)
+                    g->ring_slot_bytes = std::max<size_t>(g->ring_slot_bytes, bh->piece_off[p + 1] - bh->piece_off[p]);
+            }
+        }
+    }
     g->gate_w = gate_w;
     g->gate_b = gate_b;
     g->tbl_ids = tbl_ids;
@@ -481,6 +587,19 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     if (const char *ev = getenv("BMOE_OVERLAP")) g->overlap_fetch = atoi(ev) != 0;
     ENG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     ENG_CUDA(cudaStreamCreateWithFlags(&g->prefetch_stream, cudaStreamNonBlocking));
+    if (g->coded) {
+        int lo = 0, hi = 0;
+        ENG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        for (Ring *r : {&g->ring_copy, &g->ring_prefetch}) {
+            ENG_CUDA(cudaStreamCreateWithPriority(&r->dec, cudaStreamNonBlocking, hi));
+            for (int j = 0; j < kRingSlots; ++j) {
+                ENG_CUDA(cudaMalloc(&r->slot[j], g->ring_slot_bytes));
+                g->device_bytes += (int64_t)g->ring_slot_bytes;
+                ENG_CUDA(cudaEventCreateWithFlags(&r->copied[j], cudaEventDisableTiming));
+                ENG_CUDA(cudaEventCreateWithFlags(&r->decoded[j], cudaEventDisableTiming));
+            }
+        }
+    }
     // initial residents: synchronous upload
     std::vector<uint8_t> mask(E);
     for (int l = 0; l < L; ++l) {
@@ -489,8 +608,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
             if (!mask[e]) continue;
             int b;
             ENG_TRY(g->alloc_buffer(&b));
-            ENG_CUDA(cudaMemcpy(g->bufs[b].dev, g->host_mirror[l] + (size_t)e * g->buf_bytes, g->buf_bytes,
-                                cudaMemcpyHostToDevice));
+            ENG_TRY(g->upload(l, e, b));
             g->phys[l][e] = b;
         }
     }
@@ -500,8 +618,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
         for (int sx = 0; sx < g->Ssh; ++sx) {
             int b;
             ENG_TRY(g->alloc_buffer(&b));
-            ENG_CUDA(cudaMemcpy(g->bufs[b].dev, g->host_mirror[l] + (size_t)(E + sx) * g->buf_bytes, g->buf_bytes,
-                                cudaMemcpyHostToDevice));
+            ENG_TRY(g->upload(l, E + sx, b));
             g->shared_buf[(size_t)l * g->Ssh + sx] = b;
         }
     // workspaces
@@ -554,6 +671,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     }
     g->prev_counts.assign(L, std::vector<int32_t>(E, 0));
     g->mask_tmp.assign(E, 0);
+    g->stats = bm_engine_stats{};  // the initial uploads are not part of any step
     return BM_OK;
 }
 

@@ -27,6 +27,8 @@ class HostMirror:
     """Pinned host memory holding every expert of one layer in the arena
     layout (cudaHostAlloc of the exact size, not torch's power-of-two pool)."""
 
+    codec = 0  # 0: raw expert buffers back to back; 1: exponent-coded layer image
+
     def __init__(self, nbytes: int):
         ptr = C.c_void_p()
         N.call("bm_host_alloc", int(nbytes), C.byref(ptr))
@@ -55,6 +57,50 @@ def fill_mirror_from_device(mirror: HostMirror, src: torch.Tensor, offset: int =
     s = torch.cuda.current_stream()
     N.call("bm_memcpy", mirror.ptr + offset, src.data_ptr(), n, s.cuda_stream)
     s.synchronize()
+
+
+def coded_mirror_from_device(arena: torch.Tensor) -> HostMirror:
+    """Pinned host layer image of every expert of ``arena`` [count, elems]
+    (bf16, device) in the exponent-coded transfer format: a
+    bm_xfer_layer_header followed by one blob per expert (include/bmoe.h).
+    The engine fetches it piece by piece and rebuilds the exact bf16 bytes
+    in HBM, so fewer bytes cross PCIe per miss."""
+    from . import ops
+    count, elems = arena.shape
+    blobs = [ops.xfer_encode(arena[e]) for e in range(count)]
+    head = 256 * ((24 + 8 * (count + 1) + 255) // 256)
+    offs = [head]
+    for b in blobs:
+        offs.append(offs[-1] + 256 * ((b.numel() + 255) // 256))
+    m = HostMirror(offs[-1])
+    m.codec = 1
+    hdr = np.zeros(head // 8, np.uint64)
+    hdr[0] = np.uint64(0x314C5842 | (count << 32))  # magic "BXL1", count
+    hdr[1] = np.uint64(elems * 2)
+    hdr[2:3 + count] = np.asarray(offs, np.uint64)
+    C.memmove(m.ptr, hdr.ctypes.data, head)
+    s = torch.cuda.current_stream()
+    for b, o in zip(blobs, offs):
+        N.call("bm_memcpy", m.ptr + o, b.data_ptr(), b.numel(), s.cuda_stream)
+    s.synchronize()
+    return m
+
+
+def mirror_expert(mirror: HostMirror, e: int, elems: int, device="cuda") -> torch.Tensor:
+    """Expert e of a layer mirror as a bf16 device tensor [elems] (decoded
+    when the mirror is coded) — for checks and the CPU reference legs."""
+    from . import ops
+    if mirror.codec == 0:
+        raw = mirror.as_tensor(torch.bfloat16)[e * elems:(e + 1) * elems]
+        return raw.to(device)
+    words = (C.c_uint64 * (4 + e)).from_address(mirror.ptr)  # magic|count, raw_bytes, blob_off[...]
+    lo, hi = int(words[2 + e]), int(words[3 + e])
+    blob = torch.empty(hi - lo + 256, dtype=torch.uint8, device=device)
+    off = (-blob.data_ptr()) % 256
+    blob = blob[off:off + hi - lo]
+    s = torch.cuda.current_stream()
+    N.call("bm_memcpy", blob.data_ptr(), mirror.ptr + lo, hi - lo, s.cuda_stream)
+    return ops.xfer_decode(blob, elems)
 
 
 @dataclass
@@ -86,6 +132,7 @@ class EngineSpec:
     pcie_bw_bytes_per_s: float = 4.0e6
     expert_bytes: int | None = None
     num_shared: int = 0
+    fetch_codec: int | None = None  # None: the mirrors' format (HostMirror.codec)
 
     @property
     def buf_elems(self) -> int:
@@ -125,6 +172,7 @@ class DecodeEngine:
             1000.0 * ebytes / spec.pcie_bw_bytes_per_s
         cfg.expert_bytes = ebytes
         cfg.num_shared = int(spec.num_shared)
+        cfg.fetch_codec = int(spec.fetch_codec if spec.fetch_codec is not None else getattr(mirrors[0], "codec", 0))
         L, E = spec.num_layers, spec.num_experts
         ptrs = (C.c_void_p * L)(*[m.ptr for m in mirrors])
         tau = (C.c_double * L)(*[(-1.0 if t is None else float(t)) for t in taus])

@@ -331,3 +331,33 @@ def buddy_rank(pair_matrix64, eps: float, alpha: float, k_max: int) -> DeviceTab
 
 def sm_count() -> int:
     return int(N.lib().bm_device_sm_count())
+
+
+# ------------------------------------------------------------------ fetch codec
+XFER_CHUNK = 2048
+
+
+def xfer_encode(src) -> torch.Tensor:
+    """Lossless exponent coding of a bf16 tensor (numel a multiple of 2048)
+    into a device blob (uint8), the expert-transfer format (bm_xfer_encode)."""
+    _cuda(src, "src", torch.bfloat16)
+    n = src.numel()
+    bound = int(N.lib().bm_xfer_blob_bound(n))
+    if bound < 0:
+        raise InputError(f"xfer_encode: numel {n} must be a positive multiple of {XFER_CHUNK}")
+    blob = torch.empty(bound + 256, dtype=torch.uint8, device=src.device)
+    off = (-blob.data_ptr()) % 256
+    out = blob[off:off + bound]
+    nb = N.C.c_int64()
+    N.call("bm_xfer_encode", src.data_ptr(), n, out.data_ptr(), bound, N.C.byref(nb), _s())
+    return out[: nb.value]
+
+
+def xfer_decode(blob, n_values: int, out=None) -> torch.Tensor:
+    """Decode a blob made by xfer_encode back into n_values bf16 (bit-exact)."""
+    _cuda(blob, "blob", torch.uint8)
+    if blob.data_ptr() % 256:
+        raise InputError("xfer_decode: blob must be 256-byte aligned")
+    out = torch.empty(n_values, dtype=torch.bfloat16, device=blob.device) if out is None else out
+    N.call("bm_xfer_decode", blob.data_ptr(), out.data_ptr(), n_values, _s())
+    return out

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import ops, substrate
-from .engine import DecodeEngine, EngineSpec, HostMirror, fill_mirror_from_device
+from .engine import DecodeEngine, EngineSpec, HostMirror, coded_mirror_from_device, fill_mirror_from_device
 
 SHAPES = {
     # name: (E, k, d, f, cache_rate)
@@ -102,7 +102,9 @@ def _gen_expert(gen, d, f, device):
 def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: int = 0,
           profile_tokens: int = 4096, alpha: float = 0.95, k_max: int | None = None, tau_percentile: float = 15.0,
           clusters: int | None = None, n_tile: int = 64, device: str = "cuda", rho: int | None = 3,
-          log=None) -> Workload:
+          codec: int = 1, log=None) -> Workload:
+    """codec 1 keeps the pinned mirrors exponent-coded (bm_xfer_*: ~0.70 of
+    the bf16 bytes cross PCIe per miss, rebuilt bit-exactly in HBM); 0 raw."""
     import time
     E, k, d, f, rate = SHAPES[name]
     S = SHARED.get(name, 0)
@@ -132,8 +134,11 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
             w = _gen_expert(gen, d, f, device)
             ops.pack_expert_bf16(w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d), w[2 * f * d:].view(d, f),
                                  ops.ACT_SWIGLU, arena[e])
-        m = HostMirror((E + S) * buf_bytes)
-        fill_mirror_from_device(m, arena)
+        if codec:
+            m = coded_mirror_from_device(arena)
+        else:
+            m = HostMirror((E + S) * buf_bytes)
+            fill_mirror_from_device(m, arena)
         mirrors.append(m)
         # ---- profile this layer (full residency) ----
         r = ops.gate_topk(x, gate_w[l], gate_b[l], k)
@@ -158,7 +163,7 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
                                  ops.ACT_SWIGLU, ws)
         x = ops.combine(yp, perm, pr, kd, h_in=x)
         if log:
-            log(f"layer {l}: mirror {buf_bytes * E / 2**30:.2f} GiB, tau {taus[-1]:.4f}, "
+            log(f"layer {l}: mirror {m.nbytes / 2**30:.2f} GiB, tau {taus[-1]:.4f}, "
                 f"mean buddies {mean_len[-1]:.2f}, {time.time() - t0:.1f}s")
     torch.cuda.synchronize()
     del arena, ws
