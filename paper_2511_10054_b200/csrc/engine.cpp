@@ -438,8 +438,10 @@ struct bm_engine {
                 n += 2;
             } else {
                 const int nt = std::min(cfg.n_tile, std::max(16, (int)((B + 15) / 16 * 16)));
-                const char *ev = getenv("BMOE_FUSED");
-                const int per_call = (nt <= 64 && !(ev && atoi(ev) == 0)) ? 1 : 4;
+                // decode width: one fused launch; prefill: GEMM1 + GEMM2 (data-parallel);
+                // the A/B switches restore GEMM + fixup pairs
+                const char *ev = getenv(nt <= 64 ? "BMOE_FUSED" : "BMOE_DP");
+                const int per_call = (ev && atoi(ev) == 0) ? 4 : (nt <= 64 ? 1 : 2);
                 n += 1 + per_call * (fetched ? 2 : 1);  // split_counts + one or two FFN calls
             }
             stats.kernel_launches += n;

@@ -69,6 +69,7 @@ struct GemmParams {
     int num_ctas;             // launched grid (persistent)
     int mode;                 // epilogue: 0 SwiGLU -> H, 1 tanh -> H, 2 plain -> y_perm
     int fuse;                 // finish wholly-owned tiles in the GEMM epilogue (decode-width tiles)
+    int dp;                   // data-parallel tiles (prefill): CTA c owns whole tiles c, c+G, ... (see SegIter)
     uint8_t *h_planes;        // GEMM1 output: bf16 SW128 planes [M/64][h_rmax][64]
     int h_rmax;
     float *y_perm;            // GEMM2 output: fp32 [r_max][M]
@@ -151,6 +152,49 @@ __device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int mtile
 
 __device__ __forceinline__ long long range_start(int c, long long T, int G) { return (long long)c * T / G; }
 
+// A CTA's work as segments (tile, k-steps [st0, st1)).
+//  stream-K (decode): one contiguous range [it0, it1) of the (tile, k-step)
+//    space, so every SM streams an equal share of the weights;
+//  data-parallel (prefill, dp): whole tiles cta, cta+G, ... Tiles are
+//    m-tile major / token-chunk minor, so the CTAs running at the same time
+//    work on the chunks of the same weight m-tiles and read each weight
+//    block from DRAM once (the other chunks hit L2), and every tile is
+//    finished in the GEMM's own epilogue (no partials, no fixup kernel).
+struct SegIter {
+    bool dp;
+    int cta, G, ntiles, spt, seg;
+    long long it, it1;
+    __device__ SegIter(bool dp_, int cta_, int G_, int ntiles_, int spt_, long long it0_, long long it1_)
+        : dp(dp_), cta(cta_), G(G_), ntiles(ntiles_), spt(spt_), seg(0), it(it0_), it1(it1_) {}
+    __device__ __forceinline__ bool next(int &tile, int &st0, int &st1) {
+        if (dp) {
+            tile = cta + (seg++) * G;
+            st0 = 0;
+            st1 = spt;
+            return tile < ntiles;
+        }
+        if (it >= it1) return false;
+        tile = (int)(it / spt);
+        st0 = (int)(it - (long long)tile * spt);
+        st1 = (int)min((long long)spt, it1 - (long long)tile * spt);
+        it = (long long)tile * spt + st1;
+        return true;
+    }
+};
+
+// Expert activation in the bf16 epilogues (its output is rounded to bf16):
+// SwiGLU silu(g)*u with ex2.approx / rcp.approx, tanh with tanh.approx —
+// a few instructions instead of ~40 for expf + IEEE division, which made the
+// wide prefill epilogue ALU-bound. Every bf16 path (fused, fixup, prefill)
+// uses this one function, so they stay bitwise comparable.
+template <int NMAT>
+__device__ __forceinline__ float expert_act(float g, float u) {
+    if (NMAT == 2) return __fdividef(g, 1.0f + __expf(-g)) * u;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(g));
+    return t;
+}
+
 // Finish columns [c0, c0+16) of a tile for this thread's weight row m =
 // mtile*128 + q*32 + lane (g: gate/only accumulator, u: SwiGLU up):
 // mode 2 -> y_perm fp32 (32 lanes write 128 consecutive bytes per column);
@@ -170,7 +214,7 @@ __device__ __forceinline__ void finish16(const GemmParams &p, const TileInfo &ti
     const int gbase = (int)lane & ~7;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        const float hv = NMAT == 2 ? (g[j] / (1.0f + expf(-g[j]))) * u[j] : tanhf(g[j]);
+        const float hv = expert_act<NMAT>(g[j], u[j]);
         const float ov = __shfl_xor_sync(0xffffffffu, hv, 1);
         const __nv_bfloat162 pr2 = (lane & 1) ? __floats2bfloat162_rn(ov, hv) : __floats2bfloat162_rn(hv, ov);
         const uint32_t w = *reinterpret_cast<const uint32_t *>(&pr2);
@@ -202,8 +246,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
 
     if (warp == 0) build_sched_warp(sched, p.count, p.offset, p.E, p.n_tile);
     __syncthreads();
-    const long long T = (long long)total_tiles(sched, mtiles) * steps_per_tile;
-    const int G = (int)min((long long)p.num_ctas, T);
+    const int ntiles = total_tiles(sched, mtiles);
+    const long long T = (long long)ntiles * steps_per_tile;
+    const int G = (int)min((long long)p.num_ctas, p.dp ? (long long)ntiles : T);
     const int cta = blockIdx.x;
     if (cta >= G) return;  // uniform for the whole CTA
     const long long it0 = range_start(cta, T, G), it1 = range_start(cta + 1, T, G);
@@ -242,13 +287,12 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
 
     if (warp == 0 && lane == 0) {
         // ===================== producer =====================
-        const uint64_t pol = ptx::policy_evict_first();  // weights stream through once
+        const uint64_t pol = ptx::policy_evict_first();  // decode: weights stream through once
         int stage = 0;
         uint32_t phase = 0;
-        long long it = it0;
-        while (it < it1) {
-            const int tile = (int)(it / steps_per_tile);
-            const int st_end = (int)min((long long)steps_per_tile, it1 - (long long)tile * steps_per_tile);
+        SegIter w(p.dp, cta, G, ntiles, steps_per_tile, it0, it1);
+        int tile, st_beg, st_end;
+        while (w.next(tile, st_beg, st_end)) {
             const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
             const int buf = p.buf_of_expert[ti.e];
             // the m-tile's blocks are contiguous along k: [mt][kb][NMAT][16 KB]
@@ -256,13 +300,16 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
                                    (long long)ti.mtile * steps_per_tile * kAStage;
             const uint8_t *b_src = p.b_planes + (long long)ti.row0 * 128;
             const uint32_t bbytes = (uint32_t)ti.n * 128u;
-            for (int st = (int)(it - (long long)tile * steps_per_tile); st < st_end; ++st, ++it) {
+            for (int st = st_beg; st < st_end; ++st) {
                 ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1u);
                 const uint32_t sA = base + (uint32_t)stage * stage_bytes;
                 const uint32_t sB = sA + kAStage;
                 const uint32_t fb = full0 + 8 * stage;
                 ptx::mbar_expect_tx(fb, kAStage + (uint32_t)KPS * bbytes);
-                ptx::bulk_load_hint(sA, a_src + (long long)st * kAStage, kAStage, fb, pol);
+                if (p.dp)  // the same weight block is read by the CTAs on the m-tile's other chunks: keep it in L2
+                    ptx::bulk_load(sA, a_src + (long long)st * kAStage, kAStage, fb);
+                else
+                    ptx::bulk_load_hint(sA, a_src + (long long)st * kAStage, kAStage, fb, pol);
 #pragma unroll
                 for (int i = 0; i < KPS; ++i)
                     ptx::bulk_load(sB + i * bsz, b_src + (long long)(st * KPS + i) * p.b_plane_bytes, bbytes, fb);
@@ -282,10 +329,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        long long it = it0;
-        while (it < it1) {
-            const int tile = (int)(it / steps_per_tile);
-            const int st_end = (int)min((long long)steps_per_tile, it1 - (long long)tile * steps_per_tile);
+        SegIter w(p.dp, cta, G, ntiles, steps_per_tile, it0, it1);
+        int tile, st_beg, st_end;
+        while (w.next(tile, st_beg, st_end)) {
             const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
             const uint32_t idesc = ptx::idesc_bf16_f32(kBM, (uint32_t)ti.n);
             ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1u);
@@ -293,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
             const uint32_t d0 = tmem_base + (uint32_t)acc * acc_cols;
             const uint32_t d1 = d0 + (uint32_t)p.n_tile;
             uint32_t accum = 0;
-            for (int st = (int)(it - (long long)tile * steps_per_tile); st < st_end; ++st, ++it) {
+            for (int st = st_beg; st < st_end; ++st) {
                 ptx::mbar_wait(full0 + 8 * stage, phase);
                 ptx::tc_fence_after();
                 const uint64_t a = desc0 + (uint64_t)stage * stage_d;
@@ -331,14 +377,12 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         const int m_local = q * 32 + (int)lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        long long it = it0;
-        while (it < it1) {
-            const int tile = (int)(it / steps_per_tile);
-            const long long tile_end = (long long)(tile + 1) * steps_per_tile;
+        SegIter w(p.dp, cta, G, ntiles, steps_per_tile, it0, it1);
+        int tile, st_beg, st_end;
+        while (w.next(tile, st_beg, st_end)) {
             // this CTA owns the whole tile: finish it here (activation / output),
             // otherwise park an fp32 partial for the deterministic fixup
-            const bool whole = p.fuse && it == (long long)tile * steps_per_tile && tile_end <= it1;
-            it = min(tile_end, it1);
+            const bool whole = p.fuse && st_beg == 0 && st_end == steps_per_tile;
             const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             ptx::tc_fence_after();
@@ -417,7 +461,7 @@ __global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, 
             if (mode == 2) {
                 y_perm[(long long)row * p.M + m] = g;
             } else {
-                const float h = mode == 0 ? (g / (1.0f + expf(-g))) * u : tanhf(g);
+                const float h = mode == 0 ? expert_act<2>(g, u) : expert_act<1>(g, 0.f);
                 // bf16 SW128 image: plane m/64, chunk (m%64)/8 at position chunk ^ (row & 7)
                 __nv_bfloat16 *hp = reinterpret_cast<__nv_bfloat16 *>(h_planes);
                 const int plane = m >> 6, chunk = (m & 63) >> 3;
@@ -971,14 +1015,18 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
     // wait on the longer epilogue, so they use GEMM + fixup kernels.
     int fused = n_tile <= 64 ? 1 : 0;
     if (const char *ev = getenv("BMOE_FUSED")) fused = fused && atoi(ev) != 0;
-    int fuse = n_tile <= 64 ? 1 : 0;
-    if (const char *ev = getenv("BMOE_FUSE")) fuse = atoi(ev);
+    // Wide (prefill) tiles are data-parallel and finished in the GEMM
+    // epilogue: no partials, no fixup kernels (BMOE_DP=0: stream-K + fixups).
+    int dp = n_tile > 64 ? 1 : 0;
+    if (const char *ev = getenv("BMOE_DP")) dp = dp && atoi(ev) != 0;
+    int fuse = (n_tile <= 64 || dp) ? 1 : 0;
+    if (const char *ev = getenv("BMOE_FUSE")) fuse = dp ? 1 : atoi(ev);
     GemmParams g1{expert_count, expert_offset, buf_of_expert, (int)E, (int)f, (int)d, nmat1, (int)n_tile,
                   kps_for(nmat1, d, n_tile), arena, buf_bytes, 0, static_cast<const uint8_t *>(x_perm),
-                  r_max * 128, partials, G, act == BM_ACT_SWIGLU ? 0 : 1, fuse, h_planes, (int)r_max, nullptr};
+                  r_max * 128, partials, G, act == BM_ACT_SWIGLU ? 0 : 1, fuse, dp, h_planes, (int)r_max, nullptr};
     GemmParams g2{expert_count, expert_offset, buf_of_expert, (int)E, (int)d, (int)f, 1, (int)n_tile,
                   kps_for(1, f, n_tile), arena, buf_bytes, (long long)nmat1 * f * d * 2, h_planes, r_max * 128,
-                  partials, G, 2, fuse, nullptr, 0, y_perm};
+                  partials, G, 2, fuse, dp, nullptr, 0, y_perm};
 
     const bool timing = g_timing.enabled;
     std::lock_guard<std::mutex> lk(g_timing.mu);
@@ -988,6 +1036,7 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
         g1.kps = k1;
         g2.kps = k2;
         g1.fuse = g2.fuse = 1;
+        g1.dp = g2.dp = 0;
         int pre = 1;
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap, reinterpret_cast<unsigned *>(counters + 2 * wl.tile_cap),
@@ -1006,6 +1055,12 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
     if (timing && record_event(s)) return BM_ECUDA;
     if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
     if (timing && record_event(s)) return BM_ECUDA;
+    if (dp) {  // every tile was finished by its GEMM epilogue
+        if (timing && record_event(s)) return BM_ECUDA;
+        if (int rc = launch_gemm_dispatch(g2, G, s)) return rc;
+        if (timing && record_event(s)) return BM_ECUDA;
+        return BM_OK;
+    }
     const int fix_blocks = 4 * G;
     ffn_fixup_kernel<<<fix_blocks, kBM, 0, s>>>(g1, act == BM_ACT_SWIGLU ? 0 : 1, reinterpret_cast<uint4 *>(h_planes),
                                                 (int)r_max, nullptr);

@@ -122,7 +122,7 @@ class EngineSpec:
     temperature: float = 1.0
     gamma: float | None = None
     prefetch: bool = True
-    n_tile: int = 64
+    n_tile: int = 128  # widest token tile; decode batches use min(B rounded to 16, n_tile)
     fp32_weights: bool = False
     staging: int = 0
     load_ms: float = 9.5

@@ -101,7 +101,7 @@ def _gen_expert(gen, d, f, device):
 
 def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: int = 0,
           profile_tokens: int = 4096, alpha: float = 0.95, k_max: int | None = None, tau_percentile: float = 15.0,
-          clusters: int | None = None, n_tile: int = 64, device: str = "cuda", rho: int | None = 3,
+          clusters: int | None = None, n_tile: int = 128, device: str = "cuda", rho: int | None = 3,
           codec: int = 1, log=None) -> Workload:
     """codec 1 keeps the pinned mirrors exponent-coded (bm_xfer_*: ~0.70 of
     the bf16 bytes cross PCIe per miss, rebuilt bit-exactly in HBM); 0 raw."""

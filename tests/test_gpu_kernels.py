@@ -314,6 +314,9 @@ def _bf16_case(rng, E, d, f, B, k, act, n_tile=64, bufs=None, drop=0.1):
     (64, 2048, 1408, 16, 6, ops.ACT_SWIGLU, 32),  # DSV2-shaped, narrow n tile
     (4, 256, 512, 200, 2, ops.ACT_SWIGLU, 64),    # many tokens per expert: N chunking
     (4, 256, 512, 200, 2, ops.ACT_SWIGLU, 256),   # widest tile, single TMEM stage
+    (8, 4096, 14336, 600, 2, ops.ACT_SWIGLU, 256),  # Mixtral prefill: data-parallel tiles, epilogue-finished
+    (128, 2048, 768, 1024, 8, ops.ACT_SWIGLU, 128),  # Qwen3 prefill, double-buffered accumulator
+    (8, 128, 256, 300, 2, ops.ACT_TANH, 128),     # the reference expert, prefill width
 ])
 def test_bf16_tcgen05_ffn_vs_fp32_reference(cuda_ok, E, d, f, B, k, act, n_tile):
     """K4 bf16 tensor-core grouped FFN: rel 2e-2 (normwise per token) vs fp32."""

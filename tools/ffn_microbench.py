@@ -7,7 +7,8 @@ routes `tokens` tokens top-2 over the first `experts-active` experts, and
 times bm_expert_ffn_bf16's two GEMM kernels with CUDA events (the library's
 kernel-timing hook). Each iteration rotates through 4 arena copies so the
 weights are never L2-resident (126 MB L2 vs 1.4 GB per call).
-Prints one JSON line: per-kernel ms, algorithmic GB/s, fraction of measured HBM.
+Prints one JSON line: per-kernel ms, algorithmic GB/s, fraction of measured HBM,
+and (prefill shapes) TFLOP/s of the whole call.
 """
 
 import argparse
@@ -97,8 +98,10 @@ def main():
     out = {"experts": n_exp, "tokens": B, "k": args.k, "n_tile": args.n_tile, "gemm1_ms": g1, "gemm2_ms": g2, "call_ms": call,
            "call_gbs": (b1 + b2) / call / 1e6, "call_frac": (b1 + b2) / call / 1e6 / peak,
            "tflops_pair": (flops1 + flops2) / (g1 + g2) / 1e9,
-           "gemm1_gbs": b1 / g1 / 1e6, "gemm2_gbs": b2 / g2 / 1e6, "pair_gbs": (b1 + b2) / (g1 + g2) / 1e6,
-           "peak_gbs": peak, "gemm1_frac": b1 / g1 / 1e6 / peak, "gemm2_frac": b2 / g2 / 1e6 / peak,
+           "call_tflops": (flops1 + flops2) / call / 1e9,
+           "pair_gbs": (b1 + b2) / (g1 + g2) / 1e6, "peak_gbs": peak,
+           # a decode-width call is one fused kernel: the timing hook reports it as "gemm1" and 0 for gemm2
+           "gemm1_frac": (b1 + (b2 if g2 == 0 else 0)) / g1 / 1e6 / peak, "gemm2_frac": b2 / g2 / 1e6 / peak if g2 else None,
            "env": {k: v for k, v in os.environ.items() if k.startswith("BMOE_")}}
     print(json.dumps(out))
 
