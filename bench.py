@@ -31,16 +31,32 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-D_MODEL, D_FF, N_EXP, TOP_K = 4096, 14336, 8, 2
+# BASELINE.json configs: [1] Mixtral decode (the headline), [2] Qwen3 decode / prefill, [3] DSV2-Lite replicas
+MODELS = {
+    "mixtral": {"workload": "mixtral-8x7b-moe", "model": "Mixtral-8x7B-shaped MoE layers (random init)", "layers": 32},
+    "qwen3": {"workload": "qwen3-30b-a3b-moe", "model": "Qwen3-30B-A3B-shaped MoE layers (random init)", "layers": 48},
+    "dsv2lite": {"workload": "deepseek-v2-lite-moe",
+                 "model": "DeepSeek-V2-Lite-shaped MoE layers, 64 routed + 2 shared experts (random init)",
+                 "layers": 26},
+}
 
 
-def _peaks():
+def _shape(model: str):
+    from paper_2511_10054_b200.workload import SHAPES, SHARED
+    E, k, d, f, rate = SHAPES[model]
+    return E, k, d, f, rate, SHARED.get(model, 0)
+
+
+def _peaks(kind: str = "hbm"):
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written), else the
+    profiling guide's fallback (6.65 TB/s, 1.59 PFLOP/s burst)."""
+    key = {"hbm": "hbm_gbs", "tensor": "bf16_tflops"}[kind]
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p[key]), "measured"
     except Exception:
-        return 6650.0, "fallback"
+        return (6650.0 if kind == "hbm" else 1590.0), "fallback"
 
 
 class ClockSampler:
@@ -121,11 +137,14 @@ def _allmax(v: float, ws: int):
     return float(t.item())
 
 
-def _layers_for_host(ws: int, requested: int | None, codec: int = 1) -> int:
+def _layers_for_host(ws: int, requested: int | None, codec: int = 1, model: str = "mixtral") -> int:
+    """The model's layer count when the pinned mirrors of every replica fit
+    in 60% of host RAM, fewer otherwise (config.layers says which)."""
     from paper_2511_10054_b200.workload import host_mem_available
-    per_layer = N_EXP * 3 * D_MODEL * D_FF * 2 * (0.72 if codec else 1.0)
+    E, _, d, f, _, S = _shape(model)
+    per_layer = (E + S) * 3 * d * f * 2 * (0.72 if codec else 1.0)
     fit = int(0.6 * host_mem_available() / (ws * per_layer))
-    L = min(32, max(1, fit))
+    L = min(MODELS[model]["layers"], max(1, fit))
     return min(L, requested) if requested else L
 
 
@@ -134,7 +153,7 @@ def stage_layer_f64(wl, layer: int):
     """The reference holds float64 expert stacks (model.py:173-186); convert
     one layer's bf16 mirror once, outside any timed region."""
     from paper_2511_10054_b200.engine import mirror_expert
-    E, d, f = N_EXP, D_MODEL, D_FF
+    E, d, f = wl.eng.num_experts + wl.eng.num_shared, wl.eng.d, wl.eng.f
     out = {}
     for e in range(E):
         m = mirror_expert(wl.mirrors[layer], e, 3 * d * f).view(3, -1).float().cpu().numpy().astype(np.float64)
@@ -150,7 +169,7 @@ def cpu_reference_sample(wl, layer: int, B: int, seed: int, stacks, method: str 
     gating.py:148-165, substitution.py:193-208). Returns seconds."""
     import oracle as O
     from paper_2511_10054_b200.workload import initial_residents
-    E, k = N_EXP, TOP_K
+    E, k, S = wl.eng.num_experts, wl.eng.top_k, wl.eng.num_shared
     x = wl.tokens(seed, B).astype(np.float64)
     gw = wl.gate_w[layer].double().cpu().numpy()
     gb = wl.gate_b[layer].double().cpu().numpy()
@@ -167,6 +186,8 @@ def cpu_reference_sample(wl, layer: int, B: int, seed: int, stacks, method: str 
     else:
         ex, kd, _ = O.ondemand_plan(topk, mask)
     y = O.forward(x, ex, kd, probs, lambda e, xr: O.ffn_swiglu(xr, *stacks[e]))
+    for sx in range(S):  # shared experts: every token, weight 1
+        y = y + O.ffn_swiglu(x, *stacks[E + sx])
     O.layer_update(x, y)
     return time.perf_counter() - t0
 
@@ -178,10 +199,10 @@ def run_reference(args, ws, rank):
         return
     import torch
     from paper_2511_10054_b200 import workload as W
-    L = _layers_for_host(ws, args.layers, args.codec)
+    L = _layers_for_host(ws, args.layers, args.codec, args.model)
     # one layer's weights/tables suffice: the sample is one layer-step, the
     # metric extrapolates to the same L layers as the GPU arm
-    wl = W.build("mixtral", layers=1, max_batch=args.batch, profile_tokens=args.profile_tokens)
+    wl = W.build(args.model, layers=1, max_batch=args.batch, profile_tokens=args.profile_tokens)
     cores = len(os.sched_getaffinity(0))
     Bs = args.cpu_tokens
     stacks = stage_layer_f64(wl, 0)
@@ -192,11 +213,11 @@ def run_reference(args, ws, rank):
             times.append(sec)
     per_layer = statistics.mean(times)
     tps = Bs / (per_layer * L)
-    line = {"impl": "reference", "metric": "MoE decode tokens/sec at fixed expert-cache budget",
+    line = {"impl": "reference", "metric": _metric(args.batch),
             "value": tps, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": per_layer * L * 1000.0, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config(L, args.batch, "buddy"),
+            "config": _config(args.model, wl, L, args.batch, "buddy"),
             "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": f"{Bs} tokens x 1 layer per step (f64 numpy oracle, BLAS threads={cores}), "
                                        f"extrapolated x{L} layers"},
@@ -205,12 +226,23 @@ def run_reference(args, ws, rank):
     wl.close()
 
 
-def _config(L, B, method):
-    return {"workload": "mixtral-8x7b-moe-decode", "model": "Mixtral-8x7B-shaped MoE layers (random init)",
-            "layers": L, "experts": N_EXP, "top_k": TOP_K, "d_model": D_MODEL, "d_ff": D_FF, "cache_rate": 0.5,
-            "capacity_per_layer": N_EXP // 2, "global_batch": B, "seq_len": 1, "method": method, "rho": 3,
-            "search_rank_h": N_EXP - 1, "alpha": 0.95, "tau_percentile": 15, "policy": "lru",
-            "parallelism": "replicas", "l2": "inputs larger than L2 (1.4 GB of expert weights per layer-step)"}
+def _metric(B: int) -> str:
+    phase = "decode" if B <= 64 else "prefill"
+    return f"MoE {phase} tokens/sec at fixed expert-cache budget; expert-miss stall (ms)"
+
+
+def _config(model, wl, L, B, method):
+    E, k, d, f, rate, S = _shape(model)
+    phase = "decode" if B <= 64 else "prefill"
+    cfg = {"workload": f"{MODELS[model]['workload']}-{phase}", "model": MODELS[model]["model"],
+           "layers": L, "experts": E, "top_k": k, "d_model": d, "d_ff": f, "cache_rate": rate,
+           "capacity_per_layer": wl.eng.capacity, "global_batch": B, "seq_len": 1, "method": method, "rho": 3,
+           "search_rank_h": wl.eng.search_rank_h, "alpha": 0.95, "tau_percentile": 15, "policy": "lru",
+           "parallelism": "replicas",
+           "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
+    if S:
+        cfg["shared_experts"] = S
+    return cfg
 
 
 def gen_trace(N: int, E: int, k: int, start: int, end: int, device: str, seed: int = 11):
@@ -354,7 +386,10 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=2)
     ap.add_argument("--no-original", action="store_true", help="skip the without-buddy run")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="decode", choices=["decode", "profile"])
+    ap.add_argument("--workload", default="decode", choices=["decode", "profile"],
+                    help="decode: the offloaded MoE step (a batch > 64 tokens is a prefill chunk); "
+                         "profile: co-activation profiling sweep (configs[4])")
+    ap.add_argument("--model", default="mixtral", choices=sorted(MODELS))
     ap.add_argument("--trace-tokens", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--codec", type=int, default=1, choices=[0, 1],
                     help="1: exponent-coded pinned mirrors (lossless, fewer PCIe bytes per miss); 0: raw bf16")
@@ -379,10 +414,11 @@ def main():
     from paper_2511_10054_b200 import _native as N
     from paper_2511_10054_b200 import workload as W
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
-    L = _layers_for_host(ws, args.layers, args.codec)
+    L = _layers_for_host(ws, args.layers, args.codec, args.model)
     B, K, Wm = args.batch, args.steps, args.warmup
+    E, k_top, d, f, rate, S = _shape(args.model)
     t0 = time.time()
-    wl = W.build("mixtral", layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=rank, codec=args.codec)
+    wl = W.build(args.model, layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=rank, codec=args.codec)
     log(f"built {L} layers in {time.time() - t0:.1f}s (mean buddies {wl.mean_buddies:.2f})")
     n_steps_total = Wm + 3 * K
     x_host = torch.from_numpy(wl.tokens(2 + rank, n_steps_total * B)).pin_memory()
@@ -412,33 +448,45 @@ def main():
     N.lib().bm_set_kernel_timing(0)
     g1 = buf[0:n:2]
     g2 = buf[1:n:2]
-    # Σ algorithmic bytes over the pass / Σ FFN kernel time. A layer-step
-    # with misses issues two grouped-FFN calls (resident experts overlapped
-    # with the fetch, then the fetched ones). Decode-width calls are ONE
-    # fused kernel (GEMM1 -> SwiGLU -> GEMM2; the timing hook then reports
-    # an empty second interval), so the dominant kernel's bytes are the whole
-    # expert: W1+W3+W2 plus the activations it reads.
     launches = max(len(g1), 1)
     fused = bool(len(g2)) and float(np.max(g2)) == 0.0  # the timing hook reports 0 for one-kernel calls
-    tot_g1 = st_k["ffn_experts"] * 2 * D_MODEL * D_FF * 2 + st_k["ffn_rows"] * D_MODEL * 2  # W1+W3 + X
-    tot_g2 = st_k["ffn_experts"] * D_FF * D_MODEL * 2 + st_k["ffn_rows"] * D_FF * 2        # W2 + H
-    tot_k = tot_g1 + tot_g2 if fused else tot_g1
     n_exp = st_k["ffn_experts"] / launches
     rows = st_k["ffn_rows"] / launches
-    peak, peak_kind = _peaks()
     g1_ms, g2_ms = float(np.mean(g1)), float(np.mean(g2))
-    ach = tot_k / (float(np.sum(g1)) / 1e3) / 1e9
-    ach_pair = (tot_g1 + tot_g2) / (float(np.sum(g1) + np.sum(g2)) / 1e3) / 1e9
-    traffic = None  # DRAM bytes of one captured launch (ncu --set full), committed under profiles/
-    try:
-        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")))
-        l0 = tr["launches"][0]
-        traffic = {"dram_bytes": l0["dram_read_bytes"] + l0["dram_write_bytes"], "experts": l0["experts"],
-                   "weight_bytes": l0["weight_bytes"], "source": tr["source"]}
-    except (OSError, KeyError, ValueError):
-        pass
-    kname = ("ffn_fused_kernel (one cooperative launch: W1|W3 swap-AB GEMM -> SwiGLU -> W2 GEMM, stream-K)"
-             if fused else "ffn_gemm_kernel (GEMM1: W1|W3 swap-AB, stream-K)")
+    if fused:
+        # Decode: Σ algorithmic bytes over the pass / Σ FFN kernel time. A
+        # layer-step with misses issues two grouped-FFN calls (resident
+        # experts overlapped with the fetch, then the fetched ones), each ONE
+        # fused kernel (GEMM1 -> SwiGLU -> GEMM2), so the dominant kernel's
+        # bytes are the whole expert (W1+W3+W2) plus the activations it reads.
+        tot_k = st_k["ffn_experts"] * 3 * d * f * 2 + st_k["ffn_rows"] * (d + f) * 2
+        peak, peak_kind = _peaks("hbm")
+        ach = tot_k / (float(np.sum(g1)) / 1e3) / 1e9
+        traffic = None  # DRAM bytes of one captured launch (ncu --set full), committed under profiles/
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+            l0 = tr["launches"][0]
+            if args.model == "mixtral":
+                traffic = {"dram_bytes": l0["dram_read_bytes"] + l0["dram_write_bytes"], "experts": l0["experts"],
+                           "weight_bytes": l0["weight_bytes"], "source": tr["source"]}
+        except (OSError, KeyError, ValueError):
+            pass
+        roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": traffic,
+                    "kernel": "ffn_fused_kernel (one cooperative launch: W1|W3 swap-AB GEMM -> SwiGLU -> W2 GEMM, "
+                              "stream-K)",
+                    "algorithmic_bytes_per_launch": tot_k / launches, "avg_launch_ms": g1_ms, "peak_kind": peak_kind,
+                    "experts_per_launch": n_exp, "rows_per_launch": rows}
+    else:
+        # Prefill: Σ 6·d·f flops per executed (token, slot) row over Σ GEMM1 + GEMM2 kernel time
+        flops = 6.0 * d * f * st_k["ffn_rows"]
+        peak, peak_kind = _peaks("tensor")
+        ach = flops / (float(np.sum(g1) + np.sum(g2)) / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": None,
+                    "kernel": "ffn_gemm_kernel x2 (data-parallel tcgen05 tiles, SwiGLU / output in the epilogue)",
+                    "flops_per_call": flops / launches, "avg_gemm1_ms": g1_ms, "avg_gemm2_ms": g2_ms,
+                    "peak_kind": peak_kind + " (burst)", "experts_per_launch": n_exp, "rows_per_launch": rows}
 
     # ---------------- fetch roofline: measured pinned H2D copy rate ----------------
     h2d_peak = measure_h2d(wl)
@@ -455,7 +503,7 @@ def main():
     _timed(eng, x_dev.clone(), B, Wm, 0, torch)
     eng.stats(reset=True)
     out_host = torch.empty_like(x_host)
-    h = torch.empty(B, D_MODEL, device="cuda")
+    h = torch.empty(B, d, device="cuda")
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -493,19 +541,20 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         stacks = stage_layer_f64(wl, 0)
-        times = [cpu_reference_sample(wl, 0, args.cpu_tokens, 5000 + i, stacks) for i in range(2)]
+        times = [cpu_reference_sample(wl, 0, min(args.cpu_tokens, B), 5000 + i, stacks) for i in range(2)]
         del stacks
         per_layer = min(times)
-        cpu = {"value": args.cpu_tokens / (per_layer * L), "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)),
-               "kind": "port", "sample": f"{args.cpu_tokens} tokens x 1 layer-step (route, gates, remap, f64 forward, "
+        nb = min(args.cpu_tokens, B)
+        cpu = {"value": nb / (per_layer * L), "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)),
+               "kind": "port", "sample": f"{nb} tokens x 1 layer-step (route, gates, remap, f64 forward, "
                                          f"layer_update) via the numpy oracle, best of 2, extrapolated x{L} layers"}
 
     line = {
-        "metric": "MoE decode tokens/sec at fixed expert-cache budget; expert-miss stall (ms)",
+        "metric": _metric(B),
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": Wm,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init bf16 weights, reference-style clustered router/token stream)",
-        "config": _config(L, B, "buddy"),
+        "config": _config(args.model, wl, L, B, "buddy"),
         "stall_ms_per_step": st["stall_ms"] / K,
         "sim_stall_model": {"ondemand_misses_per_step": st["ondemand_misses"] / K,
                             "substitutions_per_step": st["substitutions"] / K},
@@ -514,19 +563,15 @@ def main():
         "wire_gb_per_step": st["wire_bytes"] / K / 1e9,
         "fetch_codec": "exponent-coded bf16 (lossless, bm_xfer)" if args.codec else "raw bf16",
         "without_buddy": orig,
-        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": traffic, "kernel": kname,
-                     "algorithmic_bytes_per_launch": tot_k / launches, "avg_launch_ms": g1_ms,
-                     "gemm2_avg_launch_ms": g2_ms, "pair_achieved_gbs": ach_pair, "peak_kind": peak_kind,
-                     "experts_per_launch": n_exp, "rows_per_launch": rows},
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "fetch_roofline": {"bound": "pcie", "achieved": fetch_gbs, "peak": h2d_peak, "unit": "GB/s",
                            "frac": (fetch_gbs / h2d_peak) if fetch_gbs else None, "effective_gbs": fetch_eff,
                            "note": "H2D wire bytes / copy-engine busy time (CUDA events around each fetch) vs "
                                    "the best pinned copy rate of 4 expert-sized copies back to back; effective_gbs = "
                                    "decoded expert bytes over the same time"},
-        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": B * D_MODEL * 4,
-                "d2h_bytes_per_step": B * D_MODEL * 4, "ms_per_step": e2e_ms / K,
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": B * d * 4,
+                "d2h_bytes_per_step": B * d * 4, "ms_per_step": e2e_ms / K,
                 "physical_fetches_per_step": st_e["physical_fetches"] / K,
                 "note": "fresh engine, same warm-up and the same K batches as `value`; pinned host in/out per step"},
         "gpu_launches": int(st["kernel_launches"]),

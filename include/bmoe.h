@@ -319,6 +319,8 @@ typedef struct {
     int32_t fetch_codec; /* 0: host_mirror[l] = raw buffers back to back; 1 (bf16 only): host_mirror[l] is an
                             exponent-coded layer image (bm_xfer_layer_header + one blob per expert), fetched
                             piece by piece through a staging ring and rebuilt in HBM by bm_xfer_decode_piece */
+    double pcie_budget_bytes; /* >= 0: adaptive distribution-gate beta (gating.BetaController, gating.py:189-221,
+                                 gate.pcie_budget_bytes config.py:94) starting at `beta`; < 0: fixed beta */
 } bm_engine_config;
 
 typedef struct {
@@ -330,6 +332,7 @@ typedef struct {
     double copy_ms;      /* measured: copy-stream time spent in expert H2D copies (CUDA events) */
     int64_t kernel_launches; /* libbmoe kernels launched (graph nodes included) */
     int64_t wire_bytes;      /* bytes actually moved host -> device for expert fetches (coded or raw) */
+    double beta;             /* the distribution-gate beta in force (adaptive when pcie_budget_bytes >= 0) */
 } bm_engine_stats;
 
 /* host_mirror[l]: pinned host memory, num_experts buffers of the arena

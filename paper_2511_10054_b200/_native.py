@@ -34,7 +34,8 @@ class EngineConfig(C.Structure):
                 ("n_tile", C.c_int32), ("fp32_weights", C.c_int32), ("rho", C.c_int64), ("beta", C.c_double),
                 ("temperature", C.c_double), ("gamma", C.c_double), ("load_ms", C.c_double),
                 ("hit_ms", C.c_double), ("compute_ms", C.c_double), ("prefetch_ms", C.c_double),
-                ("expert_bytes", C.c_int64), ("num_shared", C.c_int32), ("fetch_codec", C.c_int32)]
+                ("expert_bytes", C.c_int64), ("num_shared", C.c_int32), ("fetch_codec", C.c_int32),
+                ("pcie_budget_bytes", C.c_double)]
 
 
 class EngineStats(C.Structure):
@@ -43,7 +44,8 @@ class EngineStats(C.Structure):
                 ("prefetch_copies", C.c_int64), ("h2d_bytes", C.c_int64), ("gate_forbidden", C.c_int64),
                 ("batch_bypassed", C.c_int64), ("ffn_calls", C.c_int64), ("ffn_experts", C.c_int64),
                 ("ffn_rows", C.c_int64), ("sim_now_ms", C.c_double), ("stall_ms", C.c_double),
-                ("copy_ms", C.c_double), ("kernel_launches", C.c_int64), ("wire_bytes", C.c_int64)]
+                ("copy_ms", C.c_double), ("kernel_launches", C.c_int64), ("wire_bytes", C.c_int64),
+                ("beta", C.c_double)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

@@ -18,6 +18,13 @@
 
 namespace bm {
 void set_error(const char *fmt, ...);
+int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const void *logits, int32_t logits_f64,
+                     int64_t B, int64_t k, int64_t E, const uint32_t *resident_bitmap, const int32_t *tbl_ids,
+                     const double *tbl_w, const int32_t *tbl_len, int64_t tbl_stride, int64_t H, int64_t rho,
+                     int32_t fallback, int32_t method, double beta, const double *beta_dev, double eta, double kappa,
+                     int32_t use_local_logit, const int32_t *partition_of, double hop, int32_t *executed,
+                     uint8_t *kind, int32_t *used, double *delta_out, uint8_t *batch_allowed_out,
+                     bm_stream_t stream);
 }
 
 #define ENG_CUDA(expr)                                                                                    \
@@ -35,6 +42,41 @@ void set_error(const char *fmt, ...);
     } while (0)
 
 namespace {
+
+// gating.BetaController (gating.py:168-221): EMA of the would-be misses
+// admitted past the distribution gate at every candidate beta; every
+// `period` records beta := the largest candidate whose estimated admitted
+// volume (nhat * expert_bytes) fits the budget (derive_beta, :173-186), else
+// unchanged. f64 operations in the reference's order (no contraction).
+struct BetaController {
+    double budget = -1.0, expert_bytes = 0.0, beta = 1.0, decay = 0.9;
+    int period = 64;
+    int64_t steps = 0;
+    double grid[11] = {0.0, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0};  // DEFAULT_BETA_GRID (:170)
+    double ema[11] = {};
+    bool on() const { return budget >= 0.0; }
+    void record(double delta, int64_t miss_count) {
+        const double omd = 1.0 - decay;
+        for (int i = 0; i < 11; ++i) {
+            const double admitted = delta < grid[i] ? (double)miss_count : 0.0;
+            volatile double a = decay * ema[i];
+            volatile double b = omd * admitted;
+            ema[i] = a + b;
+        }
+        if (++steps % period == 0) {
+            bool any = false;
+            double best = 0.0;
+            for (int i = 0; i < 11; ++i) {
+                volatile double vol = ema[i] * expert_bytes;
+                if (vol <= budget && (!any || grid[i] > best)) {
+                    best = grid[i];
+                    any = true;
+                }
+            }
+            if (any) beta = best;
+        }
+    }
+};
 
 struct Buffer {
     void *dev = nullptr;
@@ -102,7 +144,9 @@ struct bm_engine {
     float *h_int = nullptr;                       // engine-owned hidden state [max_batch][d]
     uint32_t *bm_dev_all = nullptr, *bm_host_all = nullptr;
     int32_t *bo_dev_all = nullptr, *bo_host_all = nullptr;
-    std::vector<uint32_t *> bm_dev_l, bm_host_l;  // per-layer residency bitmaps
+    std::vector<uint32_t *> bm_dev_l, bm_host_l;  // per-layer residency bitmaps (+ the beta the remap uses)
+    int bm_stride = 0, beta_word = 0;            // u32 words per layer slot; beta (f64) at word beta_word
+    BetaController beta_ctl;
     std::vector<int32_t *> bo_dev_l, bo_host_l;   // per-layer buffer maps (E + shared)
     cudaStream_t cap_stream = nullptr;
     bool use_graphs = true;
@@ -246,15 +290,15 @@ struct bm_engine {
 
     // K1 gate, snapshot upload, K2 remap, packed plan readback
     int enqueue_pre(int l, float *h, int64_t B, cudaStream_t s) {
-        const int words = (E + 31) / 32;
         ENG_TRY(bm_gate_topk(h, gate_w + (size_t)l * E * d, gate_b + (size_t)l * E, B, E, d, k, cfg.temperature,
                              tau[l], cfg.gamma, logits, topk, probs, tae, margin, allowed, s));
-        ENG_CUDA(cudaMemcpyAsync(bm_dev_l[l], bm_host_l[l], words * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        ENG_TRY(bm_buddy_remap(topk, allowed, nullptr, 0, B, k, E, bm_dev_l[l],
-                               tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr, nullptr,
-                               tbl_len ? tbl_len + (size_t)l * E : nullptr, K > 0 ? K : 1, cfg.search_rank_h,
-                               cfg.rho, cfg.fallback, cfg.method, cfg.beta, 0.0, 0.0, 1, nullptr, 1.0, executed,
-                               kind, used, delta, batch_ok, s));
+        ENG_CUDA(cudaMemcpyAsync(bm_dev_l[l], bm_host_l[l], bm_stride * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        ENG_TRY(bm::buddy_remap_impl(topk, allowed, nullptr, 0, B, k, E, bm_dev_l[l],
+                                     tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr, nullptr,
+                                     tbl_len ? tbl_len + (size_t)l * E : nullptr, K > 0 ? K : 1, cfg.search_rank_h,
+                                     cfg.rho, cfg.fallback, cfg.method, cfg.beta,
+                                     reinterpret_cast<const double *>(bm_dev_l[l] + beta_word), 0.0, 0.0, 1, nullptr,
+                                     1.0, executed, kind, used, delta, batch_ok, s));
         ENG_CUDA(cudaMemcpyAsync(plan_host, plan_dev, plan_bytes(B, k), cudaMemcpyDeviceToHost, s));
         return BM_OK;
     }
@@ -352,12 +396,28 @@ struct bm_engine {
         // 3-5. K1 router, snapshot, K2 remap, plan readback (harness.py:331-361)
         const int words = (E + 31) / 32;
         ENG_TRY(bm_cache_snapshot(cache, l, nullptr, bm_host_l[l]));
+        *reinterpret_cast<double *>(bm_host_l[l] + beta_word) = beta_ctl.beta;  // harness.py:336-337
         ENG_TRY(run(g_pre, l, 0, h, B, s, [&](cudaStream_t st) { return enqueue_pre(l, h, B, st); }));
         ENG_CUDA(cudaEventRecord(plan_ev, s));
         ENG_CUDA(cudaEventSynchronize(plan_ev));
         if (cfg.method == BM_METHOD_BUDDY) {
             for (int64_t b = 0; b < B; ++b) stats.gate_forbidden += allowed_h[b] ? 0 : 1;
             stats.batch_bypassed += batch_ok_h[0] ? 0 : 1;
+            if (beta_ctl.on()) {  // controller.record(delta, miss_count) (harness.py:354-357)
+                const uint32_t *bits = bm_host_l[l];
+                auto resident = [&](int e) { return (bits[e >> 5] >> (e & 31)) & 1u; };
+                int64_t miss_slots = 0, miss_unique = 0;
+                std::vector<uint8_t> seen(E, 0);
+                for (int64_t i = 0; i < B * k; ++i) {
+                    const int e = topk_h[i];
+                    if (!resident(e)) {
+                        ++miss_slots;
+                        if (!seen[e]) ++miss_unique;
+                    }
+                    seen[e] = 1;
+                }
+                beta_ctl.record((double)miss_slots / (double)(B * k), miss_unique);  // delta as in K2
+            }
         }
         if (tracing) {
             tr_layer.push_back(l);
@@ -639,15 +699,20 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     ENG_TRY(g->hmalloc(&g->plan_host, pb));
     ENG_TRY(g->dmalloc(&g->h_int, (size_t)Bm * g->d));
     const int words = (E + 31) / 32;
-    ENG_TRY(g->dmalloc(&g->bm_dev_all, (size_t)L * words));
-    ENG_TRY(g->hmalloc(&g->bm_host_all, (size_t)L * words));
+    g->beta_word = (words + 1) & ~1;  // 8-byte aligned f64 after the bitmap
+    g->bm_stride = g->beta_word + 2;
+    ENG_TRY(g->dmalloc(&g->bm_dev_all, (size_t)L * g->bm_stride));
+    ENG_TRY(g->hmalloc(&g->bm_host_all, (size_t)L * g->bm_stride));
+    g->beta_ctl.beta = c->beta;
+    g->beta_ctl.budget = c->pcie_budget_bytes;
+    g->beta_ctl.expert_bytes = (double)c->expert_bytes;
     ENG_TRY(g->dmalloc(&g->bo_dev_all, (size_t)L * 2 * Et));
     ENG_TRY(g->hmalloc(&g->bo_host_all, (size_t)L * 2 * Et));
     ENG_TRY(g->dmalloc(&g->count_a, Et));
     ENG_TRY(g->dmalloc(&g->count_b, Et));
     for (int l = 0; l < L; ++l) {
-        g->bm_dev_l.push_back(g->bm_dev_all + (size_t)l * words);
-        g->bm_host_l.push_back(g->bm_host_all + (size_t)l * words);
+        g->bm_dev_l.push_back(g->bm_dev_all + (size_t)l * g->bm_stride);
+        g->bm_host_l.push_back(g->bm_host_all + (size_t)l * g->bm_stride);
         g->bo_dev_l.push_back(g->bo_dev_all + (size_t)l * 2 * Et);
         g->bo_host_l.push_back(g->bo_host_all + (size_t)l * 2 * Et);
     }
@@ -734,6 +799,7 @@ extern "C" int bm_engine_stats_get(bm_engine *e, bm_engine_stats *out, int32_t r
         (evs == &e->stall_ev ? e->stats.stall_ms : e->stats.copy_ms) += sum;
     }
     ENG_TRY(bm_cache_now(e->cache, &e->stats.sim_now_ms));
+    e->stats.beta = e->beta_ctl.beta;
     *out = e->stats;
     if (reset) e->stats = bm_engine_stats{};
     return BM_OK;

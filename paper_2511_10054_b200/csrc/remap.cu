@@ -41,6 +41,7 @@ struct RemapArgs {
     int32_t *used;
     double *delta_out;
     uint8_t *batch_allowed_out;
+    const double *beta_dev;  // when set, beta is read from device memory (the engine's adaptive beta)
 };
 
 __device__ __forceinline__ bool bit_of(const uint32_t *m, int e) { return (m[e >> 5] >> (e & 31)) & 1u; }
@@ -71,7 +72,8 @@ __global__ void __launch_bounds__(kRemapThreads) remap_kernel(RemapArgs a) {
     int total_miss = 0;
     for (int w = 0; w < kWarps; ++w) total_miss += miss_warp[w];
     const double delta = nreq > 0 ? ddiv((double)total_miss, (double)nreq) : 0.0;
-    const bool batch_ok = !(delta >= a.beta);
+    const double beta = a.beta_dev ? *a.beta_dev : a.beta;
+    const bool batch_ok = !(delta >= beta);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (a.delta_out) *a.delta_out = delta;
         if (a.batch_allowed_out) *a.batch_allowed_out = batch_ok ? 1 : 0;
@@ -200,15 +202,16 @@ __global__ void __launch_bounds__(kRemapThreads) remap_kernel(RemapArgs a) {
 }  // namespace
 }  // namespace bm
 
-using namespace bm;
-
-extern "C" int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed, const void *logits,
-                              int32_t logits_f64, int64_t B, int64_t k, int64_t E, const uint32_t *resident_bitmap,
-                              const int32_t *tbl_ids, const double *tbl_w, const int32_t *tbl_len,
-                              int64_t tbl_stride, int64_t H, int64_t rho, int32_t fallback, int32_t method,
-                              double beta, double eta, double kappa, int32_t use_local_logit,
-                              const int32_t *partition_of, double hop, int32_t *executed, uint8_t *kind,
-                              int32_t *used, double *delta_out, uint8_t *batch_allowed_out, bm_stream_t stream) {
+namespace bm {
+// bm_buddy_remap with an optional device-resident beta (engine.cpp: the
+// adaptive BetaController changes beta between CUDA-graph replays).
+int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const void *logits, int32_t logits_f64,
+                     int64_t B, int64_t k, int64_t E, const uint32_t *resident_bitmap, const int32_t *tbl_ids,
+                     const double *tbl_w, const int32_t *tbl_len, int64_t tbl_stride, int64_t H, int64_t rho,
+                     int32_t fallback, int32_t method, double beta, const double *beta_dev, double eta, double kappa,
+                     int32_t use_local_logit, const int32_t *partition_of, double hop, int32_t *executed,
+                     uint8_t *kind, int32_t *used, double *delta_out, uint8_t *batch_allowed_out,
+                     bm_stream_t stream) {
     BM_REQUIRE(B >= 0 && k >= 1 && k <= kMaxK && E >= 1 && E <= kMaxE, BM_EINVAL,
                "bm_buddy_remap: bad shape B=%lld k=%lld E=%lld", (long long)B, (long long)k, (long long)E);
     BM_REQUIRE(topk && resident_bitmap && executed && kind, BM_EINVAL, "bm_buddy_remap: null pointer");
@@ -226,7 +229,7 @@ extern "C" int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed,
     }
     RemapArgs a{topk, token_allowed, logits, logits_f64, (int)B, (int)k, (int)E, resident_bitmap, tbl_ids,
                 tbl_w, tbl_len, (int)tbl_stride, (int)H, (long long)rho, fallback, method, beta, eta, kappa,
-                use_local_logit, partition_of, hop, executed, kind, used, delta_out, batch_allowed_out};
+                use_local_logit, partition_of, hop, executed, kind, used, delta_out, batch_allowed_out, beta_dev};
     unsigned grid = (unsigned)((B + kWarps - 1) / kWarps);
     if (grid == 0) grid = 1;  // still publish delta for an empty batch
     if (psi && method == BM_METHOD_BUDDY)
@@ -235,6 +238,22 @@ extern "C" int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed,
         remap_kernel<false><<<grid, kRemapThreads, 0, as_stream(stream)>>>(a);
     BM_LAUNCH_CHECK();
     return BM_OK;
+}
+}  // namespace bm
+
+using namespace bm;
+
+extern "C" int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed, const void *logits,
+                              int32_t logits_f64, int64_t B, int64_t k, int64_t E, const uint32_t *resident_bitmap,
+                              const int32_t *tbl_ids, const double *tbl_w, const int32_t *tbl_len,
+                              int64_t tbl_stride, int64_t H, int64_t rho, int32_t fallback, int32_t method,
+                              double beta, double eta, double kappa, int32_t use_local_logit,
+                              const int32_t *partition_of, double hop, int32_t *executed, uint8_t *kind,
+                              int32_t *used, double *delta_out, uint8_t *batch_allowed_out, bm_stream_t stream) {
+    return buddy_remap_impl(topk, token_allowed, logits, logits_f64, B, k, E, resident_bitmap, tbl_ids, tbl_w,
+                            tbl_len, tbl_stride, H, rho, fallback, method, beta, nullptr, eta, kappa,
+                            use_local_logit, partition_of, hop, executed, kind, used, delta_out, batch_allowed_out,
+                            stream);
 }
 
 // ---------------------------------------------------------------- distribution gate alone

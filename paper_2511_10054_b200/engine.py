@@ -133,6 +133,7 @@ class EngineSpec:
     expert_bytes: int | None = None
     num_shared: int = 0
     fetch_codec: int | None = None  # None: the mirrors' format (HostMirror.codec)
+    pcie_budget_bytes: float | None = None  # adaptive beta (gating.BetaController) when set
 
     @property
     def buf_elems(self) -> int:
@@ -172,6 +173,7 @@ class DecodeEngine:
             1000.0 * ebytes / spec.pcie_bw_bytes_per_s
         cfg.expert_bytes = ebytes
         cfg.num_shared = int(spec.num_shared)
+        cfg.pcie_budget_bytes = -1.0 if spec.pcie_budget_bytes is None else float(spec.pcie_budget_bytes)
         cfg.fetch_codec = int(spec.fetch_codec if spec.fetch_codec is not None else getattr(mirrors[0], "codec", 0))
         L, E = spec.num_layers, spec.num_experts
         ptrs = (C.c_void_p * L)(*[m.ptr for m in mirrors])

@@ -36,6 +36,7 @@ DEFAULTS = {
     "stream.seed": 1, "stream.num_tokens": 10000, "stream.batch": 16, "cache.rate": 0.75, "cache.policy": "lru",
     "cost.expert_load_ms": 9.5, "cost.hit_ms": 0.0, "cost.expert_compute_ms": 0.5,
     "cost.pcie_bw_bytes_per_s": 4.0e6, "gate.temperature": 1.0, "gate.beta": 1.0, "gate.margin_gamma": None,
+    "gate.pcie_budget_bytes": None,
     "sub.h": 16, "sub.rho": None, "sub.fallback": "prefetch_original", "prefetch.enabled": True,
     "method": "buddy", "run.seed": 0, "fidelity.readout_classes": 16,
     "stream.warmup_steps": 256, "profile.laplace_eps": 1e-3, "profile.warmup_weight": 0.0,
@@ -179,7 +180,8 @@ def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=Non
                     temperature=c["gate.temperature"], gamma=c["gate.margin_gamma"], prefetch=c["prefetch.enabled"],
                     fp32_weights=True, expert_bytes=2 * spec.hidden_dim * spec.ffn_dim * 8,
                     load_ms=c["cost.expert_load_ms"], hit_ms=c["cost.hit_ms"], compute_ms=c["cost.expert_compute_ms"],
-                    pcie_bw_bytes_per_s=c["cost.pcie_bw_bytes_per_s"])
+                    pcie_bw_bytes_per_s=c["cost.pcie_bw_bytes_per_s"],
+                    pcie_budget_bytes=c["gate.pcie_budget_bytes"] if method == "buddy" else None)
     initial = [memtier.initial_residents(E, cap, c["cache.policy"], c["run.seed"], l) for l in range(L)]
     eng = DecodeEngine(es, mirrors, torch.tensor(gw, dtype=torch.float32, device=dev),
                        torch.tensor(gb, dtype=torch.float32, device=dev), ids, lens, taus, initial)

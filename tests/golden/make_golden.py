@@ -292,6 +292,40 @@ def sim_case() -> dict:
     return out
 
 
+def sim_beta_case() -> dict:
+    """The tiny pipeline's buddy simulation with the adaptive distribution
+    gate (gate.pcie_budget_bytes set -> gating.BetaController,
+    harness.py:293-297, 354-357): 1,280 tokens = 320 gate records, so beta
+    is re-derived 5 times; the budget admits ~1.5 expert misses per record."""
+    cfg = parse_config_text(TINY_SIM)
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        pdir, bdir = os.path.join(td, "p"), os.path.join(td, "b")
+        harness.cmd_profile(cfg, pdir)
+        cfg.set("io.profile_dir", pdir)
+        harness.cmd_build(cfg, bdir)
+        L = cfg["model.layers"]
+        tables = [buddies.load_table(os.path.join(bdir, f"buddies_L{l:02d}.bin")) for l in range(L)]
+        samples = harness.load_tae_samples(os.path.join(pdir, "tae_samples.txt"))
+        taus = [gating.calibrate_tau(samples[l], 15.0) for l in range(L)]
+        for budget in (1.5, 0.5):
+            c = parse_config_text(TINY_SIM)
+            c.set("method", "buddy"); c.set("stream.seed", "2"); c.set("stream.num_tokens", "1280")
+            c.set("sub.rho", "3")
+            ebytes = 2 * 128 * 256 * 8
+            c.set("gate.pcie_budget_bytes", str(budget * ebytes))
+            r = harness.run_simulation(c, tables=tables, tau_by_layer=taus)
+            tag = f"b{int(budget * 10)}"
+            out[f"{tag}_events"] = np.array([(e.time_ms, EV[e.kind], e.layer, e.token, e.expert, e.bytes, e.stall_ms)
+                                             for e in r.events], np.float64).reshape(-1, 7)
+            out[f"{tag}_gates"] = np.array([g[:8] for g in r.gate_records], np.float64).reshape(-1, 8)
+            mt = r.metrics
+            out[f"{tag}_metrics"] = np.array([mt.misses_ondemand, mt.substitutions, mt.gate_token_forbidden,
+                                              mt.gate_batch_bypassed])
+            out[f"{tag}_budget"] = np.float64(budget * ebytes)
+    return out
+
+
 def substrate_case() -> dict:
     """Samples of the reference's synthetic substrate (model.py:122-222,
     350-382) so the framework's restatement can be pinned without storing
@@ -316,6 +350,9 @@ def substrate_case() -> dict:
 
 
 def main() -> None:
+    if sys.argv[1:] == ["beta"]:  # regenerate only the adaptive-beta fixture
+        np.savez_compressed(os.path.join(OUT, "sim_tiny_beta.npz"), **sim_beta_case())
+        return
     np.savez_compressed(os.path.join(OUT, "remap_corpus_20260819.npz"), **remap_corpus(20260819, 1000))
     np.savez_compressed(os.path.join(OUT, "remap_corpus_1234.npz"), **remap_corpus(1234, 300))
     tiny = ModelSpec(num_layers=2, experts_per_layer=8, top_k=2, hidden_dim=128, ffn_dim=256,

@@ -159,3 +159,30 @@ def test_profile_build_pipeline_matches_reference(cuda_ok, tmp_path):
                     m.gate_token_forbidden, m.gate_batch_bypassed])
     assert np.array_equal(got, g["buddy_metrics"][:14]), (got, g["buddy_metrics"][:14])
     assert len(r.events) == len(g["buddy_events"])
+
+
+@pytest.mark.parametrize("tag", ["b15", "b5"])
+def test_adaptive_beta_controller_equals_reference(cuda_ok, tag):
+    """gate.pcie_budget_bytes set: the engine's BetaController replica
+    (gating.py:189-221, fed per layer-step as harness.py:354-357) moves beta
+    exactly like the reference's, so 1,280 tokens of simulation (320 gate
+    records, 5 re-derivations, 141-194 bypassed batches) give the reference's
+    event log and gate counts bit for bit."""
+    from paper_2511_10054_b200 import harness
+    g = golden("sim_tiny.npz")
+    gb = golden("sim_tiny_beta.npz")
+    cfg = {"model.layers": 4, "model.experts": 8, "model.top_k": 2, "model.hidden_dim": 128,
+           "model.ffn_dim": 256, "model.clusters": 8, "stream.batch": 16, "cache.rate": 0.5, "sub.h": 7,
+           "sub.rho": 3, "stream.seed": 2, "stream.num_tokens": 1280, "method": "buddy",
+           "gate.pcie_budget_bytes": float(gb[f"{tag}_budget"])}
+    tables = (np.stack([g[f"ids_L{l}"] for l in range(L)]), np.stack([g[f"lens_L{l}"] for l in range(L)]))
+    r = harness.run_simulation(cfg, tables=tables, tau_by_layer=list(g["taus"]))
+    from paper_2511_10054_b200.memtier import _EV_BY_CODE
+    code = {name: c for c, name in enumerate(_EV_BY_CODE)}
+    ev = np.array([(e.time_ms, code[e.kind], e.layer, e.token, e.expert, e.bytes, e.stall_ms) for e in r.events],
+                  np.float64).reshape(-1, 7)
+    ref = gb[f"{tag}_events"]
+    assert ev.shape == ref.shape and np.array_equal(ev, ref)
+    m = r.metrics
+    assert [m.misses_ondemand, m.substitutions, m.gate_token_forbidden, m.gate_batch_bypassed] == \
+        [int(v) for v in gb[f"{tag}_metrics"]]
