@@ -21,6 +21,7 @@
 //                          base[chunks] | escoff[chunks] u32 | esc[n_esc]
 // Pieces are self-contained so a fetch streams them through a small staging
 // ring: copy piece i+1 while piece i decodes (engine.cpp).
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -164,6 +165,132 @@ __device__ __forceinline__ void decode_chunk(const uint8_t *__restrict__ pb, con
             out[j >> 1] = x;
     }
     *reinterpret_cast<uint4 *>(dst + cl * kChunk + t * 8) = make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+// Warp-granular decoder: a warp owns 256 values (one eighth of a chunk) and
+// derives its escape prefix without a CTA barrier: the escape bits of the
+// chunk's earlier threads are AND-ed from the code-plane words (L1 hits) and
+// popcounted, then a warp scan places its own lanes. No __syncthreads, so
+// the dependent escape loads of one warp overlap the others' streams.
+__device__ __forceinline__ int warp_incl_scan(int x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+__device__ __forceinline__ void decode_unit(const uint8_t *__restrict__ pb, const bm_xfer_piece_header &ph,
+                                            int64_t c, int w, uint16_t *__restrict__ dst) {
+    const int lane = threadIdx.x & 31, t = w * 32 + lane;
+    const uint2 lo = __ldg(reinterpret_cast<const uint2 *>(pb + sizeof(bm_xfer_piece_header) + c * kChunk + t * 8));
+    const uint8_t *planes = pb + ph.off_planes + c * 768;
+    const uint32_t p0 = __ldg(planes + t), p1 = __ldg(planes + 256 + t), p2 = __ldg(planes + 512 + t);
+    const uint32_t *pw = reinterpret_cast<const uint32_t *>(planes);
+    int before = 0;  // escapes of threads 0 .. 32w-1 = plane words 0 .. 8w-1
+    for (int i = lane; i < 8 * w; i += 32) before += __popc(__ldg(pw + i) & __ldg(pw + 64 + i) & __ldg(pw + 128 + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    const int mine = __popc(p0 & p1 & p2);
+    const int pre = before + warp_incl_scan(mine) - mine;
+    const uint32_t base = __ldg(pb + ph.off_base + c);
+    const uint8_t *es = pb + ph.off_esc + __ldg(reinterpret_cast<const uint32_t *>(pb + ph.off_escoff) + c) + pre;
+    uint32_t out[4];
+    int k = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t low = (((j < 4) ? lo.x : lo.y) >> (8 * (j & 3))) & 0xFF;
+        const uint32_t code = ((p0 >> j) & 1u) | (((p1 >> j) & 1u) << 1) | (((p2 >> j) & 1u) << 2);
+        uint32_t e = base + code;
+        if (code == 7) e = __ldg(es + k++);
+        const uint32_t x = ((low & 0x80) << 8) | (e << 7) | (low & 0x7F);
+        if (j & 1)
+            out[j >> 1] |= x << 16;
+        else
+            out[j >> 1] = x;
+    }
+    *reinterpret_cast<uint4 *>(dst + c * kChunk + t * 8) = make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+__global__ void __launch_bounds__(kThreads) xfer_decode_piece_warp_kernel(const uint8_t *__restrict__ piece,
+                                                                          uint16_t *__restrict__ dst) {
+    const bm_xfer_piece_header ph = *reinterpret_cast<const bm_xfer_piece_header *>(piece);
+    const int warps = kThreads / 32;
+    const int64_t units = (int64_t)ph.n_chunks * 8;
+    for (int64_t u = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); u < units; u += (int64_t)gridDim.x * warps)
+        decode_unit(piece, ph, u >> 3, (int)(u & 7), dst);
+}
+
+// Wide decoder (default): a warp owns half a chunk (1024 values), a lane 32
+// consecutive values = one 32-bit word of each code plane. Every lane issues
+// 2 x 16 B (low bytes) + 3 x 4 B (planes) loads up front and writes 64 B, so
+// ~4x more bytes are in flight per thread than with 8 values per thread; the
+// upper half's escape prefix is the popcount of the lower half's plane words.
+__device__ __forceinline__ uint32_t expand_code(uint32_t w0, uint32_t w1, uint32_t w2, int j) {
+    return ((w0 >> j) & 1u) | (((w1 >> j) & 1u) << 1) | (((w2 >> j) & 1u) << 2);
+}
+
+__device__ __forceinline__ void decode_half(const uint8_t *__restrict__ pb, const bm_xfer_piece_header &ph,
+                                            int64_t c, int half, uint16_t *__restrict__ dst) {
+    const int lane = threadIdx.x & 31, wi = half * 32 + lane;  // plane word / 32-value group in the chunk
+    const uint4 *lo_p = reinterpret_cast<const uint4 *>(pb + sizeof(bm_xfer_piece_header) + c * kChunk + wi * 32);
+    const uint4 la = __ldg(lo_p), lb = __ldg(lo_p + 1);
+    const uint32_t *pw = reinterpret_cast<const uint32_t *>(pb + ph.off_planes + c * 768);
+    const uint32_t w0 = __ldg(pw + wi), w1 = __ldg(pw + 64 + wi), w2 = __ldg(pw + 128 + wi);
+    const uint32_t base = __ldg(pb + ph.off_base + c);
+    const uint32_t eo = __ldg(reinterpret_cast<const uint32_t *>(pb + ph.off_escoff) + c);
+    int before = 0;
+    if (half) before = __popc(__ldg(pw + lane) & __ldg(pw + 64 + lane) & __ldg(pw + 128 + lane));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) before += half ? __shfl_xor_sync(0xffffffffu, before, o) : 0;
+    const uint32_t escm = w0 & w1 & w2;
+    const int mine = __popc(escm);
+    const int pre = before + warp_incl_scan(mine) - mine;
+    const uint8_t *es = pb + ph.off_esc + eo + pre;
+    const uint32_t lw[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+    uint32_t out[16];
+    int k = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t low = (lw[j >> 2] >> (8 * (j & 3))) & 0xFF;
+        const uint32_t code = expand_code(w0, w1, w2, j);
+        uint32_t e = base + code;
+        if (code == 7) e = __ldg(es + k++);
+        const uint32_t x = ((low & 0x80) << 8) | (e << 7) | (low & 0x7F);
+        if (j & 1)
+            out[j >> 1] |= x << 16;
+        else
+            out[j >> 1] = x;
+    }
+    uint4 *o = reinterpret_cast<uint4 *>(dst + c * kChunk + wi * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+}
+
+__global__ void __launch_bounds__(kThreads) xfer_decode_piece_wide_kernel(const uint8_t *__restrict__ piece,
+                                                                          uint16_t *__restrict__ dst) {
+    const bm_xfer_piece_header ph = *reinterpret_cast<const bm_xfer_piece_header *>(piece);
+    const int warps = kThreads / 32;
+    const int64_t units = (int64_t)ph.n_chunks * 2;
+    for (int64_t u = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); u < units; u += (int64_t)gridDim.x * warps)
+        decode_half(piece, ph, u >> 1, (int)(u & 1), dst);
+}
+
+__global__ void __launch_bounds__(kThreads) xfer_decode_blob_wide_kernel(const uint8_t *__restrict__ blob,
+                                                                         int64_t n_chunks, uint16_t *__restrict__ dst) {
+    const auto *bh = reinterpret_cast<const bm_xfer_blob_header *>(blob);
+    const int64_t cpp = bh->piece_values / kChunk;
+    const int warps = kThreads / 32;
+    for (int64_t u = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); u < 2 * n_chunks;
+         u += (int64_t)gridDim.x * warps) {
+        const int64_t c = u >> 1;
+        const int p = (int)(c / cpp);
+        const uint8_t *pb = blob + bh->piece_off[p];
+        const bm_xfer_piece_header ph = *reinterpret_cast<const bm_xfer_piece_header *>(pb);
+        decode_half(pb, ph, c - (int64_t)p * cpp, (int)(u & 1), dst + (int64_t)p * bh->piece_values);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) xfer_decode_piece_kernel(const uint8_t *__restrict__ piece,
@@ -316,7 +443,11 @@ extern "C" int bm_xfer_decode(const uint8_t *blob, uint16_t *dst, int64_t n_valu
     BM_REQUIRE(((uintptr_t)dst & 15) == 0 && ((uintptr_t)blob & 255) == 0, BM_EINVAL,
                "bm_xfer_decode: dst must be 16-byte and blob 256-byte aligned");
     const int64_t n_chunks = n_values / kChunk;
-    xfer_decode_blob_kernel<<<grid_for(n_chunks), kThreads, 0, as_stream(stream)>>>(blob, n_chunks, dst);
+    if (const char *ev = getenv("BMOE_XFER_DECODER"); ev && atoi(ev) == 1)
+        xfer_decode_blob_kernel<<<grid_for(n_chunks), kThreads, 0, as_stream(stream)>>>(blob, n_chunks, dst);
+    else
+        xfer_decode_blob_wide_kernel<<<grid_for(n_chunks / 4 + 1), kThreads, 0, as_stream(stream)>>>(blob, n_chunks,
+                                                                                                    dst);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }
@@ -325,7 +456,16 @@ extern "C" int bm_xfer_decode_piece(const uint8_t *piece, uint16_t *dst, int64_t
     BM_REQUIRE(piece && dst && n_chunks > 0, BM_EINVAL, "bm_xfer_decode_piece: bad argument");
     BM_REQUIRE(((uintptr_t)dst & 15) == 0 && ((uintptr_t)piece & 255) == 0, BM_EINVAL,
                "bm_xfer_decode_piece: dst must be 16-byte and piece 256-byte aligned");
-    xfer_decode_piece_kernel<<<grid_for(n_chunks), kThreads, 0, as_stream(stream)>>>(piece, dst);
+    static const int variant = [] {
+        const char *ev = getenv("BMOE_XFER_DECODER");
+        return ev ? atoi(ev) : 3;
+    }();
+    if (variant == 1)
+        xfer_decode_piece_kernel<<<grid_for(n_chunks), kThreads, 0, as_stream(stream)>>>(piece, dst);
+    else if (variant == 2)
+        xfer_decode_piece_warp_kernel<<<grid_for(n_chunks), kThreads, 0, as_stream(stream)>>>(piece, dst);
+    else
+        xfer_decode_piece_wide_kernel<<<grid_for(n_chunks / 4 + 1), kThreads, 0, as_stream(stream)>>>(piece, dst);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }
