@@ -137,15 +137,35 @@ def _allmax(v: float, ws: int):
     return float(t.item())
 
 
-def _layers_for_host(ws: int, requested: int | None, codec: int = 1, model: str = "mixtral") -> int:
-    """The model's layer count when the pinned mirrors of every replica fit
-    in 60% of host RAM, fewer otherwise (config.layers says which)."""
-    from paper_2511_10054_b200.workload import host_mem_available
+def _mirror_bytes_per_layer(model: str, codec: int) -> float:
     E, _, d, f, _, S = _shape(model)
-    per_layer = (E + S) * 3 * d * f * 2 * (0.72 if codec else 1.0)
-    fit = int(0.6 * host_mem_available() / (ws * per_layer))
+    return (E + S) * 3 * d * f * 2 * (0.72 if codec else 1.0)
+
+
+def _layers_for_host(ws: int, requested: int | None, codec: int = 1, model: str = "mixtral") -> int:
+    """The model's layer count when the pinned mirrors (one per replica, or
+    one node-shared copy: ws=1) fit in 60% of host RAM, fewer otherwise
+    (config.layers says which)."""
+    from paper_2511_10054_b200.workload import host_mem_available
+    fit = int(0.6 * host_mem_available() / (ws * _mirror_bytes_per_layer(model, codec)))
     L = min(MODELS[model]["layers"], max(1, fit))
     return min(L, requested) if requested else L
+
+
+def _plan_mirrors(ws: int, local: int, args):
+    """Replicas of one model on one node share ONE expert mirror in /dev/shm
+    (SharedMirror: written by local rank 0, mapped + page-locked by every
+    rank) when it fits there; otherwise every rank keeps a private pinned
+    mirror and the layer count shrinks with the replica count."""
+    from paper_2511_10054_b200.workload import ShareSpec, shm_bytes_free
+    if ws == 1:
+        return _layers_for_host(1, args.layers, args.codec, args.model), None
+    L = _layers_for_host(1, args.layers, args.codec, args.model)
+    if shm_bytes_free() >= 1.05 * L * _mirror_bytes_per_layer(args.model, args.codec):
+        import torch.distributed as dist
+        tag = f"bmoe_{os.environ.get('TORCHELASTIC_RUN_ID', 'run')}_{os.environ.get('MASTER_PORT', '0')}_{args.model}"
+        return L, ShareSpec(tag=tag, owner=(local == 0), barrier=dist.barrier)
+    return _layers_for_host(ws, args.layers, args.codec, args.model), None
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -238,7 +258,7 @@ def _config(model, wl, L, B, method):
            "layers": L, "experts": E, "top_k": k, "d_model": d, "d_ff": f, "cache_rate": rate,
            "capacity_per_layer": wl.eng.capacity, "global_batch": B, "seq_len": 1, "method": method, "rho": 3,
            "search_rank_h": wl.eng.search_rank_h, "alpha": 0.95, "tau_percentile": 15, "policy": "lru",
-           "parallelism": "replicas",
+           "parallelism": "replicas (one process per GPU, disjoint token streams, no collective)",
            "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
     if S:
         cfg["shared_experts"] = S
@@ -414,12 +434,15 @@ def main():
     from paper_2511_10054_b200 import _native as N
     from paper_2511_10054_b200 import workload as W
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
-    L = _layers_for_host(ws, args.layers, args.codec, args.model)
+    L, share = _plan_mirrors(ws, local, args)
     B, K, Wm = args.batch, args.steps, args.warmup
     E, k_top, d, f, rate, S = _shape(args.model)
     t0 = time.time()
-    wl = W.build(args.model, layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=rank, codec=args.codec)
-    log(f"built {L} layers in {time.time() - t0:.1f}s (mean buddies {wl.mean_buddies:.2f})")
+    # replicas serve ONE model (same weights and tables on every rank) over disjoint token streams
+    wl = W.build(args.model, layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=0, codec=args.codec,
+                 share=share)
+    log(f"built {L} layers in {time.time() - t0:.1f}s (mean buddies {wl.mean_buddies:.2f}, "
+        f"mirror {'node-shared' if share else 'private'})")
     n_steps_total = Wm + 3 * K
     x_host = torch.from_numpy(wl.tokens(2 + rank, n_steps_total * B)).pin_memory()
     x_dev = x_host.to("cuda")
@@ -453,20 +476,26 @@ def main():
     n_exp = st_k["ffn_experts"] / launches
     rows = st_k["ffn_rows"] / launches
     g1_ms, g2_ms = float(np.mean(g1)), float(np.mean(g2))
-    if fused:
-        # Decode: Σ algorithmic bytes over the pass / Σ FFN kernel time. A
-        # layer-step with misses issues two grouped-FFN calls (resident
-        # experts overlapped with the fetch, then the fetched ones), each ONE
-        # fused kernel (GEMM1 -> SwiGLU -> GEMM2), so the dominant kernel's
-        # bytes are the whole expert (W1+W3+W2) plus the activations it reads.
-        tot_k = st_k["ffn_experts"] * 3 * d * f * 2 + st_k["ffn_rows"] * (d + f) * 2
-        peak, peak_kind = _peaks("hbm")
-        ach = tot_k / (float(np.sum(g1)) / 1e3) / 1e9
+    # Algorithmic bytes (every executed expert's W1+W3+W2 + the activations
+    # read) and flops (6·d·f per executed row) of the pass; the FFN's bound is
+    # whichever roofline gives the longer ideal time (decode and small-expert
+    # prefill stream weights: HBM; wide prefill tiles: tensor pipe).
+    tot_k = st_k["ffn_experts"] * 3 * d * f * 2 + st_k["ffn_rows"] * (d + f) * 2
+    flops = 6.0 * d * f * st_k["ffn_rows"]
+    hbm_peak, hbm_kind = _peaks("hbm")
+    tc_peak, tc_kind = _peaks("tensor")
+    hbm_bound = tot_k / (hbm_peak * 1e9) >= flops / (tc_peak * 1e12)
+    if fused or hbm_bound:
+        # Decode: Σ bytes / Σ FFN kernel time. A layer-step with misses issues
+        # two grouped-FFN calls (resident experts overlapped with the fetch,
+        # then the fetched ones), each ONE fused kernel at decode width.
+        peak, peak_kind = hbm_peak, hbm_kind
+        ach = tot_k / (float(np.sum(g1) + np.sum(g2)) / 1e3) / 1e9
         traffic = None  # DRAM bytes of one captured launch (ncu --set full), committed under profiles/
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
             l0 = tr["launches"][0]
-            if args.model == "mixtral":
+            if args.model == "mixtral" and fused:
                 traffic = {"dram_bytes": l0["dram_read_bytes"] + l0["dram_write_bytes"], "experts": l0["experts"],
                            "weight_bytes": l0["weight_bytes"], "source": tr["source"]}
         except (OSError, KeyError, ValueError):
@@ -474,13 +503,13 @@ def main():
         roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                     "traffic": traffic,
                     "kernel": "ffn_fused_kernel (one cooperative launch: W1|W3 swap-AB GEMM -> SwiGLU -> W2 GEMM, "
-                              "stream-K)",
+                              "stream-K)" if fused else
+                              "ffn_gemm_kernel x2 (data-parallel tcgen05 tiles, SwiGLU / output in the epilogue)",
                     "algorithmic_bytes_per_launch": tot_k / launches, "avg_launch_ms": g1_ms, "peak_kind": peak_kind,
                     "experts_per_launch": n_exp, "rows_per_launch": rows}
     else:
-        # Prefill: Σ 6·d·f flops per executed (token, slot) row over Σ GEMM1 + GEMM2 kernel time
-        flops = 6.0 * d * f * st_k["ffn_rows"]
-        peak, peak_kind = _peaks("tensor")
+        # Prefill, tensor-bound: Σ 6·d·f flops per executed (token, slot) row over Σ GEMM1 + GEMM2 time
+        peak, peak_kind = tc_peak, tc_kind
         ach = flops / (float(np.sum(g1) + np.sum(g2)) / 1e3) / 1e12
         roofline = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                     "traffic": None,
@@ -554,7 +583,9 @@ def main():
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": Wm,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init bf16 weights, reference-style clustered router/token stream)",
-        "config": _config(args.model, wl, L, B, "buddy"),
+        "config": dict(_config(args.model, wl, L, B, "buddy"),
+                       host_mirror="node-shared /dev/shm" if share else "private pinned",
+                       fetch_codec="exponent-coded bf16" if args.codec else "raw bf16"),
         "stall_ms_per_step": st["stall_ms"] / K,
         "sim_stall_model": {"ondemand_misses_per_step": st["ondemand_misses"] / K,
                             "substitutions_per_step": st["substitutions"] / K},

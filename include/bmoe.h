@@ -408,6 +408,11 @@ int bm_xfer_decode_piece(const uint8_t *piece, uint16_t *dst, int64_t n_chunks, 
 /* Pinned host allocation of exact size (cudaHostAlloc, portable). */
 int bm_host_alloc(int64_t bytes, void **out);
 int bm_host_free(void *p);
+/* Page-lock an existing host mapping for DMA (cudaHostRegister, portable;
+ * read_only != 0 adds cudaHostRegisterReadOnly). Replicas on one node share
+ * one expert mirror this way: a shared-memory file mapped by every rank. */
+int bm_host_register(void *p, int64_t bytes, int32_t read_only);
+int bm_host_unregister(void *p);
 int bm_memcpy(void *dst, const void *src, int64_t bytes, bm_stream_t stream); /* cudaMemcpyAsync default kind */
 
 #ifdef __cplusplus

@@ -63,6 +63,8 @@ _SIGS = {
     "bm_engine_device_bytes": (I64, [P]),
     "bm_host_alloc": (C.c_int, [I64, P]),
     "bm_host_free": (C.c_int, [P]),
+    "bm_host_register": (C.c_int, [P, I64, I32]),
+    "bm_host_unregister": (C.c_int, [P]),
     "bm_memcpy": (C.c_int, [P, P, I64, P]),
     "bm_xfer_blob_bound": (I64, [I64]),
     "bm_xfer_encode": (C.c_int, [P, I64, P, I64, P, P]),

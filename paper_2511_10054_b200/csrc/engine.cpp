@@ -853,6 +853,18 @@ extern "C" int bm_host_alloc(int64_t bytes, void **out) {
     return BM_OK;
 }
 
+extern "C" int bm_host_register(void *p, int64_t bytes, int32_t read_only) {
+    if (!p || bytes <= 0) return BM_EINVAL;
+    unsigned flags = cudaHostRegisterPortable | (read_only ? cudaHostRegisterReadOnly : 0u);
+    ENG_CUDA(cudaHostRegister(p, (size_t)bytes, flags));
+    return BM_OK;
+}
+
+extern "C" int bm_host_unregister(void *p) {
+    if (p) ENG_CUDA(cudaHostUnregister(p));
+    return BM_OK;
+}
+
 extern "C" int bm_host_free(void *p) {
     if (p) ENG_CUDA(cudaFreeHost(p));
     return BM_OK;

@@ -250,19 +250,33 @@ __device__ __forceinline__ void decode_half(const uint8_t *__restrict__ pb, cons
     const int pre = before + warp_incl_scan(mine) - mine;
     const uint8_t *es = pb + ph.off_esc + eo + pre;
     const uint32_t lw[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+    const uint32_t base4 = base * 0x01010101u;
     uint32_t out[16];
     int k = 0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t low = (lw[j >> 2] >> (8 * (j & 3))) & 0xFF;
-        const uint32_t code = expand_code(w0, w1, w2, j);
-        uint32_t e = base + code;
-        if (code == 7) e = __ldg(es + k++);
-        const uint32_t x = ((low & 0x80) << 8) | (e << 7) | (low & 0x7F);
-        if (j & 1)
-            out[j >> 1] |= x << 16;
-        else
-            out[j >> 1] = x;
+    for (int g = 0; g < 8; ++g) {  // 4 values per step, SIMD within a register
+        // the 4 exponents as bytes: bit j of each plane spread to byte j
+        // ((x * 0x204081) & 0x01010101 moves bit i of a nibble to bit 8i)
+        const uint32_t c4 = ((((w0 >> (4 * g)) & 0xFu) * 0x00204081u) & 0x01010101u) |
+                            (((((w1 >> (4 * g)) & 0xFu) * 0x00204081u) & 0x01010101u) << 1) |
+                            (((((w2 >> (4 * g)) & 0xFu) * 0x00204081u) & 0x01010101u) << 2);
+        uint32_t e4 = c4 + base4;  // no carries: code <= 6 and base + 6 <= 255 unless escaped
+        if ((escm >> (4 * g)) & 0xFu) {  // rare: rebuild the group byte by byte with its escapes
+            e4 = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t code = (c4 >> (8 * j)) & 0xFFu;
+                const uint32_t e = code == 7 ? (uint32_t)__ldg(es + k++) : base + code;
+                e4 |= e << (8 * j);
+            }
+        }
+        // bf16 = sign << 15 | exp << 7 | mantissa, two per output word
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t t = __byte_perm(lw[g], 0, h ? 0x4342u : 0x4140u);  // low bytes -> [b, 0, b', 0]
+            const uint32_t ep = __byte_perm(e4, 0, h ? 0x4342u : 0x4140u);
+            out[2 * g + h] = (t & 0x007F007Fu) | ((t & 0x00800080u) << 8) | (ep << 7);
+        }
     }
     uint4 *o = reinterpret_cast<uint4 *>(dst + c * kChunk + wi * 32);
 #pragma unroll

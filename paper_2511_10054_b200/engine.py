@@ -59,12 +59,69 @@ def fill_mirror_from_device(mirror: HostMirror, src: torch.Tensor, offset: int =
     s.synchronize()
 
 
-def coded_mirror_from_device(arena: torch.Tensor) -> HostMirror:
+class SharedMirror:
+    """A layer mirror in a shared-memory file (``/dev/shm``) that every
+    replica process on the node maps and page-locks (bm_host_register), so N
+    replicas of one model hold ONE host copy of the experts instead of N.
+    The owner (local rank 0) creates and fills it; the others attach
+    read-only after a barrier. Same interface as HostMirror (ptr, nbytes,
+    codec, close)."""
+
+    def __init__(self, path: str, nbytes: int = 0, create: bool = False, register: bool = True):
+        import mmap
+        import os
+        self.path, self.owner, self.registered = path, create, False
+        fd = os.open(path, os.O_RDWR | (os.O_CREAT | os.O_TRUNC if create else 0), 0o600)
+        try:
+            if create:
+                os.ftruncate(fd, int(nbytes))
+            else:
+                nbytes = os.fstat(fd).st_size
+            self._mm = mmap.mmap(fd, int(nbytes), mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+        finally:
+            os.close(fd)
+        self._buf = (C.c_char * int(nbytes)).from_buffer(self._mm)
+        self.ptr = C.addressof(self._buf)
+        self.nbytes = int(nbytes)
+        self.codec = 1 if (not create and self.nbytes >= 4 and bytes(self._buf[:4]) == b"BXL1") else 0
+        if register:
+            N.call("bm_host_register", self.ptr, self.nbytes, 0 if create else 1)
+            self.registered = True
+
+    def as_tensor(self, dtype=torch.uint8) -> torch.Tensor:
+        return torch.frombuffer(self._buf, dtype=torch.uint8).view(dtype)
+
+    def close(self):
+        import os
+        if getattr(self, "_mm", None) is None:
+            return
+        if self.registered:
+            N.lib().bm_host_unregister(self.ptr)
+            self.registered = False
+        self.ptr = None
+        del self._buf
+        self._mm.close()
+        self._mm = None
+        if self.owner:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def coded_mirror_from_device(arena: torch.Tensor, make_mirror=HostMirror):
     """Pinned host layer image of every expert of ``arena`` [count, elems]
     (bf16, device) in the exponent-coded transfer format: a
     bm_xfer_layer_header followed by one blob per expert (include/bmoe.h).
     The engine fetches it piece by piece and rebuilds the exact bf16 bytes
-    in HBM, so fewer bytes cross PCIe per miss."""
+    in HBM, so fewer bytes cross PCIe per miss. ``make_mirror(nbytes)``
+    allocates the host side (HostMirror, or a SharedMirror for replicas)."""
     from . import ops
     count, elems = arena.shape
     blobs = [ops.xfer_encode(arena[e]) for e in range(count)]
@@ -72,7 +129,7 @@ def coded_mirror_from_device(arena: torch.Tensor) -> HostMirror:
     offs = [head]
     for b in blobs:
         offs.append(offs[-1] + 256 * ((b.numel() + 255) // 256))
-    m = HostMirror(offs[-1])
+    m = make_mirror(offs[-1])
     m.codec = 1
     hdr = np.zeros(head // 8, np.uint64)
     hdr[0] = np.uint64(0x314C5842 | (count << 32))  # magic "BXL1", count

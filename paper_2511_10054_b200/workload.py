@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import ops, substrate
-from .engine import DecodeEngine, EngineSpec, HostMirror, coded_mirror_from_device, fill_mirror_from_device
+from .engine import DecodeEngine, EngineSpec, HostMirror, SharedMirror, coded_mirror_from_device, fill_mirror_from_device
 
 SHAPES = {
     # name: (E, k, d, f, cache_rate)
@@ -52,6 +52,28 @@ def host_mem_available() -> int:
     except OSError:
         pass
     return 64 << 30
+
+
+@dataclass
+class ShareSpec:
+    """Node-shared expert mirrors for replicas of one model: the owner
+    (local rank 0) writes /dev/shm/<tag>_L<l>, ``barrier()`` orders the
+    writes before the other local ranks attach."""
+    tag: str
+    owner: bool
+    barrier: object
+    directory: str = "/dev/shm"
+
+    def path(self, layer: int) -> str:
+        return os.path.join(self.directory, f"{self.tag}_L{layer:03d}")
+
+
+def shm_bytes_free(directory: str = "/dev/shm") -> int:
+    try:
+        st = os.statvfs(directory)
+        return st.f_bavail * st.f_frsize
+    except OSError:
+        return 0
 
 
 @dataclass
@@ -102,9 +124,11 @@ def _gen_expert(gen, d, f, device):
 def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: int = 0,
           profile_tokens: int = 4096, alpha: float = 0.95, k_max: int | None = None, tau_percentile: float = 15.0,
           clusters: int | None = None, n_tile: int = 128, device: str = "cuda", rho: int | None = 3,
-          codec: int = 1, log=None) -> Workload:
+          codec: int = 1, share: ShareSpec | None = None, log=None) -> Workload:
     """codec 1 keeps the pinned mirrors exponent-coded (bm_xfer_*: ~0.70 of
-    the bf16 bytes cross PCIe per miss, rebuilt bit-exactly in HBM); 0 raw."""
+    the bf16 bytes cross PCIe per miss, rebuilt bit-exactly in HBM); 0 raw.
+    share: one node-shared mirror per layer for all local replicas (every
+    rank still generates the weights on its GPU to profile its tables)."""
     import time
     E, k, d, f, rate = SHAPES[name]
     S = SHARED.get(name, 0)
@@ -134,11 +158,15 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
             w = _gen_expert(gen, d, f, device)
             ops.pack_expert_bf16(w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d), w[2 * f * d:].view(d, f),
                                  ops.ACT_SWIGLU, arena[e])
-        if codec:
-            m = coded_mirror_from_device(arena)
+        if share is not None and not share.owner:
+            m = None  # attached after the owner has written every layer
         else:
-            m = HostMirror((E + S) * buf_bytes)
-            fill_mirror_from_device(m, arena)
+            make = HostMirror if share is None else (lambda n, _l=l: SharedMirror(share.path(_l), n, create=True))
+            if codec:
+                m = coded_mirror_from_device(arena, make)
+            else:
+                m = make((E + S) * buf_bytes)
+                fill_mirror_from_device(m, arena)
         mirrors.append(m)
         # ---- profile this layer (full residency) ----
         r = ops.gate_topk(x, gate_w[l], gate_b[l], k)
@@ -163,10 +191,14 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
                                  ops.ACT_SWIGLU, ws)
         x = ops.combine(yp, perm, pr, kd, h_in=x)
         if log:
-            log(f"layer {l}: mirror {m.nbytes / 2**30:.2f} GiB, tau {taus[-1]:.4f}, "
+            log(f"layer {l}: mirror {(m.nbytes if m else 0) / 2**30:.2f} GiB, tau {taus[-1]:.4f}, "
                 f"mean buddies {mean_len[-1]:.2f}, {time.time() - t0:.1f}s")
     torch.cuda.synchronize()
     del arena, ws
+    if share is not None:
+        share.barrier()
+        if not share.owner:
+            mirrors = [SharedMirror(share.path(l)) for l in range(layers)]
     initial = [initial_residents(E, cap, 0, l) for l in range(layers)]
     es = EngineSpec(num_layers=layers, num_experts=E, top_k=k, d=d, f=f, capacity=cap, max_batch=max_batch,
                     act=ops.ACT_SWIGLU, search_rank_h=k_max, rho=rho, n_tile=n_tile, expert_bytes=buf_bytes,
