@@ -47,4 +47,23 @@ if __name__ == "__main__":
     del os.environ["BMOE_FUSED"], os.environ["BMOE_KPS"]
     torch.cuda.synchronize()
     assert torch.equal(y0, y1)
+    # prefill width: data-parallel tiles finished in the GEMM epilogue (n_tile 128, > 1 chunk per expert)
+    B3 = 300
+    tk = np.stack([rng.choice(E2, 2, replace=False) for _ in range(B3)]).astype(np.int32)
+    perm = ops.permute(torch.from_numpy(tk).cuda(), torch.zeros(B3, 2, dtype=torch.uint8).cuda(), E2)
+    xp = ops.gather_rows(torch.randn(B3, d).cuda(), perm, 1)
+    ws = ops.FfnWorkspace(E2, d, f, perm.r_max, 128)
+    ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)
+    torch.cuda.synchronize()
+    # decode engine over exponent-coded mirrors (staging ring + piece decoder + prefetch stream)
+    from paper_2511_10054_b200 import workload as W
+    wl = W.build("tiny", layers=2, max_batch=16, profile_tokens=512, codec=1)
+    eng = wl.engine("buddy")
+    x = torch.from_numpy(wl.tokens(2, 48)).cuda()
+    for s in range(3):
+        eng.step(x[s * 16:(s + 1) * 16], np.arange(s * 16, (s + 1) * 16))
+    torch.cuda.synchronize()
+    assert eng.stats()["wire_bytes"] > 0
+    eng.close()
+    wl.close()
     print("sanitize smoke ok")
