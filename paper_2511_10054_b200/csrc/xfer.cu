@@ -352,6 +352,17 @@ void piece_layout(int64_t n_chunks, int64_t n_esc, bm_xfer_piece_header *h) {
     h->bytes = (uint32_t)o;
 }
 
+// values per piece: BM_XFER_PIECE_VALUES, or BMOE_XFER_PIECE (a multiple of
+// 2048, for A/B of the fetch pipeline's granularity); recorded in each blob
+int64_t piece_values() {
+    static const int64_t v = [] {
+        const char *ev = getenv("BMOE_XFER_PIECE");
+        const long long x = ev ? atoll(ev) : 0;
+        return (x >= kChunk && x % kChunk == 0 && x <= (1LL << 30)) ? (int64_t)x : (int64_t)BM_XFER_PIECE_VALUES;
+    }();
+    return v;
+}
+
 int grid_for(int64_t n_chunks) {
     const int64_t g = std::min<int64_t>(n_chunks, (int64_t)sm_count() * 8);
     return (int)std::max<int64_t>(g, 1);
@@ -365,7 +376,7 @@ using namespace bm;
 extern "C" int64_t bm_xfer_blob_bound(int64_t n_values) {
     if (n_values <= 0 || n_values % kChunk) return -1;
     const int64_t n_chunks = n_values / kChunk;
-    const int64_t cpp = BM_XFER_PIECE_VALUES / kChunk;
+    const int64_t cpp = piece_values() / kChunk;
     const int64_t n_pieces = (n_chunks + cpp - 1) / cpp;
     int64_t total = header_bytes(n_pieces);
     for (int64_t p = 0; p < n_pieces; ++p) {
@@ -386,7 +397,7 @@ extern "C" int bm_xfer_encode(const uint16_t *src, int64_t n_values, uint8_t *bl
                "bm_xfer_encode: src must be 16-byte and blob 256-byte aligned");
     cudaStream_t s = as_stream(stream);
     const int64_t n_chunks = n_values / kChunk;
-    const int64_t cpp = BM_XFER_PIECE_VALUES / kChunk;
+    const int64_t cpp = piece_values() / kChunk;
     const int64_t n_pieces = (n_chunks + cpp - 1) / cpp;
     // pass 1: per-chunk window bases and escape counts
     uint8_t *d_base = nullptr;
@@ -409,7 +420,7 @@ extern "C" int bm_xfer_encode(const uint16_t *src, int64_t n_values, uint8_t *bl
     bh->magic = kBlobMagic;
     bh->n_pieces = (uint32_t)n_pieces;
     bh->n_values = (uint64_t)n_values;
-    bh->piece_values = (uint32_t)BM_XFER_PIECE_VALUES;
+    bh->piece_values = (uint32_t)piece_values();
     uint64_t off = hb;
     std::vector<std::vector<uint8_t>> meta(n_pieces);
     for (int64_t p = 0; p < n_pieces; ++p) {
