@@ -373,7 +373,7 @@ int64_t bm_engine_device_bytes(const bm_engine *e);
  * escaping to a per-chunk exponent stream. ~11.2 bits per value for
  * N(0, s) weights. Blobs are split into self-contained pieces of
  * BM_XFER_PIECE_VALUES values (the fetch pipeline's unit). */
-#define BM_XFER_PIECE_VALUES (8 * 1024 * 1024)
+#define BM_XFER_PIECE_VALUES (32 * 1024 * 1024)
 typedef struct {
     uint32_t magic;        /* "BXC1" */
     uint32_t n_pieces;

@@ -17,7 +17,7 @@
 // exclusive prefix of escape counts, then writes 16 bytes.
 //
 // Blob (one expert)      : BlobHeader | pieces (256-byte aligned)
-// Piece (<= 8M values)   : PieceHeader (32 B) | low[n] | planes[chunks][3][256] |
+// Piece (<= 32M values)  : PieceHeader (32 B) | low[n] | planes[chunks][3][256] |
 //                          base[chunks] | escoff[chunks] u32 | esc[n_esc]
 // Pieces are self-contained so a fetch streams them through a small staging
 // ring: copy piece i+1 while piece i decodes (engine.cpp).

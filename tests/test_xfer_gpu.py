@@ -40,7 +40,7 @@ def _np_decode(blob: np.ndarray) -> np.ndarray:
             exp[c, m] = esc[eo[c]:eo[c] + int(m.sum())]
         out.append(((low & 0x80) << 8) | (exp << 7) | (low & 0x7F))
     v = np.concatenate([o.ravel() for o in out])
-    assert v.size == n_values and (n_pieces == 1 or piece_values == 8 * 1024 * 1024)
+    assert v.size == n_values and (n_pieces == 1 or piece_values == 32 * 1024 * 1024)
     return v
 
 
@@ -60,7 +60,7 @@ def _special(n, gen):
     return x
 
 
-@pytest.mark.parametrize("n", [2048, 3 * 2048, 65536 * 3, 8 * 1024 * 1024 + 4096])
+@pytest.mark.parametrize("n", [2048, 3 * 2048, 65536 * 3, 32 * 1024 * 1024 + 4096])
 def test_roundtrip_bit_exact(cuda_ok, n):
     gen = torch.Generator(device="cuda")
     gen.manual_seed(n)
@@ -76,7 +76,7 @@ def test_ratio_and_piecewise_decode(cuda_ok):
     """N(0, 1/sqrt(fan_in)) weights: <= 0.71 of the raw bytes; decoding the
     pieces one by one (the engine's pipeline) equals the whole-blob decode."""
     from paper_2511_10054_b200 import _native as N
-    n = 3 * 4096 * 14336 // 4  # a quarter Mixtral expert, 6 pieces
+    n = 3 * 4096 * 14336 // 2  # half a Mixtral expert, 3 pieces
     x = torch.empty(n, dtype=torch.bfloat16, device="cuda")
     x[: 2 * n // 3].normal_(0.0, 4096 ** -0.5)
     x[2 * n // 3:].normal_(0.0, 14336 ** -0.5)
@@ -88,7 +88,8 @@ def test_ratio_and_piecewise_decode(cuda_ok):
     n_pieces = int(np.frombuffer(hb[4:8].tobytes(), np.uint32)[0])
     offs = np.frombuffer(blob[24:24 + 8 * (n_pieces + 1)].cpu().numpy().tobytes(), np.uint64)
     y = torch.zeros_like(x)
-    pv = 8 * 1024 * 1024
+    pv = int(np.frombuffer(hb[16:20].tobytes(), np.uint32)[0])
+    assert pv == 32 * 1024 * 1024 and n_pieces == 3
     for p in range(n_pieces):
         piece = blob[int(offs[p]):int(offs[p + 1])]
         nch = int(np.frombuffer(piece[4:8].cpu().numpy().tobytes(), np.uint32)[0])
