@@ -174,6 +174,32 @@ def test_coact_counts_large_random_vs_oracle(cuda_ok):
     assert np.array_equal(p.cpu().numpy().astype(np.float64), op)
 
 
+def test_coact_full_64m_trace_vs_one_hot_products(cuda_ok):
+    """BASELINE configs[4] at full size: the 64M-token, E=128, k=8 bench
+    trace. K6's counts and pair matrix equal an independent count — the
+    one-hot products X^T X of 4M-token slices (fp32 tensor products of 0/1
+    matrices, exact below 2^24 per slice) summed in int64 — and satisfy the
+    size-independent identities (symmetry, zero diagonal, row sums =
+    (k-1) * counts, total = N * k * (k-1))."""
+    import bench
+    N, E, k = 64 * 1024 * 1024, 128, 8
+    trace = bench.gen_trace(N, E, k, 0, N, "cuda")
+    c, p = ops.coact_count(trace, E)
+    ref = torch.zeros(E, E, dtype=torch.int64, device="cuda")
+    step = 4 * 1024 * 1024
+    for a in range(0, N, step):
+        oh = torch.zeros(min(step, N - a), E, dtype=torch.float32, device="cuda")
+        oh.scatter_(1, trace[a:a + step].long(), 1.0)
+        ref += (oh.T @ oh).round().to(torch.int64)
+        del oh
+    assert torch.equal(c, torch.diagonal(ref))
+    ref.fill_diagonal_(0)
+    assert torch.equal(p, ref)
+    assert torch.equal(p, p.T) and int(torch.diagonal(p).abs().sum()) == 0
+    assert torch.equal(p.sum(1), (k - 1) * c)
+    assert int(p.sum()) == N * k * (k - 1) and int(c.sum()) == N * k
+
+
 @pytest.mark.parametrize("k", [1, 3, 8])
 def test_coact_rejects_bad_rows(cuda_ok, k):
     """Rows with repeated / out-of-range ids are rejected (profiler.py:76-80);
