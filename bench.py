@@ -353,8 +353,10 @@ def run_profile_bench(args, ws, rank, local):
             "tokens": N, "experts": E, "top_k": k, "warmup_steps": 256, "alpha": 0.95, "k_max": 16,
             "parallelism": f"token-sharded x{ws} + NCCL all-reduce", "l2": "trace (2 GB) larger than L2"},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                         "traffic": {"dram_bytes": 2148022000 + 4829952, "per": "one 64M-token launch",
-                                     "source": "profiles/r1_coact_count.ncu-rep (ncu --set full)"} if N == 64 << 20 and ws == 1 else None,
+                         # DRAM bytes of the one 64M-token launch captured with ncu --set full
+                         "traffic": 2148022000 + 4829952 if N == 64 << 20 and ws == 1 else None,
+                         "traffic_source": "profiles/r1_coact_count.ncu-rep (ncu --set full; the launch reads the "
+                                           "2.147 GB trace once)",
                          "kernel": "coact_count_kernel", "algorithmic_bytes_per_launch": bytes_k,
                          "avg_launch_ms": k_ms, "peak_kind": peak_kind},
             "cpu_baseline": cpu, "e2e": None, "gpu_launches": 5 * args.steps, "clocks": clocks}
@@ -491,17 +493,20 @@ def main():
         # then the fetched ones), each ONE fused kernel at decode width.
         peak, peak_kind = hbm_peak, hbm_kind
         ach = tot_k / (float(np.sum(g1) + np.sum(g2)) / 1e3) / 1e9
-        traffic = None  # DRAM bytes of one captured launch (ncu --set full), committed under profiles/
+        # DRAM bytes of one captured launch (ncu --set full, committed under
+        # profiles/), with that launch's own algorithmic bytes beside it
+        traffic, traffic_launch = None, None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
             l0 = tr["launches"][0]
             if args.model == "mixtral" and fused:
-                traffic = {"dram_bytes": l0["dram_read_bytes"] + l0["dram_write_bytes"], "experts": l0["experts"],
-                           "weight_bytes": l0["weight_bytes"], "source": tr["source"]}
+                traffic = l0["dram_read_bytes"] + l0["dram_write_bytes"]
+                traffic_launch = {"experts": l0["experts"], "weight_bytes": l0["weight_bytes"],
+                                  "dram_over_weight_bytes": traffic / l0["weight_bytes"], "source": tr["source"]}
         except (OSError, KeyError, ValueError):
             pass
         roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                    "traffic": traffic,
+                    "traffic": traffic, "traffic_launch": traffic_launch,
                     "kernel": "ffn_fused_kernel (one cooperative launch: W1|W3 swap-AB GEMM -> SwiGLU -> W2 GEMM, "
                               "stream-K)" if fused else
                               "ffn_gemm_kernel x2 (data-parallel tcgen05 tiles, SwiGLU / output in the epilogue)",
