@@ -77,6 +77,7 @@ struct GemmParams {
     uint8_t *h_planes;        // GEMM1 output: bf16 SW128 planes [M/64][h_rmax][64]
     int h_rmax;
     float *y_perm;            // GEMM2 output: fp32 [r_max][M]
+    long long arena_bytes;    // whole weights arena (the CTA-pair kernel's tensor map spans it)
 };
 
 __device__ __forceinline__ int chunks_of(int c, int n_tile) { return (((c + 15) & ~15) + n_tile - 1) / n_tile; }
@@ -530,6 +531,212 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
     if constexpr (CL == 2) ptx::cluster_sync();  // neither CTA leaves while its peer may still multicast into it
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
+}
+
+// ------------------------------------------------ prefill GEMM on CTA pairs
+// cta_group::2 tcgen05 MMAs (M = 256): the two CTAs of a cluster hold the two
+// weight m-tiles of an m-tile pair, each loads ITS 128 weight rows and HALF of
+// the token chunk (N/2 rows), and the leader CTA issues M=256 MMAs that read
+// both CTAs' shared memory and write both CTAs' TMEM. Per MAC every SM then
+// moves and reads fewer operand bytes through shared memory than the
+// single-CTA tile, whose bulk-copy writes plus tensor-core reads saturate the
+// SM's shared-memory bandwidth (profiles/README.md). Each CTA finishes its own
+// m-tile in its own epilogue (SwiGLU -> H, or y), exactly as the single-CTA
+// kernel does, so the outputs are bitwise identical.
+// Both CTAs load with cta_group::2 tensor-map copies that complete on the
+// LEADER's full[s] barrier, so the leader's MMA sees both halves land
+// without a relay; the two byte-image tensor maps (weights arena, token
+// planes) are [rows][128 B] views of the pre-swizzled images.
+//   full[s]  : leader only, both CTAs' bytes (leader expects them)
+//   empty[s] : both CTAs, released by the leader's multicast commit
+//   tfull[a] : both CTAs, leader's multicast commit
+//   tempty[a]: leader only, 4 local + 4 remote epilogue-warp arrivals
+struct PairMaps {
+    CUtensorMap a;  // weights arena, uint8 [rows][128], box 128 x 256 rows
+    CUtensorMap b;  // token planes, uint8 [K/64 * r_max][128], box 128 x n_tile/2 rows
+};
+
+template <int NMAT, int KPS>
+__global__ void __launch_bounds__(kThreads, 1) ffn_gemm_2sm_kernel(GemmParams p, const __grid_constant__ PairMaps tm) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ Sched sched;
+    __shared__ __align__(8) uint64_t bars[64];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const int rank = (int)ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int mpairs = p.M / (2 * kBM);
+    const int spt = p.K / (kBK * KPS);
+
+    if (warp == 0) build_sched_warp(sched, p.count, p.offset, p.E, p.n_tile);
+    __syncthreads();
+    const int units = total_tiles(sched, mpairs);  // (expert, m-tile pair, token chunk)
+    const int G = min(p.num_ctas / 2, units);
+    const int pair = (int)(blockIdx.x >> 1);
+    if (pair >= G) return;  // uniform for both CTAs of the pair
+
+    constexpr uint32_t kAStage = (uint32_t)(KPS * NMAT) * kATileBytes;
+    const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t bbox = (uint32_t)(p.n_tile / 2) * 128u;  // bytes of one B box (a k-block of the token half)
+    const uint32_t bhalf = (bbox + 1023u) & ~1023u;
+    const uint32_t stage_bytes = kAStage + (uint32_t)KPS * bhalf;
+    const int stages = min(16, (int)((kSmemBudget - 1024) / stage_bytes));
+    const int acc_stages = (2 * NMAT * p.n_tile <= 512) ? 2 : 1;
+    const uint32_t acc_cols = acc_stages == 2 ? 256u : 512u;
+
+    const uint32_t full0 = ptx::smem_u32(&bars[0]);     // [stages] (leader)
+    const uint32_t empty0 = ptx::smem_u32(&bars[16]);   // [stages]
+    const uint32_t tfull0 = ptx::smem_u32(&bars[48]);   // [2]
+    const uint32_t tempty0 = ptx::smem_u32(&bars[50]);  // [2] (leader)
+
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < stages; ++s) {
+            ptx::mbar_init(full0 + 8 * s, 1);
+            ptx::mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull0 + 8 * a, 1);
+            ptx::mbar_init(tempty0 + 8 * a, 8);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc_pair(ptx::smem_u32(&tmem_base_sh), 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = tmem_base_sh;
+
+    if (warp == 0 && lane == 0) {
+        // ===================== producer (both CTAs): own weight m-tile + own half of the tokens
+        ptx::prefetch_tmap(&tm.a);
+        ptx::prefetch_tmap(&tm.b);
+        const uint32_t full_leader = leader ? full0 : ptx::mapa(full0, 0);
+        const int b_rows = (int)(p.b_plane_bytes / 128);  // rows per k-block plane
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = pair; u < units; u += G) {
+            const TileInfo ti = decode_tile(sched, u, mpairs, p.n_tile);
+            const int mt = 2 * ti.mtile + rank;
+            const int buf = p.buf_of_expert[ti.e];
+            const long long a_row0 = ((long long)buf * p.buf_bytes + p.mat_off + (long long)mt * spt * kAStage) / 128;
+            const int b_row0 = ti.row0 + rank * (ti.n / 2);
+            for (int st = 0; st < spt; ++st) {
+                ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+                const uint32_t sA = base + (uint32_t)stage * stage_bytes;
+                const uint32_t sB = sA + kAStage;
+                const uint32_t fb = full_leader + 8 * stage;
+                if (leader) ptx::mbar_expect_tx(full0 + 8 * stage, 2u * (kAStage + (uint32_t)KPS * bbox));
+                const long long ar = a_row0 + (long long)st * (kAStage / 128);
+#pragma unroll
+                for (int j = 0; j < (int)(kAStage / 32768); ++j)
+                    ptx::tma_load_2d_pair(sA + (uint32_t)j * 32768u, &tm.a, fb, 0, (int32_t)(ar + 256 * j));
+#pragma unroll
+                for (int i = 0; i < KPS; ++i)
+                    ptx::tma_load_2d_pair(sB + (uint32_t)i * bhalf, &tm.b, fb, 0, (st * KPS + i) * b_rows + b_row0);
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+        for (int i = 0; i < stages; ++i) {  // every stage released: no multicast commit still in flight to us
+            ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+            if (++stage == stages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ===================== leader: M=256 pair MMAs
+        const uint64_t desc0 = ptx::sw128_desc(base);
+        const uint64_t stage_d = stage_bytes >> 4, bh_d = bhalf >> 4;
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = pair; u < units; u += G) {
+            const TileInfo ti = decode_tile(sched, u, mpairs, p.n_tile);
+            const uint32_t idesc = ptx::idesc_bf16_f32(2 * kBM, (uint32_t)ti.n);
+            ptx::mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1u);
+            ptx::tc_fence_after();
+            const uint32_t d0 = tmem_base + (uint32_t)acc * acc_cols;
+            const uint32_t d1 = d0 + (uint32_t)p.n_tile;
+            uint32_t accum = 0;
+            for (int st = 0; st < spt; ++st) {
+                ptx::mbar_wait_cluster(full0 + 8 * stage, phase);
+                ptx::tc_fence_after();
+                const uint64_t a = desc0 + (uint64_t)stage * stage_d;
+                const uint64_t b = a + (kAStage >> 4);
+#pragma unroll
+                for (int i = 0; i < KPS; ++i) {
+                    const uint64_t bi = b + (uint64_t)i * bh_d;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        ptx::mma_bf16_pair(d0, a + (uint64_t)((i * NMAT) * (kATileBytes >> 4) + 2 * kk), bi + 2 * kk,
+                                           idesc, accum);
+                        if (NMAT == 2)
+                            ptx::mma_bf16_pair(d1, a + (uint64_t)((i * NMAT + 1) * (kATileBytes >> 4) + 2 * kk),
+                                               bi + 2 * kk, idesc, accum);
+                        accum = 1u;
+                    }
+                }
+                ptx::mma_commit_pair(empty0 + 8 * stage, 0x3);  // both CTAs' stage is free once these finish
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+            ptx::mma_commit_pair(tfull0 + 8 * acc, 0x3);  // both CTAs' accumulators are ready
+            if (acc_stages == 2) {
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1u;
+            } else {
+                acc_phase ^= 1u;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (both CTAs): own m-tile, all tokens of the chunk
+        const int q = warp - 4;
+        const uint32_t tempty_leader = leader ? tempty0 : ptx::mapa(tempty0, 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = pair; u < units; u += G) {
+            TileInfo ti = decode_tile(sched, u, mpairs, p.n_tile);
+            ti.mtile = 2 * ti.mtile + rank;
+            ptx::mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + (uint32_t)acc * acc_cols + ((uint32_t)(q * 32) << 16);
+            for (int c0 = 0; c0 < ti.n; c0 += 16) {
+                float g[16], uu[16];
+                ptx::tmem_ld16(tbase + (uint32_t)c0, g);
+                if (NMAT == 2) ptx::tmem_ld16(tbase + (uint32_t)(p.n_tile + c0), uu);
+                finish16<NMAT>(p, ti, c0, q, lane, g, uu);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader)
+                    ptx::mbar_arrive(tempty0 + 8 * acc);
+                else
+                    ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+            }
+            if (acc_stages == 2) {
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1u;
+            } else {
+                acc_phase ^= 1u;
+            }
+        }
+    }
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();  // neither CTA frees TMEM / leaves while the pair still works
+    ptx::tc_fence_after();
+    if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, 512);
 }
 
 // ---------------------------------------------------------------- fixups
@@ -1009,6 +1216,99 @@ int launch_gemm_cl(const GemmParams &g, int G, cudaStream_t s) {
     return launch_gemm<1, 4, CL>(g, G, s);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda):
+// a uint8 [rows][128] view of a pre-swizzled byte image, box 128 x box_rows
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int encode_rows(CUtensorMap *m, const void *base, unsigned long long rows, unsigned box_rows) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        BM_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        BM_REQUIRE(f && q == cudaDriverEntryPointSuccess, BM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(f);
+    }
+    const cuuint64_t dims[2] = {128, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    BM_REQUIRE(r == CUDA_SUCCESS, BM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return BM_OK;
+}
+
+template <int NMAT, int KPS>
+int launch_gemm_2sm(const GemmParams &g, int G, cudaStream_t s) {
+    static bool attr = false;
+    auto kern = ffn_gemm_2sm_kernel<NMAT, KPS>;
+    if (!attr) {
+        BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBudget;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static int max_clusters = 0;  // persistent pairs: only co-resident clusters
+    if (!max_clusters) {
+        cfg.gridDim = dim3((unsigned)(G & ~1));
+        BM_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
+        if (max_clusters < 1) max_clusters = 1;
+    }
+    GemmParams gp = g;
+    gp.num_ctas = 2 * std::min(G / 2, max_clusters);
+    cfg.gridDim = dim3((unsigned)gp.num_ctas);
+    PairMaps maps;
+    if (int rc = encode_rows(&maps.a, g.arena, (unsigned long long)(g.arena_bytes / 128), 256)) return rc;
+    if (int rc = encode_rows(&maps.b, g.b_planes, (unsigned long long)(g.K / kBK) * (g.b_plane_bytes / 128),
+                             (unsigned)(g.n_tile / 2)))
+        return rc;
+    BM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, gp, maps));
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+// k-blocks per stage of the CTA-pair GEMM: the largest of {2, 1} dividing
+// K/64 that leaves >= 3 stages (BMOE_KPS_2SM overrides)
+int kps_2sm(int nmat, long long K, long long n_tile) {
+    const long long bhalf = ((n_tile / 2) * 128 + 1023) / 1024 * 1024;
+    if (const char *ev = getenv("BMOE_KPS_2SM"))  // tuning override (must divide K/64 and fit twice)
+        if (atoi(ev) == 1 || (atoi(ev) == 2 && (K / kBK) % 2 == 0)) return atoi(ev);
+    int kps = 2;
+    while (kps > 1 && ((K / kBK) % kps || (kSmemBudget - 1024) / (kps * (nmat * kATileBytes + bhalf)) < 3)) kps >>= 1;
+    return kps;
+}
+
+// Data-parallel (prefill) GEMM2 (one accumulator per tile) with an even
+// number of weight m-tiles runs on CTA pairs (cta_group::2, M = 256) at
+// 256-token tiles: Mixtral 4096 x 2 0.93 -> 0.73 ms. GEMM1 keeps single CTAs:
+// with two accumulators (W1, W3) a pair tile saves only ~8% of the shared-
+// memory traffic per MAC and measured slower (1.74 vs 1.61 ms).
+// BMOE_2SM=0: single CTAs everywhere; 2: GEMM1 on pairs as well.
+bool use_2sm(const GemmParams &g) {
+    const char *ev = getenv("BMOE_2SM");
+    const int mode = ev ? atoi(ev) : 1;
+    return g.dp && mode != 0 && (g.nmat == 1 || mode == 2) && (g.M / kBM) % 2 == 0 && g.n_tile >= 32 &&
+           g.n_tile % 32 == 0;
+}
+
+int launch_gemm_2sm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
+    if (g.nmat == 2) return g.kps == 1 ? launch_gemm_2sm<2, 1>(g, G, s) : launch_gemm_2sm<2, 2>(g, G, s);
+    return g.kps == 1 ? launch_gemm_2sm<1, 1>(g, G, s) : launch_gemm_2sm<1, 2>(g, G, s);
+}
+
 // BMOE_PAIR=1 runs the data-parallel (prefill) GEMMs as CTA pairs that
 // share each weight stage through a cluster multicast. Off by default: it
 // halves the L2 reads of the weights but not the bytes each SM must hold in
@@ -1017,6 +1317,11 @@ int launch_gemm_cl(const GemmParams &g, int G, cudaStream_t s) {
 // MMAs alone 1.30 ms, operand feed alone 0.99 ms, both 1.65 ms at Mixtral
 // 4096 x 2; pairs 1.65 ms). Results are bitwise identical either way.
 int launch_gemm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
+    if (use_2sm(g)) {
+        GemmParams g2 = g;
+        g2.kps = kps_2sm(g.nmat, g.K, g.n_tile);
+        return launch_gemm_2sm_dispatch(g2, G, s);
+    }
     const char *ev = getenv("BMOE_PAIR");
     if (g.dp && ev && atoi(ev) != 0 && G >= 2) return launch_gemm_cl<2>(g, G, s);
     return launch_gemm_cl<1>(g, G, s);
@@ -1147,7 +1452,6 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
     BM_REQUIRE(r_max % 16 == 0, BM_EINVAL, "r_max must be a multiple of 16");
     BM_REQUIRE(workspace_bytes >= bm_expert_ffn_bf16_workspace(E, d, f, r_max, n_tile), BM_EINVAL,
                "workspace too small");
-    (void)n_bufs;
     if (r_max == 0) return BM_OK;
     cudaStream_t s = as_stream(stream);
     const long long buf_bytes = (act == BM_ACT_SWIGLU ? 3 : 2) * d * f * 2;
@@ -1179,6 +1483,7 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
                   kps_for(1, f, n_tile), arena, buf_bytes, (long long)nmat1 * f * d * 2, h_planes, r_max * 128,
                   partials, G, 2, fuse, dp, probe, nullptr, 0, y_perm};
 
+    g1.arena_bytes = g2.arena_bytes = n_bufs * buf_bytes;
     const bool timing = g_timing.enabled;
     std::lock_guard<std::mutex> lk(g_timing.mu);
     if (fused) {
@@ -1207,6 +1512,12 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
     if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
     if (timing && record_event(s)) return BM_ECUDA;
     if (dp) {  // every tile was finished by its GEMM epilogue
+        // GEMM2 (one accumulator per tile) keeps a double-buffered 256-token
+        // tile on CTA pairs: wider tiles halve its per-MAC operand traffic
+        if (n_tile >= 128 && use_2sm(g2)) {
+            const char *ev = getenv("BMOE_NT2");
+            g2.n_tile = ev ? atoi(ev) : 256;
+        }
         if (timing && record_event(s)) return BM_ECUDA;
         if (int rc = launch_gemm_dispatch(g2, G, s)) return rc;
         if (timing && record_event(s)) return BM_ECUDA;

@@ -426,3 +426,37 @@ def test_prefill_cta_pairs_equal_single_ctas(cuda_ok, E, d, f, B, k, act):
             os.environ.pop("BMOE_PAIR", None)
         else:
             os.environ["BMOE_PAIR"] = old
+
+
+@pytest.mark.parametrize("E,d,f,B,k,act", [
+    (8, 1024, 2048, 700, 2, ops.ACT_SWIGLU),
+    (4, 512, 1536, 1000, 2, ops.ACT_SWIGLU),
+    (16, 512, 1024, 333, 3, ops.ACT_TANH),
+])
+def test_prefill_2sm_pairs_equal_single_cta(cuda_ok, E, d, f, B, k, act):
+    """Prefill GEMMs on CTA pairs (cta_group::2, M = 256, the token half of
+    each chunk in each CTA, GEMM2 at 256-token tiles) against the single-CTA
+    kernels: every output element accumulates the same K = 16 MMA steps in
+    the same order, so the results match bitwise; and both stay within the
+    bf16 tolerance of the fp32 reference."""
+    import os
+    rng = np.random.default_rng(B + d)
+    y, ref32, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, act, 128)
+    rows = int(perm.offset[-1])
+    bo = _t(buf_of)
+    old = os.environ.get("BMOE_2SM")
+    try:
+        os.environ["BMOE_2SM"] = "0"
+        single = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows].clone()
+        for mode in ("1", "2"):  # GEMM2 on pairs (default); both GEMMs on pairs
+            os.environ["BMOE_2SM"] = mode
+            for _ in range(3):
+                pair = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows]
+                assert torch.equal(pair, single), mode
+    finally:
+        if old is None:
+            os.environ.pop("BMOE_2SM", None)
+        else:
+            os.environ["BMOE_2SM"] = old
+    rel = (torch.linalg.norm(y - ref32, dim=1) / torch.linalg.norm(ref32, dim=1).clamp_min(1e-30)).max().item()
+    assert rel <= 2e-2, rel
