@@ -739,6 +739,232 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_2sm_kernel(GemmParams p,
     if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, 512);
 }
 
+// ------------------------------------------------ prefill GEMM1 (SwiGLU) on CTA pairs, W1 | W3 split
+// The pair's M = 256 rows are W1's and W3's rows of ONE m-tile: the leader
+// CTA holds the W1 block, the peer the W3 block, each with half of a
+// 256-token chunk, so each CTA's TMEM keeps one 256-column accumulator (double
+// buffered) and per MAC every SM moves the same operand bytes as GEMM2's pair
+// tiles. SwiGLU needs g (leader) and u (peer) side by side: each CTA sends the
+// accumulator columns its peer finishes (leader: g of the upper token half,
+// peer: u of the lower half) into the peer's shared memory (DSMEM stores),
+// then finishes its own token half — the same activation and bf16 rounding
+// as every other path, so H is bitwise identical.
+//   xfull : my receive buffer holds this tile's columns (4 remote warp arrivals)
+//   xfree : my PEER's receive buffer may be overwritten (4 remote arrivals)
+template <int KPS>
+__global__ void __launch_bounds__(kThreads, 1) ffn_gemm1_split_kernel(GemmParams p, const __grid_constant__ PairMaps tm) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ Sched sched;
+    __shared__ __align__(8) uint64_t bars[64];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const int rank = (int)ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int mtiles = p.M / kBM;
+    const int kblocks = p.K / kBK;
+    const int spt = kblocks / KPS;
+
+    if (warp == 0) build_sched_warp(sched, p.count, p.offset, p.E, p.n_tile);
+    __syncthreads();
+    const int units = total_tiles(sched, mtiles);  // (expert, m-tile, token chunk)
+    const int G = min(p.num_ctas / 2, units);
+    const int pair = (int)(blockIdx.x >> 1);
+    if (pair >= G) return;
+
+    constexpr uint32_t kAStage = (uint32_t)KPS * kATileBytes;  // own matrix only
+    constexpr int kXCols = 64;                                 // columns per exchange round
+    constexpr uint32_t kXStride = kXCols * 4 + 16;             // receive-buffer row (padded: conflict-free)
+    const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t bbox = (uint32_t)(p.n_tile / 2) * 128u;
+    const uint32_t bhalf = (bbox + 1023u) & ~1023u;
+    const uint32_t stage_bytes = kAStage + (uint32_t)KPS * bhalf;
+    const uint32_t xbuf_bytes = 128u * kXStride;  // 128 rows x kXCols fp32 (+ padding)
+    const int stages = min(16, (int)((kSmemBudget - 1024 - xbuf_bytes) / stage_bytes));
+    const uint32_t xbuf = base + (uint32_t)stages * stage_bytes;
+    const uint32_t acc_cols = 256u;  // one accumulator of <= 256 token columns, double buffered
+
+    const uint32_t full0 = ptx::smem_u32(&bars[0]);     // [stages] (leader)
+    const uint32_t empty0 = ptx::smem_u32(&bars[16]);   // [stages]
+    const uint32_t tfull0 = ptx::smem_u32(&bars[48]);   // [2]
+    const uint32_t tempty0 = ptx::smem_u32(&bars[50]);  // [2] (leader)
+    const uint32_t xfull = ptx::smem_u32(&bars[52]);
+    const uint32_t xfree = ptx::smem_u32(&bars[53]);
+
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < stages; ++s) {
+            ptx::mbar_init(full0 + 8 * s, 1);
+            ptx::mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(tfull0 + 8 * a, 1);
+            ptx::mbar_init(tempty0 + 8 * a, 8);
+        }
+        ptx::mbar_init(xfull, 4);
+        ptx::mbar_init(xfree, 4);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc_pair(ptx::smem_u32(&tmem_base_sh), 512);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = tmem_base_sh;
+
+    if (warp == 0 && lane == 0) {
+        // ===================== producer (both CTAs): own matrix's weight blocks + own token half
+        ptx::prefetch_tmap(&tm.a);
+        ptx::prefetch_tmap(&tm.b);
+        const uint32_t full_leader = leader ? full0 : ptx::mapa(full0, 0);
+        const int b_rows = (int)(p.b_plane_bytes / 128);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = pair; u < units; u += G) {
+            const TileInfo ti = decode_tile(sched, u, mtiles, p.n_tile);
+            const int buf = p.buf_of_expert[ti.e];
+            // block (mt, kb, mat) of the UMMA-tiled expert: ((mt*K/64 + kb)*2 + mat) * 16 KB
+            const long long blk0 = ((long long)buf * p.buf_bytes + p.mat_off) / kATileBytes +
+                                   ((long long)ti.mtile * kblocks) * 2 + rank;
+            const int b_row0 = ti.row0 + rank * (ti.n / 2);
+            for (int st = 0; st < spt; ++st) {
+                ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+                const uint32_t sA = base + (uint32_t)stage * stage_bytes;
+                const uint32_t sB = sA + kAStage;
+                const uint32_t fb = full_leader + 8 * stage;
+                if (leader) ptx::mbar_expect_tx(full0 + 8 * stage, 2u * (kAStage + (uint32_t)KPS * bbox));
+#pragma unroll
+                for (int i = 0; i < KPS; ++i) {
+                    const long long blk = blk0 + 2LL * (st * KPS + i);
+                    ptx::tma_load_2d_pair(sA + (uint32_t)i * kATileBytes, &tm.a, fb, 0, (int32_t)(blk * 128));
+                    ptx::tma_load_2d_pair(sB + (uint32_t)i * bhalf, &tm.b, fb, 0, (st * KPS + i) * b_rows + b_row0);
+                }
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+        for (int i = 0; i < stages; ++i) {
+            ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1u);
+            if (++stage == stages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ===================== leader: M=256 pair MMAs ([W1 ; W3] rows x 256 tokens)
+        const uint64_t desc0 = ptx::sw128_desc(base);
+        const uint64_t stage_d = stage_bytes >> 4, bh_d = bhalf >> 4;
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = pair; u < units; u += G) {
+            const TileInfo ti = decode_tile(sched, u, mtiles, p.n_tile);
+            const uint32_t idesc = ptx::idesc_bf16_f32(2 * kBM, (uint32_t)ti.n);
+            ptx::mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1u);
+            ptx::tc_fence_after();
+            const uint32_t d0 = tmem_base + (uint32_t)acc * acc_cols;
+            uint32_t accum = 0;
+            for (int st = 0; st < spt; ++st) {
+                ptx::mbar_wait_cluster(full0 + 8 * stage, phase);
+                ptx::tc_fence_after();
+                const uint64_t a = desc0 + (uint64_t)stage * stage_d;
+                const uint64_t b = a + (kAStage >> 4);
+#pragma unroll
+                for (int i = 0; i < KPS; ++i) {
+                    const uint64_t ai = a + (uint64_t)i * (kATileBytes >> 4), bi = b + (uint64_t)i * bh_d;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        ptx::mma_bf16_pair(d0, ai + 2 * kk, bi + 2 * kk, idesc, accum);
+                        accum = 1u;
+                    }
+                }
+                ptx::mma_commit_pair(empty0 + 8 * stage, 0x3);
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+            ptx::mma_commit_pair(tfull0 + 8 * acc, 0x3);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1u;
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue: exchange half the accumulator, SwiGLU on own token half
+        const int q = warp - 4;
+        const int m_local = q * 32 + (int)lane;
+        const int peer = rank ^ 1;
+        const uint32_t tempty_leader = leader ? tempty0 : ptx::mapa(tempty0, 0);
+        const uint32_t peer_xbuf = ptx::mapa(xbuf, (uint32_t)peer);
+        const uint32_t peer_xfull = ptx::mapa(xfull, (uint32_t)peer);
+        const uint32_t peer_xfree = ptx::mapa(xfree, (uint32_t)peer);
+        int acc = 0;
+        uint32_t acc_phase = 0, xph = 0;
+        for (int u = pair; u < units; u += G) {
+            const TileInfo ti = decode_tile(sched, u, mtiles, p.n_tile);
+            const int csplit = ((ti.n / 2) + 15) & ~15;  // leader finishes [0, csplit), peer [csplit, n)
+            const int mine0 = leader ? 0 : csplit, mine1 = leader ? csplit : ti.n;
+            const int send0 = leader ? csplit : 0, send1 = leader ? ti.n : csplit;
+            ptx::mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + (uint32_t)acc * acc_cols + ((uint32_t)(q * 32) << 16);
+            // in rounds of kXCols columns (both halves have <= 128 columns: two rounds, always
+            // executed so the two CTAs' handshakes pair up):
+            for (int rd = 0; rd < 128 / kXCols; ++rd) {
+                // 1. my accumulator columns the peer finishes -> its receive buffer
+                const int s0 = send0 + rd * kXCols, s1 = min(send1, s0 + kXCols);
+                ptx::mbar_wait_cluster(xfree, xph ^ 1u);
+                for (int c0 = s0; c0 < s1; c0 += 16) {
+                    float v[16];
+                    ptx::tmem_ld16(tbase + (uint32_t)c0, v);
+                    const uint32_t dst = peer_xbuf + (uint32_t)m_local * kXStride + (uint32_t)(c0 - s0) * 4u;
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        ptx::st_cluster_v4(dst + 4u * j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(peer_xfull);
+                // 2. my token half: own accumulator + the peer's columns from my receive buffer
+                const int m0 = mine0 + rd * kXCols, m1 = min(mine1, m0 + kXCols);
+                ptx::mbar_wait_cluster(xfull, xph);
+                for (int c0 = m0; c0 < m1; c0 += 16) {
+                    float own[16], oth[16];
+                    ptx::tmem_ld16(tbase + (uint32_t)c0, own);
+                    const uint32_t src = xbuf + (uint32_t)m_local * kXStride + (uint32_t)(c0 - m0) * 4u;
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        ptx::ld_shared_v4(src + 4u * j, oth[j], oth[j + 1], oth[j + 2], oth[j + 3]);
+                    if (leader)
+                        finish16<2>(p, ti, c0, q, lane, own, oth);
+                    else
+                        finish16<2>(p, ti, c0, q, lane, oth, own);
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(peer_xfree);  // my receive buffer is consumed
+                xph ^= 1u;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader)
+                    ptx::mbar_arrive(tempty0 + 8 * acc);
+                else
+                    ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+            }
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1u;
+        }
+    }
+    __syncwarp();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, 512);
+}
+
 // ---------------------------------------------------------------- fixups
 __device__ __forceinline__ int cta_of(long long i, long long T, int G) {
     return (int)(((i + 1) * (long long)G - 1) / T);
@@ -1242,10 +1468,11 @@ int encode_rows(CUtensorMap *m, const void *base, unsigned long long rows, unsig
     return BM_OK;
 }
 
+// NMAT 0: GEMM1 with W1 | W3 split over the pair (ffn_gemm1_split_kernel)
 template <int NMAT, int KPS>
 int launch_gemm_2sm(const GemmParams &g, int G, cudaStream_t s) {
     static bool attr = false;
-    auto kern = ffn_gemm_2sm_kernel<NMAT, KPS>;
+    auto kern = NMAT == 0 ? ffn_gemm1_split_kernel<KPS> : ffn_gemm_2sm_kernel<NMAT == 0 ? 1 : NMAT, KPS>;
     if (!attr) {
         BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
         attr = true;
@@ -1271,7 +1498,8 @@ int launch_gemm_2sm(const GemmParams &g, int G, cudaStream_t s) {
     gp.num_ctas = 2 * std::min(G / 2, max_clusters);
     cfg.gridDim = dim3((unsigned)gp.num_ctas);
     PairMaps maps;
-    if (int rc = encode_rows(&maps.a, g.arena, (unsigned long long)(g.arena_bytes / 128), 256)) return rc;
+    if (int rc = encode_rows(&maps.a, g.arena, (unsigned long long)(g.arena_bytes / 128), NMAT == 0 ? 128 : 256))
+        return rc;
     if (int rc = encode_rows(&maps.b, g.b_planes, (unsigned long long)(g.K / kBK) * (g.b_plane_bytes / 128),
                              (unsigned)(g.n_tile / 2)))
         return rc;
@@ -1291,20 +1519,30 @@ int kps_2sm(int nmat, long long K, long long n_tile) {
     return kps;
 }
 
-// Data-parallel (prefill) GEMM2 (one accumulator per tile) with an even
-// number of weight m-tiles runs on CTA pairs (cta_group::2, M = 256) at
-// 256-token tiles: Mixtral 4096 x 2 0.93 -> 0.73 ms. GEMM1 keeps single CTAs:
-// with two accumulators (W1, W3) a pair tile saves only ~8% of the shared-
-// memory traffic per MAC and measured slower (1.74 vs 1.61 ms).
-// BMOE_2SM=0: single CTAs everywhere; 2: GEMM1 on pairs as well.
-bool use_2sm(const GemmParams &g) {
+// Data-parallel (prefill) GEMMs on CTA pairs (cta_group::2, M = 256) at
+// 256-token tiles, one accumulator per CTA (double-buffered TMEM):
+//  * GEMM2 (and a tanh GEMM1): the pair's rows are two weight m-tiles
+//    (even m-tile count): Mixtral 4096 x 2 0.93 -> 0.73 ms;
+//  * SwiGLU GEMM1: the pair's rows are W1 and W3 of one m-tile
+//    (ffn_gemm1_split_kernel, accumulator halves exchanged through DSMEM).
+// BMOE_2SM=0: single CTAs; 2: SwiGLU GEMM1 as two m-tiles x (W1, W3) instead
+// (two accumulators per CTA at 128 tokens; measured slower).
+int two_sm_mode() {
     const char *ev = getenv("BMOE_2SM");
-    const int mode = ev ? atoi(ev) : 1;
-    return g.dp && mode != 0 && (g.nmat == 1 || mode == 2) && (g.M / kBM) % 2 == 0 && g.n_tile >= 32 &&
-           g.n_tile % 32 == 0;
+    return ev ? atoi(ev) : 1;
+}
+bool use_2sm(const GemmParams &g) {
+    const int mode = two_sm_mode();
+    if (!g.dp || mode == 0 || g.n_tile < 32 || g.n_tile % 32) return false;
+    // W1 | W3 split pair: its accumulator exchange costs a few us per tile, paid
+    // back only by long tiles (Mixtral K=4096: 1.66 -> 1.51 ms; Qwen3 K=2048:
+    // 0.45 -> 0.56 ms, so shorter K keeps single CTAs)
+    if (g.nmat == 2 && mode == 1) return g.K >= 4096;
+    return (g.nmat == 1 || mode == 2) && (g.M / kBM) % 2 == 0;
 }
 
 int launch_gemm_2sm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
+    if (g.nmat == 2 && two_sm_mode() == 1) return g.kps == 1 ? launch_gemm_2sm<0, 1>(g, G, s) : launch_gemm_2sm<0, 2>(g, G, s);
     if (g.nmat == 2) return g.kps == 1 ? launch_gemm_2sm<2, 1>(g, G, s) : launch_gemm_2sm<2, 2>(g, G, s);
     return g.kps == 1 ? launch_gemm_2sm<1, 1>(g, G, s) : launch_gemm_2sm<1, 2>(g, G, s);
 }
@@ -1319,7 +1557,13 @@ int launch_gemm_2sm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
 int launch_gemm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
     if (use_2sm(g)) {
         GemmParams g2 = g;
-        g2.kps = kps_2sm(g.nmat, g.K, g.n_tile);
+        if (g.nmat == 2 && two_sm_mode() == 1) {  // W1 | W3 split: 256-token tiles, one matrix per CTA
+            g2.n_tile = 256;
+            if (const char *ev = getenv("BMOE_NT1")) g2.n_tile = atoi(ev);
+            g2.kps = 1;  // 4 stages of 32 KB beside the 66 KB receive buffer
+        } else {
+            g2.kps = kps_2sm(g.nmat, g.K, g.n_tile);
+        }
         return launch_gemm_2sm_dispatch(g2, G, s);
     }
     const char *ev = getenv("BMOE_PAIR");
