@@ -54,8 +54,6 @@ struct Sched {
     int act_off[kMaxE];
     int act_nch[kMaxE];
     int chunk_prefix[kMaxE + 1];
-    int pair_prefix[kMaxE + 1];  // token-chunk PAIRS (CTA-pair prefill): expert a's pair units are
-                                 // [mtiles*pair_prefix[a], mtiles*pair_prefix[a+1]), m-tile major
 };
 
 struct GemmParams {
@@ -90,7 +88,7 @@ __device__ void build_sched_warp(Sched &s, const int32_t *count, const int32_t *
     const int lane = (int)lane_id();
     const int per = (E + 31) / 32;
     int c[kPer];
-    int nact = 0, nch = 0, npr = 0;
+    int nact = 0, nch = 0;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
         const int e = lane * per + i;
@@ -100,22 +98,18 @@ __device__ void build_sched_warp(Sched &s, const int32_t *count, const int32_t *
     for (int i = 0; i < kPer; ++i)
         if (c[i] > 0) {
             ++nact;
-            const int nc = chunks_of(c[i], n_tile);
-            nch += nc;
-            npr += (nc + 1) >> 1;
+            nch += chunks_of(c[i], n_tile);
         }
-    int a = nact, ch = nch, pr = npr;
+    int a = nact, ch = nch;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int ya = __shfl_up_sync(0xffffffffu, a, o), yc = __shfl_up_sync(0xffffffffu, ch, o);
-        const int yp = __shfl_up_sync(0xffffffffu, pr, o);
         if (lane >= o) {
             a += ya;
             ch += yc;
-            pr += yp;
         }
     }
-    int ia = a - nact, ic = ch - nch, ip = pr - npr;
+    int ia = a - nact, ic = ch - nch;
 #pragma unroll
     for (int i = 0; i < kPer; ++i)
         if (c[i] > 0) {
@@ -125,15 +119,12 @@ __device__ void build_sched_warp(Sched &s, const int32_t *count, const int32_t *
             s.act_off[ia] = offset[e];
             s.act_nch[ia] = nc;
             s.chunk_prefix[ia] = ic;
-            s.pair_prefix[ia] = ip;
             ic += nc;
-            ip += (nc + 1) >> 1;
             ++ia;
         }
     if (lane == 31) {
         s.n_act = a;
         s.chunk_prefix[a] = ch;
-        s.pair_prefix[a] = pr;
     }
 }
 
@@ -195,55 +186,6 @@ struct SegIter {
     }
 };
 
-// Work of one CTA as (tile, k-steps, ghost) items: CL = 1 walks SegIter
-// tiles; CL = 2 (a CTA pair of a thread-block cluster, data-parallel) walks
-// pair units cta, cta+G, ... where `cta` is the cluster index.
-__device__ __forceinline__ TileInfo decode_pair(const Sched &s, int u, int mtiles, int n_tile, int rank, bool &ghost);
-
-template <int CL>
-struct WorkIter {
-    SegIter seg;
-    const Sched *s;
-    int mtiles, n_tile, rank;
-    __device__ __forceinline__ bool next(TileInfo &ti, int &tile, int &st0, int &st1, bool &ghost) {
-        if constexpr (CL == 1) {
-            if (!seg.next(tile, st0, st1)) return false;
-            ti = decode_tile(*s, tile, mtiles, n_tile);
-            ghost = false;
-            return true;
-        } else {
-            tile = seg.cta + (seg.seg++) * seg.G;
-            if (tile >= seg.ntiles) return false;
-            ti = decode_pair(*s, tile, mtiles, n_tile, rank, ghost);
-            st0 = 0;
-            st1 = seg.spt;
-            return true;
-        }
-    }
-};
-
-// CTA-pair prefill unit u: weight m-tile `mtile` of an expert for the token
-// chunks 2*cp (rank 0) and 2*cp + 1 (rank 1). A rank whose chunk does not
-// exist (odd chunk count) is a "ghost": it still loads and multicasts its
-// half of the weight block for its peer but computes nothing.
-__device__ __forceinline__ TileInfo decode_pair(const Sched &s, int u, int mtiles, int n_tile, int rank, bool &ghost) {
-    int lo = 0, hi = s.n_act - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s.pair_prefix[mid] * mtiles <= u) lo = mid; else hi = mid - 1;
-    }
-    TileInfo ti;
-    ti.e = s.act_e[lo];
-    const int np = s.pair_prefix[lo + 1] - s.pair_prefix[lo];
-    const int local = u - s.pair_prefix[lo] * mtiles;
-    ti.mtile = local / np;
-    ti.chunk = 2 * (local % np) + rank;
-    ghost = ti.chunk >= s.act_nch[lo];
-    const int npad = (s.act_cnt[lo] + 15) & ~15;
-    ti.n = ghost ? 0 : min(n_tile, npad - ti.chunk * n_tile);
-    ti.row0 = s.act_off[lo] + ti.chunk * n_tile;
-    return ti;
-}
 
 // Expert activation in the bf16 epilogues (its output is rounded to bf16):
 // SwiGLU silu(g)*u with ex2.approx / rcp.approx, tanh with tanh.approx —
@@ -295,14 +237,7 @@ __device__ __forceinline__ void finish16(const GemmParams &p, const TileInfo &ti
     }
 }
 
-// CL = 2 (prefill, data-parallel): the two CTAs of a cluster work on the
-// same weight m-tile for two token chunks; each loads HALF of every weight
-// stage and multicasts it into both CTAs' shared memory, so a weight block
-// crosses L2 -> SM once per pair instead of once per CTA (the operand feed,
-// not the tensor pipe, bounds the single-CTA prefill tiles). A stage is
-// refilled once BOTH CTAs' MMAs released it (multicast tcgen05.commit into
-// each CTA's empty barrier, count 2).
-template <int NMAT, int KPS, int CL>
+template <int NMAT, int KPS>
 __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ Sched sched;
@@ -318,13 +253,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
     __syncthreads();
     const int ntiles = total_tiles(sched, mtiles);
     const long long T = (long long)ntiles * steps_per_tile;
-    const int rank = CL == 2 ? (int)ptx::cluster_ctarank() : 0;
-    const int units = CL == 2 ? sched.pair_prefix[sched.n_act] * mtiles : ntiles;  // pair units (CL 2)
-    const int G = CL == 2 ? min(p.num_ctas / 2, units) : (int)min((long long)p.num_ctas, p.dp ? (long long)ntiles : T);
-    const int cta = CL == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-    if (cta >= G) return;  // uniform for the whole CTA (and for both CTAs of a pair)
+    const int G = (int)min((long long)p.num_ctas, p.dp ? (long long)ntiles : T);
+    const int cta = (int)blockIdx.x;
+    if (cta >= G) return;  // uniform for the whole CTA
     const long long it0 = range_start(cta, T, G), it1 = range_start(cta + 1, T, G);
-    const SegIter seg0(CL == 2 || p.dp, cta, G, units, steps_per_tile, it0, it1);
+    const SegIter seg0(p.dp, cta, G, ntiles, steps_per_tile, it0, it1);
 
     // smem: stages of [A: KPS x NMAT x 16 KB | B: KPS x bsz], 1024-aligned
     constexpr uint32_t kAStage = (uint32_t)(KPS * NMAT) * kATileBytes;
@@ -344,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < stages; ++s) {
             ptx::mbar_init(full0 + 8 * s, 1);
-            ptx::mbar_init(empty0 + 8 * s, CL);  // CL 2: both CTAs' MMAs release a stage
+            ptx::mbar_init(empty0 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(tfull0 + 8 * a, 1);
@@ -355,7 +288,6 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
     if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(&tmem_base_sh), 512);
     ptx::tc_fence_before();
     __syncthreads();
-    if constexpr (CL == 2) ptx::cluster_sync();  // the peer's barriers are initialised before any multicast
     ptx::tc_fence_after();
     const uint32_t tmem_base = tmem_base_sh;
 
@@ -364,11 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         const uint64_t pol = ptx::policy_evict_first();  // decode: weights stream through once
         int stage = 0;
         uint32_t phase = 0;
-        WorkIter<CL> w{seg0, &sched, mtiles, p.n_tile, rank};
-        TileInfo ti;
+        SegIter w = seg0;
         int tile, st_beg, st_end;
-        bool ghost;
-        while (w.next(ti, tile, st_beg, st_end, ghost)) {
+        while (w.next(tile, st_beg, st_end)) {
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
             const int buf = p.buf_of_expert[ti.e];
             // the m-tile's blocks are contiguous along k: [mt][kb][NMAT][16 KB]
             const uint8_t *a_src = p.arena + (long long)buf * p.buf_bytes + p.mat_off +
@@ -384,30 +315,15 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
                     ptx::mbar_arrive(fb);
                 } else {
                 ptx::mbar_expect_tx(fb, kAStage + (uint32_t)KPS * bbytes);
-                if constexpr (CL == 2) {  // my half of the weight stage, into both CTAs
-                    constexpr uint32_t kHalf = kAStage / 2;
-                    ptx::bulk_load_multicast(sA + (uint32_t)rank * kHalf,
-                                             a_src + (long long)st * kAStage + (long long)rank * kHalf, kHalf, fb, 0x3);
-                } else if (p.dp) {  // the CTAs on the m-tile's other chunks read the same block: keep it in L2
+                if (p.dp) {  // the CTAs on the m-tile's other chunks read the same block: keep it in L2
                     ptx::bulk_load(sA, a_src + (long long)st * kAStage, kAStage, fb);
                 } else {
                     ptx::bulk_load_hint(sA, a_src + (long long)st * kAStage, kAStage, fb, pol);
                 }
-                if (bbytes) {
 #pragma unroll
-                    for (int i = 0; i < KPS; ++i)
-                        ptx::bulk_load(sB + i * bsz, b_src + (long long)(st * KPS + i) * p.b_plane_bytes, bbytes, fb);
+                for (int i = 0; i < KPS; ++i)
+                    ptx::bulk_load(sB + i * bsz, b_src + (long long)(st * KPS + i) * p.b_plane_bytes, bbytes, fb);
                 }
-                }
-                if (++stage == stages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-            }
-        }
-        if constexpr (CL == 2) {  // every stage released by both CTAs: no remote arrive is still in flight
-            for (int i = 0; i < stages; ++i) {
-                ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1u);
                 if (++stage == stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -424,16 +340,13 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        WorkIter<CL> w{seg0, &sched, mtiles, p.n_tile, rank};
-        TileInfo ti;
+        SegIter w = seg0;
         int tile, st_beg, st_end;
-        bool ghost;
-        while (w.next(ti, tile, st_beg, st_end, ghost)) {
-            const uint32_t idesc = ptx::idesc_bf16_f32(kBM, (uint32_t)max(ti.n, 16));
-            if (!ghost) {
-                ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1u);
-                ptx::tc_fence_after();
-            }
+        while (w.next(tile, st_beg, st_end)) {
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
+            const uint32_t idesc = ptx::idesc_bf16_f32(kBM, (uint32_t)ti.n);
+            ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1u);
+            ptx::tc_fence_after();
             const uint32_t d0 = tmem_base + (uint32_t)acc * acc_cols;
             const uint32_t d1 = d0 + (uint32_t)p.n_tile;
             uint32_t accum = 0;
@@ -442,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
                 ptx::tc_fence_after();
                 const uint64_t a = desc0 + (uint64_t)stage * stage_d;
                 const uint64_t b = a + (kAStage >> 4);
-                if (!ghost && p.probe != 1) {
+                if (p.probe != 1) {
 #pragma unroll
                     for (int i = 0; i < KPS; ++i) {
                         const uint64_t bi = b + (uint64_t)i * bsz_d;
@@ -457,17 +370,12 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
                         }
                     }
                 }
-                // frees the smem stage when these MMAs finish (CL 2: in both CTAs)
-                if constexpr (CL == 2)
-                    ptx::mma_commit_multicast(empty0 + 8 * stage, 0x3);
-                else
-                    ptx::mma_commit(empty0 + 8 * stage);
+                ptx::mma_commit(empty0 + 8 * stage);  // frees the smem stage when these MMAs finish
                 if (++stage == stages) {
                     stage = 0;
                     phase ^= 1u;
                 }
             }
-            if (ghost) continue;  // no accumulator was used
             ptx::mma_commit(tfull0 + 8 * acc);  // accumulator ready for the epilogue
             if (acc_stages == 2) {
                 acc ^= 1;
@@ -482,12 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         const int m_local = q * 32 + (int)lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        WorkIter<CL> w{seg0, &sched, mtiles, p.n_tile, rank};
-        TileInfo ti;
+        SegIter w = seg0;
         int tile, st_beg, st_end;
-        bool ghost;
-        while (w.next(ti, tile, st_beg, st_end, ghost)) {
-            if (ghost) continue;
+        while (w.next(tile, st_beg, st_end)) {
+            const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
             // this CTA owns the whole tile: finish it here (activation / output),
             // otherwise park an fp32 partial for the deterministic fixup
             const bool whole = p.fuse && st_beg == 0 && st_end == steps_per_tile;
@@ -528,7 +434,6 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
     __syncwarp();
     ptx::tc_fence_before();
     __syncthreads();
-    if constexpr (CL == 2) ptx::cluster_sync();  // neither CTA leaves while its peer may still multicast into it
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
 }
@@ -1390,56 +1295,28 @@ int record_event(cudaStream_t s) {
 
 typedef void (*GemmFn)(GemmParams);
 
-template <int NMAT, int KPS, int CL>
+template <int NMAT, int KPS>
 int launch_gemm(const GemmParams &g, int G, cudaStream_t s) {
     static bool attr = false;
-    auto kern = ffn_gemm_kernel<NMAT, KPS, CL>;
+    auto kern = ffn_gemm_kernel<NMAT, KPS>;
     if (!attr) {
         BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
         attr = true;
     }
-    if constexpr (CL == 1) {
-        kern<<<G, kThreads, kSmemBudget, s>>>(g);
-    } else {  // CTA pairs: thread-block clusters of 2
-        cudaLaunchConfig_t cfg = {};
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = kSmemBudget;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        // persistent pairs: only as many clusters as can be co-resident (an SM
-        // left alone in its GPC cannot host half a pair), or a second wave of
-        // pairs would serialise behind the first
-        static int max_clusters = 0;
-        if (!max_clusters) {
-            cfg.gridDim = dim3((unsigned)(G & ~1));
-            BM_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
-            if (max_clusters < 1) max_clusters = 1;
-        }
-        GemmParams gp = g;
-        gp.num_ctas = 2 * std::min(G / 2, max_clusters);
-        cfg.gridDim = dim3((unsigned)gp.num_ctas);
-        BM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, gp));
-    }
+    kern<<<G, kThreads, kSmemBudget, s>>>(g);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }
 
-template <int CL>
-int launch_gemm_cl(const GemmParams &g, int G, cudaStream_t s) {
+int launch_gemm_1sm(const GemmParams &g, int G, cudaStream_t s) {
     if (g.nmat == 2) {
-        if (g.kps == 1) return launch_gemm<2, 1, CL>(g, G, s);
-        if (g.kps == 2) return launch_gemm<2, 2, CL>(g, G, s);
-        return launch_gemm<2, 4, CL>(g, G, s);
+        if (g.kps == 1) return launch_gemm<2, 1>(g, G, s);
+        if (g.kps == 2) return launch_gemm<2, 2>(g, G, s);
+        return launch_gemm<2, 4>(g, G, s);
     }
-    if (g.kps == 1) return launch_gemm<1, 1, CL>(g, G, s);
-    if (g.kps == 2) return launch_gemm<1, 2, CL>(g, G, s);
-    return launch_gemm<1, 4, CL>(g, G, s);
+    if (g.kps == 1) return launch_gemm<1, 1>(g, G, s);
+    if (g.kps == 2) return launch_gemm<1, 2>(g, G, s);
+    return launch_gemm<1, 4>(g, G, s);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda):
@@ -1547,13 +1424,6 @@ int launch_gemm_2sm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
     return g.kps == 1 ? launch_gemm_2sm<1, 1>(g, G, s) : launch_gemm_2sm<1, 2>(g, G, s);
 }
 
-// BMOE_PAIR=1 runs the data-parallel (prefill) GEMMs as CTA pairs that
-// share each weight stage through a cluster multicast. Off by default: it
-// halves the L2 reads of the weights but not the bytes each SM must hold in
-// flight, and the prefill GEMM is bound by how far its 2-stage (~192 KB)
-// operand pipeline can run ahead of the MMAs, not by L2 (profiles/README.md:
-// MMAs alone 1.30 ms, operand feed alone 0.99 ms, both 1.65 ms at Mixtral
-// 4096 x 2; pairs 1.65 ms). Results are bitwise identical either way.
 int launch_gemm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
     if (use_2sm(g)) {
         GemmParams g2 = g;
@@ -1566,9 +1436,7 @@ int launch_gemm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
         }
         return launch_gemm_2sm_dispatch(g2, G, s);
     }
-    const char *ev = getenv("BMOE_PAIR");
-    if (g.dp && ev && atoi(ev) != 0 && G >= 2) return launch_gemm_cl<2>(g, G, s);
-    return launch_gemm_cl<1>(g, G, s);
+    return launch_gemm_1sm(g, G, s);
 }
 
 template <int NMAT1, int KPS1, int KPS2>

@@ -401,34 +401,6 @@ def test_fused_single_launch_equals_multi_kernel(cuda_ok, E, d, f, B, k, act, n_
 
 
 @pytest.mark.parametrize("E,d,f,B,k,act", [
-    (8, 1024, 2048, 700, 2, ops.ACT_SWIGLU),   # odd chunk counts per expert -> ghost CTAs in the pairs
-    (16, 512, 1024, 333, 3, ops.ACT_TANH),
-])
-def test_prefill_cta_pairs_equal_single_ctas(cuda_ok, E, d, f, B, k, act):
-    """BMOE_PAIR=1 (CTA pairs sharing weight stages by cluster multicast,
-    ghost CTAs for odd chunk counts) computes every tile with the same MMAs
-    in the same order as single CTAs: bitwise equal outputs."""
-    import os
-    rng = np.random.default_rng(B)
-    _, _, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, act, 128)
-    rows = int(perm.offset[-1])
-    bo = _t(buf_of)
-    old = os.environ.get("BMOE_PAIR")
-    try:
-        os.environ["BMOE_PAIR"] = "0"
-        ref = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows].clone()
-        os.environ["BMOE_PAIR"] = "1"
-        for _ in range(3):
-            y = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows]
-            assert torch.equal(y, ref)
-    finally:
-        if old is None:
-            os.environ.pop("BMOE_PAIR", None)
-        else:
-            os.environ["BMOE_PAIR"] = old
-
-
-@pytest.mark.parametrize("E,d,f,B,k,act", [
     (8, 1024, 2048, 700, 2, ops.ACT_SWIGLU),
     (4, 512, 1536, 1000, 2, ops.ACT_SWIGLU),
     (16, 512, 1024, 333, 3, ops.ACT_TANH),
