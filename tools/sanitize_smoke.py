@@ -53,7 +53,16 @@ if __name__ == "__main__":
     perm = ops.permute(torch.from_numpy(tk).cuda(), torch.zeros(B3, 2, dtype=torch.uint8).cuda(), E2)
     xp = ops.gather_rows(torch.randn(B3, d).cuda(), perm, 1)
     ws = ops.FfnWorkspace(E2, d, f, perm.r_max, 128)
-    ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)
+    ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)  # GEMM2 on CTA pairs
+    # K = 4096: SwiGLU GEMM1 on CTA pairs too (W1 | W3 split, DSMEM exchange)
+    E3, d3, f3 = 4, 4096, 1024
+    tk = np.stack([rng.choice(E3, 2, replace=False) for _ in range(B3)]).astype(np.int32)
+    perm = ops.permute(torch.from_numpy(tk).cuda(), torch.zeros(B3, 2, dtype=torch.uint8).cuda(), E3)
+    xp = ops.gather_rows(torch.randn(B3, d3).cuda(), perm, 1)
+    w3 = (torch.randn(E3, 3 * d3 * f3).cuda() * 0.02).to(torch.bfloat16)
+    arena3 = ops.pack_arena_bf16(w3, d3, f3, ops.ACT_SWIGLU)
+    ws = ops.FfnWorkspace(E3, d3, f3, perm.r_max, 128)
+    ops.expert_ffn_bf16(xp, perm, arena3, torch.arange(E3, dtype=torch.int32).cuda(), d3, f3, ops.ACT_SWIGLU, ws)
     torch.cuda.synchronize()
     # decode engine over exponent-coded mirrors (staging ring + piece decoder + prefetch stream)
     from paper_2511_10054_b200 import workload as W
