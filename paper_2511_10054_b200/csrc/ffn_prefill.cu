@@ -825,7 +825,8 @@ int launch_gemm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
         if (g.nmat == 2 && two_sm_mode() == 1) {  // W1 | W3 split: 256-token tiles, one matrix per CTA
             g2.n_tile = 256;
             if (const char *ev = getenv("BMOE_NT1")) g2.n_tile = atoi(ev);
-            g2.kps = 1;  // 4 stages of 32 KB beside the 66 KB receive buffer
+            g2.kps = 1;  // 5 stages of 32 KB beside the 35 KB receive buffer
+            if (const char *kv = getenv("BMOE_KPS_SPLIT")) g2.kps = (atoi(kv) == 2 && (g.K / kBK) % 2 == 0) ? 2 : 1;
         } else {
             g2.kps = kps_2sm(g.nmat, g.K, g.n_tile);
         }

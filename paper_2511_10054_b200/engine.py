@@ -91,6 +91,17 @@ class SharedMirror:
     def as_tensor(self, dtype=torch.uint8) -> torch.Tensor:
         return torch.frombuffer(self._buf, dtype=torch.uint8).view(dtype)
 
+    def unlink(self):
+        """Remove the file name; the mappings stay valid until every process
+        closes them (the kernel frees the pages then, even after a crash)."""
+        import os
+        if self.owner:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+            self.owner = False
+
     def close(self):
         import os
         if getattr(self, "_mm", None) is None:

@@ -199,6 +199,10 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
         share.barrier()
         if not share.owner:
             mirrors = [SharedMirror(share.path(l)) for l in range(layers)]
+        share.barrier()  # every rank has mapped every layer: drop the names, so a crash cannot leak /dev/shm
+        if share.owner:
+            for m in mirrors:
+                m.unlink()
     initial = [initial_residents(E, cap, 0, l) for l in range(layers)]
     es = EngineSpec(num_layers=layers, num_experts=E, top_k=k, d=d, f=f, capacity=cap, max_batch=max_batch,
                     act=ops.ACT_SWIGLU, search_rank_h=k_max, rho=rho, n_tile=n_tile, expert_bytes=buf_bytes,
