@@ -369,10 +369,12 @@ int64_t bm_engine_device_bytes(const bm_engine *e);
  * reference counterpart: the reference's transfer is an analytic cost,
  * memtier.py:41-58; this only changes how many bytes cross PCIe, never the
  * bytes that land in HBM). A value keeps its sign+mantissa byte; its exponent
- * becomes a 3-bit code against a per-2048-value window (7 binades), code 7
- * escaping to a per-chunk exponent stream. ~11.2 bits per value for
+ * becomes a 2-bit code for the chunk's (2048 values) three most frequent
+ * exponents, or an escape followed by a 3-bit code for the next seven (code
+ * 7: the exponent byte in the piece's raw list). ~10.9 bits per value for
  * N(0, s) weights. Blobs are split into self-contained pieces of
- * BM_XFER_PIECE_VALUES values (the fetch pipeline's unit). */
+ * BM_XFER_PIECE_VALUES values (the fetch pipeline's unit); xfer.cu
+ * documents the piece layout. */
 #define BM_XFER_PIECE_VALUES (32 * 1024 * 1024)
 typedef struct {
     uint32_t magic;        /* "BXC1" */
@@ -383,9 +385,9 @@ typedef struct {
     uint64_t piece_off[1]; /* [n_pieces + 1] byte offsets from the blob start; the last = blob bytes */
 } bm_xfer_blob_header;
 typedef struct {
-    uint32_t magic; /* "BXP1" */
-    uint32_t n_chunks, n_esc;
-    uint32_t off_planes, off_base, off_escoff, off_esc, bytes; /* from the piece start; low bytes at 32 */
+    uint32_t magic; /* "BXP2" */
+    uint32_t n_chunks, n_raw;
+    uint32_t off_planes, off_meta, off_l2, off_raw, bytes; /* from the piece start; low bytes at 32 */
 } bm_xfer_piece_header;
 typedef struct {
     uint32_t magic; /* "BXL1" */

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _np_decode(blob: np.ndarray) -> np.ndarray:
-    """Reference decoder written from the header comments in bmoe.h/xfer.cu."""
+    """Reference decoder written from the format comments in bmoe.h/xfer.cu (v2)."""
     u32 = lambda a, o: int(np.frombuffer(a[o:o + 4].tobytes(), np.uint32)[0])
     u64 = lambda a, o: int(np.frombuffer(a[o:o + 8].tobytes(), np.uint64)[0])
     assert u32(blob, 0) == 0x31435842
@@ -25,19 +25,28 @@ def _np_decode(blob: np.ndarray) -> np.ndarray:
     out = []
     for p in range(n_pieces):
         pb = blob[offs[p]:offs[p + 1]]
-        magic, nch, nesc, o_pl, o_base, o_eo, o_esc, nbytes = np.frombuffer(pb[:32].tobytes(), np.uint32)
-        assert magic == 0x31505842 and nbytes == pb.size
+        magic, nch, nraw, o_pl, o_meta, o_l2, o_raw, nbytes = np.frombuffer(pb[:32].tobytes(), np.uint32)
+        assert magic == 0x32505842 and nbytes == pb.size
         low = pb[32:32 + nch * 2048].reshape(nch, 2048).astype(np.uint16)
-        planes = pb[o_pl:o_pl + nch * 768].reshape(nch, 3, 256)
-        bits = np.unpackbits(planes[..., None], axis=-1, bitorder="little")  # [nch,3,256,8]: bit j of byte t
-        code = (bits[:, 0] | (bits[:, 1] << 1) | (bits[:, 2] << 2)).reshape(nch, 2048).astype(np.uint16)
-        base = pb[o_base:o_base + nch].astype(np.uint16)
-        eo = np.frombuffer(pb[o_eo:o_eo + 4 * nch].tobytes(), np.uint32)
-        esc = pb[o_esc:o_esc + nesc].astype(np.uint16)
-        exp = base[:, None] + code
+        planes = pb[o_pl:o_pl + nch * 512].reshape(nch, 2, 256)
+        bits = np.unpackbits(planes[..., None], axis=-1, bitorder="little")  # [nch,2,256,8]: bit j of byte t
+        code1 = (bits[:, 0] | (bits[:, 1] << 1)).reshape(nch, 2048)
+        meta = np.frombuffer(pb[o_meta:o_meta + 24 * nch].tobytes(), np.uint32).reshape(nch, 6)
+        raw = np.frombuffer(pb[o_raw:o_raw + 4 * nraw].tobytes(), np.uint32)
+        exp = np.zeros((nch, 2048), np.uint16)
         for c in range(nch):
-            m = code[c] == 7
-            exp[c, m] = esc[eo[c]:eo[c] + int(m.sum())]
+            t1 = [(int(meta[c, 0]) >> (8 * q)) & 0xFF for q in range(3)]
+            t2 = [(int(meta[c, 1 + q // 4]) >> (8 * (q % 4))) & 0xFF for q in range(7)]
+            l2off, rawoff, rawn = int(meta[c, 3]), int(meta[c, 4]), int(meta[c, 5])
+            esc = np.flatnonzero(code1[c] == 3)
+            stream = np.unpackbits(pb[o_l2 + l2off:o_l2 + l2off + (3 * esc.size + 7) // 8], bitorder="little")
+            entries = {int(e) & 0xFFFF: (int(e) >> 16) & 0xFF for e in raw[rawoff:rawoff + rawn]}
+            for v in range(2048):
+                if code1[c, v] < 3:
+                    exp[c, v] = t1[code1[c, v]]
+            for i, v in enumerate(esc):
+                k2 = int(stream[3 * i]) | (int(stream[3 * i + 1]) << 1) | (int(stream[3 * i + 2]) << 2)
+                exp[c, v] = t2[k2] if k2 < 7 else entries[int(v)]
         out.append(((low & 0x80) << 8) | (exp << 7) | (low & 0x7F))
     v = np.concatenate([o.ravel() for o in out])
     assert v.size == n_values and (n_pieces == 1 or piece_values == 32 * 1024 * 1024)
@@ -73,7 +82,7 @@ def test_roundtrip_bit_exact(cuda_ok, n):
 
 
 def test_ratio_and_piecewise_decode(cuda_ok):
-    """N(0, 1/sqrt(fan_in)) weights: <= 0.71 of the raw bytes; decoding the
+    """N(0, 1/sqrt(fan_in)) weights: <= 0.69 of the raw bytes; decoding the
     pieces one by one (the engine's pipeline) equals the whole-blob decode."""
     from paper_2511_10054_b200 import _native as N
     n = 3 * 4096 * 14336 // 2  # half a Mixtral expert, 3 pieces
@@ -83,7 +92,7 @@ def test_ratio_and_piecewise_decode(cuda_ok):
     blob = ops.xfer_encode(x)
     ratio = blob.numel() / (2 * n)
     print(f"coded/raw = {ratio:.4f}")
-    assert ratio <= 0.71
+    assert ratio <= 0.69
     hb = blob[:256].cpu().numpy()
     n_pieces = int(np.frombuffer(hb[4:8].tobytes(), np.uint32)[0])
     offs = np.frombuffer(blob[24:24 + 8 * (n_pieces + 1)].cpu().numpy().tobytes(), np.uint64)
@@ -101,7 +110,7 @@ def test_ratio_and_piecewise_decode(cuda_ok):
 def test_engine_coded_mirrors_equal_raw(cuda_ok):
     """Qwen3 shape, bf16 engine, 3 layers, 4 decode steps: coded vs raw
     mirrors -> identical event logs and bitwise-identical hidden states;
-    wire bytes <= 0.71 of the expert bytes fetched."""
+    wire bytes <= 0.70 of the expert bytes fetched (small Qwen3 experts: one piece each)."""
     from paper_2511_10054_b200 import workload as W
     from paper_2511_10054_b200.engine import mirror_expert
     outs, evs, stats, w = [], [], [], []
@@ -123,4 +132,4 @@ def test_engine_coded_mirrors_equal_raw(cuda_ok):
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
     assert stats[0]["h2d_bytes"] == stats[1]["h2d_bytes"] > 0
     assert stats[0]["wire_bytes"] == stats[0]["h2d_bytes"]
-    assert stats[1]["wire_bytes"] <= 0.71 * stats[1]["h2d_bytes"], stats[1]
+    assert stats[1]["wire_bytes"] <= 0.70 * stats[1]["h2d_bytes"], stats[1]
