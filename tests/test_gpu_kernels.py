@@ -404,6 +404,7 @@ def test_fused_single_launch_equals_multi_kernel(cuda_ok, E, d, f, B, k, act, n_
     (8, 1024, 2048, 700, 2, ops.ACT_SWIGLU),
     (4, 512, 1536, 1000, 2, ops.ACT_SWIGLU),
     (16, 512, 1024, 333, 3, ops.ACT_TANH),
+    (4, 4096, 1024, 300, 2, ops.ACT_SWIGLU),  # K = 4096: SwiGLU GEMM1 on W1|W3-split pairs
 ])
 def test_prefill_2sm_pairs_equal_single_cta(cuda_ok, E, d, f, B, k, act):
     """Prefill GEMMs on CTA pairs (cta_group::2, M = 256, the token half of
@@ -416,19 +417,21 @@ def test_prefill_2sm_pairs_equal_single_cta(cuda_ok, E, d, f, B, k, act):
     y, ref32, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, act, 128)
     rows = int(perm.offset[-1])
     bo = _t(buf_of)
-    old = os.environ.get("BMOE_2SM")
+    old = {v: os.environ.get(v) for v in ("BMOE_2SM",)}
     try:
         os.environ["BMOE_2SM"] = "0"
         single = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows].clone()
-        for mode in ("1", "2"):  # GEMM2 on pairs (default); both GEMMs on pairs
+        # GEMM2 on pairs (+ W1|W3-split GEMM1 at K >= 4096: default); both GEMMs as two-m-tile pairs
+        for mode in ("1", "2"):
             os.environ["BMOE_2SM"] = mode
             for _ in range(3):
                 pair = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows]
                 assert torch.equal(pair, single), mode
     finally:
-        if old is None:
-            os.environ.pop("BMOE_2SM", None)
-        else:
-            os.environ["BMOE_2SM"] = old
+        for v, val in old.items():
+            if val is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = val
     rel = (torch.linalg.norm(y - ref32, dim=1) / torch.linalg.norm(ref32, dim=1).clamp_min(1e-30)).max().item()
     assert rel <= 2e-2, rel
