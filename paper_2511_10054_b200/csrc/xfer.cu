@@ -194,16 +194,13 @@ __device__ __forceinline__ uint32_t spread4(uint32_t x) {
     return (x | (x << 3) | (x << 6) | (x << 9)) & 0x1111u;
 }
 
-// 3 bits at relative bit r (0 <= r <= 125) of the 128-bit window {a, b}
-__device__ __forceinline__ uint32_t bits3(uint64_t a, uint64_t b, uint32_t r) {
-    uint64_t x;
-    if (r >= 64)
-        x = b >> (r - 64);
-    else if (r > 61)
-        x = (a >> r) | (b << (64 - r));
-    else
-        x = a >> r;
-    return (uint32_t)x & 7u;
+// 3 bits at relative bit r (0 <= r <= 125) of the 128-bit window {w0..w3},
+// branch-free (selects + one funnel shift)
+__device__ __forceinline__ uint32_t bits3(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t r) {
+    const uint32_t i = r >> 5;
+    const uint32_t lo = i == 0 ? w0 : (i == 1 ? w1 : (i == 2 ? w2 : w3));
+    const uint32_t hi = i == 0 ? w1 : (i == 1 ? w2 : w3);
+    return __funnelshift_r(lo, hi, r & 31) & 7u;
 }
 
 // Decoder: a warp owns half a chunk (1024 values), a lane 32 consecutive
@@ -233,10 +230,12 @@ __device__ __forceinline__ void decode_half(const uint8_t *__restrict__ pb, cons
     // 128-bit window of the level-2 stream starting at the word holding bit 3*pre
     const uint32_t sb = 3u * (uint32_t)pre;
     const uint32_t *l2 = reinterpret_cast<const uint32_t *>(pb + ph.off_l2 + l2off) + (sb >> 5);
-    uint64_t wa = 0, wb = 0;
+    uint32_t x0 = 0, x1 = 0, x2 = 0, x3 = 0;
     if (mine) {
-        wa = (uint64_t)__ldg(l2) | ((uint64_t)__ldg(l2 + 1) << 32);
-        wb = (uint64_t)__ldg(l2 + 2) | ((uint64_t)__ldg(l2 + 3) << 32);
+        x0 = __ldg(l2);
+        x1 = __ldg(l2 + 1);
+        x2 = __ldg(l2 + 2);
+        x3 = __ldg(l2 + 3);
     }
     const uint32_t *raw = reinterpret_cast<const uint32_t *>(pb + ph.off_raw) + rawoff;
     const uint32_t lw[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
@@ -248,17 +247,14 @@ __device__ __forceinline__ void decode_half(const uint8_t *__restrict__ pb, cons
         const uint32_t sel = spread4(w0 >> (4 * g)) | (spread4(w1 >> (4 * g)) << 1);
         uint32_t e4 = __byte_perm(t1, 0, sel);  // code 3 picks t1's zero byte 3: patched below
         uint32_t em = (escm >> (4 * g)) & 0xFu;
-        while (em) {
+        while (em) {  // the group's escapes, each consuming the next 3-bit level-2 code
             const int j = __ffs(em) - 1;
             em &= em - 1;
-            const uint32_t k2 = bits3(wa, wb, r);
+            const uint32_t k2 = bits3(x0, x1, x2, x3, r);
             r += 3;
-            uint32_t e;
-            if (k2 < 7) {
-                e = byte_of(t2lo, t2hi, k2);
-            } else {  // raw: the chunk's raw list, by position
+            uint32_t e = byte_of(t2lo, t2hi, k2);  // code 7 selects t2hi's zero byte 3
+            if (k2 == 7) {  // raw: the chunk's raw list, by position
                 const uint32_t pos = (uint32_t)(wi * 32 + 4 * g + j);
-                e = 0;
                 for (uint32_t i = 0; i < rawn; ++i) {
                     const uint32_t ent = __ldg(raw + i);
                     if ((ent & 0xFFFFu) == pos) e = (ent >> 16) & 0xFFu;
@@ -278,7 +274,7 @@ __device__ __forceinline__ void decode_half(const uint8_t *__restrict__ pb, cons
     for (int q = 0; q < 4; ++q) o[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
 }
 
-__global__ void __launch_bounds__(kThreads) xfer_decode_piece_kernel(const uint8_t *__restrict__ piece,
+__global__ void __launch_bounds__(kThreads, 4) xfer_decode_piece_kernel(const uint8_t *__restrict__ piece,
                                                                      uint16_t *__restrict__ dst) {
     const bm_xfer_piece_header ph = *reinterpret_cast<const bm_xfer_piece_header *>(piece);
     const int warps = kThreads / 32;
@@ -287,7 +283,7 @@ __global__ void __launch_bounds__(kThreads) xfer_decode_piece_kernel(const uint8
         decode_half(piece, ph, u >> 1, (int)(u & 1), dst);
 }
 
-__global__ void __launch_bounds__(kThreads) xfer_decode_blob_kernel(const uint8_t *__restrict__ blob, int64_t n_chunks,
+__global__ void __launch_bounds__(kThreads, 4) xfer_decode_blob_kernel(const uint8_t *__restrict__ blob, int64_t n_chunks,
                                                                     uint16_t *__restrict__ dst) {
     const auto *bh = reinterpret_cast<const bm_xfer_blob_header *>(blob);
     const int64_t cpp = bh->piece_values / kChunk;
