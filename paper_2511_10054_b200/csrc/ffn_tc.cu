@@ -91,6 +91,8 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
                                   int64_t E, int64_t d, int64_t f, int32_t act, const void *w_arena, int64_t n_bufs,
                                   const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
                                   int64_t workspace_bytes, float *y_perm, bm_stream_t stream) {
+    BM_REQUIRE(r_max >= 0, BM_EINVAL, "r_max must be >= 0");
+    if (r_max == 0) return BM_OK;  // no rows (an empty batch): nothing to compute
     BM_REQUIRE(x_perm && expert_count && expert_offset && w_arena && buf_of_expert && workspace && y_perm,
                BM_EINVAL, "bm_expert_ffn_bf16: null pointer");
     BM_REQUIRE(E >= 1 && E <= kMaxE, BM_EINVAL, "E out of range");

@@ -174,8 +174,8 @@ extern "C" int bm_gate_topk(const float *x, const float *wg, const float *bias, 
                "bm_gate_topk: bad shape B=%lld E=%lld d=%lld k=%lld", (long long)B, (long long)E, (long long)d,
                (long long)k);
     BM_REQUIRE(temperature > 0.0, BM_EINVAL, "temperature must be > 0");
+    if (B == 0) return BM_OK;  // empty batch (its tensors may have null data pointers)
     BM_REQUIRE(x && wg && topk, BM_EINVAL, "bm_gate_topk: null pointer");
-    if (B == 0) return BM_OK;
     size_t smem = (size_t)d * sizeof(float);
     BM_REQUIRE(smem <= 200 * 1024, BM_EINVAL, "bm_gate_topk: d=%lld too large", (long long)d);
     if (smem > 48 * 1024)
@@ -193,8 +193,8 @@ extern "C" int bm_select_topk_f64(const double *logits, int64_t B, int64_t E, in
     BM_REQUIRE(B >= 0 && E >= 1 && E <= kMaxE && k >= 1 && k <= kMaxK && k <= E, BM_EINVAL,
                "bm_select_topk_f64: bad shape");
     BM_REQUIRE(temperature > 0.0, BM_EINVAL, "temperature must be > 0");
-    BM_REQUIRE(logits && topk, BM_EINVAL, "bm_select_topk_f64: null pointer");
     if (B == 0) return BM_OK;
+    BM_REQUIRE(logits && topk, BM_EINVAL, "bm_select_topk_f64: null pointer");
     select_f64_kernel<<<(unsigned)B, 32, 0, as_stream(stream)>>>(logits, (int)E, (int)k, temperature, tau, gamma,
                                                                 topk, probs, probs64, tae, margin, token_allowed);
     BM_LAUNCH_CHECK();

@@ -268,7 +268,7 @@ extern "C" int bm_permute(const int32_t *executed, const uint8_t *kind, int64_t 
                           int32_t *slot_row, bm_stream_t stream) {
     BM_REQUIRE(B >= 0 && k >= 1 && E >= 1 && E <= kPermMaxE && row_align >= 1 && row_align <= 256, BM_EINVAL,
                "bm_permute: bad shape");
-    BM_REQUIRE(executed && kind && expert_count && expert_offset && row_token && slot_row, BM_EINVAL,
+    BM_REQUIRE(expert_count && expert_offset && (B == 0 || (executed && kind && row_token && slot_row)), BM_EINVAL,
                "bm_permute: null pointer");
     permute_kernel<<<1, kPermThreads, 0, as_stream(stream)>>>(executed, kind, (int)(B * k), (int)k, (int)E,
                                                              (int)row_align, expert_count, expert_offset,
@@ -280,9 +280,9 @@ extern "C" int bm_permute(const int32_t *executed, const uint8_t *kind, int64_t 
 extern "C" int bm_gather_rows(const float *x, int64_t B, int64_t d, const int32_t *row_token,
                               const int32_t *expert_offset, int64_t E, int64_t r_max, int32_t layout, void *x_perm,
                               bm_stream_t stream) {
-    BM_REQUIRE(x && row_token && expert_offset && x_perm && d >= 1 && r_max >= 0, BM_EINVAL, "bm_gather_rows: bad args");
-    (void)B;
-    if (r_max == 0) return BM_OK;
+    BM_REQUIRE(d >= 1 && r_max >= 0 && B >= 0, BM_EINVAL, "bm_gather_rows: bad args");
+    if (r_max == 0 || B == 0) return BM_OK;
+    BM_REQUIRE(x && row_token && expert_offset && x_perm, BM_EINVAL, "bm_gather_rows: null pointer");
     if (layout == 0) {
         gather_f32_kernel<<<(unsigned)r_max, 256, 0, as_stream(stream)>>>(x, (int)d, row_token, expert_offset,
                                                                           (int)E, static_cast<float *>(x_perm));
@@ -301,11 +301,11 @@ extern "C" int bm_gather_rows(const float *x, int64_t B, int64_t d, const int32_
 extern "C" int bm_combine(const float *y_perm, const int32_t *slot_row, const float *probs, const uint8_t *kind,
                           int64_t B, int64_t k, int64_t d, const float *h_in, float residual_scale, float *out,
                           bm_stream_t stream) {
-    BM_REQUIRE(y_perm && slot_row && probs && kind && out && B >= 0 && k >= 1 && d >= 1, BM_EINVAL,
-               "bm_combine: bad args");
+    BM_REQUIRE(B >= 0 && k >= 1 && d >= 1, BM_EINVAL, "bm_combine: bad args");
     BM_REQUIRE(k <= kCombineMaxSlots, BM_EINVAL, "bm_combine: k=%lld slots exceeds %d", (long long)k,
                kCombineMaxSlots);
     if (B == 0) return BM_OK;
+    BM_REQUIRE(y_perm && slot_row && probs && kind && out, BM_EINVAL, "bm_combine: null pointer");
     size_t smem = h_in ? (size_t)d * sizeof(float) : 0;
     BM_REQUIRE(smem <= 200 * 1024, BM_EINVAL, "bm_combine: d too large");
     if (smem > 48 * 1024)

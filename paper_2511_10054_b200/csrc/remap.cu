@@ -214,11 +214,12 @@ int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const vo
                      bm_stream_t stream) {
     BM_REQUIRE(B >= 0 && k >= 1 && k <= kMaxK && E >= 1 && E <= kMaxE, BM_EINVAL,
                "bm_buddy_remap: bad shape B=%lld k=%lld E=%lld", (long long)B, (long long)k, (long long)E);
-    BM_REQUIRE(topk && resident_bitmap && executed && kind, BM_EINVAL, "bm_buddy_remap: null pointer");
+    BM_REQUIRE(resident_bitmap && (B == 0 || (topk && executed && kind)), BM_EINVAL, "bm_buddy_remap: null pointer");
     BM_REQUIRE(method >= BM_METHOD_BUDDY && method <= BM_METHOD_IDENTITY, BM_EINVAL, "bad method %d", method);
     const bool psi = eta != 0.0 || kappa != 0.0;
     if (method == BM_METHOD_BUDDY) {
-        BM_REQUIRE(token_allowed && tbl_ids && tbl_len, BM_EINVAL, "bm_buddy_remap: buddy method needs gates and a table");
+        BM_REQUIRE((B == 0 || token_allowed) && tbl_ids && tbl_len, BM_EINVAL,
+                   "bm_buddy_remap: buddy method needs gates and a table");
         BM_REQUIRE(H >= 1 && H <= kMaxH && tbl_stride >= 1, BM_ECONFIG, "search rank H=%lld out of range", (long long)H);
         BM_REQUIRE(fallback == BM_FALLBACK_PREFETCH || fallback == BM_FALLBACK_DROP, BM_ECONFIG, "bad fallback");
         BM_REQUIRE(eta >= 0.0 && kappa >= 0.0, BM_ECONFIG, "eta and kappa must be nonnegative");

@@ -435,3 +435,30 @@ def test_prefill_2sm_pairs_equal_single_cta(cuda_ok, E, d, f, B, k, act):
                 os.environ[v] = val
     rel = (torch.linalg.norm(y - ref32, dim=1) / torch.linalg.norm(ref32, dim=1).clamp_min(1e-30)).max().item()
     assert rel <= 2e-2, rel
+
+
+def test_empty_inputs(cuda_ok):
+    """Empty batches and traces (the reference handles an empty decision list
+    in route_batch / substitute_batch / observe_batch / forward_batch): every
+    kernel accepts zero tokens, launches nothing harmful and returns empty or
+    zero results; δ of an empty batch is 0 (batch allowed)."""
+    E, k, d, f = 8, 2, 128, 256
+    x = torch.empty(0, d, device=DEV)
+    wg = torch.randn(E, d, device=DEV)
+    r = ops.gate_topk(x, wg, torch.zeros(E, device=DEV), k, tau=0.3)
+    assert r.topk.shape == (0, k) and r.logits.shape == (0, E)
+    ids = torch.full((E, 4), -1, dtype=torch.int32, device=DEV)
+    t = ops.DeviceTable(ids, torch.zeros(E, 4, dtype=torch.float64, device=DEV),
+                        torch.zeros(E, dtype=torch.int32, device=DEV))
+    plan = ops.buddy_remap(r.topk, r.allowed, ops.bitmap_from_mask(np.ones(E, bool), DEV), t, H=4, rho=3)
+    assert plan.executed.shape == (0, k)
+    perm = ops.permute(plan.executed, plan.kind, E)
+    assert int(perm.count.sum()) == 0
+    c, p = ops.coact_count(torch.empty(0, k, dtype=torch.int32, device=DEV), E)
+    assert int(c.sum()) == 0 and int(p.sum()) == 0
+    w = (torch.randn(E, 3 * d * f, device=DEV) * 0.05).to(torch.bfloat16)
+    arena = ops.pack_arena_bf16(w, d, f, ops.ACT_SWIGLU)
+    ws = ops.FfnWorkspace(E, d, f, max(perm.r_max, 16), 64)
+    xp = ops.gather_rows(x, perm, 1)
+    ops.expert_ffn_bf16(xp, perm, arena, torch.arange(E, dtype=torch.int32, device=DEV), d, f, ops.ACT_SWIGLU, ws)
+    torch.cuda.synchronize()
