@@ -329,7 +329,8 @@ typedef struct {
     int64_t ffn_calls, ffn_experts, ffn_rows; /* grouped-FFN launches, sum of distinct executed experts / rows */
     double sim_now_ms;   /* control-plane clock */
     double stall_ms;     /* measured: compute stream waiting on expert fetches (CUDA events) */
-    double copy_ms;      /* measured: copy-stream time spent in expert H2D copies (CUDA events) */
+    double copy_ms;      /* measured: copy-stream time spent in expert H2D copies (CUDA events; only while
+                            bm_engine_set_copy_timing is on) */
     int64_t kernel_launches; /* libbmoe kernels launched (graph nodes included) */
     int64_t wire_bytes;      /* bytes actually moved host -> device for expert fetches (coded or raw) */
     double beta;             /* the distribution-gate beta in force (adaptive when pcie_budget_bytes >= 0) */
@@ -357,6 +358,10 @@ bm_cache *bm_engine_cache(bm_engine *e);
  * residency bitmap the remap saw, batch gate, and per token/slot topk,
  * token gate, executed id and kind (all host memory; set_trace clears). */
 int bm_engine_set_trace(bm_engine *e, int32_t enable);
+/* Bracket every expert fetch's copies with timing events (stats.copy_ms, the
+ * PCIe roofline). Off by default: a timing event on the copy stream costs the
+ * copy engine ~6 us per fetch (measured), 5% of a 6.5 MB Qwen3 expert copy. */
+int bm_engine_set_copy_timing(bm_engine *e, int32_t enable);
 int bm_engine_trace_size(const bm_engine *e, int64_t *records_host, int64_t *tokens_host);
 int bm_engine_trace_get(const bm_engine *e, int32_t *layer_host, int32_t *B_host, uint32_t *bitmaps_host,
                         uint8_t *batch_ok_host, int32_t *topk_host, uint8_t *allowed_host, int32_t *executed_host,

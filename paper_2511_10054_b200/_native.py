@@ -58,6 +58,7 @@ _SIGS = {
     "bm_engine_stats_get": (C.c_int, [P, P, I32]),
     "bm_engine_cache": (P, [P]),
     "bm_engine_set_trace": (C.c_int, [P, I32]),
+    "bm_engine_set_copy_timing": (C.c_int, [P, I32]),
     "bm_engine_trace_size": (C.c_int, [P, P, P]),
     "bm_engine_trace_get": (C.c_int, [P, P, P, P, P, P, P, P, P]),
     "bm_engine_device_bytes": (I64, [P]),

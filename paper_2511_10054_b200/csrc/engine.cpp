@@ -160,6 +160,7 @@ struct bm_engine {
     std::vector<int32_t> pend_exp;
     // optional per-layer-step trace (routing, gates, snapshot, plan) for parity checks
     bool tracing = false;
+    bool copy_timing = false;
     std::vector<int32_t> tr_layer, tr_B, tr_topk, tr_exec;
     std::vector<uint8_t> tr_allowed, tr_batch_ok, tr_kind;
     std::vector<uint32_t> tr_bitmap;
@@ -230,28 +231,30 @@ struct bm_engine {
     int fetch(int l, int e, cudaStream_t s) {
         int b;
         ENG_TRY(alloc_buffer(&b));
-        cudaEvent_t c0, c1;  // copy-engine busy time, for the PCIe roofline
-        ENG_CUDA(cudaEventCreate(&c0));
-        ENG_CUDA(cudaEventCreate(&c1));
+        cudaEvent_t c0 = nullptr, c1 = nullptr;  // copy-engine busy time, for the PCIe roofline
+        if (copy_timing) {
+            ENG_CUDA(cudaEventCreate(&c0));
+            ENG_CUDA(cudaEventCreate(&c1));
+        }
         cudaStream_t done = s;
         if (coded) {
             Ring &r = (s == prefetch_stream) ? ring_prefetch : ring_copy;
             if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(r.dec, bufs[b].free_ev, 0));  // the decode writes it
-            ENG_CUDA(cudaEventRecord(c0, s));
+            if (c0) ENG_CUDA(cudaEventRecord(c0, s));
             int64_t wire = 0;
             ENG_TRY(enqueue_coded(l, e, bufs[b].dev, s, r, &wire));
-            ENG_CUDA(cudaEventRecord(c1, s));
+            if (c1) ENG_CUDA(cudaEventRecord(c1, s));
             stats.wire_bytes += wire;
             done = r.dec;
         } else {
             if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(s, bufs[b].free_ev, 0));
-            ENG_CUDA(cudaEventRecord(c0, s));
+            if (c0) ENG_CUDA(cudaEventRecord(c0, s));
             ENG_CUDA(cudaMemcpyAsync(bufs[b].dev, host_mirror[l] + (size_t)e * buf_bytes, buf_bytes,
                                      cudaMemcpyHostToDevice, s));
-            ENG_CUDA(cudaEventRecord(c1, s));
+            if (c1) ENG_CUDA(cudaEventRecord(c1, s));
             stats.wire_bytes += (int64_t)buf_bytes;
         }
-        copy_ev.emplace_back(c0, c1);
+        if (c0) copy_ev.emplace_back(c0, c1);
         ENG_CUDA(cudaEventRecord(ready[l][e], done));
         ready_pending[l][e] = 1;
         phys[l][e] = b;
@@ -806,6 +809,12 @@ extern "C" int bm_engine_stats_get(bm_engine *e, bm_engine_stats *out, int32_t r
 }
 
 extern "C" bm_cache *bm_engine_cache(bm_engine *e) { return e ? e->cache : nullptr; }
+
+extern "C" int bm_engine_set_copy_timing(bm_engine *e, int32_t enable) {
+    if (!e) return BM_EINVAL;
+    e->copy_timing = enable != 0;
+    return BM_OK;
+}
 
 extern "C" int bm_engine_set_trace(bm_engine *e, int32_t enable) {
     if (!e) return BM_EINVAL;

@@ -1,11 +1,16 @@
 // K1 — fused router: GEMV + bias + warp top-k + renormalised softmax + TAE /
-// margin token gate. One CTA per token. Replaces model.route_batch
+// margin token gate. One token per CTA cluster. Replaces model.route_batch
 // (reference model.py:231-280) and gating.tae/margin/token_gate
 // (gating.py:71-108).
 #include <float.h>
 #include <math.h>
 
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace bm {
 namespace {
@@ -13,6 +18,7 @@ namespace {
 constexpr int kGateThreads = 256;
 constexpr int kMaxE = 256;
 constexpr int kMaxK = 32;
+constexpr int kGateUnroll = 8;
 
 template <typename T>
 struct Cand {
@@ -99,14 +105,24 @@ __device__ void select_and_gate(const T *z, int E, int k, double temperature, do
     }
 }
 
+// One token per cluster of `nsplit` CTAs (grid B * nsplit): CTA r computes
+// the logits of experts [r*epc, (r+1)*epc) with one warp per expert (the
+// same lane-strided dot product for any split, so the logits are bitwise
+// independent of it) and stores them straight into CTA 0's z through
+// distributed shared memory; after the cluster barrier CTA 0 selects. With
+// one CTA per token a decode batch (B = 16) kept 16 SMs busy streaming
+// E*d*4 B of gate weights each (Qwen3: 55 us per layer); the split spreads
+// it over B * nsplit CTAs.
 __global__ void __launch_bounds__(kGateThreads) gate_kernel(const float *__restrict__ x, const float *__restrict__ wg,
                                                             const float *__restrict__ bias, int E, int d, int k,
-                                                            double temperature, double tau, double gamma,
+                                                            int nsplit, double temperature, double tau, double gamma,
                                                             float *logits, int32_t *topk, float *probs, double *tae,
                                                             double *margin, uint8_t *allowed) {
     extern __shared__ __align__(16) float smem_x[];
     __shared__ float z[kMaxE];
-    const int b = blockIdx.x;
+    const int b = blockIdx.x / nsplit, rank = blockIdx.x % nsplit;
+    const int epc = (E + nsplit - 1) / nsplit;
+    const int e0 = rank * epc, e1 = min(E, e0 + epc);
     const float *xr = x + (size_t)b * d;
     const bool vec = (d % 4) == 0;
     if (vec) {
@@ -117,20 +133,31 @@ __global__ void __launch_bounds__(kGateThreads) gate_kernel(const float *__restr
         for (int i = threadIdx.x; i < d; i += blockDim.x) smem_x[i] = xr[i];
     }
     __syncthreads();
+    const uint32_t z0 = nsplit > 1 ? ptx::mapa(ptx::smem_u32(z), 0) : 0;
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const unsigned lane = lane_id();
-    for (int e = warp; e < E; e += nwarps) {
+    for (int e = e0 + warp; e < e1; e += nwarps) {
         const float *w = wg + (size_t)e * d;
         float acc = 0.f;
         if (vec) {
             const float4 *w4 = reinterpret_cast<const float4 *>(w);
             const float4 *x4 = reinterpret_cast<const float4 *>(smem_x);
-            for (int i = lane; i < d / 4; i += 32) {
-                float4 a = __ldg(w4 + i), c = x4[i];
-                acc = fmaf(a.x, c.x, acc);
-                acc = fmaf(a.y, c.y, acc);
-                acc = fmaf(a.z, c.z, acc);
-                acc = fmaf(a.w, c.w, acc);
+            const int n4 = d / 4;
+            // kGateUnroll loads in flight per lane, then the same in-order fma chain
+            for (int i0 = lane; i0 < n4; i0 += 32 * kGateUnroll) {
+                float4 a[kGateUnroll];
+#pragma unroll
+                for (int j = 0; j < kGateUnroll; ++j)
+                    a[j] = i0 + 32 * j < n4 ? __ldg(w4 + i0 + 32 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < kGateUnroll; ++j) {
+                    if (i0 + 32 * j >= n4) break;
+                    const float4 c = x4[i0 + 32 * j];
+                    acc = fmaf(a[j].x, c.x, acc);
+                    acc = fmaf(a[j].y, c.y, acc);
+                    acc = fmaf(a[j].z, c.z, acc);
+                    acc = fmaf(a[j].w, c.w, acc);
+                }
             }
         } else {
             for (int i = lane; i < d; i += 32) acc = fmaf(__ldg(w + i), smem_x[i], acc);
@@ -138,11 +165,19 @@ __global__ void __launch_bounds__(kGateThreads) gate_kernel(const float *__restr
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         if (lane == 0) {
             float v = acc + (bias ? bias[e] : 0.f);
-            z[e] = v;
+            if (nsplit > 1)
+                asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(z0 + 4u * (uint32_t)e), "f"(v) : "memory");
+            else
+                z[e] = v;
             if (logits) logits[(size_t)b * E + e] = v;
         }
     }
-    __syncthreads();
+    if (nsplit > 1) {
+        ptx::cluster_sync();  // release the remote stores / acquire them in CTA 0
+        if (rank != 0) return;
+    } else {
+        __syncthreads();
+    }
     if (warp == 0)
         select_and_gate<float>(z, E, k, temperature, tau, gamma, topk + (size_t)b * k, probs ? probs + (size_t)b * k : nullptr,
                                nullptr, tae ? tae + b : nullptr, margin ? margin + b : nullptr,
@@ -180,10 +215,24 @@ extern "C" int bm_gate_topk(const float *x, const float *wg, const float *bias, 
     BM_REQUIRE(smem <= 200 * 1024, BM_EINVAL, "bm_gate_topk: d=%lld too large", (long long)d);
     if (smem > 48 * 1024)
         BM_CUDA_TRY(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    gate_kernel<<<(unsigned)B, kGateThreads, smem, as_stream(stream)>>>(x, wg, bias, (int)E, (int)d, (int)k,
-                                                                      temperature, tau, gamma, logits, topk, probs,
-                                                                      tae, margin, token_allowed);
-    BM_LAUNCH_CHECK();
+    // split each token over a cluster when the batch alone would leave most SMs idle
+    int nsplit = (B >= 4 * 148) ? 1 : (int)std::min<int64_t>(8, (E + 7) / 8);
+    if (const char *ev = getenv("BMOE_GATE_SPLIT"))  // A/B knob: forced cluster size (1..8)
+        if (atoi(ev) > 0) nsplit = std::min(atoi(ev), 8);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(B * nsplit));
+    lc.blockDim = dim3(kGateThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = as_stream(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)nsplit;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    BM_CUDA_TRY(cudaLaunchKernelEx(&lc, gate_kernel, x, wg, bias, (int)E, (int)d, (int)k, nsplit, temperature, tau,
+                                   gamma, logits, topk, probs, tae, margin, token_allowed));
     return BM_OK;
 }
 

@@ -133,6 +133,7 @@ constexpr int kCombineThreads = 256;
 
 constexpr int kCombineMaxSlots = 64;
 constexpr int kCombineUnroll = 8;
+constexpr int kCombineSlotGroup = 4;  // slots whose loads are in flight together
 
 // One CTA per token. The token's active slots (not dropped, with a row) are
 // staged in shared memory first; each thread then owns columns
@@ -168,16 +169,33 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const float *_
     const int ns = nsl;
     float ssq = 0.f;
     for (int i0 = threadIdx.x; i0 < d; i0 += kCombineUnroll * blockDim.x) {
-        float y[kCombineUnroll];
+        float y[kCombineUnroll], hv[kCombineUnroll];
 #pragma unroll
-        for (int u = 0; u < kCombineUnroll; ++u) y[u] = 0.f;
-        for (int s = 0; s < ns; ++s) {
-            const float *src = y_perm + (size_t)srow[s] * d;
-            const float w = sw[s];
+        for (int u = 0; u < kCombineUnroll; ++u) {
+            const int i = i0 + u * (int)blockDim.x;
+            y[u] = 0.f;
+            hv[u] = (h_in && i < d) ? h_in[(size_t)b * d + i] : 0.f;  // in flight with the slot loads
+        }
+        // slots in groups of kCombineSlotGroup: all their loads are issued
+        // before the (unchanged, in-order) fma chain consumes them
+        for (int s0 = 0; s0 < ns; s0 += kCombineSlotGroup) {
+            float a[kCombineSlotGroup][kCombineUnroll];
 #pragma unroll
-            for (int u = 0; u < kCombineUnroll; ++u) {
-                const int i = i0 + u * (int)blockDim.x;
-                if (i < d) y[u] = fmaf(w, __ldg(src + i), y[u]);
+            for (int g = 0; g < kCombineSlotGroup; ++g) {
+                if (s0 + g >= ns) break;
+                const float *src = y_perm + (size_t)srow[s0 + g] * d;
+#pragma unroll
+                for (int u = 0; u < kCombineUnroll; ++u) {
+                    const int i = i0 + u * (int)blockDim.x;
+                    a[g][u] = i < d ? __ldg(src + i) : 0.f;
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < kCombineSlotGroup; ++g) {
+                if (s0 + g >= ns) break;
+                const float w = sw[s0 + g];
+#pragma unroll
+                for (int u = 0; u < kCombineUnroll; ++u) y[u] = fmaf(w, a[g][u], y[u]);
             }
         }
 #pragma unroll
@@ -185,7 +203,7 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const float *_
             const int i = i0 + u * (int)blockDim.x;
             if (i >= d) continue;
             if (h_in) {
-                const float h = fmaf(scale, y[u], h_in[(size_t)b * d + i]);
+                const float h = fmaf(scale, y[u], hv[u]);
                 hbuf[i] = h;
                 ssq = fmaf(h, h, ssq);
             } else {

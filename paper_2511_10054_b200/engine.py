@@ -288,6 +288,10 @@ class DecodeEngine:
         return np.array([(e.time_ms, e.kind, e.layer, e.token, e.expert, e.bytes, e.stall_ms) for e in arr[:n]],
                         dtype=np.float64).reshape(-1, 7)
 
+    def set_copy_timing(self, enable: bool = True):
+        """Time each fetch's copies (stats()["copy_ms"]); costs ~6 us of copy engine per fetch."""
+        N.call("bm_engine_set_copy_timing", self._h, int(enable))
+
     def set_trace(self, enable: bool = True):
         N.call("bm_engine_set_trace", self._h, int(enable))
 
