@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(kGateThreads) gate_kernel(const float *__restr
     const int e0 = rank * epc, e1 = min(E, e0 + epc);
     const float *xr = x + (size_t)b * d;
     const bool vec = (d % 4) == 0;
+    // every CTA of the cluster must have started before CTA 0's shared memory
+    // is written remotely: arrive now, wait after the row load
+    if (nsplit > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     if (vec) {
         const float4 *src = reinterpret_cast<const float4 *>(xr);
         float4 *dst = reinterpret_cast<float4 *>(smem_x);
@@ -132,6 +135,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_kernel(const float *__restr
     } else {
         for (int i = threadIdx.x; i < d; i += blockDim.x) smem_x[i] = xr[i];
     }
+    if (nsplit > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     __syncthreads();
     const uint32_t z0 = nsplit > 1 ? ptx::mapa(ptx::smem_u32(z), 0) : 0;
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;

@@ -437,6 +437,28 @@ def test_prefill_2sm_pairs_equal_single_cta(cuda_ok, E, d, f, B, k, act):
     assert rel <= 2e-2, rel
 
 
+@pytest.mark.parametrize("B,E,d,k", [(16, 128, 2048, 8), (5, 100, 96, 6), (7, 9, 33, 2), (3, 256, 512, 8),
+                                     (600, 64, 256, 6), (16, 8, 4096, 2)])
+def test_gate_cluster_split_bitwise(cuda_ok, monkeypatch, B, E, d, k):
+    """K1 splits a token over a CTA cluster (DSMEM logits) at small B: every
+    output is bitwise equal to one CTA per token (BMOE_GATE_SPLIT=1), and the
+    logits match a float64 GEMV within fp32 rounding."""
+    g = torch.Generator(device="cpu").manual_seed(B * 1000 + E)
+    x = torch.randn(B, d, generator=g).to(DEV)
+    wg = (torch.randn(E, d, generator=g) * d ** -0.5).to(DEV)
+    b = (torch.randn(E, generator=g) * 0.1).to(DEV)
+    outs = []
+    for split in ("0", "1", "3"):
+        monkeypatch.setenv("BMOE_GATE_SPLIT", split)
+        outs.append(ops.gate_topk(x, wg, b, k, 1.0, tau=0.4, gamma=0.9))
+    for r in outs[1:]:
+        for name in ("logits", "topk", "probs", "tae", "margin", "allowed"):
+            assert torch.equal(getattr(outs[0], name), getattr(r, name)), name
+    z64 = x.double() @ wg.double().T + b.double()
+    scale = x.double().norm(dim=1, keepdim=True) * wg.double().norm(dim=1).max()
+    assert bool(((outs[0].logits.double() - z64).abs() <= 1e-5 * scale).all())
+
+
 def test_empty_inputs(cuda_ok):
     """Empty batches and traces (the reference handles an empty decision list
     in route_batch / substitute_batch / observe_batch / forward_batch): every

@@ -29,6 +29,10 @@ if __name__ == "__main__":
                            partition_of=torch.from_numpy((np.arange(E) * 3 // E).astype(np.int32)).cuda(),
                            logits=torch.randn(B, E, dtype=torch.float64).cuda())
     torch.cuda.synchronize()
+    # router split over CTA clusters (logits pushed to CTA 0 over DSMEM), E=128 and a ragged E
+    for E_, B_ in ((128, 16), (100, 5)):
+        r = ops.gate_topk(torch.randn(B_, 256).cuda(), torch.randn(E_, 256).cuda() * 0.06, torch.zeros(E_).cuda(), 8)
+    torch.cuda.synchronize()
     # fused decode FFN with many split tiles (n_tile 16, 148 CTAs over a small
     # problem) and the multi-kernel path on the same inputs: bitwise equal
     E2, d, f, B2 = 8, 512, 1024, 40
