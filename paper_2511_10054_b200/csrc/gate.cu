@@ -36,12 +36,10 @@ __device__ __forceinline__ bool better(T av, int ai, T bv, int bi) {
 template <typename T>
 __device__ void select_and_gate(const T *z, int E, int k, double temperature, double tau, double gamma,
                                 int32_t *topk, float *probs, double *probs64, double *tae, double *margin,
-                                uint8_t *allowed) {
-    // called by one full warp
+                                uint8_t *allowed, int *sel_i, double *sel_z) {
+    // called by one full warp; sel_i / sel_z: that warp's kMaxK shared scratch
     const unsigned lane = lane_id();
     unsigned taken = 0;  // bit j: element lane + 32*j already selected
-    __shared__ int sel_i[kMaxK];
-    __shared__ double sel_z[kMaxK];
     for (int s = 0; s < k; ++s) {
         T bv = T(0);
         int bi = INT_MAX;
@@ -105,75 +103,100 @@ __device__ void select_and_gate(const T *z, int E, int k, double temperature, do
     }
 }
 
-// One token per cluster of `nsplit` CTAs (grid B * nsplit): CTA r computes
-// the logits of experts [r*epc, (r+1)*epc) with one warp per expert (the
-// same lane-strided dot product for any split, so the logits are bitwise
-// independent of it) and stores them straight into CTA 0's z through
-// distributed shared memory; after the cluster barrier CTA 0 selects. With
-// one CTA per token a decode batch (B = 16) kept 16 SMs busy streaming
-// E*d*4 B of gate weights each (Qwen3: 55 us per layer); the split spreads
-// it over B * nsplit CTAs.
+// Two layouts, one per batch regime, with the same per-logit arithmetic (a
+// warp's lane-strided float4 dot product, kGateUnroll loads in flight, then
+// the xor-shuffle reduction), so the logits are bitwise independent of both:
+//  - decode (TOK = 1): one token per cluster of `nsplit` CTAs (grid B *
+//    nsplit). CTA r computes the logits of experts [r*epc, (r+1)*epc), one
+//    warp per expert, and stores them straight into CTA 0's z through
+//    distributed shared memory; after the cluster barrier CTA 0 selects. One
+//    CTA per token kept 16 SMs streaming E*d*4 B of router weights each at
+//    B = 16 (Qwen3: 55 us per layer).
+//  - prefill (TOK = 8): a CTA owns 8 tokens and each weight row it loads
+//    serves all 8 (2048 CTAs each re-reading the 1 MB router from L2 took
+//    210 us per Qwen3 chunk); warps 0..7 then select one token each.
+template <int TOK>
 __global__ void __launch_bounds__(kGateThreads) gate_kernel(const float *__restrict__ x, const float *__restrict__ wg,
-                                                            const float *__restrict__ bias, int E, int d, int k,
-                                                            int nsplit, double temperature, double tau, double gamma,
-                                                            float *logits, int32_t *topk, float *probs, double *tae,
-                                                            double *margin, uint8_t *allowed) {
-    extern __shared__ __align__(16) float smem_x[];
-    __shared__ float z[kMaxE];
-    const int b = blockIdx.x / nsplit, rank = blockIdx.x % nsplit;
+                                                            const float *__restrict__ bias, int B, int E, int d,
+                                                            int k, int nsplit, double temperature, double tau,
+                                                            double gamma, float *logits, int32_t *topk, float *probs,
+                                                            double *tae, double *margin, uint8_t *allowed) {
+    extern __shared__ __align__(16) float smem_x[];  // [TOK][d]
+    __shared__ float z[TOK][kMaxE];
+    __shared__ int sel_i[TOK][kMaxK];
+    __shared__ double sel_z[TOK][kMaxK];
+    const int grp = blockIdx.x / nsplit, rank = blockIdx.x % nsplit;
+    const int b0 = grp * TOK, nt = min(TOK, B - b0);
     const int epc = (E + nsplit - 1) / nsplit;
     const int e0 = rank * epc, e1 = min(E, e0 + epc);
-    const float *xr = x + (size_t)b * d;
     const bool vec = (d % 4) == 0;
     // every CTA of the cluster must have started before CTA 0's shared memory
     // is written remotely: arrive now, wait after the row load
     if (nsplit > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    if (vec) {
-        const float4 *src = reinterpret_cast<const float4 *>(xr);
-        float4 *dst = reinterpret_cast<float4 *>(smem_x);
-        for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
-    } else {
-        for (int i = threadIdx.x; i < d; i += blockDim.x) smem_x[i] = xr[i];
+    for (int t = 0; t < nt; ++t) {
+        const float *xr = x + (size_t)(b0 + t) * d;
+        float *xs = smem_x + (size_t)t * d;
+        if (vec) {
+            const float4 *src = reinterpret_cast<const float4 *>(xr);
+            float4 *dst = reinterpret_cast<float4 *>(xs);
+            for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
+        } else {
+            for (int i = threadIdx.x; i < d; i += blockDim.x) xs[i] = xr[i];
+        }
     }
     if (nsplit > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     __syncthreads();
-    const uint32_t z0 = nsplit > 1 ? ptx::mapa(ptx::smem_u32(z), 0) : 0;
+    const uint32_t z0 = nsplit > 1 ? ptx::mapa(ptx::smem_u32(&z[0][0]), 0) : 0;
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const unsigned lane = lane_id();
     for (int e = e0 + warp; e < e1; e += nwarps) {
         const float *w = wg + (size_t)e * d;
-        float acc = 0.f;
+        float acc[TOK];
+#pragma unroll
+        for (int t = 0; t < TOK; ++t) acc[t] = 0.f;
         if (vec) {
             const float4 *w4 = reinterpret_cast<const float4 *>(w);
-            const float4 *x4 = reinterpret_cast<const float4 *>(smem_x);
             const int n4 = d / 4;
-            // kGateUnroll loads in flight per lane, then the same in-order fma chain
             for (int i0 = lane; i0 < n4; i0 += 32 * kGateUnroll) {
                 float4 a[kGateUnroll];
 #pragma unroll
                 for (int j = 0; j < kGateUnroll; ++j)
                     a[j] = i0 + 32 * j < n4 ? __ldg(w4 + i0 + 32 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int j = 0; j < kGateUnroll; ++j) {
-                    if (i0 + 32 * j >= n4) break;
-                    const float4 c = x4[i0 + 32 * j];
-                    acc = fmaf(a[j].x, c.x, acc);
-                    acc = fmaf(a[j].y, c.y, acc);
-                    acc = fmaf(a[j].z, c.z, acc);
-                    acc = fmaf(a[j].w, c.w, acc);
+                for (int t = 0; t < TOK; ++t) {
+                    if (t >= nt) break;
+                    const float4 *x4 = reinterpret_cast<const float4 *>(smem_x + (size_t)t * d);
+#pragma unroll
+                    for (int j = 0; j < kGateUnroll; ++j) {
+                        if (i0 + 32 * j >= n4) break;
+                        const float4 c = x4[i0 + 32 * j];
+                        acc[t] = fmaf(a[j].x, c.x, acc[t]);
+                        acc[t] = fmaf(a[j].y, c.y, acc[t]);
+                        acc[t] = fmaf(a[j].z, c.z, acc[t]);
+                        acc[t] = fmaf(a[j].w, c.w, acc[t]);
+                    }
                 }
             }
         } else {
-            for (int i = lane; i < d; i += 32) acc = fmaf(__ldg(w + i), smem_x[i], acc);
+            for (int i = lane; i < d; i += 32) {
+                const float a = __ldg(w + i);
+#pragma unroll
+                for (int t = 0; t < TOK; ++t)
+                    if (t < nt) acc[t] = fmaf(a, smem_x[(size_t)t * d + i], acc[t]);
+            }
         }
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) {
-            float v = acc + (bias ? bias[e] : 0.f);
-            if (nsplit > 1)
-                asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(z0 + 4u * (uint32_t)e), "f"(v) : "memory");
-            else
-                z[e] = v;
-            if (logits) logits[(size_t)b * E + e] = v;
+#pragma unroll
+        for (int t = 0; t < TOK; ++t) {
+            float v = acc[t];
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0 && t < nt) {
+                v += bias ? bias[e] : 0.f;
+                if (nsplit > 1)
+                    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(z0 + 4u * (uint32_t)e), "f"(v) : "memory");
+                else
+                    z[t][e] = v;
+                if (logits) logits[(size_t)(b0 + t) * E + e] = v;
+            }
         }
     }
     if (nsplit > 1) {
@@ -182,10 +205,13 @@ __global__ void __launch_bounds__(kGateThreads) gate_kernel(const float *__restr
     } else {
         __syncthreads();
     }
-    if (warp == 0)
-        select_and_gate<float>(z, E, k, temperature, tau, gamma, topk + (size_t)b * k, probs ? probs + (size_t)b * k : nullptr,
-                               nullptr, tae ? tae + b : nullptr, margin ? margin + b : nullptr,
-                               allowed ? allowed + b : nullptr);
+    if (warp < nt) {
+        const int b = b0 + warp;
+        select_and_gate<float>(z[warp], E, k, temperature, tau, gamma, topk + (size_t)b * k,
+                               probs ? probs + (size_t)b * k : nullptr, nullptr, tae ? tae + b : nullptr,
+                               margin ? margin + b : nullptr, allowed ? allowed + b : nullptr, sel_i[warp],
+                               sel_z[warp]);
+    }
 }
 
 __global__ void __launch_bounds__(32) select_f64_kernel(const double *__restrict__ logits, int E, int k,
@@ -193,12 +219,15 @@ __global__ void __launch_bounds__(32) select_f64_kernel(const double *__restrict
                                                         int32_t *topk, float *probs, double *probs64,
                                                         double *tae, double *margin, uint8_t *allowed) {
     __shared__ double z[kMaxE];
+    __shared__ int sel_i[kMaxK];
+    __shared__ double sel_z[kMaxK];
     const int b = blockIdx.x;
     for (int e = threadIdx.x; e < E; e += 32) z[e] = logits[(size_t)b * E + e];
     __syncwarp();
     select_and_gate<double>(z, E, k, temperature, tau, gamma, topk + (size_t)b * k,
                             probs ? probs + (size_t)b * k : nullptr, probs64 ? probs64 + (size_t)b * k : nullptr,
-                            tae ? tae + b : nullptr, margin ? margin + b : nullptr, allowed ? allowed + b : nullptr);
+                            tae ? tae + b : nullptr, margin ? margin + b : nullptr, allowed ? allowed + b : nullptr,
+                            sel_i, sel_z);
 }
 
 }  // namespace
@@ -215,16 +244,20 @@ extern "C" int bm_gate_topk(const float *x, const float *wg, const float *bias, 
     BM_REQUIRE(temperature > 0.0, BM_EINVAL, "temperature must be > 0");
     if (B == 0) return BM_OK;  // empty batch (its tensors may have null data pointers)
     BM_REQUIRE(x && wg && topk, BM_EINVAL, "bm_gate_topk: null pointer");
-    size_t smem = (size_t)d * sizeof(float);
-    BM_REQUIRE(smem <= 200 * 1024, BM_EINVAL, "bm_gate_topk: d=%lld too large", (long long)d);
-    if (smem > 48 * 1024)
-        BM_CUDA_TRY(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // split each token over a cluster when the batch alone would leave most SMs idle
-    int nsplit = (B >= 4 * 148) ? 1 : (int)std::min<int64_t>(8, (E + 7) / 8);
+    BM_REQUIRE((size_t)d * sizeof(float) <= 200 * 1024, BM_EINVAL, "bm_gate_topk: d=%lld too large", (long long)d);
+    // small batches: split each token over a cluster; large ones: 8 tokens per CTA
+    const char *wide_env = getenv("BMOE_GATE_WIDE");  // A/B knob: 0 = one token per CTA at any B
+    const bool wide = B >= 4 * 148 && (size_t)8 * d * sizeof(float) <= 200 * 1024 && !(wide_env && atoi(wide_env) == 0);
+    int nsplit = wide ? 1 : (B >= 4 * 148 ? 1 : (int)std::min<int64_t>(8, (E + 7) / 8));
     if (const char *ev = getenv("BMOE_GATE_SPLIT"))  // A/B knob: forced cluster size (1..8)
-        if (atoi(ev) > 0) nsplit = std::min(atoi(ev), 8);
+        if (atoi(ev) > 0 && !wide) nsplit = std::min(atoi(ev), 8);
+    const int tok = wide ? 8 : 1;
+    const size_t smem = (size_t)tok * d * sizeof(float);
+    auto kern = wide ? gate_kernel<8> : gate_kernel<1>;
+    if (smem > 48 * 1024)
+        BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)(B * nsplit));
+    lc.gridDim = dim3((unsigned)(((B + tok - 1) / tok) * nsplit));
     lc.blockDim = dim3(kGateThreads);
     lc.dynamicSmemBytes = smem;
     lc.stream = as_stream(stream);
@@ -235,7 +268,7 @@ extern "C" int bm_gate_topk(const float *x, const float *wg, const float *bias, 
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    BM_CUDA_TRY(cudaLaunchKernelEx(&lc, gate_kernel, x, wg, bias, (int)E, (int)d, (int)k, nsplit, temperature, tau,
+    BM_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, x, wg, bias, (int)B, (int)E, (int)d, (int)k, nsplit, temperature, tau,
                                    gamma, logits, topk, probs, tae, margin, token_allowed));
     return BM_OK;
 }

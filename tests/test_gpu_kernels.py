@@ -438,18 +438,20 @@ def test_prefill_2sm_pairs_equal_single_cta(cuda_ok, E, d, f, B, k, act):
 
 
 @pytest.mark.parametrize("B,E,d,k", [(16, 128, 2048, 8), (5, 100, 96, 6), (7, 9, 33, 2), (3, 256, 512, 8),
-                                     (600, 64, 256, 6), (16, 8, 4096, 2)])
+                                     (600, 64, 256, 6), (16, 8, 4096, 2), (2051, 128, 2048, 8), (603, 10, 36, 3)])
 def test_gate_cluster_split_bitwise(cuda_ok, monkeypatch, B, E, d, k):
-    """K1 splits a token over a CTA cluster (DSMEM logits) at small B: every
-    output is bitwise equal to one CTA per token (BMOE_GATE_SPLIT=1), and the
-    logits match a float64 GEMV within fp32 rounding."""
+    """K1 splits a token over a CTA cluster (DSMEM logits) at small B and
+    gives a CTA 8 tokens at large B: every output is bitwise equal to one CTA
+    per token (BMOE_GATE_SPLIT=1, BMOE_GATE_WIDE=0), and the logits match a
+    float64 GEMV within fp32 rounding."""
     g = torch.Generator(device="cpu").manual_seed(B * 1000 + E)
     x = torch.randn(B, d, generator=g).to(DEV)
     wg = (torch.randn(E, d, generator=g) * d ** -0.5).to(DEV)
     b = (torch.randn(E, generator=g) * 0.1).to(DEV)
     outs = []
-    for split in ("0", "1", "3"):
+    for split, wide in (("0", "1"), ("1", "0"), ("3", "0")):
         monkeypatch.setenv("BMOE_GATE_SPLIT", split)
+        monkeypatch.setenv("BMOE_GATE_WIDE", wide)
         outs.append(ops.gate_topk(x, wg, b, k, 1.0, tau=0.4, gamma=0.9))
     for r in outs[1:]:
         for name in ("logits", "topk", "probs", "tae", "margin", "allowed"):

@@ -136,6 +136,35 @@ def test_eviction_policies_ties_to_lowest_id():
     assert log[1].expert == res[0]
 
 
+def test_lru_recency_list_matches_argmin_scan():
+    """The C++ LRU victim is the head of a recency list (O(1)); on a long
+    thrashing stream (prefill-like: most accesses miss) it evicts exactly
+    memtier's argmin(last_use), ties to the lowest id (memtier.py:162-170)."""
+    rng = np.random.default_rng(5)
+    E, cap = 64, 16
+    st = M.ResidencyState(E, cap, "lru")
+    clock, cost = M.SimClock(), M.CostModel()
+    mask = st.mask.copy()
+    last = np.where(mask, 0, -1).astype(np.int64)
+    tick = 0
+    for e in np.flatnonzero(mask):  # initial residents touched in id order
+        tick += 1
+        last[e] = tick
+    for i in range(20000):
+        e = int(rng.integers(E)) if i % 3 else int(rng.integers(8))
+        log = []
+        M.access(st, e, clock, cost, log=log)
+        if not mask[e]:
+            res = np.flatnonzero(mask)
+            v = int(res[np.argmin(last[res])])
+            assert [x.kind for x in log] == ["miss_ondemand", "evict"] and log[1].expert == v
+            mask[v] = False
+            mask[e] = True
+        tick += 1
+        last[e] = tick
+    assert np.array_equal(st.mask, mask)
+
+
 def test_policy_errors():
     with pytest.raises(ConfigurationError):
         M.ResidencyState(8, 9, "lru")

@@ -1,4 +1,4 @@
-"""Where a decode step's time goes: runs the engine for a few steps under the
+"""Where an engine step's time goes: runs the engine for a few steps under the
 CUDA activity profiler (CUPTI through torch.profiler) and reports the H2D
 copy-engine busy fraction, the gaps between copies and the GPU work and host
 phases that fill them. Usage:
@@ -8,6 +8,7 @@ phases that fill them. Usage:
 import argparse
 import json
 import os
+import re
 import sys
 
 import numpy as np
@@ -68,7 +69,8 @@ def main():
         for ka, kb, n in kern:
             o = min(b, kb) - max(a, ka)
             if o > 0:
-                short = n.split("(")[0].split("<")[0][-48:]
+                m = re.findall(r"(\w+)(?:<[^>]*>)?\(", n)
+                short = m[0] if m else n[:40]
                 by[short] = by.get(short, 0.0) + o
     kern_union = _union([(a, b) for a, b, _ in kern])
     gap_gpu_busy = 0.0
@@ -77,6 +79,12 @@ def main():
             o = min(b, kb) - max(a, ka)
             if o > 0:
                 gap_gpu_busy += o
+    per = {}
+    for a, b, n in kern:
+        m = re.findall(r"(\w+)(?:<[^>]*>)?\(", n)
+        key = m[0] if m else n[:40]
+        c, t = per.get(key, (0, 0.0))
+        per[key] = (c + 1, t + (b - a))
     hist = np.histogram([b - a for a, b in gaps], bins=[5, 20, 50, 100, 200, 500, 1e9])[0].tolist()
     out = {"model": args.model, "layers": args.layers, "steps": args.steps,
            "span_ms": (t1 - t0) / 1e3, "h2d_busy_ms": busy_us / 1e3, "h2d_busy_frac": busy_us / (t1 - t0),
@@ -84,7 +92,9 @@ def main():
            "gap_per_layer_step_us": gap_us / (args.layers * args.steps),
            "gap_hist_us[5,20,50,100,200,500,inf]": hist,
            "gpu_busy_in_gaps_ms": gap_gpu_busy / 1e3,
-           "kernels_in_gaps_ms": {k: round(v / 1e3, 3) for k, v in sorted(by.items(), key=lambda t: -t[1])[:12]}}
+           "kernels_in_gaps_ms": {k: round(v / 1e3, 3) for k, v in sorted(by.items(), key=lambda t: -t[1])[:12]},
+           "kernels": {k: {"n": c, "avg_us": round(t / c, 1), "total_ms": round(t / 1e3, 3)}
+                       for k, (c, t) in sorted(per.items(), key=lambda t: -t[1][1])}}
     # host-side ranges (engine step on the CPU timeline)
     cpu = {}
     for e in prof.events():
