@@ -432,13 +432,6 @@ struct bm_engine {
             tr_batch_ok.push_back(batch_ok_h[0]);
             tr_bitmap.insert(tr_bitmap.end(), bm_host_l[l], bm_host_l[l] + words);
         }
-        // 6. control plane: replay accesses in (token, slot) order (harness.py:363-382)
-        int64_t out4[4];
-        ENG_TRY(bm_cache_apply_plan(cache, l, B, k, tokens, topk_h, exec_h, kind_h, out4));
-        stats.executed_slots += out4[0];
-        stats.ondemand_misses += out4[1];
-        stats.substitutions += out4[2];
-        ENG_TRY(bm_cache_advance(cache, cfg.compute_ms * (double)out4[0]));
         std::vector<int32_t> &cnt = prev_counts[l];  // harness.py:384-389
         std::fill(cnt.begin(), cnt.end(), 0);
         for (int64_t i = 0; i < B * k; ++i) {
@@ -448,7 +441,10 @@ struct bm_engine {
             }
             ++cnt[exec_h[i]];
         }
-        // 7. data plane: every executed expert must be in HBM before the GEMM
+        // 7. data plane: every executed expert must be in HBM before the GEMM. The copies
+        // depend only on the plan and on which experts hold HBM buffers (buffers freed by
+        // this step's evictions are released after its compute), not on the replay, so
+        // they are enqueued first and the replay below runs on the CPU while they move.
         std::vector<cudaEvent_t> waits;
         std::vector<int> wait_experts;
         ++stats.ffn_calls;
@@ -466,6 +462,14 @@ struct bm_engine {
                 ready_pending[l][e] = 0;
             }
         }
+        // 6. control plane: replay accesses in (token, slot) order (harness.py:363-382),
+        // overlapping the copies enqueued above
+        int64_t out4[4];
+        ENG_TRY(bm_cache_apply_plan(cache, l, B, k, tokens, topk_h, exec_h, kind_h, out4));
+        stats.executed_slots += out4[0];
+        stats.ondemand_misses += out4[1];
+        stats.substitutions += out4[2];
+        ENG_TRY(bm_cache_advance(cache, cfg.compute_ms * (double)out4[0]));
         const int Et = E + Ssh;
         int32_t *bo = bo_host_l[l];  // [buffer map (Et) | fetched-this-step mask (Et)]
         for (int e = 0; e < E; ++e) {
