@@ -116,6 +116,29 @@ def test_engine_bf16_tensor_core_mode_same_decisions(cuda_ok):
     eng.close()
 
 
+def test_engine_split_fetched_ffn_same_decisions(cuda_ok, monkeypatch):
+    """A/B switch BMOE_SPLIT_FETCHED=1 (the early fetched experts' FFN runs
+    while the last copy is on the wire, a third FFN call per layer-step): the
+    control plane is untouched (identical event logs) and the outputs stay
+    within bf16 rounding of the default schedule and of the reference."""
+    g = golden("sim_tiny.npz")
+    outs, evs, launches = [], [], []
+    for v in ("0", "1"):
+        monkeypatch.setenv("BMOE_SPLIT_FETCHED", v)
+        eng = _engine("buddy", g, fp32=False)
+        outs.append(_run(eng))
+        evs.append(eng.sorted_events())
+        launches.append(eng.stats()["kernel_launches"])
+        eng.close()
+    assert launches[1] > launches[0]  # the split schedule ran (extra FFN calls)
+    assert np.array_equal(evs[0], evs[1])
+    rel = np.linalg.norm(outs[1] - outs[0], axis=1) / np.linalg.norm(outs[0], axis=1)
+    assert rel.max() <= 2e-2, rel.max()
+    ro = g["buddy_outputs"]
+    rel_ref = np.linalg.norm(outs[1] - ro, axis=1) / np.linalg.norm(ro, axis=1)
+    assert np.median(rel_ref) <= 2e-2
+
+
 def test_profile_build_pipeline_matches_reference(cuda_ok, tmp_path):
     """cmd_profile -> cmd_build on the GPU (harness.run_profile / run_build):
     co-activation counts and buddy tables bit-exact vs the reference's files

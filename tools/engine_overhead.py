@@ -42,7 +42,7 @@ def main():
     N.lib().bm_set_kernel_timing(1)
     for s in range(3, 3 + args.steps):
         eng.step(x[s * B:(s + 1) * B], np.arange(B))
-    buf = np.zeros(4 * args.steps * args.layers, np.float32)
+    buf = np.zeros(6 * args.steps * args.layers, np.float32)
     n = int(N.lib().bm_kernel_times(buf.ctypes.data, buf.size))
     N.lib().bm_set_kernel_timing(0)
     gemm = float(buf[:n].sum()) / args.steps
