@@ -39,7 +39,7 @@ extern "C" {
 enum { BM_OK = 0, BM_EINVAL = 1, BM_ECONFIG = 2, BM_EDEGENERATE = 3, BM_EINVARIANT = 4, BM_ECUDA = 5 };
 enum { BM_KIND_KEPT = 0, BM_KIND_SUBSTITUTED = 1, BM_KIND_ONDEMAND = 2, BM_KIND_DROPPED = 3 };
 enum { BM_FALLBACK_PREFETCH = 0, BM_FALLBACK_DROP = 1 };                 /* substitution.py:30-31 */
-enum { BM_METHOD_BUDDY = 0, BM_METHOD_ORIGINAL = 1, BM_METHOD_IDENTITY = 2 };
+enum { BM_METHOD_BUDDY = 0, BM_METHOD_ORIGINAL = 1, BM_METHOD_IDENTITY = 2, BM_METHOD_RANDOM = 3 };
 enum { BM_ACT_TANH = 0, BM_ACT_SWIGLU = 1 };
 enum { BM_POLICY_LRU = 0, BM_POLICY_LFU = 1, BM_POLICY_FREQ_STATIC = 2 };  /* memtier.py:31-34 */
 enum { BM_EV_HIT = 0, BM_EV_MISS_ONDEMAND = 1, BM_EV_MISS_SUBSTITUTED = 2, BM_EV_PREFETCH_ISSUE = 3,
@@ -99,6 +99,25 @@ int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed, const void
                    int32_t use_local_logit, const int32_t *partition_of, double hop, int32_t *executed,
                    uint8_t *kind, int32_t *used, double *delta_out, uint8_t *batch_allowed_out,
                    bm_stream_t stream);
+
+/* ------------------------------------------------ Random baseline (host)
+ * numpy's PCG64 bit generator state (Generator.bit_generator.state: the
+ * 128-bit state and increment, has_uint32 / uinteger), so host code can make
+ * the same draws as the reference and hand the advanced state back. */
+typedef struct {
+    uint64_t state_hi, state_lo, inc_hi, inc_lo;
+    int32_t has_uint32;
+    uint32_t uinteger;
+} bm_pcg64;
+/* substitution.random_plan (substitution.py:227-248) for B tokens in order,
+ * sharing one generator (harness.py:358-359): a resident expert is kept; a
+ * missing one is replaced by pool[rng.integers(0, pool.size)], pool = the
+ * resident experts (ascending) not yet assigned to the token, or falls back to
+ * ondemand when the pool is empty. Host memory; mask_host[E] = the snapshot. */
+int bm_random_plan(const int32_t *topk_host, int64_t B, int64_t k, const uint8_t *mask_host, int64_t E,
+                   bm_pcg64 *rng_host, int32_t *executed_host, uint8_t *kind_host, int32_t *used_host);
+/* Generator.integers(0, n) drawn `count` times (n <= 2^32), for tests. */
+int bm_pcg64_integers(bm_pcg64 *rng_host, int64_t n, int64_t count, int64_t *out_host);
 
 /* ------------------------------------------ K3 permute / K5 combine
  * bm_permute: stable grouping of the executed (token, slot) pairs by expert
@@ -321,6 +340,7 @@ typedef struct {
                             piece by piece through a staging ring and rebuilt in HBM by bm_xfer_decode_piece */
     double pcie_budget_bytes; /* >= 0: adaptive distribution-gate beta (gating.BetaController, gating.py:189-221,
                                  gate.pcie_budget_bytes config.py:94) starting at `beta`; < 0: fixed beta */
+    bm_pcg64 rng; /* method RANDOM: the generator of harness.py:299-300 (SeedSequence([run.seed, 31])) */
 } bm_engine_config;
 
 typedef struct {
@@ -334,6 +354,7 @@ typedef struct {
     int64_t kernel_launches; /* libbmoe kernels launched (graph nodes included) */
     int64_t wire_bytes;      /* bytes actually moved host -> device for expert fetches (coded or raw) */
     double beta;             /* the distribution-gate beta in force (adaptive when pcie_budget_bytes >= 0) */
+    int64_t inflight_releases; /* buffers released while their speculative fetch was still in flight */
 } bm_engine_stats;
 
 /* host_mirror[l]: pinned host memory, num_experts buffers of the arena

@@ -210,6 +210,36 @@ def ondemand_plan(topk, mask):
 
 
 # --------------------------------------------------- co-activation profiling
+def random_plan(topk, mask, rng):
+    """substitution.py:227-248 for a batch, one shared numpy Generator in
+    token order (harness.py:358-359): kept if resident, else a uniform draw
+    rng.integers(0, n) from the resident experts not yet assigned to the
+    token (ascending), else ondemand. Returns (executed, kind, used)."""
+    topk = np.asarray(topk)
+    mask = np.asarray(mask, bool)
+    B, k = topk.shape
+    ex = topk.astype(np.int64).copy()
+    kd = np.zeros((B, k), np.uint8)
+    used = np.zeros(B, np.int64)
+    res = np.flatnonzero(mask)
+    for b in range(B):
+        taken = np.zeros(mask.size, bool)
+        taken[topk[b]] = True
+        for s in range(k):
+            o = int(topk[b, s])
+            if mask[o]:
+                continue
+            pool = res[~taken[res]]
+            if pool.size == 0:
+                kd[b, s] = KIND_ONDEMAND
+                continue
+            j = int(pool[rng.integers(0, pool.size)])
+            ex[b, s], kd[b, s] = j, KIND_SUBSTITUTED
+            taken[j] = True
+            used[b] += 1
+    return ex, kd, used
+
+
 def coact_count(topk, probs, num_experts, tok0=0, warmup_steps=256, warmup_weight=0.0):
     """observe() folded over a trace, profiler.py:67-95.
 

@@ -26,6 +26,28 @@ class Event(C.Structure):
                 ("expert", C.c_int32), ("bytes", C.c_int64), ("stall_ms", C.c_double)]
 
 
+class Pcg64State(C.Structure):
+    """numpy's PCG64 bit-generator state (bm_pcg64)."""
+    _fields_ = [("state_hi", C.c_uint64), ("state_lo", C.c_uint64), ("inc_hi", C.c_uint64), ("inc_lo", C.c_uint64),
+                ("has_uint32", C.c_int32), ("uinteger", C.c_uint32)]
+
+    @classmethod
+    def from_generator(cls, rng) -> "Pcg64State":
+        st = rng.bit_generator.state
+        if st["bit_generator"] != "PCG64":
+            raise TypeError(f"need a PCG64 generator, got {st['bit_generator']}")
+        s, inc = st["state"]["state"], st["state"]["inc"]
+        m = (1 << 64) - 1
+        return cls(s >> 64, s & m, inc >> 64, inc & m, int(st["has_uint32"]), int(st["uinteger"]))
+
+    def store_into(self, rng) -> None:
+        """Write the advanced state back, so the numpy generator continues the same stream."""
+        rng.bit_generator.state = {"bit_generator": "PCG64",
+                                   "state": {"state": (self.state_hi << 64) | self.state_lo,
+                                             "inc": (self.inc_hi << 64) | self.inc_lo},
+                                   "has_uint32": int(self.has_uint32), "uinteger": int(self.uinteger)}
+
+
 class EngineConfig(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("num_experts", C.c_int32), ("top_k", C.c_int32), ("d", C.c_int32),
                 ("f", C.c_int32), ("act", C.c_int32), ("max_batch", C.c_int32), ("capacity", C.c_int32),
@@ -35,7 +57,7 @@ class EngineConfig(C.Structure):
                 ("temperature", C.c_double), ("gamma", C.c_double), ("load_ms", C.c_double),
                 ("hit_ms", C.c_double), ("compute_ms", C.c_double), ("prefetch_ms", C.c_double),
                 ("expert_bytes", C.c_int64), ("num_shared", C.c_int32), ("fetch_codec", C.c_int32),
-                ("pcie_budget_bytes", C.c_double)]
+                ("pcie_budget_bytes", C.c_double), ("rng", Pcg64State)]
 
 
 class EngineStats(C.Structure):
@@ -45,7 +67,7 @@ class EngineStats(C.Structure):
                 ("batch_bypassed", C.c_int64), ("ffn_calls", C.c_int64), ("ffn_experts", C.c_int64),
                 ("ffn_rows", C.c_int64), ("sim_now_ms", C.c_double), ("stall_ms", C.c_double),
                 ("copy_ms", C.c_double), ("kernel_launches", C.c_int64), ("wire_bytes", C.c_int64),
-                ("beta", C.c_double)]
+                ("beta", C.c_double), ("inflight_releases", C.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -78,6 +100,8 @@ _SIGS = {
     "bm_select_topk_f64": (C.c_int, [P, I64, I64, I64, F64, F64, F64, P, P, P, P, P, P, P]),
     "bm_buddy_remap": (C.c_int, [P, P, P, I32, I64, I64, I64, P, P, P, P, I64, I64, I64, I32, I32, F64, F64, F64,
                                  I32, P, F64, P, P, P, P, P, P]),
+    "bm_random_plan": (C.c_int, [P, I64, I64, P, I64, P, P, P, P]),
+    "bm_pcg64_integers": (C.c_int, [P, I64, I64, P]),
     "bm_permute_rows_max": (I64, [I64, I64, I64, I64]),
     "bm_append_shared": (C.c_int, [P, P, P, I64, I64, I64, I64, P, P, P, P]),
     "bm_split_counts": (C.c_int, [P, P, I64, P, P, P]),

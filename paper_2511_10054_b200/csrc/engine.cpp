@@ -25,6 +25,8 @@ int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const vo
                      int32_t use_local_logit, const int32_t *partition_of, double hop, int32_t *executed,
                      uint8_t *kind, int32_t *used, double *delta_out, uint8_t *batch_allowed_out,
                      bm_stream_t stream);
+int random_plan_batch(const int32_t *topk, int64_t B, int64_t k, const uint32_t *resident_bits, int64_t E,
+                      bm_pcg64 *rng, int32_t *executed, uint8_t *kind, int32_t *used);
 }
 
 #define ENG_CUDA(expr)                                                                                    \
@@ -95,6 +97,55 @@ struct Ring {
     cudaStream_t dec = nullptr;
 };
 
+// Bounded pool of timing-event pairs (stall and copy-engine busy time). A
+// pair is harvested into the running sum when its slot comes round again
+// (by then it completed long ago, so the synchronize does not block the
+// step) or when the stats are read; no event is created per step.
+struct TimingRing {
+    static constexpr int kPairs = 256;
+    cudaEvent_t a[kPairs] = {}, b[kPairs] = {};
+    bool live[kPairs] = {};
+    int head = 0;
+    double acc_ms = 0.0;
+    int init() {
+        for (int i = 0; i < kPairs; ++i) {
+            if (cudaEventCreate(&a[i]) != cudaSuccess || cudaEventCreate(&b[i]) != cudaSuccess) return BM_ECUDA;
+        }
+        return BM_OK;
+    }
+    int harvest(int i) {
+        if (!live[i]) return BM_OK;
+        ENG_CUDA(cudaEventSynchronize(b[i]));
+        float ms = 0.f;
+        ENG_CUDA(cudaEventElapsedTime(&ms, a[i], b[i]));
+        acc_ms += ms;
+        live[i] = false;
+        return BM_OK;
+    }
+    // the next pair to record into (its previous use harvested first)
+    int next(cudaEvent_t *ea, cudaEvent_t *eb) {
+        const int i = head;
+        head = (head + 1) % kPairs;
+        ENG_TRY(harvest(i));
+        live[i] = true;
+        *ea = a[i];
+        *eb = b[i];
+        return BM_OK;
+    }
+    int drain(double *out_ms) {
+        for (int i = 0; i < kPairs; ++i) ENG_TRY(harvest(i));
+        *out_ms = acc_ms;
+        acc_ms = 0.0;
+        return BM_OK;
+    }
+    void release() {
+        for (int i = 0; i < kPairs; ++i) {
+            if (a[i]) cudaEventDestroy(a[i]);
+            if (b[i]) cudaEventDestroy(b[i]);
+        }
+    }
+};
+
 }  // namespace
 
 struct bm_engine {
@@ -108,6 +159,8 @@ struct bm_engine {
     std::vector<std::vector<int>> phys;            // [L][E] buffer id or -1
     std::vector<std::vector<cudaEvent_t>> ready;   // [L][E] copy-complete events
     std::vector<std::vector<uint8_t>> ready_pending;
+    std::vector<std::vector<cudaStream_t>> ready_stream;  // [L][E] stream the ready event was recorded on
+    std::vector<cudaEvent_t> buf_ev;                      // [nbufs] free events of buffers released in flight
     std::vector<cudaEvent_t> layer_done;           // [L]
     std::vector<const uint8_t *> host_mirror;
     bool coded = false;       // host_mirror[l] is an exponent-coded layer image (cfg.fetch_codec)
@@ -147,6 +200,7 @@ struct bm_engine {
     std::vector<uint32_t *> bm_dev_l, bm_host_l;  // per-layer residency bitmaps (+ the beta the remap uses)
     int bm_stride = 0, beta_word = 0;            // u32 words per layer slot; beta (f64) at word beta_word
     BetaController beta_ctl;
+    bm_pcg64 rng{};  // method RANDOM: numpy's PCG64 stream of harness.py:299-300, advanced on the host
     std::vector<int32_t *> bo_dev_l, bo_host_l;   // per-layer buffer maps (E + shared)
     cudaStream_t cap_stream = nullptr;
     bool use_graphs = true;
@@ -159,7 +213,7 @@ struct bm_engine {
     // a third, smaller FFN launch per layer-step (FFN roofline 0.84 -> 0.81, 0.49 -> 0.36); off
     bool split_fetched = false;
     bm_engine_stats stats{};
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev, copy_ev;
+    TimingRing stall_ev, copy_ev;
     std::vector<uint8_t> mask_tmp;
     std::vector<double> pend_done;
     std::vector<int32_t> pend_exp;
@@ -237,10 +291,7 @@ struct bm_engine {
         int b;
         ENG_TRY(alloc_buffer(&b));
         cudaEvent_t c0 = nullptr, c1 = nullptr;  // copy-engine busy time, for the PCIe roofline
-        if (copy_timing) {
-            ENG_CUDA(cudaEventCreate(&c0));
-            ENG_CUDA(cudaEventCreate(&c1));
-        }
+        if (copy_timing) ENG_TRY(copy_ev.next(&c0, &c1));
         cudaStream_t done = s;
         if (coded) {
             Ring &r = (s == prefetch_stream) ? ring_prefetch : ring_copy;
@@ -259,9 +310,9 @@ struct bm_engine {
             if (c1) ENG_CUDA(cudaEventRecord(c1, s));
             stats.wire_bytes += (int64_t)buf_bytes;
         }
-        if (c0) copy_ev.emplace_back(c0, c1);
         ENG_CUDA(cudaEventRecord(ready[l][e], done));
         ready_pending[l][e] = 1;
+        ready_stream[l][e] = done;
         phys[l][e] = b;
         stats.h2d_bytes += (int64_t)buf_bytes;
         return BM_OK;
@@ -304,7 +355,8 @@ struct bm_engine {
         ENG_TRY(bm::buddy_remap_impl(topk, allowed, nullptr, 0, B, k, E, bm_dev_l[l],
                                      tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr, nullptr,
                                      tbl_len ? tbl_len + (size_t)l * E : nullptr, K > 0 ? K : 1, cfg.search_rank_h,
-                                     cfg.rho, cfg.fallback, cfg.method, cfg.beta,
+                                     cfg.rho, cfg.fallback,
+                                     cfg.method == BM_METHOD_RANDOM ? BM_METHOD_ORIGINAL : cfg.method, cfg.beta,
                                      reinterpret_cast<const double *>(bm_dev_l[l] + beta_word), 0.0, 0.0, 1, nullptr,
                                      1.0, executed, kind, used, delta, batch_ok, s));
         ENG_CUDA(cudaMemcpyAsync(plan_host, plan_dev, plan_bytes(B, k), cudaMemcpyDeviceToHost, s));
@@ -317,6 +369,8 @@ struct bm_engine {
     int enqueue_post1(int l, float *h, int64_t B, cudaStream_t s) {
         const int Et = E + Ssh, kt = k + Ssh;
         ENG_CUDA(cudaMemcpyAsync(bo_dev_l[l], bo_host_l[l], 3 * Et * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        if (cfg.method == BM_METHOD_RANDOM)  // the host-drawn plan [executed | kind] replaces K2's on-demand plan
+            ENG_CUDA(cudaMemcpyAsync(executed, exec_h, (size_t)B * k * 5, cudaMemcpyHostToDevice, s));
         const int32_t *pe = executed;
         const uint8_t *pk = kind;
         if (Ssh) {  // every token also runs the shared experts with weight 1
@@ -410,6 +464,8 @@ struct bm_engine {
         ENG_TRY(run(g_pre, l, 0, h, B, s, [&](cudaStream_t st) { return enqueue_pre(l, h, B, st); }));
         ENG_CUDA(cudaEventRecord(plan_ev, s));
         ENG_CUDA(cudaEventSynchronize(plan_ev));
+        if (cfg.method == BM_METHOD_RANDOM)  // substitution.random_plan per token (harness.py:358-359)
+            ENG_TRY(bm::random_plan_batch(topk_h, B, k, bm_host_l[l], E, &rng, exec_h, kind_h, nullptr));
         if (cfg.method == BM_METHOD_BUDDY) {
             for (int64_t b = 0; b < B; ++b) stats.gate_forbidden += allowed_h[b] ? 0 : 1;
             stats.batch_bypassed += batch_ok_h[0] ? 0 : 1;
@@ -502,8 +558,7 @@ struct bm_engine {
         const bool fetched = !waits.empty();
         if (fetched) {
             cudaEvent_t a, bb;
-            ENG_CUDA(cudaEventCreate(&a));
-            ENG_CUDA(cudaEventCreate(&bb));
+            ENG_TRY(stall_ev.next(&a, &bb));
             ENG_CUDA(cudaEventRecord(a, s));
             if (split_late) {
                 for (size_t i = 0; i + 1 < waits.size(); ++i) ENG_CUDA(cudaStreamWaitEvent(s, waits[i], 0));
@@ -513,7 +568,6 @@ struct bm_engine {
                 for (cudaEvent_t w : waits) ENG_CUDA(cudaStreamWaitEvent(s, w, 0));
             }
             ENG_CUDA(cudaEventRecord(bb, s));
-            stall_ev.emplace_back(a, bb);
         }
         ENG_TRY(run(g_post2, l, split_late ? 2 : (fetched ? 1 : 0), h, B, s,
                     [&](cudaStream_t st) { return enqueue_post2(l, h, B, fetched, split_late, st); }));
@@ -538,7 +592,19 @@ struct bm_engine {
         for (int e = 0; e < E; ++e) {
             const int b = phys[l][e];
             if (b < 0 || mask_tmp[e] || std::find(pend.begin(), pend.end(), e) != pend.end()) continue;
-            bufs[b].free_ev = layer_done[l];
+            if (ready_pending[l][e]) {
+                // Prefetched, settled and evicted before any step used it: its copy/decode may
+                // still be writing the buffer, and layer_done[l] does not follow it. The
+                // buffer's next writer waits for both (recorded on the producing stream, so
+                // the compute stream never waits for a speculative copy).
+                cudaStream_t ps = ready_stream[l][e];
+                ENG_CUDA(cudaStreamWaitEvent(ps, layer_done[l], 0));
+                ENG_CUDA(cudaEventRecord(buf_ev[b], ps));
+                bufs[b].free_ev = buf_ev[b];
+                ++stats.inflight_releases;
+            } else {
+                bufs[b].free_ev = layer_done[l];
+            }
             free_list.push_back(b);
             phys[l][e] = -1;
             ready_pending[l][e] = 0;
@@ -553,11 +619,10 @@ struct bm_engine {
                 if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : layer_done)
             if (e) cudaEventDestroy(e);
-        for (auto *evs : {&stall_ev, &copy_ev})
-            for (auto &p : *evs) {
-                cudaEventDestroy(p.first);
-                cudaEventDestroy(p.second);
-            }
+        stall_ev.release();
+        copy_ev.release();
+        for (cudaEvent_t e : buf_ev)
+            if (e) cudaEventDestroy(e);
         for (auto *m : {&g_pre, &g_post, &g_post2})
             for (auto &kv : *m)
                 if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
@@ -600,6 +665,10 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     if (L < 1 || E < 1 || E + (c->num_shared > 0 ? c->num_shared : 0) > 256 || k < 1 || k > E ||
         c->max_batch < 1 || g->cap < 0 || g->cap > E) {
         bm::set_error("engine: bad configuration");
+        return BM_ECONFIG;
+    }
+    if (c->method < BM_METHOD_BUDDY || c->method > BM_METHOD_RANDOM) {
+        bm::set_error("engine: unknown method %d", c->method);
         return BM_ECONFIG;
     }
     if (c->method == BM_METHOD_BUDDY && (!tbl_ids || !tbl_len || tbl_k < 1)) {
@@ -662,6 +731,11 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     g->phys.assign(L, std::vector<int>(E, -1));
     g->ready.assign(L, std::vector<cudaEvent_t>(E, nullptr));
     g->ready_pending.assign(L, std::vector<uint8_t>(E, 0));
+    g->ready_stream.assign(L, std::vector<cudaStream_t>(E, nullptr));
+    g->buf_ev.assign(g->nbufs, nullptr);
+    for (int b = 0; b < g->nbufs; ++b) ENG_CUDA(cudaEventCreateWithFlags(&g->buf_ev[b], cudaEventDisableTiming));
+    ENG_TRY(g->stall_ev.init());
+    ENG_TRY(g->copy_ev.init());
     g->layer_done.assign(L, nullptr);
     for (int l = 0; l < L; ++l) {
         for (int e = 0; e < E; ++e) ENG_CUDA(cudaEventCreateWithFlags(&g->ready[l][e], cudaEventDisableTiming));
@@ -729,6 +803,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     g->bm_stride = g->beta_word + 2;
     ENG_TRY(g->dmalloc(&g->bm_dev_all, (size_t)L * g->bm_stride));
     ENG_TRY(g->hmalloc(&g->bm_host_all, (size_t)L * g->bm_stride));
+    g->rng = c->rng;
     g->beta_ctl.beta = c->beta;
     g->beta_ctl.budget = c->pcie_budget_bytes;
     g->beta_ctl.expert_bytes = (double)c->expert_bytes;
@@ -813,19 +888,11 @@ extern "C" int bm_engine_step(bm_engine *e, float *h, int64_t B, const int32_t *
 
 extern "C" int bm_engine_stats_get(bm_engine *e, bm_engine_stats *out, int32_t reset) {
     if (!e || !out) return BM_EINVAL;
-    for (auto *evs : {&e->stall_ev, &e->copy_ev}) {
-        double sum = 0.0;
-        for (auto &p : *evs) {
-            ENG_CUDA(cudaEventSynchronize(p.second));
-            float ms = 0.f;
-            ENG_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
-            sum += ms;
-            cudaEventDestroy(p.first);
-            cudaEventDestroy(p.second);
-        }
-        evs->clear();
-        (evs == &e->stall_ev ? e->stats.stall_ms : e->stats.copy_ms) += sum;
-    }
+    double st = 0.0, cp = 0.0;
+    ENG_TRY(e->stall_ev.drain(&st));
+    ENG_TRY(e->copy_ev.drain(&cp));
+    e->stats.stall_ms += st;
+    e->stats.copy_ms += cp;
     ENG_TRY(bm_cache_now(e->cache, &e->stats.sim_now_ms));
     e->stats.beta = e->beta_ctl.beta;
     *out = e->stats;

@@ -20,7 +20,8 @@ from .errors import ConfigurationError
 from .ops import ACT_SWIGLU, FALLBACK_PREFETCH, METHOD_BUDDY
 
 POLICIES = {"lru": 0, "lfu": 1, "freq_static": 2}
-METHODS = {"buddy": 0, "original": 1, "identity": 2}
+METHODS = {"buddy": 0, "original": 1, "identity": 2, "random": 3}
+_RNG_TAG_RANDOM_METHOD = 31  # harness.py:44: the Random arm's stream is SeedSequence([run.seed, 31])
 
 
 class HostMirror:
@@ -202,6 +203,7 @@ class EngineSpec:
     num_shared: int = 0
     fetch_codec: int | None = None  # None: the mirrors' format (HostMirror.codec)
     pcie_budget_bytes: float | None = None  # adaptive beta (gating.BetaController) when set
+    run_seed: int = 0  # method "random": the plan stream of harness.py:299-300
 
     @property
     def buf_elems(self) -> int:
@@ -242,6 +244,8 @@ class DecodeEngine:
         cfg.expert_bytes = ebytes
         cfg.num_shared = int(spec.num_shared)
         cfg.pcie_budget_bytes = -1.0 if spec.pcie_budget_bytes is None else float(spec.pcie_budget_bytes)
+        cfg.rng = N.Pcg64State.from_generator(
+            np.random.default_rng(np.random.SeedSequence([int(spec.run_seed), _RNG_TAG_RANDOM_METHOD])))
         cfg.fetch_codec = int(spec.fetch_codec if spec.fetch_codec is not None else getattr(mirrors[0], "codec", 0))
         L, E = spec.num_layers, spec.num_experts
         ptrs = (C.c_void_p * L)(*[m.ptr for m in mirrors])

@@ -132,6 +132,14 @@ def fidelity(outputs: np.ndarray, oracle: np.ndarray, readout: np.ndarray) -> tu
     return float(cos.mean().item()), float(agree.item())
 
 
+def events_array(events) -> np.ndarray:
+    """SimEvents as an [n,7] float64 array (time, kind code, layer, token,
+    expert, bytes, stall), the layout of the golden fixtures."""
+    code = {k: i for i, k in enumerate(memtier._EV_BY_CODE)}
+    return np.array([(e.time_ms, code[e.kind], e.layer, e.token, e.expert, e.bytes, e.stall_ms) for e in events],
+                    np.float64).reshape(-1, 7)
+
+
 def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=None) -> SimResult:
     """The reference decode replay (harness.py:221-424) on the engine.
     ``tables``: dense (ids[L,E,K] int32, lens[L,E] int32) or a list of
@@ -141,8 +149,8 @@ def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=Non
     spec = _spec(c)
     L, E = spec.num_layers, spec.experts_per_layer
     method = c["method"]
-    if method not in ("buddy", "original"):
-        raise ConfigurationError(f"method {method!r} is not a hot-path method (buddy|original)")
+    if method not in ("buddy", "original", "random"):
+        raise ConfigurationError(f"unknown method {method!r} (buddy|original|random)")
     cap = int(np.floor(c["cache.rate"] * E))
     dev = torch.device("cuda", torch.cuda.current_device())
     mirrors = []
@@ -181,7 +189,8 @@ def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=Non
                     fp32_weights=True, expert_bytes=2 * spec.hidden_dim * spec.ffn_dim * 8,
                     load_ms=c["cost.expert_load_ms"], hit_ms=c["cost.hit_ms"], compute_ms=c["cost.expert_compute_ms"],
                     pcie_bw_bytes_per_s=c["cost.pcie_bw_bytes_per_s"],
-                    pcie_budget_bytes=c["gate.pcie_budget_bytes"] if method == "buddy" else None)
+                    pcie_budget_bytes=c["gate.pcie_budget_bytes"] if method == "buddy" else None,
+                    run_seed=c["run.seed"])
     initial = [memtier.initial_residents(E, cap, c["cache.policy"], c["run.seed"], l) for l in range(L)]
     eng = DecodeEngine(es, mirrors, torch.tensor(gw, dtype=torch.float32, device=dev),
                        torch.tensor(gb, dtype=torch.float32, device=dev), ids, lens, taus, initial)

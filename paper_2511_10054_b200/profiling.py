@@ -18,6 +18,7 @@ from dataclasses import dataclass
 import torch
 
 from . import ops
+from .errors import ConfigurationError, InputError
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -69,10 +70,14 @@ def count_shard(topk_shard: torch.Tensor, num_experts: int, global_start: int, w
 
 
 def profile_trace(topk: torch.Tensor, num_experts: int, warmup_steps: int = 256, group=None, sharded=True,
-                  counter=count_kernel) -> CoactCounts:
-    """Count a full trace (every rank holds it, or its own shard when
-    sharded=False with topk = the local shard and global offsets implied by
-    shard_range) and all-reduce across the process group."""
+                  counter=count_kernel, total_tokens: int | None = None) -> CoactCounts:
+    """Count a trace and all-reduce the counters across the process group.
+
+    sharded=True: every rank holds the whole trace and counts its
+    shard_range. sharded=False: ``topk`` is this rank's own shard of a
+    ``total_tokens``-token trace split by shard_range, so its first row has
+    the global index shard_range(total_tokens, rank, world)[0] (warm-up
+    weighting follows the global index, profiler.py:81-95)."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
@@ -80,6 +85,13 @@ def profile_trace(topk: torch.Tensor, num_experts: int, warmup_steps: int = 256,
     if sharded and world > 1:
         a, b = shard_range(N, rank, world)
         local = count_shard(topk[a:b], num_experts, a, warmup_steps, counter)
+    elif world > 1:
+        if total_tokens is None:
+            raise ConfigurationError("profile_trace(sharded=False) on several ranks needs total_tokens")
+        a, b = shard_range(int(total_tokens), rank, world)
+        if b - a != N:
+            raise InputError(f"rank {rank} holds {N} tokens, shard_range gives {b - a}")
+        local = count_shard(topk, num_experts, a, warmup_steps, counter)
     else:
         local = count_shard(topk, num_experts, 0, warmup_steps, counter)
     if world == 1:

@@ -326,6 +326,31 @@ def sim_beta_case() -> dict:
     return out
 
 
+def sim_random_case() -> dict:
+    """The paper's Random baseline (substitution.random_plan through
+    run_simulation(method="random"), harness.py:299-300, 358-359) on the tiny
+    config at two cache rates and two run seeds: event logs, outputs and
+    metrics, so the engine's host PCG64 replica is pinned draw for draw."""
+    out = {}
+    for rate, seed in ((0.5, 0), (0.375, 5), (0.75, 11)):
+        c = parse_config_text(TINY_SIM)
+        c.set("method", "random"); c.set("stream.seed", "2"); c.set("stream.num_tokens", "320")
+        c.set("cache.rate", str(rate)); c.set("run.seed", str(seed))
+        r = harness.run_simulation(c)
+        tag = f"c{int(rate * 1000)}_s{seed}"
+        out[f"{tag}_events"] = np.array([(e.time_ms, EV[e.kind], e.layer, e.token, e.expert, e.bytes, e.stall_ms)
+                                         for e in r.events], np.float64).reshape(-1, 7)
+        out[f"{tag}_outputs"] = r.outputs
+        mt = r.metrics
+        out[f"{tag}_metrics"] = np.array([mt.tokens_per_s, mt.stall_ms, mt.compute_ms, mt.hits,
+                                          mt.misses_ondemand, mt.misses_substituted, mt.drops,
+                                          mt.prefetch_issued, mt.prefetch_completed, mt.evictions,
+                                          mt.read_bytes, mt.substitutions, mt.fidelity_cosine,
+                                          mt.fidelity_argmax])
+        out[f"{tag}_cfg"] = np.array([rate, seed])
+    return out
+
+
 def substrate_case() -> dict:
     """Samples of the reference's synthetic substrate (model.py:122-222,
     350-382) so the framework's restatement can be pinned without storing
@@ -352,6 +377,9 @@ def substrate_case() -> dict:
 def main() -> None:
     if sys.argv[1:] == ["beta"]:  # regenerate only the adaptive-beta fixture
         np.savez_compressed(os.path.join(OUT, "sim_tiny_beta.npz"), **sim_beta_case())
+        return
+    if sys.argv[1:] == ["random"]:  # regenerate only the Random-arm fixture
+        np.savez_compressed(os.path.join(OUT, "sim_tiny_random.npz"), **sim_random_case())
         return
     np.savez_compressed(os.path.join(OUT, "remap_corpus_20260819.npz"), **remap_corpus(20260819, 1000))
     np.savez_compressed(os.path.join(OUT, "remap_corpus_1234.npz"), **remap_corpus(1234, 300))
@@ -383,6 +411,7 @@ def main() -> None:
     np.savez_compressed(os.path.join(OUT, "forward_tiny.npz"), **forward_case(tiny, 32, 5))
     np.savez_compressed(os.path.join(OUT, "sim_tiny.npz"), **sim_case())
     np.savez_compressed(os.path.join(OUT, "substrate.npz"), **substrate_case())
+    np.savez_compressed(os.path.join(OUT, "sim_tiny_random.npz"), **sim_random_case())
     print("golden fixtures written to", OUT, "with buddysim", buddysim.__version__)
 
 

@@ -96,24 +96,57 @@ def test_run_simulation_metrics_equal_reference(cuda_ok, method):
     assert abs(m.fidelity_cosine - ref[14]) <= 1e-6 and abs(m.fidelity_argmax - ref[15]) <= 1e-9
 
 
-def test_engine_bf16_tensor_core_mode_same_decisions(cuda_ok):
-    """The bf16 tcgen05 path makes the same cache decisions on this workload
-    (routing is robust to bf16 expert outputs here) and stays within the bf16
-    tolerance of the reference outputs."""
+def test_engine_bf16_tensor_core_mode_decisions_and_tolerance(cuda_ok):
+    """The bf16 tcgen05 path against the fp32 path (whose decisions equal the
+    reference's, test above): every (layer-step, token) whose routing is the
+    same in both traces must get the same plan (remap is a function of the
+    routing, the snapshot and the gates), the residency snapshots must agree
+    until the first routing difference, and tokens whose routing never
+    diverged must stay within the bf16 tolerance (max rel 2e-2) of the
+    reference outputs. The share of tokens that diverge anywhere is reported
+    and bounded."""
     g = golden("sim_tiny.npz")
-    eng = _engine("buddy", g, fp32=False)
-    out = _run(eng)
+    e32 = _engine("buddy", g)
+    e32.set_trace(True)
+    out32 = _run(e32)
+    t32 = e32.trace()
+    e32.close()
+    e16 = _engine("buddy", g, fp32=False)
+    e16.set_trace(True)
+    out16 = _run(e16)
+    t16 = e16.trace()
+    e16.close()
+    assert len(t32) == len(t16)
+    n_tok = out16.shape[0]
+    diverged = np.zeros(n_tok, bool)
+    same_route_same_plan = True
+    snapshots_equal_until_divergence = True
+    t0 = 0
+    seen_div = False
+    for a, b in zip(t32, t16):
+        B = a["topk"].shape[0]
+        step_tokens = np.arange(t0 % n_tok, t0 % n_tok + B)
+        if not seen_div:
+            snapshots_equal_until_divergence &= bool(np.array_equal(a["mask"], b["mask"]))
+        same = np.all(a["topk"] == b["topk"], axis=1) & (a["allowed"] == b["allowed"])
+        if np.array_equal(a["mask"], b["mask"]) and a["batch_ok"] == b["batch_ok"]:
+            same_route_same_plan &= bool(np.array_equal(a["executed"][same], b["executed"][same]) and
+                                         np.array_equal(a["kind"][same], b["kind"][same]))
+        planned_same = np.all(a["executed"] == b["executed"], axis=1) & np.all(a["kind"] == b["kind"], axis=1)
+        if not same.all():
+            seen_div = True
+        diverged[step_tokens[~(same & planned_same)]] = True
+        if a["layer"] == 3:
+            t0 += B
     ro = g["buddy_outputs"]
-    rel = np.linalg.norm(out - ro, axis=1) / np.linalg.norm(ro, axis=1)
-    ev = eng.sorted_events()
-    ref = g["buddy_events"]
-    n = min(len(ev), len(ref))
-    first = np.flatnonzero(np.any(ev[:n, 1:5] != ref[:n, 1:5], axis=1))
-    first = int(first[0]) if len(first) else n
-    print(f"bf16 engine: output rel median {np.median(rel):.3e} max {rel.max():.3e}; "
-          f"events identical for the first {first}/{len(ref)}")
-    assert np.median(rel) <= 2e-2, np.median(rel)
-    eng.close()
+    rel = np.linalg.norm(out16 - ro, axis=1) / np.linalg.norm(ro, axis=1)
+    frac = diverged.mean()
+    print(f"bf16 engine: {100 * frac:.2f}% of tokens routed or planned differently at some layer; "
+          f"max rel on the rest {rel[~diverged].max():.3e} (median {np.median(rel):.3e})")
+    assert same_route_same_plan
+    assert snapshots_equal_until_divergence
+    assert frac <= 0.05, frac
+    assert rel[~diverged].max() <= 2e-2, rel[~diverged].max()
 
 
 def test_engine_split_fetched_ffn_same_decisions(cuda_ok, monkeypatch):

@@ -186,3 +186,55 @@ def test_nesting_across_capacities():
         cur = set(np.flatnonzero(M.init_residency(64, c, "lru", seed=3).mask))
         assert prev <= cur
         prev = cur
+
+
+def test_random_plan_host_replica_equals_numpy_stream():
+    """bm_random_plan (C++ PCG64 + Lemire bounded draws) makes the draws of
+    numpy's Generator.integers (the reference's random_plan,
+    substitution.py:227-248): plans equal the oracle's on shared seeds, and the
+    generator state handed back equals the one numpy reaches."""
+    import ctypes
+    import oracle as O
+    from paper_2511_10054_b200 import _native as N
+    rng = np.random.default_rng(5)
+    for case in range(300):
+        E = int(rng.choice([4, 8, 33, 64, 128, 160]))
+        k = int(rng.integers(1, min(8, E) + 1))
+        B = int(rng.integers(1, 17))
+        topk = np.stack([rng.permutation(E)[:k] for _ in range(B)]).astype(np.int32)
+        mask = rng.random(E) < rng.random()
+        seed = int(rng.integers(0, 2**31))
+        ga = np.random.default_rng(np.random.SeedSequence([seed, 31]))
+        gb = np.random.default_rng(np.random.SeedSequence([seed, 31]))
+        if case % 4 == 1:  # leave a buffered 32-bit half in both
+            ga.integers(0, 7), gb.integers(0, 7)
+        ex_r, kd_r, used_r = O.random_plan(topk, mask, ga)
+        st = N.Pcg64State.from_generator(gb)
+        ex = np.empty((B, k), np.int32)
+        kd = np.empty((B, k), np.uint8)
+        used = np.empty(B, np.int32)
+        m8 = mask.astype(np.uint8)
+        N.call("bm_random_plan", topk.ctypes.data, B, k, m8.ctypes.data, E, ctypes.byref(st), ex.ctypes.data,
+               kd.ctypes.data, used.ctypes.data)
+        st.store_into(gb)
+        assert np.array_equal(ex, ex_r) and np.array_equal(kd, kd_r) and np.array_equal(used, used_r), case
+        assert ga.bit_generator.state == gb.bit_generator.state, case
+
+
+def test_random_plan_api_matches_reference_semantics():
+    """substitution.random_plan over the C-ABI advances the caller's numpy
+    generator exactly like the reference function does."""
+    from paper_2511_10054_b200.model import RouterDecision
+    from paper_2511_10054_b200.substitution import random_plan
+    import oracle as O
+    g1 = np.random.default_rng(np.random.SeedSequence([3, 31]))
+    g2 = np.random.default_rng(np.random.SeedSequence([3, 31]))
+    mask = np.array([1, 0, 1, 0, 1, 1, 0, 0], bool)
+    for t in range(50):
+        topk = np.array([(t * 3) % 8, (t * 5 + 1) % 8 if (t * 5 + 1) % 8 != (t * 3) % 8 else (t * 5 + 2) % 8])
+        d = RouterDecision(token=t, layer=0, logits=np.zeros(8), topk=topk, probs_renorm=np.array([0.6, 0.4]),
+                           temperature=1.0)
+        p = random_plan(d, mask, g1)
+        ex, kd, used = O.random_plan(topk[None], mask, g2)
+        assert [s.executed for s in p.slots] == list(ex[0]) and p.replacements_used == int(used[0])
+    assert g1.bit_generator.state == g2.bit_generator.state

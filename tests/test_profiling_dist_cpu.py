@@ -50,6 +50,12 @@ def _worker(rank, world, port, q):
             _, p_warm, _, _ = O.coact_count(g["topk"][:200], None, E, 0, 0, 0.0)
             q.put((np.array_equal(c2.pairs.double().numpy(), p_main),
                    np.array_equal(c2.warm_pairs.double().numpy(), p_warm), c2.tokens_seen == 300))
+        # each rank holds only its own shard (sharded=False): global warm-up offsets
+        a, b = P.shard_range(300, rank, world)
+        c3 = P.profile_trace(topk2[a:b].clone(), E, 200, sharded=False, counter=_oracle_counter, total_tokens=300)
+        if rank == 0:
+            q.put((torch.equal(c3.pairs, c2.pairs), torch.equal(c3.warm_pairs, c2.warm_pairs),
+                   c3.tokens_seen == 300))
     finally:
         dist.destroy_process_group()
 
@@ -72,8 +78,8 @@ def test_sharded_profile_allreduce_gloo_world2():
     for p in procs:
         p.join(timeout=120)
     assert all(p.exitcode == 0 for p in procs)
-    r1, r2 = q.get(timeout=5), q.get(timeout=5)
-    assert all(r1) and all(r2), (r1, r2)
+    r1, r2, r3 = q.get(timeout=5), q.get(timeout=5), q.get(timeout=5)
+    assert all(r1) and all(r2) and all(r3), (r1, r2, r3)
 
 
 def test_shard_ranges_cover_exactly():
