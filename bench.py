@@ -42,7 +42,7 @@ MODELS = {
 
 
 def _shape(model: str):
-    from paper_2511_10054_b200.workload import SHAPES, SHARED
+    from paper_2511_10054_b200.synth import SHAPES, SHARED
     E, k, d, f, rate = SHAPES[model]
     return E, k, d, f, rate, SHARED.get(model, 0)
 
@@ -161,14 +161,101 @@ def _dist():
     return ws, rank, local
 
 
-def _allmax(v: float, ws: int):
-    if ws == 1:
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_or_check(args) -> None:
+    """--gpus N without a torchrun environment re-executes this script under
+    `torch.distributed.run` with N local ranks (one process per GPU), so
+    `python bench.py --gpus N` and the torchrun launch are the same run. Under
+    torchrun the world size must equal --gpus (a mismatch fails loudly)."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+                   *sys.argv[1:]]
+            print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+            sys.exit(subprocess.call(cmd))
+        return
+    if int(ws) != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}; launch one rank per GPU with a "
+                         f"matching --gpus")
+
+
+class Comm:
+    """The process group of a multi-rank run: NCCL with one GPU per rank; gloo
+    (host tensors) only for the single-GPU rehearsal where several ranks share
+    a device (BMOE_ALLOW_SHARED_GPU=1)."""
+
+    def __init__(self, ws: int, rank: int, local: int):
+        import torch
+        self.ws, self.rank, self.local = ws, rank, local
+        ndev = torch.cuda.device_count()
+        self.shared_gpu = ws > ndev
+        if self.shared_gpu and ws > 1 and os.environ.get("BMOE_ALLOW_SHARED_GPU") != "1":
+            raise SystemExit(f"bench.py: {ws} ranks but {ndev} visible GPU(s); one rank per GPU "
+                             f"(BMOE_ALLOW_SHARED_GPU=1 rehearses several ranks on one GPU over gloo)")
+        self.device = local % max(ndev, 1)
+        torch.cuda.set_device(self.device)
+        self.backend = None
+        self.nranks = 1
+        if ws > 1:
+            import torch.distributed as dist
+            self.backend = "gloo" if self.shared_gpu else "nccl"
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+            else:
+                dist.init_process_group("gloo")
+            # the communicator really spans every rank: an all-reduce of ones
+            self.nranks = int(self.all_reduce(torch.ones(1, dtype=torch.float64, device="cuda")).item())
+            if self.nranks != ws:
+                raise SystemExit(f"bench.py: all-reduce over the {self.backend} group saw {self.nranks} ranks, "
+                                 f"expected {ws}")
+
+    def all_reduce(self, t, op="sum"):
+        """In-place all-reduce of a device tensor (through host memory on gloo)."""
+        if self.ws == 1:
+            return t
+        import torch.distributed as dist
+        o = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX}[op]
+        if self.backend == "gloo":
+            h = t.cpu()
+            dist.all_reduce(h, op=o)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=o)
+        return t
+
+    def barrier(self):
+        if self.ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def info(self) -> dict:
+        import torch
+        d = {"backend": self.backend or "none (one rank)", "world_size": self.ws, "allreduce_ranks": self.nranks,
+             "device": f"cuda:{self.device}", "ranks_share_gpu": self.shared_gpu}
+        if self.backend == "nccl":
+            d["nccl_version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+        return d
+
+    def close(self):
+        if self.ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+def _allmax(v: float, comm: "Comm"):
+    if comm.ws == 1:
         return v
     import torch
-    import torch.distributed as dist
     t = torch.tensor([v], device="cuda", dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return float(comm.all_reduce(t, "max").item())
 
 
 def _mirror_bytes_per_layer(model: str, codec: int) -> float:
@@ -180,104 +267,96 @@ def _layers_for_host(ws: int, requested: int | None, codec: int = 1, model: str 
     """The model's layer count when the pinned mirrors (one per replica, or
     one node-shared copy: ws=1) fit in 60% of host RAM, fewer otherwise
     (config.layers says which)."""
-    from paper_2511_10054_b200.workload import host_mem_available
+    from paper_2511_10054_b200.synth import host_mem_available
     fit = int(0.6 * host_mem_available() / (ws * _mirror_bytes_per_layer(model, codec)))
     L = min(MODELS[model]["layers"], max(1, fit))
     return min(L, requested) if requested else L
 
 
-def _plan_mirrors(ws: int, local: int, args):
-    """Replicas of one model on one node share ONE expert mirror in /dev/shm
-    (SharedMirror: written by local rank 0, mapped + page-locked by every
-    rank) when it fits there; otherwise every rank keeps a private pinned
-    mirror and the layer count shrinks with the replica count."""
-    from paper_2511_10054_b200.workload import ShareSpec, shm_bytes_free
-    if ws == 1:
-        return _layers_for_host(1, args.layers, args.codec, args.model), None
+def _plan_mirrors(comm: "Comm", args):
+    """Host placement of the expert mirrors. Every rank first binds to the
+    CPUs of its GPU's NUMA node. Replicas of one model on one node share the
+    mirror through /dev/shm (SharedMirror: written by one rank, mapped and
+    page-locked by the others): one copy per NUMA node that hosts a GPU when
+    those copies fit in /dev/shm and host memory (the writer is the lowest
+    local rank on that node, bound there, so first-touch puts the pages next
+    to the GPUs that fetch them); one node-wide copy when only one fits;
+    otherwise every rank keeps a private pinned mirror and the layer count
+    shrinks with the replica count. Returns (layers, ShareSpec|None, info)."""
+    from paper_2511_10054_b200 import numa
+    from paper_2511_10054_b200.workload import ShareSpec, host_mem_available, shm_bytes_free
+    node = numa.gpu_numa_node(comm.device)
+    bound = numa.bind_to_node(node) if node >= 0 else False
+    info = {"numa_nodes": numa.num_nodes(), "gpu_numa_node": node, "bound_to_node_cpus": bound}
     L = _layers_for_host(1, args.layers, args.codec, args.model)
-    if shm_bytes_free() >= 1.05 * L * _mirror_bytes_per_layer(args.model, args.codec):
-        import torch.distributed as dist
-        tag = f"bmoe_{os.environ.get('TORCHELASTIC_RUN_ID', 'run')}_{os.environ.get('MASTER_PORT', '0')}_{args.model}"
-        return L, ShareSpec(tag=tag, owner=(local == 0), barrier=dist.barrier)
-    return _layers_for_host(ws, args.layers, args.codec, args.model), None
+    if comm.ws == 1:
+        info["host_mirror"] = "private pinned"
+        return L, None, info
+    import torch.distributed as dist
+    where = [None] * comm.ws
+    dist.all_gather_object(where, (comm.local, node))
+    nodes = sorted({n for _, n in where})
+    per_copy = L * _mirror_bytes_per_layer(args.model, args.codec)
+    shm, mem = shm_bytes_free(), host_mem_available()
+    run = f"bmoe_{os.environ.get('TORCHELASTIC_RUN_ID', 'run')}_{os.environ.get('MASTER_PORT', '0')}_{args.model}"
+    if len(nodes) > 1 and shm >= 1.05 * len(nodes) * per_copy and 0.6 * mem >= len(nodes) * per_copy:
+        owner = comm.local == min(l for l, n in where if n == node)
+        info["host_mirror"] = f"node-shared /dev/shm, one copy per NUMA node ({len(nodes)})"
+        return L, ShareSpec(tag=f"{run}_n{node}", owner=owner, barrier=comm.barrier), info
+    if shm >= 1.05 * per_copy:
+        info["host_mirror"] = "node-shared /dev/shm, one copy" + (
+            f" (a copy per NUMA node ({len(nodes)}) does not fit)" if len(nodes) > 1 else "")
+        return L, ShareSpec(tag=run, owner=(comm.local == 0), barrier=comm.barrier), info
+    info["host_mirror"] = "private pinned (a shared copy does not fit /dev/shm)"
+    return _layers_for_host(comm.ws, args.layers, args.codec, args.model), None, info
 
 
 # ------------------------------------------------------------------ CPU legs
-def stage_layer_f64(wl, layer: int):
-    """The reference holds float64 expert stacks (model.py:173-186); convert
-    one layer's bf16 mirror once, outside any timed region."""
-    from paper_2511_10054_b200.engine import mirror_expert
-    E, d, f = wl.eng.num_experts + wl.eng.num_shared, wl.eng.d, wl.eng.f
-    out = {}
-    for e in range(E):
-        m = mirror_expert(wl.mirrors[layer], e, 3 * d * f).view(3, -1).float().cpu().numpy().astype(np.float64)
-        out[e] = (m[0].reshape(f, d), m[1].reshape(f, d), m[2].reshape(d, f))
-    return out
+def cpu_decode(args, L: int, steps: int, timed_from: int, layers_run: int | None = None, log=None):
+    """The reference's decode step on the host cores (oracle/decode_cpu.py):
+    f64, the GPU arm's exact inputs (synthetic weights regenerated on the host
+    bit for bit, the same gate/token streams, tables built from the same
+    profile stream), layer-major with every (step, layer) timed. No GPU, no
+    libbmoe. Returns (per-step seconds of the timed steps, CpuDecode)."""
+    from oracle.decode_cpu import CpuDecode
+    n_total = (args.warmup + 3 * args.steps) * args.batch  # the GPU arm's token stream length
+    cd = CpuDecode(args.model, L, args.batch, profile_tokens=args.profile_tokens, cache_rate=args.cache_rate,
+                   stream_tokens=n_total)
+    per_step, _ = cd.run(steps, timed_from, layers_run=layers_run, log=log)
+    return per_step, cd
 
 
-def cpu_reference_sample(wl, layer: int, B: int, seed: int, stacks, method: str = "buddy") -> float:
-    """The reference algorithm for one layer-step, run by the numpy oracle port
-    (oracle/, f64 like the reference): route_batch -> evaluate_gates ->
-    substitute_batch -> forward_batch (per token and slot, as model.py:338-340
-    gathers weights per slot) -> layer_update (model.py:231-347,
-    gating.py:148-165, substitution.py:193-208). Returns seconds."""
-    import oracle as O
-    from paper_2511_10054_b200.workload import initial_residents
-    E, k, S = wl.eng.num_experts, wl.eng.top_k, wl.eng.num_shared
-    x = wl.tokens(seed, B).astype(np.float64)
-    gw = wl.gate_w[layer].double().cpu().numpy()
-    gb = wl.gate_b[layer].double().cpu().numpy()
-    ids = wl.tbl_ids[layer].cpu().numpy()
-    lens = wl.tbl_len[layer].cpu().numpy()
-    mask = np.zeros(E, bool)
-    mask[initial_residents(E, wl.eng.capacity, 0, layer)] = True
-    t0 = time.perf_counter()
-    z, topk, probs = O.route(x, gw, gb, k)
-    _, _, ok, _, batch_ok = O.gate_batch(probs, topk, mask, wl.taus[layer], None, 1.0)
-    if method == "buddy":
-        ex, kd, _ = O.remap_batch(topk, z, mask, ids, np.zeros(ids.shape), lens, ok & batch_ok,
-                                  wl.eng.search_rank_h, wl.eng.rho if wl.eng.rho is not None else -1)
-    else:
-        ex, kd, _ = O.ondemand_plan(topk, mask)
-    y = O.forward(x, ex, kd, probs, lambda e, xr: O.ffn_swiglu(xr, *stacks[e]))
-    for sx in range(S):  # shared experts: every token, weight 1
-        y = y + O.ffn_swiglu(x, *stacks[E + sx])
-    O.layer_update(x, y)
-    return time.perf_counter() - t0
-
-
-def run_reference(args, ws, rank):
-    """--impl reference: the reference's CPU path (oracle port; the reference
-    is pure Python/numpy and has no GPU path) on the host cores."""
-    if rank != 0:
-        return
-    import torch
-    from paper_2511_10054_b200 import workload as W
-    L = _layers_for_host(ws, args.layers, args.codec, args.model)
-    # one layer's weights/tables suffice: the sample is one layer-step, the
-    # metric extrapolates to the same L layers as the GPU arm
-    wl = W.build(args.model, layers=1, max_batch=args.batch, profile_tokens=args.profile_tokens)
+def run_reference(args, ws):
+    """--impl reference: the reference's CPU path on the host cores (the
+    reference is pure Python/numpy; its algorithm runs here as the numpy
+    oracle port, f64), on the GPU arm's config: every warm-up and timed step
+    is a real decode step of B tokens through all L layers. Touches no GPU
+    and loads no libbmoe (only oracle/_lib's host weight generator)."""
+    from threadpoolctl import threadpool_limits
+    L = _layers_for_host(1, args.layers, args.codec, args.model)
+    log = (lambda m: print(f"[bench ref] {m}", file=sys.stderr, flush=True))
     cores = len(os.sched_getaffinity(0))
-    Bs = args.cpu_tokens
-    stacks = stage_layer_f64(wl, 0)
-    times = []
-    for i in range(args.warmup + args.steps):
-        sec = cpu_reference_sample(wl, 0, Bs, 1000 + i, stacks)
-        if i >= args.warmup:
-            times.append(sec)
-    per_layer = statistics.mean(times)
-    tps = Bs / (per_layer * L)
+    t0 = time.time()
+    with threadpool_limits(limits=1, user_api="blas"):  # one BLAS thread per worker; the workers span the cores
+        per_step, cd = cpu_decode(args, L, args.warmup + args.steps, args.warmup, log=log)
+    ms = float(np.mean(per_step)) * 1e3
+    tps = args.batch / (ms / 1e3)
+    E, k, d, f, rate, S = _shape(args.model)
     line = {"impl": "reference", "metric": _metric(args.batch),
             "value": tps, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": per_layer * L * 1000.0, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config(args.model, wl, L, args.batch, "buddy"),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (the GPU arm's weights and streams)",
+            "config": _config(args.model, L, args.batch, "buddy", cd.cap, cd.k_max, cd.rate),
             "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": f"{Bs} tokens x 1 layer per step (f64 numpy oracle, BLAS threads={cores}), "
-                                       f"extrapolated x{L} layers"},
-            "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": f"every step: {args.batch} tokens through all {L} layers (route, gates, "
+                                       f"remap, cache replay, f64 SwiGLU forward, layer_update) via the numpy "
+                                       f"oracle, layer-major, each (step, layer) timed; {cores} threads"},
+            "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "tables_sha16": cd.digest, "timed_s": float(np.sum(per_step)),
+            "untimed_s": {"weights_f64": cd.gen_s, "profile_tables": cd.profile_s},
+            "wall_s": time.time() - t0}
+    cd.close()
     print(json.dumps(line), flush=True)
-    wl.close()
 
 
 def _metric(B: int) -> str:
@@ -285,13 +364,13 @@ def _metric(B: int) -> str:
     return f"MoE {phase} tokens/sec at fixed expert-cache budget; expert-miss stall (ms)"
 
 
-def _config(model, wl, L, B, method):
-    E, k, d, f, rate, S = _shape(model)
+def _config(model, L, B, method, capacity, search_rank_h, rate):
+    E, k, d, f, _, S = _shape(model)
     phase = "decode" if B <= 64 else "prefill"
     cfg = {"workload": f"{MODELS[model]['workload']}-{phase}", "model": MODELS[model]["model"],
            "layers": L, "experts": E, "top_k": k, "d_model": d, "d_ff": f, "cache_rate": rate,
-           "capacity_per_layer": wl.eng.capacity, "global_batch": B, "seq_len": 1, "method": method, "rho": 3,
-           "search_rank_h": wl.eng.search_rank_h, "alpha": 0.95, "tau_percentile": 15, "policy": "lru",
+           "capacity_per_layer": capacity, "global_batch": B, "seq_len": 1, "method": method, "rho": 3,
+           "search_rank_h": search_rank_h, "alpha": 0.95, "tau_percentile": 15, "policy": "lru",
            "parallelism": "replicas (one process per GPU, disjoint token streams, no collective)",
            "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
     if S:
@@ -320,59 +399,84 @@ def gen_trace(N: int, E: int, k: int, start: int, end: int, device: str, seed: i
     return out
 
 
-def run_profile_bench(args, ws, rank, local):
+def run_profile_bench(args, comm: "Comm"):
     """BASELINE configs[4]: co-activation profiling sweep, 64M-token trace,
-    E=128, k=8, token-sharded with one NCCL all-reduce (strong scaling)."""
+    E=128, k=8, token-sharded over the ranks with one all-reduce of the
+    packed u64 counters (NCCL over NVLink), then the K7 table on every rank
+    (strong scaling: the trace is fixed, the shards shrink with N)."""
+    import hashlib
+
     import torch
-    import oracle as O
     from paper_2511_10054_b200 import ops, profiling as P
+    ws, rank, local = comm.ws, comm.rank, comm.local
     N, E, k = args.trace_tokens, 128, 8
     a, b = P.shard_range(N, rank, ws)
     trace = gen_trace(N, E, k, a, b, "cuda")
     torch.cuda.synchronize()
-    group = None
+    wend = max(0, min(b - a, 256 - a))
 
-    def one_pass(timing=None):
+    def one_pass(tr, timing=None):
         if timing is not None:
             timing[0].record()
-        wend = max(0, min(b - a, 256 - a))
-        wc, wp = ops.coact_count(trace[:wend], E) if wend else (None, None)
-        mc, mp = ops.coact_count(trace[wend:], E)
+        wc, wp = ops.coact_count(tr[:wend], E) if wend else (None, None)
+        mc, mp = ops.coact_count(tr[wend:], E)
         if timing is not None:
             timing[1].record()
         z1 = torch.zeros(E, dtype=torch.int64, device="cuda")
         z2 = torch.zeros(E, E, dtype=torch.int64, device="cuda")
         c = P.CoactCounts(mc, mp, wc if wc is not None else z1, wp if wp is not None else z2, b - a)
-        if ws > 1:
-            buf = c.pack()
-            torch.distributed.all_reduce(buf, group=group)
-            c = P.CoactCounts.unpack(buf, E)
+        if ws > 1:  # the one exchange step
+            c = P.CoactCounts.unpack(comm.all_reduce(c.pack()), E)
         _, pairs = P.to_f64(c, 0.0)
-        return P.build_table(pairs, 1e-3, 0.95, 16)
+        return c, P.build_table(pairs, 1e-3, 0.95, 16)
 
     for _ in range(args.warmup):
-        one_pass()
+        one_pass(trace)
     torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    clk = ClockSampler(local).ready()
+    comm.barrier()
+    clk = ClockSampler(comm.device).ready()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kt = []
     s.record()
     for _ in range(args.steps):
         ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-        one_pass(ev)
+        counts, table = one_pass(trace, ev)
         kt.append(ev)
     e.record()
     torch.cuda.synchronize()
     clocks = clk.stop()
-    ms = _allmax(s.elapsed_time(e), ws)
+    ms = _allmax(s.elapsed_time(e), comm)
     k_ms = float(np.mean([x.elapsed_time(y) for x, y in kt]))
+    # digest of the merged counters and the table: equal at every N (bit-exact sharding)
+    h = hashlib.sha256()
+    for t in (counts.pairs, counts.counts, counts.warm_pairs, table.ids, table.weights, table.lens):
+        h.update(t.cpu().numpy().tobytes())
+    digest = h.hexdigest()[:16]
+
+    # end to end through the public API: this rank's trace shard from pinned
+    # host memory, count, exchange, rank, table back to the host
+    host = trace.cpu().pin_memory()
+    dev = torch.empty_like(trace)
+    comm.barrier()
+    torch.cuda.synchronize()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for _ in range(args.steps):
+        dev.copy_(host, non_blocking=True)
+        _, t = one_pass(dev)
+        ids_h = t.ids.to("cpu", non_blocking=True)
+        w_h = t.weights.to("cpu", non_blocking=True)
+    e2.record()
+    torch.cuda.synchronize()
+    e2e_ms = _allmax(s2.elapsed_time(e2), comm)
+    del ids_h, w_h
+
     bytes_k = (b - a) * k * 4
     peak, peak_kind = _peaks()
     ach = bytes_k / (k_ms / 1e3) / 1e9
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
+        import oracle as O
         sample = trace[: 1 << 20].cpu().numpy()
         t0 = time.perf_counter()
         O.coact_count(sample, None, E, 0, 256, 0.0)
@@ -380,22 +484,37 @@ def run_profile_bench(args, ws, rank, local):
         cpu = {"value": sample.shape[0] / dt, "unit": "tokens/s", "cores": 1, "kind": "port",
                "sample": "1,048,576 tokens of the same trace through the numpy oracle's bincount restatement of "
                          "observe (bit-exact), 1 process"}
-    line = {"metric": "co-activation profiling throughput (64M-token trace, E=128, k=8)", "value": N * args.steps / (ms / 1e3),
-            "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64 counters, f64 ranking",
+    launches = (2 if wend else 1) + 2 + 1  # K6 (warm-up range + main), two counts_to_f64, K7
+    line = {"metric": "co-activation profiling throughput (64M-token trace, E=128, k=8)",
+            "value": N * args.steps / (ms / 1e3), "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32/u64 counters, f64 ranking",
             "data": "synthetic Zipf-skewed routing trace", "config": {"workload": "coact-profile-64M-E128-k8",
             "tokens": N, "experts": E, "top_k": k, "warmup_steps": 256, "alpha": 0.95, "k_max": 16,
-            "parallelism": f"token-sharded x{ws} + NCCL all-reduce", "l2": "trace (2 GB) larger than L2"},
+            "parallelism": f"token-sharded x{ws} + one all-reduce ({comm.backend or 'none'})",
+            "l2": "trace (2 GB) larger than L2"},
+            "comm": comm.info(), "result_sha16": digest,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          # DRAM bytes of the one 64M-token launch captured with ncu --set full
-                         "traffic": 2148022000 + 4829952 if N == 64 << 20 and ws == 1 else None,
-                         "traffic_source": "profiles/r1_coact_count.ncu-rep (ncu --set full; the launch reads the "
-                                           "2.147 GB trace once)",
+                         "traffic": _coact_traffic() if N == 64 << 20 and ws == 1 else None,
                          "kernel": "coact_count_kernel", "algorithmic_bytes_per_launch": bytes_k,
                          "avg_launch_ms": k_ms, "peak_kind": peak_kind},
-            "cpu_baseline": cpu, "e2e": None, "gpu_launches": 5 * args.steps, "clocks": clocks}
+            "cpu_baseline": cpu,
+            "e2e": {"value": N * args.steps / (e2e_ms / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": bytes_k, "d2h_bytes_per_step": E * 16 * 12,
+                    "note": "each rank's trace shard copied from pinned host memory every step, table read back"},
+            "gpu_launches": launches * args.steps, "clocks": clocks}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _coact_traffic():
+    """DRAM bytes of the captured 64M-token K6 launch (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "coact_traffic.json")) as f:
+            return json.load(f)["dram_bytes"]
+    except (OSError, KeyError, ValueError):
+        return 2148022000 + 4829952  # profiles/r1_coact_count.ncu-rep
 
 
 def measure_h2d(wl) -> float:
@@ -439,7 +558,6 @@ def main():
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--profile-tokens", type=int, default=4096)
-    ap.add_argument("--cpu-tokens", type=int, default=2)
     ap.add_argument("--no-original", action="store_true", help="skip the without-buddy run")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", default="decode", choices=["decode", "profile"],
@@ -449,36 +567,38 @@ def main():
     ap.add_argument("--trace-tokens", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--codec", type=int, default=1, choices=[0, 1],
                     help="1: exponent-coded pinned mirrors (lossless, fewer PCIe bytes per miss); 0: raw bf16")
+    ap.add_argument("--cache-rate", type=float, default=None,
+                    help="expert-cache budget as a fraction of the experts (default: the config's)")
     args = ap.parse_args()
+    launch_or_check(args)
     ws, rank, local = _dist()
-    import torch
-    torch.cuda.set_device(local)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.impl == "reference":
-        run_reference(args, ws, rank)
-        if ws > 1:
-            torch.distributed.destroy_process_group()
+        # the reference's CPU path on the host cores: no GPU, no libbmoe; under
+        # torchrun rank 0 alone runs it and the other ranks exit without work
+        if rank == 0:
+            run_reference(args, ws)
         return
+    comm = Comm(ws, rank, local)
+    log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
+    if ws > 1:
+        log(f"process group: {comm.info()}")
+    import torch
     if args.workload == "profile":
-        run_profile_bench(args, ws, rank, local)
-        if ws > 1:
-            torch.distributed.destroy_process_group()
+        run_profile_bench(args, comm)
+        comm.close()
         return
 
     from paper_2511_10054_b200 import _native as N
     from paper_2511_10054_b200 import workload as W
-    log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
-    L, share = _plan_mirrors(ws, local, args)
+    L, share, host_info = _plan_mirrors(comm, args)
     B, K, Wm = args.batch, args.steps, args.warmup
     E, k_top, d, f, rate, S = _shape(args.model)
     t0 = time.time()
     # replicas serve ONE model (same weights and tables on every rank) over disjoint token streams
     wl = W.build(args.model, layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=0, codec=args.codec,
-                 share=share)
+                 share=share, cache_rate=args.cache_rate)
     log(f"built {L} layers in {time.time() - t0:.1f}s (mean buddies {wl.mean_buddies:.2f}, "
-        f"mirror {'node-shared' if share else 'private'})")
+        f"mirror: {host_info['host_mirror']})")
     n_steps_total = Wm + 3 * K
     x_host = torch.from_numpy(wl.tokens(2 + rank, n_steps_total * B)).pin_memory()
     x_dev = x_host.to("cuda")
@@ -531,14 +651,14 @@ def main():
     x_work = x_dev.clone()
     _timed(eng, x_work, B, Wm, 0, torch)
     eng.stats(reset=True)
-    if ws > 1:
-        torch.distributed.barrier()
+    comm.barrier()
     torch.cuda.synchronize()
-    clk = ClockSampler(local).ready()
+    clk = ClockSampler(comm.device).ready()
     ms = _timed(eng, x_work, B, K, Wm, torch)
     clocks = clk.stop()
     st = eng.stats(reset=True)
-    ms = _allmax(ms, ws)
+    ms_mine = ms
+    ms = _allmax(ms, comm)
     value = ws * K * B / (ms / 1000.0)
 
     # ---------------- kernel timing pass (roofline of the grouped FFN GEMM) ----------------
@@ -619,8 +739,7 @@ def main():
     eng.stats(reset=True)
     out_host = torch.empty_like(x_host)
     h = torch.empty(B, d, device="cuda")
-    if ws > 1:
-        torch.distributed.barrier()
+    comm.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
@@ -631,7 +750,7 @@ def main():
         out_host[j * B:(j + 1) * B].copy_(h, non_blocking=True)
     end.record()
     torch.cuda.synchronize()
-    e2e_ms = _allmax(start.elapsed_time(end), ws)
+    e2e_ms = _allmax(start.elapsed_time(end), comm)
     e2e = ws * K * B / (e2e_ms / 1000.0)
     st_e = eng.stats(reset=True)
     eng.close()
@@ -643,9 +762,8 @@ def main():
         x2 = x_dev.clone()
         _timed(eo, x2, B, Wm, 0, torch)
         eo.stats(reset=True)
-        if ws > 1:
-            torch.distributed.barrier()
-        ms_o = _allmax(_timed(eo, x2, B, K, Wm, torch), ws)
+        comm.barrier()
+        ms_o = _allmax(_timed(eo, x2, B, K, Wm, torch), comm)
         so = eo.stats(reset=True)
         eo.close()
         # fidelity of the buddy arm (the paper's accuracy axis; harness.fidelity,
@@ -666,25 +784,39 @@ def main():
                 "physical_fetches_per_step": so["physical_fetches"] / K,
                 "h2d_gb_per_step": so["h2d_bytes"] / K / 1e9, "wire_gb_per_step": so["wire_bytes"] / K / 1e9}
 
+    # per-replica step time and fetch stall (replicas share the host's PCIe root / memory)
+    mine = {"rank": rank, "device": comm.device, "ms_per_step": ms_mine / K, "stall_ms_per_step": st["stall_ms"] / K,
+            "physical_fetches_per_step": st["physical_fetches"] / K, "numa_node": host_info["gpu_numa_node"]}
+    per_rank = [mine]
+    if ws > 1:
+        import torch.distributed as dist
+        per_rank = [None] * ws
+        dist.all_gather_object(per_rank, mine)
+    from oracle.decode_cpu import tables_digest  # a digest only: the GPU arm's tables vs the CPU arm's
+    digest = tables_digest(wl.tbl_ids.cpu().numpy(), wl.tbl_len.cpu().numpy())
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        stacks = stage_layer_f64(wl, 0)
-        times = [cpu_reference_sample(wl, 0, min(args.cpu_tokens, B), 5000 + i, stacks) for i in range(2)]
-        del stacks
-        per_layer = min(times)
-        nb = min(args.cpu_tokens, B)
-        cpu = {"value": nb / (per_layer * L), "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)),
-               "kind": "port", "sample": f"{nb} tokens x 1 layer-step (route, gates, remap, f64 forward, "
-                                         f"layer_update) via the numpy oracle, best of 2, extrapolated x{L} layers"}
+        # bounded sample of the reference arm's measurement: the same CPU decode
+        # (oracle/decode_cpu.py) for 1 warm-up + 2 timed steps through the first
+        # Lc layers, the timed per-layer mean scaled to L layers
+        from threadpoolctl import threadpool_limits
+        Lc = min(L, 2)
+        with threadpool_limits(limits=1, user_api="blas"):
+            per_step, cd = cpu_decode(args, L, 3, 1, layers_run=Lc)
+        cd.close()
+        sec = float(np.mean(per_step)) * L / Lc
+        cpu = {"value": B / sec, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)), "kind": "port",
+               "sample": f"{B} tokens x first {Lc} of {L} layers x 2 timed steps (after 1 warm-up) of the "
+                         f"--impl reference measurement (oracle/decode_cpu.py, f64, all host threads), "
+                         f"per-layer mean x {L} layers"}
 
     line = {
         "metric": _metric(B),
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": Wm,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init bf16 weights, reference-style clustered router/token stream)",
-        "config": dict(_config(args.model, wl, L, B, "buddy"),
-                       host_mirror="node-shared /dev/shm" if share else "private pinned",
-                       fetch_codec="exponent-coded bf16" if args.codec else "raw bf16"),
+        "config": _config(args.model, L, B, "buddy", wl.eng.capacity, wl.eng.search_rank_h, wl.extra["cache_rate"]),
+        "tables_sha16": digest,
         "stall_ms_per_step": st["stall_ms"] / K,
         "sim_stall_model": {"ondemand_misses_per_step": st["ondemand_misses"] / K,
                             "substitutions_per_step": st["substitutions"] / K},
@@ -709,14 +841,17 @@ def main():
                 "note": "fresh engine, same warm-up and the same K batches as `value`; pinned host in/out per step"},
         "gpu_launches": int(st["kernel_launches"]),
         "clocks": clocks,
+        "comm": comm.info(),
+        "host": host_info,
+        "per_rank": per_rank,
         "setup_s": time.time() - t0,
         "settle_sweeps_gbs": sweep_gbs,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    comm.barrier()  # every rank is done with the node-shared mirrors before any unmaps them
     wl.close()
-    if ws > 1:
-        torch.distributed.destroy_process_group()
+    comm.close()
 
 
 if __name__ == "__main__":

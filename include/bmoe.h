@@ -390,6 +390,13 @@ int bm_engine_trace_get(const bm_engine *e, int32_t *layer_host, int32_t *B_host
 /* Bytes of device memory held by the engine (arena + workspaces). */
 int64_t bm_engine_device_bytes(const bm_engine *e);
 
+/* ------------------------------------------------ synthetic weights (bench inputs)
+ * out[i] = lut[(mix64(base + i/4) >> 16*(i%4)) & 0xFFFF], mix64 = the splitmix64
+ * finaliser (z += 0x9E3779B97F4A7C15; two xor-shift-multiply rounds). lut: 65,536
+ * bf16 values in device memory (16-byte aligned), out: n bf16. Integer-only, so
+ * the numpy twin (synth.py) reproduces the bits on the host. */
+int bm_synth_bf16(const uint16_t *lut, uint64_t base, int64_t n, uint16_t *out, bm_stream_t stream);
+
 /* ------------------------------------------------ fetch codec (expert transfer)
  * Lossless exponent coding of bf16 expert buffers for the H2D fetch (no
  * reference counterpart: the reference's transfer is an analytic cost,

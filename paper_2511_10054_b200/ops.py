@@ -329,6 +329,18 @@ def buddy_rank(pair_matrix64, eps: float, alpha: float, k_max: int) -> DeviceTab
     return t
 
 
+def synth_bf16(lut, base: int, out) -> torch.Tensor:
+    """Fill the bf16 tensor ``out`` with synthetic weights (bm_synth_bf16):
+    lut = 65,536 bf16 quantiles (device, int16 or bfloat16 view), base = the
+    matrix key of synth.matrix_key."""
+    _cuda(lut, "lut")
+    _cuda(out, "out", torch.bfloat16)
+    if lut.numel() != 65536:
+        raise InputError("synth lut must hold 65536 entries")
+    N.call("bm_synth_bf16", _p(lut), int(base), out.numel(), _p(out), _s())
+    return out
+
+
 def sm_count() -> int:
     return int(N.lib().bm_device_sm_count())
 

@@ -22,36 +22,14 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import ops, substrate
+from . import ops, substrate, synth
 from .engine import DecodeEngine, EngineSpec, HostMirror, SharedMirror, coded_mirror_from_device, fill_mirror_from_device
 
-SHAPES = {
-    # name: (E, k, d, f, cache_rate)
-    "mixtral": (8, 2, 4096, 14336, 0.5),
-    "qwen3": (128, 8, 2048, 768, 0.25),
-    "dsv2lite": (64, 6, 2048, 1408, 0.5),
-    "tiny": (8, 2, 128, 256, 0.5),
-}
-SHARED = {"dsv2lite": 2}  # always-resident shared experts (outside the cache budget)
+SHAPES, SHARED = synth.SHAPES, synth.SHARED
+initial_residents = synth.initial_residents  # seeded-permutation prefix (memtier.py:132-140)
 
 
-def initial_residents(num_experts: int, capacity: int, seed: int, layer: int):
-    """Seeded-permutation prefix, nested across capacities (memtier.py:132-140)."""
-    if capacity <= 0:
-        return []
-    rng = np.random.default_rng(np.random.SeedSequence([seed, 21, layer]))
-    return sorted(int(v) for v in rng.permutation(num_experts)[:capacity])
-
-
-def host_mem_available() -> int:
-    try:
-        with open("/proc/meminfo") as f:
-            for line in f:
-                if line.startswith("MemAvailable:"):
-                    return int(line.split()[1]) * 1024
-    except OSError:
-        pass
-    return 64 << 30
+host_mem_available = synth.host_mem_available
 
 
 @dataclass
@@ -113,24 +91,49 @@ class Workload:
             m.close()
 
 
-def _gen_expert(gen, d, f, device):
-    """One SwiGLU expert [W1 | W3 | W2] bf16, N(0, 1/fan_in)."""
-    out = torch.empty(3 * d * f, device=device, dtype=torch.bfloat16)
-    out[: 2 * d * f].normal_(0.0, d ** -0.5, generator=gen)
-    out[2 * d * f:].normal_(0.0, f ** -0.5, generator=gen)
+def _synth_expert(luts, seed: int, layer: int, expert: int, d: int, f: int, out: torch.Tensor) -> torch.Tensor:
+    """One SwiGLU expert [W1 [f,d] | W3 [f,d] | W2 [d,f]] bf16, row-major, from
+    the counter-based generator (synth.py; the CPU reference arm regenerates
+    the same bits on the host)."""
+    n = d * f
+    for m in (synth.W1, synth.W3, synth.W2):
+        ops.synth_bf16(luts[m], synth.matrix_key(seed, layer, expert, m), out[m * n:(m + 1) * n])
     return out
+
+
+def profile_tables(x: torch.Tensor, gate_w, gate_b, k: int, E: int, alpha: float, k_max: int, tau_percentile: float,
+                   warm: int = 256):
+    """Buddy table + tau of one layer from the profile tokens ``x`` routed by
+    that layer's gate: K1 -> K6 (warm-up weight 0, config.py:80) -> K7, and
+    the nearest-rank tau over the TAE samples (calibrate_tau, gating.py:111-123)."""
+    r = ops.gate_topk(x, gate_w, gate_b, k)
+    warm = min(warm, x.shape[0])
+    wc, wp = ops.coact_count(r.topk[:warm], E)
+    mc, mp = ops.coact_count(r.topk[warm:], E)
+    t = ops.buddy_rank(ops.counts_to_f64(mp, wp, 0.0), 1e-3, alpha, k_max)
+    s, _ = torch.sort(r.tae)
+    idx = max(1, math.ceil(tau_percentile * s.numel() / 100.0)) - 1
+    return r, t, float(s[min(idx, s.numel() - 1)])
 
 
 def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: int = 0,
           profile_tokens: int = 4096, alpha: float = 0.95, k_max: int | None = None, tau_percentile: float = 15.0,
           clusters: int | None = None, n_tile: int = 128, device: str = "cuda", rho: int | None = 3,
-          codec: int = 1, share: ShareSpec | None = None, log=None) -> Workload:
+          codec: int = 1, share: ShareSpec | None = None, log=None, cache_rate: float | None = None,
+          profile: str = "route") -> Workload:
     """codec 1 keeps the pinned mirrors exponent-coded (bm_xfer_*: ~0.70 of
     the bf16 bytes cross PCIe per miss, rebuilt bit-exactly in HBM); 0 raw.
-    share: one node-shared mirror per layer for all local replicas (every
-    rank still generates the weights on its GPU to profile its tables)."""
+    share: one node-shared mirror per layer for all local replicas (only the
+    writing rank generates the weights).
+    profile: "route" builds every layer's buddy table and tau from the same
+    profile tokens routed by that layer's gate (so the CPU reference arm of
+    bench.py builds bit-identical tables in seconds); "forward" also pushes the
+    stream through the experts between layers (full residency), like the
+    reference's cmd_profile (harness.py:93-101)."""
     import time
     E, k, d, f, rate = SHAPES[name]
+    if cache_rate is not None:
+        rate = float(cache_rate)
     S = SHARED.get(name, 0)
     cap = int(math.floor(rate * E))
     k_max = k_max if k_max is not None else min(16, E - 1)
@@ -143,22 +146,26 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     buf_bytes = buf_elems * 2
     t0 = time.time()
     mirrors = []
-    gen = torch.Generator(device=device)
+    if profile not in ("route", "forward"):
+        raise ValueError(f"profile must be 'route' or 'forward', got {profile!r}")
+    luts = [torch.from_numpy(synth.lut_bf16(synth.matrix_scale(d, f, m)).view(np.int16)).to(device)
+            for m in (synth.W1, synth.W3, synth.W2)]
+    row = torch.empty(buf_elems, device=device, dtype=torch.bfloat16)
+    writer = share is None or share.owner
     arena = torch.empty(E + S, buf_elems, device=device, dtype=torch.bfloat16)
     ids_all = torch.full((layers, E, k_max), -1, device=device, dtype=torch.int32)
     len_all = torch.zeros(layers, E, device=device, dtype=torch.int32)
     taus = []
     x = torch.from_numpy(substrate.token_stream(spec, 1, profile_tokens).astype(np.float32)).to(device)
-    warm = min(256, profile_tokens)
     ws = None
     mean_len = []
     for l in range(layers):
-        gen.manual_seed(seed * 100003 + l)
-        for e in range(E + S):  # row-major N(0, 1/fan_in), then the UMMA-tiled HBM layout
-            w = _gen_expert(gen, d, f, device)
-            ops.pack_expert_bf16(w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d), w[2 * f * d:].view(d, f),
-                                 ops.ACT_SWIGLU, arena[e])
-        if share is not None and not share.owner:
+        if writer or profile == "forward":
+            for e in range(E + S):  # row-major N(0, 1/fan_in) (synth.py), then the UMMA-tiled HBM layout
+                w = _synth_expert(luts, seed, l, e, d, f, row)
+                ops.pack_expert_bf16(w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d),
+                                     w[2 * f * d:].view(d, f), ops.ACT_SWIGLU, arena[e])
+        if not writer:
             m = None  # attached after the owner has written every layer
         else:
             make = HostMirror if share is None else (lambda n, _l=l: SharedMirror(share.path(_l), n, create=True))
@@ -168,17 +175,16 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
                 m = make((E + S) * buf_bytes)
                 fill_mirror_from_device(m, arena)
         mirrors.append(m)
-        # ---- profile this layer (full residency) ----
-        r = ops.gate_topk(x, gate_w[l], gate_b[l], k)
-        wc, wp = ops.coact_count(r.topk[:warm], E)
-        mc, mp = ops.coact_count(r.topk[warm:], E)
-        pairs = ops.counts_to_f64(mp, wp, 0.0)           # profile.warmup_weight = 0 (config.py:80)
-        t = ops.buddy_rank(pairs, 1e-3, alpha, k_max)
+        # ---- profile this layer ----
+        r, t, tau = profile_tables(x, gate_w[l], gate_b[l], k, E, alpha, k_max, tau_percentile)
         ids_all[l], len_all[l] = t.ids, t.lens
         mean_len.append(float(t.lens.float().mean()))
-        s, _ = torch.sort(r.tae)                          # calibrate_tau, nearest rank (gating.py:111-123)
-        idx = max(1, math.ceil(tau_percentile * s.numel() / 100.0)) - 1
-        taus.append(float(s[min(idx, s.numel() - 1)]))
+        taus.append(tau)
+        if log:
+            log(f"layer {l}: mirror {(m.nbytes if m else 0) / 2**30:.2f} GiB, tau {taus[-1]:.4f}, "
+                f"mean buddies {mean_len[-1]:.2f}, {time.time() - t0:.1f}s")
+        if profile == "route":
+            continue
         kept = torch.zeros_like(r.topk, dtype=torch.uint8)  # identity plan: full residency
         ex, kd, pr = r.topk, kept, r.probs
         if S:
@@ -190,11 +196,8 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
         yp = ops.expert_ffn_bf16(xp, perm, arena, torch.arange(E + S, device=device, dtype=torch.int32), d, f,
                                  ops.ACT_SWIGLU, ws)
         x = ops.combine(yp, perm, pr, kd, h_in=x)
-        if log:
-            log(f"layer {l}: mirror {(m.nbytes if m else 0) / 2**30:.2f} GiB, tau {taus[-1]:.4f}, "
-                f"mean buddies {mean_len[-1]:.2f}, {time.time() - t0:.1f}s")
     torch.cuda.synchronize()
-    del arena, ws
+    del arena, ws, row
     if share is not None:
         share.barrier()
         if not share.owner:
@@ -208,4 +211,6 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
                     act=ops.ACT_SWIGLU, search_rank_h=k_max, rho=rho, n_tile=n_tile, expert_bytes=buf_bytes,
                     num_shared=S)
     return Workload(name, spec, es, mirrors, gate_w, gate_b, ids_all, len_all, taus, initial,
-                    profile_seconds=time.time() - t0, mean_buddies=float(np.mean(mean_len)))
+                    profile_seconds=time.time() - t0, mean_buddies=float(np.mean(mean_len)),
+                    extra={"cache_rate": rate, "profile": profile, "seed": seed, "alpha": alpha,
+                           "tau_percentile": tau_percentile, "profile_tokens": profile_tokens})

@@ -60,15 +60,18 @@ def _bf16_mirrors(L, E, d, f, seed):
     return mirrors
 
 
-@pytest.mark.parametrize("policy", ["lfu", "lru"])
-def test_speculative_fetch_evicted_unused_keeps_weights_intact(cuda_ok, policy):
+@pytest.mark.parametrize("policy,B,steps", [("lfu", 1, 96), ("lru", 8, 24)])
+def test_speculative_fetch_evicted_unused_keeps_weights_intact(cuda_ok, policy, B, steps):
     """method=original executes every routed expert exactly, so its outputs do
     not depend on the cache at all: a small LFU/LRU cache with prefetch on and
     25 MB experts (copies long enough to be in flight when their expert is
     evicted unused) must give the outputs of a cache that holds every expert.
     A buffer reused while its speculative copy still lands would corrupt an
-    expert (relative error ~1, far above the 1e-3 allowed for the different
-    grouping of the FFN launches)."""
+    expert (relative error ~1, far above the 1e-2 allowed for the different
+    grouping of the FFN launches: bf16 intermediates, measured <= 1.1e-3).
+    LFU at B=1 makes the predictor fire: an expert executed early in a step is
+    evicted by a later miss of the same step, gets prefetched, lands with
+    frequency 0 and is the next victim, possibly before its copy finished."""
     spec = substrate.ModelSpec(num_layers=3, experts_per_layer=8, top_k=2, hidden_dim=1024, ffn_dim=4096,
                                num_clusters=8)
     L, E, k, d, f = 3, 8, 2, 1024, 4096
@@ -76,27 +79,30 @@ def test_speculative_fetch_evicted_unused_keeps_weights_intact(cuda_ok, policy):
     gw, gb = substrate.gate_weights(spec)
     gwt = torch.tensor(gw, dtype=torch.float32, device="cuda")
     gbt = torch.tensor(gb, dtype=torch.float32, device="cuda")
-    x0 = torch.from_numpy(substrate.token_stream(spec, 4, 8 * 24).astype(np.float32)).cuda()
+    x0 = torch.from_numpy(substrate.token_stream(spec, 4, B * steps).astype(np.float32)).cuda()
     outs, rel = {}, None
-    for cap in (2, E):
-        es = EngineSpec(num_layers=L, num_experts=E, top_k=k, d=d, f=f, capacity=cap, max_batch=8,
+    for cap in (4 if B == 1 else 2, E):
+        es = EngineSpec(num_layers=L, num_experts=E, top_k=k, d=d, f=f, capacity=cap, max_batch=B,
                         method="original", policy=policy, prefetch=True, expert_bytes=3 * d * f * 2,
                         load_ms=9.5, hit_ms=0.0, compute_ms=0.5, pcie_bw_bytes_per_s=4.0e9)
         eng = DecodeEngine(es, mirrors, gwt, gbt, None, None, [-1.0] * L,
                            [list(range(cap))] * L)
         x = x0.clone()
-        for s in range(24):
-            eng.step(x[s * 8:(s + 1) * 8], np.arange(s * 8, (s + 1) * 8))
+        for s in range(steps):
+            eng.step(x[s * B:(s + 1) * B], np.arange(s * B, (s + 1) * B))
         torch.cuda.synchronize()
         st = eng.stats()
         eng.close()
         outs[cap] = (x.double().cpu().numpy(), st)
-    a, b = outs[2][0], outs[E][0]
+    small = min(outs)
+    a, b = outs[small][0], outs[E][0]
     rel = np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)
-    st = outs[2][1]
+    st = outs[small][1]
     print(f"{policy}: physical fetches {st['physical_fetches']}, prefetch copies {st['prefetch_copies']}, "
           f"in-flight releases {st['inflight_releases']}, max rel {rel.max():.2e}")
     assert st["physical_fetches"] > 0
-    assert rel.max() <= 1e-3, rel.max()
+    if policy == "lfu":
+        assert st["prefetch_copies"] > 0
+    assert rel.max() <= 1e-2, rel.max()
     for m in mirrors:
         m.close()
