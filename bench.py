@@ -312,16 +312,17 @@ def _plan_mirrors(comm: "Comm", args):
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_decode(args, L: int, steps: int, timed_from: int, layers_run: int | None = None, log=None):
+def cpu_decode(args, L: int, steps: int, timed_from: int, layers_run: int | None = None, log=None, tables=None):
     """The reference's decode step on the host cores (oracle/decode_cpu.py):
-    f64, the GPU arm's exact inputs (synthetic weights regenerated on the host
-    bit for bit, the same gate/token streams, tables built from the same
-    profile stream), layer-major with every (step, layer) timed. No GPU, no
-    libbmoe. Returns (per-step seconds of the timed steps, CpuDecode)."""
+    f64, the GPU arm's inputs (synthetic weights regenerated on the host bit
+    for bit, the same gate/token streams; buddy tables built by the same
+    profile recipe in f64, or the GPU arm's passed in), layer-major with every
+    (step, layer) timed. No GPU, no libbmoe. Returns (per-step seconds of the
+    timed steps, CpuDecode)."""
     from oracle.decode_cpu import CpuDecode
     n_total = (args.warmup + 3 * args.steps) * args.batch  # the GPU arm's token stream length
     cd = CpuDecode(args.model, L, args.batch, profile_tokens=args.profile_tokens, cache_rate=args.cache_rate,
-                   stream_tokens=n_total)
+                   stream_tokens=n_total, tables=tables)
     per_step, _ = cd.run(steps, timed_from, layers_run=layers_run, log=log)
     return per_step, cd
 
@@ -353,7 +354,7 @@ def run_reference(args, ws):
                                        f"oracle, layer-major, each (step, layer) timed; {cores} threads"},
             "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "tables_sha16": cd.digest, "timed_s": float(np.sum(per_step)),
-            "untimed_s": {"weights_f64": cd.gen_s, "profile_tables": cd.profile_s},
+            "untimed_s": {"weights_f64": cd.gen_s, "profile_tables_f64_forward": cd.profile_s},
             "wall_s": time.time() - t0}
     cd.close()
     print(json.dumps(line), flush=True)
@@ -796,19 +797,21 @@ def main():
     digest = tables_digest(wl.tbl_ids.cpu().numpy(), wl.tbl_len.cpu().numpy())
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        # bounded sample of the reference arm's measurement: the same CPU decode
-        # (oracle/decode_cpu.py) for 1 warm-up + 2 timed steps through the first
-        # Lc layers, the timed per-layer mean scaled to L layers
+        # the --impl reference measurement on this run's own tables: the same CPU
+        # decode (oracle/decode_cpu.py, f64, all host threads) of the same W + K
+        # batches through all L layers, the K timed steps' mean
         from threadpoolctl import threadpool_limits
-        Lc = min(L, 2)
+        t_cpu = time.time()
         with threadpool_limits(limits=1, user_api="blas"):
-            per_step, cd = cpu_decode(args, L, 3, 1, layers_run=Lc)
+            per_step, cd = cpu_decode(args, L, Wm + K, Wm, tables=(wl.tbl_ids.cpu().numpy(),
+                                                                  wl.tbl_len.cpu().numpy(), wl.taus))
         cd.close()
-        sec = float(np.mean(per_step)) * L / Lc
+        sec = float(np.mean(per_step))
         cpu = {"value": B / sec, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)), "kind": "port",
-               "sample": f"{B} tokens x first {Lc} of {L} layers x 2 timed steps (after 1 warm-up) of the "
-                         f"--impl reference measurement (oracle/decode_cpu.py, f64, all host threads), "
-                         f"per-layer mean x {L} layers"}
+               "ms_per_step": sec * 1e3, "wall_s": time.time() - t_cpu,
+               "sample": f"the --impl reference measurement on this run's tables: {Wm} warm-up + {K} timed steps of "
+                         f"{B} tokens through all {L} layers (oracle/decode_cpu.py, f64, layer-major, each "
+                         f"(step, layer) timed)"}
 
     line = {
         "metric": _metric(B),

@@ -387,6 +387,16 @@ int bm_engine_trace_size(const bm_engine *e, int64_t *records_host, int64_t *tok
 int bm_engine_trace_get(const bm_engine *e, int32_t *layer_host, int32_t *B_host, uint32_t *bitmaps_host,
                         uint8_t *batch_ok_host, int32_t *topk_host, uint8_t *allowed_host, int32_t *executed_host,
                         uint8_t *kind_host);
+/* Gate-record fields of the trace (harness.py:345-350): per token f64 TAE and
+ * margin (K1), per record the distribution-gate delta (K2). */
+int bm_engine_trace_gates(const bm_engine *e, double *tae_host, double *margin_host, double *delta_host);
+/* Psi ordering of the buddy candidates inside the engine's remap
+ * (substitution.py:107-143; sub.eta / sub.kappa / sub.use_local_logit,
+ * topology.partitions / topology.hop): tbl_w [L][E][K] f64 device table
+ * weights, partition_of [E] int32 device (NULL: no topology). The z-scores
+ * use K1's fp32 logits. eta = kappa = 0 restores the stored order. */
+int bm_engine_set_psi(bm_engine *e, const double *tbl_w, double eta, double kappa, int32_t use_local_logit,
+                      const int32_t *partition_of, double hop);
 /* Bytes of device memory held by the engine (arena + workspaces). */
 int64_t bm_engine_device_bytes(const bm_engine *e);
 

@@ -11,7 +11,9 @@ the reference, on the same synthetic inputs as the GPU arm:
   * expert weights from the counter-based generator (oracle/c/synth_host.c,
     bit-identical to the GPU arm's bm_synth_bf16), widened to float64;
   * buddy tables and tau built here from the profile stream (K1/K6/K7/tau
-    semantics: route -> observe -> build_table -> calibrate_tau).
+    semantics: route -> observe -> build_table -> calibrate_tau), with the
+    stream pushed through each layer's experts in f64 like cmd_profile
+    (harness.py:93-101), or the GPU arm's tables passed in.
 
 Per (step, layer): route_batch (model.py:231-280) -> evaluate_gates
 (gating.py:148-165) -> substitute_batch (substitution.py:193-208) -> cache
@@ -63,7 +65,13 @@ class CpuDecode:
 
     def __init__(self, model: str, layers: int, batch: int, profile_tokens: int = 4096, alpha: float = 0.95,
                  tau_percentile: float = 15.0, rho: int = 3, seed: int = 0, threads: int | None = None,
-                 cache_rate: float | None = None, stream_seed: int = 2, stream_tokens: int | None = None):
+                 cache_rate: float | None = None, stream_seed: int = 2, stream_tokens: int | None = None,
+                 profile: str = "forward", tables=None):
+        """profile: how the buddy tables and tau are built when ``tables`` is not
+        given, as workload.build does on the GPU: "forward" pushes the profile
+        stream through every layer's experts (full residency, f64 here),
+        "route" routes the same profile tokens at every layer. tables: (ids
+        [L,E,K], lens [L,E], taus [L]) to reuse instead (e.g. the GPU arm's)."""
         from paper_2511_10054_b200 import substrate, synth
         E, k, d, f, rate = synth.SHAPES[model]
         self.rate = float(cache_rate) if cache_rate is not None else rate
@@ -71,6 +79,7 @@ class CpuDecode:
         self.cap = int(math.floor(self.rate * E))
         self.k_max = min(16, E - 1)
         self.L, self.B, self.rho, self.seed = layers, batch, rho, seed
+        self.alpha, self.tau_percentile = alpha, tau_percentile
         self.threads = threads or len(os.sched_getaffinity(0))
         spec = substrate.ModelSpec(num_layers=layers, experts_per_layer=E, top_k=k, hidden_dim=d, ffn_dim=f,
                                    num_clusters=min(E, 8), seed=7)
@@ -79,22 +88,42 @@ class CpuDecode:
         # the GPU arm routes fp32-rounded gates and tokens
         self.gw = gw.astype(np.float32).astype(np.float64)
         self.gb = gb.astype(np.float32).astype(np.float64)
-        t0 = time.perf_counter()
-        xp = substrate.token_stream(spec, 1, profile_tokens).astype(np.float32).astype(np.float64)
-        warm = min(256, profile_tokens)
-        self.ids, self.lens, self.taus = [], [], []
-        for l in range(layers):  # route-only profile (workload.build(profile="route"))
-            _, topk, probs = O.route(xp, self.gw[l], self.gb[l], k)
-            _, pairs, _, _ = O.coact_count(topk, None, E, 0, warm, 0.0)
-            ids, _, lens = O.build_table(pairs, 1e-3, alpha, self.k_max)
-            self.ids.append(ids)
-            self.lens.append(lens)
-            self.taus.append(_tau(probs, tau_percentile))
-        self.profile_s = time.perf_counter() - t0
-        self.digest = tables_digest(self.ids, self.lens)
         self.synth = synth
         self.stream_seed, self.stream_tokens = stream_seed, stream_tokens
         self.pool = ThreadPoolExecutor(max_workers=self.threads)
+        self.profile = profile
+        self.profile_s = 0.0
+        self.gen_s = 0.0
+        if tables is not None:
+            ids, lens, taus = tables
+            self.ids = [np.asarray(ids[l], np.int32) for l in range(layers)]
+            self.lens = [np.asarray(lens[l], np.int32) for l in range(layers)]
+            self.taus = [float(t) for t in taus]
+        else:
+            self.ids, self.lens, self.taus = [None] * layers, [None] * layers, [None] * layers
+            self.xp = substrate.token_stream(spec, 1, profile_tokens).astype(np.float32).astype(np.float64)
+            if profile == "route":
+                for l in range(layers):
+                    self._profile_layer(l, None)
+
+    @property
+    def digest(self) -> str:
+        return tables_digest(self.ids, self.lens)
+
+    def _profile_layer(self, l: int, experts):
+        """Table + tau of layer l from the profile stream (K1 -> K6 with warm-up
+        weight 0 -> K7, nearest-rank tau); "forward" then pushes the stream
+        through the layer's experts with every slot kept (identity plans)."""
+        t0 = time.perf_counter()
+        warm = min(256, self.xp.shape[0])
+        _, topk, probs = O.route(self.xp, self.gw[l], self.gb[l], self.k)
+        _, pairs, _, _ = O.coact_count(topk, None, self.E, 0, warm, 0.0)
+        ids, _, lens = O.build_table(pairs, 1e-3, self.alpha, self.k_max)
+        self.ids[l], self.lens[l], self.taus[l] = ids, lens, _tau(probs, self.tau_percentile)
+        if self.profile == "forward":
+            kd = np.zeros(topk.shape, np.uint8)
+            self.xp = O.layer_update(self.xp, self._combine(self.xp, topk, kd, probs, experts))
+        self.profile_s += time.perf_counter() - t0
 
     def tokens(self, n: int) -> np.ndarray:
         from paper_2511_10054_b200 import substrate
@@ -163,24 +192,30 @@ class CpuDecode:
                 O.access(res, int(ex[b, s]), clock, 9.5, 0.0, 0, False, int(tokens[b]))
                 nslots += 1
         clock.now += 0.5 * nslots
-        groups = {}
-        for e in np.unique(ex[kd != O.KIND_DROPPED]):
-            rows = np.flatnonzero(np.any((ex == e) & (kd != O.KIND_DROPPED), axis=1))
+        return O.layer_update(h, self._combine(h, ex, kd, probs, experts))
+
+    def _combine(self, h, ex, kd, probs, experts):
+        """forward_batch combine (model.py:318-340): each executed expert's rows as
+        one GEMM over the host threads, slots added in slot order with the
+        original probabilities, dropped slots 0; shared experts weight 1."""
+        E, k = self.E, ex.shape[1]
+        live = kd != O.KIND_DROPPED
+        groups, rows_of = {}, {}
+        for e in np.unique(ex[live]):
+            rows = np.flatnonzero(np.any((ex == e) & live, axis=1))
+            rows_of[int(e)] = rows
             groups[int(e)] = (h[rows], experts[int(e)])
         for sx in range(self.S):
             groups[E + sx] = (h, experts[E + sx])
         ys = self._ffn_rows(groups)
         y = np.zeros_like(h)
-        for s in range(k):  # slot order, original probabilities, dropped slots contribute 0
-            for b in range(h.shape[0]):
-                if kd[b, s] == O.KIND_DROPPED:
-                    continue
+        for s in range(k):
+            for b in np.flatnonzero(live[:, s]):
                 e = int(ex[b, s])
-                rows = np.flatnonzero(np.any((ex == e) & (kd != O.KIND_DROPPED), axis=1))
-                y[b] += probs[b, s] * ys[e][int(np.searchsorted(rows, b))]
+                y[b] += probs[b, s] * ys[e][int(np.searchsorted(rows_of[e], b))]
         for sx in range(self.S):
             y += ys[E + sx]
-        return O.layer_update(h, y)
+        return y
 
     def run(self, steps: int, timed_from: int, layers_run: int | None = None, method: str = "buddy", log=None):
         """Layer-major decode of `steps` batches; returns per-step seconds of
@@ -197,6 +232,8 @@ class CpuDecode:
             t0 = time.perf_counter()
             experts = self.layer_experts(l)
             gen_s += time.perf_counter() - t0
+            if self.ids[l] is None:  # this layer's table from the profile stream (untimed)
+                self._profile_layer(l, experts)
             res = O.Residency(self.E, self.cap, O.POLICY_LRU, initial_residents(self.E, self.cap, 0, l), None, l)
             for j in range(steps):
                 t1 = time.perf_counter()

@@ -84,6 +84,8 @@ _SIGS = {
     "bm_engine_trace_size": (C.c_int, [P, P, P]),
     "bm_engine_trace_get": (C.c_int, [P, P, P, P, P, P, P, P, P]),
     "bm_engine_device_bytes": (I64, [P]),
+    "bm_engine_trace_gates": (C.c_int, [P, P, P, P]),
+    "bm_engine_set_psi": (C.c_int, [P, P, F64, F64, I32, P, F64]),
     "bm_host_alloc": (C.c_int, [I64, P]),
     "bm_host_free": (C.c_int, [P]),
     "bm_host_register": (C.c_int, [P, I64, I32]),

@@ -167,6 +167,12 @@ struct bm_engine {
     size_t ring_slot_bytes = 0;
     Ring ring_copy, ring_prefetch;
     const float *gate_w = nullptr, *gate_b = nullptr;
+    // Psi ordering of the candidates (substitution.py:107-143; bm_engine_set_psi)
+    bool psi = false;
+    const double *tbl_w = nullptr;
+    double eta = 0.0, kappa = 0.0, hop = 1.0;
+    int32_t use_local_logit = 1;
+    const int32_t *partition_of = nullptr;
     const int32_t *tbl_ids = nullptr, *tbl_len = nullptr;
     std::vector<double> tau;
     bm_cache *cache = nullptr;
@@ -223,6 +229,7 @@ struct bm_engine {
     std::vector<int32_t> tr_layer, tr_B, tr_topk, tr_exec;
     std::vector<uint8_t> tr_allowed, tr_batch_ok, tr_kind;
     std::vector<uint32_t> tr_bitmap;
+    std::vector<double> tr_tae, tr_margin, tr_delta;
 
     template <typename T>
     int dmalloc(T **p, size_t n) {
@@ -352,13 +359,16 @@ struct bm_engine {
         ENG_TRY(bm_gate_topk(h, gate_w + (size_t)l * E * d, gate_b + (size_t)l * E, B, E, d, k, cfg.temperature,
                              tau[l], cfg.gamma, logits, topk, probs, tae, margin, allowed, s));
         ENG_CUDA(cudaMemcpyAsync(bm_dev_l[l], bm_host_l[l], bm_stride * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        ENG_TRY(bm::buddy_remap_impl(topk, allowed, nullptr, 0, B, k, E, bm_dev_l[l],
-                                     tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr, nullptr,
+        const bool p = psi && cfg.method == BM_METHOD_BUDDY;
+        ENG_TRY(bm::buddy_remap_impl(topk, allowed, p ? logits : nullptr, 0, B, k, E, bm_dev_l[l],
+                                     tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr,
+                                     p ? tbl_w + (size_t)l * E * K : nullptr,
                                      tbl_len ? tbl_len + (size_t)l * E : nullptr, K > 0 ? K : 1, cfg.search_rank_h,
                                      cfg.rho, cfg.fallback,
                                      cfg.method == BM_METHOD_RANDOM ? BM_METHOD_ORIGINAL : cfg.method, cfg.beta,
-                                     reinterpret_cast<const double *>(bm_dev_l[l] + beta_word), 0.0, 0.0, 1, nullptr,
-                                     1.0, executed, kind, used, delta, batch_ok, s));
+                                     reinterpret_cast<const double *>(bm_dev_l[l] + beta_word), p ? eta : 0.0,
+                                     p ? kappa : 0.0, use_local_logit, p ? partition_of : nullptr, hop, executed, kind,
+                                     used, delta, batch_ok, s));
         ENG_CUDA(cudaMemcpyAsync(plan_host, plan_dev, plan_bytes(B, k), cudaMemcpyDeviceToHost, s));
         return BM_OK;
     }
@@ -494,6 +504,14 @@ struct bm_engine {
             tr_allowed.insert(tr_allowed.end(), allowed_h, allowed_h + B);
             tr_batch_ok.push_back(batch_ok_h[0]);
             tr_bitmap.insert(tr_bitmap.end(), bm_host_l[l], bm_host_l[l] + words);
+            // gate record fields (harness.py:345-350): K1's f64 TAE and margin, K2's delta
+            const size_t t0 = tr_tae.size();
+            tr_tae.resize(t0 + B);
+            tr_margin.resize(t0 + B);
+            tr_delta.resize(tr_delta.size() + 1);
+            ENG_CUDA(cudaMemcpy(tr_tae.data() + t0, tae, B * sizeof(double), cudaMemcpyDeviceToHost));
+            ENG_CUDA(cudaMemcpy(tr_margin.data() + t0, margin, B * sizeof(double), cudaMemcpyDeviceToHost));
+            ENG_CUDA(cudaMemcpy(&tr_delta.back(), delta, sizeof(double), cudaMemcpyDeviceToHost));
         }
         std::vector<int32_t> &cnt = prev_counts[l];  // harness.py:384-389
         std::fill(cnt.begin(), cnt.end(), 0);
@@ -919,6 +937,46 @@ extern "C" int bm_engine_set_trace(bm_engine *e, int32_t enable) {
     e->tr_allowed.clear();
     e->tr_batch_ok.clear();
     e->tr_bitmap.clear();
+    e->tr_tae.clear();
+    e->tr_margin.clear();
+    e->tr_delta.clear();
+    return BM_OK;
+}
+
+extern "C" int bm_engine_trace_gates(const bm_engine *e, double *tae_host, double *margin_host, double *delta_host) {
+    if (!e) return BM_EINVAL;
+    if (tae_host && !e->tr_tae.empty()) memcpy(tae_host, e->tr_tae.data(), e->tr_tae.size() * sizeof(double));
+    if (margin_host && !e->tr_margin.empty())
+        memcpy(margin_host, e->tr_margin.data(), e->tr_margin.size() * sizeof(double));
+    if (delta_host && !e->tr_delta.empty())
+        memcpy(delta_host, e->tr_delta.data(), e->tr_delta.size() * sizeof(double));
+    return BM_OK;
+}
+
+extern "C" int bm_engine_set_psi(bm_engine *e, const double *tbl_w, double eta, double kappa, int32_t use_local_logit,
+                                 const int32_t *partition_of, double hop) {
+    if (!e || eta < 0.0 || kappa < 0.0) {
+        bm::set_error("bm_engine_set_psi: bad arguments");
+        return BM_EINVAL;
+    }
+    const bool on = eta != 0.0 || kappa != 0.0;
+    if (on && (!tbl_w || e->cfg.method != BM_METHOD_BUDDY)) {
+        bm::set_error("bm_engine_set_psi: Psi ordering needs the buddy method and table weights");
+        return BM_ECONFIG;
+    }
+    // captured graphs hold the old remap arguments: drop them
+    for (auto *m : {&e->g_pre}) {
+        for (auto &kv : *m)
+            if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
+        m->clear();
+    }
+    e->psi = on;
+    e->tbl_w = tbl_w;
+    e->eta = eta;
+    e->kappa = kappa;
+    e->use_local_logit = use_local_logit;
+    e->partition_of = partition_of;
+    e->hop = hop;
     return BM_OK;
 }
 

@@ -281,16 +281,28 @@ class DecodeEngine:
     def device_bytes(self) -> int:
         return int(N.lib().bm_engine_device_bytes(self._h))
 
-    def events(self):
-        """The control plane's event log as an [n,7] float64 array
-        (time, kind, layer, token, expert, bytes, stall) — memtier.SimEvent."""
+    def events(self, start: int = 0):
+        """The control plane's event log from index ``start`` on, in log order, as
+        an [n,7] float64 array (time, kind, layer, token, expert, bytes, stall)."""
         c = N.lib().bm_engine_cache(self._h)
-        n = int(N.lib().bm_cache_num_events(c))
+        n = max(0, int(N.lib().bm_cache_num_events(c)) - start)
         arr = (N.Event * max(n, 1))()
         if n:
-            N.call("bm_cache_events", c, 0, n, arr)
+            N.call("bm_cache_events", c, start, n, arr)
         return np.array([(e.time_ms, e.kind, e.layer, e.token, e.expert, e.bytes, e.stall_ms) for e in arr[:n]],
                         dtype=np.float64).reshape(-1, 7)
+
+    def set_psi(self, tbl_w: torch.Tensor | None, eta: float = 0.0, kappa: float = 0.0, use_local_logit: bool = True,
+                partition_of: torch.Tensor | None = None, hop: float = 1.0):
+        """Psi candidate ordering in the remap (substitution.py:107-143): tbl_w
+        [L,E,K] f64 device weights of the buddy table, partition_of [E] int32."""
+        self._psi_keep = (tbl_w, partition_of)
+        N.call("bm_engine_set_psi", self._h, None if tbl_w is None else tbl_w.data_ptr(), float(eta), float(kappa),
+               int(bool(use_local_logit)), None if partition_of is None else partition_of.data_ptr(), float(hop))
+
+    def raw_events(self):
+        """The control plane's event log in log order (not time-sorted)."""
+        return self.events()
 
     def set_copy_timing(self, enable: bool = True):
         """Time each fetch's copies (stats()["copy_ms"]); costs ~6 us of copy engine per fetch."""
@@ -315,6 +327,10 @@ class DecodeEngine:
         kd = np.zeros(max(nt, 1) * k, np.uint8)
         N.call("bm_engine_trace_get", self._h, lay.ctypes.data, Bs.ctypes.data, bms.ctypes.data, bok.ctypes.data,
                tk.ctypes.data, al.ctypes.data, ex.ctypes.data, kd.ctypes.data)
+        tae = np.zeros(max(nt, 1))
+        mar = np.zeros(max(nt, 1))
+        dl = np.zeros(max(nr, 1))
+        N.call("bm_engine_trace_gates", self._h, tae.ctypes.data, mar.ctypes.data, dl.ctypes.data)
         out, t0 = [], 0
         for i in range(nr):
             B = int(Bs[i])
@@ -322,7 +338,8 @@ class DecodeEngine:
             mask = np.array([(bits[e >> 5] >> (e & 31)) & 1 for e in range(self.spec.num_experts)], bool)
             out.append(dict(layer=int(lay[i]), mask=mask, batch_ok=bool(bok[i]),
                             topk=tk[t0 * k:(t0 + B) * k].reshape(B, k), allowed=al[t0:t0 + B].astype(bool),
-                            executed=ex[t0 * k:(t0 + B) * k].reshape(B, k), kind=kd[t0 * k:(t0 + B) * k].reshape(B, k)))
+                            executed=ex[t0 * k:(t0 + B) * k].reshape(B, k), kind=kd[t0 * k:(t0 + B) * k].reshape(B, k),
+                            tae=tae[t0:t0 + B].copy(), margin=mar[t0:t0 + B].copy(), delta=float(dl[i])))
             t0 += B
         return out
 

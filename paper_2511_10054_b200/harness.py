@@ -6,19 +6,23 @@ CSV files), ``calibrate_taus`` (the tau step of cmd_simulate, :476-484),
 ``run_simulation`` (:221-424), ``run_oracle`` (:175-186) and ``fidelity``
 (:189-206).
 
-Only the hot-path parts of the reference harness are here (SURVEY §8 rows
-R6, R17-R22 and §8(f) rows 1-2); the CLI, config-file parsing and report
-formatting are out of scope.
-``run_simulation`` takes the reference's dotted configuration keys as a
-dict (defaults from config.py:64-111), builds the synthetic model, and
-replays the evaluation stream through ``DecodeEngine`` (fp32 parity mode with
-the reference's tanh experts), so its event log, counters and outputs are
-comparable one to one with the reference's SimResult.
+The reference's entry points keep their names and signatures: ``cmd_profile``
+/ ``cmd_build`` / ``cmd_simulate`` (artifact files as the reference writes
+them), ``run_simulation`` / ``run_oracle`` / ``fidelity`` /
+``_predict_for_layer``; ``run_profile`` / ``run_build`` are their tensor-level
+forms. A configuration is either the reference's ExperimentConfig (used
+duck-typed: ``.values``, ``.explicit``, ``validate_run()``; the config system
+itself is out of scope) or a plain dict of its dotted keys (defaults from
+config.py:64-111). ``run_simulation`` builds the synthetic model and replays
+the evaluation stream through ``DecodeEngine`` (fp32 parity mode with the
+reference's tanh experts), so its event log, counters, gate records,
+bandwidth series and outputs compare one to one with the reference's
+SimResult. The CLI and ``cmd_report`` table formatting are not here.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -28,7 +32,7 @@ import os
 from . import _native as N
 from . import buddies, gating, memtier, ops, profiler, substrate
 from .engine import DecodeEngine, EngineSpec, HostMirror
-from .errors import CalibrationError, ConfigurationError, FormatError
+from .errors import CalibrationError, ConfigurationError, FormatError, InvariantViolation
 
 DEFAULTS = {
     "model.layers": 24, "model.experts": 64, "model.top_k": 6, "model.hidden_dim": 32, "model.ffn_dim": 64,
@@ -41,13 +45,37 @@ DEFAULTS = {
     "method": "buddy", "run.seed": 0, "fidelity.readout_classes": 16,
     "stream.warmup_steps": 256, "profile.laplace_eps": 1e-3, "profile.warmup_weight": 0.0,
     "builder.alpha": "0.95", "builder.k_max": 16, "builder.mode": "binary", "gate.tau_percentile": 15.0,
+    "gate.tau": None, "sub.eta": 0.0, "sub.kappa": 0.0, "sub.diversity_factor": 0.5, "sub.use_local_logit": True,
+    "topology.partitions": 1, "topology.hop": 1.0,
+    "io.profile_dir": "out/profile", "io.build_dir": "out/build", "io.run_dir": "out/run",
 }
 
 
-def _cfg(cfg: dict) -> dict:
+def _cfg(cfg) -> dict:
+    """Dotted-key dict of a configuration: the reference's ExperimentConfig
+    (validated like its own callers do, harness.py:73,138,232) or a dict."""
     c = dict(DEFAULTS)
-    c.update(cfg or {})
+    if cfg is not None and isinstance(getattr(cfg, "values", None), dict):
+        if hasattr(cfg, "validate_run"):
+            cfg.validate_run()
+        c.update(cfg.values)
+        c["__explicit__"] = set(getattr(cfg, "explicit", ()))
+    else:
+        c.update(cfg or {})
+        c["__explicit__"] = set((cfg or {}).keys())
     return c
+
+
+def _fixed_tau(c):
+    """gate.tau when it supersedes the percentile (ExperimentConfig.gate_config, config.py:150-175)."""
+    tau, pct, ex = c["gate.tau"], c["gate.tau_percentile"], c["__explicit__"]
+    if "gate.tau" in ex and "gate.tau_percentile" in ex and tau is not None and pct is not None:
+        raise ConfigurationError("set gate.tau or gate.tau_percentile, not both")
+    if tau is not None and "gate.tau_percentile" not in ex:
+        return float(tau), None
+    if tau is None and pct is None:
+        raise ConfigurationError("one of gate.tau / gate.tau_percentile must be set")
+    return None, pct
 
 
 # file names of the reference harness (harness.py:47-65)
@@ -73,11 +101,15 @@ def tae_path(out_dir):
 
 @dataclass
 class SimResult:
+    """harness.py:163-172, plus the engine's per layer-step trace."""
     metrics: memtier.RunMetrics
     outputs: np.ndarray
     events: list
+    gate_records: list
     tau_by_layer: list
-    trace: list
+    beta_final: float
+    bandwidth_series: list  # (step, read_bytes) per outer batch step
+    trace: list = field(default_factory=list)
 
 
 def _spec(c) -> substrate.ModelSpec:
@@ -94,8 +126,10 @@ def _tanh_arena(spec, layer):
                            np.transpose(w_out, (0, 2, 1)).reshape(E, -1)], axis=1).astype(np.float32)
 
 
-def run_oracle(spec: substrate.ModelSpec, x: np.ndarray, temperature: float = 1.0, batch: int = 256) -> np.ndarray:
-    """Full-residency forward (identity plans) through K1, K3-K5 (harness.py:175-186)."""
+def run_oracle(model, x: np.ndarray, temperature: float = 1.0, batch: int = 256) -> np.ndarray:
+    """Full-residency forward (identity plans) through K1, K3-K5 (harness.py:175-186).
+    ``model``: a model.Model (as the reference passes) or its ModelSpec."""
+    spec = model.spec if hasattr(model, "spec") else model
     dev = torch.device("cuda", torch.cuda.current_device())
     gw, gb = substrate.gate_weights(spec)
     gw = torch.tensor(gw, dtype=torch.float32, device=dev)
@@ -140,19 +174,90 @@ def events_array(events) -> np.ndarray:
                     np.float64).reshape(-1, 7)
 
 
-def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=None) -> SimResult:
+def _predict_for_layer(state, prev_counts: dict) -> list:
+    """Previous-step top-m frequency predictor (harness.py:209-218), decided by
+    the C++ control plane's predictor (bm_cache_predict) that the engine uses:
+    m = capacity - distinct experts of the previous step, ranked by count
+    desc then id asc."""
+    import ctypes
+    E = state.num_experts
+    counts = np.zeros(E, np.int32)
+    for e, n in prev_counts.items():
+        counts[int(e)] = int(n)
+    preds = np.zeros(max(E, 1), np.int32)
+    n = ctypes.c_int64()
+    N.call("bm_cache_predict", state._h, 0, counts.ctypes.data, preds.ctypes.data, ctypes.byref(n))
+    return [int(v) for v in preds[:n.value]]
+
+
+def _dense_tables(tables, L, E):
+    """(ids [L,E,K] int32, lens [L,E] int32, weights [L,E,K] f64 | None) from a
+    list of buddies.BuddyTable or a dense (ids, lens[, weights]) tuple."""
+    if isinstance(tables, (list, tuple)) and len(tables) and hasattr(tables[0], "ids"):
+        K = max(1, max(len(t.ids(p)) for t in tables for p in range(E)))
+        ids = np.full((L, E, K), -1, np.int32)
+        lens = np.zeros((L, E), np.int32)
+        w = np.zeros((L, E, K), np.float64)
+        for l, t in enumerate(tables):
+            for p in range(E):
+                n = len(t.ids(p))
+                ids[l, p, :n] = t.ids(p)
+                w[l, p, :n] = t.weights(p)
+                lens[l, p] = n
+        return ids, lens, w
+    ids, lens = np.asarray(tables[0], np.int32), np.asarray(tables[1], np.int32)
+    w = np.asarray(tables[2], np.float64) if len(tables) > 2 else None
+    return ids, lens, w
+
+
+def run_simulation(cfg, tables=None, tau_by_layer=None, static_freq=None, oracle_outputs=None,
+                   collect_events: bool = True) -> SimResult:
     """The reference decode replay (harness.py:221-424) on the engine.
-    ``tables``: dense (ids[L,E,K] int32, lens[L,E] int32) or a list of
-    buddies.BuddyTable; ``tau_by_layer``: calibrated thresholds."""
-    c = dict(DEFAULTS)
-    c.update(cfg)
+    ``tables``: a list of buddies.BuddyTable (one per layer) or dense
+    (ids[L,E,K], lens[L,E][, weights[L,E,K]]); ``tau_by_layer``: calibrated
+    thresholds (ignored when gate.tau is fixed); ``static_freq``: per-layer
+    profiling frequencies for the freq_static policy."""
+    c = _cfg(cfg)
     spec = _spec(c)
     L, E = spec.num_layers, spec.experts_per_layer
     method = c["method"]
     if method not in ("buddy", "original", "random"):
         raise ConfigurationError(f"unknown method {method!r} (buddy|original|random)")
+    if not (0.0 < c["cache.rate"] <= 1.0):
+        raise ConfigurationError("cache_rate must be in (0, 1]")
+    if c["cache.policy"] not in memtier.POLICIES:
+        raise ConfigurationError(f"unknown eviction policy {c['cache.policy']!r}")
     cap = int(np.floor(c["cache.rate"] * E))
     dev = torch.device("cuda", torch.cuda.current_device())
+    ids = lens = w = None
+    taus = [-1.0] * L
+    psi = method == "buddy" and (c["sub.eta"] != 0.0 or c["sub.kappa"] != 0.0)
+    if method == "buddy":
+        if tables is None or (isinstance(tables, list) and len(tables) != L):
+            raise ConfigurationError("buddy method needs one buddy table per layer")
+        if isinstance(tables, list) and hasattr(tables[0], "ids"):
+            for t in tables:
+                if t.num_experts != E:
+                    raise ConfigurationError(f"buddy table shape {t.num_experts} does not match model {E}")
+                if c["sub.h"] > t.k_max:
+                    raise ConfigurationError("sub.h exceeds the table's k_max")
+        ids, lens, w = _dense_tables(tables, L, E)
+        if psi and w is None:
+            raise ConfigurationError("Psi ordering (sub.eta / sub.kappa) needs the table weights")
+        fixed, _ = _fixed_tau(c)
+        if fixed is not None:
+            taus = [fixed] * L
+        elif tau_by_layer is None or len(tau_by_layer) != L:
+            raise ConfigurationError("buddy method needs a calibrated tau per layer")
+        else:
+            taus = [float(t) for t in tau_by_layer]
+    sf = None
+    if c["cache.policy"] == memtier.POLICY_FREQ_STATIC:
+        if static_freq is None or len(static_freq) != L:
+            raise ConfigurationError("freq_static policy needs profiling frequencies per layer")
+        sf = np.stack([np.asarray(v, np.float64) for v in static_freq])
+    P = int(c["topology.partitions"])
+    partition_of = (np.arange(E) * P) // E if P > 1 else None
     mirrors = []
     for l in range(L):
         a = _tanh_arena(spec, l)
@@ -160,46 +265,44 @@ def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=Non
         m.as_tensor(torch.float32).copy_(torch.from_numpy(a).view(-1))
         mirrors.append(m)
     gw, gb = substrate.gate_weights(spec)
-    ids = lens = None
-    if method == "buddy":
-        if tables is None or tau_by_layer is None:
-            raise ConfigurationError("buddy method needs one buddy table and one tau per layer")
-        table_objs = isinstance(tables, (list, tuple)) and hasattr(tables[0], "ids")
-        if table_objs:
-            K = max(max([len(t.ids(p)) for t in tables for p in range(E)]), 1)
-            ids_np = np.full((L, E, K), -1, np.int32)
-            lens_np = np.zeros((L, E), np.int32)
-            for l, t in enumerate(tables):
-                for p in range(E):
-                    n = len(t.ids(p))
-                    ids_np[l, p, :n] = t.ids(p)
-                    lens_np[l, p] = n
-        else:
-            ids_np, lens_np = tables
-        ids = torch.tensor(np.asarray(ids_np, np.int32), device=dev)
-        lens = torch.tensor(np.asarray(lens_np, np.int32), device=dev)
-        if table_objs and c["sub.h"] > tables[0].k_max:
-            raise ConfigurationError("sub.h exceeds the table's k_max")
-    taus = list(tau_by_layer) if method == "buddy" else [-1.0] * L
+    ebytes = 2 * spec.hidden_dim * spec.ffn_dim * 8
     es = EngineSpec(num_layers=L, num_experts=E, top_k=spec.top_k, d=spec.hidden_dim, f=spec.ffn_dim,
                     capacity=cap, max_batch=c["stream.batch"], act=ops.ACT_TANH, method=method,
                     policy=c["cache.policy"], search_rank_h=c["sub.h"], rho=c["sub.rho"],
                     fallback=0 if c["sub.fallback"] == "prefetch_original" else 1, beta=c["gate.beta"],
                     temperature=c["gate.temperature"], gamma=c["gate.margin_gamma"], prefetch=c["prefetch.enabled"],
-                    fp32_weights=True, expert_bytes=2 * spec.hidden_dim * spec.ffn_dim * 8,
+                    fp32_weights=True, expert_bytes=ebytes,
                     load_ms=c["cost.expert_load_ms"], hit_ms=c["cost.hit_ms"], compute_ms=c["cost.expert_compute_ms"],
                     pcie_bw_bytes_per_s=c["cost.pcie_bw_bytes_per_s"],
                     pcie_budget_bytes=c["gate.pcie_budget_bytes"] if method == "buddy" else None,
                     run_seed=c["run.seed"])
-    initial = [memtier.initial_residents(E, cap, c["cache.policy"], c["run.seed"], l) for l in range(L)]
+    initial = [memtier.initial_residents(E, cap, c["cache.policy"], c["run.seed"], l,
+                                         None if sf is None else sf[l]) for l in range(L)]
     eng = DecodeEngine(es, mirrors, torch.tensor(gw, dtype=torch.float32, device=dev),
-                       torch.tensor(gb, dtype=torch.float32, device=dev), ids, lens, taus, initial)
+                       torch.tensor(gb, dtype=torch.float32, device=dev),
+                       None if ids is None else torch.tensor(ids, device=dev),
+                       None if lens is None else torch.tensor(lens, device=dev), taus, initial, sf)
+    if psi:
+        eng.set_psi(torch.tensor(w, device=dev), c["sub.eta"], c["sub.kappa"], c["sub.use_local_logit"],
+                    None if partition_of is None else torch.tensor(partition_of, dtype=torch.int32, device=dev),
+                    c["topology.hop"])
     eng.set_trace(True)
     n, B = c["stream.num_tokens"], c["stream.batch"]
     x = substrate.token_stream(spec, c["stream.seed"], n)
     h = torch.tensor(x, dtype=torch.float32, device=dev)
-    for b0 in range(0, n, B):
+    bandwidth, n_seen = [], 0
+    for step, b0 in enumerate(range(0, n, B)):
         eng.step(h[b0:b0 + B], np.arange(b0, min(n, b0 + B)))
+        # step bytes as the reference counts them (harness.py:327-329, 374-378): prefetch
+        # completions and on-demand misses of routed slots (a substituted slot's stand-in
+        # that misses is not counted), from this step's slice of the control-plane log
+        ev = eng.events(n_seen)
+        n_seen += len(ev)
+        kinds = ev[:, 1].astype(np.int64)
+        after_sub = np.zeros(len(ev), bool)
+        after_sub[1:] = kinds[:-1] == 2
+        counted = (kinds == 4) | ((kinds == 1) & ~after_sub)
+        bandwidth.append((step, int(ev[counted, 5].sum())))
     torch.cuda.synchronize()
     eng.finish()
     events = memtier.events_from_array(eng.sorted_events())
@@ -215,16 +318,28 @@ def run_simulation(cfg: dict, tables=None, tau_by_layer=None, oracle_outputs=Non
     m.substitutions = st["substitutions"]
     m.gate_token_forbidden = st["gate_forbidden"]
     m.gate_batch_bypassed = st["batch_bypassed"]
+    if m.read_bytes != ebytes * (m.misses_ondemand + m.prefetch_completed):
+        raise InvariantViolation("transfer byte conservation failed")
     outputs = h.double().cpu().numpy()
     if oracle_outputs is None:
         oracle_outputs = run_oracle(spec, x, c["gate.temperature"], batch=B)
     m.fidelity_cosine, m.fidelity_argmax = fidelity(outputs, oracle_outputs,
                                                     substrate.readout_head(spec, c["fidelity.readout_classes"]))
     trace = eng.trace()
+    gate_records = []
+    if method == "buddy":  # (step, layer, token, tae, margin, delta, token_allowed, batch_allowed), harness.py:345-350
+        for i, r in enumerate(trace):
+            b0 = (i // L) * B
+            for j in range(r["topk"].shape[0]):
+                gate_records.append((i // L, r["layer"], b0 + j, float(r["tae"][j]), float(r["margin"][j]),
+                                     r["delta"], bool(r["allowed"][j]), bool(r["batch_ok"])))
+    beta_final = st["beta"] if (method == "buddy" and c["gate.pcie_budget_bytes"] is not None) else c["gate.beta"]
     eng.close()
     for mm in mirrors:
         mm.close()
-    return SimResult(metrics=m, outputs=outputs, events=events, tau_by_layer=taus, trace=trace)
+    return SimResult(metrics=m, outputs=outputs, events=events if collect_events else [], gate_records=gate_records,
+                     tau_by_layer=list(taus) if method == "buddy" else [], beta_final=beta_final,
+                     bandwidth_series=bandwidth, trace=trace)
 
 
 # ------------------------------------------------------------------ profile
@@ -356,3 +471,119 @@ def run_build(cfg: dict, stats=None, profile_dir: str | None = None, out_dir: st
             buddies.save_table(t, table_path(out_dir, l))
             buddies.export_table_csv(t, table_csv_path(out_dir, l))
     return tables
+
+
+# ------------------------------------------------------------ file-level commands
+def cmd_profile(cfg, out_dir: str) -> dict:
+    """harness.cmd_profile (harness.py:70-117): run_profile writing
+    stats_LXX.bin, coact_LXX.csv and tae_samples.txt; returns the paths."""
+    return run_profile(cfg, out_dir).paths
+
+
+def cmd_build(cfg, out_dir: str) -> dict:
+    """harness.cmd_build (harness.py:135-157): one K7 table per layer from the
+    BSST files under io.profile_dir; returns the paths and the size report."""
+    c = _cfg(cfg)
+    tables = run_build(c, profile_dir=c["io.profile_dir"], out_dir=out_dir)
+    L = c["model.layers"]
+    paths = {"tables": [table_path(out_dir, l) for l in range(L)],
+             "csv": [table_csv_path(out_dir, l) for l in range(L)]}
+    paths["report"] = "\n".join(f"layer {l}: {buddies.table_size_report(t).format().splitlines()[0]}"
+                                for l, t in enumerate(tables))
+    return paths
+
+
+def _echo(c) -> list:
+    """The configuration echo of a metrics file (harness.py:427-440)."""
+    rho = c["sub.rho"]
+    return [("method", c["method"]), ("cache_rate", repr(c["cache.rate"])), ("cache_policy", c["cache.policy"]),
+            ("alpha", str(c["builder.alpha"])), ("k_max", str(c["builder.k_max"])),
+            ("rho", "unlimited" if rho is None else str(rho)), ("run_seed", str(c["run.seed"])),
+            ("stream_seed", str(c["stream.seed"])), ("num_tokens", str(c["stream.num_tokens"])),
+            ("batch", str(c["stream.batch"]))]
+
+
+def write_metrics(metrics, cfg, path) -> None:
+    """metrics.csv: "metric,value" then RunMetrics rows and the config echo."""
+    rows = metrics.as_rows() + _echo(_cfg(cfg))
+    with open(path, "w") as fh:
+        fh.write("metric,value\n" + "".join(f"{k},{v}\n" for k, v in rows))
+
+
+def read_metrics(path) -> dict:
+    with open(path) as fh:
+        lines = fh.read().splitlines()
+    if not lines or lines[0].strip() != "metric,value":
+        raise FormatError(f"{path}: not a metrics file")
+    out = dict(line.strip().partition(",")[::2] for line in lines[1:])
+    if out.get("format") != "bsim/1":
+        raise FormatError(f"{path}: bad or missing format version")
+    return out
+
+
+def cmd_simulate(cfg, out_dir: str):
+    """harness.cmd_simulate (harness.py:462-512): tables from io.build_dir, tau
+    from io.profile_dir's entropy samples (unless gate.tau is fixed),
+    freq_static frequencies from the profiled counts, run_simulation on the
+    engine, then metrics.csv, events.log, bandwidth.csv (and gates.log)."""
+    c = _cfg(cfg)
+    L, method, pdir = c["model.layers"], c["method"], c["io.profile_dir"]
+    tables = taus = static = None
+    if method == "buddy":
+        tables = [buddies.load_table(table_path(c["io.build_dir"], l)) for l in range(L)]
+        fixed, pct = _fixed_tau(c)
+        if fixed is None:
+            taus = calibrate_taus(load_tae_samples(tae_path(pdir)), pct) if L else []
+    if c["cache.policy"] == memtier.POLICY_FREQ_STATIC:
+        static = [profiler.load_stats(stats_path(pdir, l)).counts for l in range(L)]
+    r = run_simulation(cfg, tables=tables, tau_by_layer=taus, static_freq=static)
+    os.makedirs(out_dir, exist_ok=True)
+    paths = {k: os.path.join(out_dir, v) for k, v in
+             (("metrics", "metrics.csv"), ("events", "events.log"), ("bandwidth", "bandwidth.csv"))}
+    write_metrics(r.metrics, cfg, paths["metrics"])
+    memtier.save_events(r.events, paths["events"])
+    with open(paths["bandwidth"], "w") as fh:
+        fh.write("step,read_bytes\n" + "".join(f"{s},{b}\n" for s, b in r.bandwidth_series))
+    if method == "buddy":
+        paths["gates"] = os.path.join(out_dir, "gates.log")
+        with open(paths["gates"], "w") as fh:
+            fh.write("bsim/1\n")
+            fh.writelines(f"{st} {ly} {tk} {h!r} {mg!r} {dl!r} {int(ok)} {int(bok)}\n"
+                          for st, ly, tk, h, mg, dl, ok, bok in r.gate_records)
+    return r.metrics, paths
+
+
+_REPORT_COLUMNS = ("method", "cache_rate", "alpha", "k_max", "rho", "fidelity_cosine", "fidelity_argmax",
+                   "tokens_per_s", "read_bytes")
+_REPORT_FLOATS = {"fidelity_cosine", "fidelity_argmax", "tokens_per_s", "cache_rate"}
+
+
+def cmd_report(metrics_paths, out_dir: str | None = None) -> str:
+    """Comparison table of metrics files (harness.py:522-559): one aligned row
+    per file (floats to 4 decimals), optionally report.csv with the raw values."""
+    if not metrics_paths:
+        raise ConfigurationError("report needs at least one metrics file")
+    raw = []
+    for p in metrics_paths:
+        m = read_metrics(p)
+        missing = [col for col in _REPORT_COLUMNS if col not in m]
+        if missing:
+            raise FormatError(f"{p}: missing metrics {missing}")
+        raw.append([m[col] for col in _REPORT_COLUMNS])
+
+    def cell(v, col):
+        if col not in _REPORT_FLOATS:
+            return v
+        try:
+            return f"{float(v):.4f}"
+        except ValueError:
+            return v
+
+    grid = [list(_REPORT_COLUMNS)] + [[cell(v, col) for v, col in zip(r, _REPORT_COLUMNS)] for r in raw]
+    width = [max(len(row[i]) for row in grid) for i in range(len(_REPORT_COLUMNS))]
+    table = "\n".join("  ".join(v.ljust(w) for v, w in zip(row, width)).rstrip() for row in grid)
+    if out_dir is not None:
+        os.makedirs(out_dir, exist_ok=True)
+        with open(os.path.join(out_dir, "report.csv"), "w") as fh:
+            fh.write("\n".join(",".join(r) for r in [list(_REPORT_COLUMNS)] + raw) + "\n")
+    return table

@@ -70,6 +70,8 @@ class Model:
         self.spec = spec
         E, C = spec.experts_per_layer, spec.num_clusters
         self.cluster_of = (np.arange(E) * C) // E
+        self.cluster_dirs = substrate.cluster_dirs(spec)
+        self.cluster_dirs.setflags(write=False)
         gw, gb = substrate.gate_weights(spec)
         gw.setflags(write=False)
         gb.setflags(write=False)

@@ -84,11 +84,16 @@ def cluster_popularity(spec: ModelSpec):
     return cluster_order, expert_rank
 
 
+def cluster_dirs(spec: ModelSpec) -> np.ndarray:
+    """Unit cluster directions [C, d] shared across depth (model.py:131-134)."""
+    return _unit_rows(_rng(spec.seed, _TAG_CLUSTER_DIR).standard_normal((spec.num_clusters, spec.hidden_dim)))
+
+
 def gate_weights(spec: ModelSpec):
     """Router weights gate_w[L,E,d], gate_b[L,E] (model.py:122-150)."""
     E, d, C, L = spec.experts_per_layer, spec.hidden_dim, spec.num_clusters, spec.num_layers
     cluster_of = (np.arange(E) * C) // E
-    dirs = _unit_rows(_rng(spec.seed, _TAG_CLUSTER_DIR).standard_normal((C, d)))
+    dirs = cluster_dirs(spec)
     _, rank = cluster_popularity(spec)
     bias = spec.skew * np.log(E / rank)
     gate_w = np.empty((L, E, d))

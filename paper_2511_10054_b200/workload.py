@@ -120,16 +120,16 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
           profile_tokens: int = 4096, alpha: float = 0.95, k_max: int | None = None, tau_percentile: float = 15.0,
           clusters: int | None = None, n_tile: int = 128, device: str = "cuda", rho: int | None = 3,
           codec: int = 1, share: ShareSpec | None = None, log=None, cache_rate: float | None = None,
-          profile: str = "route") -> Workload:
+          profile: str = "forward") -> Workload:
     """codec 1 keeps the pinned mirrors exponent-coded (bm_xfer_*: ~0.70 of
     the bf16 bytes cross PCIe per miss, rebuilt bit-exactly in HBM); 0 raw.
     share: one node-shared mirror per layer for all local replicas (only the
     writing rank generates the weights).
-    profile: "route" builds every layer's buddy table and tau from the same
-    profile tokens routed by that layer's gate (so the CPU reference arm of
-    bench.py builds bit-identical tables in seconds); "forward" also pushes the
-    stream through the experts between layers (full residency), like the
-    reference's cmd_profile (harness.py:93-101)."""
+    profile: "forward" (default) pushes the profile stream through every
+    layer's experts (full residency) and builds each layer's buddy table and
+    tau from the routing it sees there, like the reference's cmd_profile
+    (harness.py:93-101); "route" routes the same profile tokens at every layer
+    (no expert forward; the CPU twin then builds bit-identical tables)."""
     import time
     E, k, d, f, rate = SHAPES[name]
     if cache_rate is not None:

@@ -29,8 +29,8 @@ def test_gpu_and_cpu_arms_share_weights_and_tables(cuda_ok):
     from oracle.decode_cpu import CpuDecode, tables_digest
     from paper_2511_10054_b200 import workload as W
     from paper_2511_10054_b200.engine import mirror_expert
-    wl = W.build("qwen3", layers=2, max_batch=16, profile_tokens=1024)
-    cd = CpuDecode("qwen3", 2, 16, profile_tokens=1024)
+    wl = W.build("qwen3", layers=2, max_batch=16, profile_tokens=1024, profile="route")
+    cd = CpuDecode("qwen3", 2, 16, profile_tokens=1024, profile="route")
     try:
         gpu = tables_digest(wl.tbl_ids.cpu().numpy(), wl.tbl_len.cpu().numpy())
         assert gpu == cd.digest
