@@ -158,6 +158,12 @@ int bm_gather_rows(const float *x, int64_t B, int64_t d, const int32_t *row_toke
  * (model.py:343-347), else out = y. Fixed slot order: deterministic. */
 int bm_combine(const float *y_perm, const int32_t *slot_row, const float *probs, const uint8_t *kind, int64_t B,
                int64_t k, int64_t d, const float *h_in, float residual_scale, float *out, bm_stream_t stream);
+/* The same K3 gather / K5 combine + layer_update in float64 (the reference's
+ * precision; model.forward_batch / layer_update of the Python API). */
+int bm_gather_rows_f64(const double *x, int64_t B, int64_t d, const int32_t *row_token, const int32_t *expert_offset,
+                       int64_t E, int64_t r_max, double *x_perm, bm_stream_t stream);
+int bm_combine_f64(const double *y_perm, const int32_t *slot_row, const double *probs, const uint8_t *kind, int64_t B,
+                   int64_t k, int64_t d, const double *h_in, double residual_scale, double *out, bm_stream_t stream);
 
 /* ------------------------------------------------- K4 grouped expert FFN
  * Expert weights live in an "arena" of equally sized buffers; buffer b holds
@@ -171,6 +177,10 @@ int bm_expert_ffn_f32(const float *x_perm, const int32_t *expert_count, const in
                       int64_t d, int64_t f, int32_t act, const float *w_arena, int64_t buf_elems,
                       const int32_t *buf_of_expert, int64_t r_max, float *h_ws, float *y_perm,
                       bm_stream_t stream);
+/* float64 SIMT tiles of the same grouped FFN (reference precision). */
+int bm_expert_ffn_f64(const double *x_perm, const int32_t *expert_count, const int32_t *expert_offset, int64_t E,
+                      int64_t d, int64_t f, int32_t act, const double *w_arena, int64_t buf_elems,
+                      const int32_t *buf_of_expert, int64_t r_max, double *h_ws, double *y_perm, bm_stream_t stream);
 
 /* bf16 tensor-core mode: persistent stream-K tcgen05/TMEM/TMA GEMMs with
  * weights as the M=128 operand ("swap-AB": decode token counts are the N

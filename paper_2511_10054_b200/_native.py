@@ -112,6 +112,9 @@ _SIGS = {
     "bm_gather_rows": (C.c_int, [P, I64, I64, P, P, I64, I64, I32, P, P]),
     "bm_combine": (C.c_int, [P, P, P, P, I64, I64, I64, P, F32, P, P]),
     "bm_expert_ffn_f32": (C.c_int, [P, P, P, I64, I64, I64, I32, P, I64, P, I64, P, P, P]),
+    "bm_expert_ffn_f64": (C.c_int, [P, P, P, I64, I64, I64, I32, P, I64, P, I64, P, P, P]),
+    "bm_gather_rows_f64": (C.c_int, [P, I64, I64, P, P, I64, I64, P, P]),
+    "bm_combine_f64": (C.c_int, [P, P, P, P, I64, I64, I64, P, F64, P, P]),
     "bm_pack_expert_bf16": (C.c_int, [P, P, P, I64, I64, I32, P, P]),
     "bm_expert_ffn_bf16_workspace": (I64, [I64, I64, I64, I64, I64]),
     "bm_expert_ffn_bf16": (C.c_int, [P, P, P, I64, I64, I64, I32, P, I64, P, I64, I64, P, I64, P, P]),

@@ -132,26 +132,51 @@ __global__ void gather_sw128_kernel(const float *__restrict__ x, int d, const in
 constexpr int kCombineThreads = 256;
 
 constexpr int kCombineMaxSlots = 64;
-constexpr int kCombineUnroll = 8;
+constexpr int kCombineUnroll = 2;     // vectors per thread and slot in flight together
 constexpr int kCombineSlotGroup = 4;  // slots whose loads are in flight together
 
+template <typename T, int VEC>
+struct alignas(sizeof(T) * VEC) VecT {
+    T v[VEC];
+};
+
+// read-only-path load of a 4/8/16-byte vector
+template <typename V>
+__device__ __forceinline__ V ldg_vec(const V *p) {
+    V out;
+    if constexpr (sizeof(V) == 16) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4 *>(p));
+        memcpy(&out, &u, 16);
+    } else if constexpr (sizeof(V) == 8) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2 *>(p));
+        memcpy(&out, &u, 8);
+    } else {
+        const unsigned u = __ldg(reinterpret_cast<const unsigned *>(p));
+        memcpy(&out, &u, 4);
+    }
+    return out;
+}
+
 // One CTA per token. The token's active slots (not dropped, with a row) are
-// staged in shared memory first; each thread then owns columns
-// i = tid + u*blockDim.x and issues the loads of 8 columns per slot at once
-// (the former one-column-at-a-time loop was latency-bound at ~25 us). The
-// arithmetic is unchanged: y = fma(p_s, y_s, y) over slots in order, and
-// each thread accumulates its sum of squares over its columns in ascending
-// order, so results are bitwise the same.
-__global__ void __launch_bounds__(kCombineThreads) combine_kernel(const float *__restrict__ y_perm,
+// staged in shared memory first; each thread then owns VEC consecutive
+// columns per vector (16-byte loads of y_perm and h: float4 / double2) and
+// issues the loads of kCombineUnroll vectors of kCombineSlotGroup slots
+// before their in-order fma chain: y = fma(p_s, y_s, y) over slots in slot
+// order per column (model.py:334-340), then h + 0.5 y and the RMS
+// normalisation of layer_update (model.py:343-347) in the same pass.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kCombineThreads) combine_kernel(const T *__restrict__ y_perm,
                                                                   const int32_t *__restrict__ slot_row,
-                                                                  const float *__restrict__ probs,
+                                                                  const T *__restrict__ probs,
                                                                   const uint8_t *__restrict__ kind, int k, int d,
-                                                                  const float *h_in, float scale,
-                                                                  float *out) {  // out may alias h_in
-    extern __shared__ __align__(16) float hbuf[];
-    __shared__ float red[kCombineThreads / 32];
+                                                                  const T *h_in, T scale,
+                                                                  T *out) {  // out may alias h_in
+    using V = VecT<T, VEC>;
+    extern __shared__ __align__(16) uint8_t hraw[];
+    T *hbuf = reinterpret_cast<T *>(hraw);
+    __shared__ T red[kCombineThreads / 32];
     __shared__ int srow[kCombineMaxSlots];
-    __shared__ float sw[kCombineMaxSlots];
+    __shared__ T sw[kCombineMaxSlots];
     __shared__ int nsl;
     const int b = blockIdx.x;
     if (threadIdx.x == 0) {
@@ -167,47 +192,52 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const float *_
     }
     __syncthreads();
     const int ns = nsl;
-    float ssq = 0.f;
-    for (int i0 = threadIdx.x; i0 < d; i0 += kCombineUnroll * blockDim.x) {
-        float y[kCombineUnroll], hv[kCombineUnroll];
+    T ssq = 0;
+    const int step = (int)blockDim.x * VEC;
+    for (int i0 = (int)threadIdx.x * VEC; i0 < d; i0 += kCombineUnroll * step) {
+        V y[kCombineUnroll], hv[kCombineUnroll];
 #pragma unroll
         for (int u = 0; u < kCombineUnroll; ++u) {
-            const int i = i0 + u * (int)blockDim.x;
-            y[u] = 0.f;
-            hv[u] = (h_in && i < d) ? h_in[(size_t)b * d + i] : 0.f;  // in flight with the slot loads
+            const int i = i0 + u * step;
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) y[u].v[c] = hv[u].v[c] = 0;
+            if (h_in && i < d) hv[u] = *reinterpret_cast<const V *>(h_in + (size_t)b * d + i);
         }
-        // slots in groups of kCombineSlotGroup: all their loads are issued
-        // before the (unchanged, in-order) fma chain consumes them
         for (int s0 = 0; s0 < ns; s0 += kCombineSlotGroup) {
-            float a[kCombineSlotGroup][kCombineUnroll];
+            V a[kCombineSlotGroup][kCombineUnroll];
 #pragma unroll
             for (int g = 0; g < kCombineSlotGroup; ++g) {
                 if (s0 + g >= ns) break;
-                const float *src = y_perm + (size_t)srow[s0 + g] * d;
+                const T *src = y_perm + (size_t)srow[s0 + g] * d;
 #pragma unroll
                 for (int u = 0; u < kCombineUnroll; ++u) {
-                    const int i = i0 + u * (int)blockDim.x;
-                    a[g][u] = i < d ? __ldg(src + i) : 0.f;
+                    const int i = i0 + u * step;
+                    if (i < d) a[g][u] = ldg_vec(reinterpret_cast<const V *>(src + i));
                 }
             }
 #pragma unroll
             for (int g = 0; g < kCombineSlotGroup; ++g) {
                 if (s0 + g >= ns) break;
-                const float w = sw[s0 + g];
+                const T w = sw[s0 + g];
 #pragma unroll
-                for (int u = 0; u < kCombineUnroll; ++u) y[u] = fmaf(w, a[g][u], y[u]);
+                for (int u = 0; u < kCombineUnroll; ++u)
+#pragma unroll
+                    for (int c = 0; c < VEC; ++c) y[u].v[c] = fma(w, a[g][u].v[c], y[u].v[c]);
             }
         }
 #pragma unroll
         for (int u = 0; u < kCombineUnroll; ++u) {
-            const int i = i0 + u * (int)blockDim.x;
+            const int i = i0 + u * step;
             if (i >= d) continue;
             if (h_in) {
-                const float h = fmaf(scale, y[u], hv[u]);
-                hbuf[i] = h;
-                ssq = fmaf(h, h, ssq);
+#pragma unroll
+                for (int c = 0; c < VEC; ++c) {
+                    const T h = fma(scale, y[u].v[c], hv[u].v[c]);
+                    hbuf[i + c] = h;
+                    ssq = fma(h, h, ssq);
+                }
             } else {
-                out[(size_t)b * d + i] = y[u];
+                *reinterpret_cast<V *>(out + (size_t)b * d + i) = y[u];
             }
         }
     }
@@ -215,11 +245,35 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const float *_
     for (int o = 16; o > 0; o >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
     if (lane_id() == 0) red[threadIdx.x >> 5] = ssq;
     __syncthreads();
-    float tot = 0.f;
+    T tot = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
-    const float rms = sqrtf(tot / (float)d);
-    const float inv = 1.0f / fmaxf(rms, 1e-12f);
+    const T rms = sqrt(tot / (T)d);
+    const T inv = (T)1 / fmax(rms, (T)1e-12);
     for (int i = threadIdx.x; i < d; i += blockDim.x) out[(size_t)b * d + i] = hbuf[i] * inv;
+}
+
+template <typename T, int VEC>
+int launch_combine(const T *y_perm, const int32_t *slot_row, const T *probs, const uint8_t *kind, int64_t B,
+                   int64_t k, int64_t d, const T *h_in, T scale, T *out, cudaStream_t s) {
+    const size_t smem = h_in ? (size_t)d * sizeof(T) : 0;
+    BM_REQUIRE(smem <= 200 * 1024, BM_EINVAL, "bm_combine: d too large");
+    if (smem > 48 * 1024)
+        BM_CUDA_TRY(cudaFuncSetAttribute(combine_kernel<T, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+    combine_kernel<T, VEC><<<(unsigned)B, kCombineThreads, smem, s>>>(y_perm, slot_row, probs, kind, (int)k, (int)d,
+                                                                      h_in, scale, out);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
+// layout 0 in f64: row-major [r_max][d] (the reference-precision forward)
+__global__ void gather_f64_kernel(const double *__restrict__ x, int d, const int32_t *__restrict__ row_token,
+                                  const int32_t *__restrict__ expert_offset, int E, double *__restrict__ out) {
+    const int rows = expert_offset[E];
+    const int r = blockIdx.x;
+    if (r >= rows) return;
+    const int t = row_token[r];
+    for (int i = threadIdx.x; i < d; i += blockDim.x) out[(size_t)r * d + i] = t < 0 ? 0.0 : x[(size_t)t * d + i];
 }
 
 __global__ void split_counts_kernel(const int32_t *__restrict__ count, const int32_t *__restrict__ mask, int E,
@@ -316,20 +370,42 @@ extern "C" int bm_gather_rows(const float *x, int64_t B, int64_t d, const int32_
     return BM_OK;
 }
 
-extern "C" int bm_combine(const float *y_perm, const int32_t *slot_row, const float *probs, const uint8_t *kind,
-                          int64_t B, int64_t k, int64_t d, const float *h_in, float residual_scale, float *out,
-                          bm_stream_t stream) {
+template <typename T>
+static int combine_any(const T *y_perm, const int32_t *slot_row, const T *probs, const uint8_t *kind, int64_t B,
+                       int64_t k, int64_t d, const T *h_in, T residual_scale, T *out, bm_stream_t stream) {
     BM_REQUIRE(B >= 0 && k >= 1 && d >= 1, BM_EINVAL, "bm_combine: bad args");
     BM_REQUIRE(k <= kCombineMaxSlots, BM_EINVAL, "bm_combine: k=%lld slots exceeds %d", (long long)k,
                kCombineMaxSlots);
     if (B == 0) return BM_OK;
     BM_REQUIRE(y_perm && slot_row && probs && kind && out, BM_EINVAL, "bm_combine: null pointer");
-    size_t smem = h_in ? (size_t)d * sizeof(float) : 0;
-    BM_REQUIRE(smem <= 200 * 1024, BM_EINVAL, "bm_combine: d too large");
-    if (smem > 48 * 1024)
-        BM_CUDA_TRY(cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    combine_kernel<<<(unsigned)B, kCombineThreads, smem, as_stream(stream)>>>(y_perm, slot_row, probs, kind, (int)k,
-                                                                            (int)d, h_in, residual_scale, out);
+    constexpr int VEC = 16 / sizeof(T);
+    const bool vec = d % VEC == 0 && ((reinterpret_cast<uintptr_t>(y_perm) | reinterpret_cast<uintptr_t>(out) |
+                                       reinterpret_cast<uintptr_t>(h_in)) & 15) == 0;
+    cudaStream_t s = as_stream(stream);
+    return vec ? launch_combine<T, VEC>(y_perm, slot_row, probs, kind, B, k, d, h_in, residual_scale, out, s)
+               : launch_combine<T, 1>(y_perm, slot_row, probs, kind, B, k, d, h_in, residual_scale, out, s);
+}
+
+extern "C" int bm_combine(const float *y_perm, const int32_t *slot_row, const float *probs, const uint8_t *kind,
+                          int64_t B, int64_t k, int64_t d, const float *h_in, float residual_scale, float *out,
+                          bm_stream_t stream) {
+    return combine_any<float>(y_perm, slot_row, probs, kind, B, k, d, h_in, residual_scale, out, stream);
+}
+
+extern "C" int bm_combine_f64(const double *y_perm, const int32_t *slot_row, const double *probs,
+                              const uint8_t *kind, int64_t B, int64_t k, int64_t d, const double *h_in,
+                              double residual_scale, double *out, bm_stream_t stream) {
+    return combine_any<double>(y_perm, slot_row, probs, kind, B, k, d, h_in, residual_scale, out, stream);
+}
+
+extern "C" int bm_gather_rows_f64(const double *x, int64_t B, int64_t d, const int32_t *row_token,
+                                  const int32_t *expert_offset, int64_t E, int64_t r_max, double *x_perm,
+                                  bm_stream_t stream) {
+    BM_REQUIRE(d >= 1 && r_max >= 0 && B >= 0, BM_EINVAL, "bm_gather_rows_f64: bad args");
+    if (r_max == 0 || B == 0) return BM_OK;
+    BM_REQUIRE(x && row_token && expert_offset && x_perm, BM_EINVAL, "bm_gather_rows_f64: null pointer");
+    gather_f64_kernel<<<(unsigned)r_max, 256, 0, as_stream(stream)>>>(x, (int)d, row_token, expert_offset, (int)E,
+                                                                      x_perm);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }

@@ -2,9 +2,11 @@
 (model.py:1-382) with routing, forward and layer_update on the GPU.
 
 ``route_batch`` runs K1 (fused fp32 gate + top-k); ``forward_batch`` runs
-K3 permute -> K4 fp32 grouped FFN (the reference's tanh expert, parity
-mode) -> K5 combine; ``layer_update`` is K5's epilogue. Inputs/outputs stay
-numpy float64 like the reference; the arithmetic is the CUDA path.
+K3 permute -> K4 grouped FFN (the reference's tanh expert) -> K5 combine;
+``layer_update`` is K5's epilogue. Inputs/outputs stay numpy float64 like the
+reference, and so does the arithmetic of this API's forward: the f64 SIMT
+variants of K4/K5 (the engine's fp32 parity path and bf16 tensor-core path
+are the throughput forms of the same kernels).
 """
 
 from __future__ import annotations
@@ -41,13 +43,14 @@ class Expert:
 
     def __call__(self, x: np.ndarray) -> np.ndarray:
         # single-expert convenience: route through the grouped FFN with one slot
+        one_d = np.asarray(x).ndim == 1
         x = np.atleast_2d(np.asarray(x, dtype=np.float64))
         B = x.shape[0]
         E, d, f = 1, self.w_in.shape[0], self.w_in.shape[1]
         arena = np.concatenate([self.w_in.T.reshape(1, -1), self.w_out.T.reshape(1, -1)], axis=1)
         y = _grouped_forward(x, np.zeros((B, 1), np.int64), np.zeros((B, 1), np.uint8), np.ones((B, 1)),
-                             torch.tensor(arena, dtype=torch.float32, device=_dev()), E, d, f)
-        return y if np.asarray(x).ndim > 1 else y[0]
+                             torch.tensor(arena, dtype=torch.float64, device=_dev()), E, d, f)
+        return y if one_d is False else y[0]
 
 
 @dataclass(frozen=True)
@@ -114,13 +117,13 @@ class Model:
         return self._dev_gate[0][layer], self._dev_gate[1][layer]
 
     def device_arena(self, layer: int):
-        """fp32 TANH arena [E, f*d + d*f]: [Win^T | Wout^T] per expert."""
+        """f64 TANH arena [E, f*d + d*f]: [Win^T | Wout^T] per expert."""
         if layer not in self._dev_arena:
             w_in, w_out = self.layer_stack(layer)
             E = w_in.shape[0]
             arena = np.concatenate([np.transpose(w_in, (0, 2, 1)).reshape(E, -1),
                                     np.transpose(w_out, (0, 2, 1)).reshape(E, -1)], axis=1)
-            self._dev_arena[layer] = torch.tensor(arena, dtype=torch.float32, device=_dev())
+            self._dev_arena[layer] = torch.tensor(arena, dtype=torch.float64, device=_dev())
         return self._dev_arena[layer]
 
 
@@ -184,8 +187,8 @@ def _grouped_forward(x, ids, kinds, weights, arena, E, d, f, h_in=False):
     dev = arena.device
     ex = torch.tensor(ids, dtype=torch.int32, device=dev)
     kd = torch.tensor(kinds, dtype=torch.uint8, device=dev)
-    pr = torch.tensor(weights, dtype=torch.float32, device=dev)
-    xd = torch.tensor(x, dtype=torch.float32, device=dev)
+    pr = torch.tensor(weights, dtype=torch.float64, device=dev)
+    xd = torch.tensor(x, dtype=torch.float64, device=dev)
     perm = ops.permute(ex, kd, E)
     xp = ops.gather_rows(xd, perm, 0)
     yp = ops.expert_ffn_f32(xp, perm, arena, torch.arange(E, dtype=torch.int32, device=dev), d, f, ops.ACT_TANH)
@@ -194,7 +197,7 @@ def _grouped_forward(x, ids, kinds, weights, arena, E, d, f, h_in=False):
 
 
 def forward_batch(model: Model, x: np.ndarray, decisions, plans=None) -> np.ndarray:
-    """K3 -> K4 (fp32 SIMT, tanh) -> K5 over one layer (model.py:318-340):
+    """K3 -> K4 (f64 SIMT, tanh) -> K5 over one layer (model.py:318-340):
     weights are the ORIGINAL p~, dropped slots contribute 0, no renormalisation."""
     x = np.atleast_2d(np.asarray(x, dtype=np.float64))
     n = x.shape[0]
@@ -227,9 +230,9 @@ def layer_update(h: np.ndarray, y: np.ndarray) -> np.ndarray:
     y = np.atleast_2d(np.asarray(y, dtype=np.float64))
     dev = _dev()
     B, d = h.shape
-    yd = torch.tensor(y, dtype=torch.float32, device=dev)
-    hd = torch.tensor(h, dtype=torch.float32, device=dev)
+    yd = torch.tensor(y, dtype=torch.float64, device=dev)
+    hd = torch.tensor(h, dtype=torch.float64, device=dev)
     perm = ops.Permutation(None, None, None, torch.arange(B, dtype=torch.int32, device=dev), B)
-    out = ops.combine(yd, perm, torch.ones(B, 1, device=dev), torch.zeros(B, 1, dtype=torch.uint8, device=dev),
-                      h_in=hd, residual_scale=_RESIDUAL_SCALE)
+    out = ops.combine(yd, perm, torch.ones(B, 1, dtype=torch.float64, device=dev),
+                      torch.zeros(B, 1, dtype=torch.uint8, device=dev), h_in=hd, residual_scale=_RESIDUAL_SCALE)
     return out.double().cpu().numpy()

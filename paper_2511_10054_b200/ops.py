@@ -194,10 +194,16 @@ def append_shared(executed, kind, probs, num_experts: int, num_shared: int):
 
 
 def gather_rows(x, perm: Permutation, layout: int = 0):
-    """Permuted activations: layout 0 fp32 [r_max,d]; layout 1 bf16 SW128 planes."""
-    _cuda(x, "x", torch.float32)
+    """Permuted activations: layout 0 row-major [r_max,d] in x's dtype (fp32, or
+    f64 for the reference-precision path); layout 1 bf16 SW128 planes."""
     B, d = x.shape
     E = perm.count.shape[0]
+    if layout == 0 and x.dtype == torch.float64:
+        _cuda(x, "x", torch.float64)
+        out = torch.empty(perm.r_max, d, device=x.device, dtype=torch.float64)
+        N.call("bm_gather_rows_f64", _p(x), B, d, _p(perm.row_token), _p(perm.offset), E, perm.r_max, _p(out), _s())
+        return out
+    _cuda(x, "x", torch.float32)
     if layout == 0:
         out = torch.empty(perm.r_max, d, device=x.device, dtype=torch.float32)
     else:
@@ -207,26 +213,33 @@ def gather_rows(x, perm: Permutation, layout: int = 0):
 
 
 def combine(y_perm, perm: Permutation, probs, kind, h_in=None, residual_scale: float = 0.5, out=None):
-    """K5: gate-weighted combine (+ layer_update when h_in is given)."""
+    """K5: gate-weighted combine (+ layer_update when h_in is given); fp32, or
+    f64 when y_perm is float64 (then probs / h_in / out are float64 too)."""
     B, k = probs.shape
     d = y_perm.shape[-1]
+    f64 = y_perm.dtype == torch.float64
+    dt = torch.float64 if f64 else torch.float32
+    for t, nm in ((y_perm, "y_perm"), (probs, "probs")) + (((h_in, "h_in"),) if h_in is not None else ()):
+        _cuda(t, nm, dt)
     if out is None:
-        out = torch.empty(B, d, device=y_perm.device, dtype=torch.float32)
-    N.call("bm_combine", _p(y_perm), _p(perm.slot_row), _p(probs), _p(kind), B, k, d, _p(h_in),
-           float(residual_scale), _p(out), _s())
+        out = torch.empty(B, d, device=y_perm.device, dtype=dt)
+    N.call("bm_combine_f64" if f64 else "bm_combine", _p(y_perm), _p(perm.slot_row), _p(probs), _p(kind), B, k, d,
+           _p(h_in), float(residual_scale), _p(out), _s())
     return out
 
 
 def expert_ffn_f32(x_perm, perm: Permutation, w_arena, buf_of_expert, d: int, f: int, act: int):
-    """fp32 SIMT parity-mode grouped FFN over an arena of expert buffers."""
+    """SIMT grouped FFN over an arena of expert buffers: fp32 (parity mode), or
+    f64 (the reference's precision) when x_perm and w_arena are float64."""
     E = perm.count.shape[0]
-    _cuda(x_perm, "x_perm", torch.float32)
-    _cuda(w_arena, "w_arena", torch.float32)
-    h = torch.empty(perm.r_max, f, device=x_perm.device, dtype=torch.float32)
-    y = torch.empty(perm.r_max, d, device=x_perm.device, dtype=torch.float32)
+    dt = torch.float64 if x_perm.dtype == torch.float64 else torch.float32
+    _cuda(x_perm, "x_perm", dt)
+    _cuda(w_arena, "w_arena", dt)
+    h = torch.empty(perm.r_max, f, device=x_perm.device, dtype=dt)
+    y = torch.empty(perm.r_max, d, device=x_perm.device, dtype=dt)
     buf_elems = w_arena.shape[1] if w_arena.dim() == 2 else w_arena[0].numel()
-    N.call("bm_expert_ffn_f32", _p(x_perm), _p(perm.count), _p(perm.offset), E, d, f, act, _p(w_arena),
-           buf_elems, _p(buf_of_expert), perm.r_max, _p(h), _p(y), _s())
+    N.call("bm_expert_ffn_f64" if dt == torch.float64 else "bm_expert_ffn_f32", _p(x_perm), _p(perm.count),
+           _p(perm.offset), E, d, f, act, _p(w_arena), buf_elems, _p(buf_of_expert), perm.r_max, _p(h), _p(y), _s())
     return y
 
 

@@ -53,42 +53,78 @@ class CoActivationStats:
         self._pw = torch.zeros(E, E, dtype=torch.float64, device=dev)
         # float matrices given explicitly (load_stats / merge of foreign stats)
         self._f64 = None
+        self._host = None
         if counts is not None or pair_counts is not None or pair_weights is not None:
-            self._f64 = (np.zeros(E) if counts is None else np.asarray(counts, np.float64),
-                         np.zeros((E, E)) if pair_counts is None else np.asarray(pair_counts, np.float64))
-            if pair_weights is not None:
-                self._pw = torch.tensor(np.asarray(pair_weights, np.float64), device=dev)
+            self._f64 = (np.zeros(E) if counts is None else np.array(counts, np.float64),
+                         np.zeros((E, E)) if pair_counts is None else np.array(pair_counts, np.float64),
+                         np.zeros((E, E)) if pair_weights is None else np.array(pair_weights, np.float64))
+            self._pw = torch.tensor(self._f64[2], device=dev)
 
     def config_tuple(self) -> tuple:
         return (self.layer, self.num_experts, self.warmup_steps, self.warmup_weight, self.laplace_eps)
 
     # reference-visible float64 views ------------------------------------
+    # The reference's stats are plain numpy arrays that callers may edit in
+    # place (tests poke ties into pair_counts). The views below are therefore
+    # materialised once into host arrays that stay writable; the next device
+    # operation folds them back: unchanged views are dropped (the integer
+    # counters stay authoritative), edited ones become the stats' float state.
+    def _views(self):
+        if self._f64 is not None:
+            return self._f64
+        if self._host is None:
+            c = ops.counts_to_f64(self._c, self._wc, self.warmup_weight).cpu().numpy()
+            p = ops.counts_to_f64(self._p, self._wp, self.warmup_weight).cpu().numpy()
+            w = self._pw.cpu().numpy()
+            self._host = ((c, p, w), (c.copy(), p.copy(), w.copy()))
+        return self._host[0]
+
+    def _sync(self):
+        if self._host is None:
+            return
+        views, snap = self._host
+        self._host = None
+        if all(np.array_equal(v, s0) for v, s0 in zip(views, snap)):
+            return
+        self._f64 = views
+        self._pw = torch.tensor(views[2], device=_dev())
+
     @property
     def counts(self) -> np.ndarray:
-        if self._f64 is not None:
-            return self._f64[0]
-        return ops.counts_to_f64(self._c, self._wc, self.warmup_weight).cpu().numpy()
+        return self._views()[0]
+
+    @counts.setter
+    def counts(self, value):
+        np.copyto(self._views()[0], np.asarray(value, np.float64))
 
     @property
     def pair_counts(self) -> np.ndarray:
-        if self._f64 is not None:
-            return self._f64[1]
-        return ops.counts_to_f64(self._p, self._wp, self.warmup_weight).cpu().numpy()
+        return self._views()[1]
+
+    @pair_counts.setter
+    def pair_counts(self, value):
+        np.copyto(self._views()[1], np.asarray(value, np.float64))
 
     @property
     def pair_weights(self) -> np.ndarray:
-        return self._pw.cpu().numpy()
+        return self._views()[2]
+
+    @pair_weights.setter
+    def pair_weights(self, value):
+        np.copyto(self._views()[2], np.asarray(value, np.float64))
 
     def device_matrix(self, mode: str) -> torch.Tensor:
+        self._sync()
+        if self._f64 is not None:
+            return torch.tensor(self._f64[2] if mode == "weighted" else self._f64[1], device=_dev())
         if mode == "weighted":
             return self._pw
-        if self._f64 is not None:
-            return torch.tensor(self._f64[1], device=_dev())
         return ops.counts_to_f64(self._p, self._wp, self.warmup_weight)
 
     # accumulation ------------------------------------------------------------
     def observe_tensors(self, topk: torch.Tensor, probs: torch.Tensor | None, first_step: int) -> None:
         """K6 over rows of a batch whose global steps are first_step, first_step+1, ..."""
+        self._sync()
         if self._f64 is not None:
             raise InputError("stats loaded from floats cannot accumulate further")
         n = topk.shape[0]
@@ -167,12 +203,14 @@ def merge(a: CoActivationStats, b: CoActivationStats) -> CoActivationStats:
         raise InputError("cannot merge stats with different layer/shape/config")
     out = CoActivationStats(a.layer, a.num_experts, a.warmup_steps, a.warmup_weight, a.laplace_eps,
                             a.tokens_seen + b.tokens_seen)
+    a._sync()
+    b._sync()
     if a._f64 is None and b._f64 is None:
         for name in ("_c", "_p", "_wc", "_wp", "_pw"):
             setattr(out, name, getattr(a, name) + getattr(b, name))
     else:  # reference float semantics: a + b of the float views
-        out._f64 = (a.counts + b.counts, a.pair_counts + b.pair_counts)
-        out._pw = a._pw + b._pw
+        out._f64 = (a.counts + b.counts, a.pair_counts + b.pair_counts, a.pair_weights + b.pair_weights)
+        out._pw = torch.tensor(out._f64[2], device=_dev())
     return out
 
 

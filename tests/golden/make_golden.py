@@ -95,6 +95,33 @@ def routing_case(spec: ModelSpec, stream_seed: int, n: int, layer: int = 0, T: f
                 margin=np.array([gating.margin(d) for d in ds]))
 
 
+def routing_shape_case(E: int, k: int, d: int, n: int, n_logits: int = 1024) -> dict:
+    """route_batch at a BASELINE shape (Mixtral 8/2/4096, Qwen3 128/8/2048,
+    DSV2-Lite 64/6/2048) on the reference substrate with the bench's router
+    spec (seed 7, min(E, 8) clusters; token stream seed 2), then observe over
+    every routed token (warm-up 256, weight 0) and build_table (alpha 0.95,
+    k_max 16). The tokens are not stored: substrate.token_stream regenerates
+    them bit-identically. Logits/probs are kept for the first n_logits rows."""
+    spec = ModelSpec(num_layers=1, experts_per_layer=E, top_k=k, hidden_dim=d, ffn_dim=64,
+                     num_clusters=min(E, 8), seed=7)
+    m = build_model(spec)
+    x = token_stream(spec, 2, n)
+    ds = route_batch(m, x, 0)
+    st = profiler.CoActivationStats(layer=0, num_experts=E, warmup_steps=256, warmup_weight=0.0, laplace_eps=1e-3)
+    for dd in ds:
+        profiler.observe(st, dd, step=dd.token)
+    t = buddies.build_table(st, alpha=0.95, k_max=min(16, E - 1))
+    K = min(16, E - 1)
+    ids = np.full((E, K), -1, np.int32); w = np.zeros((E, K)); lens = np.zeros(E, np.int32)
+    for p in range(E):
+        li = t.ids(p); ids[p, :len(li)] = li; w[p, :len(li)] = t.weights(p); lens[p] = len(li)
+    return dict(E=E, k=k, d=d, n=n, topk=np.stack([dd.topk for dd in ds]).astype(np.int16),
+                logits=np.stack([dd.logits for dd in ds[:n_logits]]),
+                probs=np.stack([dd.probs_renorm for dd in ds[:n_logits]]),
+                tae=np.array([gating.tae(dd) for dd in ds[:n_logits]]),
+                counts=st.counts, pairs=st.pair_counts, ids=ids, w=w, lens=lens)
+
+
 def coact_case(spec: ModelSpec, n: int, warmup_steps: int, warmup_weight: float, eps: float,
                builds, stream_seed: int = 1) -> dict:
     """observe (profiler.py:67-95) over a routed stream, then build_table
@@ -377,6 +404,11 @@ def substrate_case() -> dict:
 def main() -> None:
     if sys.argv[1:] == ["beta"]:  # regenerate only the adaptive-beta fixture
         np.savez_compressed(os.path.join(OUT, "sim_tiny_beta.npz"), **sim_beta_case())
+        return
+    if sys.argv[1:] == ["shapes"]:  # routing + tables at the BASELINE shapes
+        for name, E, k, d, n in (("mixtral", 8, 2, 4096, 16384), ("qwen3", 128, 8, 2048, 32768),
+                                 ("dsv2", 64, 6, 2048, 32768)):
+            np.savez_compressed(os.path.join(OUT, f"routing_{name}.npz"), **routing_shape_case(E, k, d, n))
         return
     if sys.argv[1:] == ["random"]:  # regenerate only the Random-arm fixture
         np.savez_compressed(os.path.join(OUT, "sim_tiny_random.npz"), **sim_random_case())

@@ -58,9 +58,11 @@ def test_model_routing_and_forward(cuda_ok):
                    for p in plans])
     ref = O.forward(x, ex, kd, np.stack([d.probs_renorm for d in ds]),
                     lambda e, xr: O.ffn_tanh(xr, w_in[e], w_out[e]))
-    assert np.max(np.linalg.norm(y - ref, axis=1) / np.linalg.norm(ref, axis=1)) <= 1e-5
+    # the Python API forward runs the f64 SIMT kernels: the reference's precision
+    assert np.max(np.linalg.norm(y - ref, axis=1) / np.linalg.norm(ref, axis=1)) <= 1e-12
     h = model.layer_update(x, y)
-    assert np.allclose(np.sqrt(np.mean(h ** 2, axis=1)), 1.0, atol=1e-5)
+    assert np.allclose(np.sqrt(np.mean(h ** 2, axis=1)), 1.0, atol=1e-12)
+    np.testing.assert_allclose(h, O.layer_update(x, y), rtol=0, atol=1e-13)
     bad = [substitution.ReplacementPlan(0, 1, (substitution.PlanSlot(0, 9, "substituted"),
                                                substitution.PlanSlot(1, 1, "kept")), 1)] + plans[1:]
     with pytest.raises(InternalError):

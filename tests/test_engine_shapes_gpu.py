@@ -72,9 +72,11 @@ def test_dsv2_shared_experts_numerics(cuda_ok):
     then layer_update: rel 2e-2 per token."""
     wl = W.build("dsv2lite", layers=1, max_batch=8, profile_tokens=512)
     E, S, d, f = 64, 2, 2048, 1408
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(0)  # workload seed 0, layer 0: regenerate the row-major weights
-    experts = [W._gen_expert(gen, d, f, "cuda").float() for _ in range(E + S)]
+    from paper_2511_10054_b200 import synth
+    luts = [torch.from_numpy(synth.lut_bf16(synth.matrix_scale(d, f, m)).view(np.int16)).cuda() for m in range(3)]
+    # workload seed 0, layer 0: regenerate the row-major weights
+    experts = [W._synth_expert(luts, 0, 0, e, d, f, torch.empty(3 * d * f, dtype=torch.bfloat16, device="cuda")).float()
+               for e in range(E + S)]
     eng = wl.engine("buddy")
     eng.set_trace(True)
     x = torch.from_numpy(wl.tokens(2, 8)).cuda()
