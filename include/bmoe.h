@@ -100,6 +100,25 @@ int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed, const void
                    uint8_t *kind, int32_t *used, double *delta_out, uint8_t *batch_allowed_out,
                    bm_stream_t stream);
 
+/* ------------------------------------------------ adaptive distribution-gate beta (host)
+ * gating.derive_beta (gating.py:173-186): the largest grid value whose
+ * estimated admitted volume nhat * expert_bytes fits the budget, else the
+ * current beta. BetaController (gating.py:189-221): per record an EMA of the
+ * would-be misses admitted at every candidate (delta < candidate), beta
+ * re-derived every `period` records. The engine drives the same state. */
+#define BM_BETA_MAX_GRID 64
+typedef struct {
+    double budget_bytes, expert_bytes, beta, decay;
+    int64_t period, steps;
+    int32_t n_grid, pad_;
+    double grid[BM_BETA_MAX_GRID], ema[BM_BETA_MAX_GRID];
+} bm_beta_state;
+int bm_derive_beta(double budget_bytes, double expert_bytes, const double *grid_host, const double *nhat_host,
+                   int32_t n, double current_beta, double *beta_out);
+int bm_beta_init(bm_beta_state *state_host, double budget_bytes, double expert_bytes, double initial_beta,
+                 const double *grid_host, int32_t n, double decay, int64_t period);
+int bm_beta_record(bm_beta_state *state_host, double delta, int64_t miss_count, double *beta_out);
+
 /* ------------------------------------------------ Random baseline (host)
  * numpy's PCG64 bit generator state (Generator.bit_generator.state: the
  * 128-bit state and increment, has_uint32 / uinteger), so host code can make

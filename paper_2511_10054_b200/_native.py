@@ -48,6 +48,13 @@ class Pcg64State(C.Structure):
                                    "has_uint32": int(self.has_uint32), "uinteger": int(self.uinteger)}
 
 
+class BetaState(C.Structure):
+    """bm_beta_state (adaptive distribution-gate beta)."""
+    _fields_ = [("budget_bytes", C.c_double), ("expert_bytes", C.c_double), ("beta", C.c_double),
+                ("decay", C.c_double), ("period", C.c_int64), ("steps", C.c_int64), ("n_grid", C.c_int32),
+                ("pad_", C.c_int32), ("grid", C.c_double * 64), ("ema", C.c_double * 64)]
+
+
 class EngineConfig(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("num_experts", C.c_int32), ("top_k", C.c_int32), ("d", C.c_int32),
                 ("f", C.c_int32), ("act", C.c_int32), ("max_batch", C.c_int32), ("capacity", C.c_int32),
@@ -102,6 +109,9 @@ _SIGS = {
     "bm_select_topk_f64": (C.c_int, [P, I64, I64, I64, F64, F64, F64, P, P, P, P, P, P, P]),
     "bm_buddy_remap": (C.c_int, [P, P, P, I32, I64, I64, I64, P, P, P, P, I64, I64, I64, I32, I32, F64, F64, F64,
                                  I32, P, F64, P, P, P, P, P, P]),
+    "bm_derive_beta": (C.c_int, [F64, F64, P, P, I32, F64, P]),
+    "bm_beta_init": (C.c_int, [P, F64, F64, F64, P, I32, F64, I64]),
+    "bm_beta_record": (C.c_int, [P, F64, I64, P]),
     "bm_random_plan": (C.c_int, [P, I64, I64, P, I64, P, P, P, P]),
     "bm_pcg64_integers": (C.c_int, [P, I64, I64, P]),
     "bm_synth_bf16": (C.c_int, [P, C.c_uint64, I64, P, P]),

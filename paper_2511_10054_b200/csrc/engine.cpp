@@ -45,39 +45,22 @@ int random_plan_batch(const int32_t *topk, int64_t B, int64_t k, const uint32_t 
 
 namespace {
 
-// gating.BetaController (gating.py:168-221): EMA of the would-be misses
-// admitted past the distribution gate at every candidate beta; every
-// `period` records beta := the largest candidate whose estimated admitted
-// volume (nhat * expert_bytes) fits the budget (derive_beta, :173-186), else
-// unchanged. f64 operations in the reference's order (no contraction).
+// gating.BetaController (gating.py:168-221) over the shared host
+// implementation in beta.cpp (bm_beta_*), on the default candidate grid.
 struct BetaController {
-    double budget = -1.0, expert_bytes = 0.0, beta = 1.0, decay = 0.9;
-    int period = 64;
-    int64_t steps = 0;
-    double grid[11] = {0.0, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0};  // DEFAULT_BETA_GRID (:170)
-    double ema[11] = {};
-    bool on() const { return budget >= 0.0; }
-    void record(double delta, int64_t miss_count) {
-        const double omd = 1.0 - decay;
-        for (int i = 0; i < 11; ++i) {
-            const double admitted = delta < grid[i] ? (double)miss_count : 0.0;
-            volatile double a = decay * ema[i];
-            volatile double b = omd * admitted;
-            ema[i] = a + b;
-        }
-        if (++steps % period == 0) {
-            bool any = false;
-            double best = 0.0;
-            for (int i = 0; i < 11; ++i) {
-                volatile double vol = ema[i] * expert_bytes;
-                if (vol <= budget && (!any || grid[i] > best)) {
-                    best = grid[i];
-                    any = true;
-                }
-            }
-            if (any) beta = best;
-        }
+    bm_beta_state st{};
+    bool active = false;
+    double beta = 1.0;
+    bool on() const { return active; }
+    int init(double budget, double expert_bytes, double initial) {
+        beta = initial;
+        active = budget >= 0.0;
+        if (!active) return BM_OK;
+        double grid[11];
+        for (int i = 0; i < 11; ++i) grid[i] = (double)i / 10.0;  // DEFAULT_BETA_GRID (gating.py:170)
+        return bm_beta_init(&st, budget, expert_bytes, initial, grid, 11, 0.9, 64);
     }
+    int record(double delta, int64_t miss_count) { return bm_beta_record(&st, delta, miss_count, &beta); }
 };
 
 struct Buffer {
@@ -492,7 +475,7 @@ struct bm_engine {
                     }
                     seen[e] = 1;
                 }
-                beta_ctl.record((double)miss_slots / (double)(B * k), miss_unique);  // delta as in K2
+                ENG_TRY(beta_ctl.record((double)miss_slots / (double)(B * k), miss_unique));  // delta as in K2
             }
         }
         if (tracing) {
@@ -822,9 +805,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     ENG_TRY(g->dmalloc(&g->bm_dev_all, (size_t)L * g->bm_stride));
     ENG_TRY(g->hmalloc(&g->bm_host_all, (size_t)L * g->bm_stride));
     g->rng = c->rng;
-    g->beta_ctl.beta = c->beta;
-    g->beta_ctl.budget = c->pcie_budget_bytes;
-    g->beta_ctl.expert_bytes = (double)c->expert_bytes;
+    ENG_TRY(g->beta_ctl.init(c->pcie_budget_bytes, (double)c->expert_bytes, c->beta));
     ENG_TRY(g->dmalloc(&g->bo_dev_all, (size_t)L * 3 * Et));
     ENG_TRY(g->hmalloc(&g->bo_host_all, (size_t)L * 3 * Et));
     ENG_TRY(g->dmalloc(&g->count_a, Et));

@@ -145,3 +145,24 @@ def test_memtier_oracle_replays_reference_events(idx, pol):
     assert np.array_equal(ev, g["events"])
     assert np.array_equal(st.mask, g["final_mask"]) and np.array_equal(st.last_use, g["final_last_use"])
     assert np.array_equal(st.freq, g["final_freq"]) and st.waste_evictions == int(g["waste"])
+
+
+@pytest.mark.parametrize("name", ["mixtral", "qwen3", "dsv2"])
+def test_oracle_at_baseline_shapes(name):
+    """The oracle's f64 routing reproduces the reference's at the BASELINE
+    shapes (first 512 tokens, regenerated by the substrate restatement), and
+    its counts / table over the reference's routing are bit-exact."""
+    from paper_2511_10054_b200 import substrate
+    g = golden(f"routing_{name}.npz")
+    E, k, d = int(g["E"]), int(g["k"]), int(g["d"])
+    spec = substrate.ModelSpec(num_layers=1, experts_per_layer=E, top_k=k, hidden_dim=d, ffn_dim=64,
+                               num_clusters=min(E, 8), seed=7)
+    gw, gb = substrate.gate_weights(spec)
+    x = substrate.token_stream(spec, 2, int(g["n"]))[:512]
+    z, tk, pr = O.route(x, gw[0], gb[0], k)
+    np.testing.assert_allclose(z, g["logits"][:512], rtol=0, atol=1e-12)
+    assert np.array_equal(tk, g["topk"][:512].astype(np.int64))
+    c, p, _, _ = O.coact_count(g["topk"].astype(np.int64), None, E, 0, 256, 0.0)
+    assert np.array_equal(c, g["counts"]) and np.array_equal(p, g["pairs"])
+    ids, w, lens = O.build_table(p, 1e-3, 0.95, min(16, E - 1))
+    assert np.array_equal(ids, g["ids"]) and np.array_equal(w, g["w"]) and np.array_equal(lens, g["lens"])
