@@ -366,6 +366,7 @@ def _metric(B: int) -> str:
 
 
 def _config(model, L, B, method, capacity, search_rank_h, rate):
+    from paper_2511_10054_b200.synth import CLUSTERS, SPREAD
     E, k, d, f, _, S = _shape(model)
     phase = "decode" if B <= 64 else "prefill"
     cfg = {"workload": f"{MODELS[model]['workload']}-{phase}", "model": MODELS[model]["model"],
@@ -373,6 +374,8 @@ def _config(model, L, B, method, capacity, search_rank_h, rate):
            "capacity_per_layer": capacity, "global_batch": B, "seq_len": 1, "method": method, "rho": 3,
            "search_rank_h": search_rank_h, "alpha": 0.95, "tau_percentile": 15, "policy": "lru",
            "parallelism": "replicas (one process per GPU, disjoint token streams, no collective)",
+           "expert_weights": f"clustered synthetic, {CLUSTERS[model]} clusters shared with the router, spread {SPREAD} "
+                      f"(model.py:161-171 recipe), bf16",
            "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
     if S:
         cfg["shared_experts"] = S
@@ -757,7 +760,7 @@ def main():
     eng.close()
 
     # ---------------- without buddy (method=original, on-demand fetch) ----------------
-    orig, fidelity = None, None
+    orig, fidelity, random_arm = None, None, None
     if not args.no_original:
         eo = wl.engine("original")
         x2 = x_dev.clone()
@@ -773,13 +776,32 @@ def main():
         # reference's seeded readout head
         from paper_2511_10054_b200 import harness, substrate
         rows = slice(Wm * B, (Wm + K) * B)
-        cos, agree = harness.fidelity(x_work[rows].double().cpu().numpy(), x2[rows].double().cpu().numpy(),
-                                      substrate.readout_head(wl.spec, 16))
+        head = substrate.readout_head(wl.spec, 16)
+        exact = x2[rows].double().cpu().numpy()
+        cos, agree = harness.fidelity(x_work[rows].double().cpu().numpy(), exact, head)
+        # the paper's Random baseline on the same batches (substitution.random_plan
+        # through the engine's host PCG64 stream, harness.py:299-300, 358-359)
+        er = wl.engine("random")
+        x3 = x_dev.clone()
+        _timed(er, x3, B, Wm, 0, torch)
+        er.stats(reset=True)
+        comm.barrier()
+        ms_r = _allmax(_timed(er, x3, B, K, Wm, torch), comm)
+        sr = er.stats(reset=True)
+        er.close()
+        cos_r, agree_r = harness.fidelity(x3[rows].double().cpu().numpy(), exact, head)
+        clu = wl.extra.get("clusters")
         fidelity = {"cosine_mean": cos, "argmax_agreement": agree, "tokens": K * B,
+                    "random_cosine_mean": cos_r, "random_argmax_agreement": agree_r,
+                    "buddy_minus_random_cosine": cos - cos_r,
                     "vs": "method=original (every expert exact, fetched on demand)",
-                    "note": "random-init experts share no function, so a substituted buddy is an unrelated "
-                            "expert here; on the reference's clustered substrate the engine reproduces the "
-                            "reference's own fidelity (tests/test_engine_gpu.py)"}
+                    "note": (f"clustered synthetic experts ({clu} clusters, spread {wl.extra.get('spread')}): a "
+                             f"buddy is a cluster mate, a random stand-in usually is not"
+                             if wl.extra.get("clustered") else
+                             "independent random-init experts: a substituted buddy is an unrelated expert")}
+        random_arm = {"value": ws * K * B / (ms_r / 1000.0), "unit": "tokens/s", "ms_per_step": ms_r / K,
+                      "stall_ms_per_step": sr["stall_ms"] / K, "substitutions_per_step": sr["substitutions"] / K,
+                      "physical_fetches_per_step": sr["physical_fetches"] / K}
         orig = {"value": ws * K * B / (ms_o / 1000.0), "unit": "tokens/s", "ms_per_step": ms_o / K,
                 "stall_ms_per_step": so["stall_ms"] / K, "ondemand_misses_per_step": so["ondemand_misses"] / K,
                 "physical_fetches_per_step": so["physical_fetches"] / K,
@@ -828,6 +850,7 @@ def main():
         "wire_gb_per_step": st["wire_bytes"] / K / 1e9,
         "fetch_codec": "exponent-coded bf16 (lossless, bm_xfer)" if args.codec else "raw bf16",
         "without_buddy": orig,
+        "random_substitution": random_arm,
         "fidelity": fidelity,
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -435,6 +435,11 @@ int64_t bm_engine_device_bytes(const bm_engine *e);
  * bf16 values in device memory (16-byte aligned), out: n bf16. Integer-only, so
  * the numpy twin (synth.py) reproduces the bits on the host. */
 int bm_synth_bf16(const uint16_t *lut, uint64_t base, int64_t n, uint16_t *out, bm_stream_t stream);
+/* Clustered experts (model.py:161-171 recipe): out[i] = bf16_rn(b + spread * e) in
+ * fp32 (rounded per operation), b = value i of the cluster's base matrix
+ * (key base_key), e = value i of the expert's delta matrix (key delta_key). */
+int bm_synth_mix_bf16(const uint16_t *lut, uint64_t base_key, uint64_t delta_key, float spread, int64_t n,
+                      uint16_t *out, bm_stream_t stream);
 
 /* ------------------------------------------------ fetch codec (expert transfer)
  * Lossless exponent coding of bf16 expert buffers for the H2D fetch (no

@@ -66,7 +66,7 @@ class CpuDecode:
     def __init__(self, model: str, layers: int, batch: int, profile_tokens: int = 4096, alpha: float = 0.95,
                  tau_percentile: float = 15.0, rho: int = 3, seed: int = 0, threads: int | None = None,
                  cache_rate: float | None = None, stream_seed: int = 2, stream_tokens: int | None = None,
-                 profile: str = "forward", tables=None):
+                 profile: str = "forward", tables=None, clustered: bool = True):
         """profile: how the buddy tables and tau are built when ``tables`` is not
         given, as workload.build does on the GPU: "forward" pushes the profile
         stream through every layer's experts (full residency, f64 here),
@@ -81,8 +81,11 @@ class CpuDecode:
         self.L, self.B, self.rho, self.seed = layers, batch, rho, seed
         self.alpha, self.tau_percentile = alpha, tau_percentile
         self.threads = threads or len(os.sched_getaffinity(0))
+        C = synth.CLUSTERS[model] if clustered else min(E, 8)
+        self.clustered = clustered
+        self.cl_of = synth.cluster_of(E, C) if clustered else None
         spec = substrate.ModelSpec(num_layers=layers, experts_per_layer=E, top_k=k, hidden_dim=d, ffn_dim=f,
-                                   num_clusters=min(E, 8), seed=7)
+                                   num_clusters=C, seed=7)
         self.spec = spec
         gw, gb = substrate.gate_weights(spec)
         # the GPU arm routes fp32-rounded gates and tokens
@@ -134,13 +137,19 @@ class CpuDecode:
         """float64 (W1 [f,d], W3 [f,d], W2 [d,f]) of every expert of layer l (untimed),
         all matrices' chunks spread over the thread pool."""
         s, d, f = self.synth, self.d, self.f
-        luts = [np.ascontiguousarray(s.bf16_to_f64(s.lut_bf16(s.matrix_scale(d, f, m)))) for m in (s.W1, s.W3, s.W2)]
+        luts16 = [np.ascontiguousarray(s.lut_bf16(s.matrix_scale(d, f, m))) for m in (s.W1, s.W3, s.W2)]
+        luts = [np.ascontiguousarray(s.bf16_to_f64(t)) for t in luts16]
         out, tasks = {}, []
         for e in range(self.E + self.S):
             mats = []
             for m, shape in ((s.W1, (f, d)), (s.W3, (f, d)), (s.W2, (d, f))):
                 a = np.empty(shape, np.float64)
-                tasks += synth_host.fill_tasks(s.matrix_key(self.seed, l, e, m), d * f, luts[m], a.reshape(-1))
+                if self.clustered and e < self.E:  # base_cluster + spread * delta_e (model.py:161-171)
+                    tasks += synth_host.fill_mix_tasks(s.base_key(self.seed, l, int(self.cl_of[e]), m),
+                                                       s.matrix_key(self.seed, l, e, m), s.SPREAD, d * f, luts16[m],
+                                                       a.reshape(-1))
+                else:
+                    tasks += synth_host.fill_tasks(s.matrix_key(self.seed, l, e, m), d * f, luts[m], a.reshape(-1))
                 mats.append(a)
             out[e] = tuple(mats)
         list(self.pool.map(lambda t: t(), tasks))

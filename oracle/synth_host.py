@@ -22,6 +22,9 @@ def _lib():
         _h = C.CDLL(_LIB)
         _h.synth_f64_range.restype = None
         _h.synth_f64_range.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+        _h.synth_mix_f64_range.restype = None
+        _h.synth_mix_f64_range.argtypes = [C.c_uint64, C.c_uint64, C.c_float, C.c_int64, C.c_int64, C.c_int64,
+                                           C.c_void_p, C.c_void_p]
     return _h
 
 
@@ -38,6 +41,19 @@ def fill_tasks(base: int, n: int, lut64: np.ndarray, out: np.ndarray, chunk: int
     def one(s0):
         return lambda: lib.synth_f64_range(C.c_uint64(base), n, s0, min(chunk, n - s0), lut64.ctypes.data,
                                            out[s0:].ctypes.data)
+    return [one(s0) for s0 in range(0, n, chunk)]
+
+
+def fill_mix_tasks(base_key: int, delta_key: int, spread: float, n: int, lut16: np.ndarray, out: np.ndarray,
+                   chunk: int = 1 << 22):
+    """Callables filling out[0:n] with a clustered matrix: bf16_rn(b + spread*e) as f64."""
+    lib = _lib()
+    if lib is None:
+        raise RuntimeError(f"{_LIB} not built (make -C oracle)")
+
+    def one(s0):
+        return lambda: lib.synth_mix_f64_range(C.c_uint64(base_key), C.c_uint64(delta_key), C.c_float(spread), n, s0,
+                                               min(chunk, n - s0), lut16.ctypes.data, out[s0:].ctypes.data)
     return [one(s0) for s0 in range(0, n, chunk)]
 
 

@@ -115,6 +115,7 @@ _SIGS = {
     "bm_random_plan": (C.c_int, [P, I64, I64, P, I64, P, P, P, P]),
     "bm_pcg64_integers": (C.c_int, [P, I64, I64, P]),
     "bm_synth_bf16": (C.c_int, [P, C.c_uint64, I64, P, P]),
+    "bm_synth_mix_bf16": (C.c_int, [P, C.c_uint64, C.c_uint64, F32, I64, P, P]),
     "bm_permute_rows_max": (I64, [I64, I64, I64, I64]),
     "bm_append_shared": (C.c_int, [P, P, P, I64, I64, I64, I64, P, P, P, P]),
     "bm_split_counts": (C.c_int, [P, P, I64, P, P, P]),

@@ -7,6 +7,8 @@
 // GPU arm's exact weights without touching the GPU.
 #include <algorithm>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace {
@@ -49,7 +51,49 @@ __global__ void synth_kernel(const uint16_t *__restrict__ lut, uint64_t base, in
     }
 }
 
+// clustered experts (the reference's recipe, model.py:161-171): value =
+// bf16_rn(base + spread * delta), base and delta two hashed matrices, the sum
+// rounded once in fp32 (no contraction) so the host twin reproduces it
+__global__ void synth_mix_kernel(const uint16_t *__restrict__ lut, uint64_t base_key, uint64_t delta_key, float spread,
+                                 int64_t n, uint16_t *__restrict__ out) {
+    extern __shared__ __align__(16) uint16_t s_lut[];
+    for (int i = threadIdx.x; i < 65536 / 8; i += blockDim.x)
+        reinterpret_cast<uint4 *>(s_lut)[i] = reinterpret_cast<const uint4 *>(lut)[i];
+    __syncthreads();
+    const int64_t groups = (n + 3) / 4;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t zb = mix64(base_key + (uint64_t)g), zd = mix64(delta_key + (uint64_t)g);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = 4 * g + j;
+            if (i >= n) break;
+            const float b = __uint_as_float((uint32_t)s_lut[(zb >> (16 * j)) & 0xFFFFu] << 16);
+            const float dl = __uint_as_float((uint32_t)s_lut[(zd >> (16 * j)) & 0xFFFFu] << 16);
+            const float v = __fadd_rn(b, __fmul_rn(spread, dl));
+            const __nv_bfloat16 h = __float2bfloat16_rn(v);
+            out[i] = *reinterpret_cast<const uint16_t *>(&h);
+        }
+    }
+}
+
 }  // namespace
+
+extern "C" int bm_synth_mix_bf16(const uint16_t *lut, uint64_t base_key, uint64_t delta_key, float spread, int64_t n,
+                                 uint16_t *out, bm_stream_t stream) {
+    BM_REQUIRE(n >= 0 && (n == 0 || (lut && out)), BM_EINVAL, "bm_synth_mix_bf16: bad arguments");
+    BM_REQUIRE((reinterpret_cast<uintptr_t>(lut) & 15) == 0, BM_EINVAL, "bm_synth_mix_bf16: lut must be 16-byte aligned");
+    if (n == 0) return BM_OK;
+    static bool attr = false;
+    if (!attr) {
+        BM_CUDA_TRY(cudaFuncSetAttribute(synth_mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 * 2));
+        attr = true;
+    }
+    const int64_t groups = (n + 3) / 4;
+    const int blocks = (int)std::min<int64_t>((groups + 511) / 512, (int64_t)bm::sm_count());
+    synth_mix_kernel<<<blocks, 512, 65536 * 2, bm::as_stream(stream)>>>(lut, base_key, delta_key, spread, n, out);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
 
 extern "C" int bm_synth_bf16(const uint16_t *lut, uint64_t base, int64_t n, uint16_t *out, bm_stream_t stream) {
     BM_REQUIRE(n >= 0 && (n == 0 || (lut && out)), BM_EINVAL, "bm_synth_bf16: bad arguments");

@@ -43,6 +43,13 @@ SHAPES = {
     "tiny": (8, 2, 128, 256, 0.5),
 }
 SHARED = {"dsv2lite": 2}  # always-resident shared experts (outside the cache budget)
+# Clustered synthetic experts (the reference's substrate recipe, model.py:161-171):
+# expert e of cluster c = base_c + SPREAD * delta_e, with the router built on
+# the same clusters (substrate.ModelSpec.num_clusters), so a buddy is a cluster
+# mate and substitution fidelity means something. Cluster counts leave room
+# for a top-k inside one cluster plus spare mates.
+CLUSTERS = {"mixtral": 2, "qwen3": 8, "dsv2lite": 4, "tiny": 2}
+SPREAD = 0.1  # model.cluster_spread default (config.py)
 
 
 def host_mem_available() -> int:
@@ -91,6 +98,29 @@ def matrix_key(seed: int, layer: int, expert: int, matrix: int) -> int:
     any matrix's n/4 counters)."""
     k = (((seed * 1_000_003 + layer) * 4099 + expert) * 4 + matrix) & ((1 << 24) - 1)
     return (k << 40) & ((1 << 64) - 1)
+
+
+def base_key(seed: int, layer: int, cluster: int, matrix: int) -> int:
+    """Hash base of cluster ``cluster``'s base matrix: the expert-key space
+    with the top bit set (expert keys stay below 2^63)."""
+    k = matrix_key(seed, layer, cluster, matrix)
+    if k >> 63:
+        raise ValueError("seed too large for the synthetic key space")
+    return k | (1 << 63)
+
+
+def cluster_of(num_experts: int, clusters: int) -> np.ndarray:
+    """Contiguous cluster blocks (model.py:126-130)."""
+    return (np.arange(num_experts) * clusters) // num_experts
+
+
+def mix_bits(base_bits: np.ndarray, delta_bits: np.ndarray, spread: float) -> np.ndarray:
+    """bf16_rn(b + spread * e) with fp32 operations, each rounded (the kernel's
+    __fadd_rn(b, __fmul_rn(spread, e)))."""
+    b = (base_bits.astype(np.uint32) << np.uint32(16)).view(np.float32)
+    e = (delta_bits.astype(np.uint32) << np.uint32(16)).view(np.float32)
+    v = b + np.float32(spread) * e
+    return _bf16_bits(v)
 
 
 def matrix_scale(d: int, f: int, matrix: int) -> float:

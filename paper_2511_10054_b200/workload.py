@@ -22,6 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import _native as N
 from . import ops, substrate, synth
 from .engine import DecodeEngine, EngineSpec, HostMirror, SharedMirror, coded_mirror_from_device, fill_mirror_from_device
 
@@ -91,13 +92,21 @@ class Workload:
             m.close()
 
 
-def _synth_expert(luts, seed: int, layer: int, expert: int, d: int, f: int, out: torch.Tensor) -> torch.Tensor:
+def _synth_expert(luts, seed: int, layer: int, expert: int, d: int, f: int, out: torch.Tensor,
+                  cluster: int | None = None, spread: float = synth.SPREAD) -> torch.Tensor:
     """One SwiGLU expert [W1 [f,d] | W3 [f,d] | W2 [d,f]] bf16, row-major, from
     the counter-based generator (synth.py; the CPU reference arm regenerates
-    the same bits on the host)."""
+    the same bits on the host): N(0, 1/fan_in) values, or with ``cluster``
+    the clustered recipe base_cluster + spread * delta_expert."""
     n = d * f
     for m in (synth.W1, synth.W3, synth.W2):
-        ops.synth_bf16(luts[m], synth.matrix_key(seed, layer, expert, m), out[m * n:(m + 1) * n])
+        dst = out[m * n:(m + 1) * n]
+        if cluster is None:
+            ops.synth_bf16(luts[m], synth.matrix_key(seed, layer, expert, m), dst)
+        else:
+            N.call("bm_synth_mix_bf16", luts[m].data_ptr(), synth.base_key(seed, layer, cluster, m),
+                   synth.matrix_key(seed, layer, expert, m), float(spread), n, dst.data_ptr(),
+                   torch.cuda.current_stream().cuda_stream)
     return out
 
 
@@ -120,7 +129,7 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
           profile_tokens: int = 4096, alpha: float = 0.95, k_max: int | None = None, tau_percentile: float = 15.0,
           clusters: int | None = None, n_tile: int = 128, device: str = "cuda", rho: int | None = 3,
           codec: int = 1, share: ShareSpec | None = None, log=None, cache_rate: float | None = None,
-          profile: str = "forward") -> Workload:
+          profile: str = "forward", clustered: bool = True) -> Workload:
     """codec 1 keeps the pinned mirrors exponent-coded (bm_xfer_*: ~0.70 of
     the bf16 bytes cross PCIe per miss, rebuilt bit-exactly in HBM); 0 raw.
     share: one node-shared mirror per layer for all local replicas (only the
@@ -129,7 +138,10 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     layer's experts (full residency) and builds each layer's buddy table and
     tau from the routing it sees there, like the reference's cmd_profile
     (harness.py:93-101); "route" routes the same profile tokens at every layer
-    (no expert forward; the CPU twin then builds bit-identical tables)."""
+    (no expert forward; the CPU twin then builds bit-identical tables).
+    clustered: experts follow the reference's clustered recipe on
+    synth.CLUSTERS[name] clusters shared with the router (else independent
+    N(0, 1/fan_in) experts and min(E, 8) router clusters)."""
     import time
     E, k, d, f, rate = SHAPES[name]
     if cache_rate is not None:
@@ -137,8 +149,11 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     S = SHARED.get(name, 0)
     cap = int(math.floor(rate * E))
     k_max = k_max if k_max is not None else min(16, E - 1)
+    if clusters is None:
+        clusters = synth.CLUSTERS[name] if clustered else min(E, 8)
     spec = substrate.ModelSpec(num_layers=layers, experts_per_layer=E, top_k=k, hidden_dim=d, ffn_dim=f,
-                               num_clusters=clusters if clusters is not None else min(E, 8), seed=7)
+                               num_clusters=clusters, seed=7)
+    cl_of = synth.cluster_of(E, clusters) if clustered else None
     gw, gb = substrate.gate_weights(spec)
     gate_w = torch.from_numpy(gw.astype(np.float32)).to(device)
     gate_b = torch.from_numpy(gb.astype(np.float32)).to(device)
@@ -162,7 +177,8 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     for l in range(layers):
         if writer or profile == "forward":
             for e in range(E + S):  # row-major N(0, 1/fan_in) (synth.py), then the UMMA-tiled HBM layout
-                w = _synth_expert(luts, seed, l, e, d, f, row)
+                w = _synth_expert(luts, seed, l, e, d, f, row,
+                                  None if cl_of is None or e >= E else int(cl_of[e]))
                 ops.pack_expert_bf16(w[: f * d].view(f, d), w[f * d: 2 * f * d].view(f, d),
                                      w[2 * f * d:].view(d, f), ops.ACT_SWIGLU, arena[e])
         if not writer:
@@ -213,4 +229,5 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     return Workload(name, spec, es, mirrors, gate_w, gate_b, ids_all, len_all, taus, initial,
                     profile_seconds=time.time() - t0, mean_buddies=float(np.mean(mean_len)),
                     extra={"cache_rate": rate, "profile": profile, "seed": seed, "alpha": alpha,
+                           "clusters": clusters, "clustered": clustered, "spread": synth.SPREAD if clustered else None,
                            "tau_percentile": tau_percentile, "profile_tokens": profile_tokens})

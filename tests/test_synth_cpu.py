@@ -53,3 +53,23 @@ def test_distribution_and_distinct_streams():
     assert not np.array_equal(a, b) and abs(np.corrcoef(a, b)[0, 1]) < 5e-3
     keys = {synth.matrix_key(s, l, e, m) for s in (0, 1) for l in range(48) for e in range(130) for m in range(3)}
     assert len(keys) == 2 * 48 * 130 * 3
+
+
+def test_clustered_twins_agree(host_lib):
+    """Clustered experts (base_cluster + spread * delta, fp32 then bf16): the
+    numpy twin and the oracle's C twin agree bit for bit, and cluster mates
+    are near-identical while other clusters are unrelated."""
+    d, f = 2048, 768
+    n = d * f + 3
+    lut16 = synth.lut_bf16(synth.matrix_scale(d, f, synth.W2))
+    mats = []
+    for e, c in ((0, 0), (1, 0), (5, 1)):
+        bk, dk = synth.base_key(0, 2, c, synth.W2), synth.matrix_key(0, 2, e, synth.W2)
+        ref = synth.bf16_to_f64(synth.mix_bits(synth.synth_bits(bk, n, lut16), synth.synth_bits(dk, n, lut16),
+                                               synth.SPREAD))
+        out = np.empty(n)
+        for t in host_lib.fill_mix_tasks(bk, dk, synth.SPREAD, n, lut16, out, chunk=1 << 16):
+            t()
+        assert np.array_equal(ref, out)
+        mats.append(ref)
+    assert np.corrcoef(mats[0], mats[1])[0, 1] > 0.98 and abs(np.corrcoef(mats[0], mats[2])[0, 1]) < 0.01

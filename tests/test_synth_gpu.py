@@ -46,3 +46,17 @@ def test_gpu_and_cpu_arms_share_weights_and_tables(cuda_ok):
     finally:
         cd.close()
         wl.close()
+
+
+@pytest.mark.parametrize("n", [3, 4099, 2048 * 768 + 1])
+def test_clustered_kernel_equals_numpy_twin(cuda_ok, n):
+    from paper_2511_10054_b200 import _native as N
+    lut = synth.lut_bf16(synth.matrix_scale(2048, 768, synth.W1))
+    bk, dk = synth.base_key(0, 1, 3, synth.W1), synth.matrix_key(0, 1, 42, synth.W1)
+    dev_lut = torch.from_numpy(lut.view(np.int16)).cuda()
+    out = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    N.call("bm_synth_mix_bf16", dev_lut.data_ptr(), bk, dk, synth.SPREAD, n, out.data_ptr(),
+           torch.cuda.current_stream().cuda_stream)
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    ref = synth.mix_bits(synth.synth_bits(bk, n, lut), synth.synth_bits(dk, n, lut), synth.SPREAD)
+    assert np.array_equal(got, ref)
