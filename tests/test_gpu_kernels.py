@@ -486,3 +486,37 @@ def test_empty_inputs(cuda_ok):
     xp = ops.gather_rows(x, perm, 1)
     ops.expert_ffn_bf16(xp, perm, arena, torch.arange(E, dtype=torch.int32, device=DEV), d, f, ops.ACT_SWIGLU, ws)
     torch.cuda.synchronize()
+
+
+def test_split_gemm1_dsmem_exchange_under_timing_stress(cuda_ok):
+    """The CTA-pair SwiGLU GEMM1 exchanges its W1/W3 halves through DSMEM,
+    ordered by cluster-scope mbarriers (racecheck does not model those and
+    reports the 4 exchanges as hazards, profiles/r1e_sanitizer.txt). A real
+    race would make the result depend on timing: 40 launches, each with a
+    different background load on a second stream skewing when the two CTAs of
+    a pair reach the exchange, must all equal the single-CTA result bitwise."""
+    import os
+    rng = np.random.default_rng(77)
+    E, d, f, B, k = 4, 4096, 1024, 300, 2
+    y, ref32, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, ops.ACT_SWIGLU, 128)
+    rows = int(perm.offset[-1])
+    bo = _t(buf_of)
+    old = os.environ.get("BMOE_2SM")
+    side = torch.cuda.Stream()
+    junk = torch.randn(8 << 20, device=DEV)
+    try:
+        os.environ["BMOE_2SM"] = "0"
+        single = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
+        os.environ.pop("BMOE_2SM")  # default: W1|W3-split GEMM1 on CTA pairs at K >= 4096
+        for i in range(40):
+            with torch.cuda.stream(side):
+                for _ in range(i % 5):
+                    junk.mul_(1.0000001)  # occupies some SMs while the pairs start
+            out = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows]
+            assert torch.equal(out, single), i
+        torch.cuda.synchronize()
+    finally:
+        if old is None:
+            os.environ.pop("BMOE_2SM", None)
+        else:
+            os.environ["BMOE_2SM"] = old
