@@ -149,6 +149,15 @@ int64_t bm_permute_rows_max(int64_t B, int64_t k, int64_t E, int64_t row_align);
 int bm_permute(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E, int64_t row_align,
                int32_t *expert_count, int32_t *expert_offset, int32_t *row_token, int32_t *slot_row,
                bm_stream_t stream);
+/* The same permute with a caller-owned chunk scratch of
+ * bm_permute_scratch_elems(B, k, E) int32: plans of 4+ chunks of 1024 slots
+ * (prefill) then run as three multi-CTA kernels (chunk histograms, chunk
+ * bases + offsets, scatter) with bitwise the same rows; without it (or below
+ * 4 chunks) one CTA walks the chunks. */
+int bm_permute_scratch_elems(int64_t B, int64_t k, int64_t E);
+int bm_permute_ws(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E, int64_t row_align,
+                  int32_t *expert_count, int32_t *expert_offset, int32_t *row_token, int32_t *slot_row,
+                  int32_t *chunk_scratch, int64_t scratch_elems, bm_stream_t stream);
 
 /* Extend a plan [B][k] with S always-executed shared experts E..E+S-1 (kind
  * kept, weight 1): outputs [B][k+S] (DeepSeek-V2-style shared experts). */

@@ -120,6 +120,8 @@ _SIGS = {
     "bm_append_shared": (C.c_int, [P, P, P, I64, I64, I64, I64, P, P, P, P]),
     "bm_split_counts": (C.c_int, [P, P, I64, P, P, P]),
     "bm_permute": (C.c_int, [P, P, I64, I64, I64, I64, P, P, P, P, P]),
+    "bm_permute_scratch_elems": (C.c_int, [I64, I64, I64]),
+    "bm_permute_ws": (C.c_int, [P, P, I64, I64, I64, I64, P, P, P, P, P, I64, P]),
     "bm_gather_rows": (C.c_int, [P, I64, I64, P, P, I64, I64, I32, P, P]),
     "bm_combine": (C.c_int, [P, P, P, P, I64, I64, I64, P, F32, P, P]),
     "bm_expert_ffn_f32": (C.c_int, [P, P, P, I64, I64, I64, I32, P, I64, P, I64, P, P, P]),

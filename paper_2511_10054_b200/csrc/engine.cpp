@@ -167,6 +167,8 @@ struct bm_engine {
     int32_t *topk = nullptr, *executed = nullptr;
     uint8_t *kind = nullptr, *allowed = nullptr, *batch_ok = nullptr;
     int32_t *count = nullptr, *offset = nullptr, *row_token = nullptr, *slot_row = nullptr;
+    int32_t *perm_scratch = nullptr;  // chunk histograms of the multi-CTA permute (prefill plans)
+    int64_t perm_scratch_elems = 0;
     // shared experts (always resident, outside the budget): plan extended to k + Ssh slots
     int Ssh = 0;
     int32_t *exec_ext = nullptr;
@@ -371,7 +373,8 @@ struct bm_engine {
             pe = exec_ext;
             pk = kind_ext;
         }
-        ENG_TRY(bm_permute(pe, pk, B, kt, Et, 16, count, offset, row_token, slot_row, s));
+        ENG_TRY(bm_permute_ws(pe, pk, B, kt, Et, 16, count, offset, row_token, slot_row, perm_scratch,
+                              perm_scratch_elems, s));
         if (cfg.fp32_weights) {
             ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 0, x_perm, s));
             return BM_OK;  // the fp32 parity path runs in one piece after the waits
@@ -572,8 +575,8 @@ struct bm_engine {
         }
         ENG_TRY(run(g_post2, l, split_late ? 2 : (fetched ? 1 : 0), h, B, s,
                     [&](cudaStream_t st) { return enqueue_post2(l, h, B, fetched, split_late, st); }));
-        {  // gate, remap, permute, gather, combine (+ append_shared) + the FFN kernels
-            int64_t n = 5 + (Ssh ? 1 : 0);
+        {  // gate, remap, permute (3 kernels at prefill sizes), gather, combine (+ append_shared) + the FFN kernels
+            int64_t n = 5 + (Ssh ? 1 : 0) + ((int64_t)B * (k + Ssh) >= 4 * 1024 ? 2 : 0);
             if (cfg.fp32_weights) {
                 n += 2;
             } else {
@@ -628,7 +631,8 @@ struct bm_engine {
             for (auto &kv : *m)
                 if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
         void *dptrs[] = {exec_ext, kind_ext, probs_ext, logits, probs, y_perm, h_ws, tae, margin, delta, used,
-                         plan_dev, h_int, bm_dev_all, bo_dev_all, count, offset, row_token, slot_row, x_perm, ffn_ws,
+                         plan_dev, h_int, bm_dev_all, bo_dev_all, count, offset, row_token, slot_row, perm_scratch,
+                         x_perm, ffn_ws,
                          count_a, count_b, count_bc, count_c};
         for (void *p : dptrs)
             if (p) cudaFree(p);
@@ -822,6 +826,8 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     ENG_TRY(g->dmalloc(&g->offset, Et + 1));
     ENG_TRY(g->dmalloc(&g->row_token, g->r_max + 16));
     ENG_TRY(g->dmalloc(&g->slot_row, Bm * kt));
+    g->perm_scratch_elems = bm_permute_scratch_elems(Bm, kt, Et);
+    ENG_TRY(g->dmalloc(&g->perm_scratch, (size_t)std::max<int64_t>(g->perm_scratch_elems, 1)));
     if (g->Ssh) {
         ENG_TRY(g->dmalloc(&g->exec_ext, Bm * kt));
         ENG_TRY(g->dmalloc(&g->kind_ext, Bm * kt));

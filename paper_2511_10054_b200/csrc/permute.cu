@@ -84,6 +84,95 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(const int32_t *__
     }
 }
 
+// Multi-CTA permute for prefill-size plans (B*k > one chunk): the single
+// CTA above walks 1024-slot chunks one after another (16 at a 2048-token
+// top-8 chunk, ~78 us). Here chunk c is CTA c: (1) every CTA histograms its
+// chunk, (2) one CTA turns the chunk histograms into expert offsets and each
+// chunk's per-expert base (exclusive prefix over chunks = the running base
+// of the single CTA), (3) every CTA ranks its chunk exactly like pass 2
+// above. Same rows for every slot, bit for bit.
+constexpr int kChunk = kPermThreads;
+
+__global__ void __launch_bounds__(kPermThreads) permute_hist_kernel(const int32_t *__restrict__ executed,
+                                                                    const uint8_t *__restrict__ kind, int nslots,
+                                                                    int E, int32_t *__restrict__ chunk_hist) {
+    __shared__ int cnt[kPermMaxE];
+    for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+    __syncthreads();
+    const int i = blockIdx.x * kChunk + threadIdx.x;
+    if (i < nslots && kind[i] != BM_KIND_DROPPED) atomicAdd(&cnt[executed[i]], 1);
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += blockDim.x) chunk_hist[(size_t)blockIdx.x * E + e] = cnt[e];
+}
+
+__global__ void __launch_bounds__(kPermThreads) permute_scan_kernel(int32_t *__restrict__ chunk_hist, int nchunks,
+                                                                    int E, int align, int32_t *expert_count,
+                                                                    int32_t *expert_offset, int32_t *row_token) {
+    __shared__ int tot[kPermMaxE];
+    __shared__ int off[kPermMaxE + 1];
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {  // per expert: exclusive prefix over chunks, in place
+        int run = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int v = chunk_hist[(size_t)c * E + e];
+            chunk_hist[(size_t)c * E + e] = run;
+            run += v;
+        }
+        tot[e] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int e = 0; e < E; ++e) {
+            off[e] = run;
+            run += (tot[e] + align - 1) / align * align;
+        }
+        off[E] = run;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += blockDim.x) expert_count[e] = tot[e];
+    for (int e = threadIdx.x; e <= E; e += blockDim.x) expert_offset[e] = off[e];
+    for (int e = 0; e < E; ++e)  // padding rows
+        for (int r = off[e] + tot[e] + threadIdx.x; r < off[e + 1]; r += blockDim.x) row_token[r] = -1;
+}
+
+__global__ void __launch_bounds__(kPermThreads) permute_scatter_kernel(const int32_t *__restrict__ executed,
+                                                                       const uint8_t *__restrict__ kind, int nslots,
+                                                                       int k, int E,
+                                                                       const int32_t *__restrict__ chunk_base,
+                                                                       const int32_t *__restrict__ expert_offset,
+                                                                       int32_t *row_token, int32_t *slot_row) {
+    __shared__ int warp_cnt[kPermThreads / 32][kPermMaxE];
+    const int tid = threadIdx.x, warp = tid >> 5, nw = blockDim.x >> 5;
+    const unsigned lane = lane_id();
+    for (int i = tid; i < nw * E; i += blockDim.x) (&warp_cnt[0][0])[(i / E) * kPermMaxE + (i % E)] = 0;
+    __syncthreads();
+    const int i = blockIdx.x * kChunk + tid;
+    int e = -1;
+    if (i < nslots && kind[i] != BM_KIND_DROPPED) e = executed[i];
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (e >= 0 && rank == 0) warp_cnt[warp][e] = __popc(peers);
+    __syncthreads();
+    for (int x = tid; x < E; x += blockDim.x) {
+        int run = 0;
+        for (int w = 0; w < nw; ++w) {
+            const int v = warp_cnt[w][x];
+            warp_cnt[w][x] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    if (i < nslots) {
+        if (e >= 0) {
+            const int row = expert_offset[e] + chunk_base[(size_t)blockIdx.x * E + e] + warp_cnt[warp][e] + rank;
+            row_token[row] = i / k;
+            slot_row[i] = row;
+        } else {
+            slot_row[i] = -1;
+        }
+    }
+}
+
 // layout 0: fp32 row-major [r_max][d]
 __global__ void gather_f32_kernel(const float *__restrict__ x, int d, const int32_t *__restrict__ row_token,
                                   const int32_t *__restrict__ expert_offset, int E, float *__restrict__ out) {
@@ -335,18 +424,49 @@ extern "C" int64_t bm_permute_rows_max(int64_t B, int64_t k, int64_t E, int64_t 
     return n + segs * (row_align - 1);
 }
 
-extern "C" int bm_permute(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E,
-                          int64_t row_align, int32_t *expert_count, int32_t *expert_offset, int32_t *row_token,
-                          int32_t *slot_row, bm_stream_t stream) {
+extern "C" int bm_permute_scratch_elems(int64_t B, int64_t k, int64_t E) {
+    return (int)(((B * k + kChunk - 1) / kChunk) * E);
+}
+
+extern "C" int bm_permute_ws(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E,
+                             int64_t row_align, int32_t *expert_count, int32_t *expert_offset, int32_t *row_token,
+                             int32_t *slot_row, int32_t *chunk_scratch, int64_t scratch_elems, bm_stream_t stream) {
     BM_REQUIRE(B >= 0 && k >= 1 && E >= 1 && E <= kPermMaxE && row_align >= 1 && row_align <= 256, BM_EINVAL,
                "bm_permute: bad shape");
     BM_REQUIRE(expert_count && expert_offset && (B == 0 || (executed && kind && row_token && slot_row)), BM_EINVAL,
                "bm_permute: null pointer");
-    permute_kernel<<<1, kPermThreads, 0, as_stream(stream)>>>(executed, kind, (int)(B * k), (int)k, (int)E,
-                                                             (int)row_align, expert_count, expert_offset,
-                                                             row_token, slot_row);
+    const int64_t nslots = B * k, nchunks = (nslots + kChunk - 1) / kChunk;
+    static const int multi_env = [] {
+        const char *ev = getenv("BMOE_PERMUTE_MULTI");  // A/B switch: 0 = always one CTA
+        return ev ? atoi(ev) : -1;
+    }();
+    const bool multi = chunk_scratch && scratch_elems >= nchunks * E && nchunks >= 2 &&
+                       (multi_env < 0 ? nchunks >= 4 : multi_env != 0);
+    cudaStream_t st = as_stream(stream);
+    if (multi) {  // per-chunk histograms -> chunk bases (in place) + offsets -> scatter
+        permute_hist_kernel<<<(unsigned)nchunks, kPermThreads, 0, st>>>(executed, kind, (int)nslots, (int)E,
+                                                                       chunk_scratch);
+        BM_LAUNCH_CHECK();
+        permute_scan_kernel<<<1, kPermThreads, 0, st>>>(chunk_scratch, (int)nchunks, (int)E, (int)row_align,
+                                                         expert_count, expert_offset, row_token);
+        BM_LAUNCH_CHECK();
+        permute_scatter_kernel<<<(unsigned)nchunks, kPermThreads, 0, st>>>(executed, kind, (int)nslots, (int)k,
+                                                                           (int)E, chunk_scratch, expert_offset,
+                                                                           row_token, slot_row);
+        BM_LAUNCH_CHECK();
+        return BM_OK;
+    }
+    permute_kernel<<<1, kPermThreads, 0, st>>>(executed, kind, (int)nslots, (int)k, (int)E, (int)row_align,
+                                               expert_count, expert_offset, row_token, slot_row);
     BM_LAUNCH_CHECK();
     return BM_OK;
+}
+
+extern "C" int bm_permute(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E,
+                          int64_t row_align, int32_t *expert_count, int32_t *expert_offset, int32_t *row_token,
+                          int32_t *slot_row, bm_stream_t stream) {
+    return bm_permute_ws(executed, kind, B, k, E, row_align, expert_count, expert_offset, row_token, slot_row,
+                         nullptr, 0, stream);
 }
 
 extern "C" int bm_gather_rows(const float *x, int64_t B, int64_t d, const int32_t *row_token,

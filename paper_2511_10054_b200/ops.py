@@ -175,8 +175,10 @@ def permute(executed, kind, num_experts: int, align: int = ROW_ALIGN) -> Permuta
                     torch.empty(num_experts + 1, device=dev, dtype=torch.int32),
                     torch.full((max(r_max, 1),), -1, device=dev, dtype=torch.int32),
                     torch.empty(B * k, device=dev, dtype=torch.int32), r_max)
-    N.call("bm_permute", _p(executed), _p(kind), B, k, num_experts, align, _p(p.count), _p(p.offset),
-           _p(p.row_token), _p(p.slot_row), _s())
+    ns = int(N.lib().bm_permute_scratch_elems(B, k, num_experts))
+    scratch = torch.empty(max(ns, 1), device=dev, dtype=torch.int32)
+    N.call("bm_permute_ws", _p(executed), _p(kind), B, k, num_experts, align, _p(p.count), _p(p.offset),
+           _p(p.row_token), _p(p.slot_row), _p(scratch), ns, _s())
     return p
 
 

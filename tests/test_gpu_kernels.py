@@ -520,3 +520,26 @@ def test_split_gemm1_dsmem_exchange_under_timing_stress(cuda_ok):
             os.environ.pop("BMOE_2SM", None)
         else:
             os.environ["BMOE_2SM"] = old
+
+
+@pytest.mark.parametrize("B,k,E,drop", [(2048, 8, 128, 0.0), (2051, 8, 128, 0.1), (8192, 8, 128, 0.0),
+                                        (700, 6, 66, 0.2), (4096, 2, 8, 0.05), (513, 8, 256, 0.0)])
+def test_multi_cta_permute_equals_single_cta(cuda_ok, B, k, E, drop):
+    """Prefill-size plans take the three-kernel multi-CTA permute (chunk
+    histograms, chunk bases, scatter); every output — counts, padded offsets,
+    row tokens (padding -1) and slot rows — must equal the single-CTA kernel's
+    bit for bit, dropped slots included."""
+    from paper_2511_10054_b200 import _native as N
+    rng = np.random.default_rng(B + E)
+    ex = torch.tensor(np.stack([rng.choice(E, k, replace=False) for _ in range(B)]).astype(np.int32), device=DEV)
+    kd = torch.tensor((rng.random((B, k)) < drop).astype(np.uint8) * 3, device=DEV)
+    multi = ops.permute(ex, kd, E)
+    single = ops.Permutation(torch.empty_like(multi.count), torch.empty_like(multi.offset),
+                             torch.full_like(multi.row_token, -7), torch.empty_like(multi.slot_row), multi.r_max)
+    N.call("bm_permute", ex.data_ptr(), kd.data_ptr(), B, k, E, 16, single.count.data_ptr(),
+           single.offset.data_ptr(), single.row_token.data_ptr(), single.slot_row.data_ptr(),
+           torch.cuda.current_stream().cuda_stream)
+    rows = int(single.offset[-1])
+    assert torch.equal(multi.count, single.count) and torch.equal(multi.offset, single.offset)
+    assert torch.equal(multi.slot_row, single.slot_row)
+    assert torch.equal(multi.row_token[:rows], single.row_token[:rows])
