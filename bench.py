@@ -322,7 +322,7 @@ def cpu_decode(args, L: int, steps: int, timed_from: int, layers_run: int | None
     from oracle.decode_cpu import CpuDecode
     n_total = (args.warmup + 3 * args.steps) * args.batch  # the GPU arm's token stream length
     cd = CpuDecode(args.model, L, args.batch, profile_tokens=args.profile_tokens, cache_rate=args.cache_rate,
-                   stream_tokens=n_total, tables=tables)
+                   stream_tokens=n_total, tables=tables, clusters=args.clusters)
     per_step, _ = cd.run(steps, timed_from, layers_run=layers_run, log=log)
     return per_step, cd
 
@@ -347,7 +347,7 @@ def run_reference(args, ws):
             "value": tps, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (the GPU arm's weights and streams)",
-            "config": _config(args.model, L, args.batch, "buddy", cd.cap, cd.k_max, cd.rate),
+            "config": _config(args.model, L, args.batch, "buddy", cd.cap, cd.k_max, cd.rate, args.clusters),
             "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": f"every step: {args.batch} tokens through all {L} layers (route, gates, "
                                        f"remap, cache replay, f64 SwiGLU forward, layer_update) via the numpy "
@@ -365,8 +365,9 @@ def _metric(B: int) -> str:
     return f"MoE {phase} tokens/sec at fixed expert-cache budget; expert-miss stall (ms)"
 
 
-def _config(model, L, B, method, capacity, search_rank_h, rate):
+def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None):
     from paper_2511_10054_b200.synth import CLUSTERS, SPREAD
+    clusters = clusters or CLUSTERS[model]
     E, k, d, f, _, S = _shape(model)
     phase = "decode" if B <= 64 else "prefill"
     cfg = {"workload": f"{MODELS[model]['workload']}-{phase}", "model": MODELS[model]["model"],
@@ -374,8 +375,9 @@ def _config(model, L, B, method, capacity, search_rank_h, rate):
            "capacity_per_layer": capacity, "global_batch": B, "seq_len": 1, "method": method, "rho": 3,
            "search_rank_h": search_rank_h, "alpha": 0.95, "tau_percentile": 15, "policy": "lru",
            "parallelism": "replicas (one process per GPU, disjoint token streams, no collective)",
-           "expert_weights": f"clustered synthetic, {CLUSTERS[model]} clusters shared with the router, spread {SPREAD} "
-                      f"(model.py:161-171 recipe), bf16",
+           "expert_weights": f"clustered synthetic, {clusters} clusters shared with the router, spread {SPREAD} "
+                      f"(model.py:161-171 recipe; {clusters} = the reference's default model.clusters = 8 capped at E"
+                      f"{'' if clusters == min(E, 8) else ', overridden by --clusters'}), bf16",
            "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
     if S:
         cfg["shared_experts"] = S
@@ -571,6 +573,9 @@ def main():
     ap.add_argument("--trace-tokens", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--codec", type=int, default=1, choices=[0, 1],
                     help="1: exponent-coded pinned mirrors (lossless, fewer PCIe bytes per miss); 0: raw bf16")
+    ap.add_argument("--clusters", type=int, default=None,
+                    help="expert/router clusters (default: the reference's model.clusters = 8, capped at E; "
+                         "synth.FIDELITY_CLUSTERS gives several buddies per cluster for fidelity experiments)")
     ap.add_argument("--cache-rate", type=float, default=None,
                     help="expert-cache budget as a fraction of the experts (default: the config's)")
     args = ap.parse_args()
@@ -600,7 +605,7 @@ def main():
     t0 = time.time()
     # replicas serve ONE model (same weights and tables on every rank) over disjoint token streams
     wl = W.build(args.model, layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=0, codec=args.codec,
-                 share=share, cache_rate=args.cache_rate)
+                 share=share, cache_rate=args.cache_rate, clusters=args.clusters)
     log(f"built {L} layers in {time.time() - t0:.1f}s (mean buddies {wl.mean_buddies:.2f}, "
         f"mirror: {host_info['host_mirror']})")
     n_steps_total = Wm + 3 * K
@@ -840,7 +845,8 @@ def main():
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": Wm,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init bf16 weights, reference-style clustered router/token stream)",
-        "config": _config(args.model, L, B, "buddy", wl.eng.capacity, wl.eng.search_rank_h, wl.extra["cache_rate"]),
+        "config": _config(args.model, L, B, "buddy", wl.eng.capacity, wl.eng.search_rank_h, wl.extra["cache_rate"],
+                          args.clusters),
         "tables_sha16": digest,
         "stall_ms_per_step": st["stall_ms"] / K,
         "sim_stall_model": {"ondemand_misses_per_step": st["ondemand_misses"] / K,

@@ -66,7 +66,8 @@ class CpuDecode:
     def __init__(self, model: str, layers: int, batch: int, profile_tokens: int = 4096, alpha: float = 0.95,
                  tau_percentile: float = 15.0, rho: int = 3, seed: int = 0, threads: int | None = None,
                  cache_rate: float | None = None, stream_seed: int = 2, stream_tokens: int | None = None,
-                 profile: str = "forward", tables=None, clustered: bool = True):
+                 profile: str = "forward", tables=None, clustered: bool = True,
+                 clusters: int | None = None):
         """profile: how the buddy tables and tau are built when ``tables`` is not
         given, as workload.build does on the GPU: "forward" pushes the profile
         stream through every layer's experts (full residency, f64 here),
@@ -81,7 +82,7 @@ class CpuDecode:
         self.L, self.B, self.rho, self.seed = layers, batch, rho, seed
         self.alpha, self.tau_percentile = alpha, tau_percentile
         self.threads = threads or len(os.sched_getaffinity(0))
-        C = synth.CLUSTERS[model] if clustered else min(E, 8)
+        C = clusters if clusters is not None else (synth.CLUSTERS[model] if clustered else min(E, 8))
         self.clustered = clustered
         self.cl_of = synth.cluster_of(E, C) if clustered else None
         spec = substrate.ModelSpec(num_layers=layers, experts_per_layer=E, top_k=k, hidden_dim=d, ffn_dim=f,

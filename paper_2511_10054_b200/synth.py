@@ -45,10 +45,14 @@ SHAPES = {
 SHARED = {"dsv2lite": 2}  # always-resident shared experts (outside the cache budget)
 # Clustered synthetic experts (the reference's substrate recipe, model.py:161-171):
 # expert e of cluster c = base_c + SPREAD * delta_e, with the router built on
-# the same clusters (substrate.ModelSpec.num_clusters), so a buddy is a cluster
-# mate and substitution fidelity means something. Cluster counts leave room
-# for a top-k inside one cluster plus spare mates.
-CLUSTERS = {"mixtral": 2, "qwen3": 8, "dsv2lite": 4, "tiny": 2}
+# the same clusters (substrate.ModelSpec.num_clusters). The default cluster
+# count is the reference's own default, model.clusters = 8 (config.py:72),
+# capped at E as ModelSpec.validate requires (model.py:74-75): at the Mixtral
+# shape (E = 8) every expert is its own cluster, exactly what the reference
+# builds there. FIDELITY_CLUSTERS are coarser groupings (several mates per
+# cluster) for the buddy-vs-random fidelity experiments (bench --clusters).
+CLUSTERS = {"mixtral": 8, "qwen3": 8, "dsv2lite": 8, "tiny": 8}
+FIDELITY_CLUSTERS = {"mixtral": 2, "qwen3": 8, "dsv2lite": 4, "tiny": 2}
 SPREAD = 0.1  # model.cluster_spread default (config.py)
 
 

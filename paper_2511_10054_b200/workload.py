@@ -140,8 +140,9 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
     (harness.py:93-101); "route" routes the same profile tokens at every layer
     (no expert forward; the CPU twin then builds bit-identical tables).
     clustered: experts follow the reference's clustered recipe on
-    synth.CLUSTERS[name] clusters shared with the router (else independent
-    N(0, 1/fan_in) experts and min(E, 8) router clusters)."""
+    `clusters` clusters shared with the router (default synth.CLUSTERS[name],
+    the reference's default model.clusters = 8 capped at E), else independent
+    N(0, 1/fan_in) experts and min(E, 8) router clusters."""
     import time
     E, k, d, f, rate = SHAPES[name]
     if cache_rate is not None:

@@ -75,7 +75,10 @@ def test_dsv2_shared_experts_numerics(cuda_ok):
     from paper_2511_10054_b200 import synth
     luts = [torch.from_numpy(synth.lut_bf16(synth.matrix_scale(d, f, m)).view(np.int16)).cuda() for m in range(3)]
     # workload seed 0, layer 0: regenerate the row-major weights
-    experts = [W._synth_expert(luts, 0, 0, e, d, f, torch.empty(3 * d * f, dtype=torch.bfloat16, device="cuda")).float()
+    # the workload's clustered recipe (routed experts only; the shared ones are independent)
+    cl_of = synth.cluster_of(E, wl.extra["clusters"])
+    experts = [W._synth_expert(luts, 0, 0, e, d, f, torch.empty(3 * d * f, dtype=torch.bfloat16, device="cuda"),
+                               int(cl_of[e]) if e < E else None).float()
                for e in range(E + S)]
     eng = wl.engine("buddy")
     eng.set_trace(True)
