@@ -322,7 +322,8 @@ def cpu_decode(args, L: int, steps: int, timed_from: int, layers_run: int | None
     from oracle.decode_cpu import CpuDecode
     n_total = (args.warmup + 3 * args.steps) * args.batch  # the GPU arm's token stream length
     cd = CpuDecode(args.model, L, args.batch, profile_tokens=args.profile_tokens, cache_rate=args.cache_rate,
-                   stream_tokens=n_total, tables=tables, clusters=args.clusters)
+                   stream_tokens=n_total, tables=tables, clusters=args.clusters,
+                   clustered=args.experts == "clustered")
     per_step, _ = cd.run(steps, timed_from, layers_run=layers_run, log=log)
     return per_step, cd
 
@@ -347,7 +348,8 @@ def run_reference(args, ws):
             "value": tps, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (the GPU arm's weights and streams)",
-            "config": _config(args.model, L, args.batch, "buddy", cd.cap, cd.k_max, cd.rate, args.clusters),
+            "config": _config(args.model, L, args.batch, "buddy", cd.cap, cd.k_max, cd.rate, args.clusters,
+                              args.experts),
             "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": f"every step: {args.batch} tokens through all {L} layers (route, gates, "
                                        f"remap, cache replay, f64 SwiGLU forward, layer_update) via the numpy "
@@ -365,7 +367,7 @@ def _metric(B: int) -> str:
     return f"MoE {phase} tokens/sec at fixed expert-cache budget; expert-miss stall (ms)"
 
 
-def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None):
+def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None, experts="clustered"):
     from paper_2511_10054_b200.synth import CLUSTERS, SPREAD
     clusters = clusters or CLUSTERS[model]
     E, k, d, f, _, S = _shape(model)
@@ -378,6 +380,8 @@ def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None):
            "expert_weights": f"clustered synthetic, {clusters} clusters shared with the router, spread {SPREAD} "
                       f"(model.py:161-171 recipe; {clusters} = the reference's default model.clusters = 8 capped at E"
                       f"{'' if clusters == min(E, 8) else ', overridden by --clusters'}), bf16",
+           **({} if experts == "clustered" else {"expert_weights": "independent N(0, 1/fan_in) experts (round 1's "
+                                                                  "workload), router on min(E, 8) clusters, bf16"}),
            "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
     if S:
         cfg["shared_experts"] = S
@@ -573,6 +577,9 @@ def main():
     ap.add_argument("--trace-tokens", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--codec", type=int, default=1, choices=[0, 1],
                     help="1: exponent-coded pinned mirrors (lossless, fewer PCIe bytes per miss); 0: raw bf16")
+    ap.add_argument("--experts", default="clustered", choices=["clustered", "independent"],
+                    help="expert weights: the reference's clustered recipe (default) or independent N(0, 1/fan_in) "
+                         "experts (round 1's workload; router on min(E, 8) clusters)")
     ap.add_argument("--clusters", type=int, default=None,
                     help="expert/router clusters (default: the reference's model.clusters = 8, capped at E; "
                          "synth.FIDELITY_CLUSTERS gives several buddies per cluster for fidelity experiments)")
@@ -605,7 +612,8 @@ def main():
     t0 = time.time()
     # replicas serve ONE model (same weights and tables on every rank) over disjoint token streams
     wl = W.build(args.model, layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=0, codec=args.codec,
-                 share=share, cache_rate=args.cache_rate, clusters=args.clusters)
+                 share=share, cache_rate=args.cache_rate, clusters=args.clusters,
+                 clustered=args.experts == "clustered")
     log(f"built {L} layers in {time.time() - t0:.1f}s (mean buddies {wl.mean_buddies:.2f}, "
         f"mirror: {host_info['host_mirror']})")
     n_steps_total = Wm + 3 * K
@@ -846,7 +854,7 @@ def main():
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init bf16 weights, reference-style clustered router/token stream)",
         "config": _config(args.model, L, B, "buddy", wl.eng.capacity, wl.eng.search_rank_h, wl.extra["cache_rate"],
-                          args.clusters),
+                          args.clusters, args.experts),
         "tables_sha16": digest,
         "stall_ms_per_step": st["stall_ms"] / K,
         "sim_stall_model": {"ondemand_misses_per_step": st["ondemand_misses"] / K,

@@ -379,6 +379,9 @@ typedef struct {
     double pcie_budget_bytes; /* >= 0: adaptive distribution-gate beta (gating.BetaController, gating.py:189-221,
                                  gate.pcie_budget_bytes config.py:94) starting at `beta`; < 0: fixed beta */
     bm_pcg64 rng; /* method RANDOM: the generator of harness.py:299-300 (SeedSequence([run.seed, 31])) */
+    int32_t beta_wire_bytes; /* adaptive beta's bytes per admitted miss: 0 = expert_bytes (the reference's
+                                cost model, gating.py:189-221), 1 = the measured mean of the bytes a
+                                physical fetch moved over PCIe so far (coded size with fetch_codec) */
 } bm_engine_config;
 
 typedef struct {

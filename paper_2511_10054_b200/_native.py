@@ -64,7 +64,7 @@ class EngineConfig(C.Structure):
                 ("temperature", C.c_double), ("gamma", C.c_double), ("load_ms", C.c_double),
                 ("hit_ms", C.c_double), ("compute_ms", C.c_double), ("prefetch_ms", C.c_double),
                 ("expert_bytes", C.c_int64), ("num_shared", C.c_int32), ("fetch_codec", C.c_int32),
-                ("pcie_budget_bytes", C.c_double), ("rng", Pcg64State)]
+                ("pcie_budget_bytes", C.c_double), ("rng", Pcg64State), ("beta_wire_bytes", C.c_int32)]
 
 
 class EngineStats(C.Structure):

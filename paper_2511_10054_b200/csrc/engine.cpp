@@ -61,6 +61,8 @@ struct BetaController {
         return bm_beta_init(&st, budget, expert_bytes, initial, grid, 11, 0.9, 64);
     }
     int record(double delta, int64_t miss_count) { return bm_beta_record(&st, delta, miss_count, &beta); }
+    // beta_wire_bytes: the budget check prices a miss at what a fetch measurably moved
+    void set_miss_bytes(double b) { st.expert_bytes = b; }
 };
 
 struct Buffer {
@@ -191,6 +193,7 @@ struct bm_engine {
     std::vector<uint32_t *> bm_dev_l, bm_host_l;  // per-layer residency bitmaps (+ the beta the remap uses)
     int bm_stride = 0, beta_word = 0;            // u32 words per layer slot; beta (f64) at word beta_word
     BetaController beta_ctl;
+    int64_t wire_total = 0, fetch_total = 0;  // every physical fetch since creation (stats resets keep them)
     bm_pcg64 rng{};  // method RANDOM: numpy's PCG64 stream of harness.py:299-300, advanced on the host
     std::vector<int32_t *> bo_dev_l, bo_host_l;   // per-layer buffer maps (E + shared)
     cudaStream_t cap_stream = nullptr;
@@ -293,6 +296,7 @@ struct bm_engine {
             ENG_TRY(enqueue_coded(l, e, bufs[b].dev, s, r, &wire));
             if (c1) ENG_CUDA(cudaEventRecord(c1, s));
             stats.wire_bytes += wire;
+            wire_total += wire;
             done = r.dec;
         } else {
             if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(s, bufs[b].free_ev, 0));
@@ -301,7 +305,9 @@ struct bm_engine {
                                      cudaMemcpyHostToDevice, s));
             if (c1) ENG_CUDA(cudaEventRecord(c1, s));
             stats.wire_bytes += (int64_t)buf_bytes;
+            wire_total += (int64_t)buf_bytes;
         }
+        ++fetch_total;
         ENG_CUDA(cudaEventRecord(ready[l][e], done));
         ready_pending[l][e] = 1;
         ready_stream[l][e] = done;
@@ -478,6 +484,8 @@ struct bm_engine {
                     }
                     seen[e] = 1;
                 }
+                if (cfg.beta_wire_bytes && fetch_total > 0)
+                    beta_ctl.set_miss_bytes((double)wire_total / (double)fetch_total);
                 ENG_TRY(beta_ctl.record((double)miss_slots / (double)(B * k), miss_unique));  // delta as in K2
             }
         }

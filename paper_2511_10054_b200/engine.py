@@ -203,6 +203,8 @@ class EngineSpec:
     num_shared: int = 0
     fetch_codec: int | None = None  # None: the mirrors' format (HostMirror.codec)
     pcie_budget_bytes: float | None = None  # adaptive beta (gating.BetaController) when set
+    beta_bytes: str = "logical"  # adaptive beta prices a miss at expert_bytes ("logical", the reference's
+    #                             cost model) or at the measured mean wire bytes of a fetch ("wire")
     run_seed: int = 0  # method "random": the plan stream of harness.py:299-300
 
     @property
@@ -244,6 +246,9 @@ class DecodeEngine:
         cfg.expert_bytes = ebytes
         cfg.num_shared = int(spec.num_shared)
         cfg.pcie_budget_bytes = -1.0 if spec.pcie_budget_bytes is None else float(spec.pcie_budget_bytes)
+        if spec.beta_bytes not in ("logical", "wire"):
+            raise ConfigurationError(f"beta_bytes must be 'logical' or 'wire', got {spec.beta_bytes!r}")
+        cfg.beta_wire_bytes = int(spec.beta_bytes == "wire")
         cfg.rng = N.Pcg64State.from_generator(
             np.random.default_rng(np.random.SeedSequence([int(spec.run_seed), _RNG_TAG_RANDOM_METHOD])))
         cfg.fetch_codec = int(spec.fetch_codec if spec.fetch_codec is not None else getattr(mirrors[0], "codec", 0))

@@ -133,3 +133,39 @@ def test_engine_coded_mirrors_equal_raw(cuda_ok):
     assert stats[0]["h2d_bytes"] == stats[1]["h2d_bytes"] > 0
     assert stats[0]["wire_bytes"] == stats[0]["h2d_bytes"]
     assert stats[1]["wire_bytes"] <= 0.70 * stats[1]["h2d_bytes"], stats[1]
+
+
+def test_adaptive_beta_on_measured_wire_bytes(cuda_ok):
+    """beta_bytes="wire": the adaptive distribution gate prices an admitted
+    miss at the mean bytes a physical fetch actually moved over PCIe instead
+    of the logical expert size (gating.py:189-221 prices expert_bytes). With
+    raw mirrors the two are the same number, so the runs are identical (events,
+    beta); with exponent-coded mirrors (~0.68 of the bytes) a miss is cheaper,
+    so under the same budget beta never ends lower and, for a budget between
+    the two volumes, ends higher. 72 layer-steps: one re-derivation (period 64)."""
+    from paper_2511_10054_b200 import workload as W
+    for codec in (0, 1):
+        wl = W.build("qwen3", layers=3, max_batch=16, profile_tokens=1024, codec=codec)
+        x0 = torch.from_numpy(wl.tokens(2, 24 * 16)).cuda()
+        betas = {}
+        for budget in (1e8, 2.5e8, 4e8, 6e8, 2e9):
+            for mode in ("logical", "wire"):
+                eng = wl.engine("buddy", pcie_budget_bytes=budget, beta_bytes=mode, beta=0.3)
+                x = x0.clone()
+                for s in range(24):
+                    eng.step(x[s * 16:(s + 1) * 16], np.arange(s * 16, (s + 1) * 16))
+                torch.cuda.synchronize()
+                st = eng.stats()
+                betas[budget, mode] = (st["beta"], eng.events(), x.cpu().numpy(), st["wire_bytes"], st["h2d_bytes"])
+                eng.close()
+        for budget in (1e8, 2.5e8, 4e8, 6e8, 2e9):
+            lo, wi = betas[budget, "logical"], betas[budget, "wire"]
+            if codec == 0:
+                assert lo[0] == wi[0]
+                assert np.array_equal(lo[1], wi[1]) and np.array_equal(lo[2].view(np.uint32), wi[2].view(np.uint32))
+            else:
+                assert wi[0] >= lo[0], (budget, lo[0], wi[0])
+        if codec == 1:
+            assert any(betas[b, "wire"][0] > betas[b, "logical"][0] for b in (1e8, 2.5e8, 4e8, 6e8, 2e9)), \
+                {b: (betas[b, "logical"][0], betas[b, "wire"][0]) for b in (1e8, 2.5e8, 4e8, 6e8, 2e9)}
+        wl.close()
