@@ -239,6 +239,11 @@ int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const in
                        const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
                        int64_t workspace_bytes, float *y_perm, bm_stream_t stream);
 
+/* Diagnostics: with BMOE_FFN_TRACE=1 in the environment the fused decode FFN
+ * records 8 globaltimer stamps (ns) per CTA of its last call (entry, setup,
+ * GEMM1 loads issued, GEMM1 MMAs committed, GEMM1 epilogue done, barrier seen,
+ * GEMM2 epilogue done, exit); copies up to cap of them, returns the count. */
+int64_t bm_ffn_trace_read(uint64_t *out_host, int64_t cap);
 /* Kernel timing for the bench's roofline: after bm_set_kernel_timing(1)
  * every bm_expert_ffn_bf16 call records CUDA events on its stream around its
  * two GEMM kernels; bm_kernel_times() waits for them and writes 2 floats per

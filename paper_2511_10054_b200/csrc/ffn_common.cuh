@@ -230,7 +230,9 @@ struct FusedParams {
     int tile_cap;
     unsigned *grid_bar;  // [0] arrivals, [1] generation
     int prefetch_w2;     // stream W2's first stages before the barrier opens
+    unsigned long long *trace;  // diagnostics (BMOE_FFN_TRACE): kTracePts globaltimer stamps per CTA, else null
 };
+constexpr int kTracePts = 8;
 
 // CTA that processes stream-K iteration i of T over G CTAs
 __device__ __forceinline__ int cta_of(long long i, long long T, int G) {

@@ -38,7 +38,7 @@ struct Geom {
 template <int NMAT, int KPS>
 __device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &gm, int &stage, uint32_t &phase,
                               long long it0, long long it1, int spt, uint64_t pol, const unsigned *gate,
-                              unsigned gen0, int prefetch) {
+                              unsigned gen0, int prefetch, unsigned long long *gate_stamp = nullptr) {
     constexpr uint32_t kA = (uint32_t)(KPS * NMAT) * kATileBytes;
     const int mtiles = P.M / kBM;
     int cur = -1;
@@ -66,6 +66,7 @@ __device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &g
     long long it = it0;
     if (gate && !prefetch) {
         while (ptx::ld_acquire_gpu(gate) == gen0) __nanosleep(64);
+        if (gate_stamp) *gate_stamp = ptx::globaltimer();
         ptx::fence_proxy_async_global();
     } else if (gate) {
         // the weights do not depend on H: A parts of the first stages now ...
@@ -85,6 +86,7 @@ __device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &g
         }
         // ... then the H parts once every CTA has finished phase 1
         while (ptx::ld_acquire_gpu(gate) == gen0) __nanosleep(64);
+        if (gate_stamp) *gate_stamp = ptx::globaltimer();
         ptx::fence_proxy_async_global();
         int stg = stage0;
         for (long long j = it0; j < pre_end; ++j) {
@@ -253,6 +255,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
 
     const int warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
+    // phase trace (diagnostics): 0 entry, 1 setup done, 2 GEMM1 loads issued, 3 GEMM1 MMAs committed,
+    // 4 GEMM1 epilogue done, 5 barrier seen by the producer, 6 GEMM2 epilogue done, 7 exit
+    unsigned long long *tr = fp.trace ? fp.trace + (size_t)blockIdx.x * kTracePts : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = ptx::globaltimer();
     const GemmParams &P1 = fp.g[0];
     const GemmParams &P2 = fp.g[1];
     const int n_tile = P1.n_tile;
@@ -292,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = tmem_base_sh;
+    if (tr && threadIdx.x == 0) tr[1] = ptx::globaltimer();
 
     const int cta = blockIdx.x, Gn = gridDim.x;
     const int spt1 = P1.K / (kBK * KPS1), spt2 = P2.K / (kBK * KPS2);
@@ -306,15 +313,17 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         if (cta < G1)
             fused_produce<NMAT1, KPS1>(P1, sched, gm, stage, phase, range_start(cta, T1, G1),
                                        range_start(cta + 1, T1, G1), spt1, pol, nullptr, 0, 0);
+        if (tr) tr[2] = ptx::globaltimer();
         if (cta < G2)
             fused_produce<1, KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2), range_start(cta + 1, T2, G2),
-                                   spt2, pol, fp.grid_bar + 1, gen0, fp.prefetch_w2);
+                                   spt2, pol, fp.grid_bar + 1, gen0, fp.prefetch_w2, tr ? tr + 5 : nullptr);
     } else if (warp == 1 && lane == 0) {
         int stage = 0, acc = 0;
         uint32_t phase = 0, acc_phase = 0;
         if (cta < G1)
             fused_mma<NMAT1, KPS1>(P1, sched, gm, stage, phase, acc, acc_phase, range_start(cta, T1, G1),
                                    range_start(cta + 1, T1, G1), spt1, tmem_base);
+        if (tr) tr[3] = ptx::globaltimer();
         if (cta < G2)
             fused_mma<1, KPS2>(P2, sched, gm, stage, phase, acc, acc_phase, range_start(cta, T2, G2),
                                range_start(cta + 1, T2, G2), spt2, tmem_base);
@@ -324,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         uint32_t acc_phase = 0;
         fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, T1, G1, cta, spt1, tmem_base, q, lane);
         // H of this CTA is written: publish it (to the bulk-copy proxy too) and arrive
+        if (tr && q == 0 && lane == 0) tr[4] = ptx::globaltimer();
         ptx::fence_proxy_async_global();
         __threadfence();
         ptx::named_bar_sync(1, 128);
@@ -337,12 +347,14 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         }
         fused_epilogue<1>(P2, sched, gm, fp.arrive + fp.tile_cap, acc, acc_phase, T2, G2, cta, spt2, tmem_base, q,
                           lane);
+        if (tr && q == 0 && lane == 0) tr[6] = ptx::globaltimer();
     }
     __syncwarp();
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
+    if (tr && threadIdx.x == 0) tr[7] = ptx::globaltimer();
 }
 
 template <int NMAT1, int KPS1, int KPS2>

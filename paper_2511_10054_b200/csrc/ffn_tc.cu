@@ -83,6 +83,28 @@ WsLayout ws_layout(long long E, long long d, long long f, long long r_max, long 
 using namespace bm;
 using namespace bm::ffn;
 
+// Diagnostics (BMOE_FFN_TRACE=1): per-CTA globaltimer stamps of the fused
+// decode kernel's phases (ffn_decode.cu), overwritten by every fused call.
+static unsigned long long *g_trace = nullptr;
+static int g_trace_ctas = 0;
+static unsigned long long *trace_buffer(int G) {
+    static const bool on = getenv("BMOE_FFN_TRACE") && atoi(getenv("BMOE_FFN_TRACE")) != 0;
+    if (!on) return nullptr;
+    if (!g_trace) {
+        if (cudaMalloc(&g_trace, (size_t)G * kTracePts * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        cudaMemset(g_trace, 0, (size_t)G * kTracePts * sizeof(unsigned long long));
+        g_trace_ctas = G;
+    }
+    return g_trace;
+}
+
+extern "C" int64_t bm_ffn_trace_read(uint64_t *out_host, int64_t cap) {
+    if (!g_trace || !out_host) return 0;
+    const int64_t n = std::min<int64_t>(cap, (int64_t)g_trace_ctas * kTracePts);
+    if (cudaMemcpy(out_host, g_trace, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return n;
+}
+
 extern "C" int64_t bm_expert_ffn_bf16_workspace(int64_t E, int64_t d, int64_t f, int64_t r_max, int64_t n_tile) {
     return ws_layout(E, d, f, r_max, n_tile).total;
 }
@@ -146,7 +168,7 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
         int pre = 1;
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap, reinterpret_cast<unsigned *>(counters + 2 * wl.tile_cap),
-                       pre};
+                       pre, trace_buffer(G)};
         // timing record: [start, end] of the one kernel, then an empty GEMM2 interval
         if (timing && record_event(s)) return BM_ECUDA;
         const int rc = launch_fused_dispatch(fp, nmat1, k1, k2, G, s);

@@ -37,6 +37,9 @@ def main():
     ap.add_argument("--n-tile", type=int, default=16)
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--k", type=int, default=2, help="slots per token (top-k)")
+    ap.add_argument("--trace", action="store_true",
+                    help="phase trace of the fused decode kernel (needs BMOE_FFN_TRACE=1): per-CTA globaltimer "
+                         "stamps of single graph replays, as microseconds after the first CTA's entry")
     args = ap.parse_args()
     E, d, f, B, A = args.E, args.d, args.f, args.tokens, args.experts_active
     dev = "cuda"
@@ -103,6 +106,23 @@ def main():
            # a decode-width call is one fused kernel: the timing hook reports it as "gemm1" and 0 for gemm2
            "gemm1_frac": (b1 + (b2 if g2 == 0 else 0)) / g1 / 1e6 / peak, "gemm2_frac": b2 / g2 / 1e6 / peak if g2 else None,
            "env": {k: v for k, v in os.environ.items() if k.startswith("BMOE_")}}
+    if args.trace:
+        names = ["entry", "setup", "g1_loads_issued", "g1_mma_done", "g1_epi_done", "barrier_seen", "g2_epi_done",
+                 "exit"]
+        G = torch.cuda.get_device_properties(0).multi_processor_count
+        rows = []
+        for i in range(20):
+            graphs[i % len(graphs)].replay()
+            torch.cuda.synchronize()
+            st = np.zeros(G * 8, np.uint64)
+            n = int(N.lib().bm_ffn_trace_read(st.ctypes.data, st.size))
+            st = st[:n].reshape(-1, 8).astype(np.float64)
+            t0 = st[:, 0].min()
+            rel = np.where(st > 0, (st - t0) / 1000.0, np.nan)
+            rows.append([[np.nanmin(rel[:, j]), np.nanmedian(rel[:, j]), np.nanmax(rel[:, j])] for j in range(8)])
+        med = np.median(np.array(rows), axis=0)
+        out["trace_us"] = {nm: {"min": round(float(a), 2), "med": round(float(b), 2), "max": round(float(c), 2)}
+                           for nm, (a, b, c) in zip(names, med)}
     print(json.dumps(out))
 
 
