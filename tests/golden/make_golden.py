@@ -319,6 +319,25 @@ def sim_case() -> dict:
     return out
 
 
+def files_case() -> dict:
+    """The raw bytes of every file the reference's cmd_profile -> cmd_build
+    write for the tiny config (harness.py:70-157: stats_LXX.bin (BSST v1),
+    coact_LXX.csv, tae_samples.txt, buddies_LXX.bin (BSBT v1), buddies_LXX.csv),
+    so the GPU pipeline's files can be compared byte for byte."""
+    cfg = parse_config_text(TINY_SIM)
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        pdir, bdir = os.path.join(td, "p"), os.path.join(td, "b")
+        harness.cmd_profile(cfg, pdir)
+        cfg.set("io.profile_dir", pdir)
+        harness.cmd_build(cfg, bdir)
+        for tag, d in (("p", pdir), ("b", bdir)):
+            for name in sorted(os.listdir(d)):
+                with open(os.path.join(d, name), "rb") as fh:
+                    out[f"{tag}/{name}"] = np.frombuffer(fh.read(), np.uint8)
+    return out
+
+
 def sim_beta_case() -> dict:
     """The tiny pipeline's buddy simulation with the adaptive distribution
     gate (gate.pcie_budget_bytes set -> gating.BetaController,
@@ -410,6 +429,9 @@ def main() -> None:
                                  ("dsv2", 64, 6, 2048, 32768)):
             np.savez_compressed(os.path.join(OUT, f"routing_{name}.npz"), **routing_shape_case(E, k, d, n))
         return
+    if sys.argv[1:] == ["files"]:  # regenerate only the profile/build file bytes
+        np.savez_compressed(os.path.join(OUT, "files_tiny.npz"), **files_case())
+        return
     if sys.argv[1:] == ["random"]:  # regenerate only the Random-arm fixture
         np.savez_compressed(os.path.join(OUT, "sim_tiny_random.npz"), **sim_random_case())
         return
@@ -444,6 +466,7 @@ def main() -> None:
     np.savez_compressed(os.path.join(OUT, "sim_tiny.npz"), **sim_case())
     np.savez_compressed(os.path.join(OUT, "substrate.npz"), **substrate_case())
     np.savez_compressed(os.path.join(OUT, "sim_tiny_random.npz"), **sim_random_case())
+    np.savez_compressed(os.path.join(OUT, "files_tiny.npz"), **files_case())
     print("golden fixtures written to", OUT, "with buddysim", buddysim.__version__)
 
 

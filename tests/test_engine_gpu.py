@@ -5,6 +5,8 @@ miss, substitution, eviction, prefetch, with simulated times and bytes) must
 equal the reference's bit for bit, and the outputs (fp32 parity mode, tanh
 experts) must match the reference's f64 outputs within 1e-4 relative."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -206,6 +208,18 @@ def test_profile_build_pipeline_matches_reference(cuda_ok, tmp_path):
             n = int(g[f"lens_L{l}"][p])
             assert list(t.ids(p)) == list(g[f"ids_L{l}"][p, :n]) == list(tables[l].ids(p)), (l, p)
             assert np.array_equal(t.weights(p), g[f"w_L{l}"][p, :n])
+    # the files the GPU pipeline wrote are byte-identical to the reference's own (files_tiny.npz:
+    # its cmd_profile / cmd_build output), except tae_samples.txt (fp32 router entropies, checked above)
+    zf = golden("files_tiny.npz")
+    n_files = 0
+    for key in zf.files:
+        tag, name = key.split("/")
+        if name == "tae_samples.txt":
+            continue
+        with open(os.path.join(pdir if tag == "p" else bdir, name), "rb") as fh:
+            assert fh.read() == zf[key].tobytes(), key
+        n_files += 1
+    assert n_files == 16
     sim = dict(TINY)
     sim.update({"method": "buddy", "stream.seed": 2, "stream.num_tokens": 320, "sub.rho": 3})
     r = harness.run_simulation(sim, tables=tables, tau_by_layer=taus)
