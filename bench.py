@@ -322,7 +322,7 @@ def cpu_decode(args, L: int, steps: int, timed_from: int, layers_run: int | None
     from oracle.decode_cpu import CpuDecode
     n_total = (args.warmup + 3 * args.steps) * args.batch  # the GPU arm's token stream length
     cd = CpuDecode(args.model, L, args.batch, profile_tokens=args.profile_tokens, cache_rate=args.cache_rate,
-                   stream_tokens=n_total, tables=tables, clusters=args.clusters,
+                   stream_tokens=n_total, tables=tables, clusters=args.clusters, seed=args.weight_seed,
                    clustered=args.experts == "clustered")
     per_step, _ = cd.run(steps, timed_from, layers_run=layers_run, log=log)
     return per_step, cd
@@ -385,6 +385,8 @@ def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None, e
            "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
     if S:
         cfg["shared_experts"] = S
+    if getattr(_config, "weight_seed", 0):
+        cfg["weight_seed"] = _config.weight_seed
     return cfg
 
 
@@ -580,12 +582,15 @@ def main():
     ap.add_argument("--experts", default="clustered", choices=["clustered", "independent"],
                     help="expert weights: the reference's clustered recipe (default) or independent N(0, 1/fan_in) "
                          "experts (round 1's workload; router on min(E, 8) clusters)")
+    ap.add_argument("--weight-seed", type=int, default=0,
+                    help="seed of the synthetic expert weights (the workload instance; tables are re-profiled)")
     ap.add_argument("--clusters", type=int, default=None,
                     help="expert/router clusters (default: the reference's model.clusters = 8, capped at E; "
                          "synth.FIDELITY_CLUSTERS gives several buddies per cluster for fidelity experiments)")
     ap.add_argument("--cache-rate", type=float, default=None,
                     help="expert-cache budget as a fraction of the experts (default: the config's)")
     args = ap.parse_args()
+    _config.weight_seed = args.weight_seed
     launch_or_check(args)
     ws, rank, local = _dist()
     if args.impl == "reference":
@@ -611,7 +616,8 @@ def main():
     E, k_top, d, f, rate, S = _shape(args.model)
     t0 = time.time()
     # replicas serve ONE model (same weights and tables on every rank) over disjoint token streams
-    wl = W.build(args.model, layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=0, codec=args.codec,
+    wl = W.build(args.model, layers=L, max_batch=B, profile_tokens=args.profile_tokens, seed=args.weight_seed,
+                 codec=args.codec,
                  share=share, cache_rate=args.cache_rate, clusters=args.clusters,
                  clustered=args.experts == "clustered")
     log(f"built {L} layers in {time.time() - t0:.1f}s (mean buddies {wl.mean_buddies:.2f}, "

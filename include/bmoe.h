@@ -239,6 +239,17 @@ int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const in
                        const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
                        int64_t workspace_bytes, float *y_perm, bm_stream_t stream);
 
+/* bm_expert_ffn_bf16 followed by bm_combine(y_perm, slot_row, probs, kind, B,
+ * k, d, h, residual_scale, h): the gate-weighted combine + layer_update of
+ * forward_batch / layer_update (model.py:334-347) in place on h [B][d] fp32.
+ * At decode widths (n_tile <= 64) both run in ONE launch (the combine after a
+ * second grid barrier of the fused FFN), bit-identical to the two calls. */
+int bm_expert_ffn_bf16_combine(const void *x_perm, const int32_t *expert_count, const int32_t *expert_offset,
+                               int64_t E, int64_t d, int64_t f, int32_t act, const void *w_arena, int64_t n_bufs,
+                               const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
+                               int64_t workspace_bytes, float *y_perm, const int32_t *slot_row, const float *probs,
+                               const uint8_t *kind, int64_t B, int64_t k, float *h, float residual_scale,
+                               bm_stream_t stream);
 /* Diagnostics: with BMOE_FFN_TRACE=1 in the environment the fused decode FFN
  * records 8 globaltimer stamps (ns) per CTA of its last call (entry, setup,
  * GEMM1 loads issued, GEMM1 MMAs committed, GEMM1 epilogue done, barrier seen,

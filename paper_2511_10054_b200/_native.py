@@ -131,6 +131,8 @@ _SIGS = {
     "bm_pack_expert_bf16": (C.c_int, [P, P, P, I64, I64, I32, P, P]),
     "bm_expert_ffn_bf16_workspace": (I64, [I64, I64, I64, I64, I64]),
     "bm_expert_ffn_bf16": (C.c_int, [P, P, P, I64, I64, I64, I32, P, I64, P, I64, I64, P, I64, P, P]),
+    "bm_expert_ffn_bf16_combine": (C.c_int, [P, P, P, I64, I64, I64, I32, P, I64, P, I64, I64, P, I64, P,
+                                             P, P, P, I64, I64, P, F32, P]),
     "bm_set_kernel_timing": (C.c_int, [I32]),
     "bm_ffn_trace_read": (C.c_int64, [P, I64]),
     "bm_kernel_times": (I64, [P, I64]),

@@ -206,6 +206,8 @@ struct bm_engine {
     // +0.7% Mixtral / +0.8% Qwen3 decode tokens/s (within run-to-run noise), at the price of
     // a third, smaller FFN launch per layer-step (FFN roofline 0.84 -> 0.81, 0.49 -> 0.36); off
     bool split_fetched = false;
+    // K5 joins the layer-step's last bf16 FFN launch (bm_expert_ffn_bf16_combine; BMOE_FUSE_COMBINE=0: own launch)
+    bool fuse_combine = true;
     bm_engine_stats stats{};
     TimingRing stall_ev, copy_ev;
     std::vector<uint8_t> mask_tmp;
@@ -367,7 +369,7 @@ struct bm_engine {
     // Post phase, part 1 (before the fetch waits): buffer map + fetch mask
     // upload, K3 permute, gather, and — bf16 path — K4 over the experts that
     // are already in HBM, overlapping the H2D copies of the missing ones.
-    int enqueue_post1(int l, float *h, int64_t B, cudaStream_t s) {
+    int enqueue_post1(int l, float *h, int64_t B, bool with_combine, cudaStream_t s) {
         const int Et = E + Ssh, kt = k + Ssh;
         ENG_CUDA(cudaMemcpyAsync(bo_dev_l[l], bo_host_l[l], 3 * Et * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         if (cfg.method == BM_METHOD_RANDOM)  // the host-drawn plan [executed | kind] replaces K2's on-demand plan
@@ -388,13 +390,22 @@ struct bm_engine {
         ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 1, x_perm, s));
         ENG_TRY(bm_split_counts(count, bo_dev_l[l] + Et, Et, count_a, count_bc, s));
         ENG_TRY(bm_split_counts(count_bc, bo_dev_l[l] + 2 * Et, Et, count_b, count_c, s));
-        return ffn_bf16(l, B, count_a, s);
+        return ffn_bf16(l, h, B, count_a, with_combine, s);
     }
 
-    int ffn_bf16(int l, int64_t B, const int32_t *cnt, cudaStream_t s) {
+    // no expert gets more than B rows: the token tile is sized to the batch
+    int token_tile(int64_t B) const { return std::min(cfg.n_tile, std::max(16, (int)((B + 15) / 16 * 16))); }
+
+    // K4 over the experts with rows in cnt; with_combine: K5 (+ layer_update, in place on h)
+    // joins it (one launch at decode widths, bm_expert_ffn_bf16_combine)
+    int ffn_bf16(int l, float *h, int64_t B, const int32_t *cnt, bool with_combine, cudaStream_t s) {
         const int Et = E + Ssh;
-        // no expert gets more than B rows: size the token tile to the batch
-        const int nt = std::min(cfg.n_tile, std::max(16, (int)((B + 15) / 16 * 16)));
+        const int nt = token_tile(B);
+        if (with_combine)
+            return bm_expert_ffn_bf16_combine(x_perm, cnt, offset, Et, d, f, cfg.act, arena, nbufs, bo_dev_l[l],
+                                              r_max, nt, ffn_ws, ffn_ws_bytes, y_perm, slot_row,
+                                              Ssh ? probs_ext : probs, Ssh ? kind_ext : kind, B, k + Ssh, h, 0.5f,
+                                              s);
         return bm_expert_ffn_bf16(x_perm, cnt, offset, Et, d, f, cfg.act, arena, nbufs, bo_dev_l[l], r_max, nt,
                                   ffn_ws, ffn_ws_bytes, y_perm, s);
     }
@@ -407,8 +418,10 @@ struct bm_engine {
             ENG_TRY(bm_expert_ffn_f32(static_cast<float *>(x_perm), count, offset, Et, d, f, cfg.act,
                                       reinterpret_cast<const float *>(arena), buf_elems, bo_dev_l[l], r_max, h_ws,
                                       y_perm, s));
-        } else if (fetched) {
-            ENG_TRY(ffn_bf16(l, B, late_only ? count_c : count_b, s));
+        } else if (fetched) {  // the last FFN call of the layer-step carries the combine
+            return ffn_bf16(l, h, B, late_only ? count_c : count_b, fuse_combine, s);
+        } else if (fuse_combine) {
+            return BM_OK;  // it ran with the resident experts' FFN (post1)
         }
         ENG_TRY(bm_combine(y_perm, slot_row, Ssh ? probs_ext : probs, Ssh ? kind_ext : kind, B, kt, d, h, 0.5f, h, s));
         return BM_OK;
@@ -566,15 +579,16 @@ struct bm_engine {
         stats.ffn_experts += Ssh;
         stats.ffn_rows += (int64_t)B * Ssh;
         // 8. K3 -> K4 (resident experts) || H2D of the missing ones -> K4 (fetched) -> K5
-        ENG_TRY(run(g_post, l, 0, h, B, s, [&](cudaStream_t st) { return enqueue_post1(l, h, B, st); }));
         const bool fetched = !waits.empty();
+        ENG_TRY(run(g_post, l, fetched ? 0 : 1, h, B, s,
+                    [&](cudaStream_t st) { return enqueue_post1(l, h, B, fuse_combine && !fetched, st); }));
         if (fetched) {
             cudaEvent_t a, bb;
             ENG_TRY(stall_ev.next(&a, &bb));
             ENG_CUDA(cudaEventRecord(a, s));
             if (split_late) {
                 for (size_t i = 0; i + 1 < waits.size(); ++i) ENG_CUDA(cudaStreamWaitEvent(s, waits[i], 0));
-                ENG_TRY(ffn_bf16(l, B, count_b, s));  // the early fetched experts
+                ENG_TRY(ffn_bf16(l, h, B, count_b, false, s));  // the early fetched experts
                 ENG_CUDA(cudaStreamWaitEvent(s, waits.back(), 0));
             } else {
                 for (cudaEvent_t w : waits) ENG_CUDA(cudaStreamWaitEvent(s, w, 0));
@@ -594,6 +608,7 @@ struct bm_engine {
                 const char *ev = getenv(nt <= 64 ? "BMOE_FUSED" : "BMOE_DP");
                 const int per_call = (ev && atoi(ev) == 0) ? 4 : (nt <= 64 ? 1 : 2);
                 n += 2 + per_call * (1 + (fetched ? 1 : 0) + (split_late ? 1 : 0));  // split_counts x2 + FFN calls
+                if (fuse_combine && nt <= 64 && per_call == 1) --n;  // K5 ran inside the last fused FFN launch
             }
             stats.kernel_launches += n;
         }
@@ -760,6 +775,8 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     if (const char *ev = getenv("BMOE_GRAPHS")) g->use_graphs = atoi(ev) != 0;
     if (const char *ev = getenv("BMOE_OVERLAP")) g->overlap_fetch = atoi(ev) != 0;
     if (const char *ev = getenv("BMOE_SPLIT_FETCHED")) g->split_fetched = atoi(ev) != 0;  // A/B switch
+    if (const char *ev = getenv("BMOE_FUSE_COMBINE")) g->fuse_combine = atoi(ev) != 0;  // A/B switch
+    if (g->cfg.fp32_weights) g->fuse_combine = false;  // the fp32 parity path keeps K5 separate
     ENG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     ENG_CUDA(cudaStreamCreateWithFlags(&g->prefetch_stream, cudaStreamNonBlocking));
     if (g->coded) {

@@ -224,6 +224,17 @@ __device__ __forceinline__ void finish16(const GemmParams &p, const TileInfo &ti
     }
 }
 
+// gate-weighted combine + layer_update fused behind the FFN (B = 0: none):
+// h[b] = rmsnorm(h[b] + scale * sum_s probs[b,s] * y_perm[slot_row[b,s]])
+struct CombineArgs {
+    const int32_t *slot_row;
+    const float *probs;
+    const uint8_t *kind;
+    float *h;
+    float scale;
+    int B, k;
+};
+
 struct FusedParams {
     GemmParams g[2];
     int *arrive;         // [2][tile_cap] split-tile arrival counters
@@ -231,6 +242,8 @@ struct FusedParams {
     unsigned *grid_bar;  // [0] arrivals, [1] generation
     int prefetch_w2;     // stream W2's first stages before the barrier opens
     unsigned long long *trace;  // diagnostics (BMOE_FFN_TRACE): kTracePts globaltimer stamps per CTA, else null
+    CombineArgs cmb;            // K5 after a second grid barrier, in the same launch
+    int pdl;                    // launched with programmatic stream serialization (griddepcontrol.wait first)
 };
 constexpr int kTracePts = 8;
 

@@ -8,6 +8,7 @@
 // persistent CTA per SM walks an equal share of the (tile, k-step) space.
 // Warp roles (256 threads): w0 producer (bulk copies), w1 MMA issuer (one
 // thread; precomputed descriptors), w2 TMEM allocator, w4-7 epilogue.
+#include "combine.cuh"
 #include "ffn_common.cuh"
 
 namespace bm {
@@ -262,6 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     const GemmParams &P1 = fp.g[0];
     const GemmParams &P2 = fp.g[1];
     const int n_tile = P1.n_tile;
+    // launched with programmatic stream serialization (fp.pdl): nothing below reads
+    // what the preceding kernel writes before this wait
+    if (fp.pdl && warp == 0) ptx::grid_dep_wait();
     if (warp == 0) build_sched_warp(sched, P1.count, P1.offset, P1.E, n_tile);
     // the barrier generation cannot advance before this CTA arrives, so
     // reading it here (before the __syncthreads) is race-free
@@ -354,6 +358,31 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
+    if (fp.cmb.B > 0) {
+        // K5 (gate-weighted combine + layer_update, in place on h) once every
+        // CTA's y tiles are written: a second grid barrier, then token b on CTA
+        // b (mod G) with all 256 threads -- combine_kernel's own code and thread
+        // count, so h is bit-identical to the separate launch.
+        __shared__ CombineShared<float> csh;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned *gen = fp.grid_bar + 1;
+            while (ptx::ld_acquire_gpu(gen) == gen0) __nanosleep(64);  // barrier 1 done: its count is reset
+            const unsigned prev = atomicAdd(fp.grid_bar, 1u);
+            if (prev == (unsigned)Gn - 1u) {
+                fp.grid_bar[0] = 0u;
+                __threadfence();
+                atomicAdd(fp.grid_bar + 1, 1u);
+            }
+            while (ptx::ld_acquire_gpu(gen) - gen0 < 2u) __nanosleep(64);
+        }
+        __syncthreads();
+        float *hbuf = reinterpret_cast<float *>(smem_raw);
+        for (int b = cta; b < fp.cmb.B; b += Gn)
+            combine_token<float, 4, true>(b, P2.y_perm, fp.cmb.slot_row, fp.cmb.probs, fp.cmb.kind, fp.cmb.k, P2.M,
+                                          fp.cmb.h, fp.cmb.scale, fp.cmb.h, hbuf, csh);
+    }
     if (tr && threadIdx.x == 0) tr[7] = ptx::globaltimer();
 }
 
@@ -370,11 +399,23 @@ int launch_fused(const FusedParams &fp, int G, cudaStream_t s) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = kSmemFused;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
-    at[0].val.cooperative = 1;
+    // the grid barrier needs every CTA resident: a cooperative launch guarantees it
+    // (BMOE_COOP=0: a plain launch, resident in practice at one CTA per SM);
+    // fp.pdl: programmatic stream serialization, so the launch and the prologue
+    // (barrier init, TMEM allocation) overlap the preceding kernel
+    static const int coop = getenv("BMOE_COOP") ? atoi(getenv("BMOE_COOP")) : 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na++].val.cooperative = 1;
+    }
+    if (fp.pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     BM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, fp));
     return BM_OK;
 }

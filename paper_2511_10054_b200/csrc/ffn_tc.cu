@@ -109,12 +109,46 @@ extern "C" int64_t bm_expert_ffn_bf16_workspace(int64_t E, int64_t d, int64_t f,
     return ws_layout(E, d, f, r_max, n_tile).total;
 }
 
+static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const int32_t *expert_offset, int64_t E,
+                         int64_t d, int64_t f, int32_t act, const void *w_arena, int64_t n_bufs,
+                         const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
+                         int64_t workspace_bytes, float *y_perm, bm_stream_t stream, const CombineArgs *cmb);
+
 extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_count, const int32_t *expert_offset,
                                   int64_t E, int64_t d, int64_t f, int32_t act, const void *w_arena, int64_t n_bufs,
                                   const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
                                   int64_t workspace_bytes, float *y_perm, bm_stream_t stream) {
+    return ffn_bf16_impl(x_perm, expert_count, expert_offset, E, d, f, act, w_arena, n_bufs, buf_of_expert, r_max,
+                         n_tile, workspace, workspace_bytes, y_perm, stream, nullptr);
+}
+
+extern "C" int bm_expert_ffn_bf16_combine(const void *x_perm, const int32_t *expert_count,
+                                          const int32_t *expert_offset, int64_t E, int64_t d, int64_t f, int32_t act,
+                                          const void *w_arena, int64_t n_bufs, const int32_t *buf_of_expert,
+                                          int64_t r_max, int64_t n_tile, void *workspace, int64_t workspace_bytes,
+                                          float *y_perm, const int32_t *slot_row, const float *probs,
+                                          const uint8_t *kind, int64_t B, int64_t k, float *h, float residual_scale,
+                                          bm_stream_t stream) {
+    BM_REQUIRE(B >= 0 && k >= 1 && k <= 64, BM_EINVAL, "bm_expert_ffn_bf16_combine: bad B/k");
+    if (B == 0) return BM_OK;
+    BM_REQUIRE(slot_row && probs && kind && h, BM_EINVAL, "bm_expert_ffn_bf16_combine: null pointer");
+    const CombineArgs cmb{slot_row, probs, kind, h, residual_scale, (int)B, (int)k};
+    return ffn_bf16_impl(x_perm, expert_count, expert_offset, E, d, f, act, w_arena, n_bufs, buf_of_expert, r_max,
+                         n_tile, workspace, workspace_bytes, y_perm, stream, &cmb);
+}
+
+static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const int32_t *expert_offset, int64_t E,
+                         int64_t d, int64_t f, int32_t act, const void *w_arena, int64_t n_bufs,
+                         const int32_t *buf_of_expert, int64_t r_max, int64_t n_tile, void *workspace,
+                         int64_t workspace_bytes, float *y_perm, bm_stream_t stream, const CombineArgs *cmb) {
+    // the combine (if any) after the FFN, as its own launch: bm_combine's exact computation
+    auto separate_combine = [&]() -> int {
+        if (!cmb) return BM_OK;
+        return bm_combine(y_perm, cmb->slot_row, cmb->probs, cmb->kind, cmb->B, cmb->k, d, cmb->h, cmb->scale,
+                          cmb->h, stream);
+    };
     BM_REQUIRE(r_max >= 0, BM_EINVAL, "r_max must be >= 0");
-    if (r_max == 0) return BM_OK;  // no rows (an empty batch): nothing to compute
+    if (r_max == 0) return separate_combine();  // no rows (an empty batch): nothing to compute
     BM_REQUIRE(x_perm && expert_count && expert_offset && w_arena && buf_of_expert && workspace && y_perm,
                BM_EINVAL, "bm_expert_ffn_bf16: null pointer");
     BM_REQUIRE(E >= 1 && E <= kMaxE, BM_EINVAL, "E out of range");
@@ -168,7 +202,13 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
         int pre = 1;
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap, reinterpret_cast<unsigned *>(counters + 2 * wl.tile_cap),
-                       pre, trace_buffer(G)};
+                       pre, trace_buffer(G), CombineArgs{}, 0};
+        static const int pdl = getenv("BMOE_PDL") ? atoi(getenv("BMOE_PDL")) : 0;
+        fp.pdl = pdl;
+        // the combine joins the launch when bm_combine would take its 16-byte vector path (same code then)
+        const bool fuse_cmb = cmb && d % 4 == 0 && d * 4 <= kSmemBudget &&
+                              ((reinterpret_cast<uintptr_t>(y_perm) | reinterpret_cast<uintptr_t>(cmb->h)) & 15) == 0;
+        if (fuse_cmb) fp.cmb = *cmb;
         // timing record: [start, end] of the one kernel, then an empty GEMM2 interval
         if (timing && record_event(s)) return BM_ECUDA;
         const int rc = launch_fused_dispatch(fp, nmat1, k1, k2, G, s);
@@ -178,7 +218,7 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
             g_timing.ev.push_back(nullptr);  // no second kernel: GEMM2 interval reported as 0
             g_timing.ev.push_back(nullptr);
         }
-        return BM_OK;
+        return fuse_cmb ? BM_OK : separate_combine();
     }
     if (timing && record_event(s)) return BM_ECUDA;
     if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
@@ -193,7 +233,7 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
         if (timing && record_event(s)) return BM_ECUDA;
         if (int rc = launch_gemm_dispatch(g2, G, s)) return rc;
         if (timing && record_event(s)) return BM_ECUDA;
-        return BM_OK;
+        return separate_combine();
     }
     const int fix_blocks = 4 * G;
     if (int rc = launch_fixup(g1, act == BM_ACT_SWIGLU ? 0 : 1, reinterpret_cast<uint4 *>(h_planes), (int)r_max,
@@ -203,7 +243,7 @@ extern "C" int bm_expert_ffn_bf16(const void *x_perm, const int32_t *expert_coun
     if (int rc = launch_gemm_dispatch(g2, G, s)) return rc;
     if (timing && record_event(s)) return BM_ECUDA;
     if (int rc = launch_fixup(g2, 2, nullptr, 0, y_perm, fix_blocks, s)) return rc;
-    return BM_OK;
+    return separate_combine();
 }
 
 extern "C" int bm_set_kernel_timing(int32_t enable) {

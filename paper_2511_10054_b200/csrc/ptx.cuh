@@ -20,6 +20,11 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
+// programmatic dependent launch: wait for the preceding kernel of the stream
+// (and its memory) / let the next kernel's launch begin
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));

@@ -295,6 +295,25 @@ def expert_ffn_bf16(x_perm_sw, perm: Permutation, w_arena, buf_of_expert, d: int
     return y_perm
 
 
+def expert_ffn_bf16_combine(x_perm_sw, perm: Permutation, w_arena, buf_of_expert, d: int, f: int, act: int,
+                            ws: FfnWorkspace, probs, kind, h, residual_scale: float = 0.5, y_perm=None):
+    """K4 + K5: the bf16 grouped FFN, then the gate-weighted combine and
+    layer_update in place on h [B][d] fp32 (model.py:334-347). At decode
+    widths one launch does both (bit-identical to expert_ffn_bf16 + combine)."""
+    E = perm.count.shape[0]
+    B, k = probs.shape
+    _cuda(x_perm_sw, "x_perm", torch.bfloat16)
+    _cuda(w_arena, "w_arena", torch.bfloat16)
+    _cuda(probs, "probs", torch.float32)
+    _cuda(h, "h", torch.float32)
+    if y_perm is None:
+        y_perm = torch.empty(perm.r_max, d, device=x_perm_sw.device, dtype=torch.float32)
+    N.call("bm_expert_ffn_bf16_combine", _p(x_perm_sw), _p(perm.count), _p(perm.offset), E, d, f, act, _p(w_arena),
+           w_arena.shape[0], _p(buf_of_expert), perm.r_max, ws.n_tile, _p(ws.buf), ws.nbytes, _p(y_perm),
+           _p(perm.slot_row), _p(probs), _p(kind), B, k, _p(h), float(residual_scale), _s())
+    return h
+
+
 def coact_count(topk, num_experts: int, counts=None, pairs=None, check: bool = True):
     """K6: accumulate binary co-activation counts (u64, stored in int64 tensors).
 

@@ -132,3 +132,35 @@ def test_engine_decisions_bit_exact_at_baseline_shapes(cuda_ok, name, layers, B)
     assert st["tokens"] == steps * B and np.isfinite(x.cpu().numpy()).all()
     eng.close()
     wl.close()
+
+
+def test_engine_fused_combine_equals_separate_launch():
+    """The engine's layer-step runs K5 inside its last fused FFN launch
+    (post1 when nothing is fetched, else post2); with BMOE_FUSE_COMBINE=0 it is
+    its own launch. Hidden states bitwise equal, event logs equal, one kernel
+    launch fewer per decode layer-step."""
+    import os
+    wl = W.build("qwen3", layers=3, max_batch=16, profile_tokens=1024)
+    outs, evs, launches = [], [], []
+    old = os.environ.get("BMOE_FUSE_COMBINE")
+    try:
+        for flag in ("0", "1"):
+            os.environ["BMOE_FUSE_COMBINE"] = flag
+            eng = wl.engine("buddy")
+            x = torch.from_numpy(wl.tokens(2, 64)).cuda()
+            for s in range(4):
+                eng.step(x[s * 16:(s + 1) * 16], np.arange(s * 16, (s + 1) * 16))
+            torch.cuda.synchronize()
+            outs.append(x.cpu().numpy())
+            evs.append(eng.events())
+            launches.append(eng.stats()["kernel_launches"])
+            eng.close()
+    finally:
+        if old is None:
+            os.environ.pop("BMOE_FUSE_COMBINE", None)
+        else:
+            os.environ["BMOE_FUSE_COMBINE"] = old
+        wl.close()
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    assert np.array_equal(evs[0], evs[1])
+    assert launches[0] - launches[1] == 3 * 4, launches

@@ -543,3 +543,29 @@ def test_multi_cta_permute_equals_single_cta(cuda_ok, B, k, E, drop):
     assert torch.equal(multi.count, single.count) and torch.equal(multi.offset, single.offset)
     assert torch.equal(multi.slot_row, single.slot_row)
     assert torch.equal(multi.row_token[:rows], single.row_token[:rows])
+
+
+@pytest.mark.parametrize("E,d,f,B,k,n_tile", [
+    (8, 4096, 14336, 16, 2, 16),   # Mixtral decode
+    (128, 2048, 768, 16, 8, 16),   # Qwen3 decode (k = 8 slots per token)
+    (64, 2048, 1408, 200, 6, 64),  # more tokens than CTAs: CTAs combine several tokens
+    (8, 512, 1024, 300, 2, 128),   # prefill width: GEMM kernels, then the separate combine
+])
+def test_ffn_combine_one_launch_equals_two(cuda_ok, E, d, f, B, k, n_tile):
+    """bm_expert_ffn_bf16_combine (north_star (c): the grouped FFN with the
+    gate-weighted combine fused) runs K5 + layer_update after a second grid
+    barrier of the fused decode launch, with combine_kernel's own code: h is
+    bitwise identical to expert_ffn_bf16 followed by combine(h_in=h), over
+    repeats (the barrier generations advance twice per launch)."""
+    seed = E * 7 + B
+    topk, kind, probs = _plan(np.random.default_rng(seed), B, E, k)
+    _, _, (xp, perm, arena, buf_of, ws) = _bf16_case(np.random.default_rng(seed), E, d, f, B, k, ops.ACT_SWIGLU,
+                                                     n_tile)
+    bo, pr, kd = _t(buf_of), _t(probs), _t(kind)
+    h0 = torch.randn(B, d, device=DEV, generator=torch.Generator(device=DEV).manual_seed(seed))
+    y = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)
+    ref = ops.combine(y, perm, pr, kd, h_in=h0.clone(), residual_scale=0.5)
+    for _ in range(10):
+        h = h0.clone()
+        ops.expert_ffn_bf16_combine(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws, pr, kd, h, 0.5)
+        assert torch.equal(h, ref)
