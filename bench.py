@@ -380,8 +380,10 @@ def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None, e
            "expert_weights": f"clustered synthetic, {clusters} clusters shared with the router, spread {SPREAD} "
                       f"(model.py:161-171 recipe; {clusters} = the reference's default model.clusters = 8 capped at E"
                       f"{'' if clusters == min(E, 8) else ', overridden by --clusters'}), bf16",
-           **({} if experts == "clustered" else {"expert_weights": "independent N(0, 1/fan_in) experts (round 1's "
-                                                                  "workload), router on min(E, 8) clusters, bf16"}),
+           **({} if experts == "clustered" else {"expert_weights": "independent N(0, 1/fan_in) experts, router on "
+                                                                  "min(E, 8) clusters (the reference's default "
+                                                                  "model.clusters = 8 = E: one expert per cluster), "
+                                                                  "bf16"}),
            "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
     if S:
         cfg["shared_experts"] = S
@@ -579,9 +581,12 @@ def main():
     ap.add_argument("--trace-tokens", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--codec", type=int, default=1, choices=[0, 1],
                     help="1: exponent-coded pinned mirrors (lossless, fewer PCIe bytes per miss); 0: raw bf16")
-    ap.add_argument("--experts", default="clustered", choices=["clustered", "independent"],
-                    help="expert weights: the reference's clustered recipe (default) or independent N(0, 1/fan_in) "
-                         "experts (round 1's workload; router on min(E, 8) clusters)")
+    ap.add_argument("--experts", default="auto", choices=["auto", "clustered", "independent"],
+                    help="expert weights: the reference's clustered recipe (base_c + 0.1 delta_e on the router's "
+                         "clusters) or independent N(0, 1/fan_in) experts (router on min(E, 8) clusters). auto: "
+                         "clustered when the cluster count is below E (Qwen3, DSV2: several experts per cluster); "
+                         "independent when every expert is its own cluster (Mixtral, E = 8 = the reference's default "
+                         "model.clusters), where the recipe has no shared structure")
     ap.add_argument("--weight-seed", type=int, default=0,
                     help="seed of the synthetic expert weights (the workload instance; tables are re-profiled)")
     ap.add_argument("--clusters", type=int, default=None,
@@ -590,6 +595,10 @@ def main():
     ap.add_argument("--cache-rate", type=float, default=None,
                     help="expert-cache budget as a fraction of the experts (default: the config's)")
     args = ap.parse_args()
+    if args.experts == "auto":
+        from paper_2511_10054_b200.synth import CLUSTERS
+        E_ = _shape(args.model)[0]
+        args.experts = "clustered" if (args.clusters or CLUSTERS[args.model]) < E_ else "independent"
     _config.weight_seed = args.weight_seed
     launch_or_check(args)
     ws, rank, local = _dist()

@@ -419,7 +419,8 @@ struct bm_engine {
                                       reinterpret_cast<const float *>(arena), buf_elems, bo_dev_l[l], r_max, h_ws,
                                       y_perm, s));
         } else if (fetched) {  // the last FFN call of the layer-step carries the combine
-            return ffn_bf16(l, h, B, late_only ? count_c : count_b, fuse_combine, s);
+            ENG_TRY(ffn_bf16(l, h, B, late_only ? count_c : count_b, fuse_combine, s));
+            if (fuse_combine) return BM_OK;
         } else if (fuse_combine) {
             return BM_OK;  // it ran with the resident experts' FFN (post1)
         }

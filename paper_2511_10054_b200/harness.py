@@ -374,7 +374,9 @@ def run_profile(cfg: dict, out_dir: str | None = None) -> ProfileResult:
     stats = [profiler.CoActivationStats(layer=l, num_experts=E, warmup_steps=c["stream.warmup_steps"],
                                         warmup_weight=c["profile.warmup_weight"],
                                         laplace_eps=c["profile.laplace_eps"]) for l in range(L)]
-    weighted = c["builder.mode"] == "weighted" or c["profile.warmup_weight"] != 0.0
+    # pair weights are always accumulated, like observe() does (profiler.py:81-95): the
+    # BSST files carry them whichever builder mode reads them later
+    weighted = True
     n, B = c["stream.num_tokens"], c["stream.batch"]
     x = substrate.token_stream(spec, c["stream.seed"], n)
     xd = torch.tensor(x, dtype=torch.float32, device=dev)
