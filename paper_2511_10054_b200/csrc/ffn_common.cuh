@@ -74,12 +74,14 @@ inline __device__ void build_sched_warp(Sched &s, const int32_t *count, const in
     constexpr int kPer = kMaxE / 32;
     const int lane = (int)lane_id();
     const int per = (E + 31) / 32;
-    int c[kPer];
+    int c[kPer], o[kPer];
     int nact = 0, nch = 0;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
+    for (int i = 0; i < kPer; ++i) {  // counts and offsets in one round of loads
         const int e = lane * per + i;
-        c[i] = (i < per && e < E) ? count[e] : 0;
+        const bool in = i < per && e < E;
+        c[i] = in ? count[e] : 0;
+        o[i] = in ? offset[e] : 0;
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i)
@@ -103,7 +105,7 @@ inline __device__ void build_sched_warp(Sched &s, const int32_t *count, const in
             const int e = lane * per + i, nc = chunks_of(c[i], n_tile);
             s.act_e[ia] = e;
             s.act_cnt[ia] = c[i];
-            s.act_off[ia] = offset[e];
+            s.act_off[ia] = o[i];
             s.act_nch[ia] = nc;
             s.chunk_prefix[ia] = ic;
             ic += nc;
@@ -239,7 +241,11 @@ struct FusedParams {
     GemmParams g[2];
     int *arrive;         // [2][tile_cap] split-tile arrival counters
     int tile_cap;
-    unsigned *grid_bar;  // [0] arrivals, [1] generation
+    // grid barrier: a monotonic 64-bit arrival count. Every launch's barriers take
+    // G arrivals each, so at a CTA's entry floor(count / G) * G is the base of this
+    // launch (no instance of this launch can complete before the CTA arrives), and
+    // barrier n of the launch has passed once the count reaches base + n * G.
+    unsigned long long *grid_bar;
     int prefetch_w2;     // stream W2's first stages before the barrier opens
     unsigned long long *trace;  // diagnostics (BMOE_FFN_TRACE): kTracePts globaltimer stamps per CTA, else null
     CombineArgs cmb;            // K5 after a second grid barrier, in the same launch

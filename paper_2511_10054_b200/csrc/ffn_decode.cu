@@ -38,8 +38,9 @@ struct Geom {
 
 template <int NMAT, int KPS>
 __device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &gm, int &stage, uint32_t &phase,
-                              long long it0, long long it1, int spt, uint64_t pol, const unsigned *gate,
-                              unsigned gen0, int prefetch, unsigned long long *gate_stamp = nullptr) {
+                              long long it0, long long it1, int spt, uint64_t pol,
+                              const unsigned long long *gate, unsigned long long gate_target, int prefetch,
+                              unsigned long long *gate_stamp = nullptr) {
     constexpr uint32_t kA = (uint32_t)(KPS * NMAT) * kATileBytes;
     const int mtiles = P.M / kBM;
     int cur = -1;
@@ -66,7 +67,7 @@ __device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &g
     };
     long long it = it0;
     if (gate && !prefetch) {
-        while (ptx::ld_acquire_gpu(gate) == gen0) __nanosleep(64);
+        while (ptx::ld_acquire_gpu_u64(gate) < gate_target) __nanosleep(32);
         if (gate_stamp) *gate_stamp = ptx::globaltimer();
         ptx::fence_proxy_async_global();
     } else if (gate) {
@@ -86,7 +87,7 @@ __device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &g
             }
         }
         // ... then the H parts once every CTA has finished phase 1
-        while (ptx::ld_acquire_gpu(gate) == gen0) __nanosleep(64);
+        while (ptx::ld_acquire_gpu_u64(gate) < gate_target) __nanosleep(32);
         if (gate_stamp) *gate_stamp = ptx::globaltimer();
         ptx::fence_proxy_async_global();
         int stg = stage0;
@@ -213,12 +214,29 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
 #pragma unroll
                     for (int j = 0; j < 16; ++j) u[j] = 0.f + o[j];
                 }
-                for (int c = cta + 1; c <= c1; ++c) {
-                    const float *src = P.partials + ((long long)tile + c) * slot_elems;
+                // the partials of kGrp contributors are loaded together (one L2 round trip),
+                // then added in CTA order: the sum is the same as one slot at a time
+                constexpr int kGrp = NMAT == 2 ? 2 : 4;
+                for (int c0 = cta + 1; c0 <= c1; c0 += kGrp) {
+                    float pg[kGrp][16], pu[kGrp][NMAT == 2 ? 16 : 1];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        g[j] += __ldcg(src + (long long)(cc + j) * kBM + m_local);
-                        if (NMAT == 2) u[j] += __ldcg(src + (long long)(P.n_tile + cc + j) * kBM + m_local);
+                    for (int x = 0; x < kGrp; ++x) {
+                        if (c0 + x > c1) break;
+                        const float *src = P.partials + ((long long)tile + c0 + x) * slot_elems;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            pg[x][j] = __ldcg(src + (long long)(cc + j) * kBM + m_local);
+                            if (NMAT == 2) pu[x][j] = __ldcg(src + (long long)(P.n_tile + cc + j) * kBM + m_local);
+                        }
+                    }
+#pragma unroll
+                    for (int x = 0; x < kGrp; ++x) {
+                        if (c0 + x > c1) break;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            g[j] += pg[x][j];
+                            if (NMAT == 2) u[j] += pu[x][j];
+                        }
                     }
                 }
                 finish16<NMAT>(P, ti, cc, q, lane, g, u);
@@ -267,10 +285,12 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     // what the preceding kernel writes before this wait
     if (fp.pdl && warp == 0) ptx::grid_dep_wait();
     if (warp == 0) build_sched_warp(sched, P1.count, P1.offset, P1.E, n_tile);
-    // the barrier generation cannot advance before this CTA arrives, so
-    // reading it here (before the __syncthreads) is race-free
-    unsigned gen0 = 0;
-    if (threadIdx.x == 0) gen0 = *reinterpret_cast<volatile unsigned *>(fp.grid_bar + 1);
+    // no barrier instance of this launch can complete before this CTA arrives,
+    // so the count read here rounds down to the launch's base (see FusedParams)
+    unsigned long long bar0 = 0;
+    if (threadIdx.x == 0)
+        bar0 = *reinterpret_cast<volatile unsigned long long *>(fp.grid_bar) / (unsigned long long)gridDim.x *
+               (unsigned long long)gridDim.x;
 
     constexpr uint32_t kA1 = (uint32_t)(KPS1 * NMAT1) * kATileBytes, kA2 = (uint32_t)KPS2 * kATileBytes;
     constexpr uint32_t kAmax = kA1 > kA2 ? kA1 : kA2;
@@ -320,7 +340,8 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         if (tr) tr[2] = ptx::globaltimer();
         if (cta < G2)
             fused_produce<1, KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2), range_start(cta + 1, T2, G2),
-                                   spt2, pol, fp.grid_bar + 1, gen0, fp.prefetch_w2, tr ? tr + 5 : nullptr);
+                                   spt2, pol, fp.grid_bar, bar0 + (unsigned long long)Gn, fp.prefetch_w2,
+                                   tr ? tr + 5 : nullptr);
     } else if (warp == 1 && lane == 0) {
         int stage = 0, acc = 0;
         uint32_t phase = 0, acc_phase = 0;
@@ -341,14 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         ptx::fence_proxy_async_global();
         __threadfence();
         ptx::named_bar_sync(1, 128);
-        if (q == 0 && lane == 0) {
-            const unsigned prev = atomicAdd(fp.grid_bar, 1u);
-            if (prev == (unsigned)Gn - 1u) {
-                fp.grid_bar[0] = 0u;
-                __threadfence();
-                atomicAdd(fp.grid_bar + 1, 1u);
-            }
-        }
+        if (q == 0 && lane == 0) atomicAdd(fp.grid_bar, 1ull);
         fused_epilogue<1>(P2, sched, gm, fp.arrive + fp.tile_cap, acc, acc_phase, T2, G2, cta, spt2, tmem_base, q,
                           lane);
         if (tr && q == 0 && lane == 0) tr[6] = ptx::globaltimer();
@@ -367,15 +381,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) {
-            const unsigned *gen = fp.grid_bar + 1;
-            while (ptx::ld_acquire_gpu(gen) == gen0) __nanosleep(64);  // barrier 1 done: its count is reset
-            const unsigned prev = atomicAdd(fp.grid_bar, 1u);
-            if (prev == (unsigned)Gn - 1u) {
-                fp.grid_bar[0] = 0u;
-                __threadfence();
-                atomicAdd(fp.grid_bar + 1, 1u);
-            }
-            while (ptx::ld_acquire_gpu(gen) - gen0 < 2u) __nanosleep(64);
+            // barrier 2 counts only after barrier 1 has completed, or a fast CTA's second
+            // arrival could stand in for a slow CTA's first
+            while (ptx::ld_acquire_gpu_u64(fp.grid_bar) < bar0 + (unsigned long long)Gn) __nanosleep(32);
+            atomicAdd(fp.grid_bar, 1ull);
+            while (ptx::ld_acquire_gpu_u64(fp.grid_bar) < bar0 + 2ull * (unsigned long long)Gn) __nanosleep(32);
         }
         __syncthreads();
         float *hbuf = reinterpret_cast<float *>(smem_raw);

@@ -63,7 +63,7 @@ namespace ffn {
 // workspace: [fp32 partial slots | bf16 SW128 H planes | split-tile arrival
 // counters (2 phases) + grid barrier]; the counters must start at zero.
 struct WsLayout {
-    long long partial_bytes, h_off, h_bytes, ctr_off, tile_cap, total;
+    long long partial_bytes, h_off, h_bytes, ctr_off, bar_off, tile_cap, total;
 };
 WsLayout ws_layout(long long E, long long d, long long f, long long r_max, long long n_tile) {
     WsLayout w;
@@ -74,7 +74,8 @@ WsLayout ws_layout(long long E, long long d, long long f, long long r_max, long 
     w.h_off = w.partial_bytes;
     w.h_bytes = (((f / 64) * r_max * 128 + 1023) / 1024) * 1024;
     w.ctr_off = w.h_off + w.h_bytes;
-    w.total = w.ctr_off + (2 * w.tile_cap + 2) * 4;
+    w.bar_off = ((w.ctr_off + 2 * w.tile_cap * 4 + 7) / 8) * 8;  // the 64-bit grid barrier count
+    w.total = w.bar_off + 8;
     return w;
 }
 }  // namespace ffn
@@ -201,7 +202,8 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         g1.dp = g2.dp = 0;
         int pre = 1;
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
-        FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap, reinterpret_cast<unsigned *>(counters + 2 * wl.tile_cap),
+        FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap,
+                       reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off),
                        pre, trace_buffer(G), CombineArgs{}, 0};
         static const int pdl = getenv("BMOE_PDL") ? atoi(getenv("BMOE_PDL")) : 0;
         fp.pdl = pdl;
