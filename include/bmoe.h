@@ -251,9 +251,11 @@ int bm_expert_ffn_bf16_combine(const void *x_perm, const int32_t *expert_count, 
                                const uint8_t *kind, int64_t B, int64_t k, float *h, float residual_scale,
                                bm_stream_t stream);
 /* Diagnostics: with BMOE_FFN_TRACE=1 in the environment the fused decode FFN
- * records 8 globaltimer stamps (ns) per CTA of its last call (entry, setup,
- * GEMM1 loads issued, GEMM1 MMAs committed, GEMM1 epilogue done, barrier seen,
- * GEMM2 epilogue done, exit); copies up to cap of them, returns the count. */
+ * records 12 globaltimer stamps (ns) per CTA of its last call (entry, setup,
+ * GEMM1 loads issued, GEMM1 MMAs committed, GEMM1 epilogue done, H ready /
+ * barrier seen, GEMM2 epilogue done, exit, last GEMM1 accumulator ready, last
+ * split-tile arrival seen, first GEMM2 stage landed, GEMM2 MMAs committed);
+ * copies up to cap of them, returns the count. */
 int64_t bm_ffn_trace_read(uint64_t *out_host, int64_t cap);
 /* Kernel timing for the bench's roofline: after bm_set_kernel_timing(1)
  * every bm_expert_ffn_bf16 call records CUDA events on its stream around its

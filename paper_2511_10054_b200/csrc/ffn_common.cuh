@@ -122,6 +122,7 @@ __device__ __forceinline__ int total_tiles(const Sched &s, int mtiles) { return 
 struct TileInfo {
     int e, mtile, chunk, n;  // n = columns (tokens, padded to 16) of this tile
     int row0;                // first permuted row of the chunk
+    int nch;                 // token chunks of expert e
 };
 
 __device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int mtiles, int n_tile) {
@@ -134,6 +135,7 @@ __device__ __forceinline__ TileInfo decode_tile(const Sched &s, int t, int mtile
     ti.e = s.act_e[lo];
     const int local = t - s.chunk_prefix[lo] * mtiles;
     const int nch = s.act_nch[lo];
+    ti.nch = nch;
     ti.mtile = local / nch;
     ti.chunk = local % nch;
     const int npad = (s.act_cnt[lo] + 15) & ~15;
@@ -250,8 +252,13 @@ struct FusedParams {
     unsigned long long *trace;  // diagnostics (BMOE_FFN_TRACE): kTracePts globaltimer stamps per CTA, else null
     CombineArgs cmb;            // K5 after a second grid barrier, in the same launch
     int pdl;                    // launched with programmatic stream serialization (griddepcontrol.wait first)
+    // per-expert H readiness (null: GEMM2 waits for the whole of GEMM1 at the grid barrier):
+    // h_ready[e] counts expert e's finished GEMM1 tiles; a GEMM2 stage of expert e loads its
+    // H part once all mtiles1 * nch(e) of them are in. The last CTA to leave resets them.
+    int *h_ready;
+    unsigned long long *exit_count;  // monotonic, G per launch
 };
-constexpr int kTracePts = 8;
+constexpr int kTracePts = 12;
 
 // CTA that processes stream-K iteration i of T over G CTAs
 __device__ __forceinline__ int cta_of(long long i, long long T, int G) {

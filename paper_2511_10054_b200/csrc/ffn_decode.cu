@@ -114,9 +114,96 @@ __device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &g
     }
 }
 
+// GEMM2 producer under per-expert H readiness: the A part (W2, independent of
+// H) of up to `stages` iterations is issued ahead while the next stage's expert
+// is not ready yet; a stage's H part goes out once h_ready[e] is complete.
+template <int KPS>
+__device__ void fused_produce_ready(const GemmParams &P, const Sched &s, const Geom &gm, int &stage, uint32_t &phase,
+                                    long long it0, long long it1, int spt, uint64_t pol, const int *h_ready,
+                                    int mtiles1, unsigned long long *gate_stamp) {
+    constexpr uint32_t kA = (uint32_t)KPS * kATileBytes;
+    const int mtiles = P.M / kBM;
+    auto tile_of = [&](long long it, int &st, TileInfo &ti) {
+        const int tile = (int)(it / spt);
+        st = (int)(it - (long long)tile * spt);
+        ti = decode_tile(s, tile, mtiles, P.n_tile);
+    };
+    auto a_src = [&](const TileInfo &ti, int st) {
+        return P.arena + (long long)P.buf_of_expert[ti.e] * P.buf_bytes + P.mat_off +
+               (long long)ti.mtile * spt * kA + (long long)st * kA;
+    };
+    auto issue_b = [&](int stg, int st, const TileInfo &ti) {
+        const uint32_t sB = gm.base + (uint32_t)stg * gm.stage_bytes + gm.b_off;
+        const uint32_t fb = gm.full0 + 8 * stg;
+        const uint8_t *b_tile = P.b_planes + (long long)ti.row0 * 128;
+#pragma unroll
+        for (int i = 0; i < KPS; ++i)
+            ptx::bulk_load(sB + i * gm.bsz, b_tile + (long long)(st * KPS + i) * P.b_plane_bytes,
+                           (uint32_t)ti.n * 128u, fb);
+    };
+    long long ia = it0, ib = it0;  // next iteration whose A part / H part is issued
+    int stage_a = stage;
+    uint32_t phase_a = phase;
+    int ready_e = -1;
+    bool stamped = false;
+    while (ib < it1) {
+        int st;
+        TileInfo ti;
+        tile_of(ib, st, ti);
+        const int need = mtiles1 * ti.nch;
+        bool rdy = ti.e == ready_e || ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(h_ready + ti.e)) >=
+                                          (unsigned)need;
+        if (!rdy && ia < it1 && ia - ib < gm.stages) {  // stream W2 ahead meanwhile
+            int sta;
+            TileInfo tia;
+            tile_of(ia, sta, tia);
+            ptx::mbar_wait(gm.empty0 + 8 * stage_a, phase_a ^ 1u);
+            const uint32_t fb = gm.full0 + 8 * stage_a;
+            ptx::mbar_expect_tx_only(fb, kA);
+            ptx::bulk_load_hint(gm.base + (uint32_t)stage_a * gm.stage_bytes, a_src(tia, sta), kA, fb, pol);
+            if (++stage_a == gm.stages) {
+                stage_a = 0;
+                phase_a ^= 1u;
+            }
+            ++ia;
+            continue;
+        }
+        while (!rdy) {
+            __nanosleep(32);
+            rdy = ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(h_ready + ti.e)) >= (unsigned)need;
+        }
+        if (ti.e != ready_e) ptx::fence_proxy_async_global();  // H (generic writes) -> bulk-copy reads
+        ready_e = ti.e;
+        if (gate_stamp && !stamped) {
+            *gate_stamp = ptx::globaltimer();
+            stamped = true;
+        }
+        const uint32_t fb = gm.full0 + 8 * stage;
+        if (ia == ib) {  // A part not issued ahead: both parts now
+            ptx::mbar_wait(gm.empty0 + 8 * stage, phase ^ 1u);
+            ptx::mbar_expect_tx(fb, kA + (uint32_t)KPS * (uint32_t)ti.n * 128u);
+            ptx::bulk_load_hint(gm.base + (uint32_t)stage * gm.stage_bytes, a_src(ti, st), kA, fb, pol);
+            if (++stage_a == gm.stages) {
+                stage_a = 0;
+                phase_a ^= 1u;
+            }
+            ++ia;
+        } else {
+            ptx::mbar_expect_tx(fb, (uint32_t)KPS * (uint32_t)ti.n * 128u);  // the stage's arrive
+        }
+        issue_b(stage, st, ti);
+        if (++stage == gm.stages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+        ++ib;
+    }
+}
+
 template <int NMAT, int KPS>
 __device__ void fused_mma(const GemmParams &P, const Sched &s, const Geom &gm, int &stage, uint32_t &phase, int &acc,
-                          uint32_t &acc_phase, long long it0, long long it1, int spt, uint32_t tmem_base) {
+                          uint32_t &acc_phase, long long it0, long long it1, int spt, uint32_t tmem_base,
+                          unsigned long long *first_full = nullptr) {
     const int mtiles = P.M / kBM;
     const uint64_t desc0 = ptx::sw128_desc(gm.base);
     const uint64_t stage_d = gm.stage_bytes >> 4, bsz_d = gm.bsz >> 4, boff_d = gm.b_off >> 4;
@@ -134,6 +221,10 @@ __device__ void fused_mma(const GemmParams &P, const Sched &s, const Geom &gm, i
         for (int st = (int)(it - (long long)tile * spt); st < st_end; ++st, ++it) {
             ptx::mbar_wait(gm.full0 + 8 * stage, phase);
             ptx::tc_fence_after();
+            if (first_full) {
+                *first_full = ptx::globaltimer();
+                first_full = nullptr;
+            }
             const uint64_t a = desc0 + (uint64_t)stage * stage_d;
             const uint64_t b = a + boff_d;
 #pragma unroll
@@ -172,7 +263,7 @@ __device__ void fused_mma(const GemmParams &P, const Sched &s, const Geom &gm, i
 template <int NMAT>
 __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &gm, int *arrive, int &acc,
                                uint32_t &acc_phase, long long T, int G, int cta, int spt, uint32_t tmem_base, int q,
-                               unsigned lane) {
+                               unsigned lane, int *h_ready = nullptr, unsigned long long *tr = nullptr) {
     if (cta >= G) return;
     const int mtiles = P.M / kBM;
     const long long it0 = range_start(cta, T, G), it1 = range_start(cta + 1, T, G);
@@ -188,6 +279,7 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
         const TileInfo ti = decode_tile(s, tile, mtiles, P.n_tile);
         ptx::mbar_wait(gm.tfull0 + 8 * acc, acc_phase);
         ptx::tc_fence_after();
+        if (tr && m_local == 0) tr[8] = ptx::globaltimer();  // last accumulator ready
         const uint32_t tbase = tmem_base + (uint32_t)acc * 256u + ((uint32_t)(q * 32) << 16);
         if (whole) {
             for (int c0 = 0; c0 < ti.n; c0 += 16) {
@@ -202,6 +294,7 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
                 while (ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(arrive + tile)) < (unsigned)(c1 - cta))
                     __nanosleep(32);
                 arrive[tile] = 0;  // every contributor has arrived: reset for the next launch
+                if (tr) tr[9] = ptx::globaltimer();
             }
             ptx::named_bar_sync(1, 128);
             for (int cc = 0; cc < ti.n; cc += 16) {
@@ -257,6 +350,12 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
         if (lane == 0) ptx::mbar_arrive(gm.tempty0 + 8 * acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1u;
+        if (h_ready && (whole || reducer)) {  // this tile's H rows are written: publish them
+            ptx::fence_proxy_async_global();
+            __threadfence();
+            ptx::named_bar_sync(1, 128);
+            if (m_local == 0) atomicAdd(h_ready + ti.e, 1);
+        }
         if (!whole && !reducer) {  // publish the partial, then arrive
             __threadfence();
             ptx::named_bar_sync(1, 128);
@@ -284,13 +383,13 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     // launched with programmatic stream serialization (fp.pdl): nothing below reads
     // what the preceding kernel writes before this wait
     if (fp.pdl && warp == 0) ptx::grid_dep_wait();
-    if (warp == 0) build_sched_warp(sched, P1.count, P1.offset, P1.E, n_tile);
     // no barrier instance of this launch can complete before this CTA arrives,
-    // so the count read here rounds down to the launch's base (see FusedParams)
+    // so the count read here rounds down to the launch's base (see FusedParams);
+    // issued ahead of the schedule's loads so the two round trips overlap
     unsigned long long bar0 = 0;
-    if (threadIdx.x == 0)
-        bar0 = *reinterpret_cast<volatile unsigned long long *>(fp.grid_bar) / (unsigned long long)gridDim.x *
-               (unsigned long long)gridDim.x;
+    if (threadIdx.x == 0) bar0 = *reinterpret_cast<volatile unsigned long long *>(fp.grid_bar);
+    if (warp == 0) build_sched_warp(sched, P1.count, P1.offset, P1.E, n_tile);
+    if (threadIdx.x == 0) bar0 = bar0 / (unsigned long long)gridDim.x * (unsigned long long)gridDim.x;
 
     constexpr uint32_t kA1 = (uint32_t)(KPS1 * NMAT1) * kATileBytes, kA2 = (uint32_t)KPS2 * kATileBytes;
     constexpr uint32_t kAmax = kA1 > kA2 ? kA1 : kA2;
@@ -338,10 +437,16 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
             fused_produce<NMAT1, KPS1>(P1, sched, gm, stage, phase, range_start(cta, T1, G1),
                                        range_start(cta + 1, T1, G1), spt1, pol, nullptr, 0, 0);
         if (tr) tr[2] = ptx::globaltimer();
-        if (cta < G2)
-            fused_produce<1, KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2), range_start(cta + 1, T2, G2),
-                                   spt2, pol, fp.grid_bar, bar0 + (unsigned long long)Gn, fp.prefetch_w2,
-                                   tr ? tr + 5 : nullptr);
+        if (cta < G2) {
+            if (fp.h_ready)
+                fused_produce_ready<KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2),
+                                          range_start(cta + 1, T2, G2), spt2, pol, fp.h_ready, P1.M / kBM,
+                                          tr ? tr + 5 : nullptr);
+            else
+                fused_produce<1, KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2),
+                                       range_start(cta + 1, T2, G2), spt2, pol, fp.grid_bar,
+                                       bar0 + (unsigned long long)Gn, fp.prefetch_w2, tr ? tr + 5 : nullptr);
+        }
     } else if (warp == 1 && lane == 0) {
         int stage = 0, acc = 0;
         uint32_t phase = 0, acc_phase = 0;
@@ -351,12 +456,14 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         if (tr) tr[3] = ptx::globaltimer();
         if (cta < G2)
             fused_mma<1, KPS2>(P2, sched, gm, stage, phase, acc, acc_phase, range_start(cta, T2, G2),
-                               range_start(cta + 1, T2, G2), spt2, tmem_base);
+                               range_start(cta + 1, T2, G2), spt2, tmem_base, tr ? tr + 10 : nullptr);
+        if (tr) tr[11] = ptx::globaltimer();
     } else if (warp >= 4) {
         const int q = warp - 4;
         int acc = 0;
         uint32_t acc_phase = 0;
-        fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, T1, G1, cta, spt1, tmem_base, q, lane);
+        fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, T1, G1, cta, spt1, tmem_base, q, lane,
+                              fp.h_ready, tr);
         // H of this CTA is written: publish it (to the bulk-copy proxy too) and arrive
         if (tr && q == 0 && lane == 0) tr[4] = ptx::globaltimer();
         ptx::fence_proxy_async_global();
@@ -372,6 +479,15 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
+    if (fp.h_ready && threadIdx.x == 0) {
+        // every read of h_ready in this CTA is done; the last CTA out resets them for the next launch
+        __threadfence();  // this CTA's h_ready updates (other threads, ordered by the barrier above) first
+        const unsigned long long prev = atomicAdd(fp.exit_count, 1ull);
+        if ((prev + 1ull) % (unsigned long long)Gn == 0ull) {
+            __threadfence();
+            for (int e = 0; e < P1.E; ++e) fp.h_ready[e] = 0;
+        }
+    }
     if (fp.cmb.B > 0) {
         // K5 (gate-weighted combine + layer_update, in place on h) once every
         // CTA's y tiles are written: a second grid barrier, then token b on CTA

@@ -75,7 +75,7 @@ WsLayout ws_layout(long long E, long long d, long long f, long long r_max, long 
     w.h_bytes = (((f / 64) * r_max * 128 + 1023) / 1024) * 1024;
     w.ctr_off = w.h_off + w.h_bytes;
     w.bar_off = ((w.ctr_off + 2 * w.tile_cap * 4 + 7) / 8) * 8;  // the 64-bit grid barrier count
-    w.total = w.bar_off + 8;
+    w.total = w.bar_off + 16 + kMaxE * 4;  // [grid barrier | exit count | h_ready[kMaxE]]
     return w;
 }
 }  // namespace ffn
@@ -88,14 +88,14 @@ using namespace bm::ffn;
 // decode kernel's phases (ffn_decode.cu), overwritten by every fused call.
 static unsigned long long *g_trace = nullptr;
 static int g_trace_ctas = 0;
-static unsigned long long *trace_buffer(int G) {
+static unsigned long long *trace_buffer(int G, cudaStream_t s) {
     static const bool on = getenv("BMOE_FFN_TRACE") && atoi(getenv("BMOE_FFN_TRACE")) != 0;
     if (!on) return nullptr;
     if (!g_trace) {
         if (cudaMalloc(&g_trace, (size_t)G * kTracePts * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
-        cudaMemset(g_trace, 0, (size_t)G * kTracePts * sizeof(unsigned long long));
         g_trace_ctas = G;
     }
+    cudaMemsetAsync(g_trace, 0, (size_t)G * kTracePts * sizeof(unsigned long long), s);  // unset stamps read 0
     return g_trace;
 }
 
@@ -204,7 +204,12 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap,
                        reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off),
-                       pre, trace_buffer(G), CombineArgs{}, 0};
+                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr};
+        static const int h_ready = getenv("BMOE_H_READY") ? atoi(getenv("BMOE_H_READY")) : 1;
+        if (h_ready) {
+            fp.exit_count = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off + 8);
+            fp.h_ready = reinterpret_cast<int *>(static_cast<uint8_t *>(workspace) + wl.bar_off + 16);
+        }
         static const int pdl = getenv("BMOE_PDL") ? atoi(getenv("BMOE_PDL")) : 0;
         fp.pdl = pdl;
         // the combine joins the launch when bm_combine would take its 16-byte vector path (same code then)

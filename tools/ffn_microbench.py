@@ -107,19 +107,20 @@ def main():
            "gemm1_frac": (b1 + (b2 if g2 == 0 else 0)) / g1 / 1e6 / peak, "gemm2_frac": b2 / g2 / 1e6 / peak if g2 else None,
            "env": {k: v for k, v in os.environ.items() if k.startswith("BMOE_")}}
     if args.trace:
-        names = ["entry", "setup", "g1_loads_issued", "g1_mma_done", "g1_epi_done", "barrier_seen", "g2_epi_done",
-                 "exit"]
+        names = ["entry", "setup", "g1_loads_issued", "g1_mma_done", "g1_epi_done", "h_ready_seen", "g2_epi_done",
+                 "exit", "g1_last_acc_ready", "g1_split_arrivals_seen", "g2_first_stage", "g2_mma_done"]
+        NP = len(names)
         G = torch.cuda.get_device_properties(0).multi_processor_count
         rows = []
         for i in range(20):
             graphs[i % len(graphs)].replay()
             torch.cuda.synchronize()
-            st = np.zeros(G * 8, np.uint64)
+            st = np.zeros(G * NP, np.uint64)
             n = int(N.lib().bm_ffn_trace_read(st.ctypes.data, st.size))
-            st = st[:n].reshape(-1, 8).astype(np.float64)
+            st = st[:n].reshape(-1, NP).astype(np.float64)
             t0 = st[:, 0].min()
             rel = np.where(st > 0, (st - t0) / 1000.0, np.nan)
-            rows.append([[np.nanmin(rel[:, j]), np.nanmedian(rel[:, j]), np.nanmax(rel[:, j])] for j in range(8)])
+            rows.append([[np.nanmin(rel[:, j]), np.nanmedian(rel[:, j]), np.nanmax(rel[:, j])] for j in range(NP)])
         med = np.median(np.array(rows), axis=0)
         out["trace_us"] = {nm: {"min": round(float(a), 2), "med": round(float(b), 2), "max": round(float(c), 2)}
                            for nm, (a, b, c) in zip(names, med)}
