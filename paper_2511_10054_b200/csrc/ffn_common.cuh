@@ -253,10 +253,12 @@ struct FusedParams {
     CombineArgs cmb;            // K5 after a second grid barrier, in the same launch
     int pdl;                    // launched with programmatic stream serialization (griddepcontrol.wait first)
     // per-expert H readiness (null: GEMM2 waits for the whole of GEMM1 at the grid barrier):
-    // h_ready[e] counts expert e's finished GEMM1 tiles; a GEMM2 stage of expert e loads its
-    // H part once all mtiles1 * nch(e) of them are in. The last CTA to leave resets them.
+    // h_ready[p][e] counts expert e's finished GEMM1 tiles; a GEMM2 stage of expert e loads its
+    // H part once all mtiles1 * nch(e) of them are in. Two arrays alternate by launch parity
+    // (launch n = floor(launch_count / G), every CTA adds 1 on exit, fire and forget): launch
+    // n counts in h_ready[n & 1] and clears h_ready[(n + 1) & 1], which launch n - 1 used.
     int *h_ready;
-    unsigned long long *exit_count;  // monotonic, G per launch
+    unsigned long long *launch_count;
 };
 constexpr int kTracePts = 12;
 

@@ -123,24 +123,25 @@ __device__ void fused_produce_ready(const GemmParams &P, const Sched &s, const G
                                     int mtiles1, unsigned long long *gate_stamp) {
     constexpr uint32_t kA = (uint32_t)KPS * kATileBytes;
     const int mtiles = P.M / kBM;
-    auto tile_of = [&](long long it, int &st, TileInfo &ti) {
+    struct Cur {  // one cursor's tile cache (the tile decode and buffer lookup once per tile)
+        int tile = -1, e = 0, need = 0;
+        const uint8_t *a = nullptr, *b = nullptr;
+        uint32_t bbytes = 0;
+    };
+    auto locate = [&](Cur &c, long long it, int &st) {
         const int tile = (int)(it / spt);
         st = (int)(it - (long long)tile * spt);
-        ti = decode_tile(s, tile, mtiles, P.n_tile);
+        if (tile != c.tile) {
+            c.tile = tile;
+            const TileInfo ti = decode_tile(s, tile, mtiles, P.n_tile);
+            c.e = ti.e;
+            c.need = mtiles1 * ti.nch;
+            c.a = P.arena + (long long)P.buf_of_expert[ti.e] * P.buf_bytes + P.mat_off + (long long)ti.mtile * spt * kA;
+            c.b = P.b_planes + (long long)ti.row0 * 128;
+            c.bbytes = (uint32_t)ti.n * 128u;
+        }
     };
-    auto a_src = [&](const TileInfo &ti, int st) {
-        return P.arena + (long long)P.buf_of_expert[ti.e] * P.buf_bytes + P.mat_off +
-               (long long)ti.mtile * spt * kA + (long long)st * kA;
-    };
-    auto issue_b = [&](int stg, int st, const TileInfo &ti) {
-        const uint32_t sB = gm.base + (uint32_t)stg * gm.stage_bytes + gm.b_off;
-        const uint32_t fb = gm.full0 + 8 * stg;
-        const uint8_t *b_tile = P.b_planes + (long long)ti.row0 * 128;
-#pragma unroll
-        for (int i = 0; i < KPS; ++i)
-            ptx::bulk_load(sB + i * gm.bsz, b_tile + (long long)(st * KPS + i) * P.b_plane_bytes,
-                           (uint32_t)ti.n * 128u, fb);
-    };
+    Cur ca, cb;
     long long ia = it0, ib = it0;  // next iteration whose A part / H part is issued
     int stage_a = stage;
     uint32_t phase_a = phase;
@@ -148,19 +149,16 @@ __device__ void fused_produce_ready(const GemmParams &P, const Sched &s, const G
     bool stamped = false;
     while (ib < it1) {
         int st;
-        TileInfo ti;
-        tile_of(ib, st, ti);
-        const int need = mtiles1 * ti.nch;
-        bool rdy = ti.e == ready_e || ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(h_ready + ti.e)) >=
-                                          (unsigned)need;
+        locate(cb, ib, st);
+        bool rdy = cb.e == ready_e ||
+                   ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(h_ready + cb.e)) >= (unsigned)cb.need;
         if (!rdy && ia < it1 && ia - ib < gm.stages) {  // stream W2 ahead meanwhile
             int sta;
-            TileInfo tia;
-            tile_of(ia, sta, tia);
+            locate(ca, ia, sta);
             ptx::mbar_wait(gm.empty0 + 8 * stage_a, phase_a ^ 1u);
             const uint32_t fb = gm.full0 + 8 * stage_a;
             ptx::mbar_expect_tx_only(fb, kA);
-            ptx::bulk_load_hint(gm.base + (uint32_t)stage_a * gm.stage_bytes, a_src(tia, sta), kA, fb, pol);
+            ptx::bulk_load_hint(gm.base + (uint32_t)stage_a * gm.stage_bytes, ca.a + (long long)sta * kA, kA, fb, pol);
             if (++stage_a == gm.stages) {
                 stage_a = 0;
                 phase_a ^= 1u;
@@ -170,10 +168,10 @@ __device__ void fused_produce_ready(const GemmParams &P, const Sched &s, const G
         }
         while (!rdy) {
             __nanosleep(32);
-            rdy = ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(h_ready + ti.e)) >= (unsigned)need;
+            rdy = ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(h_ready + cb.e)) >= (unsigned)cb.need;
         }
-        if (ti.e != ready_e) ptx::fence_proxy_async_global();  // H (generic writes) -> bulk-copy reads
-        ready_e = ti.e;
+        if (cb.e != ready_e) ptx::fence_proxy_async_global();  // H (generic writes) -> bulk-copy reads
+        ready_e = cb.e;
         if (gate_stamp && !stamped) {
             *gate_stamp = ptx::globaltimer();
             stamped = true;
@@ -181,17 +179,20 @@ __device__ void fused_produce_ready(const GemmParams &P, const Sched &s, const G
         const uint32_t fb = gm.full0 + 8 * stage;
         if (ia == ib) {  // A part not issued ahead: both parts now
             ptx::mbar_wait(gm.empty0 + 8 * stage, phase ^ 1u);
-            ptx::mbar_expect_tx(fb, kA + (uint32_t)KPS * (uint32_t)ti.n * 128u);
-            ptx::bulk_load_hint(gm.base + (uint32_t)stage * gm.stage_bytes, a_src(ti, st), kA, fb, pol);
+            ptx::mbar_expect_tx(fb, kA + (uint32_t)KPS * cb.bbytes);
+            ptx::bulk_load_hint(gm.base + (uint32_t)stage * gm.stage_bytes, cb.a + (long long)st * kA, kA, fb, pol);
             if (++stage_a == gm.stages) {
                 stage_a = 0;
                 phase_a ^= 1u;
             }
             ++ia;
         } else {
-            ptx::mbar_expect_tx(fb, (uint32_t)KPS * (uint32_t)ti.n * 128u);  // the stage's arrive
+            ptx::mbar_expect_tx(fb, (uint32_t)KPS * cb.bbytes);  // the stage's arrive
         }
-        issue_b(stage, st, ti);
+        const uint32_t sB = gm.base + (uint32_t)stage * gm.stage_bytes + gm.b_off;
+#pragma unroll
+        for (int i = 0; i < KPS; ++i)
+            ptx::bulk_load(sB + i * gm.bsz, cb.b + (long long)(st * KPS + i) * P.b_plane_bytes, cb.bbytes, fb);
         if (++stage == gm.stages) {
             stage = 0;
             phase ^= 1u;
@@ -390,6 +391,16 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     if (threadIdx.x == 0) bar0 = *reinterpret_cast<volatile unsigned long long *>(fp.grid_bar);
     if (warp == 0) build_sched_warp(sched, P1.count, P1.offset, P1.E, n_tile);
     if (threadIdx.x == 0) bar0 = bar0 / (unsigned long long)gridDim.x * (unsigned long long)gridDim.x;
+    // per-expert H readiness: this launch's counter array (see FusedParams)
+    __shared__ int *h_ready_sh;
+    if (fp.h_ready && threadIdx.x == 32) {  // warp 1 lane 0 (warp 0 builds the schedule)
+        if (fp.pdl) ptx::grid_dep_wait();
+        const unsigned long long n = *reinterpret_cast<volatile unsigned long long *>(fp.launch_count) /
+                                     (unsigned long long)gridDim.x;
+        h_ready_sh = fp.h_ready + (n & 1ull) * kMaxE;
+        if (blockIdx.x == 0)  // the array launch n - 1 used is next launch's: clear it
+            for (int e = 0; e < P1.E; ++e) fp.h_ready[((n + 1ull) & 1ull) * kMaxE + e] = 0;
+    }
 
     constexpr uint32_t kA1 = (uint32_t)(KPS1 * NMAT1) * kATileBytes, kA2 = (uint32_t)KPS2 * kATileBytes;
     constexpr uint32_t kAmax = kA1 > kA2 ? kA1 : kA2;
@@ -421,6 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = tmem_base_sh;
+    int *const h_ready = fp.h_ready ? h_ready_sh : nullptr;
     if (tr && threadIdx.x == 0) tr[1] = ptx::globaltimer();
 
     const int cta = blockIdx.x, Gn = gridDim.x;
@@ -438,9 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
                                        range_start(cta + 1, T1, G1), spt1, pol, nullptr, 0, 0);
         if (tr) tr[2] = ptx::globaltimer();
         if (cta < G2) {
-            if (fp.h_ready)
+            if (h_ready)
                 fused_produce_ready<KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2),
-                                          range_start(cta + 1, T2, G2), spt2, pol, fp.h_ready, P1.M / kBM,
+                                          range_start(cta + 1, T2, G2), spt2, pol, h_ready, P1.M / kBM,
                                           tr ? tr + 5 : nullptr);
             else
                 fused_produce<1, KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2),
@@ -463,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         int acc = 0;
         uint32_t acc_phase = 0;
         fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, T1, G1, cta, spt1, tmem_base, q, lane,
-                              fp.h_ready, tr);
+                              h_ready, tr);
         // H of this CTA is written: publish it (to the bulk-copy proxy too) and arrive
         if (tr && q == 0 && lane == 0) tr[4] = ptx::globaltimer();
         ptx::fence_proxy_async_global();
@@ -479,15 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
-    if (fp.h_ready && threadIdx.x == 0) {
-        // every read of h_ready in this CTA is done; the last CTA out resets them for the next launch
-        __threadfence();  // this CTA's h_ready updates (other threads, ordered by the barrier above) first
-        const unsigned long long prev = atomicAdd(fp.exit_count, 1ull);
-        if ((prev + 1ull) % (unsigned long long)Gn == 0ull) {
-            __threadfence();
-            for (int e = 0; e < P1.E; ++e) fp.h_ready[e] = 0;
-        }
-    }
+    if (fp.h_ready && threadIdx.x == 0) atomicAdd(fp.launch_count, 1ull);  // result unused: a reduction
     if (fp.cmb.B > 0) {
         // K5 (gate-weighted combine + layer_update, in place on h) once every
         // CTA's y tiles are written: a second grid barrier, then token b on CTA

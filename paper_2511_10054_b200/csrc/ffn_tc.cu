@@ -63,19 +63,22 @@ namespace ffn {
 // workspace: [fp32 partial slots | bf16 SW128 H planes | split-tile arrival
 // counters (2 phases) + grid barrier]; the counters must start at zero.
 struct WsLayout {
-    long long partial_bytes, h_off, h_bytes, ctr_off, bar_off, tile_cap, total;
+    long long slot_set_bytes, partial_bytes, h_off, h_bytes, ctr_off, bar_off, tile_cap, total;
 };
 WsLayout ws_layout(long long E, long long d, long long f, long long r_max, long long n_tile) {
     WsLayout w;
     const long long M = std::max(d, f);
     w.tile_cap = max_tiles(E, M, r_max, n_tile);
     const long long slots = w.tile_cap + sm_count() + 1;
-    w.partial_bytes = ((slots * 2 * n_tile * kBM * 4 + 1023) / 1024) * 1024;
+    // two slot sets: the fused decode kernel's GEMM2 may run while GEMM1 split tiles are still
+    // being reduced (per-expert H readiness), so each GEMM has its own
+    w.slot_set_bytes = ((slots * 2 * n_tile * kBM * 4 + 1023) / 1024) * 1024;
+    w.partial_bytes = 2 * w.slot_set_bytes;
     w.h_off = w.partial_bytes;
     w.h_bytes = (((f / 64) * r_max * 128 + 1023) / 1024) * 1024;
     w.ctr_off = w.h_off + w.h_bytes;
     w.bar_off = ((w.ctr_off + 2 * w.tile_cap * 4 + 7) / 8) * 8;  // the 64-bit grid barrier count
-    w.total = w.bar_off + 16 + kMaxE * 4;  // [grid barrier | exit count | h_ready[kMaxE]]
+    w.total = w.bar_off + 16 + 2 * kMaxE * 4;  // [grid barrier | launch count | h_ready[2][kMaxE]]
     return w;
 }
 }  // namespace ffn
@@ -206,8 +209,9 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
                        reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off),
                        pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr};
         static const int h_ready = getenv("BMOE_H_READY") ? atoi(getenv("BMOE_H_READY")) : 1;
+        fp.g[1].partials = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + wl.slot_set_bytes);
         if (h_ready) {
-            fp.exit_count = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off + 8);
+            fp.launch_count = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off + 8);
             fp.h_ready = reinterpret_cast<int *>(static_cast<uint8_t *>(workspace) + wl.bar_off + 16);
         }
         static const int pdl = getenv("BMOE_PDL") ? atoi(getenv("BMOE_PDL")) : 0;
