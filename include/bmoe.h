@@ -513,6 +513,12 @@ int bm_xfer_decode(const uint8_t *blob, uint16_t *dst, int64_t n_values, bm_stre
 /* Decode one piece (device copy, 256-byte aligned) of n_chunks chunks into
  * dst (the piece's first value). */
 int bm_xfer_decode_piece(const uint8_t *piece, uint16_t *dst, int64_t n_chunks, bm_stream_t stream);
+/* The same on at most max_ctas CTAs (0: the full grid). The engine decodes the
+ * pieces that are not on its critical path (all but an expert's last) on a
+ * narrow grid, so they stream alongside the copies instead of taking HBM and
+ * issue slots from the FFN running at the same time. */
+int bm_xfer_decode_piece_ctas(const uint8_t *piece, uint16_t *dst, int64_t n_chunks, int32_t max_ctas,
+                              bm_stream_t stream);
 
 /* Pinned host allocation of exact size (cudaHostAlloc, portable). */
 int bm_host_alloc(int64_t bytes, void **out);

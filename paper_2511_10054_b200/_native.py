@@ -102,6 +102,7 @@ _SIGS = {
     "bm_xfer_encode": (C.c_int, [P, I64, P, I64, P, P]),
     "bm_xfer_decode": (C.c_int, [P, P, I64, P]),
     "bm_xfer_decode_piece": (C.c_int, [P, P, I64, P]),
+    "bm_xfer_decode_piece_ctas": (C.c_int, [P, P, I64, I32, P]),
     "bm_abi_version": (C.c_int, []),
     "bm_last_error": (C.c_char_p, []),
     "bm_device_sm_count": (C.c_int, []),

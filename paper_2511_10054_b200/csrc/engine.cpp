@@ -208,6 +208,8 @@ struct bm_engine {
     bool split_fetched = false;
     // K5 joins the layer-step's last bf16 FFN launch (bm_expert_ffn_bf16_combine; BMOE_FUSE_COMBINE=0: own launch)
     bool fuse_combine = true;
+    // CTAs for the decode of pieces off the critical path (BMOE_DECODE_NARROW; 0: full grid)
+    int32_t decode_narrow = 296;
     bm_engine_stats stats{};
     TimingRing stall_ev, copy_ev;
     std::vector<uint8_t> mask_tmp;
@@ -273,8 +275,12 @@ struct bm_engine {
             ENG_CUDA(cudaEventRecord(r.copied[j], s));
             ENG_CUDA(cudaStreamWaitEvent(r.dec, r.copied[j], 0));
             const auto *ph = reinterpret_cast<const bm_xfer_piece_header *>(blob + bh->piece_off[p]);
-            ENG_TRY(bm_xfer_decode_piece(r.slot[j], static_cast<uint16_t *>(dst) + (size_t)p * bh->piece_values,
-                                         ph->n_chunks, r.dec));
+            // an expert's last piece gates its FFN: full grid; the others only have to keep
+            // up with the copy of the next piece, so they take a narrow grid (decode_narrow)
+            const bool last = p + 1 == bh->n_pieces;
+            ENG_TRY(bm_xfer_decode_piece_ctas(r.slot[j],
+                                              static_cast<uint16_t *>(dst) + (size_t)p * bh->piece_values,
+                                              ph->n_chunks, last ? 0 : decode_narrow, r.dec));
             ENG_CUDA(cudaEventRecord(r.decoded[j], r.dec));
             r.used[j] = true;
             *wire += (int64_t)sz;
@@ -777,6 +783,7 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     if (const char *ev = getenv("BMOE_OVERLAP")) g->overlap_fetch = atoi(ev) != 0;
     if (const char *ev = getenv("BMOE_SPLIT_FETCHED")) g->split_fetched = atoi(ev) != 0;  // A/B switch
     if (const char *ev = getenv("BMOE_FUSE_COMBINE")) g->fuse_combine = atoi(ev) != 0;  // A/B switch
+    if (const char *ev = getenv("BMOE_DECODE_NARROW")) g->decode_narrow = atoi(ev);       // A/B switch
     if (g->cfg.fp32_weights) g->fuse_combine = false;  // the fp32 parity path keeps K5 separate
     ENG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     ENG_CUDA(cudaStreamCreateWithFlags(&g->prefetch_stream, cudaStreamNonBlocking));

@@ -438,11 +438,18 @@ extern "C" int bm_xfer_decode(const uint8_t *blob, uint16_t *dst, int64_t n_valu
     return BM_OK;
 }
 
-extern "C" int bm_xfer_decode_piece(const uint8_t *piece, uint16_t *dst, int64_t n_chunks, bm_stream_t stream) {
-    BM_REQUIRE(piece && dst && n_chunks > 0, BM_EINVAL, "bm_xfer_decode_piece: bad argument");
+extern "C" int bm_xfer_decode_piece_ctas(const uint8_t *piece, uint16_t *dst, int64_t n_chunks, int32_t max_ctas,
+                                         bm_stream_t stream) {
+    BM_REQUIRE(piece && dst && n_chunks > 0 && max_ctas >= 0, BM_EINVAL, "bm_xfer_decode_piece: bad argument");
     BM_REQUIRE(((uintptr_t)dst & 15) == 0 && ((uintptr_t)piece & 255) == 0, BM_EINVAL,
                "bm_xfer_decode_piece: dst must be 16-byte and piece 256-byte aligned");
-    xfer_decode_piece_kernel<<<grid_for(n_chunks / 4 + 1), kThreads, 0, as_stream(stream)>>>(piece, dst);
+    int grid = grid_for(n_chunks / 4 + 1);
+    if (max_ctas > 0) grid = std::min(grid, (int)max_ctas);
+    xfer_decode_piece_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(piece, dst);
     BM_LAUNCH_CHECK();
     return BM_OK;
+}
+
+extern "C" int bm_xfer_decode_piece(const uint8_t *piece, uint16_t *dst, int64_t n_chunks, bm_stream_t stream) {
+    return bm_xfer_decode_piece_ctas(piece, dst, n_chunks, 0, stream);
 }
