@@ -262,7 +262,9 @@ struct bm_engine {
     // Coded transfer of expert e of layer l into dst: each piece is copied
     // into a ring slot on stream s and decoded on the ring's decode stream.
     // Returns the wire bytes; the decode stream holds the completion.
-    int enqueue_coded(int l, int e, void *dst, cudaStream_t s, Ring &r, int64_t *wire) {
+    // critical: the expert whose arrival the layer-step's last FFN waits for; only its last
+    // piece is decoded on the full grid
+    int enqueue_coded(int l, int e, void *dst, cudaStream_t s, Ring &r, int64_t *wire, bool critical = true) {
         const bm_xfer_blob_header *bh = blob_of(l, e);
         const uint8_t *blob = reinterpret_cast<const uint8_t *>(bh);
         *wire = 0;
@@ -277,7 +279,7 @@ struct bm_engine {
             const auto *ph = reinterpret_cast<const bm_xfer_piece_header *>(blob + bh->piece_off[p]);
             // an expert's last piece gates its FFN: full grid; the others only have to keep
             // up with the copy of the next piece, so they take a narrow grid (decode_narrow)
-            const bool last = p + 1 == bh->n_pieces;
+            const bool last = critical && p + 1 == bh->n_pieces;
             ENG_TRY(bm_xfer_decode_piece_ctas(r.slot[j],
                                               static_cast<uint16_t *>(dst) + (size_t)p * bh->piece_values,
                                               ph->n_chunks, last ? 0 : decode_narrow, r.dec));
@@ -290,7 +292,7 @@ struct bm_engine {
     }
 
     // H2D of expert e of layer l into a fresh buffer on stream s
-    int fetch(int l, int e, cudaStream_t s) {
+    int fetch(int l, int e, cudaStream_t s, bool critical = true) {
         int b;
         ENG_TRY(alloc_buffer(&b));
         cudaEvent_t c0 = nullptr, c1 = nullptr;  // copy-engine busy time, for the PCIe roofline
@@ -301,7 +303,7 @@ struct bm_engine {
             if (bufs[b].free_ev) ENG_CUDA(cudaStreamWaitEvent(r.dec, bufs[b].free_ev, 0));  // the decode writes it
             if (c0) ENG_CUDA(cudaEventRecord(c0, s));
             int64_t wire = 0;
-            ENG_TRY(enqueue_coded(l, e, bufs[b].dev, s, r, &wire));
+            ENG_TRY(enqueue_coded(l, e, bufs[b].dev, s, r, &wire, critical));
             if (c1) ENG_CUDA(cudaEventRecord(c1, s));
             stats.wire_bytes += wire;
             wire_total += wire;
@@ -472,7 +474,7 @@ struct bm_engine {
                 for (int e : after) {
                     if (std::find(before.begin(), before.end(), e) != before.end()) continue;
                     if (phys[t][e] >= 0 || (int)free_list.size() <= reserve) continue;  // keep the on-demand reserve
-                    ENG_TRY(fetch(t, e, prefetch_stream));
+                    ENG_TRY(fetch(t, e, prefetch_stream, false));  // speculative: never critical
                     ++stats.prefetch_copies;
                 }
             }
@@ -543,12 +545,15 @@ struct bm_engine {
         std::vector<cudaEvent_t> waits;
         std::vector<int> wait_experts;
         ++stats.ffn_calls;
+        int last_fetch = -1;  // the copies go out in expert order: the last one gates the FFN
+        for (int e = 0; e < E; ++e)
+            if (cnt[e] && phys[l][e] < 0) last_fetch = e;
         for (int e = 0; e < E; ++e) {
             if (!cnt[e]) continue;
             ++stats.ffn_experts;
             stats.ffn_rows += cnt[e];
             if (phys[l][e] < 0) {
-                ENG_TRY(fetch(l, e, copy_stream));
+                ENG_TRY(fetch(l, e, copy_stream, e == last_fetch));
                 ++stats.physical_fetches;
             }
             if (ready_pending[l][e]) {
