@@ -703,6 +703,9 @@ def main():
     eng.set_copy_timing(False)
     buf = (np.zeros(6 * L * K + 8, np.float32))
     n = int(N.lib().bm_kernel_times(buf.ctypes.data, buf.size))
+    spans = np.zeros(3 * L * K + 8, np.float32)
+    n_sp = int(N.lib().bm_kernel_spans(spans.ctypes.data, spans.size))
+    spans = spans[:max(n_sp, 0)]
     N.lib().bm_set_kernel_timing(0)
     g1 = buf[0:n:2]
     g2 = buf[1:n:2]
@@ -716,6 +719,8 @@ def main():
     # whichever roofline gives the longer ideal time (decode and small-expert
     # prefill stream weights: HBM; wide prefill tiles: tensor pipe).
     tot_k = st_k["ffn_experts"] * 3 * d * f * 2 + st_k["ffn_rows"] * (d + f) * 2
+    if fused:  # the fused launches also run K5 + layer_update once per layer-step: y rows read, h read + written
+        tot_k += L * K * (B * (k_top + S) * d * 4 + 2 * B * d * 4)
     flops = 6.0 * d * f * st_k["ffn_rows"]
     hbm_peak, hbm_kind = _peaks("hbm")
     tc_peak, tc_kind = _peaks("tensor")
@@ -745,6 +750,11 @@ def main():
                               "ffn_gemm_kernel x2 (data-parallel tcgen05 tiles, SwiGLU / output in the epilogue)",
                     "algorithmic_bytes_per_launch": tot_k / launches, "avg_launch_ms": g1_ms, "peak_kind": peak_kind,
                     "experts_per_launch": n_exp, "rows_per_launch": rows}
+        if fused and len(spans) and float(np.sum(spans)) > 0:
+            # cross-check: the kernels' own on-device spans (globaltimer, first CTA in to last CTA out),
+            # which leave out the launch latency the events of the eager timing pass include
+            roofline["avg_kernel_span_ms"] = float(np.mean(spans))
+            roofline["frac_kernel_span"] = tot_k / (float(np.sum(spans)) / 1e3) / 1e9 / peak
     else:
         # Prefill, tensor-bound: Σ 6·d·f flops per executed (token, slot) row over Σ GEMM1 + GEMM2 time
         peak, peak_kind = tc_peak, tc_kind

@@ -266,6 +266,10 @@ int64_t bm_ffn_trace_read(uint64_t *out_host, int64_t cap);
 int bm_set_kernel_timing(int32_t enable);
 int bm_kernel_timing_enabled(void);
 int64_t bm_kernel_times(float *out_host, int64_t cap);
+/* One float per timed call: the fused decode kernel's on-device span in ms
+ * (first CTA's entry to last CTA's exit, globaltimer), 0 for calls without
+ * one; a cross-check of the events, which also see the launch. */
+int64_t bm_kernel_spans(float *out_host, int64_t cap);
 
 /* ------------------------------------- K6/K7 co-activation and buddy ranking
  * bm_coact_count: topk[N][k] int32 accumulated into counts[E] and the

@@ -137,6 +137,7 @@ _SIGS = {
     "bm_set_kernel_timing": (C.c_int, [I32]),
     "bm_ffn_trace_read": (C.c_int64, [P, I64]),
     "bm_kernel_times": (I64, [P, I64]),
+    "bm_kernel_spans": (I64, [P, I64]),
     "bm_kernel_timing_enabled": (C.c_int, []),
     "bm_coact_count": (C.c_int, [P, I64, I64, I64, P, P, P, P]),
     "bm_coact_weighted": (C.c_int, [P, P, I64, I64, I64, F64, P, P]),

@@ -259,6 +259,7 @@ struct FusedParams {
     // n counts in h_ready[n & 1] and clears h_ready[(n + 1) & 1], which launch n - 1 used.
     int *h_ready;
     unsigned long long *launch_count;
+    unsigned long long *span;  // kernel timing: [min entry, max exit] globaltimer of this launch, else null
 };
 constexpr int kTracePts = 12;
 

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     // 4 GEMM1 epilogue done, 5 barrier seen by the producer, 6 GEMM2 epilogue done, 7 exit
     unsigned long long *tr = fp.trace ? fp.trace + (size_t)blockIdx.x * kTracePts : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = ptx::globaltimer();
+    if (fp.span && threadIdx.x == 0) atomicMin(fp.span, ptx::globaltimer());
     const GemmParams &P1 = fp.g[0];
     const GemmParams &P2 = fp.g[1];
     const int n_tile = P1.n_tile;
@@ -514,6 +515,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
                                           fp.cmb.h, fp.cmb.scale, fp.cmb.h, hbuf, csh);
     }
     if (tr && threadIdx.x == 0) tr[7] = ptx::globaltimer();
+    if (fp.span) {
+        __syncthreads();  // the combine's last stores of this CTA are issued
+        if (threadIdx.x == 0) atomicMax(fp.span + 1, ptx::globaltimer());
+    }
 }
 
 template <int NMAT1, int KPS1, int KPS2>

@@ -44,8 +44,30 @@ long long max_tiles(long long E, long long M, long long r_max, long long n_tile)
 struct Timing {
     bool enabled = false;
     std::vector<cudaEvent_t> ev;  // 4 per call: before/after GEMM1, before/after GEMM2
+    // fused decode calls also stamp their on-device span: [first CTA entry, last CTA exit]
+    // (globaltimer ns), one slot pair per timed call, beside the events
+    unsigned long long *span = nullptr;
+    int64_t span_cap = 0, span_n = 0;
+    std::vector<int64_t> span_of_call;  // slot per call, -1 for calls without one
     std::mutex mu;
 } g_timing;
+
+// next span slot (reset to [UINT64_MAX, 0] on s) for a fused call being timed, or null
+unsigned long long *next_span(cudaStream_t s) {
+    if (!g_timing.span) {
+        g_timing.span_cap = 1 << 16;
+        if (cudaMalloc(&g_timing.span, (size_t)g_timing.span_cap * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+            g_timing.span = nullptr;
+            return nullptr;
+        }
+    }
+    if (g_timing.span_n >= g_timing.span_cap) return nullptr;
+    unsigned long long *p = g_timing.span + 2 * g_timing.span_n;
+    cudaMemsetAsync(p, 0xff, sizeof(unsigned long long), s);
+    cudaMemsetAsync(p + 1, 0, sizeof(unsigned long long), s);
+    g_timing.span_of_call.push_back(g_timing.span_n++);
+    return p;
+}
 
 int record_event(cudaStream_t s) {
     cudaEvent_t e;
@@ -207,7 +229,7 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap,
                        reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off),
-                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr};
+                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr, nullptr};
         static const int h_ready = getenv("BMOE_H_READY") ? atoi(getenv("BMOE_H_READY")) : 1;
         fp.g[1].partials = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + wl.slot_set_bytes);
         if (h_ready) {
@@ -221,6 +243,7 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
                               ((reinterpret_cast<uintptr_t>(y_perm) | reinterpret_cast<uintptr_t>(cmb->h)) & 15) == 0;
         if (fuse_cmb) fp.cmb = *cmb;
         // timing record: [start, end] of the one kernel, then an empty GEMM2 interval
+        if (timing) fp.span = next_span(s);
         if (timing && record_event(s)) return BM_ECUDA;
         const int rc = launch_fused_dispatch(fp, nmat1, k1, k2, G, s);
         if (rc) return rc;
@@ -231,6 +254,7 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         }
         return fuse_cmb ? BM_OK : separate_combine();
     }
+    if (timing) g_timing.span_of_call.push_back(-1);
     if (timing && record_event(s)) return BM_ECUDA;
     if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
     if (timing && record_event(s)) return BM_ECUDA;
@@ -262,8 +286,28 @@ extern "C" int bm_set_kernel_timing(int32_t enable) {
     for (cudaEvent_t e : g_timing.ev)
         if (e) cudaEventDestroy(e);
     g_timing.ev.clear();
+    g_timing.span_of_call.clear();
+    g_timing.span_n = 0;
     g_timing.enabled = enable != 0;
     return BM_OK;
+}
+
+// One float per bm_expert_ffn_bf16 call since timing was enabled: the fused
+// decode kernel's on-device span in ms (first CTA entry to last CTA exit,
+// globaltimer), 0 for calls without one (prefill GEMMs). Synchronises.
+extern "C" int64_t bm_kernel_spans(float *out_host, int64_t cap) {
+    std::lock_guard<std::mutex> lk(g_timing.mu);
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    std::vector<unsigned long long> raw((size_t)g_timing.span_n * 2);
+    if (g_timing.span_n && cudaMemcpy(raw.data(), g_timing.span, raw.size() * sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    int64_t n = 0;
+    for (int64_t slot : g_timing.span_of_call) {
+        if (n >= cap) break;
+        out_host[n++] = slot < 0 ? 0.f : (float)((double)(raw[2 * slot + 1] - raw[2 * slot]) * 1e-6);
+    }
+    return n;
 }
 
 extern "C" int bm_kernel_timing_enabled(void) { return g_timing.enabled ? 1 : 0; }
