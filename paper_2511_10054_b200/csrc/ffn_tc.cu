@@ -52,6 +52,23 @@ struct Timing {
     std::mutex mu;
 } g_timing;
 
+// Timing pass only: hold the stream for a few microseconds before a timed
+// call's start event, so the host has enqueued event + kernel + event before
+// the GPU reaches them and the interval does not include the host's launch
+// latency (the engine's timing pass launches eagerly; its timed runs replay
+// CUDA graphs, where consecutive kernels start back to back).
+__global__ void hold_kernel(unsigned long long ns) {
+    const unsigned long long t0 = ptx::globaltimer();
+    while (ptx::globaltimer() - t0 < ns) __nanosleep(500);
+}
+int hold_stream(cudaStream_t s) {
+    static const long long ns = getenv("BMOE_TIMING_HOLD_NS") ? atoll(getenv("BMOE_TIMING_HOLD_NS")) : 30000;
+    if (ns <= 0) return BM_OK;
+    hold_kernel<<<1, 32, 0, s>>>((unsigned long long)ns);
+    BM_LAUNCH_CHECK();
+    return BM_OK;
+}
+
 // next span slot (reset to [UINT64_MAX, 0] on s) for a fused call being timed, or null
 unsigned long long *next_span(cudaStream_t s) {
     if (!g_timing.span) {
@@ -243,7 +260,10 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
                               ((reinterpret_cast<uintptr_t>(y_perm) | reinterpret_cast<uintptr_t>(cmb->h)) & 15) == 0;
         if (fuse_cmb) fp.cmb = *cmb;
         // timing record: [start, end] of the one kernel, then an empty GEMM2 interval
-        if (timing) fp.span = next_span(s);
+        if (timing) {
+            fp.span = next_span(s);
+            if (int rc = hold_stream(s)) return rc;
+        }
         if (timing && record_event(s)) return BM_ECUDA;
         const int rc = launch_fused_dispatch(fp, nmat1, k1, k2, G, s);
         if (rc) return rc;
@@ -254,7 +274,10 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         }
         return fuse_cmb ? BM_OK : separate_combine();
     }
-    if (timing) g_timing.span_of_call.push_back(-1);
+    if (timing) {
+        g_timing.span_of_call.push_back(-1);
+        if (int rc = hold_stream(s)) return rc;
+    }
     if (timing && record_event(s)) return BM_ECUDA;
     if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
     if (timing && record_event(s)) return BM_ECUDA;
