@@ -735,7 +735,7 @@ def main():
         # profiles/), with that launch's own algorithmic bytes beside it
         traffic, traffic_launch = None, None
         try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r1e_traffic.json")))
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r2_traffic.json")))
             l0 = tr["launches"][0]
             if args.model == "mixtral" and fused:
                 traffic = l0["dram_read_bytes"] + l0["dram_write_bytes"]
