@@ -1,0 +1,74 @@
+// Launch-overhead probe: event-timed back-to-back launches of empty kernels
+// shaped like the fused decode FFN (148 CTAs x 256 threads, 216 KB dynamic
+// shared memory, cooperative or not) against a plain small kernel, plus the
+// kernels' own globaltimer spans. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ unsigned long long span[2];
+__device__ __forceinline__ unsigned long long gt() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__global__ void empty_kernel(int work_ns) {
+    extern __shared__ unsigned char sm[];
+    if (threadIdx.x == 0) atomicMin(&span[0], gt());
+    if (work_ns) {
+        unsigned long long t0 = gt();
+        while (gt() - t0 < (unsigned long long)work_ns) __nanosleep(200);
+    }
+    if (threadIdx.x == 0) { sm[0] = 1; atomicMax(&span[1], gt()); }
+}
+
+static float run(int smem, int coop, int blocks, int threads, int work_ns, float *span_us) {
+    cudaFuncSetAttribute(empty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float tot = 0, stot = 0;
+    const int iters = 50;
+    for (int i = 0; i < iters + 5; ++i) {
+        unsigned long long init[2] = {~0ull, 0ull};
+        cudaMemcpyToSymbol(span, init, sizeof(init));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(blocks);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = coop;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaEventRecord(a);
+        cudaLaunchKernelEx(&cfg, empty_kernel, work_ns);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        unsigned long long got[2];
+        cudaMemcpyFromSymbol(got, span, sizeof(got));
+        if (i >= 5) {
+            tot += ms;
+            stot += (got[1] - got[0]) * 1e-3f;
+        }
+    }
+    *span_us = stot / iters;
+    return tot / iters * 1000.f;
+}
+
+int main() {
+    struct { int smem, coop, blocks, threads, work; const char *name; } cases[] = {
+        {0, 0, 148, 256, 0, "plain 148x256, no smem"},
+        {216 * 1024, 0, 148, 256, 0, "148x256, 216 KB smem"},
+        {216 * 1024, 1, 148, 256, 0, "148x256, 216 KB smem, cooperative"},
+        {216 * 1024, 1, 148, 256, 20000, "same + 20 us of work"},
+        {0, 0, 148, 256, 20000, "no smem + 20 us of work"},
+    };
+    for (auto &c : cases) {
+        float sp;
+        float us = run(c.smem, c.coop, c.blocks, c.threads, c.work, &sp);
+        printf("{\"case\": \"%s\", \"event_us\": %.2f, \"span_us\": %.2f, \"gap_us\": %.2f}\n", c.name, us, sp, us - sp);
+    }
+    return 0;
+}
