@@ -18,7 +18,8 @@ __global__ void empty_kernel(int work_ns) {
         unsigned long long t0 = gt();
         while (gt() - t0 < (unsigned long long)work_ns) __nanosleep(200);
     }
-    if (threadIdx.x == 0) { sm[0] = 1; atomicMax(&span[1], gt()); }
+    if (work_ns < 0) sm[0] = 1;  // keeps the dynamic buffer referenced
+    if (threadIdx.x == 0) atomicMax(&span[1], gt());
 }
 
 static float run(int smem, int coop, int blocks, int threads, int work_ns, float *span_us) {
@@ -41,7 +42,8 @@ static float run(int smem, int coop, int blocks, int threads, int work_ns, float
         cfg.attrs = at;
         cfg.numAttrs = 1;
         cudaEventRecord(a);
-        cudaLaunchKernelEx(&cfg, empty_kernel, work_ns);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, empty_kernel, work_ns);
+        if (e != cudaSuccess) { printf("launch error: %s\n", cudaGetErrorString(e)); return -1.f; }
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
@@ -58,6 +60,7 @@ static float run(int smem, int coop, int blocks, int threads, int work_ns, float
 }
 
 int main() {
+    cudaFree(0);
     struct { int smem, coop, blocks, threads, work; const char *name; } cases[] = {
         {0, 0, 148, 256, 0, "plain 148x256, no smem"},
         {216 * 1024, 0, 148, 256, 0, "148x256, 216 KB smem"},
