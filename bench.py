@@ -349,7 +349,7 @@ def run_reference(args, ws):
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (the GPU arm's weights and streams)",
             "config": _config(args.model, L, args.batch, "buddy", cd.cap, cd.k_max, cd.rate, args.clusters,
-                              args.experts),
+                              args.experts, args.weight_seed),
             "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": f"every step: {args.batch} tokens through all {L} layers (route, gates, "
                                        f"remap, cache replay, f64 SwiGLU forward, layer_update) via the numpy "
@@ -367,7 +367,7 @@ def _metric(B: int) -> str:
     return f"MoE {phase} tokens/sec at fixed expert-cache budget; expert-miss stall (ms)"
 
 
-def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None, experts="clustered"):
+def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None, experts="clustered", weight_seed=0):
     from paper_2511_10054_b200.synth import CLUSTERS, SPREAD
     clusters = clusters or CLUSTERS[model]
     E, k, d, f, _, S = _shape(model)
@@ -387,8 +387,8 @@ def _config(model, L, B, method, capacity, search_rank_h, rate, clusters=None, e
            "l2": f"inputs larger than L2 ({(E + S) * 3 * d * f * 2 / 1e9:.2f} GB of expert weights per layer)"}
     if S:
         cfg["shared_experts"] = S
-    if getattr(_config, "weight_seed", 0):
-        cfg["weight_seed"] = _config.weight_seed
+    if weight_seed:
+        cfg["weight_seed"] = weight_seed
     return cfg
 
 
@@ -599,7 +599,6 @@ def main():
         from paper_2511_10054_b200.synth import CLUSTERS
         E_ = _shape(args.model)[0]
         args.experts = "clustered" if (args.clusters or CLUSTERS[args.model]) < E_ else "independent"
-    _config.weight_seed = args.weight_seed
     launch_or_check(args)
     ws, rank, local = _dist()
     if args.impl == "reference":
@@ -879,7 +878,7 @@ def main():
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init bf16 weights, reference-style clustered router/token stream)",
         "config": _config(args.model, L, B, "buddy", wl.eng.capacity, wl.eng.search_rank_h, wl.extra["cache_rate"],
-                          args.clusters, args.experts),
+                          args.clusters, args.experts, args.weight_seed),
         "tables_sha16": digest,
         "stall_ms_per_step": st["stall_ms"] / K,
         "sim_stall_model": {"ondemand_misses_per_step": st["ondemand_misses"] / K,

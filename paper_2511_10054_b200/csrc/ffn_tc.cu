@@ -256,7 +256,7 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         static const int pdl = getenv("BMOE_PDL") ? atoi(getenv("BMOE_PDL")) : 0;
         fp.pdl = pdl;
         // the combine joins the launch when bm_combine would take its 16-byte vector path (same code then)
-        const bool fuse_cmb = cmb && d % 4 == 0 && d * 4 <= kSmemBudget &&
+        const bool fuse_cmb = cmb && d % 4 == 0 && d * 4 <= 200 * 1024 &&  // h row in the pipeline smem (as bm_combine)
                               ((reinterpret_cast<uintptr_t>(y_perm) | reinterpret_cast<uintptr_t>(cmb->h)) & 15) == 0;
         if (fuse_cmb) fp.cmb = *cmb;
         // timing record: [start, end] of the one kernel, then an empty GEMM2 interval

@@ -105,6 +105,15 @@ def test_ratio_and_piecewise_decode(cuda_ok):
         N.call("bm_xfer_decode_piece", piece.data_ptr(), y[p * pv:].data_ptr(), nch,
                torch.cuda.current_stream().cuda_stream)
     assert np.array_equal(_bits(x), _bits(y))
+    # the engine's narrow decode of pieces off its critical path (few CTAs, grid-stride) is the same
+    for ctas in (1, 37, 296):
+        y.zero_()
+        for p in range(n_pieces):
+            piece = blob[int(offs[p]):int(offs[p + 1])]
+            nch = int(np.frombuffer(piece[4:8].cpu().numpy().tobytes(), np.uint32)[0])
+            N.call("bm_xfer_decode_piece_ctas", piece.data_ptr(), y[p * pv:].data_ptr(), nch, ctas,
+                   torch.cuda.current_stream().cuda_stream)
+        assert np.array_equal(_bits(x), _bits(y)), ctas
 
 
 def test_engine_coded_mirrors_equal_raw(cuda_ok):
