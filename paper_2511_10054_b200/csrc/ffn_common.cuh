@@ -260,6 +260,7 @@ struct FusedParams {
     int *h_ready;
     unsigned long long *launch_count;
     unsigned long long *span;  // kernel timing: [min entry, max exit] globaltimer of this launch, else null
+    int w2_l2_pf;              // GEMM2 stages past the smem ring prefetched into L2 on entering GEMM2
 };
 constexpr int kTracePts = 12;
 
