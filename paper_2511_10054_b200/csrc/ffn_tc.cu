@@ -99,25 +99,32 @@ int record_event(cudaStream_t s) {
 
 namespace bm {
 namespace ffn {
-// workspace: [fp32 partial slots | bf16 SW128 H planes | split-tile arrival
-// counters (2 phases) + grid barrier]; the counters must start at zero.
+// workspace: [persistent state: grid barrier, launch count, H readiness, split-tile
+// arrival counters | fp32 partial slots (2 sets) | bf16 SW128 H planes]; the state must
+// start at zero (the kernels keep it consistent from then on).
 struct WsLayout {
-    long long slot_set_bytes, partial_bytes, h_off, h_bytes, ctr_off, bar_off, tile_cap, total;
+    long long slot_set_bytes, partial_off, partial_bytes, h_off, h_bytes, ctr_off, bar_off, tile_cap, total;
 };
 WsLayout ws_layout(long long E, long long d, long long f, long long r_max, long long n_tile) {
     WsLayout w;
     const long long M = std::max(d, f);
-    w.tile_cap = max_tiles(E, M, r_max, n_tile);
-    const long long slots = w.tile_cap + sm_count() + 1;
-    // two slot sets: the fused decode kernel's GEMM2 may run while GEMM1 split tiles are still
-    // being reduced (per-expert H readiness), so each GEMM has its own
+    // Persistent state first, at offsets that do not depend on the call's token tile (a
+    // workspace serves calls of any n_tile up to the one it was sized for, and the counters
+    // must survive between them): [grid barrier u64 | launch count u64 | h_ready[2][kMaxE] |
+    // split-tile arrival counters, 2 phases x the tile count of the narrowest tile (16)].
+    w.tile_cap = max_tiles(E, M, r_max, 16);
+    w.bar_off = 0;
+    w.ctr_off = 16 + 2 * kMaxE * 4;
+    const long long state = ((w.ctr_off + 2 * w.tile_cap * 4 + 1023) / 1024) * 1024;
+    // scratch: two split-tile slot sets (the fused decode kernel's GEMM2 may run while GEMM1
+    // split tiles are still being reduced, per-expert H readiness), then the H planes
+    const long long slots = max_tiles(E, M, r_max, n_tile) + sm_count() + 1;
     w.slot_set_bytes = ((slots * 2 * n_tile * kBM * 4 + 1023) / 1024) * 1024;
+    w.partial_off = state;
     w.partial_bytes = 2 * w.slot_set_bytes;
-    w.h_off = w.partial_bytes;
+    w.h_off = w.partial_off + w.partial_bytes;
     w.h_bytes = (((f / 64) * r_max * 128 + 1023) / 1024) * 1024;
-    w.ctr_off = w.h_off + w.h_bytes;
-    w.bar_off = ((w.ctr_off + 2 * w.tile_cap * 4 + 7) / 8) * 8;  // the 64-bit grid barrier count
-    w.total = w.bar_off + 16 + 2 * kMaxE * 4;  // [grid barrier | launch count | h_ready[2][kMaxE]]
+    w.total = w.h_off + w.h_bytes;
     return w;
 }
 }  // namespace ffn
@@ -205,7 +212,7 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
     cudaStream_t s = as_stream(stream);
     const long long buf_bytes = (act == BM_ACT_SWIGLU ? 3 : 2) * d * f * 2;
     const WsLayout wl = ws_layout(E, d, f, r_max, n_tile);
-    float *partials = static_cast<float *>(workspace);
+    float *partials = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + wl.partial_off);
     uint8_t *h_planes = static_cast<uint8_t *>(workspace) + wl.h_off;
     int *counters = reinterpret_cast<int *>(static_cast<uint8_t *>(workspace) + wl.ctr_off);
     const int G = sm_count();
@@ -250,7 +257,8 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         static const int w2_pf = getenv("BMOE_W2_L2PF") ? atoi(getenv("BMOE_W2_L2PF")) : 8;
         fp.w2_l2_pf = w2_pf;
         static const int h_ready = getenv("BMOE_H_READY") ? atoi(getenv("BMOE_H_READY")) : 1;
-        fp.g[1].partials = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + wl.slot_set_bytes);
+        fp.g[1].partials = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + wl.partial_off +
+                                                     wl.slot_set_bytes);
         if (h_ready) {
             fp.launch_count = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off + 8);
             fp.h_ready = reinterpret_cast<int *>(static_cast<uint8_t *>(workspace) + wl.bar_off + 16);

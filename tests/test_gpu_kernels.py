@@ -569,3 +569,25 @@ def test_ffn_combine_one_launch_equals_two(cuda_ok, E, d, f, B, k, n_tile):
         h = h0.clone()
         ops.expert_ffn_bf16_combine(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws, pr, kd, h, 0.5)
         assert torch.equal(h, ref)
+
+
+def test_fused_workspace_shared_across_token_tiles(cuda_ok):
+    """One workspace serves decode calls of different token tiles (an engine's
+    batches of 16 and 64 tokens): the barrier count, launch count, H readiness
+    and arrival counters live at offsets independent of n_tile, so interleaved
+    calls with n_tile 64 / 16 / 32 on one buffer give exactly what fresh
+    workspaces give."""
+    import copy
+    E, d, f, B, k = 16, 1024, 2048, 48, 2
+    seed = 91
+    _, _, (xp, perm, arena, buf_of, ws) = _bf16_case(np.random.default_rng(seed), E, d, f, B, k, ops.ACT_SWIGLU, 64)
+    bo = _t(buf_of)
+    rows = int(perm.offset[-1])
+    shared = ops.FfnWorkspace(E, d, f, perm.r_max, 64)
+    for nt in (64, 16, 32, 16, 64, 32):
+        fresh = ops.FfnWorkspace(E, d, f, perm.r_max, nt)
+        ref = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, fresh)[:rows].clone()
+        view = copy.copy(shared)
+        view.n_tile = nt
+        got = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, view)[:rows]
+        assert torch.equal(got, ref), nt
