@@ -254,7 +254,7 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap,
                        reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off),
                        pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr, nullptr, 0};
-        static const int w2_pf = getenv("BMOE_W2_L2PF") ? atoi(getenv("BMOE_W2_L2PF")) : 8;
+        static const int w2_pf = getenv("BMOE_W2_L2PF") ? atoi(getenv("BMOE_W2_L2PF")) : 0;  // measured slower: off
         fp.w2_l2_pf = w2_pf;
         static const int h_ready = getenv("BMOE_H_READY") ? atoi(getenv("BMOE_H_READY")) : 1;
         fp.g[1].partials = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + wl.partial_off +
