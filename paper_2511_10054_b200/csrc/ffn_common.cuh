@@ -261,7 +261,9 @@ struct FusedParams {
     unsigned long long *launch_count;
     unsigned long long *span;  // kernel timing: [min entry, max exit] globaltimer of this launch, else null
     int w2_l2_pf;              // GEMM2 stages past the smem ring prefetched into L2 on entering GEMM2
+    int groups;                // expert groups whose GEMM1 / GEMM2 phases interleave (needs h_ready; <= kMaxGroups)
 };
+constexpr int kMaxGroups = 4;
 constexpr int kTracePts = 12;
 
 // CTA that processes stream-K iteration i of T over G CTAs

@@ -274,11 +274,12 @@ __device__ void fused_mma(const GemmParams &P, const Sched &s, const Geom &gm, i
 // the reducer's critical path.
 template <int NMAT>
 __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &gm, int *arrive, int &acc,
-                               uint32_t &acc_phase, long long T, int G, int cta, int spt, uint32_t tmem_base, int q,
-                               unsigned lane, int *h_ready = nullptr, unsigned long long *tr = nullptr) {
+                               uint32_t &acc_phase, long long base, long long T, int G, int slot_off, int cta, int spt,
+                               uint32_t tmem_base, int q, unsigned lane, int *h_ready = nullptr,
+                               unsigned long long *tr = nullptr) {
     if (cta >= G) return;
     const int mtiles = P.M / kBM;
-    const long long it0 = range_start(cta, T, G), it1 = range_start(cta + 1, T, G);
+    const long long it0 = base + range_start(cta, T, G), it1 = base + range_start(cta + 1, T, G);
     const long long slot_elems = 2LL * P.n_tile * kBM;
     const int m_local = q * 32 + (int)lane;
     long long it = it0;
@@ -301,7 +302,7 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
                 finish16<NMAT>(P, ti, c0, q, lane, g, u);
             }
         } else if (reducer) {
-            const int c1 = cta_of((long long)(tile + 1) * spt - 1, T, G);
+            const int c1 = cta_of((long long)(tile + 1) * spt - 1 - base, T, G);
             if (m_local == 0) {
                 while (ptx::ld_acquire_gpu(reinterpret_cast<const unsigned *>(arrive + tile)) < (unsigned)(c1 - cta))
                     __nanosleep(32);
@@ -327,7 +328,7 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
 #pragma unroll
                     for (int x = 0; x < kGrp; ++x) {
                         if (c0 + x > c1) break;
-                        const float *src = P.partials + ((long long)tile + c0 + x) * slot_elems;
+                        const float *src = P.partials + ((long long)tile + c0 + x + slot_off) * slot_elems;
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             pg[x][j] = __ldcg(src + (long long)(cc + j) * kBM + m_local);
@@ -347,7 +348,7 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
                 finish16<NMAT>(P, ti, cc, q, lane, g, u);
             }
         } else {
-            float *dst = P.partials + ((long long)tile + cta) * slot_elems;
+            float *dst = P.partials + ((long long)tile + cta + slot_off) * slot_elems;
 #pragma unroll
             for (int m = 0; m < NMAT; ++m)
                 for (int c0 = 0; c0 < ti.n; c0 += 16) {
@@ -374,6 +375,41 @@ __device__ void fused_epilogue(const GemmParams &P, const Sched &s, const Geom &
             if (m_local == 0) atomicAdd(arrive + tile, 1);
         }
     }
+}
+
+// The call's work as phases: with ng expert groups (contiguous in the
+// schedule) the order is G1(0), G1(1), G2(0), G1(2), G2(1), ..., G2(ng-1), so
+// each group's GEMM2 follows the NEXT group's GEMM1 and finds its H (per-
+// expert readiness) already written instead of waiting at the end of the
+// whole GEMM1 stream. Each phase is its own stream-K range over the CTAs
+// (iterations [base, base + T)); its split-tile partial slots are offset by
+// g * G so the overlapping phases of one GEMM never share a slot.
+struct Phase {
+    bool g2;
+    int g, G, slot_off;
+    long long base, T;
+};
+__device__ __forceinline__ Phase phase_at(int p, int ng, const Sched &s, int mtiles1, int mtiles2, int spt1,
+                                          int spt2, int Gn) {
+    Phase ph;
+    if (p == 0) {
+        ph.g2 = false;
+        ph.g = 0;
+    } else if (p == 2 * ng - 1) {
+        ph.g2 = true;
+        ph.g = ng - 1;
+    } else {
+        const int k = p - 1;
+        ph.g2 = (k & 1) != 0;
+        ph.g = ph.g2 ? (k - 1) / 2 : k / 2 + 1;
+    }
+    const int a0 = ph.g * s.n_act / ng, a1 = (ph.g + 1) * s.n_act / ng;
+    const int mt = ph.g2 ? mtiles2 : mtiles1, spt = ph.g2 ? spt2 : spt1;
+    ph.base = (long long)mt * s.chunk_prefix[a0] * spt;
+    ph.T = (long long)mt * (s.chunk_prefix[a1] - s.chunk_prefix[a0]) * spt;
+    ph.G = (int)min((long long)Gn, ph.T);
+    ph.slot_off = ph.g * Gn;
+    return ph;
 }
 
 template <int NMAT1, int KPS1, int KPS2>
@@ -449,53 +485,74 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
 
     const int cta = blockIdx.x, Gn = gridDim.x;
     const int spt1 = P1.K / (kBK * KPS1), spt2 = P2.K / (kBK * KPS2);
-    const long long T1 = (long long)total_tiles(sched, P1.M / kBM) * spt1;
-    const long long T2 = (long long)total_tiles(sched, P2.M / kBM) * spt2;
-    const int G1 = (int)min((long long)Gn, T1), G2 = (int)min((long long)Gn, T2);
+    const int mtiles1 = P1.M / kBM, mtiles2 = P2.M / kBM;
+    // expert groups (see phase_at): only with per-expert readiness, at most one per expert
+    const int ng = h_ready ? max(1, min(fp.groups, sched.n_act)) : 1;
+    const int n_ph = 2 * ng;
+    const int last_g1 = ng == 1 ? 0 : n_ph - 3;  // the phase index of G1(ng - 1)
 
     if (warp == 0 && lane == 0) {
         const uint64_t pol = ptx::policy_evict_first();  // weights stream through once
         int stage = 0;
         uint32_t phase = 0;
-        if (cta < G1)
-            fused_produce<NMAT1, KPS1>(P1, sched, gm, stage, phase, range_start(cta, T1, G1),
-                                       range_start(cta + 1, T1, G1), spt1, pol, nullptr, 0, 0);
-        if (tr) tr[2] = ptx::globaltimer();
-        if (cta < G2) {
-            if (h_ready)
-                fused_produce_ready<KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2),
-                                          range_start(cta + 1, T2, G2), spt2, pol, h_ready, P1.M / kBM, fp.w2_l2_pf,
-                                          tr ? tr + 5 : nullptr);
-            else
-                fused_produce<1, KPS2>(P2, sched, gm, stage, phase, range_start(cta, T2, G2),
-                                       range_start(cta + 1, T2, G2), spt2, pol, fp.grid_bar,
-                                       bar0 + (unsigned long long)Gn, fp.prefetch_w2, tr ? tr + 5 : nullptr);
+        for (int p = 0; p < n_ph; ++p) {
+            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn);
+            if (cta < ph.G) {
+                const long long i0 = ph.base + range_start(cta, ph.T, ph.G);
+                const long long i1 = ph.base + range_start(cta + 1, ph.T, ph.G);
+                if (!ph.g2)
+                    fused_produce<NMAT1, KPS1>(P1, sched, gm, stage, phase, i0, i1, spt1, pol, nullptr, 0, 0);
+                else if (h_ready)
+                    fused_produce_ready<KPS2>(P2, sched, gm, stage, phase, i0, i1, spt2, pol, h_ready, mtiles1,
+                                              fp.w2_l2_pf, tr && ph.g == 0 ? tr + 5 : nullptr);
+                else
+                    fused_produce<1, KPS2>(P2, sched, gm, stage, phase, i0, i1, spt2, pol, fp.grid_bar,
+                                           bar0 + (unsigned long long)Gn, fp.prefetch_w2, tr ? tr + 5 : nullptr);
+            }
+            if (tr && p == last_g1) tr[2] = ptx::globaltimer();
         }
     } else if (warp == 1 && lane == 0) {
         int stage = 0, acc = 0;
         uint32_t phase = 0, acc_phase = 0;
-        if (cta < G1)
-            fused_mma<NMAT1, KPS1>(P1, sched, gm, stage, phase, acc, acc_phase, range_start(cta, T1, G1),
-                                   range_start(cta + 1, T1, G1), spt1, tmem_base);
-        if (tr) tr[3] = ptx::globaltimer();
-        if (cta < G2)
-            fused_mma<1, KPS2>(P2, sched, gm, stage, phase, acc, acc_phase, range_start(cta, T2, G2),
-                               range_start(cta + 1, T2, G2), spt2, tmem_base, tr ? tr + 10 : nullptr);
+        bool first_g2 = true;
+        for (int p = 0; p < n_ph; ++p) {
+            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn);
+            if (cta < ph.G) {
+                const long long i0 = ph.base + range_start(cta, ph.T, ph.G);
+                const long long i1 = ph.base + range_start(cta + 1, ph.T, ph.G);
+                if (!ph.g2) {
+                    fused_mma<NMAT1, KPS1>(P1, sched, gm, stage, phase, acc, acc_phase, i0, i1, spt1, tmem_base);
+                } else {
+                    fused_mma<1, KPS2>(P2, sched, gm, stage, phase, acc, acc_phase, i0, i1, spt2, tmem_base,
+                                       tr && first_g2 ? tr + 10 : nullptr);
+                    first_g2 = false;
+                }
+            }
+            if (tr && p == last_g1) tr[3] = ptx::globaltimer();
+        }
         if (tr) tr[11] = ptx::globaltimer();
     } else if (warp >= 4) {
         const int q = warp - 4;
         int acc = 0;
         uint32_t acc_phase = 0;
-        fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, T1, G1, cta, spt1, tmem_base, q, lane,
-                              h_ready, tr);
-        // H of this CTA is written: publish it (to the bulk-copy proxy too) and arrive
-        if (tr && q == 0 && lane == 0) tr[4] = ptx::globaltimer();
-        ptx::fence_proxy_async_global();
-        __threadfence();
-        ptx::named_bar_sync(1, 128);
-        if (q == 0 && lane == 0) atomicAdd(fp.grid_bar, 1ull);
-        fused_epilogue<1>(P2, sched, gm, fp.arrive + fp.tile_cap, acc, acc_phase, T2, G2, cta, spt2, tmem_base, q,
-                          lane);
+        for (int p = 0; p < n_ph; ++p) {
+            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn);
+            if (!ph.g2)
+                fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, ph.base, ph.T, ph.G, ph.slot_off, cta,
+                                      spt1, tmem_base, q, lane, h_ready, tr);
+            else
+                fused_epilogue<1>(P2, sched, gm, fp.arrive + fp.tile_cap, acc, acc_phase, ph.base, ph.T, ph.G,
+                                  ph.slot_off, cta, spt2, tmem_base, q, lane);
+            if (p == last_g1) {
+                // all of this CTA's H is written: publish it (to the bulk-copy proxy too) and
+                // arrive at barrier 1 (GEMM2 waits on it without per-expert readiness)
+                if (tr && q == 0 && lane == 0) tr[4] = ptx::globaltimer();
+                ptx::fence_proxy_async_global();
+                __threadfence();
+                ptx::named_bar_sync(1, 128);
+                if (q == 0 && lane == 0) atomicAdd(fp.grid_bar, 1ull);
+            }
+        }
         if (tr && q == 0 && lane == 0) tr[6] = ptx::globaltimer();
     }
     __syncwarp();

@@ -118,7 +118,7 @@ WsLayout ws_layout(long long E, long long d, long long f, long long r_max, long 
     const long long state = ((w.ctr_off + 2 * w.tile_cap * 4 + 1023) / 1024) * 1024;
     // scratch: two split-tile slot sets (the fused decode kernel's GEMM2 may run while GEMM1
     // split tiles are still being reduced, per-expert H readiness), then the H planes
-    const long long slots = max_tiles(E, M, r_max, n_tile) + sm_count() + 1;
+    const long long slots = max_tiles(E, M, r_max, n_tile) + kMaxGroups * sm_count() + 1;  // + group offsets
     w.slot_set_bytes = ((slots * 2 * n_tile * kBM * 4 + 1023) / 1024) * 1024;
     w.partial_off = state;
     w.partial_bytes = 2 * w.slot_set_bytes;
@@ -253,7 +253,9 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap,
                        reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off),
-                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr, nullptr, 0};
+                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr, nullptr, 0, 1};
+        const char *gv = getenv("BMOE_FFN_GROUPS");  // read per call: tests switch it
+        fp.groups = std::max(1, std::min(gv ? atoi(gv) : 3, kMaxGroups));
         static const int w2_pf = getenv("BMOE_W2_L2PF") ? atoi(getenv("BMOE_W2_L2PF")) : 0;  // measured slower: off
         fp.w2_l2_pf = w2_pf;
         static const int h_ready = getenv("BMOE_H_READY") ? atoi(getenv("BMOE_H_READY")) : 1;

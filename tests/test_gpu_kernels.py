@@ -383,9 +383,10 @@ def test_fused_single_launch_equals_multi_kernel(cuda_ok, E, d, f, B, k, act, n_
     _, _, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, act, n_tile)
     rows = int(perm.offset[-1])
     bo = _t(buf_of)
-    saved = {v: os.environ.get(v) for v in ("BMOE_FUSED", "BMOE_KPS")}
+    saved = {v: os.environ.get(v) for v in ("BMOE_FUSED", "BMOE_KPS", "BMOE_FFN_GROUPS")}
     try:
         os.environ["BMOE_KPS"] = "2"  # same k-steps per stage -> same stream-K split in both paths
+        os.environ["BMOE_FFN_GROUPS"] = "1"  # one stream-K range per GEMM, as the separate kernels
         os.environ["BMOE_FUSED"] = "0"
         ref = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows].clone()
         os.environ["BMOE_FUSED"] = "1"
@@ -591,3 +592,37 @@ def test_fused_workspace_shared_across_token_tiles(cuda_ok):
         view.n_tile = nt
         got = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, view)[:rows]
         assert torch.equal(got, ref), nt
+
+
+
+@pytest.mark.parametrize("E,d,f,B,k,n_tile", [
+    (8, 4096, 14336, 16, 2, 16),   # Mixtral decode: 2-4 experts, one per group
+    (128, 2048, 768, 16, 8, 16),   # Qwen3 decode: many small experts, 3 groups
+    (64, 2048, 1408, 64, 6, 64),   # DSV2-shaped (GEMM2 K/64 = 22), wider tile
+])
+def test_fused_expert_groups(cuda_ok, E, d, f, B, k, n_tile):
+    """Interleaved expert-group phases (G1(0), G1(1), G2(0), ..., BMOE_FFN_GROUPS)
+    change where the stream-K ranges split tiles, so partial sums are added
+    at other points: within fp32 rounding of the one-range kernel (and of the
+    torch fp32 reference within the bf16 bound), and bitwise repeatable."""
+    import os
+    rng = np.random.default_rng(E + B + d + 1)
+    y, ref32, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, ops.ACT_SWIGLU, n_tile)
+    rows = int(perm.offset[-1])
+    bo = _t(buf_of)
+    saved = os.environ.get("BMOE_FFN_GROUPS")
+    try:
+        os.environ["BMOE_FFN_GROUPS"] = "1"
+        one = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
+        for g in ("2", "3", "4"):
+            os.environ["BMOE_FFN_GROUPS"] = g
+            first = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
+            for _ in range(5):
+                assert torch.equal(ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows], first)
+            rel = ((first - one).norm(dim=1) / one.norm(dim=1).clamp_min(1e-30)).max().item()
+            assert rel <= 1e-5, (g, rel)
+    finally:
+        if saved is None:
+            os.environ.pop("BMOE_FFN_GROUPS", None)
+        else:
+            os.environ["BMOE_FFN_GROUPS"] = saved
