@@ -487,7 +487,13 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
     const int spt1 = P1.K / (kBK * KPS1), spt2 = P2.K / (kBK * KPS2);
     const int mtiles1 = P1.M / kBM, mtiles2 = P2.M / kBM;
     // expert groups (see phase_at): only with per-expert readiness, at most one per expert
-    const int ng = h_ready ? max(1, min(fp.groups, sched.n_act)) : 1;
+    // and only while every GEMM1 phase keeps >= group_min_iters k-steps per CTA (short phases
+    // split every tile across many CTAs: measured slower for calls of many small experts)
+    const long long T1all = (long long)total_tiles(sched, mtiles1) * spt1;
+    const int ng = h_ready ? max(1, (int)min((long long)min(fp.groups, sched.n_act),
+                                             fp.group_min_iters > 0 ? T1all / ((long long)fp.group_min_iters * Gn)
+                                                                    : (long long)kMaxGroups))
+                           : 1;
     const int n_ph = 2 * ng;
     const int last_g1 = ng == 1 ? 0 : n_ph - 3;  // the phase index of G1(ng - 1)
 

@@ -601,17 +601,20 @@ def test_fused_workspace_shared_across_token_tiles(cuda_ok):
     (64, 2048, 1408, 64, 6, 64),   # DSV2-shaped (GEMM2 K/64 = 22), wider tile
 ])
 def test_fused_expert_groups(cuda_ok, E, d, f, B, k, n_tile):
-    """Interleaved expert-group phases (G1(0), G1(1), G2(0), ..., BMOE_FFN_GROUPS)
-    change where the stream-K ranges split tiles, so partial sums are added
-    at other points: within fp32 rounding of the one-range kernel (and of the
-    torch fp32 reference within the bf16 bound), and bitwise repeatable."""
+    """Interleaved expert-group phases (G1(0), G1(1), G2(0), ..., BMOE_FFN_GROUPS,
+    forced here at every size with BMOE_FFN_GROUP_ITERS=0) change where the
+    stream-K ranges split tiles, so GEMM1's partial sums meet in another
+    order and an H value near a bf16 rounding boundary can round the other
+    way: within 5e-3 of the one-range kernel (the bf16 tolerance is 2e-2),
+    and bitwise repeatable."""
     import os
     rng = np.random.default_rng(E + B + d + 1)
     y, ref32, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, ops.ACT_SWIGLU, n_tile)
     rows = int(perm.offset[-1])
     bo = _t(buf_of)
-    saved = os.environ.get("BMOE_FFN_GROUPS")
+    saved = {v: os.environ.get(v) for v in ("BMOE_FFN_GROUPS", "BMOE_FFN_GROUP_ITERS")}
     try:
+        os.environ["BMOE_FFN_GROUP_ITERS"] = "0"
         os.environ["BMOE_FFN_GROUPS"] = "1"
         one = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
         for g in ("2", "3", "4"):
@@ -620,9 +623,10 @@ def test_fused_expert_groups(cuda_ok, E, d, f, B, k, n_tile):
             for _ in range(5):
                 assert torch.equal(ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows], first)
             rel = ((first - one).norm(dim=1) / one.norm(dim=1).clamp_min(1e-30)).max().item()
-            assert rel <= 1e-5, (g, rel)
+            assert rel <= 5e-3, (g, rel)
     finally:
-        if saved is None:
-            os.environ.pop("BMOE_FFN_GROUPS", None)
-        else:
-            os.environ["BMOE_FFN_GROUPS"] = saved
+        for v, val in saved.items():
+            if val is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = val
