@@ -36,28 +36,42 @@ __global__ void __launch_bounds__(kCountThreads) coact_count_kernel(const int32_
     const long long t0 = (long long)blockIdx.x * per_block;
     const long long t1 = min(N, t0 + per_block);
     if constexpr (KC == 8) {
+        // The eight ids are sorted first (a 19-comparator network on unsigned values, so
+        // negative ids sort last like out-of-range ones): range and duplicate checks become
+        // one compare on the largest id and seven on neighbours, and every pair (x < y) is
+        // already ordered, so its cell is rowbase(id_x) + id_y with the seven row bases
+        // computed once -- one add per pair instead of a min, max and triangle index.
         for (long long t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
             const int4 *p = reinterpret_cast<const int4 *>(topk + t * 8);
             int4 a = __ldg(p), b = __ldg(p + 1);
-            int id[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            bool bad = false;  // profiler.py:76-80: ids in range and distinct, else the row is rejected
+            unsigned id[8] = {(unsigned)a.x, (unsigned)a.y, (unsigned)a.z, (unsigned)a.w,
+                              (unsigned)b.x, (unsigned)b.y, (unsigned)b.z, (unsigned)b.w};
+            auto cx = [&](int u, int v) {
+                const unsigned lo = min(id[u], id[v]), hi = max(id[u], id[v]);
+                id[u] = lo;
+                id[v] = hi;
+            };
+            // Batcher odd-even merge sort, n = 8
+            cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7);
+            cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7);
+            cx(1, 2); cx(5, 6);
+            cx(0, 4); cx(1, 5); cx(2, 6); cx(3, 7);
+            cx(2, 4); cx(3, 5);
+            cx(1, 2); cx(3, 4); cx(5, 6);
+            // profiler.py:76-80: ids in range and distinct, else the row is rejected
+            bool bad = id[7] >= (unsigned)E;
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                bad |= (unsigned)id[x] >= (unsigned)E;
-#pragma unroll
-                for (int y = x + 1; y < 8; ++y) bad |= id[x] == id[y];
-            }
+            for (int x = 0; x < 7; ++x) bad |= id[x] == id[x + 1];
             if (bad) {
                 atomicAdd(invalid, 1);
                 continue;
             }
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
+            for (int x = 0; x < 7; ++x) {
+                const int i = (int)id[x];
+                const int base = i * E - ((i * (i - 1)) >> 1) - i;  // tri(i, j, E) = base + j
 #pragma unroll
-                for (int y = x + 1; y < 8; ++y) {
-                    int i = min(id[x], id[y]), j = max(id[x], id[y]);
-                    atomicAdd(&tcount[tri(i, j, E)], 1u);
-                }
+                for (int y = x + 1; y < 8; ++y) atomicAdd(&tcount[base + (int)id[y]], 1u);
             }
         }
     } else {
