@@ -630,3 +630,30 @@ def test_fused_expert_groups(cuda_ok, E, d, f, B, k, n_tile):
                 os.environ.pop(v, None)
             else:
                 os.environ[v] = val
+
+
+def test_kernel_timing_spans(cuda_ok):
+    """The bench's FFN timing hook: every fused decode call gets a CUDA-event
+    duration and an on-device span (first CTA in to last CTA out) with
+    0 < span <= events; prefill-width calls report span 0."""
+    from paper_2511_10054_b200 import _native as N
+    E, d, f, B, k = 8, 1024, 2048, 16, 2
+    _, _, (xp, perm, arena, buf_of, ws) = _bf16_case(np.random.default_rng(3), E, d, f, B, k, ops.ACT_SWIGLU, 16)
+    bo = _t(buf_of)
+    _, _, (xp2, perm2, arena2, buf_of2, ws2) = _bf16_case(np.random.default_rng(4), E, d, f, 300, k,
+                                                          ops.ACT_SWIGLU, 128)
+    N.lib().bm_set_kernel_timing(1)
+    try:
+        for _ in range(3):
+            ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)
+        ops.expert_ffn_bf16(xp2, perm2, arena2, _t(buf_of2), d, f, ops.ACT_SWIGLU, ws2)
+        times = np.zeros(16, np.float32)
+        n = int(N.lib().bm_kernel_times(times.ctypes.data, times.size))
+        spans = np.zeros(8, np.float32)
+        m = int(N.lib().bm_kernel_spans(spans.ctypes.data, spans.size))
+    finally:
+        N.lib().bm_set_kernel_timing(0)
+    assert n == 8 and m == 4
+    ev = times[0:n:2]
+    assert np.all(spans[:3] > 0) and np.all(spans[:3] <= ev[:3] + 1e-3), (spans, ev)
+    assert spans[3] == 0.0
