@@ -27,6 +27,12 @@ int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const vo
                      bm_stream_t stream);
 int random_plan_batch(const int32_t *topk, int64_t B, int64_t k, const uint32_t *resident_bits, int64_t E,
                       bm_pcg64 *rng, int32_t *executed, uint8_t *kind, int32_t *used);
+namespace ffn {  // timing of FFN launches inside captured graphs (ffn_tc.cu)
+void *ffn_timing_take_capture();
+void ffn_timing_replayed(void *group);
+int ffn_timing_harvest();
+void ffn_timing_release(void *group);
+}  // namespace ffn
 }
 
 #define ENG_CUDA(expr)                                                                                    \
@@ -199,6 +205,7 @@ struct bm_engine {
     cudaStream_t cap_stream = nullptr;
     bool use_graphs = true;
     std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> g_pre, g_post, g_post2;
+    std::map<cudaGraphExec_t, void *> timing_groups;  // timed FFN calls captured in a graph
     // split expert counts: resident | fetched (early + late) -> early | late
     int32_t *count_a = nullptr, *count_b = nullptr, *count_bc = nullptr, *count_c = nullptr;
     bool overlap_fetch = true;  // run resident experts' GEMMs while misses stream in (BMOE_OVERLAP=0 disables)
@@ -438,24 +445,35 @@ struct bm_engine {
 
     // Replay a per-(layer, B) CUDA graph of enqueue_pre/post (captured on the
     // second occurrence; the first runs eagerly and warms lazy attributes).
+    // With kernel timing on, separate graphs are captured whose FFN launches are bracketed
+    // by external event nodes (and span stamps), so the timing pass measures the kernels as
+    // the timed run launches them; each replay's times are read back after the step.
     template <typename Body>
     int run(std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> &cache_g, int l, int variant,
             float *h, int64_t B, cudaStream_t s, Body body) {
         (void)h;
-        if (!use_graphs || bm_kernel_timing_enabled()) return body(s);
-        auto &slot = cache_g[{l * 3 + variant, B}];
+        if (!use_graphs) return body(s);
+        const bool timing = bm_kernel_timing_enabled() != 0;
+        auto &slot = cache_g[{l * 3 + variant + (timing ? (1 << 20) : 0), B}];
         if (slot.second == nullptr) {
-            if (slot.first++ == 0) return body(s);
+            if (!timing && slot.first++ == 0) return body(s);
             cudaGraph_t g;
             ENG_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
             int rc = body(cap_stream);
             cudaError_t ce = cudaStreamEndCapture(cap_stream, &g);
+            void *grp = bm::ffn::ffn_timing_take_capture();
+            if (rc != BM_OK || ce != cudaSuccess) bm::ffn::ffn_timing_release(grp);
             if (rc != BM_OK) return rc;
             ENG_CUDA(ce);
             ENG_CUDA(cudaGraphInstantiate(&slot.second, g, 0));
             cudaGraphDestroy(g);
+            if (grp) timing_groups[slot.second] = grp;
         }
         ENG_CUDA(cudaGraphLaunch(slot.second, s));
+        if (timing) {
+            auto it = timing_groups.find(slot.second);
+            if (it != timing_groups.end()) bm::ffn::ffn_timing_replayed(it->second);
+        }
         return BM_OK;
     }
 
@@ -665,6 +683,7 @@ struct bm_engine {
         for (auto *m : {&g_pre, &g_post, &g_post2})
             for (auto &kv : *m)
                 if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
+        for (auto &kv : timing_groups) bm::ffn::ffn_timing_release(kv.second);
         void *dptrs[] = {exec_ext, kind_ext, probs_ext, logits, probs, y_perm, h_ws, tae, margin, delta, used,
                          plan_dev, h_int, bm_dev_all, bo_dev_all, count, offset, row_token, slot_row, perm_scratch,
                          x_perm, ffn_ws,
@@ -929,6 +948,10 @@ extern "C" int bm_engine_step(bm_engine *e, float *h, int64_t B, const int32_t *
     ENG_CUDA(cudaMemcpyAsync(e->h_int, h, (size_t)B * e->d * sizeof(float), cudaMemcpyDeviceToDevice, s));
     for (int l = 0; l < e->L; ++l) ENG_TRY(e->layer_step(l, e->h_int, B, tokens_host, s));
     ENG_CUDA(cudaMemcpyAsync(h, e->h_int, (size_t)B * e->d * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    if (bm_kernel_timing_enabled()) {  // read the timed graph launches before their next replay
+        ENG_CUDA(cudaStreamSynchronize(s));
+        ENG_TRY(bm::ffn::ffn_timing_harvest());
+    }
     e->stats.tokens += B;
     return BM_OK;
 }

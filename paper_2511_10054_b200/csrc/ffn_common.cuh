@@ -279,6 +279,11 @@ bool use_2sm(const GemmParams &g);                                      // CTA-p
 int kps_for(int nmat, long long K, long long n_tile);                   // k-blocks per pipeline stage
 int launch_fixup(const GemmParams &g, int mode, uint4 *h_planes, int h_rmax, float *y_perm, int blocks,
                  cudaStream_t s);                                       // stream-K split-tile reduction
+// kernel timing of FFN calls inside captured graphs (ffn_tc.cu; the engine's timing pass)
+void *ffn_timing_take_capture();      // the timed calls recorded during the capture just ended
+void ffn_timing_replayed(void *group);  // that graph was launched
+int ffn_timing_harvest();             // read the replayed groups (their launches completed)
+void ffn_timing_release(void *group);
 // decode (ffn_decode.cu)
 void fused_kps(int nmat1, long long d, long long f, long long n_tile, int *k1, int *k2);
 int launch_fused_dispatch(const FusedParams &fp, int nmat1, int kps1, int kps2, int G, cudaStream_t s);

@@ -40,37 +40,61 @@ long long max_tiles(long long E, long long M, long long r_max, long long n_tile)
     return (M / kBM) * (segs + r_max / n_tile + 1);
 }
 
-// kernel timing (for the bench's roofline), off by default
+// kernel timing (for the bench's roofline), off by default. Each timed call
+// is a record of 4 events (before/after GEMM1, before/after GEMM2; a fused
+// decode call is one kernel: events 2-3 null) and, for fused calls, an
+// on-device span slot [first CTA entry, last CTA exit] (globaltimer ns).
+// Eager calls' records are read when the times are asked for. Calls made
+// while the stream is being captured record their events as external
+// event nodes of the graph: their records go to the capture's group
+// (ffn_timing_take_capture), the engine marks the group after each replay
+// of its graph (ffn_timing_replayed) and reads it back before the next
+// replay (ffn_timing_harvest), so CUDA graphs time their FFN launches too.
+struct CallRec {
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t span_slot = -1;
+};
 struct Timing {
     bool enabled = false;
-    std::vector<cudaEvent_t> ev;  // 4 per call: before/after GEMM1, before/after GEMM2
-    // fused decode calls also stamp their on-device span: [first CTA entry, last CTA exit]
-    // (globaltimer ns), one slot pair per timed call, beside the events
-    unsigned long long *span = nullptr;
-    int64_t span_cap = 0, span_n = 0;
-    std::vector<int64_t> span_of_call;  // slot per call, -1 for calls without one
+    std::vector<CallRec> eager;              // eager calls since timing was enabled, unread
+    std::vector<CallRec> capturing;          // calls recorded into the graph being captured
+    std::vector<std::vector<CallRec> *> replayed;  // graph groups replayed since the last harvest
+    std::vector<float> res_ms;               // 2 per read call (GEMM1 ms, GEMM2 ms)
+    std::vector<float> res_span;             // 1 per read call (span ms, 0 without one)
+    unsigned long long *span = nullptr;      // slots: eager ones from the bottom, graph ones from the top
+    int64_t span_cap = 0, span_n = 0, span_graph_n = 0;
     std::mutex mu;
 } g_timing;
 
-// Timing pass only: hold the stream for a few microseconds before a timed
-// call's start event, so the host has enqueued event + kernel + event before
-// the GPU reaches them and the interval does not include the host's launch
-// latency (the engine's timing pass launches eagerly; its timed runs replay
-// CUDA graphs, where consecutive kernels start back to back).
+bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
+}
+
+// Timing pass only: hold the stream for a few microseconds before an eager
+// timed call's start event, so the host has enqueued event + kernel + event
+// before the GPU reaches them (not needed inside a graph).
 __global__ void hold_kernel(unsigned long long ns) {
     const unsigned long long t0 = ptx::globaltimer();
     while (ptx::globaltimer() - t0 < ns) __nanosleep(500);
 }
 int hold_stream(cudaStream_t s) {
     static const long long ns = getenv("BMOE_TIMING_HOLD_NS") ? atoll(getenv("BMOE_TIMING_HOLD_NS")) : 30000;
-    if (ns <= 0) return BM_OK;
+    if (ns <= 0 || capturing(s)) return BM_OK;
     hold_kernel<<<1, 32, 0, s>>>((unsigned long long)ns);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }
 
-// next span slot (reset to [UINT64_MAX, 0] on s) for a fused call being timed, or null
-unsigned long long *next_span(cudaStream_t s) {
+CallRec &new_call(cudaStream_t s) {
+    auto &v = capturing(s) ? g_timing.capturing : g_timing.eager;
+    v.emplace_back();
+    return v.back();
+}
+
+// a span slot (reset to [UINT64_MAX, 0] on s, as graph nodes when capturing) for the
+// fused call `rec` being timed, or null
+unsigned long long *next_span(cudaStream_t s, CallRec &rec) {
     if (!g_timing.span) {
         g_timing.span_cap = 1 << 16;
         if (cudaMalloc(&g_timing.span, (size_t)g_timing.span_cap * 2 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -78,20 +102,55 @@ unsigned long long *next_span(cudaStream_t s) {
             return nullptr;
         }
     }
-    if (g_timing.span_n >= g_timing.span_cap) return nullptr;
-    unsigned long long *p = g_timing.span + 2 * g_timing.span_n;
+    int64_t slot;
+    if (capturing(s)) {
+        if (g_timing.span_n + g_timing.span_graph_n >= g_timing.span_cap) return nullptr;
+        slot = g_timing.span_cap - 1 - g_timing.span_graph_n++;
+    } else {
+        if (g_timing.span_n + g_timing.span_graph_n >= g_timing.span_cap) return nullptr;
+        slot = g_timing.span_n++;
+    }
+    unsigned long long *p = g_timing.span + 2 * slot;
     cudaMemsetAsync(p, 0xff, sizeof(unsigned long long), s);
     cudaMemsetAsync(p + 1, 0, sizeof(unsigned long long), s);
-    g_timing.span_of_call.push_back(g_timing.span_n++);
+    rec.span_slot = slot;
     return p;
 }
 
-int record_event(cudaStream_t s) {
+int record_event(cudaStream_t s, CallRec &rec, int i) {
     cudaEvent_t e;
     BM_CUDA_TRY(cudaEventCreate(&e));
-    BM_CUDA_TRY(cudaEventRecord(e, s));
-    g_timing.ev.push_back(e);
+    if (capturing(s))
+        BM_CUDA_TRY(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));  // a node the host can read
+    else
+        BM_CUDA_TRY(cudaEventRecord(e, s));
+    rec.ev[i] = e;
     return BM_OK;
+}
+
+// read one record's times into the results (its events must have completed)
+int read_call(const CallRec &r) {
+    float a = 0.f, b = 0.f, sp = 0.f;
+    if (cudaEventElapsedTime(&a, r.ev[0], r.ev[1]) != cudaSuccess) return BM_ECUDA;
+    if (r.ev[2] && cudaEventElapsedTime(&b, r.ev[2], r.ev[3]) != cudaSuccess) return BM_ECUDA;
+    if (r.span_slot >= 0) {
+        unsigned long long v[2];
+        if (cudaMemcpy(v, g_timing.span + 2 * r.span_slot, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return BM_ECUDA;
+        sp = (float)((double)(v[1] - v[0]) * 1e-6);
+    }
+    g_timing.res_ms.push_back(a);
+    g_timing.res_ms.push_back(b);
+    g_timing.res_span.push_back(sp);
+    return BM_OK;
+}
+
+void destroy_call(CallRec &r) {
+    for (cudaEvent_t &e : r.ev)
+        if (e) {
+            cudaEventDestroy(e);
+            e = nullptr;
+        }
 }
 
 }  // namespace ffn
@@ -242,6 +301,7 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
     g1.arena_bytes = g2.arena_bytes = n_bufs * buf_bytes;
     const bool timing = g_timing.enabled;
     std::lock_guard<std::mutex> lk(g_timing.mu);
+    CallRec *rec = timing ? &new_call(s) : nullptr;
     if (fused) {
         int k1 = 1, k2 = 1;
         fused_kps(nmat1, d, f, n_tile, &k1, &k2);
@@ -274,26 +334,20 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         if (fuse_cmb) fp.cmb = *cmb;
         // timing record: [start, end] of the one kernel, then an empty GEMM2 interval
         if (timing) {
-            fp.span = next_span(s);
+            fp.span = next_span(s, *rec);
             if (int rc = hold_stream(s)) return rc;
         }
-        if (timing && record_event(s)) return BM_ECUDA;
+        if (timing && record_event(s, *rec, 0)) return BM_ECUDA;
         const int rc = launch_fused_dispatch(fp, nmat1, k1, k2, G, s);
         if (rc) return rc;
-        if (timing) {
-            if (record_event(s)) return BM_ECUDA;
-            g_timing.ev.push_back(nullptr);  // no second kernel: GEMM2 interval reported as 0
-            g_timing.ev.push_back(nullptr);
-        }
+        if (timing && record_event(s, *rec, 1)) return BM_ECUDA;  // one kernel: GEMM2 interval reported as 0
         return fuse_cmb ? BM_OK : separate_combine();
     }
-    if (timing) {
-        g_timing.span_of_call.push_back(-1);
+    if (timing)
         if (int rc = hold_stream(s)) return rc;
-    }
-    if (timing && record_event(s)) return BM_ECUDA;
+    if (timing && record_event(s, *rec, 0)) return BM_ECUDA;
     if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
-    if (timing && record_event(s)) return BM_ECUDA;
+    if (timing && record_event(s, *rec, 1)) return BM_ECUDA;
     if (dp) {  // every tile was finished by its GEMM epilogue
         // GEMM2 (one accumulator per tile) keeps a double-buffered 256-token
         // tile on CTA pairs: wider tiles halve its per-MAC operand traffic
@@ -301,47 +355,88 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
             const char *ev = getenv("BMOE_NT2");
             g2.n_tile = ev ? atoi(ev) : 256;
         }
-        if (timing && record_event(s)) return BM_ECUDA;
+        if (timing && record_event(s, *rec, 2)) return BM_ECUDA;
         if (int rc = launch_gemm_dispatch(g2, G, s)) return rc;
-        if (timing && record_event(s)) return BM_ECUDA;
+        if (timing && record_event(s, *rec, 3)) return BM_ECUDA;
         return separate_combine();
     }
     const int fix_blocks = 4 * G;
     if (int rc = launch_fixup(g1, act == BM_ACT_SWIGLU ? 0 : 1, reinterpret_cast<uint4 *>(h_planes), (int)r_max,
                               nullptr, fix_blocks, s))
         return rc;
-    if (timing && record_event(s)) return BM_ECUDA;
+    if (timing && record_event(s, *rec, 2)) return BM_ECUDA;
     if (int rc = launch_gemm_dispatch(g2, G, s)) return rc;
-    if (timing && record_event(s)) return BM_ECUDA;
+    if (timing && record_event(s, *rec, 3)) return BM_ECUDA;
     if (int rc = launch_fixup(g2, 2, nullptr, 0, y_perm, fix_blocks, s)) return rc;
     return separate_combine();
 }
 
 extern "C" int bm_set_kernel_timing(int32_t enable) {
     std::lock_guard<std::mutex> lk(g_timing.mu);
-    for (cudaEvent_t e : g_timing.ev)
-        if (e) cudaEventDestroy(e);
-    g_timing.ev.clear();
-    g_timing.span_of_call.clear();
+    for (CallRec &r : g_timing.eager) destroy_call(r);
+    g_timing.eager.clear();
+    g_timing.replayed.clear();
+    g_timing.res_ms.clear();
+    g_timing.res_span.clear();
     g_timing.span_n = 0;
     g_timing.enabled = enable != 0;
     return BM_OK;
 }
+
+namespace bm {
+namespace ffn {
+// the engine's side of graph timing (see Timing)
+void *ffn_timing_take_capture() {
+    std::lock_guard<std::mutex> lk(g_timing.mu);
+    if (g_timing.capturing.empty()) return nullptr;
+    auto *grp = new std::vector<CallRec>(std::move(g_timing.capturing));
+    g_timing.capturing.clear();
+    return grp;
+}
+void ffn_timing_replayed(void *group) {
+    if (!group) return;
+    std::lock_guard<std::mutex> lk(g_timing.mu);
+    if (g_timing.enabled) g_timing.replayed.push_back(static_cast<std::vector<CallRec> *>(group));
+}
+int ffn_timing_harvest() {  // the replayed graphs' launches must have completed
+    std::lock_guard<std::mutex> lk(g_timing.mu);
+    for (auto *grp : g_timing.replayed)
+        for (const CallRec &r : *grp)
+            if (int rc = read_call(r)) return rc;
+    g_timing.replayed.clear();
+    return BM_OK;
+}
+void ffn_timing_release(void *group) {
+    if (!group) return;
+    std::lock_guard<std::mutex> lk(g_timing.mu);
+    auto *grp = static_cast<std::vector<CallRec> *>(group);
+    for (CallRec &r : *grp) destroy_call(r);
+    delete grp;
+}
+// eager records -> results (synchronises on their last events)
+int read_eager() {
+    for (CallRec &r : g_timing.eager) {
+        cudaEvent_t last = r.ev[3] ? r.ev[3] : r.ev[1];
+        if (cudaEventSynchronize(last) != cudaSuccess) return BM_ECUDA;
+        if (int rc = read_call(r)) return rc;
+        destroy_call(r);
+    }
+    g_timing.eager.clear();
+    return BM_OK;
+}
+}  // namespace ffn
+}  // namespace bm
 
 // One float per bm_expert_ffn_bf16 call since timing was enabled: the fused
 // decode kernel's on-device span in ms (first CTA entry to last CTA exit,
 // globaltimer), 0 for calls without one (prefill GEMMs). Synchronises.
 extern "C" int64_t bm_kernel_spans(float *out_host, int64_t cap) {
     std::lock_guard<std::mutex> lk(g_timing.mu);
-    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-    std::vector<unsigned long long> raw((size_t)g_timing.span_n * 2);
-    if (g_timing.span_n && cudaMemcpy(raw.data(), g_timing.span, raw.size() * sizeof(unsigned long long),
-                                      cudaMemcpyDeviceToHost) != cudaSuccess)
-        return -1;
+    if (read_eager() != BM_OK) return -1;
     int64_t n = 0;
-    for (int64_t slot : g_timing.span_of_call) {
+    for (float v : g_timing.res_span) {
         if (n >= cap) break;
-        out_host[n++] = slot < 0 ? 0.f : (float)((double)(raw[2 * slot + 1] - raw[2 * slot]) * 1e-6);
+        out_host[n++] = v;
     }
     return n;
 }
@@ -349,18 +444,15 @@ extern "C" int64_t bm_kernel_spans(float *out_host, int64_t cap) {
 extern "C" int bm_kernel_timing_enabled(void) { return g_timing.enabled ? 1 : 0; }
 
 // Two floats per bm_expert_ffn_bf16 call since timing was enabled: GEMM1
-// and GEMM2 kernel durations in ms (CUDA events on the launching stream).
+// and GEMM2 kernel durations in ms (CUDA events on the launching stream,
+// inside the captured graph for calls replayed from one).
 extern "C" int64_t bm_kernel_times(float *out_host, int64_t cap) {
     std::lock_guard<std::mutex> lk(g_timing.mu);
+    if (read_eager() != BM_OK) return -1;
     int64_t n = 0;
-    for (size_t i = 0; i + 3 < g_timing.ev.size() && n + 2 <= cap; i += 4) {
-        const bool one = g_timing.ev[i + 2] == nullptr;  // fused decode call: one kernel
-        if (cudaEventSynchronize(g_timing.ev[one ? i + 1 : i + 3]) != cudaSuccess) return -1;
-        float a = 0.f, b = 0.f;
-        cudaEventElapsedTime(&a, g_timing.ev[i], g_timing.ev[i + 1]);
-        if (!one) cudaEventElapsedTime(&b, g_timing.ev[i + 2], g_timing.ev[i + 3]);
-        out_host[n++] = a;
-        out_host[n++] = b;
+    for (float v : g_timing.res_ms) {
+        if (n >= cap) break;
+        out_host[n++] = v;
     }
     return n;
 }
