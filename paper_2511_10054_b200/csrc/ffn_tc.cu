@@ -95,13 +95,7 @@ CallRec &new_call(cudaStream_t s) {
 // a span slot (reset to [UINT64_MAX, 0] on s, as graph nodes when capturing) for the
 // fused call `rec` being timed, or null
 unsigned long long *next_span(cudaStream_t s, CallRec &rec) {
-    if (!g_timing.span) {
-        g_timing.span_cap = 1 << 16;
-        if (cudaMalloc(&g_timing.span, (size_t)g_timing.span_cap * 2 * sizeof(unsigned long long)) != cudaSuccess) {
-            g_timing.span = nullptr;
-            return nullptr;
-        }
-    }
+    if (!g_timing.span) return nullptr;  // allocated when timing is switched on (not during a capture)
     int64_t slot;
     if (capturing(s)) {
         if (g_timing.span_n + g_timing.span_graph_n >= g_timing.span_cap) return nullptr;
@@ -380,6 +374,10 @@ extern "C" int bm_set_kernel_timing(int32_t enable) {
     g_timing.res_span.clear();
     g_timing.span_n = 0;
     g_timing.enabled = enable != 0;
+    if (g_timing.enabled && !g_timing.span) {
+        g_timing.span_cap = 1 << 16;
+        BM_CUDA_TRY(cudaMalloc(&g_timing.span, (size_t)g_timing.span_cap * 2 * sizeof(unsigned long long)));
+    }
     return BM_OK;
 }
 
