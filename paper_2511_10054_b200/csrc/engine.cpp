@@ -808,10 +808,6 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     if (const char *ev = getenv("BMOE_SPLIT_FETCHED")) g->split_fetched = atoi(ev) != 0;  // A/B switch
     if (const char *ev = getenv("BMOE_FUSE_COMBINE")) g->fuse_combine = atoi(ev) != 0;  // A/B switch
     if (const char *ev = getenv("BMOE_DECODE_NARROW")) g->decode_narrow = atoi(ev);       // A/B switch
-    // the fused FFN runs with 216 KB of shared memory between kernels that use little: keep the
-    // SMs in the shared-memory-heavy configuration (BMOE_PREFER_SHARED=1) instead of switching
-    if (const char *ev = getenv("BMOE_PREFER_SHARED"))
-        if (atoi(ev) != 0) ENG_CUDA(cudaDeviceSetCacheConfig(cudaFuncCachePreferShared));
     if (g->cfg.fp32_weights) g->fuse_combine = false;  // the fp32 parity path keeps K5 separate
     ENG_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
     ENG_CUDA(cudaStreamCreateWithFlags(&g->prefetch_stream, cudaStreamNonBlocking));

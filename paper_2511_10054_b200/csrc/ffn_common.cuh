@@ -260,7 +260,6 @@ struct FusedParams {
     int *h_ready;
     unsigned long long *launch_count;
     unsigned long long *span;  // kernel timing: [min entry, max exit] globaltimer of this launch, else null
-    int w2_l2_pf;              // GEMM2 stages past the smem ring prefetched into L2 on entering GEMM2
     int groups;                // expert groups whose GEMM1 / GEMM2 phases interleave (needs h_ready; <= kMaxGroups)
     int group_min_iters;       // ... while each GEMM1 phase keeps this many k-steps per CTA (0: no limit)
 };

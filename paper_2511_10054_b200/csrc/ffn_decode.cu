@@ -120,7 +120,7 @@ __device__ void fused_produce(const GemmParams &P, const Sched &s, const Geom &g
 template <int KPS>
 __device__ void fused_produce_ready(const GemmParams &P, const Sched &s, const Geom &gm, int &stage, uint32_t &phase,
                                     long long it0, long long it1, int spt, uint64_t pol, const int *h_ready,
-                                    int mtiles1, int l2_pf, unsigned long long *gate_stamp) {
+                                    int mtiles1, unsigned long long *gate_stamp) {
     constexpr uint32_t kA = (uint32_t)KPS * kATileBytes;
     const int mtiles = P.M / kBM;
     struct Cur {  // one cursor's tile cache (the tile decode and buffer lookup once per tile)
@@ -142,17 +142,6 @@ __device__ void fused_produce_ready(const GemmParams &P, const Sched &s, const G
         }
     };
     Cur ca, cb;
-    // W2 beyond the smem ring goes to L2 now: HBM keeps streaming through the GEMM1 tail and
-    // the wait for H, and those stages later load from L2 (no slot is needed for a prefetch)
-    if (l2_pf > 0) {
-        Cur cp;
-        const long long p1 = min(it1, it0 + (long long)gm.stages + l2_pf);
-        for (long long j = it0 + gm.stages; j < p1; ++j) {
-            int stp;
-            locate(cp, j, stp);
-            ptx::bulk_prefetch_l2(cp.a + (long long)stp * kA, kA);
-        }
-    }
     long long ia = it0, ib = it0;  // next iteration whose A part / H part is issued
     int stage_a = stage;
     uint32_t phase_a = phase;
@@ -510,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
                     fused_produce<NMAT1, KPS1>(P1, sched, gm, stage, phase, i0, i1, spt1, pol, nullptr, 0, 0);
                 else if (h_ready)
                     fused_produce_ready<KPS2>(P2, sched, gm, stage, phase, i0, i1, spt2, pol, h_ready, mtiles1,
-                                              fp.w2_l2_pf, tr && ph.g == 0 ? tr + 5 : nullptr);
+                                              tr && ph.g == 0 ? tr + 5 : nullptr);
                 else
                     fused_produce<1, KPS2>(P2, sched, gm, stage, phase, i0, i1, spt2, pol, fp.grid_bar,
                                            bar0 + (unsigned long long)Gn, fp.prefetch_w2, tr ? tr + 5 : nullptr);

@@ -307,12 +307,10 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap,
                        reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off),
-                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr, nullptr, 0, 1, 12};
+                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr, nullptr, 1, 12};
         const char *gv = getenv("BMOE_FFN_GROUPS");  // read per call: tests switch it
         fp.groups = std::max(1, std::min(gv ? atoi(gv) : 3, kMaxGroups));
         if (const char *mi = getenv("BMOE_FFN_GROUP_ITERS")) fp.group_min_iters = std::max(0, atoi(mi));
-        static const int w2_pf = getenv("BMOE_W2_L2PF") ? atoi(getenv("BMOE_W2_L2PF")) : 0;  // measured slower: off
-        fp.w2_l2_pf = w2_pf;
         static const int h_ready = getenv("BMOE_H_READY") ? atoi(getenv("BMOE_H_READY")) : 1;
         fp.g[1].partials = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + wl.partial_off +
                                                      wl.slot_set_bytes);
