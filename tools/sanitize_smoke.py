@@ -51,6 +51,17 @@ if __name__ == "__main__":
     del os.environ["BMOE_FUSED"], os.environ["BMOE_KPS"]
     torch.cuda.synchronize()
     assert torch.equal(y0, y1)
+    # interleaved expert-group phases (forced) and the combine fused behind the FFN
+    os.environ["BMOE_FFN_GROUP_ITERS"] = "0"
+    os.environ["BMOE_FFN_GROUPS"] = "3"
+    y3 = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
+    pr = torch.rand(B2, 2).cuda()
+    h = torch.randn(B2, d).cuda()
+    ops.expert_ffn_bf16_combine(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws, pr,
+                                torch.zeros(B2, 2, dtype=torch.uint8).cuda(), h, 0.5)
+    del os.environ["BMOE_FFN_GROUP_ITERS"], os.environ["BMOE_FFN_GROUPS"]
+    torch.cuda.synchronize()
+    assert torch.isfinite(y3).all() and torch.isfinite(h).all()
     # prefill width: data-parallel tiles finished in the GEMM epilogue (n_tile 128, > 1 chunk per expert)
     B3 = 300
     tk = np.stack([rng.choice(E2, 2, replace=False) for _ in range(B3)]).astype(np.int32)
