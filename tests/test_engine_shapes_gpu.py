@@ -164,3 +164,36 @@ def test_engine_fused_combine_equals_separate_launch():
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
     assert np.array_equal(evs[0], evs[1])
     assert launches[0] - launches[1] == 3 * 4, launches
+
+
+def test_engine_varying_batch_sizes_graphs_equal_eager():
+    """One engine serving decode batches of different sizes (16, 64, 8, 64,
+    16 tokens: token tiles 16 / 64 / 16, graphs captured per (layer, B)) over
+    one FFN workspace: hidden states bitwise equal to the same sequence run
+    eagerly without graphs, and event logs equal."""
+    import os
+    wl = W.build("qwen3", layers=2, max_batch=64, profile_tokens=1024)
+    sizes = (16, 64, 8, 64, 16, 16, 64)
+    outs, evs = [], []
+    old = os.environ.get("BMOE_GRAPHS")
+    try:
+        for graphs in ("1", "0"):
+            os.environ["BMOE_GRAPHS"] = graphs
+            eng = wl.engine("buddy")
+            x = torch.from_numpy(wl.tokens(5, sum(sizes))).cuda()
+            o = 0
+            for B in sizes:
+                eng.step(x[o:o + B], np.arange(o, o + B))
+                o += B
+            torch.cuda.synchronize()
+            outs.append(x.cpu().numpy())
+            evs.append(eng.events())
+            eng.close()
+    finally:
+        if old is None:
+            os.environ.pop("BMOE_GRAPHS", None)
+        else:
+            os.environ["BMOE_GRAPHS"] = old
+        wl.close()
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    assert np.array_equal(evs[0], evs[1])
