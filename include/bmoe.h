@@ -214,12 +214,16 @@ int bm_expert_ffn_f64(const double *x_perm, const int32_t *expert_count, const i
  * weights as the M=128 operand ("swap-AB": decode token counts are the N
  * dimension), fused SwiGLU/tanh, deterministic (split tiles are summed in
  * fixed CTA order, never with float atomics). x_perm is layout 1 (bf16 SW128 planes over d). Workspace from
- * bm_expert_ffn_bf16_workspace(): holds the fp32 partial tiles, the
- * SW128 bf16 intermediate H and the split-tile / grid-barrier counters; it
- * must be ZEROED ONCE when allocated (the counters are self-cleaning).
+ * bm_expert_ffn_bf16_workspace(): the persistent state of the decode kernel
+ * (grid-barrier and launch counts, per-expert H readiness, split-tile
+ * arrival counters; at offsets that do not depend on n_tile, so a workspace
+ * sized for one n_tile serves every smaller one), the fp32 partial tiles and
+ * the SW128 bf16 intermediate H. It must be ZEROED ONCE when allocated, and
+ * serves one stream at a time (calls on it must be stream-ordered).
  * y_perm fp32 [r_max][d]. Decode-width tiles (n_tile <= 64) run as ONE
  * cooperative launch (GEMM1 -> activation -> GEMM2, split tiles reduced in
- * kernel, one grid barrier); wider tiles run GEMM + fixup kernels.
+ * kernel, each expert's GEMM2 waiting only for its own H); wider tiles run
+ * data-parallel GEMM kernels.
  * Requires d % 128 == 0, f % 128 == 0. n_tile (16..256, multiple of 16)
  * caps the per-tile token count; larger expert segments are chunked. */
 /* bf16 expert buffers use the HBM-native "UMMA-tiled" layout: each weight
