@@ -18,7 +18,8 @@ namespace {
 constexpr int kGateThreads = 256;
 constexpr int kMaxE = 256;
 constexpr int kMaxK = 32;
-constexpr int kGateUnroll = 8;
+constexpr int kGateUnroll = 16;  // float4 weight loads in flight per lane (d = 2048: a whole row at once)
+constexpr int kGateMaxSplit = 16;  // CTAs per token in a cluster (non-portable size above 8)
 
 template <typename T>
 struct Cand {
@@ -248,14 +249,23 @@ extern "C" int bm_gate_topk(const float *x, const float *wg, const float *bias, 
     // small batches: split each token over a cluster; large ones: 8 tokens per CTA
     const char *wide_env = getenv("BMOE_GATE_WIDE");  // A/B knob: 0 = one token per CTA at any B
     const bool wide = B >= 4 * 148 && (size_t)8 * d * sizeof(float) <= 200 * 1024 && !(wide_env && atoi(wide_env) == 0);
-    int nsplit = wide ? 1 : (B >= 4 * 148 ? 1 : (int)std::min<int64_t>(8, (E + 7) / 8));
-    if (const char *ev = getenv("BMOE_GATE_SPLIT"))  // A/B knob: forced cluster size (1..8)
-        if (atoi(ev) > 0 && !wide) nsplit = std::min(atoi(ev), 8);
+    // small batches: up to 16 CTAs per token (8 experts each), so every warp owns about one expert
+    // row and loads it in one round; the per-logit arithmetic does not depend on the split
+    int nsplit = wide ? 1 : (B >= 4 * 148 ? 1 : (int)std::min<int64_t>(kGateMaxSplit, (E + 7) / 8));
+    if (const char *ev = getenv("BMOE_GATE_SPLIT"))  // A/B knob: forced cluster size (1..16)
+        if (atoi(ev) > 0 && !wide) nsplit = std::min(atoi(ev), kGateMaxSplit);
     const int tok = wide ? 8 : 1;
     const size_t smem = (size_t)tok * d * sizeof(float);
     auto kern = wide ? gate_kernel<8> : gate_kernel<1>;
     if (smem > 48 * 1024)
         BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (nsplit > 8) {
+        static bool nonportable = false;
+        if (!nonportable) {
+            BM_CUDA_TRY(cudaFuncSetAttribute(gate_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            nonportable = true;
+        }
+    }
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(((B + tok - 1) / tok) * nsplit));
     lc.blockDim = dim3(kGateThreads);

@@ -4,6 +4,8 @@
 // (model.py:294-347).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "combine.cuh"
 #include "common.cuh"
 
@@ -33,20 +35,36 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(const int32_t *__
     for (int i = tid; i < nslots; i += blockDim.x)
         if (kind[i] != BM_KIND_DROPPED) atomicAdd(&cnt[executed[i]], 1);
     __syncthreads();
-    if (tid == 0) {
-        int run = 0;
-        for (int e = 0; e < E; ++e) {
-            off[e] = run;
-            run += (cnt[e] + align - 1) / align * align;
+    if (warp == 0) {  // segment offsets: one warp scans the padded counts (8 experts per lane)
+        constexpr int kPer = kPermMaxE / 32;
+        int v[kPer], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int e = (int)lane * kPer + j;
+            v[j] = e < E ? (cnt[e] + align - 1) / align * align : 0;
+            sum += v[j];
         }
-        off[E] = run;
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += y;
+        }
+        int run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int e = (int)lane * kPer + j;
+            if (e < E) off[e] = run;
+            run += v[j];
+        }
+        if (lane == 31) off[E] = incl;
     }
     __syncthreads();
     for (int e = tid; e < E; e += blockDim.x) expert_count[e] = cnt[e];
     for (int e = tid; e <= E; e += blockDim.x) expert_offset[e] = off[e];
-    // padding rows
-    for (int e = 0; e < E; ++e)
-        for (int r = off[e] + cnt[e] + tid; r < off[e + 1]; r += blockDim.x) row_token[r] = -1;
+    // padding rows (fewer than `align` per expert)
+    for (int e = tid; e < E; e += blockDim.x)
+        for (int r = off[e] + cnt[e]; r < off[e + 1]; ++r) row_token[r] = -1;
     // pass 2: stable rank of each slot inside its expert segment, chunk by chunk
     const int nw = blockDim.x >> 5;
     for (int c0 = 0; c0 < nslots; c0 += blockDim.x) {
@@ -347,8 +365,11 @@ extern "C" int bm_permute_ws(const int32_t *executed, const uint8_t *kind, int64
         BM_LAUNCH_CHECK();
         return BM_OK;
     }
-    permute_kernel<<<1, kPermThreads, 0, st>>>(executed, kind, (int)nslots, (int)k, (int)E, (int)row_align,
-                                               expert_count, expert_offset, row_token, slot_row);
+    // one CTA, as many warps as the slots need (a decode plan of 128 slots: 4 warps, so the
+    // per-chunk loops over warps and the barriers stay short); ranks do not depend on it
+    const int threads = (int)std::min<int64_t>(kPermThreads, std::max<int64_t>(64, (nslots + 31) / 32 * 32));
+    permute_kernel<<<1, threads, 0, st>>>(executed, kind, (int)nslots, (int)k, (int)E, (int)row_align,
+                                          expert_count, expert_offset, row_token, slot_row);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }
