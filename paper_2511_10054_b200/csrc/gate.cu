@@ -71,30 +71,30 @@ __device__ void select_and_gate(const T *z, int E, int k, double temperature, do
         }
     }
     __syncwarp();
+    // softmax(z/T) restricted to the selection (model.py:259,262-263): the max
+    // over all E of z/T is the top-1's, the full denominator cancels in the
+    // renormalisation. Lane i evaluates the exp / log of selected value i (the
+    // f64 transcendentals in parallel); the sums run in index order on lane 0,
+    // exactly as a sequential loop would add them.
+    const double zmax = sel_z[0] / temperature;
+    const double ei = lane < (unsigned)k ? exp(sel_z[lane] / temperature - zmax) : 0.0;
+    double s = 0.0;
+    for (int i = 0; i < k; ++i) s += __shfl_sync(0xffffffffu, ei, i);  // every lane: the same order
+    const double pi = ei / s;
+    const double hi = (lane < (unsigned)k && pi > 0.0) ? pi * log(pi) : 0.0;
+    if (lane < (unsigned)k) {
+        topk[lane] = sel_i[lane];
+        if (probs) probs[lane] = (float)pi;
+        if (probs64) probs64[lane] = pi;
+    }
+    double h = 0.0;
+    for (int i = 0; i < k; ++i) h -= __shfl_sync(0xffffffffu, hi, i);
+    const double p0 = __shfl_sync(0xffffffffu, pi, 0), p1 = __shfl_sync(0xffffffffu, pi, 1);
     if (lane == 0) {
-        // softmax(z/T) restricted to the selection (model.py:259,262-263):
-        // the max over all E of z/T is the top-1's, the full denominator
-        // cancels in the renormalisation.
-        double zmax = sel_z[0] / temperature;
-        double e[kMaxK];
-        double s = 0.0;
-        for (int i = 0; i < k; ++i) {
-            e[i] = exp(sel_z[i] / temperature - zmax);
-            s += e[i];
-        }
-        double h = 0.0;
-        for (int i = 0; i < k; ++i) {
-            double p = e[i] / s;
-            e[i] = p;
-            topk[i] = sel_i[i];
-            if (probs) probs[i] = (float)p;
-            if (probs64) probs64[i] = p;
-            if (p > 0.0) h -= p * log(p);
-        }
         double t = 0.0, m = 1.0;
         if (k > 1) {
             t = fmin(1.0, fmax(0.0, h / log((double)k)));
-            m = e[0] - e[1];
+            m = p0 - p1;
         }
         if (tae) *tae = t;
         if (margin) *margin = m;
