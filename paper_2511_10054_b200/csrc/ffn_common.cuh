@@ -262,6 +262,7 @@ struct FusedParams {
     unsigned long long *span;  // kernel timing: [min entry, max exit] globaltimer of this launch, else null
     int groups;                // expert groups whose GEMM1 / GEMM2 phases interleave (needs h_ready; <= kMaxGroups)
     int group_min_iters;       // ... while each GEMM1 phase keeps this many k-steps per CTA (0: no limit)
+    int min_iters;             // k-steps per CTA below which a phase runs on fewer CTAs (1: all CTAs)
 };
 constexpr int kMaxGroups = 4;
 constexpr int kTracePts = 12;

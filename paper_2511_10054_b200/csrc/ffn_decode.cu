@@ -379,7 +379,7 @@ struct Phase {
     long long base, T;
 };
 __device__ __forceinline__ Phase phase_at(int p, int ng, const Sched &s, int mtiles1, int mtiles2, int spt1,
-                                          int spt2, int Gn) {
+                                          int spt2, int Gn, int min_iters) {
     Phase ph;
     if (p == 0) {
         ph.g2 = false;
@@ -396,7 +396,10 @@ __device__ __forceinline__ Phase phase_at(int p, int ng, const Sched &s, int mti
     const int mt = ph.g2 ? mtiles2 : mtiles1, spt = ph.g2 ? spt2 : spt1;
     ph.base = (long long)mt * s.chunk_prefix[a0] * spt;
     ph.T = (long long)mt * (s.chunk_prefix[a1] - s.chunk_prefix[a0]) * spt;
-    ph.G = (int)min((long long)Gn, ph.T);
+    // a tiny phase (a few small experts) on fewer CTAs, each with >= min_iters k-steps: every
+    // CTA streams more, but no tile is split over many CTAs (a split reducer adds every
+    // contributor's partial tile)
+    ph.G = (int)min((long long)Gn, max(min(ph.T, 1LL), ph.T / max(1, min_iters)));
     ph.slot_off = ph.g * Gn;
     return ph;
 }
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         int stage = 0;
         uint32_t phase = 0;
         for (int p = 0; p < n_ph; ++p) {
-            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn);
+            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn, fp.min_iters);
             if (cta < ph.G) {
                 const long long i0 = ph.base + range_start(cta, ph.T, ph.G);
                 const long long i1 = ph.base + range_start(cta + 1, ph.T, ph.G);
@@ -511,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         uint32_t phase = 0, acc_phase = 0;
         bool first_g2 = true;
         for (int p = 0; p < n_ph; ++p) {
-            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn);
+            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn, fp.min_iters);
             if (cta < ph.G) {
                 const long long i0 = ph.base + range_start(cta, ph.T, ph.G);
                 const long long i1 = ph.base + range_start(cta + 1, ph.T, ph.G);
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_fused_kernel(const __grid_con
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int p = 0; p < n_ph; ++p) {
-            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn);
+            const Phase ph = phase_at(p, ng, sched, mtiles1, mtiles2, spt1, spt2, Gn, fp.min_iters);
             if (!ph.g2)
                 fused_epilogue<NMAT1>(P1, sched, gm, fp.arrive, acc, acc_phase, ph.base, ph.T, ph.G, ph.slot_off, cta,
                                       spt1, tmem_base, q, lane, h_ready, tr);

@@ -383,10 +383,11 @@ def test_fused_single_launch_equals_multi_kernel(cuda_ok, E, d, f, B, k, act, n_
     _, _, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, act, n_tile)
     rows = int(perm.offset[-1])
     bo = _t(buf_of)
-    saved = {v: os.environ.get(v) for v in ("BMOE_FUSED", "BMOE_KPS", "BMOE_FFN_GROUPS")}
+    saved = {v: os.environ.get(v) for v in ("BMOE_FUSED", "BMOE_KPS", "BMOE_FFN_GROUPS", "BMOE_FFN_MIN_ITERS")}
     try:
         os.environ["BMOE_KPS"] = "2"  # same k-steps per stage -> same stream-K split in both paths
-        os.environ["BMOE_FFN_GROUPS"] = "1"  # one stream-K range per GEMM, as the separate kernels
+        os.environ["BMOE_FFN_GROUPS"] = "1"  # one stream-K range per GEMM over all CTAs, as the separate kernels
+        os.environ["BMOE_FFN_MIN_ITERS"] = "1"
         os.environ["BMOE_FUSED"] = "0"
         ref = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, act, ws)[:rows].clone()
         os.environ["BMOE_FUSED"] = "1"

@@ -45,10 +45,11 @@ if __name__ == "__main__":
     bo = torch.arange(E2, dtype=torch.int32).cuda()
     rows = int(perm.offset[-1])
     os.environ["BMOE_KPS"] = "2"
+    os.environ["BMOE_FFN_MIN_ITERS"] = "1"  # every CTA in the stream-K range, as the separate kernels
     y1 = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
     os.environ["BMOE_FUSED"] = "0"
     y0 = ops.expert_ffn_bf16(xp, perm, arena, bo, d, f, ops.ACT_SWIGLU, ws)[:rows].clone()
-    del os.environ["BMOE_FUSED"], os.environ["BMOE_KPS"]
+    del os.environ["BMOE_FUSED"], os.environ["BMOE_KPS"], os.environ["BMOE_FFN_MIN_ITERS"]
     torch.cuda.synchronize()
     assert torch.equal(y0, y1)
     # interleaved expert-group phases (forced) and the combine fused behind the FFN
