@@ -399,7 +399,7 @@ __device__ __forceinline__ Phase phase_at(int p, int ng, const Sched &s, int mti
     // a tiny phase (a few small experts) on fewer CTAs, each with >= min_iters k-steps: every
     // CTA streams more, but no tile is split over many CTAs (a split reducer adds every
     // contributor's partial tile)
-    ph.G = (int)min((long long)Gn, max(min(ph.T, 1LL), ph.T / max(1, min_iters)));
+    ph.G = (int)min((long long)Gn, max(min(ph.T, 1LL), ph.T / max(1, min_iters)));  // default 2 (A/B: profiles/r2s_mi_ab.jsonl)
     ph.slot_off = ph.g * Gn;
     return ph;
 }

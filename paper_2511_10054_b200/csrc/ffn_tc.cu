@@ -307,7 +307,7 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
         if (const char *ev = getenv("BMOE_PREFETCH_W2")) pre = atoi(ev);
         FusedParams fp{{g1, g2}, counters, (int)wl.tile_cap,
                        reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + wl.bar_off),
-                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr, nullptr, 1, 12, 4};
+                       pre, trace_buffer(G, s), CombineArgs{}, 0, nullptr, nullptr, nullptr, 1, 12, 2};
         if (const char *mi = getenv("BMOE_FFN_MIN_ITERS")) fp.min_iters = std::max(1, atoi(mi));
         const char *gv = getenv("BMOE_FFN_GROUPS");  // read per call: tests switch it
         fp.groups = std::max(1, std::min(gv ? atoi(gv) : 3, kMaxGroups));

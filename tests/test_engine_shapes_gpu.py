@@ -134,13 +134,15 @@ def test_engine_decisions_bit_exact_at_baseline_shapes(cuda_ok, name, layers, B)
     wl.close()
 
 
-def test_engine_fused_combine_equals_separate_launch():
+@pytest.mark.parametrize("model", ["qwen3", "dsv2lite"])
+def test_engine_fused_combine_equals_separate_launch(model):
     """The engine's layer-step runs K5 inside its last fused FFN launch
-    (post1 when nothing is fetched, else post2); with BMOE_FUSE_COMBINE=0 it is
-    its own launch. Hidden states bitwise equal, event logs equal, one kernel
-    launch fewer per decode layer-step."""
+    (post1 when nothing is fetched, else post2; DSV2: the shared experts'
+    slots ride along); with BMOE_FUSE_COMBINE=0 it is its own launch. Hidden
+    states bitwise equal, event logs equal, one kernel launch fewer per decode
+    layer-step."""
     import os
-    wl = W.build("qwen3", layers=3, max_batch=16, profile_tokens=1024)
+    wl = W.build(model, layers=3, max_batch=16, profile_tokens=1024)
     outs, evs, launches = [], [], []
     old = os.environ.get("BMOE_FUSE_COMBINE")
     try:

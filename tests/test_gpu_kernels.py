@@ -658,3 +658,22 @@ def test_kernel_timing_spans(cuda_ok):
     ev = times[0:n:2]
     assert np.all(spans[:3] > 0) and np.all(spans[:3] <= ev[:3] + 1e-3), (spans, ev)
     assert spans[3] == 0.0
+
+
+def test_ffn_phase_trace(cuda_ok, monkeypatch):
+    """BMOE_FFN_TRACE: the fused decode kernel's per-CTA phase stamps are
+    ordered (entry <= setup <= exit) and every CTA stamps its entry and exit."""
+    from paper_2511_10054_b200 import _native as N
+    monkeypatch.setenv("BMOE_FFN_TRACE", "1")
+    E, d, f, B, k = 8, 1024, 2048, 16, 2
+    _, _, (xp, perm, arena, buf_of, ws) = _bf16_case(np.random.default_rng(8), E, d, f, B, k, ops.ACT_SWIGLU, 16)
+    ops.expert_ffn_bf16(xp, perm, arena, _t(buf_of), d, f, ops.ACT_SWIGLU, ws)
+    torch.cuda.synchronize()
+    G = torch.cuda.get_device_properties(0).multi_processor_count
+    st = np.zeros(G * 12, np.uint64)
+    n = int(N.lib().bm_ffn_trace_read(st.ctypes.data, st.size))
+    if n == 0:
+        pytest.skip("trace buffer was not enabled in this process (BMOE_FFN_TRACE read at first use)")
+    st = st[:n].reshape(-1, 12).astype(np.int64)
+    assert np.all(st[:, 0] > 0) and np.all(st[:, 7] > 0)
+    assert np.all(st[:, 0] <= st[:, 1]) and np.all(st[:, 1] <= st[:, 7])
