@@ -191,8 +191,8 @@ using namespace bm::ffn;
 static unsigned long long *g_trace = nullptr;
 static int g_trace_ctas = 0;
 static unsigned long long *trace_buffer(int G, cudaStream_t s) {
-    static const bool on = getenv("BMOE_FFN_TRACE") && atoi(getenv("BMOE_FFN_TRACE")) != 0;
-    if (!on) return nullptr;
+    const char *ev = getenv("BMOE_FFN_TRACE");  // read per call (tests switch it)
+    if (!ev || atoi(ev) == 0) return nullptr;
     if (!g_trace) {
         if (cudaMalloc(&g_trace, (size_t)G * kTracePts * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
         g_trace_ctas = G;
