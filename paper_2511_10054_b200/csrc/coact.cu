@@ -2,8 +2,11 @@
 // and K7 buddy ranking (one warp per pivot, bit-exact f64 in numpy order).
 // Reference: profiler.observe / conditional_row (profiler.py:67-119),
 // buddies.cft_prefix / build_table (buddies.py:79-129).
+#include <algorithm>
+
 #include "common.cuh"
 #include "numpy_order.cuh"
+#include "ptx.cuh"
 
 namespace bm {
 namespace {
@@ -120,6 +123,147 @@ __global__ void __launch_bounds__(kCountThreads) coact_count_kernel(const int32_
             }
         }
     }
+}
+
+// K6 on the tensor cores (E <= 128): the co-activation matrix is X^T X over
+// the trace's one-hot rows, X[t][e] = 1 if token t routed to expert e. A
+// stage holds 256 tokens as two 128-token K blocks of X^T in the UMMA
+// K-major, 128B-swizzled layout (expert e's row: one byte per token), built
+// in shared memory by 256 builder threads (one token each: zero the stage,
+// then one byte store per id); one thread issues tcgen05.mma kind::i8 with
+// A = B = that block (D[i][j] += sum_t X[t][i] X[t][j], u8 x u8 -> s32 in
+// TMEM, exact), so the diagonal is the per-expert count and the rest the
+// pair counts, both symmetric halves. Rows with an out-of-range or repeated
+// id are rejected like observe() does (profiler.py:76-80). At the end each
+// CTA adds its 128 x 128 accumulator to the u64 counters.
+constexpr int kTcBuild = 256;                // builder threads = tokens per stage
+constexpr int kTcThreads = kTcBuild + 32;    // + the MMA warp
+constexpr int kTcStages = 3;
+constexpr uint32_t kTcSub = 128 * 128;       // one 128-token K block: 128 expert rows x 128 B
+constexpr uint32_t kTcStage = 2 * kTcSub;    // 256 tokens
+constexpr size_t kTcSmem = (size_t)kTcStages * kTcStage + 1024;
+
+template <int KC>
+__global__ void __launch_bounds__(kTcThreads) coact_tc_kernel(const int32_t *__restrict__ topk, long long N, int k_rt,
+                                                              int E, long long per_block,
+                                                              unsigned long long *__restrict__ counts,
+                                                              unsigned long long *__restrict__ pairs,
+                                                              int *__restrict__ invalid) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2 * kTcStages + 1];
+    __shared__ uint32_t tmem_sh;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const unsigned lane = lane_id();
+    const int k = KC > 0 ? KC : k_rt;
+    const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - ptx::smem_u32(smem_raw));
+    const uint32_t full0 = ptx::smem_u32(&bars[0]), empty0 = ptx::smem_u32(&bars[kTcStages]),
+                   done = ptx::smem_u32(&bars[2 * kTcStages]);
+    const long long t0 = (long long)blockIdx.x * per_block, t1 = min(N, t0 + per_block);
+    const long long nchunks = t1 > t0 ? (t1 - t0 + kTcBuild - 1) / kTcBuild : 0;
+    if (tid == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            ptx::mbar_init(full0 + 8 * s, kTcBuild);
+            ptx::mbar_init(empty0 + 8 * s, 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == kTcBuild / 32) ptx::tmem_alloc(ptx::smem_u32(&tmem_sh), 128);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_sh;
+    if (warp < kTcBuild / 32) {
+        int bad = 0;
+        const int sub = tid >> 7, tl = tid & 127;
+        for (long long c = 0; c < nchunks; ++c) {
+            const int s = (int)(c % kTcStages);
+            const uint32_t ph = (uint32_t)((c / kTcStages) & 1);
+            const long long t = t0 + c * kTcBuild + tid;
+            int id[KC > 0 ? KC : 32];
+            bool ok = t < t1;
+            if (ok) {
+                if constexpr (KC == 8) {
+                    const int4 *p = reinterpret_cast<const int4 *>(topk + t * 8);
+                    const int4 a = __ldg(p), b = __ldg(p + 1);
+                    id[0] = a.x; id[1] = a.y; id[2] = a.z; id[3] = a.w;
+                    id[4] = b.x; id[5] = b.y; id[6] = b.z; id[7] = b.w;
+                } else {
+                    for (int x = 0; x < k; ++x) id[x] = __ldg(topk + t * k + x);
+                }
+                bool badrow = false;
+#pragma unroll
+                for (int x = 0; x < (KC > 0 ? KC : 32); ++x) {
+                    if (x >= k) break;
+                    badrow |= (unsigned)id[x] >= (unsigned)E;
+                    for (int y = 0; y < x; ++y) badrow |= id[x] == id[y];
+                }
+                if (badrow) {
+                    ++bad;
+                    ok = false;
+                }
+            }
+            ptx::mbar_wait(empty0 + 8 * s, ph ^ 1u);  // the MMAs that read this stage are done
+            uint4 *z = reinterpret_cast<uint4 *>(base_ptr + (size_t)s * kTcStage);
+#pragma unroll
+            for (int m = 0; m < (int)(kTcStage / 16 / kTcBuild); ++m) z[tid + kTcBuild * m] = make_uint4(0, 0, 0, 0);
+            ptx::named_bar_sync(1, kTcBuild);
+            if (ok) {
+                uint8_t *blk = base_ptr + (size_t)s * kTcStage + (size_t)sub * kTcSub;
+                const uint32_t col = (uint32_t)(tl & 15), chunk = (uint32_t)(tl >> 4);
+                for (int x = 0; x < k; ++x) {
+                    const uint32_t e = (uint32_t)id[x];
+                    blk[e * 128u + (((chunk ^ (e & 7u)) << 4) | col)] = 1;
+                }
+            }
+            ptx::fence_proxy_async_shared();
+            ptx::mbar_arrive(full0 + 8 * s);
+        }
+        if (bad) atomicAdd(invalid, bad);
+    } else if (lane == 0) {  // the MMA issuer
+        const uint32_t idesc = ptx::idesc_u8_s32(128, 128);
+        for (long long c = 0; c < nchunks; ++c) {
+            const int s = (int)(c % kTcStages);
+            const uint32_t ph = (uint32_t)((c / kTcStages) & 1);
+            ptx::mbar_wait(full0 + 8 * s, ph);
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {
+                const uint64_t d = ptx::sw128_desc(base + (uint32_t)s * kTcStage + (uint32_t)sb * kTcSub);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)  // K = 32 tokens per MMA: 32 bytes along the row
+                    ptx::mma_i8(tmem, d + 2 * kk, d + 2 * kk, idesc, (c | sb | kk) != 0 ? 1u : 0u);
+            }
+            ptx::mma_commit(empty0 + 8 * s);
+        }
+        if (nchunks > 0) ptx::mma_commit(done);
+    }
+    // epilogue: warp w < 4 reads TMEM lanes 32w.. (rows i) x 128 columns (j)
+    if (warp < 4 && nchunks > 0) {
+        ptx::mbar_wait(done, 0);
+        ptx::tc_fence_after();
+        const int i = warp * 32 + (int)lane;
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+            float v[16];
+            ptx::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            if (i >= E) continue;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int col = c0 + j;
+                const unsigned long long n = (unsigned long long)__float_as_uint(v[j]);
+                if (col >= E || n == 0) continue;
+                if (col == i)
+                    atomicAdd(&counts[i], n);
+                else
+                    atomicAdd(&pairs[(size_t)i * E + col], n);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == kTcBuild / 32) ptx::tmem_dealloc(tmem, 128);
 }
 
 __global__ void coact_weighted_kernel(const int32_t *__restrict__ topk, const float *__restrict__ probs, long long N,
@@ -280,6 +424,29 @@ extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t
                "bm_coact_count: bad shape N=%lld k=%lld E=%lld", (long long)N, (long long)k, (long long)E);
     BM_REQUIRE(counts && pairs && invalid_rows && (topk || N == 0), BM_EINVAL, "bm_coact_count: null pointer");
     if (N == 0) return BM_OK;
+    // tensor-core path for E <= 128 (BMOE_COACT_TC=0: the shared-memory atomics kernel)
+    static const int tc_env = getenv("BMOE_COACT_TC") ? atoi(getenv("BMOE_COACT_TC")) : 1;
+    if (tc_env && E <= 128 && (k != 8 || (reinterpret_cast<uintptr_t>(topk) & 15) == 0)) {
+        auto tk = k == 8 ? coact_tc_kernel<8> : coact_tc_kernel<0>;
+        static bool attr = false;
+        if (!attr) {
+            BM_CUDA_TRY(cudaFuncSetAttribute(coact_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kTcSmem));
+            BM_CUDA_TRY(cudaFuncSetAttribute(coact_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kTcSmem));
+            attr = true;
+        }
+        int per_sm = 1;
+        BM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tk, kTcThreads, kTcSmem));
+        long long blocks = (long long)sm_count() * std::max(1, std::min(per_sm, 2));
+        const long long need = (N + 4LL * kTcBuild - 1) / (4LL * kTcBuild);  // >= 4 stages per CTA
+        blocks = std::max(1LL, std::min(blocks, need));
+        const long long per_block = (N + blocks - 1) / blocks;
+        tk<<<(unsigned)blocks, kTcThreads, kTcSmem, as_stream(stream)>>>(topk, N, (int)k, (int)E, per_block, counts,
+                                                                         pairs, invalid_rows);
+        BM_LAUNCH_CHECK();
+        return BM_OK;
+    }
     const size_t smem = (size_t)E * (E + 1) / 2 * sizeof(uint32_t);
     auto kern = k == 8 ? coact_count_kernel<8> : coact_count_kernel<0>;
     BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
