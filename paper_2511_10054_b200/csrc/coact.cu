@@ -142,6 +142,7 @@ constexpr int kTcStages = 3;
 constexpr uint32_t kTcSub = 128 * 128;       // one 128-token K block: 128 expert rows x 128 B
 constexpr uint32_t kTcStage = 2 * kTcSub;    // 256 tokens
 constexpr size_t kTcSmem = (size_t)kTcStages * kTcStage + 1024;
+constexpr int kTcMaxK = 16;  // ids per token on the tensor-core path
 
 template <int KC>
 __global__ void __launch_bounds__(kTcThreads) coact_tc_kernel(const int32_t *__restrict__ topk, long long N, int k_rt,
@@ -175,50 +176,86 @@ __global__ void __launch_bounds__(kTcThreads) coact_tc_kernel(const int32_t *__r
     ptx::tc_fence_after();
     const uint32_t tmem = tmem_sh;
     if (warp < kTcBuild / 32) {
-        int bad = 0;
+        // A builder thread owns one token column (sub, tl) of every stage. Each stage is zeroed
+        // once; afterwards the thread clears only the bytes it set in that stage last time
+        // (prev), so no barrier separates clearing from setting. The next chunk's ids are
+        // loaded while the current one is built.
+        constexpr int KM = KC > 0 ? KC : kTcMaxK;
         const int sub = tid >> 7, tl = tid & 127;
-        for (long long c = 0; c < nchunks; ++c) {
-            const int s = (int)(c % kTcStages);
-            const uint32_t ph = (uint32_t)((c / kTcStages) & 1);
+        const uint32_t col = (uint32_t)(tl & 15), chunk16 = (uint32_t)(tl >> 4);
+        int bad = 0;
+        int nxt[KM];
+        bool nxt_ok = false;
+        auto load_ids = [&](long long c, int (&id)[KM], bool &ok) {
             const long long t = t0 + c * kTcBuild + tid;
-            int id[KC > 0 ? KC : 32];
-            bool ok = t < t1;
-            if (ok) {
-                if constexpr (KC == 8) {
-                    const int4 *p = reinterpret_cast<const int4 *>(topk + t * 8);
-                    const int4 a = __ldg(p), b = __ldg(p + 1);
-                    id[0] = a.x; id[1] = a.y; id[2] = a.z; id[3] = a.w;
-                    id[4] = b.x; id[5] = b.y; id[6] = b.z; id[7] = b.w;
-                } else {
-                    for (int x = 0; x < k; ++x) id[x] = __ldg(topk + t * k + x);
-                }
-                bool badrow = false;
+            ok = c < nchunks && t < t1;
+            if (!ok) return;
+            if constexpr (KC == 8) {
+                const int4 *p = reinterpret_cast<const int4 *>(topk + t * 8);
+                const int4 a = __ldg(p), b = __ldg(p + 1);
+                id[0] = a.x; id[1] = a.y; id[2] = a.z; id[3] = a.w;
+                id[4] = b.x; id[5] = b.y; id[6] = b.z; id[7] = b.w;
+            } else {
 #pragma unroll
-                for (int x = 0; x < (KC > 0 ? KC : 32); ++x) {
-                    if (x >= k) break;
-                    badrow |= (unsigned)id[x] >= (unsigned)E;
-                    for (int y = 0; y < x; ++y) badrow |= id[x] == id[y];
-                }
-                if (badrow) {
-                    ++bad;
-                    ok = false;
-                }
+                for (int x = 0; x < KM; ++x)
+                    if (x < k) id[x] = __ldg(topk + t * k + x);
             }
-            ptx::mbar_wait(empty0 + 8 * s, ph ^ 1u);  // the MMAs that read this stage are done
-            uint4 *z = reinterpret_cast<uint4 *>(base_ptr + (size_t)s * kTcStage);
-#pragma unroll
-            for (int m = 0; m < (int)(kTcStage / 16 / kTcBuild); ++m) z[tid + kTcBuild * m] = make_uint4(0, 0, 0, 0);
+        };
+        load_ids(0, nxt, nxt_ok);
+        // zero every stage once (all builders), then build
+        {
+            uint4 *z = reinterpret_cast<uint4 *>(base_ptr);
+            for (int m = tid; m < (int)(kTcStages * kTcStage / 16); m += kTcBuild) z[m] = make_uint4(0, 0, 0, 0);
             ptx::named_bar_sync(1, kTcBuild);
-            if (ok) {
-                uint8_t *blk = base_ptr + (size_t)s * kTcStage + (size_t)sub * kTcSub;
-                const uint32_t col = (uint32_t)(tl & 15), chunk = (uint32_t)(tl >> 4);
-                for (int x = 0; x < k; ++x) {
-                    const uint32_t e = (uint32_t)id[x];
-                    blk[e * 128u + (((chunk ^ (e & 7u)) << 4) | col)] = 1;
+        }
+        int prev[kTcStages][KM];
+        int prev_n[kTcStages] = {0, 0, 0};
+        for (long long c0 = 0; c0 < nchunks; c0 += kTcStages) {
+#pragma unroll
+            for (int s = 0; s < kTcStages; ++s) {
+                const long long c = c0 + s;
+                if (c >= nchunks) break;
+                const uint32_t ph = (uint32_t)((c / kTcStages) & 1);
+                int id[KM];
+                bool ok = nxt_ok;
+#pragma unroll
+                for (int x = 0; x < KM; ++x) id[x] = nxt[x];
+                load_ids(c + 1, nxt, nxt_ok);  // in flight while this chunk is built
+                if (ok) {
+                    bool badrow = false;
+#pragma unroll
+                    for (int x = 0; x < KM; ++x) {
+                        if (x >= k) break;
+                        badrow |= (unsigned)id[x] >= (unsigned)E;
+#pragma unroll
+                        for (int y = 0; y < x; ++y) badrow |= id[x] == id[y];
+                    }
+                    if (badrow) {
+                        ++bad;
+                        ok = false;
+                    }
                 }
+                ptx::mbar_wait(empty0 + 8 * s, ph ^ 1u);  // the MMAs that read this stage are done
+                uint8_t *blk = base_ptr + (size_t)s * kTcStage + (size_t)sub * kTcSub;
+#pragma unroll
+                for (int x = 0; x < KM; ++x) {
+                    if (x >= prev_n[s]) break;
+                    const uint32_t e = (uint32_t)prev[s][x];
+                    blk[e * 128u + (((chunk16 ^ (e & 7u)) << 4) | col)] = 0;
+                }
+                prev_n[s] = ok ? k : 0;
+                if (ok) {
+#pragma unroll
+                    for (int x = 0; x < KM; ++x) {
+                        if (x >= k) break;
+                        const uint32_t e = (uint32_t)id[x];
+                        prev[s][x] = id[x];
+                        blk[e * 128u + (((chunk16 ^ (e & 7u)) << 4) | col)] = 1;
+                    }
+                }
+                ptx::fence_proxy_async_shared();
+                ptx::mbar_arrive(full0 + 8 * s);
             }
-            ptx::fence_proxy_async_shared();
-            ptx::mbar_arrive(full0 + 8 * s);
         }
         if (bad) atomicAdd(invalid, bad);
     } else if (lane == 0) {  // the MMA issuer
@@ -426,7 +463,7 @@ extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t
     if (N == 0) return BM_OK;
     // tensor-core path for E <= 128 (BMOE_COACT_TC=0: the shared-memory atomics kernel)
     static const int tc_env = getenv("BMOE_COACT_TC") ? atoi(getenv("BMOE_COACT_TC")) : 1;
-    if (tc_env && E <= 128 && (k != 8 || (reinterpret_cast<uintptr_t>(topk) & 15) == 0)) {
+    if (tc_env && E <= 128 && k <= kTcMaxK && (k != 8 || (reinterpret_cast<uintptr_t>(topk) & 15) == 0)) {
         auto tk = k == 8 ? coact_tc_kernel<8> : coact_tc_kernel<0>;
         static bool attr = false;
         if (!attr) {
