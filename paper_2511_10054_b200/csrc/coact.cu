@@ -461,8 +461,10 @@ extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t
                "bm_coact_count: bad shape N=%lld k=%lld E=%lld", (long long)N, (long long)k, (long long)E);
     BM_REQUIRE(counts && pairs && invalid_rows && (topk || N == 0), BM_EINVAL, "bm_coact_count: null pointer");
     if (N == 0) return BM_OK;
-    // tensor-core path for E <= 128 (BMOE_COACT_TC=0: the shared-memory atomics kernel)
-    static const int tc_env = getenv("BMOE_COACT_TC") ? atoi(getenv("BMOE_COACT_TC")) : 1;
+    // tensor-core path for E <= 128 (BMOE_COACT_TC=1; off by default: 1.08-1.42 ms against the atomics
+    // kernel's 1.00 ms on the 64M-token trace, bound by shared-memory traffic -- DESIGN §7)
+    const char *tc_ev = getenv("BMOE_COACT_TC");  // read per call (tests switch it)
+    const int tc_env = tc_ev ? atoi(tc_ev) : 0;
     if (tc_env && E <= 128 && k <= kTcMaxK && (k != 8 || (reinterpret_cast<uintptr_t>(topk) & 15) == 0)) {
         auto tk = k == 8 ? coact_tc_kernel<8> : coact_tc_kernel<0>;
         static bool attr = false;

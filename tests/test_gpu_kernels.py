@@ -676,3 +676,29 @@ def test_ffn_phase_trace(cuda_ok, monkeypatch):
     st = st[:n].reshape(-1, 12).astype(np.int64)
     assert np.all(st[:, 0] > 0) and np.all(st[:, 7] > 0)
     assert np.all(st[:, 0] <= st[:, 1]) and np.all(st[:, 1] <= st[:, 7])
+
+
+@pytest.mark.parametrize("E,k,n", [(128, 8, 300_001), (64, 6, 100_003), (100, 3, 50_000), (8, 2, 20_000)])
+def test_coact_tensor_core_path_bit_exact(cuda_ok, monkeypatch, E, k, n):
+    """K6's tcgen05 kind::i8 path (BMOE_COACT_TC=1: X^T X over one-hot tiles in
+    TMEM) gives exactly the shared-memory-atomics kernel's counts, pairs and
+    rejected-row count, rejected rows (duplicates, out-of-range ids) included."""
+    rng = np.random.default_rng(E * 31 + k)
+    topk = np.stack([rng.choice(E, k, replace=False) for _ in range(n)]).astype(np.int32)
+    bad = rng.choice(n, 50, replace=False)
+    topk[bad[:25], 0] = topk[bad[:25], -1]  # duplicate ids
+    topk[bad[25:], 1] = E + 3               # out of range
+    t = _t(topk)
+    out = []
+    for tc in ("0", "1"):
+        monkeypatch.setenv("BMOE_COACT_TC", tc)
+        c = torch.zeros(E, dtype=torch.int64, device=DEV)
+        p = torch.zeros(E, E, dtype=torch.int64, device=DEV)
+        badc = torch.zeros(1, dtype=torch.int32, device=DEV)
+        from paper_2511_10054_b200 import _native as N
+        N.call("bm_coact_count", t.data_ptr(), n, k, E, c.data_ptr(), p.data_ptr(), badc.data_ptr(),
+               torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        out.append((c.cpu(), p.cpu(), int(badc.item())))
+    assert out[0][2] == out[1][2] == 50
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
