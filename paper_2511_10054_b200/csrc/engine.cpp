@@ -24,7 +24,8 @@ int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const vo
                      int32_t fallback, int32_t method, double beta, const double *beta_dev, double eta, double kappa,
                      int32_t use_local_logit, const int32_t *partition_of, double hop, int32_t *executed,
                      uint8_t *kind, int32_t *used, double *delta_out, uint8_t *batch_allowed_out,
-                     bm_stream_t stream);
+                     bm_stream_t stream, int32_t *hp_topk, int32_t *hp_executed, uint8_t *hp_kind,
+                     uint8_t *hp_allowed, uint8_t *hp_batch_ok);
 int random_plan_batch(const int32_t *topk, int64_t B, int64_t k, const uint32_t *resident_bits, int64_t E,
                       bm_pcg64 *rng, int32_t *executed, uint8_t *kind, int32_t *used);
 namespace ffn {  // timing of FFN launches inside captured graphs (ffn_tc.cu)
@@ -193,10 +194,17 @@ struct bm_engine {
     std::vector<std::vector<int32_t>> prev_counts;  // [L][E]
     // packed plan readback, per-layer staging (graph-stable addresses), graphs
     uint8_t *plan_dev = nullptr, *plan_host = nullptr;
+    uint8_t *plan_host_dev = nullptr;  // the same pinned plan seen from the device (mapped)
+    int32_t *topk_hd = nullptr, *exec_hd = nullptr;
+    uint8_t *kind_hd = nullptr, *allowed_hd = nullptr, *batch_ok_hd = nullptr;
     float *h_int = nullptr;                       // engine-owned hidden state [max_batch][d]
     uint32_t *bm_dev_all = nullptr, *bm_host_all = nullptr;
     int32_t *bo_dev_all = nullptr, *bo_host_all = nullptr;
     std::vector<uint32_t *> bm_dev_l, bm_host_l;  // per-layer residency bitmaps (+ the beta the remap uses)
+    std::vector<uint32_t *> bm_hostdev_l;         // bm_host_l seen from the device (mapped pinned memory)
+    // the remap reads the snapshot and writes the packed plan through mapped pinned memory: no
+    // upload or readback copy on the layer-step's host round trip (BMOE_ZERO_COPY=0: the copies)
+    bool zero_copy = true;
     int bm_stride = 0, beta_word = 0;            // u32 words per layer slot; beta (f64) at word beta_word
     BetaController beta_ctl;
     int64_t wire_total = 0, fetch_total = 0;  // every physical fetch since creation (stats resets keep them)
@@ -238,7 +246,7 @@ struct bm_engine {
     }
     template <typename T>
     int hmalloc(T **p, size_t n) {
-        ENG_CUDA(cudaHostAlloc(reinterpret_cast<void **>(p), n * sizeof(T) + 16, cudaHostAllocPortable));
+        ENG_CUDA(cudaHostAlloc(reinterpret_cast<void **>(p), n * sizeof(T) + 16, cudaHostAllocPortable | cudaHostAllocMapped));
         return BM_OK;
     }
 
@@ -359,6 +367,11 @@ struct bm_engine {
         kind_h = reinterpret_cast<uint8_t *>(exec_h + B * k);
         allowed_h = kind_h + B * k;
         batch_ok_h = allowed_h + B;
+        topk_hd = reinterpret_cast<int32_t *>(plan_host_dev);
+        exec_hd = topk_hd + B * k;
+        kind_hd = reinterpret_cast<uint8_t *>(exec_hd + B * k);
+        allowed_hd = kind_hd + B * k;
+        batch_ok_hd = allowed_hd + B;
     }
     static size_t plan_bytes(int64_t B, int k) { return (size_t)B * k * 9 + (size_t)B + 1; }
 
@@ -366,18 +379,23 @@ struct bm_engine {
     int enqueue_pre(int l, float *h, int64_t B, cudaStream_t s) {
         ENG_TRY(bm_gate_topk(h, gate_w + (size_t)l * E * d, gate_b + (size_t)l * E, B, E, d, k, cfg.temperature,
                              tau[l], cfg.gamma, logits, topk, probs, tae, margin, allowed, s));
-        ENG_CUDA(cudaMemcpyAsync(bm_dev_l[l], bm_host_l[l], bm_stride * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        const bool zc = zero_copy && plan_host_dev;
+        if (!zc)
+            ENG_CUDA(cudaMemcpyAsync(bm_dev_l[l], bm_host_l[l], bm_stride * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                     s));
+        uint32_t *bits = zc ? bm_hostdev_l[l] : bm_dev_l[l];
         const bool p = psi && cfg.method == BM_METHOD_BUDDY;
-        ENG_TRY(bm::buddy_remap_impl(topk, allowed, p ? logits : nullptr, 0, B, k, E, bm_dev_l[l],
+        ENG_TRY(bm::buddy_remap_impl(topk, allowed, p ? logits : nullptr, 0, B, k, E, bits,
                                      tbl_ids ? tbl_ids + (size_t)l * E * K : nullptr,
                                      p ? tbl_w + (size_t)l * E * K : nullptr,
                                      tbl_len ? tbl_len + (size_t)l * E : nullptr, K > 0 ? K : 1, cfg.search_rank_h,
                                      cfg.rho, cfg.fallback,
                                      cfg.method == BM_METHOD_RANDOM ? BM_METHOD_ORIGINAL : cfg.method, cfg.beta,
-                                     reinterpret_cast<const double *>(bm_dev_l[l] + beta_word), p ? eta : 0.0,
+                                     reinterpret_cast<const double *>(bits + beta_word), p ? eta : 0.0,
                                      p ? kappa : 0.0, use_local_logit, p ? partition_of : nullptr, hop, executed, kind,
-                                     used, delta, batch_ok, s));
-        ENG_CUDA(cudaMemcpyAsync(plan_host, plan_dev, plan_bytes(B, k), cudaMemcpyDeviceToHost, s));
+                                     used, delta, batch_ok, s, zc ? topk_hd : nullptr, zc ? exec_hd : nullptr,
+                                     zc ? kind_hd : nullptr, zc ? allowed_hd : nullptr, zc ? batch_ok_hd : nullptr));
+        if (!zc) ENG_CUDA(cudaMemcpyAsync(plan_host, plan_dev, plan_bytes(B, k), cudaMemcpyDeviceToHost, s));
         return BM_OK;
     }
 
@@ -859,6 +877,14 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     const size_t pb = bm_engine::plan_bytes(Bm, k) + 64;
     ENG_TRY(g->dmalloc(&g->plan_dev, pb));
     ENG_TRY(g->hmalloc(&g->plan_host, pb));
+    if (const char *ev = getenv("BMOE_ZERO_COPY")) g->zero_copy = atoi(ev) != 0;
+    if (g->zero_copy) {  // pinned allocations are mapped (portable, UVA): their device-side addresses
+        void *pd = nullptr;
+        if (cudaHostGetDevicePointer(&pd, g->plan_host, 0) == cudaSuccess)
+            g->plan_host_dev = static_cast<uint8_t *>(pd);
+        else
+            cudaGetLastError();
+    }
     ENG_TRY(g->dmalloc(&g->h_int, (size_t)Bm * g->d));
     const int words = (E + 31) / 32;
     g->beta_word = (words + 1) & ~1;  // 8-byte aligned f64 after the bitmap
@@ -876,6 +902,11 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
     for (int l = 0; l < L; ++l) {
         g->bm_dev_l.push_back(g->bm_dev_all + (size_t)l * g->bm_stride);
         g->bm_host_l.push_back(g->bm_host_all + (size_t)l * g->bm_stride);
+        if (g->plan_host_dev) {
+            void *pd = nullptr;
+            ENG_CUDA(cudaHostGetDevicePointer(&pd, g->bm_host_l.back(), 0));
+            g->bm_hostdev_l.push_back(static_cast<uint32_t *>(pd));
+        }
         g->bo_dev_l.push_back(g->bo_dev_all + (size_t)l * 3 * Et);
         g->bo_host_l.push_back(g->bo_host_all + (size_t)l * 3 * Et);
     }

@@ -19,6 +19,14 @@ constexpr int kMaxH = 256;
 constexpr int kMaxK = 32;
 constexpr double kZClamp = 3.0;  // substitution.py:33
 
+// The engine's packed plan in mapped pinned host memory: the kernel writes its
+// plan (and the router's top-k and token gate it read) straight to the host,
+// so the engine's layer-step has no readback copy (null fields: none).
+struct HostPlan {
+    int32_t *topk, *executed;
+    uint8_t *kind, *allowed, *batch_ok;
+};
+
 struct RemapArgs {
     const int32_t *topk;
     const uint8_t *token_allowed;
@@ -42,6 +50,7 @@ struct RemapArgs {
     double *delta_out;
     uint8_t *batch_allowed_out;
     const double *beta_dev;  // when set, beta is read from device memory (the engine's adaptive beta)
+    HostPlan hp;             // the engine's mapped host plan (null: none)
 };
 
 __device__ __forceinline__ bool bit_of(const uint32_t *m, int e) { return (m[e >> 5] >> (e & 31)) & 1u; }
@@ -77,6 +86,7 @@ __global__ void __launch_bounds__(kRemapThreads) remap_kernel(RemapArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (a.delta_out) *a.delta_out = delta;
         if (a.batch_allowed_out) *a.batch_allowed_out = batch_ok ? 1 : 0;
+        if (a.hp.batch_ok) *a.hp.batch_ok = batch_ok ? 1 : 0;
     }
 
     const int b = blockIdx.x * kWarps + warp;
@@ -86,10 +96,19 @@ __global__ void __launch_bounds__(kRemapThreads) remap_kernel(RemapArgs a) {
     int32_t *ex = a.executed + (size_t)b * k;
     uint8_t *kd = a.kind + (size_t)b * k;
 
+    if (a.hp.topk) {  // the router's part of the host plan
+        if (lane < (unsigned)k) a.hp.topk[(size_t)b * k + lane] = my_e;
+        if (lane == 0) a.hp.allowed[b] = a.token_allowed ? a.token_allowed[b] : 1;
+    }
     if (a.method != BM_METHOD_BUDDY) {
         if (lane < (unsigned)k) {
+            const uint8_t kk = (a.method == BM_METHOD_IDENTITY || bit_of(res, my_e)) ? BM_KIND_KEPT : BM_KIND_ONDEMAND;
             ex[lane] = my_e;
-            kd[lane] = (a.method == BM_METHOD_IDENTITY || bit_of(res, my_e)) ? BM_KIND_KEPT : BM_KIND_ONDEMAND;
+            kd[lane] = kk;
+            if (a.hp.executed) {
+                a.hp.executed[(size_t)b * k + lane] = my_e;
+                a.hp.kind[(size_t)b * k + lane] = kk;
+            }
         }
         if (lane == 0 && a.used) a.used[b] = 0;
         return;
@@ -195,6 +214,10 @@ __global__ void __launch_bounds__(kRemapThreads) remap_kernel(RemapArgs a) {
     if (lane < (unsigned)k) {
         ex[lane] = out_e;
         kd[lane] = (uint8_t)out_kind;
+        if (a.hp.executed) {
+            a.hp.executed[(size_t)b * k + lane] = out_e;
+            a.hp.kind[(size_t)b * k + lane] = (uint8_t)out_kind;
+        }
     }
     if (lane == 0 && a.used) a.used[b] = (int32_t)used;
 }
@@ -211,7 +234,8 @@ int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const vo
                      int32_t fallback, int32_t method, double beta, const double *beta_dev, double eta, double kappa,
                      int32_t use_local_logit, const int32_t *partition_of, double hop, int32_t *executed,
                      uint8_t *kind, int32_t *used, double *delta_out, uint8_t *batch_allowed_out,
-                     bm_stream_t stream) {
+                     bm_stream_t stream, int32_t *hp_topk, int32_t *hp_executed, uint8_t *hp_kind,
+                     uint8_t *hp_allowed, uint8_t *hp_batch_ok) {
     BM_REQUIRE(B >= 0 && k >= 1 && k <= kMaxK && E >= 1 && E <= kMaxE, BM_EINVAL,
                "bm_buddy_remap: bad shape B=%lld k=%lld E=%lld", (long long)B, (long long)k, (long long)E);
     BM_REQUIRE(resident_bitmap && (B == 0 || (topk && executed && kind)), BM_EINVAL, "bm_buddy_remap: null pointer");
@@ -230,7 +254,8 @@ int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const vo
     }
     RemapArgs a{topk, token_allowed, logits, logits_f64, (int)B, (int)k, (int)E, resident_bitmap, tbl_ids,
                 tbl_w, tbl_len, (int)tbl_stride, (int)H, (long long)rho, fallback, method, beta, eta, kappa,
-                use_local_logit, partition_of, hop, executed, kind, used, delta_out, batch_allowed_out, beta_dev};
+                use_local_logit, partition_of, hop, executed, kind, used, delta_out, batch_allowed_out, beta_dev,
+                HostPlan{hp_topk, hp_executed, hp_kind, hp_allowed, hp_batch_ok}};
     unsigned grid = (unsigned)((B + kWarps - 1) / kWarps);
     if (grid == 0) grid = 1;  // still publish delta for an empty batch
     if (psi && method == BM_METHOD_BUDDY)
@@ -254,7 +279,7 @@ extern "C" int bm_buddy_remap(const int32_t *topk, const uint8_t *token_allowed,
     return buddy_remap_impl(topk, token_allowed, logits, logits_f64, B, k, E, resident_bitmap, tbl_ids, tbl_w,
                             tbl_len, tbl_stride, H, rho, fallback, method, beta, nullptr, eta, kappa,
                             use_local_logit, partition_of, hop, executed, kind, used, delta_out, batch_allowed_out,
-                            stream);
+                            stream, nullptr, nullptr, nullptr, nullptr, nullptr);
 }
 
 // ---------------------------------------------------------------- distribution gate alone

@@ -199,3 +199,35 @@ def test_engine_varying_batch_sizes_graphs_equal_eager():
         wl.close()
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
     assert np.array_equal(evs[0], evs[1])
+
+
+def test_engine_zero_copy_plan_equals_copies():
+    """The remap reads the residency snapshot and writes the packed plan
+    through mapped pinned memory (no upload / readback copy on the host round
+    trip); BMOE_ZERO_COPY=0 restores the copies. Same decisions, events and
+    hidden states bit for bit, with the buddy and the Random method."""
+    import os
+    wl = W.build("qwen3", layers=3, max_batch=16, profile_tokens=1024)
+    old = os.environ.get("BMOE_ZERO_COPY")
+    try:
+        for method in ("buddy", "random", "original"):
+            outs, evs = [], []
+            for zc in ("1", "0"):
+                os.environ["BMOE_ZERO_COPY"] = zc
+                eng = wl.engine(method)
+                x = torch.from_numpy(wl.tokens(4, 80)).cuda()
+                for s, B in enumerate((16, 16, 1, 16, 8)):
+                    o = sum((16, 16, 1, 16, 8)[:s])
+                    eng.step(x[o:o + B], np.arange(o, o + B))
+                torch.cuda.synchronize()
+                outs.append(x.cpu().numpy())
+                evs.append(eng.events())
+                eng.close()
+            assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32)), method
+            assert np.array_equal(evs[0], evs[1]), method
+    finally:
+        if old is None:
+            os.environ.pop("BMOE_ZERO_COPY", None)
+        else:
+            os.environ["BMOE_ZERO_COPY"] = old
+        wl.close()
