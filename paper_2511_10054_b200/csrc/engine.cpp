@@ -28,10 +28,6 @@ int buddy_remap_impl(const int32_t *topk, const uint8_t *token_allowed, const vo
                      uint8_t *hp_allowed, uint8_t *hp_batch_ok);
 int random_plan_batch(const int32_t *topk, int64_t B, int64_t k, const uint32_t *resident_bits, int64_t E,
                       bm_pcg64 *rng, int32_t *executed, uint8_t *kind, int32_t *used);
-int permute_ws_impl(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E, int64_t row_align,
-                    int32_t *expert_count, int32_t *expert_offset, int32_t *row_token, int32_t *slot_row,
-                    int32_t *chunk_scratch, int64_t scratch_elems, bm_stream_t stream, const int32_t *stage_src,
-                    int32_t *stage_dst, int32_t stage_n);
 namespace ffn {  // timing of FFN launches inside captured graphs (ffn_tc.cu)
 void *ffn_timing_take_capture();
 void ffn_timing_replayed(void *group);
@@ -214,7 +210,6 @@ struct bm_engine {
     int64_t wire_total = 0, fetch_total = 0;  // every physical fetch since creation (stats resets keep them)
     bm_pcg64 rng{};  // method RANDOM: numpy's PCG64 stream of harness.py:299-300, advanced on the host
     std::vector<int32_t *> bo_dev_l, bo_host_l;   // per-layer buffer maps (E + shared)
-    std::vector<int32_t *> bo_hostdev_l;          // bo_host_l seen from the device (zero copy: the permute copies it)
     cudaStream_t cap_stream = nullptr;
     bool use_graphs = true;
     std::map<std::pair<int, int64_t>, std::pair<int, cudaGraphExec_t>> g_pre, g_post, g_post2;
@@ -409,10 +404,7 @@ struct bm_engine {
     // are already in HBM, overlapping the H2D copies of the missing ones.
     int enqueue_post1(int l, float *h, int64_t B, bool with_combine, cudaStream_t s) {
         const int Et = E + Ssh, kt = k + Ssh;
-        const bool zc = zero_copy && !bo_hostdev_l.empty();
-        if (!zc)
-            ENG_CUDA(cudaMemcpyAsync(bo_dev_l[l], bo_host_l[l], 3 * Et * sizeof(int32_t), cudaMemcpyHostToDevice,
-                                     s));
+        ENG_CUDA(cudaMemcpyAsync(bo_dev_l[l], bo_host_l[l], 3 * Et * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         if (cfg.method == BM_METHOD_RANDOM)  // the host-drawn plan [executed | kind] replaces K2's on-demand plan
             ENG_CUDA(cudaMemcpyAsync(executed, exec_h, (size_t)B * k * 5, cudaMemcpyHostToDevice, s));
         const int32_t *pe = executed;
@@ -422,9 +414,8 @@ struct bm_engine {
             pe = exec_ext;
             pk = kind_ext;
         }
-        ENG_TRY(bm::permute_ws_impl(pe, pk, B, kt, Et, 16, count, offset, row_token, slot_row, perm_scratch,
-                                    perm_scratch_elems, s, zc ? bo_hostdev_l[l] : nullptr, zc ? bo_dev_l[l] : nullptr,
-                                    zc ? 3 * Et : 0));
+        ENG_TRY(bm_permute_ws(pe, pk, B, kt, Et, 16, count, offset, row_token, slot_row, perm_scratch,
+                              perm_scratch_elems, s));
         if (cfg.fp32_weights) {
             ENG_TRY(bm_gather_rows(h, B, d, row_token, offset, Et, r_max, 0, x_perm, s));
             return BM_OK;  // the fp32 parity path runs in one piece after the waits
@@ -918,11 +909,6 @@ static int engine_init(bm_engine *g, const bm_engine_config *c, const void *cons
         }
         g->bo_dev_l.push_back(g->bo_dev_all + (size_t)l * 3 * Et);
         g->bo_host_l.push_back(g->bo_host_all + (size_t)l * 3 * Et);
-        if (g->plan_host_dev) {
-            void *pd = nullptr;
-            ENG_CUDA(cudaHostGetDevicePointer(&pd, g->bo_host_l.back(), 0));
-            g->bo_hostdev_l.push_back(static_cast<int32_t *>(pd));
-        }
     }
     ENG_TRY(g->dmalloc(&g->count, Et));
     ENG_TRY(g->dmalloc(&g->offset, Et + 1));

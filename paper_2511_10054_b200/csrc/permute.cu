@@ -19,11 +19,8 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(const int32_t *__
                                                                const uint8_t *__restrict__ kind, int nslots, int k,
                                                                int E, int align, int32_t *expert_count,
                                                                int32_t *expert_offset, int32_t *row_token,
-                                                               int32_t *slot_row, const int32_t *stage_src,
-                                                               int32_t *stage_dst, int stage_n) {
+                                                               int32_t *slot_row) {
     __shared__ int cnt[kPermMaxE];
-    // the engine's per-layer buffer map rides along: mapped pinned host -> device (no copy node)
-    for (int i = threadIdx.x; i < stage_n; i += blockDim.x) stage_dst[i] = stage_src[i];
     __shared__ int off[kPermMaxE + 1];
     __shared__ int base[kPermMaxE];
     __shared__ int warp_cnt[kPermThreads / 32][kPermMaxE];
@@ -117,12 +114,8 @@ constexpr int kChunk = kPermThreads;
 
 __global__ void __launch_bounds__(kPermThreads) permute_hist_kernel(const int32_t *__restrict__ executed,
                                                                     const uint8_t *__restrict__ kind, int nslots,
-                                                                    int E, int32_t *__restrict__ chunk_hist,
-                                                                    const int32_t *stage_src, int32_t *stage_dst,
-                                                                    int stage_n) {
+                                                                    int E, int32_t *__restrict__ chunk_hist) {
     __shared__ int cnt[kPermMaxE];
-    if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i < stage_n; i += blockDim.x) stage_dst[i] = stage_src[i];
     for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
     __syncthreads();
     const int i = blockIdx.x * kChunk + threadIdx.x;
@@ -344,26 +337,9 @@ extern "C" int bm_permute_scratch_elems(int64_t B, int64_t k, int64_t E) {
     return (int)(((B * k + kChunk - 1) / kChunk) * E);
 }
 
-namespace bm {
-// bm_permute_ws plus an optional word copy (stage_src -> stage_dst, stage_n words) done by the
-// permute's first kernel: the engine's buffer map, read from mapped pinned host memory
-int permute_ws_impl(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E, int64_t row_align,
-                    int32_t *expert_count, int32_t *expert_offset, int32_t *row_token, int32_t *slot_row,
-                    int32_t *chunk_scratch, int64_t scratch_elems, bm_stream_t stream, const int32_t *stage_src,
-                    int32_t *stage_dst, int32_t stage_n);
-}  // namespace bm
-
 extern "C" int bm_permute_ws(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E,
                              int64_t row_align, int32_t *expert_count, int32_t *expert_offset, int32_t *row_token,
                              int32_t *slot_row, int32_t *chunk_scratch, int64_t scratch_elems, bm_stream_t stream) {
-    return bm::permute_ws_impl(executed, kind, B, k, E, row_align, expert_count, expert_offset, row_token, slot_row,
-                               chunk_scratch, scratch_elems, stream, nullptr, nullptr, 0);
-}
-
-int bm::permute_ws_impl(const int32_t *executed, const uint8_t *kind, int64_t B, int64_t k, int64_t E,
-                        int64_t row_align, int32_t *expert_count, int32_t *expert_offset, int32_t *row_token,
-                        int32_t *slot_row, int32_t *chunk_scratch, int64_t scratch_elems, bm_stream_t stream,
-                        const int32_t *stage_src, int32_t *stage_dst, int32_t stage_n) {
     BM_REQUIRE(B >= 0 && k >= 1 && E >= 1 && E <= kPermMaxE && row_align >= 1 && row_align <= 256, BM_EINVAL,
                "bm_permute: bad shape");
     BM_REQUIRE(expert_count && expert_offset && (B == 0 || (executed && kind && row_token && slot_row)), BM_EINVAL,
@@ -378,7 +354,7 @@ int bm::permute_ws_impl(const int32_t *executed, const uint8_t *kind, int64_t B,
     cudaStream_t st = as_stream(stream);
     if (multi) {  // per-chunk histograms -> chunk bases (in place) + offsets -> scatter
         permute_hist_kernel<<<(unsigned)nchunks, kPermThreads, 0, st>>>(executed, kind, (int)nslots, (int)E,
-                                                                       chunk_scratch, stage_src, stage_dst, stage_n);
+                                                                       chunk_scratch);
         BM_LAUNCH_CHECK();
         permute_scan_kernel<<<1, kPermThreads, 0, st>>>(chunk_scratch, (int)nchunks, (int)E, (int)row_align,
                                                          expert_count, expert_offset, row_token);
@@ -393,8 +369,7 @@ int bm::permute_ws_impl(const int32_t *executed, const uint8_t *kind, int64_t B,
     // per-chunk loops over warps and the barriers stay short); ranks do not depend on it
     const int threads = (int)std::min<int64_t>(kPermThreads, std::max<int64_t>(64, (nslots + 31) / 32 * 32));
     permute_kernel<<<1, threads, 0, st>>>(executed, kind, (int)nslots, (int)k, (int)E, (int)row_align,
-                                          expert_count, expert_offset, row_token, slot_row, stage_src, stage_dst,
-                                          stage_n);
+                                          expert_count, expert_offset, row_token, slot_row);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }
