@@ -71,21 +71,6 @@ bool capturing(cudaStream_t s) {
     return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
 }
 
-// Timing pass only: hold the stream for a few microseconds before an eager
-// timed call's start event, so the host has enqueued event + kernel + event
-// before the GPU reaches them (not needed inside a graph).
-__global__ void hold_kernel(unsigned long long ns) {
-    const unsigned long long t0 = ptx::globaltimer();
-    while (ptx::globaltimer() - t0 < ns) __nanosleep(500);
-}
-int hold_stream(cudaStream_t s) {
-    static const long long ns = getenv("BMOE_TIMING_HOLD_NS") ? atoll(getenv("BMOE_TIMING_HOLD_NS")) : 30000;
-    if (ns <= 0 || capturing(s)) return BM_OK;
-    hold_kernel<<<1, 32, 0, s>>>((unsigned long long)ns);
-    BM_LAUNCH_CHECK();
-    return BM_OK;
-}
-
 CallRec &new_call(cudaStream_t s) {
     auto &v = capturing(s) ? g_timing.capturing : g_timing.eager;
     v.emplace_back();
@@ -326,18 +311,13 @@ static int ffn_bf16_impl(const void *x_perm, const int32_t *expert_count, const 
                               ((reinterpret_cast<uintptr_t>(y_perm) | reinterpret_cast<uintptr_t>(cmb->h)) & 15) == 0;
         if (fuse_cmb) fp.cmb = *cmb;
         // timing record: [start, end] of the one kernel, then an empty GEMM2 interval
-        if (timing) {
-            fp.span = next_span(s, *rec);
-            if (int rc = hold_stream(s)) return rc;
-        }
+        if (timing) fp.span = next_span(s, *rec);
         if (timing && record_event(s, *rec, 0)) return BM_ECUDA;
         const int rc = launch_fused_dispatch(fp, nmat1, k1, k2, G, s);
         if (rc) return rc;
         if (timing && record_event(s, *rec, 1)) return BM_ECUDA;  // one kernel: GEMM2 interval reported as 0
         return fuse_cmb ? BM_OK : separate_combine();
     }
-    if (timing)
-        if (int rc = hold_stream(s)) return rc;
     if (timing && record_event(s, *rec, 0)) return BM_ECUDA;
     if (int rc = launch_gemm_dispatch(g1, G, s)) return rc;
     if (timing && record_event(s, *rec, 1)) return BM_ECUDA;
