@@ -484,12 +484,16 @@ int bm_synth_mix_bf16(const uint16_t *lut, uint64_t base_key, uint64_t delta_key
  * reference counterpart: the reference's transfer is an analytic cost,
  * memtier.py:41-58; this only changes how many bytes cross PCIe, never the
  * bytes that land in HBM). A value keeps its sign+mantissa byte; its exponent
- * becomes a 2-bit code for the chunk's (2048 values) three most frequent
- * exponents, or an escape followed by a 3-bit code for the next seven (code
- * 7: the exponent byte in the piece's raw list). ~10.9 bits per value for
- * N(0, s) weights. Blobs are split into self-contained pieces of
- * BM_XFER_PIECE_VALUES values (the fetch pipeline's unit); xfer.cu
- * documents the piece layout. */
+ * is coded. Piece format v3 ("BXP3", the default): one canonical Huffman code
+ * of the exponent per piece (<= 12 bits per code), 32 lane streams per
+ * 8192-value chunk, ~10.7 bits per value for N(0, s) weights (xfer_v3.cuh
+ * documents the layout). Format v2 ("BXP2", BMOE_XFER_FORMAT=2; the layout
+ * struct below): a 2-bit code for the chunk's (2048 values) three most
+ * frequent exponents, or an escape followed by a 3-bit code for the next seven
+ * (code 7: the exponent byte in the piece's raw list), ~10.9 bits per value.
+ * The decoders dispatch on the piece magic. Blobs are split into
+ * self-contained pieces of BM_XFER_PIECE_VALUES values (the fetch pipeline's
+ * unit). */
 #define BM_XFER_PIECE_VALUES (32 * 1024 * 1024)
 typedef struct {
     uint32_t magic;        /* "BXC1" */
@@ -500,7 +504,8 @@ typedef struct {
     uint64_t piece_off[1]; /* [n_pieces + 1] byte offsets from the blob start; the last = blob bytes */
 } bm_xfer_blob_header;
 typedef struct {
-    uint32_t magic; /* "BXP2" */
+    uint32_t magic; /* "BXP2" (v3 pieces: "BXP3", n_chunks of 8192 values at the same offset,
+                       bytes at the same offset; the rest per xfer_v3.cuh) */
     uint32_t n_chunks, n_raw;
     uint32_t off_planes, off_meta, off_l2, off_raw, bytes; /* from the piece start; low bytes at 32 */
 } bm_xfer_piece_header;
@@ -518,8 +523,8 @@ int bm_xfer_encode(const uint16_t *src, int64_t n_values, uint8_t *blob, int64_t
                    bm_stream_t stream);
 /* Decode a whole blob (device) into dst [n_values] bf16 (device). */
 int bm_xfer_decode(const uint8_t *blob, uint16_t *dst, int64_t n_values, bm_stream_t stream);
-/* Decode one piece (device copy, 256-byte aligned) of n_chunks chunks into
- * dst (the piece's first value). */
+/* Decode one piece (device copy, 256-byte aligned) into dst (the piece's
+ * first value); n_chunks = the piece header's (sizes the grid only). */
 int bm_xfer_decode_piece(const uint8_t *piece, uint16_t *dst, int64_t n_chunks, bm_stream_t stream);
 /* The same on at most max_ctas CTAs (0: the full grid). The engine decodes the
  * pieces that are not on its critical path (all but an expert's last) on a

@@ -1,4 +1,6 @@
-// Exponent-coded expert transfer ("fetch codec"), format v2.
+// Exponent-coded expert transfer ("fetch codec"). New blobs use piece format
+// v3 (xfer_v3.cuh: a per-piece Huffman code of the exponent, ~10.7 bits per
+// value); format v2 below stays decodable and selectable (BMOE_XFER_FORMAT=2).
 //
 // The offloaded decode step is bound by PCIe: every on-demand miss moves a
 // whole expert (336 MiB at the Mixtral shape) from the pinned host mirror
@@ -86,6 +88,8 @@ __device__ __forceinline__ const bm_xfer_piece_header *piece_at(const uint8_t *b
 __device__ __forceinline__ uint32_t byte_of(uint32_t lo, uint32_t hi, uint32_t i) {
     return __byte_perm(lo, hi, i) & 0xFFu;
 }
+
+#include "xfer_v3.cuh"
 
 // Pass 1 of the encoder: per chunk, the three most frequent exponents (t1)
 // and the next seven (t2), ties to the lower exponent; escape and raw counts.
@@ -276,25 +280,50 @@ __device__ __forceinline__ void decode_half(const uint8_t *__restrict__ pb, cons
 
 __global__ void __launch_bounds__(kThreads, 4) xfer_decode_piece_kernel(const uint8_t *__restrict__ piece,
                                                                      uint16_t *__restrict__ dst) {
+    const int warps = kThreads / 32, warp = threadIdx.x >> 5;
+    if (*reinterpret_cast<const uint32_t *>(piece) == kPieceMagic3) {  // v3: one warp per chunk
+        __shared__ __align__(16) uint16_t table[1 << kTB];
+        __shared__ uint32_t stage[kThreads / 32][kStageWords];
+        const PieceV3 ph = *reinterpret_cast<const PieceV3 *>(piece);
+        const uint4 *t = reinterpret_cast<const uint4 *>(piece + ph.off_table);
+        for (int i = threadIdx.x; i < (2 << kTB) / 16; i += kThreads) reinterpret_cast<uint4 *>(table)[i] = __ldg(t + i);
+        __syncthreads();
+        for (uint32_t c = blockIdx.x * warps + warp; c < ph.n_chunks; c += gridDim.x * warps)
+            x3_decode_chunk(piece, ph, c, table, stage[warp], dst);
+        return;
+    }
     const bm_xfer_piece_header ph = *reinterpret_cast<const bm_xfer_piece_header *>(piece);
-    const int warps = kThreads / 32;
     const int64_t units = (int64_t)ph.n_chunks * 2;
-    for (int64_t u = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); u < units; u += (int64_t)gridDim.x * warps)
+    for (int64_t u = (int64_t)blockIdx.x * warps + warp; u < units; u += (int64_t)gridDim.x * warps)
         decode_half(piece, ph, u >> 1, (int)(u & 1), dst);
 }
 
-__global__ void __launch_bounds__(kThreads, 4) xfer_decode_blob_kernel(const uint8_t *__restrict__ blob, int64_t n_chunks,
+// Whole blob, one warp per kC3 values: a v3 chunk, or the v2 half-chunks it spans.
+__global__ void __launch_bounds__(kThreads, 4) xfer_decode_blob_kernel(const uint8_t *__restrict__ blob, int64_t n_values,
                                                                     uint16_t *__restrict__ dst) {
     const auto *bh = reinterpret_cast<const bm_xfer_blob_header *>(blob);
-    const int64_t cpp = bh->piece_values / kChunk;
+    const int64_t pv = bh->piece_values;
     const int warps = kThreads / 32;
-    for (int64_t u = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); u < 2 * n_chunks;
-         u += (int64_t)gridDim.x * warps) {
-        const int64_t c = u >> 1;
-        const int p = (int)(c / cpp);
-        const uint8_t *pb = blob + bh->piece_off[p];
-        const bm_xfer_piece_header ph = *reinterpret_cast<const bm_xfer_piece_header *>(pb);
-        decode_half(pb, ph, c - (int64_t)p * cpp, (int)(u & 1), dst + (int64_t)p * bh->piece_values);
+    const int64_t units = (n_values + kC3 - 1) / kC3;
+    for (int64_t u = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); u < units; u += (int64_t)gridDim.x * warps) {
+        const int64_t v = u * kC3;
+        const int p0 = (int)(v / pv);
+        const uint8_t *pb0 = blob + bh->piece_off[p0];
+        if (*reinterpret_cast<const uint32_t *>(pb0) == kPieceMagic3) {  // v3 pieces hold whole chunks
+            const PieceV3 ph = *reinterpret_cast<const PieceV3 *>(pb0);
+            x3_decode_chunk(pb0, ph, (uint32_t)((v - p0 * pv) / kC3),
+                            reinterpret_cast<const uint16_t *>(pb0 + ph.off_table), nullptr, dst + p0 * pv);
+            continue;
+        }
+        for (int h = 0; h < 2 * kC3 / kChunk; ++h) {
+            const int64_t vh = v + (int64_t)h * (kChunk / 2);
+            if (vh >= n_values) break;
+            const int p = (int)(vh / pv);
+            const int64_t vp = vh - p * pv;
+            const uint8_t *pb = blob + bh->piece_off[p];
+            const bm_xfer_piece_header ph = *reinterpret_cast<const bm_xfer_piece_header *>(pb);
+            decode_half(pb, ph, vp / kChunk, (int)((vp / (kChunk / 2)) & 1), dst + p * pv);
+        }
     }
 }
 
@@ -333,6 +362,14 @@ int64_t piece_values() {
     return v;
 }
 
+// piece format of new blobs: BMOE_XFER_FORMAT = 2 or 3 (read per call, default 3);
+// v3 needs pieces of whole kC3 chunks
+int xfer_format() {
+    const char *ev = getenv("BMOE_XFER_FORMAT");
+    const int f = (ev && atoi(ev) == 2) ? 2 : 3;
+    return (f == 3 && piece_values() % kC3 == 0) ? 3 : 2;
+}
+
 int grid_for(int64_t n_chunks) {
     const int64_t g = std::min<int64_t>(n_chunks, (int64_t)sm_count() * 8);
     return (int)std::max<int64_t>(g, 1);
@@ -353,10 +390,97 @@ extern "C" int64_t bm_xfer_blob_bound(int64_t n_values) {
         bm_xfer_piece_header h;
         const int64_t nc = std::min(cpp, n_chunks - p * cpp);
         piece_layout(nc, nc * l2_bytes(kChunk), (uint64_t)nc * kChunk, &h);  // worst case: every value raw
-        total += h.bytes;
+        int64_t b = h.bytes;
+        if (piece_values() % kC3 == 0) {  // v3 worst case: every code kTB bits
+            PieceV3 h3;
+            const int64_t nv = nc * kChunk, nc3 = (nv + kC3 - 1) / kC3;
+            x3_layout((uint32_t)nv, (uint32_t)nc3, (uint64_t)nc3 * (kC3 * kTB / 32), &h3);
+            b = std::max<int64_t>(b, h3.bytes);
+        }
+        total += b;
     }
     return total;
 }
+
+namespace bm {
+namespace {
+// v3 encoder: exponent histograms per piece -> length-limited canonical
+// Huffman tables (host) -> stream lengths per lane -> layout (host) -> pack.
+int encode_v3(const uint16_t *src, int64_t n_values, uint8_t *blob, int64_t blob_cap, int64_t *blob_bytes_host,
+              cudaStream_t s) {
+    const int64_t pv = piece_values(), cpp = pv / kC3;
+    const int64_t n_chunks = (n_values + kC3 - 1) / kC3, n_pieces = (n_values + pv - 1) / pv;
+    uint32_t *d_hist = nullptr, *d_enc = nullptr;
+    uint16_t *d_lens = nullptr;
+    BM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&d_hist), n_pieces * 256 * 4, s));
+    BM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&d_enc), n_pieces * 256 * 4, s));
+    BM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&d_lens), n_chunks * 32 * 2, s));
+    BM_CUDA_TRY(cudaMemsetAsync(d_hist, 0, n_pieces * 256 * 4, s));
+    x3_hist_kernel<<<grid_for(n_chunks), 256, 0, s>>>(src, n_values, cpp, d_hist);
+    BM_LAUNCH_CHECK();
+    std::vector<uint32_t> hist(n_pieces * 256), enc(n_pieces * 256);
+    std::vector<uint16_t> tables(n_pieces << kTB), lens(n_chunks * 32);
+    BM_CUDA_TRY(cudaMemcpyAsync(hist.data(), d_hist, hist.size() * 4, cudaMemcpyDeviceToHost, s));
+    BM_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int64_t p = 0; p < n_pieces; ++p) {
+        uint8_t len[256];
+        x3_code_lengths(hist.data() + p * 256, len);
+        x3_tables(len, enc.data() + p * 256, tables.data() + (p << kTB));
+    }
+    BM_CUDA_TRY(cudaMemcpyAsync(d_enc, enc.data(), enc.size() * 4, cudaMemcpyHostToDevice, s));
+    x3_lens_kernel<<<grid_for((n_chunks * 32 + 255) / 256), 256, 0, s>>>(src, n_values, cpp, d_enc, d_lens);
+    BM_LAUNCH_CHECK();
+    BM_CUDA_TRY(cudaMemcpyAsync(lens.data(), d_lens, lens.size() * 2, cudaMemcpyDeviceToHost, s));
+    BM_CUDA_TRY(cudaStreamSynchronize(s));
+    // layout: chunk stream bases and piece sizes
+    const int64_t hb = header_bytes(n_pieces);
+    std::vector<uint8_t> head(hb, 0);
+    auto *bh = reinterpret_cast<bm_xfer_blob_header *>(head.data());
+    bh->magic = kBlobMagic;
+    bh->n_pieces = (uint32_t)n_pieces;
+    bh->n_values = (uint64_t)n_values;
+    bh->piece_values = (uint32_t)pv;
+    std::vector<uint32_t> cbase(n_chunks);
+    std::vector<PieceV3> phs(n_pieces);
+    uint64_t off = hb;
+    for (int64_t p = 0; p < n_pieces; ++p) {
+        const int64_t c0 = p * cpp, nc = std::min(cpp, n_chunks - c0);
+        uint64_t words = 0;
+        for (int64_t c = c0; c < c0 + nc; ++c) {
+            cbase[c] = (uint32_t)words;
+            uint64_t bits = 0;
+            for (int l = 0; l < 32; ++l) bits += lens[c * 32 + l];
+            words += (bits + 31) / 32;
+        }
+        x3_layout((uint32_t)std::min<int64_t>(pv, n_values - p * pv), (uint32_t)nc, words, &phs[p]);
+        bh->piece_off[p] = off;
+        off += phs[p].bytes;
+    }
+    bh->piece_off[n_pieces] = off;
+    BM_REQUIRE((int64_t)off <= blob_cap, BM_EINVAL, "bm_xfer_encode: blob_cap %lld < %llu bytes",
+               (long long)blob_cap, (unsigned long long)off);
+    BM_CUDA_TRY(cudaMemsetAsync(blob, 0, off, s));  // streams are OR-ed in
+    BM_CUDA_TRY(cudaMemcpyAsync(blob, head.data(), hb, cudaMemcpyHostToDevice, s));
+    for (int64_t p = 0; p < n_pieces; ++p) {
+        uint8_t *pb = blob + bh->piece_off[p];
+        const int64_t c0 = p * cpp, nc = std::min(cpp, n_chunks - c0);
+        BM_CUDA_TRY(cudaMemcpyAsync(pb, &phs[p], sizeof(PieceV3), cudaMemcpyHostToDevice, s));
+        BM_CUDA_TRY(cudaMemcpyAsync(pb + phs[p].off_table, tables.data() + (p << kTB), 2 << kTB,
+                                    cudaMemcpyHostToDevice, s));
+        BM_CUDA_TRY(cudaMemcpyAsync(pb + phs[p].off_lens, lens.data() + c0 * 32, nc * 64, cudaMemcpyHostToDevice, s));
+        BM_CUDA_TRY(cudaMemcpyAsync(pb + phs[p].off_cbase, cbase.data() + c0, nc * 4, cudaMemcpyHostToDevice, s));
+    }
+    x3_pack_kernel<<<grid_for((n_chunks + 7) / 8), 256, 0, s>>>(src, n_values, cpp, d_enc, blob);
+    BM_LAUNCH_CHECK();
+    BM_CUDA_TRY(cudaStreamSynchronize(s));  // the host images above must outlive their copies
+    BM_CUDA_TRY(cudaFreeAsync(d_hist, s));
+    BM_CUDA_TRY(cudaFreeAsync(d_enc, s));
+    BM_CUDA_TRY(cudaFreeAsync(d_lens, s));
+    *blob_bytes_host = (int64_t)off;
+    return BM_OK;
+}
+}  // namespace
+}  // namespace bm
 
 extern "C" int bm_xfer_encode(const uint16_t *src, int64_t n_values, uint8_t *blob, int64_t blob_cap,
                               int64_t *blob_bytes_host, bm_stream_t stream) {
@@ -366,6 +490,7 @@ extern "C" int bm_xfer_encode(const uint16_t *src, int64_t n_values, uint8_t *bl
     BM_REQUIRE(((uintptr_t)src & 15) == 0 && ((uintptr_t)blob & 255) == 0, BM_EINVAL,
                "bm_xfer_encode: src must be 16-byte and blob 256-byte aligned");
     cudaStream_t s = as_stream(stream);
+    if (xfer_format() == 3) return encode_v3(src, n_values, blob, blob_cap, blob_bytes_host, s);
     const int64_t n_chunks = n_values / kChunk;
     const int64_t cpp = piece_values() / kChunk;
     const int64_t n_pieces = (n_chunks + cpp - 1) / cpp;
@@ -432,8 +557,8 @@ extern "C" int bm_xfer_decode(const uint8_t *blob, uint16_t *dst, int64_t n_valu
                (long long)n_values);
     BM_REQUIRE(((uintptr_t)dst & 15) == 0 && ((uintptr_t)blob & 255) == 0, BM_EINVAL,
                "bm_xfer_decode: dst must be 16-byte and blob 256-byte aligned");
-    const int64_t n_chunks = n_values / kChunk;
-    xfer_decode_blob_kernel<<<grid_for(n_chunks / 4 + 1), kThreads, 0, as_stream(stream)>>>(blob, n_chunks, dst);
+    xfer_decode_blob_kernel<<<grid_for((n_values + kC3 - 1) / kC3 / 8 + 1), kThreads, 0, as_stream(stream)>>>(
+        blob, n_values, dst);
     BM_LAUNCH_CHECK();
     return BM_OK;
 }

@@ -130,7 +130,7 @@ def build(name: str = "mixtral", layers: int = 32, max_batch: int = 16, seed: in
           clusters: int | None = None, n_tile: int = 128, device: str = "cuda", rho: int | None = 3,
           codec: int = 1, share: ShareSpec | None = None, log=None, cache_rate: float | None = None,
           profile: str = "forward", clustered: bool = True) -> Workload:
-    """codec 1 keeps the pinned mirrors exponent-coded (bm_xfer_*: ~0.70 of
+    """codec 1 keeps the pinned mirrors exponent-coded (bm_xfer_*: ~0.67 of
     the bf16 bytes cross PCIe per miss, rebuilt bit-exactly in HBM); 0 raw.
     share: one node-shared mirror per layer for all local replicas (only the
     writing rank generates the weights).

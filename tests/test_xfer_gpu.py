@@ -14,8 +14,36 @@ from paper_2511_10054_b200 import ops
 pytestmark = pytest.mark.gpu
 
 
+def _np_decode_v3(pb: np.ndarray) -> np.ndarray:
+    """Piece format v3 (xfer_v3.cuh): low bytes, a 4096-entry decode table,
+    per-lane stream bit lengths and per-chunk stream bases; lane l of a chunk
+    owns the 16-value groups g*32 + l and reads one LSB-first bit stream."""
+    magic, nch, nv, o_tab, o_lens, o_cb, o_st, nbytes = np.frombuffer(pb[:32].tobytes(), np.uint32)
+    assert magic == 0x33505842 and nbytes == pb.size
+    low = pb[32:32 + nv].astype(np.uint16)
+    table = np.frombuffer(pb[o_tab:o_tab + 8192].tobytes(), np.uint16)
+    lens = np.frombuffer(pb[o_lens:o_lens + 64 * nch].tobytes(), np.uint16).reshape(nch, 32)
+    cbase = np.frombuffer(pb[o_cb:o_cb + 4 * nch].tobytes(), np.uint32)
+    bits = np.unpackbits(pb[o_st:], bitorder="little")
+    exp = np.zeros(nv, np.uint16)
+    for c in range(nch):
+        v0 = c * 8192
+        per = min(8192, nv - v0) // 32
+        start = 32 * int(cbase[c]) + np.concatenate([[0], np.cumsum(lens[c].astype(np.int64))[:-1]])
+        for l in range(32):
+            pos = int(start[l])
+            for v in range(per):
+                peek = int(np.dot(bits[pos:pos + 12].astype(np.int64), 1 << np.arange(12)))
+                ent = int(table[peek])
+                exp[v0 + ((v // 16) * 32 + l) * 16 + v % 16] = ent & 0xFF
+                pos += ent >> 8
+            assert pos == start[l] + lens[c, l]
+    return ((low & 0x80) << 8) | (exp << 7) | (low & 0x7F)
+
+
 def _np_decode(blob: np.ndarray) -> np.ndarray:
-    """Reference decoder written from the format comments in bmoe.h/xfer.cu (v2)."""
+    """Reference decoder written from the format comments in bmoe.h/xfer.cu
+    (v2) and xfer_v3.cuh (v3)."""
     u32 = lambda a, o: int(np.frombuffer(a[o:o + 4].tobytes(), np.uint32)[0])
     u64 = lambda a, o: int(np.frombuffer(a[o:o + 8].tobytes(), np.uint64)[0])
     assert u32(blob, 0) == 0x31435842
@@ -25,6 +53,9 @@ def _np_decode(blob: np.ndarray) -> np.ndarray:
     out = []
     for p in range(n_pieces):
         pb = blob[offs[p]:offs[p + 1]]
+        if int(np.frombuffer(pb[:4].tobytes(), np.uint32)[0]) == 0x33505842:
+            out.append(_np_decode_v3(pb))
+            continue
         magic, nch, nraw, o_pl, o_meta, o_l2, o_raw, nbytes = np.frombuffer(pb[:32].tobytes(), np.uint32)
         assert magic == 0x32505842 and nbytes == pb.size
         low = pb[32:32 + nch * 2048].reshape(nch, 2048).astype(np.uint16)
@@ -69,21 +100,35 @@ def _special(n, gen):
     return x
 
 
-@pytest.mark.parametrize("n", [2048, 3 * 2048, 65536 * 3, 32 * 1024 * 1024 + 4096])
-def test_roundtrip_bit_exact(cuda_ok, n):
+@pytest.fixture(params=[2, 3], ids=["v2", "v3"])
+def xfer_format(request, monkeypatch):
+    """Piece format of the blobs the test encodes (BMOE_XFER_FORMAT, read per call)."""
+    monkeypatch.setenv("BMOE_XFER_FORMAT", str(request.param))
+    return request.param
+
+
+def _piece_format(blob) -> int:
+    off0 = int(np.frombuffer(blob[24:32].cpu().numpy().tobytes(), np.uint64)[0])
+    return {0x32505842: 2, 0x33505842: 3}[int(np.frombuffer(blob[off0:off0 + 4].cpu().numpy().tobytes(), np.uint32)[0])]
+
+
+@pytest.mark.parametrize("n", [2048, 3 * 2048, 8192 + 2048, 65536 * 3, 32 * 1024 * 1024 + 4096])
+def test_roundtrip_bit_exact(cuda_ok, xfer_format, n):
     gen = torch.Generator(device="cuda")
     gen.manual_seed(n)
     x = _special(n, gen)
     blob = ops.xfer_encode(x)
+    assert _piece_format(blob) == xfer_format
     y = ops.xfer_decode(blob, n)
     assert np.array_equal(_bits(x), _bits(y))
     if n <= 65536 * 3:
         assert np.array_equal(_np_decode(blob.cpu().numpy()), _bits(x))
 
 
-def test_ratio_and_piecewise_decode(cuda_ok):
-    """N(0, 1/sqrt(fan_in)) weights: <= 0.69 of the raw bytes; decoding the
-    pieces one by one (the engine's pipeline) equals the whole-blob decode."""
+def test_ratio_and_piecewise_decode(cuda_ok, xfer_format):
+    """N(0, 1/sqrt(fan_in)) weights: <= 0.69 of the raw bytes (v3: <= 0.67);
+    decoding the pieces one by one (the engine's pipeline) equals the
+    whole-blob decode."""
     from paper_2511_10054_b200 import _native as N
     n = 3 * 4096 * 14336 // 2  # half a Mixtral expert, 3 pieces
     x = torch.empty(n, dtype=torch.bfloat16, device="cuda")
@@ -92,7 +137,7 @@ def test_ratio_and_piecewise_decode(cuda_ok):
     blob = ops.xfer_encode(x)
     ratio = blob.numel() / (2 * n)
     print(f"coded/raw = {ratio:.4f}")
-    assert ratio <= 0.69
+    assert ratio <= (0.69 if xfer_format == 2 else 0.67)
     hb = blob[:256].cpu().numpy()
     n_pieces = int(np.frombuffer(hb[4:8].tobytes(), np.uint32)[0])
     offs = np.frombuffer(blob[24:24 + 8 * (n_pieces + 1)].cpu().numpy().tobytes(), np.uint64)
@@ -178,3 +223,12 @@ def test_adaptive_beta_on_measured_wire_bytes(cuda_ok):
             assert any(betas[b, "wire"][0] > betas[b, "logical"][0] for b in (1e8, 2.5e8, 4e8, 6e8, 2e9)), \
                 {b: (betas[b, "logical"][0], betas[b, "wire"][0]) for b in (1e8, 2.5e8, 4e8, 6e8, 2e9)}
         wl.close()
+
+
+@pytest.mark.parametrize("fill", [0.0, 1.0, -3.5])
+def test_roundtrip_single_exponent(cuda_ok, xfer_format, fill):
+    """A blob whose exponent takes one value (v3: a one-symbol code, 1 bit per value)."""
+    x = torch.full((3 * 8192 + 2048,), fill, dtype=torch.bfloat16, device="cuda")
+    blob = ops.xfer_encode(x)
+    assert np.array_equal(_bits(ops.xfer_decode(blob, x.numel())), _bits(x))
+    assert np.array_equal(_np_decode(blob.cpu().numpy()), _bits(x))
