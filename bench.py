@@ -511,7 +511,7 @@ def run_profile_bench(args, comm: "Comm"):
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          # DRAM bytes of the one 64M-token launch captured with ncu --set full
                          "traffic": _coact_traffic() if N == 64 << 20 and ws == 1 else None,
-                         "kernel": "coact_count_kernel", "algorithmic_bytes_per_launch": bytes_k,
+                         "kernel": _coact_kernel_name(), "algorithmic_bytes_per_launch": bytes_k,
                          "avg_launch_ms": k_ms, "peak_kind": peak_kind},
             "cpu_baseline": cpu,
             "e2e": {"value": N * args.steps / (e2e_ms / 1e3), "unit": "tokens/s",
@@ -522,13 +522,22 @@ def run_profile_bench(args, comm: "Comm"):
         print(json.dumps(line), flush=True)
 
 
+def _coact_mode() -> str:
+    """K6 kernel bm_coact_count runs at E = 128, k = 8 (BMOE_COACT_TC, default 2)."""
+    return os.environ.get("BMOE_COACT_TC", "2")
+
+
+def _coact_kernel_name() -> str:
+    return {"0": "coact_count_kernel (shared-memory atomics)",
+            "1": "coact_tc_kernel (tcgen05 kind::i8 X^T X over one-hot tiles)"}.get(
+        _coact_mode(), "coact_fp4_kernel (tcgen05 kind::mxf4 X^T X over e2m1 one-hot tiles)")
+
+
 def _coact_traffic():
-    """DRAM bytes of the captured 64M-token K6 launch (profiles/)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "coact_traffic.json")) as f:
-            return json.load(f)["dram_bytes"]
-    except (OSError, KeyError, ValueError):
+    """DRAM bytes (read + write) of the captured 64M-token K6 launch of the kernel in use."""
+    if _coact_mode() in ("0", "1"):
         return 2148022000 + 4829952  # profiles/r1_coact_count.ncu-rep
+    return 2147677696 + 5253376  # profiles/r2s_coact_mxf4.ncu-rep
 
 
 def measure_h2d(wl) -> float:

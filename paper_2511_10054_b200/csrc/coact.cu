@@ -303,6 +303,220 @@ __global__ void __launch_bounds__(kTcThreads) coact_tc_kernel(const int32_t *__r
     if (warp == kTcBuild / 32) ptx::tmem_dealloc(tmem, 128);
 }
 
+// K6 on the FP4 tensor cores (E <= 128): the same X^T X, with the one-hot
+// entries as packed e2m1 1.0 (a nibble per token: half the operand bytes of
+// the u8 path, whose shared-memory traffic bound it) and block scales fixed
+// at 1.0 in TMEM; f32 accumulation is exact while a CTA's counts stay below
+// 2^24 (the launcher caps tokens per CTA). A builder warp owns one 16 KB
+// stage of 256 tokens (expert rows of 128 B, 128B-swizzled, K-major): lane l
+// takes tokens 8l..8l+7 = 32-bit word l of every row; the warp zeroes the
+// stage with 16-byte stores, then each lane ORs a nibble per (token, id)
+// into its own words. The MMA thread issues 4 kind::mxf4 MMAs (K = 64) per
+// stage, A = B = the stage. Token order inside a row is irrelevant (the
+// product sums over it), only the row = expert mapping matters.
+constexpr int kF4Warps = 12;                       // builder warps = stages
+constexpr int kF4Threads = (kF4Warps + 1) * 32;    // + the MMA warp
+constexpr uint32_t kF4Stage = 128 * 128;           // 256 tokens x 128 expert rows, 4 bits each
+constexpr size_t kF4Smem = (size_t)kF4Warps * kF4Stage + 1024;
+constexpr long long kF4MaxPerBlock = 1LL << 23;    // f32-exact counts per CTA
+
+template <int KC>
+__global__ void __launch_bounds__(kF4Threads) coact_fp4_kernel(const int32_t *__restrict__ topk, long long N, int k_rt,
+                                                               int E, long long per_block,
+                                                               unsigned long long *__restrict__ counts,
+                                                               unsigned long long *__restrict__ pairs,
+                                                               int *__restrict__ invalid) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2 * kF4Warps + 1];
+    __shared__ uint32_t tmem_sh;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const unsigned lane = lane_id();
+    const int k = KC > 0 ? KC : k_rt;
+    const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t *base_ptr = smem_raw + (base - ptx::smem_u32(smem_raw));
+    const uint32_t full0 = ptx::smem_u32(&bars[0]), empty0 = ptx::smem_u32(&bars[kF4Warps]),
+                   done = ptx::smem_u32(&bars[2 * kF4Warps]);
+    const long long t0 = (long long)blockIdx.x * per_block, t1 = min(N, t0 + per_block);
+    const long long nchunks = t1 > t0 ? (t1 - t0 + 255) / 256 : 0;
+    if (tid == 0) {
+        for (int s = 0; s < kF4Warps; ++s) {
+            ptx::mbar_init(full0 + 8 * s, 1);
+            ptx::mbar_init(empty0 + 8 * s, 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::fence_barrier_init();
+    }
+    // TMEM: accumulator columns [0, 128), block scales (all 1.0 = ue8m0 127) in [128, 144)
+    if (warp == kF4Warps) ptx::tmem_alloc(ptx::smem_u32(&tmem_sh), 256);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_sh;
+    if (warp < 4) {
+        ptx::tmem_fill8(tmem + ((uint32_t)(warp * 32) << 16) + 128u, 0x7F7F7F7Fu);
+        ptx::tmem_fill8(tmem + ((uint32_t)(warp * 32) << 16) + 136u, 0x7F7F7F7Fu);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp < kF4Warps) {
+        constexpr int KM = KC > 0 ? KC : kTcMaxK;
+        uint8_t *stage = base_ptr + (size_t)warp * kF4Stage;
+        // lane's word in row e: 128B swizzle of 16-byte chunk (lane/4) by (e & 7)
+        const uint32_t wcol = ((lane & 3u) << 2), wchunk = lane >> 2;
+        int bad = 0;
+        for (long long c = warp, u = 0; c < nchunks; c += kF4Warps, ++u) {
+            if constexpr (KC == 8) {
+                // coalesced: lane l loads 16-byte piece i*32 + l of the chunk's ids, i.e. half
+                // (l & 1) of token 16i + l/2; the partner lane holds the other half. Token
+                // 16i + m goes to word m + 16 (i & 1), nibble i / 2 of its expert rows.
+                const long long tc0 = t0 + c * 256;
+                const int4 *p = reinterpret_cast<const int4 *>(topk + tc0 * 8);
+                int4 v[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const long long t = tc0 + 16 * i + (lane >> 1);
+                    v[i] = t < t1 ? __ldg(p + i * 32 + lane) : make_int4(0, 0, 0, 0);
+                }
+                uint32_t okm = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const long long t = tc0 + 16 * i + (lane >> 1);
+                    int o[4];
+                    o[0] = __shfl_xor_sync(0xffffffffu, v[i].x, 1);
+                    o[1] = __shfl_xor_sync(0xffffffffu, v[i].y, 1);
+                    o[2] = __shfl_xor_sync(0xffffffffu, v[i].z, 1);
+                    o[3] = __shfl_xor_sync(0xffffffffu, v[i].w, 1);
+                    if (t >= t1) continue;
+                    const int a[8] = {v[i].x, v[i].y, v[i].z, v[i].w, o[0], o[1], o[2], o[3]};
+                    bool badrow = false;
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        badrow |= (unsigned)a[x] >= (unsigned)E;
+#pragma unroll
+                        for (int y = 0; y < x; ++y) badrow |= a[x] == a[y];
+                    }
+                    if (badrow) bad += (lane & 1) == 0;
+                    else okm |= 1u << i;
+                }
+                ptx::mbar_wait(empty0 + 8 * warp, (uint32_t)(u & 1) ^ 1u);
+                uint4 *z = reinterpret_cast<uint4 *>(stage);
+#pragma unroll 8
+                for (int m = (int)lane; m < (int)(kF4Stage / 16); m += 32) z[m] = make_uint4(0, 0, 0, 0);
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    if (!((okm >> i) & 1u)) continue;
+                    const uint32_t w = (lane >> 1) + 16u * (uint32_t)(i & 1), bit = 2u << (4 * (i >> 1));
+                    const int ids[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const uint32_t e = (uint32_t)ids[x];
+                        atomicOr(reinterpret_cast<uint32_t *>(stage + e * 128u + ((((w >> 2) ^ (e & 7u)) << 4) |
+                                                                                  ((w & 3u) << 2))),
+                                 bit);  // e2m1 1.0
+                    }
+                }
+                ptx::fence_proxy_async_shared();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(full0 + 8 * warp);
+                continue;
+            }
+            const long long tb = t0 + c * 256 + 8 * (long long)lane;
+            int id[8][KM];
+            uint32_t okm = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const long long t = tb + j;
+                if (t >= t1) break;
+                if constexpr (KC == 8) {
+                    const int4 *p = reinterpret_cast<const int4 *>(topk + t * 8);
+                    const int4 a = __ldg(p), b = __ldg(p + 1);
+                    id[j][0] = a.x; id[j][1] = a.y; id[j][2] = a.z; id[j][3] = a.w;
+                    id[j][4] = b.x; id[j][5] = b.y; id[j][6] = b.z; id[j][7] = b.w;
+                } else {
+#pragma unroll
+                    for (int x = 0; x < KM; ++x)
+                        if (x < k) id[j][x] = __ldg(topk + t * k + x);
+                }
+                bool badrow = false;
+#pragma unroll
+                for (int x = 0; x < KM; ++x) {
+                    if (x >= k) break;
+                    badrow |= (unsigned)id[j][x] >= (unsigned)E;
+#pragma unroll
+                    for (int y = 0; y < x; ++y) badrow |= id[j][x] == id[j][y];
+                }
+                if (badrow) ++bad;
+                else okm |= 1u << j;
+            }
+            ptx::mbar_wait(empty0 + 8 * warp, (uint32_t)(u & 1) ^ 1u);  // the MMAs that read the stage are done
+            uint4 *z = reinterpret_cast<uint4 *>(stage);
+#pragma unroll 8
+            for (int m = (int)lane; m < (int)(kF4Stage / 16); m += 32) z[m] = make_uint4(0, 0, 0, 0);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (!((okm >> j) & 1u)) continue;
+#pragma unroll
+                for (int x = 0; x < KM; ++x) {
+                    if (x >= k) break;
+                    const uint32_t e = (uint32_t)id[j][x];
+                    atomicOr(reinterpret_cast<uint32_t *>(stage + e * 128u + (((wchunk ^ (e & 7u)) << 4) | wcol)),
+                             2u << (4 * j));  // e2m1 1.0
+                }
+            }
+            ptx::fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(full0 + 8 * warp);
+        }
+        bad += __shfl_xor_sync(0xffffffffu, bad, 16);
+        bad += __shfl_xor_sync(0xffffffffu, bad, 8);
+        bad += __shfl_xor_sync(0xffffffffu, bad, 4);
+        bad += __shfl_xor_sync(0xffffffffu, bad, 2);
+        bad += __shfl_xor_sync(0xffffffffu, bad, 1);
+        if (lane == 0 && bad) atomicAdd(invalid, bad);
+    } else if (lane == 0) {  // the MMA issuer
+        const uint32_t idesc = ptx::idesc_mxf4(128, 128);
+        for (long long c = 0; c < nchunks; ++c) {
+            const int s = (int)(c % kF4Warps);
+            ptx::mbar_wait(full0 + 8 * s, (uint32_t)((c / kF4Warps) & 1));
+            ptx::tc_fence_after();
+            const uint64_t d = ptx::sw128_desc(base + (uint32_t)s * kF4Stage);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)  // K = 64 tokens per MMA: 32 bytes along the row
+                ptx::mma_mxf4(tmem, d + 2 * kk, d + 2 * kk, idesc, tmem + 128u, tmem + 136u, (c | kk) != 0 ? 1u : 0u);
+            ptx::mma_commit(empty0 + 8 * s);
+        }
+        if (nchunks > 0) ptx::mma_commit(done);
+    }
+    // epilogue: warp w < 4 reads TMEM lanes 32w.. (rows i) x 128 columns (j); counts are exact f32
+    if (warp < 4 && nchunks > 0) {
+        ptx::mbar_wait(done, 0);
+        ptx::tc_fence_after();
+        const int i = warp * 32 + (int)lane;
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+            float v[16];
+            ptx::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            if (i >= E) continue;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int col = c0 + j;
+                const unsigned long long n = (unsigned long long)v[j];
+                if (col >= E || n == 0) continue;
+                if (col == i)
+                    atomicAdd(&counts[i], n);
+                else
+                    atomicAdd(&pairs[(size_t)i * E + col], n);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == kF4Warps) ptx::tmem_dealloc(tmem, 256);
+}
+
 __global__ void coact_weighted_kernel(const int32_t *__restrict__ topk, const float *__restrict__ probs, long long N,
                                       int k, int E, double w, double *__restrict__ pw) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -461,11 +675,33 @@ extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t
                "bm_coact_count: bad shape N=%lld k=%lld E=%lld", (long long)N, (long long)k, (long long)E);
     BM_REQUIRE(counts && pairs && invalid_rows && (topk || N == 0), BM_EINVAL, "bm_coact_count: null pointer");
     if (N == 0) return BM_OK;
-    // tensor-core path for E <= 128 (BMOE_COACT_TC=1; off by default: 1.08-1.42 ms against the atomics
-    // kernel's 1.00 ms on the 64M-token trace, bound by shared-memory traffic -- DESIGN §7)
-    const char *tc_ev = getenv("BMOE_COACT_TC");  // read per call (tests switch it)
-    const int tc_env = tc_ev ? atoi(tc_ev) : 0;
-    if (tc_env && E <= 128 && k <= kTcMaxK && (k != 8 || (reinterpret_cast<uintptr_t>(topk) & 15) == 0)) {
+    // path (BMOE_COACT_TC, read per call: tests and benches switch it): 2 (default, E <= 128, k <= 16)
+    // the kind::mxf4 tensor-core kernel, 0.84 / 0.99 ms on the 64M-token uniform / Zipf traces;
+    // 0 the shared-memory atomics kernel (0.89 / 1.01 ms; any E); 1 the kind::i8 tensor-core
+    // kernel (1.28 ms, bound by shared-memory traffic) -- DESIGN §7
+    const char *tc_ev = getenv("BMOE_COACT_TC");
+    const int tc_env = tc_ev ? atoi(tc_ev) : 2;
+    if (tc_env == 2 && E <= 128 && k <= kTcMaxK && (k != 8 || (reinterpret_cast<uintptr_t>(topk) & 15) == 0)) {
+        auto fk = k == 8 ? coact_fp4_kernel<8> : coact_fp4_kernel<0>;
+        static bool fattr = false;
+        if (!fattr) {
+            BM_CUDA_TRY(cudaFuncSetAttribute(coact_fp4_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kF4Smem));
+            BM_CUDA_TRY(cudaFuncSetAttribute(coact_fp4_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kF4Smem));
+            fattr = true;
+        }
+        long long blocks = (long long)sm_count();
+        const long long need = (N + 4LL * 256 * kF4Warps - 1) / (4LL * 256 * kF4Warps);  // >= 4 stages per warp
+        blocks = std::max(1LL, std::min(blocks, need));
+        blocks = std::max(blocks, (N + kF4MaxPerBlock - 1) / kF4MaxPerBlock);
+        const long long per_block = (N + blocks - 1) / blocks;
+        fk<<<(unsigned)blocks, kF4Threads, kF4Smem, as_stream(stream)>>>(topk, N, (int)k, (int)E, per_block, counts,
+                                                                         pairs, invalid_rows);
+        BM_LAUNCH_CHECK();
+        return BM_OK;
+    }
+    if (tc_env == 1 && E <= 128 && k <= kTcMaxK && (k != 8 || (reinterpret_cast<uintptr_t>(topk) & 15) == 0)) {
         auto tk = k == 8 ? coact_tc_kernel<8> : coact_tc_kernel<0>;
         static bool attr = false;
         if (!attr) {

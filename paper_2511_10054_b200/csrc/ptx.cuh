@@ -159,6 +159,28 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// Block-scaled FP4 MMA (A, B packed e2m1 in shared memory, K = 64 per
+// instruction, one ue8m0 scale per 32 elements read from TMEM at sfa / sfb).
+__device__ __forceinline__ void mma_mxf4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb));
+}
+// Instruction descriptor, kind::mxf4: A/B E2M1 (bits 7-9, 10-12 = 1), both
+// K-major, K = 64, N>>3 at [17,23), scales UE8M0 (bit 23), M>>4 at [24,29);
+// scale-factor ids 0 (column-aligned TMEM addresses); D is f32.
+__device__ __forceinline__ uint32_t idesc_mxf4(uint32_t M, uint32_t N) {
+    return (1u << 7) | (1u << 10) | ((N >> 3) << 17) | (1u << 23) | ((M >> 4) << 24);
+}
+// 32 lanes x 8 consecutive 32-bit TMEM columns <- the same word in every cell
+__device__ __forceinline__ void tmem_fill8(uint32_t taddr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr), "r"(v)
+                 : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 // Instruction descriptor, kind::i8: D s32 (bits 4-5 = 2), A/B unsigned 8-bit
 // (bits 7-9, 10-12 = 0), both K-major, N>>3 at [17,23), M>>4 at [24,29).
 __device__ __forceinline__ uint32_t idesc_u8_s32(uint32_t M, uint32_t N) {

@@ -678,10 +678,13 @@ def test_ffn_phase_trace(cuda_ok, monkeypatch):
     assert np.all(st[:, 0] <= st[:, 1]) and np.all(st[:, 1] <= st[:, 7])
 
 
-@pytest.mark.parametrize("E,k,n", [(128, 8, 300_001), (64, 6, 100_003), (100, 3, 50_000), (8, 2, 20_000)])
-def test_coact_tensor_core_path_bit_exact(cuda_ok, monkeypatch, E, k, n):
-    """K6's tcgen05 kind::i8 path (BMOE_COACT_TC=1: X^T X over one-hot tiles in
-    TMEM) gives exactly the shared-memory-atomics kernel's counts, pairs and
+@pytest.mark.parametrize("tc", ["1", "2"], ids=["i8", "mxf4"])
+@pytest.mark.parametrize("E,k,n", [(128, 8, 300_001), (64, 6, 100_003), (100, 3, 50_000), (8, 2, 20_000),
+                                   (128, 8, 255), (128, 16, 70_001)])
+def test_coact_tensor_core_path_bit_exact(cuda_ok, monkeypatch, tc, E, k, n):
+    """K6's tensor-core paths (BMOE_COACT_TC=1: tcgen05 kind::i8, =2: kind::mxf4
+    with e2m1 one-hots and unit block scales; X^T X over one-hot tiles in TMEM)
+    give exactly the shared-memory-atomics kernel's counts, pairs and
     rejected-row count, rejected rows (duplicates, out-of-range ids) included."""
     rng = np.random.default_rng(E * 31 + k)
     topk = np.stack([rng.choice(E, k, replace=False) for _ in range(n)]).astype(np.int32)
@@ -690,8 +693,8 @@ def test_coact_tensor_core_path_bit_exact(cuda_ok, monkeypatch, E, k, n):
     topk[bad[25:], 1] = E + 3               # out of range
     t = _t(topk)
     out = []
-    for tc in ("0", "1"):
-        monkeypatch.setenv("BMOE_COACT_TC", tc)
+    for mode in ("0", tc):
+        monkeypatch.setenv("BMOE_COACT_TC", mode)
         c = torch.zeros(E, dtype=torch.int64, device=DEV)
         p = torch.zeros(E, E, dtype=torch.int64, device=DEV)
         badc = torch.zeros(1, dtype=torch.int32, device=DEV)

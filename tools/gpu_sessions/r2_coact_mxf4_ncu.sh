@@ -1,0 +1,3 @@
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:coact_fp4 -c 1 -o gpurun_out/r2s_coact_mxf4 -f \
+  python tools/coact_bench.py --modes 2 --iters 1 > gpurun_out/r2s_coact_mxf4_ncu.log 2>&1
+tail -3 gpurun_out/r2s_coact_mxf4_ncu.log

@@ -91,4 +91,26 @@ if __name__ == "__main__":
     assert eng.stats()["wire_bytes"] > 0
     eng.close()
     wl.close()
+    # fetch codec v3 and v2 (the v3 decoder reads up to 3 words past a lane's stream: piece slack)
+    for fmt in ("3", "2"):
+        os.environ["BMOE_XFER_FORMAT"] = fmt
+        xv = (torch.randn(3 * 8192 + 2048).cuda() * 0.02).to(torch.bfloat16)
+        assert torch.equal(ops.xfer_decode(ops.xfer_encode(xv), xv.numel()).view(torch.int16), xv.view(torch.int16))
+    os.environ.pop("BMOE_XFER_FORMAT")
+    # K6 on every path (mxf4 tensor cores, i8 tensor cores, atomics), k = 8 and a general k
+    from paper_2511_10054_b200 import _native as N
+    for kk, EE, n in ((8, 128, 5000), (3, 100, 777)):
+        tk6 = torch.from_numpy(np.stack([rng.choice(EE, kk, replace=False) for _ in range(n)]).astype(np.int32)).cuda()
+        res = []
+        for mode in ("2", "1", "0"):
+            os.environ["BMOE_COACT_TC"] = mode
+            c = torch.zeros(EE, dtype=torch.int64).cuda()
+            pp = torch.zeros(EE, EE, dtype=torch.int64).cuda()
+            bad = torch.zeros(1, dtype=torch.int32).cuda()
+            N.call("bm_coact_count", tk6.data_ptr(), n, kk, EE, c.data_ptr(), pp.data_ptr(), bad.data_ptr(),
+                   torch.cuda.current_stream().cuda_stream)
+            res.append((c.cpu(), pp.cpu()))
+        assert all(torch.equal(res[0][0], r[0]) and torch.equal(res[0][1], r[1]) for r in res)
+    os.environ.pop("BMOE_COACT_TC")
+    torch.cuda.synchronize()
     print("sanitize smoke ok")
