@@ -58,7 +58,7 @@ __device__ __forceinline__ void x3_decode_lanes(const uint32_t *w, uint32_t star
             uint32_t e4 = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                if (nbits < 32) {
+                if ((j & 1) == 0 && nbits < 32) {  // >= 32 bits cover the next two codes (<= 12 bits each)
                     buf |= (uint64_t)nxt << nbits;
                     nbits += 32;
                     nxt = word(++wi);
