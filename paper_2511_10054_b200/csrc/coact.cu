@@ -320,12 +320,42 @@ constexpr uint32_t kF4Stage = 128 * 128;           // 256 tokens x 128 expert ro
 constexpr size_t kF4Smem = (size_t)kF4Warps * kF4Stage + 1024;
 constexpr long long kF4MaxPerBlock = 1LL << 23;    // f32-exact counts per CTA
 
-template <int KC>
+// Transposed build (TB: the builder warps of BMOE_COACT_TB_MASK): lane = token. A lane turns
+// its token's ids into a 128-bit expert mask in registers (rejecting the row
+// when the mask's popcount is not k or a bit lies at or above E: exactly the
+// out-of-range / duplicate test of profiler.py:76-80), the warp transposes
+// each 32x32 bit block of (token, expert) with five xor-shuffle butterflies,
+// and lane b then holds, for expert 32j + b, the bit set of its 32 tokens:
+// one 16-byte chunk of that expert's row (word q, nibble n of the chunk <-
+// token 4n + q, as e2m1 1.0). The warp writes whole chunks with 16-byte
+// stores, 32 rows x one chunk per instruction: conflict-free under the 128B
+// swizzle, no zero fill and no shared-memory atomics.
+__device__ __forceinline__ uint32_t bit_transpose32(uint32_t x, unsigned lane) {
+    // the two byte-granular stages are one PRMT each: lower lane [x0 x1 y0 y1] / [x0 y0 x2 y2],
+    // upper lane [y2 y3 x2 x3] / [y1 x1 y3 x3] (y = the partner's word)
+    uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16);
+    x = __byte_perm(x, y, (lane & 16u) ? 0x3276u : 0x5410u);
+    y = __shfl_xor_sync(0xffffffffu, x, 8);
+    x = __byte_perm(x, y, (lane & 8u) ? 0x3715u : 0x6240u);
+#pragma unroll
+    for (int s = 4; s >= 1; s >>= 1) {
+        const uint32_t m = s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;  // bits whose index has bit s clear
+        const bool up = (lane & (unsigned)s) != 0;
+        const uint32_t keep = up ? ~m : m;
+        y = __shfl_xor_sync(0xffffffffu, x, s);
+        // lower lane takes (y << s) & ~m, upper lane (y >> s) & m: both a rotation of y
+        // (the wrapped bits fall outside the half taken)
+        x = (x & keep) | (__funnelshift_l(y, y, up ? 32 - s : s) & ~keep);
+    }
+    return x;
+}
+
+template <int KC, bool TB>
 __global__ void __launch_bounds__(kF4Threads) coact_fp4_kernel(const int32_t *__restrict__ topk, long long N, int k_rt,
                                                                int E, long long per_block,
                                                                unsigned long long *__restrict__ counts,
                                                                unsigned long long *__restrict__ pairs,
-                                                               int *__restrict__ invalid) {
+                                                               int *__restrict__ invalid, uint32_t tb_mask) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[2 * kF4Warps + 1];
     __shared__ uint32_t tmem_sh;
@@ -365,6 +395,77 @@ __global__ void __launch_bounds__(kF4Threads) coact_fp4_kernel(const int32_t *__
         // lane's word in row e: 128B swizzle of 16-byte chunk (lane/4) by (e & 7)
         const uint32_t wcol = ((lane & 3u) << 2), wchunk = lane >> 2;
         int bad = 0;
+        if (TB && ((tb_mask >> warp) & 1u)) {
+            uint32_t okw[4];  // expert bits below E, per 32-expert word
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int n = min(max(E - 32 * j, 0), 32);
+                okw[j] = n == 32 ? ~0u : ((1u << n) - 1u);
+            }
+            // k = 8: lane holds the ids of token tc0 + 32 g + lane for g = 0..7; group g of the
+            // next stage is loaded as soon as group g of this one is turned into its mask
+            constexpr int KP = KC == 8 ? 8 : 1;
+            int4 ia[KP], ib[KP];
+            auto load8 = [&](long long c, int g, int4 &a, int4 &b) {
+                const long long t = t0 + c * 256 + 32 * g + (long long)lane;
+                a = make_int4(-1, -1, -1, -1);
+                b = a;
+                if (c < nchunks && t < t1) {
+                    const int4 *p = reinterpret_cast<const int4 *>(topk + t * 8);
+                    a = __ldg(p);
+                    b = __ldg(p + 1);
+                }
+            };
+            if constexpr (KC == 8) {
+#pragma unroll
+                for (int g = 0; g < 8; ++g) load8(warp, g, ia[g], ib[g]);
+            }
+            for (long long c = warp, u = 0; c < nchunks; c += kF4Warps, ++u) {
+                const long long tc0 = t0 + c * 256;
+                ptx::mbar_wait(empty0 + 8 * warp, (uint32_t)(u & 1) ^ 1u);  // the MMAs that read the stage are done
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const long long t = tc0 + 32 * g + (long long)lane;
+                    // 128-bit expert mask as four words: bit (e - 32 j) of word j; shl clamps, so
+                    // an id outside [0, 128) (negative ones wrap to huge) sets no bit
+                    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int x = 0; x < KM; ++x) {
+                        if (x >= k) break;
+                        int v;
+                        if constexpr (KC == 8) {
+                            const int4 &q = x < 4 ? ia[g] : ib[g];
+                            const int r = x & 3;
+                            v = r == 0 ? q.x : r == 1 ? q.y : r == 2 ? q.z : q.w;
+                        } else {
+                            v = t < t1 ? __ldg(topk + t * k + x) : -1;
+                        }
+                        const uint32_t e = (uint32_t)v;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) w[j] |= ptx::shl_clamp(1u, e - 32u * (uint32_t)j);
+                    }
+                    if constexpr (KC == 8) load8(c + kF4Warps, g, ia[g], ib[g]);
+                    const bool live = t < t1;
+                    const bool ok = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]) == k &&
+                                    ((w[0] & ~okw[0]) | (w[1] & ~okw[1]) | (w[2] & ~okw[2]) | (w[3] & ~okw[3])) == 0u;
+                    if (live && !ok) ++bad;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t col = bit_transpose32(ok ? w[j] : 0u, lane);  // bit t: token 32g + t has expert 32j + lane
+                        const uint32_t e = 32u * (uint32_t)j + lane;
+                        // e2m1 1.0 (0b0010): the shifts are multiplies (FMA pipe), only the four
+                        // masks use the integer ALU, which this build is bound by
+                        const uint4 q = make_uint4((col * 2u) & 0x22222222u, col & 0x22222222u,
+                                                   __umulhi(col, 0x80000000u) & 0x22222222u,
+                                                   __umulhi(col, 0x40000000u) & 0x22222222u);
+                        *reinterpret_cast<uint4 *>(stage + e * 128u + (((uint32_t)g ^ (e & 7u)) << 4)) = q;
+                    }
+                }
+                ptx::fence_proxy_async_shared();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(full0 + 8 * warp);
+            }
+        } else
         for (long long c = warp, u = 0; c < nchunks; c += kF4Warps, ++u) {
             if constexpr (KC == 8) {
                 // coalesced: lane l loads 16-byte piece i*32 + l of the chunk's ids, i.e. half
@@ -682,13 +783,20 @@ extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t
     const char *tc_ev = getenv("BMOE_COACT_TC");
     const int tc_env = tc_ev ? atoi(tc_ev) : 2;
     if (tc_env == 2 && E <= 128 && k <= kTcMaxK && (k != 8 || (reinterpret_cast<uintptr_t>(topk) & 15) == 0)) {
-        auto fk = k == 8 ? coact_fp4_kernel<8> : coact_fp4_kernel<0>;
+        // builder warps (bit i = warp i) that build their one-hot tiles by register bit transposes
+        // (BMOE_COACT_TB_MASK, default none: every warp ORs nibbles into shared memory). Measured on
+        // the 64M-token trace (profiles/r2s_coact_mix.jsonl): ORs 0.84-0.87 ms (shared-memory bound),
+        // transposes 0.95 ms (integer-ALU bound), mixes 1.47-1.65 ms (the transposes' shuffles queue
+        // behind the ORs' bank-conflicted ATOMS on the same MIO pipe) -- DESIGN §7
+        const char *mk = getenv("BMOE_COACT_TB_MASK");
+        const uint32_t tb_mask = mk ? (uint32_t)strtoul(mk, nullptr, 0) & ((1u << kF4Warps) - 1u) : 0u;
+        auto fk = tb_mask ? (k == 8 ? coact_fp4_kernel<8, true> : coact_fp4_kernel<0, true>)
+                          : (k == 8 ? coact_fp4_kernel<8, false> : coact_fp4_kernel<0, false>);
         static bool fattr = false;
         if (!fattr) {
-            BM_CUDA_TRY(cudaFuncSetAttribute(coact_fp4_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kF4Smem));
-            BM_CUDA_TRY(cudaFuncSetAttribute(coact_fp4_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kF4Smem));
+            for (auto f : {coact_fp4_kernel<8, true>, coact_fp4_kernel<0, true>, coact_fp4_kernel<8, false>,
+                           coact_fp4_kernel<0, false>})
+                BM_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4Smem));
             fattr = true;
         }
         long long blocks = (long long)sm_count();
@@ -697,7 +805,7 @@ extern "C" int bm_coact_count(const int32_t *topk, int64_t N, int64_t k, int64_t
         blocks = std::max(blocks, (N + kF4MaxPerBlock - 1) / kF4MaxPerBlock);
         const long long per_block = (N + blocks - 1) / blocks;
         fk<<<(unsigned)blocks, kF4Threads, kF4Smem, as_stream(stream)>>>(topk, N, (int)k, (int)E, per_block, counts,
-                                                                         pairs, invalid_rows);
+                                                                         pairs, invalid_rows, tb_mask);
         BM_LAUNCH_CHECK();
         return BM_OK;
     }

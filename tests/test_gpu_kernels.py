@@ -678,12 +678,14 @@ def test_ffn_phase_trace(cuda_ok, monkeypatch):
     assert np.all(st[:, 0] <= st[:, 1]) and np.all(st[:, 1] <= st[:, 7])
 
 
-@pytest.mark.parametrize("tc", ["1", "2"], ids=["i8", "mxf4"])
+@pytest.mark.parametrize("tc", ["1", "2", "2:0xFFF", "2:0xAAA"], ids=["i8", "mxf4", "mxf4_tb_build", "mxf4_mixed_build"])
 @pytest.mark.parametrize("E,k,n", [(128, 8, 300_001), (64, 6, 100_003), (100, 3, 50_000), (8, 2, 20_000),
                                    (128, 8, 255), (128, 16, 70_001)])
 def test_coact_tensor_core_path_bit_exact(cuda_ok, monkeypatch, tc, E, k, n):
     """K6's tensor-core paths (BMOE_COACT_TC=1: tcgen05 kind::i8, =2: kind::mxf4
-    with e2m1 one-hots and unit block scales; X^T X over one-hot tiles in TMEM)
+    with e2m1 one-hots, built by shared-memory ORs, or by register bit
+    transposes in the builder warps of BMOE_COACT_TB_MASK (0xFFF: all, 0xAAA:
+    every other one); unit block scales, X^T X over one-hot tiles in TMEM)
     give exactly the shared-memory-atomics kernel's counts, pairs and
     rejected-row count, rejected rows (duplicates, out-of-range ids) included."""
     rng = np.random.default_rng(E * 31 + k)
@@ -694,7 +696,12 @@ def test_coact_tensor_core_path_bit_exact(cuda_ok, monkeypatch, tc, E, k, n):
     t = _t(topk)
     out = []
     for mode in ("0", tc):
+        mode, _, mask = mode.partition(":")
         monkeypatch.setenv("BMOE_COACT_TC", mode)
+        if mask:
+            monkeypatch.setenv("BMOE_COACT_TB_MASK", mask)
+        else:
+            monkeypatch.delenv("BMOE_COACT_TB_MASK", raising=False)
         c = torch.zeros(E, dtype=torch.int64, device=DEV)
         p = torch.zeros(E, E, dtype=torch.int64, device=DEV)
         badc = torch.zeros(1, dtype=torch.int32, device=DEV)
