@@ -13,8 +13,17 @@
 namespace bm {
 namespace ffn {
 
-template <int NMAT, int KPS>
+// TM (token-major SwiGLU GEMM1, data-parallel 128-token tiles): the MMA takes
+// the tokens as A (M = 128) and the m-tile's W1 and W3 blocks, which lie back
+// to back in the stage, as ONE B operand (N = 256), instead of two MMAs with
+// the weights as A. Per k-block the tensor core then reads 48 KB of operands
+// instead of 64 KB (tokens once, not once per matrix), which is what bounds
+// these tiles (shared-memory bandwidth, profiles/README.md). The accumulator
+// is [token lane][W1 | W3 column], so a lane finishes 16 consecutive f of its
+// token with two 16-byte H stores, no shuffles.
+template <int NMAT, int KPS, bool TM = false>
 __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
+    static_assert(!TM || NMAT == 2, "token-major tiles are the SwiGLU GEMM1");
     extern __shared__ uint8_t smem_raw[];
     __shared__ Sched sched;
     __shared__ __align__(8) uint64_t bars[64];
@@ -120,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
         int tile, st_beg, st_end;
         while (w.next(tile, st_beg, st_end)) {
             const TileInfo ti = decode_tile(sched, tile, mtiles, p.n_tile);
-            const uint32_t idesc = ptx::idesc_bf16_f32(kBM, (uint32_t)ti.n);
+            const uint32_t idesc = TM ? ptx::idesc_bf16_f32(kBM, 2 * kBM) : ptx::idesc_bf16_f32(kBM, (uint32_t)ti.n);
             ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1u);
             ptx::tc_fence_after();
             const uint32_t d0 = tmem_base + (uint32_t)acc * acc_cols;
@@ -131,7 +140,17 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
                 ptx::tc_fence_after();
                 const uint64_t a = desc0 + (uint64_t)stage * stage_d;
                 const uint64_t b = a + (kAStage >> 4);
-                if (p.probe != 1) {
+                if (TM && p.probe != 1) {  // A = the token rows, B = [W1 ; W3] (256 rows)
+#pragma unroll
+                    for (int i = 0; i < KPS; ++i) {
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 16; ++kk) {
+                            ptx::mma_bf16(d0, b + (uint64_t)i * bsz_d + 2 * kk,
+                                          a + (uint64_t)((i * NMAT) * (kATileBytes >> 4) + 2 * kk), idesc, accum);
+                            accum = 1u;
+                        }
+                    }
+                } else if (p.probe != 1) {
 #pragma unroll
                     for (int i = 0; i < KPS; ++i) {
                         const uint64_t bi = b + (uint64_t)i * bsz_d;
@@ -176,7 +195,27 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
             ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + (uint32_t)acc * acc_cols + ((uint32_t)(q * 32) << 16);
-            if (whole) {
+            if (TM) {  // lane = token row m_local of the tile; columns [0,128) W1, [128,256) W3
+                const int row = ti.row0 + m_local;
+                for (int c0 = 0; c0 < kBM; c0 += 16) {
+                    float g[16], u[16];
+                    ptx::tmem_ld16(tbase + (uint32_t)c0, g);
+                    ptx::tmem_ld16(tbase + (uint32_t)(kBM + c0), u);
+                    if (m_local < ti.n) {
+                        uint32_t w[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const __nv_bfloat162 pr = __floats2bfloat162_rn(expert_act<2>(g[2 * j], u[2 * j]),
+                                                                            expert_act<2>(g[2 * j + 1], u[2 * j + 1]));
+                            w[j] = *reinterpret_cast<const uint32_t *>(&pr);
+                        }
+                        const int f0 = ti.mtile * kBM + c0, plane = f0 >> 6, chunk = (f0 & 63) >> 3;
+                        uint4 *dst = reinterpret_cast<uint4 *>(p.h_planes) + ((long long)plane * p.h_rmax + row) * 8;
+                        dst[chunk ^ (row & 7)] = make_uint4(w[0], w[1], w[2], w[3]);
+                        dst[(chunk + 1) ^ (row & 7)] = make_uint4(w[4], w[5], w[6], w[7]);
+                    }
+                }
+            } else if (whole) {
                 for (int c0 = 0; c0 < ti.n; c0 += 16) {
                     float g[16], u[16];
                     ptx::tmem_ld16(tbase + (uint32_t)c0, g);
@@ -690,10 +729,10 @@ __global__ void __launch_bounds__(kBM) ffn_fixup_kernel(GemmParams p, int mode, 
     }
 }
 
-template <int NMAT, int KPS>
+template <int NMAT, int KPS, bool TM = false>
 int launch_gemm(const GemmParams &g, int G, cudaStream_t s) {
     static bool attr = false;
-    auto kern = ffn_gemm_kernel<NMAT, KPS>;
+    auto kern = ffn_gemm_kernel<NMAT, KPS, TM>;
     if (!attr) {
         BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
         attr = true;
@@ -703,7 +742,20 @@ int launch_gemm(const GemmParams &g, int G, cudaStream_t s) {
     return BM_OK;
 }
 
+// token-major SwiGLU GEMM1 tiles (BMOE_TM, read per call; default on): data-parallel
+// 128-token tiles finished in their own epilogue
+bool use_tm(const GemmParams &g) {
+    const char *ev = getenv("BMOE_TM");
+    return (!ev || atoi(ev) != 0) && g.nmat == 2 && g.mode == 0 && g.dp && g.fuse && g.n_tile == 128 &&
+           g.probe == 0;
+}
+
 int launch_gemm_1sm(const GemmParams &g, int G, cudaStream_t s) {
+    if (use_tm(g)) {
+        if (g.kps == 1) return launch_gemm<2, 1, true>(g, G, s);
+        if (g.kps == 2) return launch_gemm<2, 2, true>(g, G, s);
+        return launch_gemm<2, 4, true>(g, G, s);
+    }
     if (g.nmat == 2) {
         if (g.kps == 1) return launch_gemm<2, 1>(g, G, s);
         if (g.kps == 2) return launch_gemm<2, 2>(g, G, s);
