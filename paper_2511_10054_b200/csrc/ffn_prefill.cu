@@ -13,6 +13,23 @@
 namespace bm {
 namespace ffn {
 
+// Token-major SwiGLU finish: g / u hold W1 / W3 rows [c0, c0+16) of m-tile
+// `mtile` for token `row`; SwiGLU -> bf16 -> the two 16-byte chunks of H.
+__device__ __forceinline__ void finish_tm16(const GemmParams &p, int mtile, int row, int c0, const float (&g)[16],
+                                            const float (&u)[16]) {
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const __nv_bfloat162 pr =
+            __floats2bfloat162_rn(expert_act<2>(g[2 * j], u[2 * j]), expert_act<2>(g[2 * j + 1], u[2 * j + 1]));
+        w[j] = *reinterpret_cast<const uint32_t *>(&pr);
+    }
+    const int f0 = mtile * kBM + c0, plane = f0 >> 6, chunk = (f0 & 63) >> 3;
+    uint4 *dst = reinterpret_cast<uint4 *>(p.h_planes) + ((long long)plane * p.h_rmax + row) * 8;
+    dst[chunk ^ (row & 7)] = make_uint4(w[0], w[1], w[2], w[3]);
+    dst[(chunk + 1) ^ (row & 7)] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 // TM (token-major SwiGLU GEMM1, data-parallel 128-token tiles): the MMA takes
 // the tokens as A (M = 128) and the m-tile's W1 and W3 blocks, which lie back
 // to back in the stage, as ONE B operand (N = 256), instead of two MMAs with
@@ -201,19 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_kernel(GemmParams p) {
                     float g[16], u[16];
                     ptx::tmem_ld16(tbase + (uint32_t)c0, g);
                     ptx::tmem_ld16(tbase + (uint32_t)(kBM + c0), u);
-                    if (m_local < ti.n) {
-                        uint32_t w[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const __nv_bfloat162 pr = __floats2bfloat162_rn(expert_act<2>(g[2 * j], u[2 * j]),
-                                                                            expert_act<2>(g[2 * j + 1], u[2 * j + 1]));
-                            w[j] = *reinterpret_cast<const uint32_t *>(&pr);
-                        }
-                        const int f0 = ti.mtile * kBM + c0, plane = f0 >> 6, chunk = (f0 & 63) >> 3;
-                        uint4 *dst = reinterpret_cast<uint4 *>(p.h_planes) + ((long long)plane * p.h_rmax + row) * 8;
-                        dst[chunk ^ (row & 7)] = make_uint4(w[0], w[1], w[2], w[3]);
-                        dst[(chunk + 1) ^ (row & 7)] = make_uint4(w[4], w[5], w[6], w[7]);
-                    }
+                    if (m_local < ti.n) finish_tm16(p, ti.mtile, row, c0, g, u);
                 }
             } else if (whole) {
                 for (int c0 = 0; c0 < ti.n; c0 += 16) {
@@ -471,7 +476,12 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm_2sm_kernel(GemmParams p,
 // as every other path, so H is bitwise identical.
 //   xfull : my receive buffer holds this tile's columns (4 remote warp arrivals)
 //   xfree : my PEER's receive buffer may be overwritten (4 remote arrivals)
-template <int KPS>
+// TMP (token-major pair, BMOE_TM=2): the same loads, with the operands' roles
+// swapped: A = the pair's 256 tokens (each CTA's token half = its 128 rows of
+// A), B = [W1 ; W3] as N = 256 split along N (W1 block in the leader, W3 in
+// the peer). Each CTA's TMEM then holds its own tokens x (W1 | W3) and
+// finishes SwiGLU locally: no DSMEM exchange.
+template <int KPS, bool TMP = false>
 __global__ void __launch_bounds__(kThreads, 1) ffn_gemm1_split_kernel(GemmParams p, const __grid_constant__ PairMaps tm) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ Sched sched;
@@ -582,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm1_split_kernel(GemmParams
         uint32_t acc_phase = 0;
         for (int u = pair; u < units; u += G) {
             const TileInfo ti = decode_tile(sched, u, mtiles, p.n_tile);
-            const uint32_t idesc = ptx::idesc_bf16_f32(2 * kBM, (uint32_t)ti.n);
+            const uint32_t idesc = TMP ? ptx::idesc_bf16_f32(2 * kBM, 2 * kBM) : ptx::idesc_bf16_f32(2 * kBM, (uint32_t)ti.n);
             ptx::mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1u);
             ptx::tc_fence_after();
             const uint32_t d0 = tmem_base + (uint32_t)acc * acc_cols;
@@ -597,7 +607,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm1_split_kernel(GemmParams
                     const uint64_t ai = a + (uint64_t)i * (kATileBytes >> 4), bi = b + (uint64_t)i * bh_d;
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
-                        ptx::mma_bf16_pair(d0, ai + 2 * kk, bi + 2 * kk, idesc, accum);
+                        if (TMP)
+                            ptx::mma_bf16_pair(d0, bi + 2 * kk, ai + 2 * kk, idesc, accum);
+                        else
+                            ptx::mma_bf16_pair(d0, ai + 2 * kk, bi + 2 * kk, idesc, accum);
                         accum = 1u;
                     }
                 }
@@ -608,6 +621,38 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_gemm1_split_kernel(GemmParams
                 }
             }
             ptx::mma_commit_pair(tfull0 + 8 * acc, 0x3);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1u;
+        }
+    } else if (TMP && warp >= 4) {
+        // ===================== epilogue (token-major): own tokens x (W1 | W3), SwiGLU in place
+        const int q = warp - 4;
+        const int m_local = q * 32 + (int)lane;
+        const uint32_t tempty_leader = leader ? tempty0 : ptx::mapa(tempty0, 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = pair; u < units; u += G) {
+            const TileInfo ti = decode_tile(sched, u, mtiles, p.n_tile);
+            const int h0 = ti.n / 2;  // the producers' split: leader tokens [0, h0), peer [h0, n)
+            const int mine = leader ? h0 : ti.n - h0;
+            const int row = ti.row0 + (leader ? 0 : h0) + m_local;
+            ptx::mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + (uint32_t)acc * acc_cols + ((uint32_t)(q * 32) << 16);
+            for (int c0 = 0; c0 < kBM; c0 += 16) {
+                float g[16], uu[16];
+                ptx::tmem_ld16(tbase + (uint32_t)c0, g);
+                ptx::tmem_ld16(tbase + (uint32_t)(kBM + c0), uu);
+                if (m_local < mine) finish_tm16(p, ti.mtile, row, c0, g, uu);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader)
+                    ptx::mbar_arrive(tempty0 + 8 * acc);
+                else
+                    ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1u;
         }
@@ -744,9 +789,9 @@ int launch_gemm(const GemmParams &g, int G, cudaStream_t s) {
 
 // token-major SwiGLU GEMM1 tiles (BMOE_TM, read per call; default on): data-parallel
 // 128-token tiles finished in their own epilogue
+int tm_mode();
 bool use_tm(const GemmParams &g) {
-    const char *ev = getenv("BMOE_TM");
-    return (!ev || atoi(ev) != 0) && g.nmat == 2 && g.mode == 0 && g.dp && g.fuse && g.n_tile == 128 &&
+    return tm_mode() != 0 && g.nmat == 2 && g.mode == 0 && g.dp && g.fuse && g.n_tile == 128 &&
            g.probe == 0;
 }
 
@@ -796,7 +841,9 @@ int encode_rows(CUtensorMap *m, const void *base, unsigned long long rows, unsig
 template <int NMAT, int KPS>
 int launch_gemm_2sm(const GemmParams &g, int G, cudaStream_t s) {
     static bool attr = false;
-    auto kern = NMAT == 0 ? ffn_gemm1_split_kernel<KPS> : ffn_gemm_2sm_kernel<NMAT == 0 ? 1 : NMAT, KPS>;
+    auto kern = NMAT == 0    ? ffn_gemm1_split_kernel<KPS>
+                : NMAT == -1 ? ffn_gemm1_split_kernel<KPS, true>
+                             : ffn_gemm_2sm_kernel<NMAT <= 0 ? 1 : NMAT, KPS>;
     if (!attr) {
         BM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
         attr = true;
@@ -822,7 +869,7 @@ int launch_gemm_2sm(const GemmParams &g, int G, cudaStream_t s) {
     gp.num_ctas = 2 * std::min(G / 2, max_clusters);
     cfg.gridDim = dim3((unsigned)gp.num_ctas);
     PairMaps maps;
-    if (int rc = encode_rows(&maps.a, g.arena, (unsigned long long)(g.arena_bytes / 128), NMAT == 0 ? 128 : 256))
+    if (int rc = encode_rows(&maps.a, g.arena, (unsigned long long)(g.arena_bytes / 128), NMAT <= 0 ? 128 : 256))
         return rc;
     if (int rc = encode_rows(&maps.b, g.b_planes, (unsigned long long)(g.K / kBK) * (g.b_plane_bytes / 128),
                              (unsigned)(g.n_tile / 2)))
@@ -855,17 +902,34 @@ int two_sm_mode() {
     const char *ev = getenv("BMOE_2SM");
     return ev ? atoi(ev) : 1;
 }
+// BMOE_TM (read per call): 0 weight-major GEMM1 tiles everywhere, 1 token-major single-CTA
+// tiles, 2 token-major CTA pairs (ffn_gemm1_split_kernel<KPS, true>) at any K, 3 (default)
+// pairs once the call averages >= 256 rows per expert, else single CTAs: the 256-token pair
+// tiles half-fill at fewer rows (Qwen3 2048 x 8, 128 rows / expert: 0.173 vs 0.168 ms single;
+// 8192 x 8: 0.394 vs 0.432 ms; profiles/r2s_prefill_tmp.jsonl)
+int tm_mode() {
+    const char *ev = getenv("BMOE_TM");
+    return ev ? atoi(ev) : 3;
+}
+bool tm_pair(const GemmParams &g) {
+    const int m = tm_mode();
+    return (m == 2 || (m == 3 && (long long)g.h_rmax >= 256LL * g.E)) && g.nmat == 2 && g.mode == 0 && g.dp &&
+           g.fuse;
+}
+
 bool use_2sm(const GemmParams &g) {
     const int mode = two_sm_mode();
     if (!g.dp || mode == 0 || g.n_tile < 32 || g.n_tile % 32) return false;
     // W1 | W3 split pair: its accumulator exchange costs a few us per tile, paid
     // back only by long tiles (Mixtral K=4096: 1.66 -> 1.51 ms; Qwen3 K=2048:
     // 0.45 -> 0.56 ms, so shorter K keeps single CTAs)
-    if (g.nmat == 2 && mode == 1) return g.K >= 4096;
+    if (g.nmat == 2 && mode == 1) return g.K >= 4096 || tm_pair(g);
     return (g.nmat == 1 || mode == 2) && (g.M / kBM) % 2 == 0;
 }
 
 int launch_gemm_2sm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
+    if (g.nmat == 2 && two_sm_mode() == 1 && tm_pair(g))
+        return g.kps == 1 ? launch_gemm_2sm<-1, 1>(g, G, s) : launch_gemm_2sm<-1, 2>(g, G, s);
     if (g.nmat == 2 && two_sm_mode() == 1) return g.kps == 1 ? launch_gemm_2sm<0, 1>(g, G, s) : launch_gemm_2sm<0, 2>(g, G, s);
     if (g.nmat == 2) return g.kps == 1 ? launch_gemm_2sm<2, 1>(g, G, s) : launch_gemm_2sm<2, 2>(g, G, s);
     return g.kps == 1 ? launch_gemm_2sm<1, 1>(g, G, s) : launch_gemm_2sm<1, 2>(g, G, s);
@@ -876,7 +940,7 @@ int launch_gemm_dispatch(const GemmParams &g, int G, cudaStream_t s) {
         GemmParams g2 = g;
         if (g.nmat == 2 && two_sm_mode() == 1) {  // W1 | W3 split: 256-token tiles, one matrix per CTA
             g2.n_tile = 256;
-            if (const char *ev = getenv("BMOE_NT1")) g2.n_tile = atoi(ev);
+            if (const char *ev = getenv("BMOE_NT1"); ev && !tm_pair(g)) g2.n_tile = atoi(ev);  // token-major: 2 x 128 rows
             g2.kps = 1;  // 5 stages of 32 KB beside the 35 KB receive buffer
             if (const char *kv = getenv("BMOE_KPS_SPLIT")) g2.kps = (atoi(kv) == 2 && (g.K / kBK) % 2 == 0) ? 2 : 1;
         } else {

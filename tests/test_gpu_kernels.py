@@ -439,17 +439,21 @@ def test_prefill_2sm_pairs_equal_single_cta(cuda_ok, E, d, f, B, k, act):
     assert rel <= 2e-2, rel
 
 
-@pytest.mark.parametrize("E,d,f,B,k", [(16, 2048, 768, 1500, 8), (8, 2048, 1408, 900, 6), (4, 1024, 512, 77, 2)])
-def test_prefill_token_major_gemm1_bitwise(cuda_ok, monkeypatch, E, d, f, B, k):
-    """The token-major SwiGLU GEMM1 tiles (BMOE_TM=1: tokens as the MMA's A,
-    [W1 ; W3] as one N = 256 B operand) give every real row bitwise the
+@pytest.mark.parametrize("tm", ["1", "2"], ids=["single_cta", "cta_pair"])
+@pytest.mark.parametrize("E,d,f,B,k", [(16, 2048, 768, 1500, 8), (8, 2048, 1408, 900, 6), (4, 1024, 512, 77, 2),
+                                       (4, 4096, 1024, 600, 2)])
+def test_prefill_token_major_gemm1_bitwise(cuda_ok, monkeypatch, tm, E, d, f, B, k):
+    """The token-major SwiGLU GEMM1 tiles (tokens as the MMA's A, [W1 ; W3]
+    as one N = 256 B operand; BMOE_TM=1 single CTAs, =2 CTA pairs with the
+    B operand split W1 | W3 across the pair) give every real row bitwise the
     result of the weight-major tiles (BMOE_TM=0): each output element is the
     same K = 16 step chain."""
     rng = np.random.default_rng(B + f)
+    monkeypatch.setenv("BMOE_TM", tm)
     y, ref32, (xp, perm, arena, buf_of, ws) = _bf16_case(rng, E, d, f, B, k, ops.ACT_SWIGLU, 128)
     real = perm.row_token >= 0
     out = []
-    for tm in ("0", "1"):
+    for tm in ("0", tm):
         monkeypatch.setenv("BMOE_TM", tm)
         out.append(ops.expert_ffn_bf16(xp, perm, arena, _t(buf_of), d, f, ops.ACT_SWIGLU, ws)[real].clone())
     assert torch.equal(out[0], out[1])
