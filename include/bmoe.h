@@ -282,8 +282,12 @@ int64_t bm_kernel_spans(float *out_host, int64_t cap);
  * are rejected like observe() rejects them (profiler.py:76-80): they are not
  * counted and *invalid_rows (device int32, accumulated) is incremented, so
  * the caller raises InputError after reading it back.
- * Shared-memory-privatised per-CTA counters, flushed with 64-bit adds; for
- * k >= 2 the diagonal is derived as rowsum/(k-1) (exact for distinct ids).
+ * For E <= 128, k <= 16 (default BMOE_COACT_TC=2) the count is X^T X on the
+ * FP4 tensor cores (tcgen05.mma kind::mxf4 over e2m1 one-hot tiles, exact f32
+ * accumulation per CTA); otherwise (or BMOE_COACT_TC=0) shared-memory-
+ * privatised per-CTA counters, flushed with 64-bit adds, with the diagonal
+ * derived as rowsum/(k-1) for k >= 2 (exact for distinct ids). Every path
+ * gives the same counts bit for bit.
  * Warm-up down-weighting is applied by the caller by counting the warm-up
  * token range separately (the weights are exact dyadic scalars).
  * Accumulates (does not clear). Limits: E <= 256, k <= 32. */
